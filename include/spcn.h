@@ -1,0 +1,158 @@
+/*
+ * spcn.h — C ABI of libspcn.so, the B200 (sm_100a) hot path of
+ * structure-preserving color normalization (SPCN).
+ *
+ * Every entry point replaces one function of the reference package
+ * `slidenorm` (/root/reference/pkg/src/slidenorm, cited as src/<file>:<line>).
+ * The ABI is plain C: device pointers + sizes, a cudaStream_t passed as
+ * `void*`, no C++ or torch types.  Calls are stream-ordered and do not
+ * synchronize the host unless stated; they are reentrant across host threads
+ * and streams (no global mutable state except a thread-local error string).
+ *
+ * Return codes map 1:1 onto the reference exception taxonomy
+ * (src/errors.py:1-36; ValueError for argument checks).
+ */
+#ifndef SPCN_H_
+#define SPCN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define SPCN_OK 0
+#define SPCN_EINVAL 1            /* ValueError (argument / invariant check)   */
+#define SPCN_EBLANK 2            /* BlankSlideError        src/errors.py:24   */
+#define SPCN_EINSUFFICIENT 3     /* InsufficientPixelsError src/errors.py:28  */
+#define SPCN_ESTAIN_ABSENT 4     /* StainAbsentError       src/errors.py:32   */
+#define SPCN_EDEGENERATE 5       /* DegenerateStainError   src/errors.py:36   */
+#define SPCN_ECUDA 6             /* CUDA runtime error                          */
+#define SPCN_ENCCL 7             /* collective error (multi-GPU stats)          */
+
+/* ---- precision of the per-pixel transform ------------------------------ */
+#define SPCN_PREC_EXACT 0   /* fp32 fast path + certified rounding; pixels whose
+                               rounding is not certified are recomputed in fp64
+                               in the reference's operation order: output is
+                               byte-identical to src/pipeline.py:260-272      */
+#define SPCN_PREC_FAST 1    /* fp32 only (±1 LSB vs the reference)            */
+#define SPCN_PREC_STRICT 2  /* fp64 for every pixel, reference operation order */
+
+/* Parameters of one source→target recoloring (src/pipeline.py:260
+ * `_process_strip(pixels, src_i0, src_basis, code_lam, factors, tgt_basis,
+ * tgt_i0)`).  Bases are row-major 3x2 (basis[c*2+j], channel c, stain j). */
+typedef struct spcn_xform_params {
+  double src_i0[3];
+  double src_basis[6];
+  double code_lam;          /* >= 0; reference default 0.0 (src/pipeline.py:277) */
+  double factors[2];        /* tgt_p99 / src_p99 (src/normalize.py:103-112)      */
+  double tgt_basis[6];
+  double tgt_i0[3];
+  const double* od_table;   /* optional host pointer to the (3,256) fp64 OD table
+                               ln(i0_c/clip(i,1,i0_c)) for i=0..255 computed by the
+                               caller with the reference's own expression
+                               (src/optics.py:89-94); NULL = computed with libm  */
+  int32_t precision;        /* SPCN_PREC_*                                       */
+  int32_t max_sweeps;       /* CD sweep cap, reference 2000 (src/stain_sep.py:168) */
+} spcn_xform_params;
+
+/* Device workspace (bytes) needed by spcn_xform_rgb8 for `npix` pixels.     */
+size_t spcn_xform_workspace_bytes(int64_t npix);
+
+/* Recolor `npix` packed RGB8 pixels: src → dst (both device pointers, may be
+ * the same buffer).  Replaces `_process_strip` src/pipeline.py:260-272
+ * (= beer_lambert src/optics.py:71 + code_densities src/stain_sep.py:168 +
+ * normalize_block src/normalize.py:115).  Host-side checks mirror
+ * validate_basis (src/stain_sep.py:89-101), the normalize_block factor check
+ * (src/normalize.py:141-142) and beer_lambert's i0 check (src/optics.py:90). */
+int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix,
+                    const spcn_xform_params* p, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* Number of pixels the last EXACT-mode call on `workspace` sent to the fp64
+ * repair path (synchronizes `stream`; diagnostics only).                    */
+int spcn_xform_repair_count(const void* workspace, void* stream, int64_t* count);
+
+/* Per-pixel density coding: od (3,n) fp64 device, h (2,n) fp64 device.
+ * Replaces code_densities src/stain_sep.py:168-201 (bit-identical: same
+ * operation order, same bitwise CD fixed point, same sweep cap).            */
+int spcn_code_densities(const double* od, double* h, int64_t n,
+                        const double* basis, double lam, int32_t max_sweeps,
+                        void* stream);
+
+/* Recombination + inverse Beer-Lambert: h (2,n) fp64 device → out (n,3) u8.
+ * Replaces normalize_block src/normalize.py:115-151.                        */
+int spcn_normalize_block(const double* h, uint8_t* out, int64_t n,
+                         const double* factors, const double* tgt_basis,
+                         const double* tgt_i0, void* stream);
+
+/* Beer-Lambert OD of packed RGB8 pixels: px (n,3) u8 → od (3,n) fp64
+ * (channel-major, the layout code_densities consumes).  Replaces
+ * beer_lambert src/optics.py:71-94 via the same 256-entry table.           */
+int spcn_beer_lambert(const uint8_t* px, double* od, int64_t n,
+                      const double* i0, const double* od_table, void* stream);
+
+/* Inverse Beer-Lambert: od (n,3) fp64 device → out (n,3) u8,
+ * floor(i0_c*exp(-v)+0.5) clipped to [0,255].  Replaces inverse_beer_lambert
+ * src/optics.py:97-110.                                                     */
+int spcn_inverse_beer_lambert(const double* od, uint8_t* out, int64_t n,
+                              const double* i0, void* stream);
+
+/* ---- fit: pixel sampling (src/pipeline.py:128-200) -------------------- */
+#define SPCN_SAMPLE_CHUNK 4096   /* raster-order pixels per counting chunk  */
+
+/* A rectangular region of an RGB8 image in device memory: pixel (row, col)
+ * of the patch is at byte 3*(base + row*row_stride + col) of `img`.        */
+typedef struct spcn_patch {
+  int64_t base;        /* pixel offset of the top-left pixel                 */
+  int32_t width, height;
+  int64_t row_stride;  /* pixels between consecutive rows                    */
+} spcn_patch;
+
+/* What the visit loop decided to take from one visited patch.               */
+typedef struct spcn_patch_take {
+  int64_t take_nonwhite;   /* first N non-white pixels in raster order        */
+  int64_t out_base;        /* where they go in the output sample (pixels)     */
+  int32_t take_bright[3];  /* first N values > thr per channel (bright pools) */
+  int32_t problem;         /* which fit problem's bright histogram to feed     */
+} spcn_patch_take;
+
+/* Per-chunk counts for `npatches` patches (device array of spcn_patch):
+ * counts[(p*max_chunks + k)*4 + {0,1,2,3}] = #non-white, #R>thr, #G>thr,
+ * #B>thr among raster pixels [k*CHUNK, (k+1)*CHUNK) of patch p.  Non-white
+ * means "not all channels > thr" (src/pipeline.py:176).                     */
+int spcn_sample_count(const uint8_t* img, const spcn_patch* patches, int32_t npatches,
+                      int32_t max_chunks, int32_t white_threshold, int32_t* counts,
+                      void* stream);
+
+/* Ordered compaction of the decided takes: the first take_nonwhite non-white
+ * pixels of each patch (raster order) → out_px[out_base ...] (RGB8), and the
+ * first take_bright[c] values > thr of channel c → bright_hist[problem][c][v]
+ * (+=, caller zeroes).  Reproduces the raster-order prefixes of
+ * src/pipeline.py:167-181 exactly.                                          */
+int spcn_sample_compact(const uint8_t* img, const spcn_patch* patches, int32_t npatches,
+                        int32_t max_chunks, int32_t white_threshold, const int32_t* counts,
+                        const spcn_patch_take* takes, uint8_t* out_px, int32_t* bright_hist,
+                        void* stream);
+
+/* Background i0 per problem and channel: exact 80th percentile of the bright
+ * pool given as 256-bin counts (estimate_max_intensity src/optics.py:35-68).
+ * Empty pools give 255 and empty[p*3+c] = 1 (the reference's warning case). */
+int spcn_i0_from_hist(const int32_t* hist, int32_t nprob, double* i0, int32_t* empty,
+                      void* stream);
+
+/* Per-problem OD tables lut[p][c][i] = ln(i0[p][c] / clip(i,1,i0[p][c])).   */
+int spcn_od_tables(const double* i0, int32_t nprob, double* lut, void* stream);
+
+/* Thread-local description of the last error ("" if none).                 */
+const char* spcn_last_error(void);
+
+/* Library version string.                                                   */
+const char* spcn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPCN_H_ */

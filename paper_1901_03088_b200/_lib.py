@@ -1,0 +1,127 @@
+"""ctypes binding of libspcn.so (the C ABI declared in include/spcn.h).
+
+The library is the product path: there is no CPU fallback.  Loading fails
+loudly when the .so is missing or when a call is made without a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspcn.so")
+
+SPCN_OK = 0
+SPCN_EINVAL = 1
+SPCN_EBLANK = 2
+SPCN_EINSUFFICIENT = 3
+SPCN_ESTAIN_ABSENT = 4
+SPCN_EDEGENERATE = 5
+SPCN_ECUDA = 6
+SPCN_ENCCL = 7
+
+PREC = {"exact": 0, "fast": 1, "strict": 2}
+
+# every symbol include/spcn.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "spcn_xform_workspace_bytes", "spcn_xform_rgb8", "spcn_xform_repair_count",
+    "spcn_code_densities", "spcn_normalize_block", "spcn_beer_lambert",
+    "spcn_inverse_beer_lambert", "spcn_last_error", "spcn_version",
+)
+
+
+class XformParams(ctypes.Structure):
+    _fields_ = [
+        ("src_i0", ctypes.c_double * 3),
+        ("src_basis", ctypes.c_double * 6),
+        ("code_lam", ctypes.c_double),
+        ("factors", ctypes.c_double * 2),
+        ("tgt_basis", ctypes.c_double * 6),
+        ("tgt_i0", ctypes.c_double * 3),
+        ("od_table", ctypes.POINTER(ctypes.c_double)),
+        ("precision", ctypes.c_int32),
+        ("max_sweeps", ctypes.c_int32),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+DBL = ctypes.c_double
+I32 = ctypes.c_int32
+SZ = ctypes.c_size_t
+
+_SIGS = {
+    "spcn_xform_workspace_bytes": (SZ, [I64]),
+    "spcn_xform_rgb8": (ctypes.c_int, [P, P, I64, ctypes.POINTER(XformParams), P, SZ, P]),
+    "spcn_xform_repair_count": (ctypes.c_int, [P, P, ctypes.POINTER(I64)]),
+    "spcn_code_densities": (ctypes.c_int, [P, P, I64, P, DBL, I32, P]),
+    "spcn_normalize_block": (ctypes.c_int, [P, P, I64, P, P, P, P]),
+    "spcn_beer_lambert": (ctypes.c_int, [P, P, I64, P, P, P]),
+    "spcn_inverse_beer_lambert": (ctypes.c_int, [P, P, I64, P, P]),
+    "spcn_last_error": (ctypes.c_char_p, []),
+    "spcn_version": (ctypes.c_char_p, []),
+}
+
+
+def lib():
+    """Load libspcn.so once; raise if it is absent (no fallback path)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(
+                        f"libspcn.so not built ({LIB_PATH}); run "
+                        "`python -m paper_1901_03088_b200._build` — there is no CPU fallback")
+                h = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+                for name, (res, args) in _SIGS.items():
+                    fn = getattr(h, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = h
+    return _lib
+
+
+def declare(name, restype, argtypes):
+    """Register the signature of an additional entry point (used by the fit/stats modules)."""
+    fn = getattr(lib(), name)
+    fn.restype = restype
+    fn.argtypes = argtypes
+    return fn
+
+
+_CODE_TO_EXC = {
+    SPCN_EINVAL: ValueError,
+    SPCN_EBLANK: errors.BlankSlideError,
+    SPCN_EINSUFFICIENT: errors.InsufficientPixelsError,
+    SPCN_ESTAIN_ABSENT: errors.StainAbsentError,
+    SPCN_EDEGENERATE: errors.DegenerateStainError,
+}
+
+
+def check(rc: int, what: str = "") -> None:
+    """Translate a libspcn status code into the reference's exception type."""
+    if rc == SPCN_OK:
+        return
+    msg = lib().spcn_last_error().decode("utf-8", "replace")
+    exc = _CODE_TO_EXC.get(rc)
+    if exc is None:
+        raise RuntimeError(f"{what}: libspcn error {rc}: {msg}")
+    raise exc(msg)
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int:
+    return int(t.data_ptr())

@@ -1,0 +1,312 @@
+// api.cu — extern "C" entry points of libspcn.so (see include/spcn.h).
+//
+// Host-side validation mirrors the reference's argument checks so error
+// behaviour is the same: validate_basis (src/stain_sep.py:89-101),
+// beer_lambert's i0 check (src/optics.py:90-91), code_densities' lam check
+// (src/stain_sep.py:188-189), normalize_block's factor check
+// (src/normalize.py:141-142).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "spcn.h"
+#include "spcn_device.cuh"
+#include "xform.h"
+
+using namespace spcn;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SPCN_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// validate_basis, src/stain_sep.py:89-101 (norm as np.linalg.norm: sqrt of the sum of squares)
+int check_basis(const double* w, const char* role) {
+  for (int k = 0; k < 6; ++k) {
+    if (!std::isfinite(w[k])) return fail(SPCN_EINVAL, std::string(role) + " basis contains non-finite entries");
+    if (w[k] < 0) return fail(SPCN_EINVAL, std::string(role) + " basis entries must be non-negative");
+  }
+  for (int j = 0; j < 2; ++j) {
+    const double nrm = std::sqrt(w[0 * 2 + j] * w[0 * 2 + j] + w[1 * 2 + j] * w[1 * 2 + j] +
+                                 w[2 * 2 + j] * w[2 * 2 + j]);
+    if (std::fabs(nrm - 1.0) > 1e-9)
+      return fail(SPCN_EINVAL, std::string(role) + " basis columns must have unit L2 norm");
+  }
+  return SPCN_OK;
+}
+
+// Gram entries in the reference's scalar order (src/stain_sep.py:197-199).
+// This file is compiled with -ffp-contract=off so no FMA is formed here.
+void gram(const double* w, double& g00, double& g01, double& g11) {
+  g00 = w[0] * w[0] + w[2] * w[2] + w[4] * w[4];
+  g11 = w[1] * w[1] + w[3] * w[3] + w[5] * w[5];
+  g01 = w[0] * w[1] + w[2] * w[3] + w[4] * w[5];
+}
+
+// OD table: ln(i0_c / clip(i, 1, i0_c)), src/optics.py:92-94.
+void od_table(const double* i0, const double* given, double lut[3][256]) {
+  if (given) {
+    std::memcpy(lut, given, sizeof(double) * 3 * 256);
+    return;
+  }
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 256; ++i) {
+      double x = static_cast<double>(i);
+      x = x < 1.0 ? 1.0 : (x > i0[c] ? i0[c] : x);
+      lut[c][i] = std::log(i0[c] / x);
+    }
+}
+
+void fill_strict(StrictP& sp, const double* lut_src, const double* ws, const double* wt,
+                 const double* f, const double* i0t, double lam, int max_sweeps) {
+  std::memcpy(sp.lut, lut_src, sizeof(sp.lut));
+  for (int c = 0; c < 3; ++c)
+    for (int j = 0; j < 2; ++j) {
+      sp.ws[c][j] = ws ? ws[c * 2 + j] : 0.0;
+      sp.wt[c][j] = wt ? wt[c * 2 + j] : 0.0;
+    }
+  sp.f[0] = f ? f[0] : 1.0;
+  sp.f[1] = f ? f[1] : 1.0;
+  for (int c = 0; c < 3; ++c) sp.i0t[c] = i0t ? i0t[c] : 255.0;
+  if (ws) {
+    gram(ws, sp.g00, sp.g01, sp.g11);
+    sp.det = sp.g00 * sp.g11 - sp.g01 * sp.g01;
+  }
+  sp.lam = lam;
+  sp.tol = 0.0;
+  sp.max_sweeps = max_sweeps;
+  sp.pad_ = 0;
+}
+
+// fp32 coefficients + the certification bound (DESIGN.md §Certified rounding).
+// Returns false when the fast path must not be used (ill-conditioned basis,
+// target i0 outside [0,255], or a target i0 sitting on a rounding tie).
+bool fill_fast(FastP& fp, const StrictP& sp, bool exact) {
+  const double g00 = sp.g00, g01 = sp.g01, g11 = sp.g11, det = sp.det;
+  if (!(det > 1e-6 * g00 * g11) || !(g00 > 0) || !(g11 > 0)) return false;
+  for (int c = 0; c < 3; ++c)
+    if (!(sp.i0t[c] >= 0.0 && sp.i0t[c] <= 255.0)) return false;
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 256; ++i) fp.lut[c][i] = static_cast<float>(sp.lut[c][i]);
+  for (int c = 0; c < 3; ++c)
+    for (int j = 0; j < 2; ++j) fp.w[c][j] = static_cast<float>(sp.ws[c][j]);
+  fp.nlam = static_cast<float>(-sp.lam);
+  const double A = g11 / det, C = g01 / det, E = 1.0 / g11, F = g01 / g11, G = 1.0 / g00,
+               H = g01 / g00;
+  fp.A = (float)A; fp.C = (float)C; fp.E = (float)E;
+  fp.F = (float)F; fp.G = (float)G; fp.H = (float)H;
+  const double log2e = 1.4426950408889634;
+  double Kabs[3][2];
+  for (int c = 0; c < 3; ++c)
+    for (int j = 0; j < 2; ++j) {
+      const double k = -log2e * sp.wt[c][j] * sp.f[j];
+      fp.K[c][j] = static_cast<float>(k);
+      Kabs[c][j] = std::fabs(k);
+    }
+  for (int c = 0; c < 3; ++c) fp.i0t[c] = static_cast<float>(sp.i0t[c]);
+  fp.lam4 = static_cast<float>(4.0 * sp.lam);
+  // error chain, per unit u*T (u = 2^-24, T = t0 + t1 + 4 lam)
+  const double P0 = A + C, D0 = 8.0 * (A + C);
+  const double D1 = 7.0 * E + F * D0 + 3.0 * F * P0;
+  const double P1 = E + F * P0;
+  const double Dh0 = 7.0 * G + H * D1 + 3.0 * H * P1;
+  const double H0 = G + H * P1;
+  double L = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    const double l = Kabs[c][0] * Dh0 + Kabs[c][1] * D1 + 3.0 * (Kabs[c][0] * H0 + Kabs[c][1] * P1);
+    L = l > L ? l : L;
+  }
+  const double u = std::ldexp(1.0, -24), ln2 = 0.6931471805599453;
+  const double a1 = 1.25 * ln2 * u * L * 1.001;
+  const double a0 = 1.25 * (std::ldexp(1.0, -21) + std::ldexp(1.0, -21));
+  fp.a1 = static_cast<float>(a1 * (1.0 + 1e-6));
+  fp.a0 = static_cast<float>(a0 * (1.0 + 1e-6));
+  if (!exact) return true;
+  // worst-case T over all u8 inputs: OD is largest at i = 0
+  double tmax = 4.0 * sp.lam;
+  for (int c = 0; c < 3; ++c) tmax += (sp.ws[c][0] + sp.ws[c][1]) * sp.lut[c][0];
+  if (a1 * tmax + a0 > 1e-3) return false;
+  // zero-density pixels render exactly i0_t; the interval around an exact tie
+  // (i0_t = k + 0.5) can never certify, so such targets take the strict path
+  const double a_zero = a1 * 4.0 * sp.lam + a0;
+  for (int c = 0; c < 3; ++c) {
+    const double fr = sp.i0t[c] - std::floor(sp.i0t[c]);
+    if (std::fabs(fr - 0.5) <= 2.0 * a_zero * sp.i0t[c] + 1e-9) return false;
+  }
+  return true;
+}
+
+constexpr size_t kWsHeader = 16;
+
+}  // namespace
+
+extern "C" {
+
+const char* spcn_last_error(void) { return g_err.c_str(); }
+
+const char* spcn_version(void) { return "spcn-b200 0.1.0 (sm_100a)"; }
+
+size_t spcn_xform_workspace_bytes(int64_t npix) {
+  const int64_t cap = 65536 + (npix > 0 ? npix / 32 : 0);
+  return kWsHeader + static_cast<size_t>(cap) * 8;
+}
+
+int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_xform_params* p,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!p) return fail(SPCN_EINVAL, "params is NULL");
+  if (npix < 0) return fail(SPCN_EINVAL, "npix must be >= 0");
+  if (npix == 0) return SPCN_OK;
+  if (!src || !dst) return fail(SPCN_EINVAL, "src/dst is NULL");
+  if (p->precision < 0 || p->precision > 2) return fail(SPCN_EINVAL, "unknown precision");
+  for (int c = 0; c < 3; ++c) {
+    if (!(p->src_i0[c] >= 1.0) || !std::isfinite(p->src_i0[c]))
+      return fail(SPCN_EINVAL, "i0 components must be >= 1");
+    if (!std::isfinite(p->tgt_i0[c])) return fail(SPCN_EINVAL, "target i0 must be finite");
+  }
+  int rc = check_basis(p->src_basis, "source");
+  if (rc) return rc;
+  if ((rc = check_basis(p->tgt_basis, "target"))) return rc;
+  if (!(p->code_lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
+  for (int j = 0; j < 2; ++j)
+    if (!(p->factors[j] > 0.0) || !std::isfinite(p->factors[j]))
+      return fail(SPCN_EINVAL, "factors must be positive and finite");
+  if (p->max_sweeps < 0) return fail(SPCN_EINVAL, "max_sweeps must be >= 0");
+
+  double lut[3][256];
+  od_table(p->src_i0, p->od_table, lut);
+  static thread_local StrictP sp;
+  static thread_local FastP fp;
+  fill_strict(sp, &lut[0][0], p->src_basis, p->tgt_basis, p->factors, p->tgt_i0, p->code_lam,
+              p->max_sweeps);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool exact = p->precision == SPCN_PREC_EXACT;
+  bool fast_ok = p->precision != SPCN_PREC_STRICT && fill_fast(fp, sp, exact);
+
+  // 16-byte alignment of the vector body (both buffers must share the phase)
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
+  if (((sa - da) & 15u) != 0) fast_ok = false;
+  int64_t head = static_cast<int64_t>(((16 - (sa & 15u)) * 11u) & 15u);  // 3*head == -sa (mod 16)
+  if (head > npix) head = npix;
+  const int64_t body = fast_ok ? ((npix - head) / 16) * 16 : 0;
+  if (!fast_ok || body == 0) {
+    cudaError_t e = launch_xform_strict(src, dst, npix, sp, st);
+    return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "xform_strict");
+  }
+  unsigned long long* count = nullptr;
+  unsigned long long* items = nullptr;
+  unsigned long long cap = 0;
+  if (exact) {
+    if (!workspace || workspace_bytes < kWsHeader + 8)
+      return fail(SPCN_EINVAL, "EXACT precision needs a workspace (spcn_xform_workspace_bytes)");
+    count = static_cast<unsigned long long*>(workspace);
+    items = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + kWsHeader);
+    cap = (workspace_bytes - kWsHeader) / 8;
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_fail(e, "memset");
+  }
+  cudaError_t e;
+  if (head > 0 && (e = launch_xform_strict(src, dst, head, sp, st)) != cudaSuccess)
+    return cuda_fail(e, "xform_head");
+  e = launch_xform_tma(exact ? 0 : 1, src + 3 * head, dst + 3 * head, body, fp, sp, count, items,
+                       cap, st);
+  if (e != cudaSuccess) return cuda_fail(e, "xform_tma");
+  if (exact && (e = launch_xform_repair(dst + 3 * head, sp, count, items, cap, st)) != cudaSuccess)
+    return cuda_fail(e, "xform_repair");
+  const int64_t tail0 = head + body;
+  if (tail0 < npix &&
+      (e = launch_xform_strict(src + 3 * tail0, dst + 3 * tail0, npix - tail0, sp, st)) != cudaSuccess)
+    return cuda_fail(e, "xform_tail");
+  return SPCN_OK;
+}
+
+int spcn_xform_repair_count(const void* workspace, void* stream, int64_t* count) {
+  g_err.clear();
+  if (!workspace || !count) return fail(SPCN_EINVAL, "NULL argument");
+  unsigned long long c = 0;
+  cudaError_t e = cudaMemcpyAsync(&c, workspace, sizeof(c), cudaMemcpyDeviceToHost,
+                                  static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "repair_count");
+  *count = static_cast<int64_t>(c);
+  return SPCN_OK;
+}
+
+int spcn_code_densities(const double* od, double* h, int64_t n, const double* basis, double lam,
+                        int32_t max_sweeps, void* stream) {
+  g_err.clear();
+  if (n < 0) return fail(SPCN_EINVAL, "n must be >= 0");
+  if (!basis) return fail(SPCN_EINVAL, "basis is NULL");
+  int rc = check_basis(basis, "stain");
+  if (rc) return rc;
+  if (!(lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
+  if (max_sweeps < 0) return fail(SPCN_EINVAL, "max_sweeps must be >= 0");
+  if (n == 0) return SPCN_OK;
+  if (!od || !h) return fail(SPCN_EINVAL, "od/h is NULL");
+  static thread_local StrictP sp;
+  static const double zero_lut[3 * 256] = {0};
+  fill_strict(sp, zero_lut, basis, nullptr, nullptr, nullptr, lam, max_sweeps);
+  cudaError_t e = launch_code_densities(od, h, n, sp, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "code_densities");
+}
+
+int spcn_normalize_block(const double* h, uint8_t* out, int64_t n, const double* factors,
+                         const double* tgt_basis, const double* tgt_i0, void* stream) {
+  g_err.clear();
+  if (n < 0) return fail(SPCN_EINVAL, "n must be >= 0");
+  if (!factors || !tgt_basis || !tgt_i0) return fail(SPCN_EINVAL, "NULL argument");
+  int rc = check_basis(tgt_basis, "target");
+  if (rc) return rc;
+  for (int j = 0; j < 2; ++j)
+    if (!(factors[j] > 0.0) || !std::isfinite(factors[j]))
+      return fail(SPCN_EINVAL, "factors must be positive and finite");
+  if (n == 0) return SPCN_OK;
+  if (!h || !out) return fail(SPCN_EINVAL, "h/out is NULL");
+  static thread_local StrictP sp;
+  static const double zero_lut[3 * 256] = {0};
+  fill_strict(sp, zero_lut, nullptr, tgt_basis, factors, tgt_i0, 0.0, 0);
+  cudaError_t e = launch_normalize_block(h, out, n, sp, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "normalize_block");
+}
+
+int spcn_beer_lambert(const uint8_t* px, double* od, int64_t n, const double* i0,
+                      const double* od_table_in, void* stream) {
+  g_err.clear();
+  if (n < 0) return fail(SPCN_EINVAL, "n must be >= 0");
+  if (!i0) return fail(SPCN_EINVAL, "i0 is NULL");
+  for (int c = 0; c < 3; ++c)
+    if (!(i0[c] >= 1.0)) return fail(SPCN_EINVAL, "i0 components must be >= 1");
+  if (n == 0) return SPCN_OK;
+  if (!px || !od) return fail(SPCN_EINVAL, "px/od is NULL");
+  double lut[3][256];
+  od_table(i0, od_table_in, lut);
+  static thread_local StrictP sp;
+  fill_strict(sp, &lut[0][0], nullptr, nullptr, nullptr, nullptr, 0.0, 0);
+  cudaError_t e = launch_beer_lambert(px, od, n, sp, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "beer_lambert");
+}
+
+int spcn_inverse_beer_lambert(const double* od, uint8_t* out, int64_t n, const double* i0,
+                              void* stream) {
+  g_err.clear();
+  if (n < 0) return fail(SPCN_EINVAL, "n must be >= 0");
+  if (!i0) return fail(SPCN_EINVAL, "i0 is NULL");
+  if (n == 0) return SPCN_OK;
+  if (!od || !out) return fail(SPCN_EINVAL, "od/out is NULL");
+  static thread_local StrictP sp;
+  static const double zero_lut[3 * 256] = {0};
+  fill_strict(sp, zero_lut, nullptr, nullptr, nullptr, i0, 0.0, 0);
+  cudaError_t e = launch_inverse_bl(od, out, n, sp, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "inverse_beer_lambert");
+}
+
+}  // extern "C"

@@ -1,0 +1,251 @@
+// sample.cu — device side of the fit's pixel sampling (K4) and background
+// estimate (K5).
+//
+// Reference: sample_pixels src/pipeline.py:128-200 and estimate_max_intensity
+// src/optics.py:35-68.  The reference visits seeded random patches in order,
+// keeps per channel the first `cap` values > thr in raster order (bright
+// pools), and the first `target - collected` non-white pixels in raster order
+// of each non-background patch.  The visit logic depends only on per-patch
+// counts, so it runs in two data-parallel passes with a tiny host step
+// between them:
+//   k_sample_count   per-patch, per-4096-pixel-chunk counts (non-white and
+//                    bright per channel) — integer work, exact;
+//   (host)           replays the reference's visit loop on the counts;
+//   k_sample_compact ordered compaction: block scan inside each chunk plus the
+//                    prefix of earlier chunks gives every pixel its raster rank,
+//                    so "first N in raster order" is reproduced exactly; the
+//                    taken bright values go straight into 256-bin histograms.
+//   k_i0_from_hist   exact 80th percentile of the bright pools from the counts.
+#include "spcn_device.cuh"
+#include "spcn.h"
+#include "sample.h"
+
+namespace spcn {
+
+constexpr int kChunk = SPCN_SAMPLE_CHUNK;     // raster pixels per chunk (4096)
+constexpr int kSThreads = 256;
+constexpr int kPerThread = kChunk / kSThreads; // 16
+
+__device__ __forceinline__ const uint8_t* patch_px(const uint8_t* img, const spcn_patch& p,
+                                                   int64_t r) {
+  const int64_t row = r / p.width, col = r - row * p.width;
+  return img + 3 * (p.base + row * p.row_stride + col);
+}
+
+template <int N>
+__device__ __forceinline__ void block_sum(int (&v)[N], int (*scratch)[N]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < N; ++q) scratch[warp][q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      int s = 0;
+      for (int w = 0; w < kSThreads / 32; ++w) s += scratch[w][q];
+      v[q] = s;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSThreads) k_sample_count(const uint8_t* __restrict__ img,
+                                                            const spcn_patch* __restrict__ patches,
+                                                            int max_chunks, int thr,
+                                                            int32_t* __restrict__ counts) {
+  const int k = blockIdx.x, pi = blockIdx.y;
+  const spcn_patch p = patches[pi];
+  const int64_t npx = (int64_t)p.width * p.height;
+  const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
+  int c[4] = {0, 0, 0, 0};  // non-white, bright R, G, B
+  if ((int64_t)k * kChunk < npx) {
+    for (int j = 0; j < kPerThread; ++j) {
+      const int64_t r = r0 + j;
+      if (r >= npx) break;
+      const uint8_t* q = patch_px(img, p, r);
+      const int a = q[0], b = q[1], d = q[2];
+      c[0] += !(a > thr && b > thr && d > thr);
+      c[1] += a > thr;
+      c[2] += b > thr;
+      c[3] += d > thr;
+    }
+  }
+  __shared__ int scratch[kSThreads / 32][4];
+  block_sum<4>(c, scratch);
+  if (threadIdx.x == 0) {
+    int32_t* o = counts + ((int64_t)pi * max_chunks + k) * 4;
+    o[0] = c[0]; o[1] = c[1]; o[2] = c[2]; o[3] = c[3];
+  }
+}
+
+__global__ void __launch_bounds__(kSThreads) k_sample_compact(
+    const uint8_t* __restrict__ img, const spcn_patch* __restrict__ patches, int max_chunks,
+    int thr, const int32_t* __restrict__ counts, const spcn_patch_take* __restrict__ takes,
+    uint8_t* __restrict__ out_px, int32_t* __restrict__ bright_hist) {
+  const int k = blockIdx.x, pi = blockIdx.y;
+  const spcn_patch p = patches[pi];
+  const spcn_patch_take tk = takes[pi];
+  const int64_t npx = (int64_t)p.width * p.height;
+  if ((int64_t)k * kChunk >= npx) return;
+  __shared__ int s_pre[4];
+  __shared__ int scratch[kSThreads / 32][4];
+  __shared__ int s_hist[3][256];
+  __shared__ int s_wsum[kSThreads / 32][4];
+  // prefix over earlier chunks of this patch
+  int pre[4] = {0, 0, 0, 0};
+  for (int j = threadIdx.x; j < k; j += kSThreads) {
+    const int32_t* c = counts + ((int64_t)pi * max_chunks + j) * 4;
+    pre[0] += c[0]; pre[1] += c[1]; pre[2] += c[2]; pre[3] += c[3];
+  }
+  block_sum<4>(pre, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 4; ++q) s_pre[q] = pre[q];
+  for (int i = threadIdx.x; i < 3 * 256; i += kSThreads) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t pnw = s_pre[0];
+  const int pb[3] = {s_pre[1], s_pre[2], s_pre[3]};
+  const bool need = pnw < tk.take_nonwhite || pb[0] < tk.take_bright[0] ||
+                    pb[1] < tk.take_bright[1] || pb[2] < tk.take_bright[2];
+  if (!need) return;  // uniform across the block
+
+  // per-thread flags for its 16 raster-consecutive pixels
+  const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
+  uint32_t rgb[kPerThread];
+  int cnt[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j) {
+    const int64_t r = r0 + j;
+    if (r < npx) {
+      const uint8_t* q = patch_px(img, p, r);
+      rgb[j] = q[0] | (q[1] << 8) | (q[2] << 16);
+      const int a = q[0], b = q[1], d = q[2];
+      cnt[0] += !(a > thr && b > thr && d > thr);
+      cnt[1] += a > thr;
+      cnt[2] += b > thr;
+      cnt[3] += d > thr;
+    } else {
+      rgb[j] = 0xffffffffu;  // sentinel: not a pixel
+    }
+  }
+  // block exclusive scan of the four counters
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    inc[q] = cnt[q];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc[q], off);
+      if (lane >= off) inc[q] += y;
+    }
+  }
+  if (lane == 31)
+    for (int q = 0; q < 4; ++q) s_wsum[warp][q] = inc[q];
+  __syncthreads();
+  int rank[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_wsum[w][q];
+    rank[q] = s_pre[q] + wpre + inc[q] - cnt[q];
+  }
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j) {
+    if (rgb[j] == 0xffffffffu) continue;
+    const int a = rgb[j] & 255, b = (rgb[j] >> 8) & 255, d = (rgb[j] >> 16) & 255;
+    if (!(a > thr && b > thr && d > thr)) {
+      if (rank[0] < tk.take_nonwhite) {
+        uint8_t* o = out_px + 3 * (tk.out_base + rank[0]);
+        o[0] = a; o[1] = b; o[2] = d;
+      }
+      ++rank[0];
+    }
+    if (a > thr) { if (rank[1] < tk.take_bright[0]) atomicAdd(&s_hist[0][a], 1); ++rank[1]; }
+    if (b > thr) { if (rank[2] < tk.take_bright[1]) atomicAdd(&s_hist[1][b], 1); ++rank[2]; }
+    if (d > thr) { if (rank[3] < tk.take_bright[2]) atomicAdd(&s_hist[2][d], 1); ++rank[3]; }
+  }
+  __syncthreads();
+  int32_t* gh = bright_hist + (int64_t)tk.problem * 3 * 256;
+  for (int i = threadIdx.x; i < 3 * 256; i += kSThreads) {
+    const int v = (&s_hist[0][0])[i];
+    if (v) atomicAdd(&gh[i], v);
+  }
+}
+
+// Exact 80th percentile of 8-bit pools from their 256-bin counts
+// (percentile src/order_stats.py:27-36 on the expanded multiset).
+__global__ void k_i0_from_hist(const int32_t* __restrict__ hist, int nprob,
+                               double* __restrict__ i0, int32_t* __restrict__ empty) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nprob * 3) return;
+  const int32_t* h = hist + (int64_t)idx * 256;
+  int64_t n = 0;
+  for (int v = 0; v < 256; ++v) n += h[v];
+  if (n == 0) {
+    i0[idx] = 255.0;
+    empty[idx] = 1;
+    return;
+  }
+  empty[idx] = 0;
+  const double rank = __dmul_rn(80.0 / 100.0, (double)(n - 1));
+  const int64_t lo = (int64_t)floor(rank), hi = (int64_t)ceil(rank);
+  int64_t cum = 0;
+  int lov = -1, hiv = -1;
+  for (int v = 0; v < 256 && hiv < 0; ++v) {
+    cum += h[v];
+    if (lov < 0 && cum > lo) lov = v;
+    if (cum > hi) hiv = v;
+  }
+  const double frac = __dsub_rn(rank, (double)lo);
+  i0[idx] = __dadd_rn((double)lov, __dmul_rn(__dsub_rn((double)hiv, (double)lov), frac));
+}
+
+// Per-problem OD tables ln(i0_c / clip(i, 1, i0_c)) (src/optics.py:92-94).
+__global__ void k_od_tables(const double* __restrict__ i0, int nprob, double* __restrict__ lut) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nprob * 3 * 256) return;
+  const int64_t pc = idx / 256;
+  const int i = (int)(idx - pc * 256);
+  const double a = i0[pc];
+  double x = (double)i;
+  x = x < 1.0 ? 1.0 : (x > a ? a : x);
+  lut[idx] = log(__ddiv_rn(a, x));
+}
+
+cudaError_t launch_sample_count(const uint8_t* img, const spcn_patch* patches, int npatches,
+                                int max_chunks, int thr, int32_t* counts, cudaStream_t st) {
+  if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;
+  k_sample_count<<<dim3(max_chunks, npatches), kSThreads, 0, st>>>(img, patches, max_chunks, thr,
+                                                                   counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches, int npatches,
+                                  int max_chunks, int thr, const int32_t* counts,
+                                  const spcn_patch_take* takes, uint8_t* out_px,
+                                  int32_t* bright_hist, cudaStream_t st) {
+  if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;
+  k_sample_compact<<<dim3(max_chunks, npatches), kSThreads, 0, st>>>(
+      img, patches, max_chunks, thr, counts, takes, out_px, bright_hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_i0_from_hist(const int32_t* hist, int nprob, double* i0, int32_t* empty,
+                                cudaStream_t st) {
+  if (nprob <= 0) return cudaSuccess;
+  k_i0_from_hist<<<(nprob * 3 + 127) / 128, 128, 0, st>>>(hist, nprob, i0, empty);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_od_tables(const double* i0, int nprob, double* lut, cudaStream_t st) {
+  if (nprob <= 0) return cudaSuccess;
+  const int64_t n = (int64_t)nprob * 3 * 256;
+  k_od_tables<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(i0, nprob, lut);
+  return cudaGetLastError();
+}
+
+}  // namespace spcn

@@ -1,0 +1,17 @@
+// sample.h — launch interface of the sampling / i0 kernels (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "spcn.h"
+
+namespace spcn {
+cudaError_t launch_sample_count(const uint8_t* img, const spcn_patch* patches, int npatches,
+                                int max_chunks, int thr, int32_t* counts, cudaStream_t st);
+cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches, int npatches,
+                                  int max_chunks, int thr, const int32_t* counts,
+                                  const spcn_patch_take* takes, uint8_t* out_px,
+                                  int32_t* bright_hist, cudaStream_t st);
+cudaError_t launch_i0_from_hist(const int32_t* hist, int nprob, double* i0, int32_t* empty,
+                                cudaStream_t st);
+cudaError_t launch_od_tables(const double* i0, int nprob, double* lut, cudaStream_t st);
+}  // namespace spcn

@@ -1,0 +1,72 @@
+"""The per-pixel hot unit: ``process_strip`` ≙ src/pipeline.py:260-272.
+
+``process_strip(pixels, src_i0, src_basis, code_lam, factors, tgt_basis,
+tgt_i0)`` has the reference's signature and semantics (pure per pixel, any
+chunking gives identical bytes) and runs one fused libspcn launch
+(``spcn_xform_rgb8``).  ``XformPlan`` prepares the C parameter block once per
+(source, target) pair so a whole-slide transform pays the host setup once.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _dev, _lib
+from .optics import od_table
+
+
+class XformPlan:
+    """Packed spcn_xform_params for one recoloring (host-side, reusable)."""
+
+    def __init__(self, src_i0, src_basis, code_lam, factors, tgt_basis, tgt_i0,
+                 precision: str = "exact", max_sweeps: int = 2000):
+        if precision not in _lib.PREC:
+            raise ValueError(f"precision must be one of {sorted(_lib.PREC)}")
+        self.table = od_table(src_i0)               # exact reference OD table (host numpy)
+        p = _lib.XformParams()
+        p.src_i0[:] = [float(x) for x in _dev.f64_array(src_i0, 3, "src_i0")]
+        p.src_basis[:] = [float(x) for x in _dev.f64_array(src_basis, 6, "src_basis")]
+        p.code_lam = float(code_lam)
+        p.factors[:] = [float(x) for x in _dev.f64_array(factors, 2, "factors")]
+        p.tgt_basis[:] = [float(x) for x in _dev.f64_array(tgt_basis, 6, "tgt_basis")]
+        p.tgt_i0[:] = [float(x) for x in _dev.f64_array(tgt_i0, 3, "tgt_i0")]
+        p.od_table = self.table.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        p.precision = _lib.PREC[precision]
+        p.max_sweeps = int(max_sweeps)
+        self.params = p
+        self.precision = precision
+
+    def run(self, src, dst, npix: int, stream=None) -> None:
+        """src/dst: CUDA uint8 tensors (or raw device pointers) holding npix RGB pixels."""
+        L = _lib.lib()
+        ws_bytes = int(L.spcn_xform_workspace_bytes(int(npix)))
+        ws = _dev.workspace(ws_bytes)
+        sp = src if isinstance(src, int) else _lib.ptr(src)
+        dp = dst if isinstance(dst, int) else _lib.ptr(dst)
+        _lib.check(L.spcn_xform_rgb8(sp, dp, int(npix), ctypes.byref(self.params), _lib.ptr(ws),
+                                     ws_bytes, _lib.stream_handle(stream)), "xform_rgb8")
+
+    def repair_count(self, stream=None) -> int:
+        """Pixels sent to the fp64 repair path by the last EXACT run (synchronizes)."""
+        L = _lib.lib()
+        ws = _dev.workspace(16)
+        out = ctypes.c_int64(0)
+        _lib.check(L.spcn_xform_repair_count(_lib.ptr(ws), _lib.stream_handle(stream),
+                                             ctypes.byref(out)), "repair_count")
+        return int(out.value)
+
+
+def process_strip(pixels, src_i0, src_basis, code_lam, factors, tgt_basis, tgt_i0,
+                  precision: str = "exact", out=None):
+    """Recolor one strip (src/pipeline.py:260-272).  numpy in → numpy out,
+    CUDA tensor in → CUDA tensor out (``out`` may be given for the latter)."""
+    t = _dev.torch()
+    host = not _dev.is_tensor(pixels)
+    src = _dev.to_device(pixels, dtype=t.uint8)
+    if src.ndim != 3 or src.shape[2] != 3:
+        raise ValueError("pixels must be (h, w, 3) uint8")
+    dst = out if out is not None else t.empty_like(src)
+    plan = XformPlan(src_i0, src_basis, code_lam, factors, tgt_basis, tgt_i0, precision)
+    plan.run(src, dst, src.numel() // 3)
+    return dst.cpu().numpy() if host else dst

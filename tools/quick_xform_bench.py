@@ -1,0 +1,45 @@
+"""Quick device-resident timing of the recolor kernel per precision mode.
+
+python tools/quick_xform_bench.py [--mpx 100]
+Prints ms, Mpx/s, GB/s (6 B/px algorithmic) and the EXACT repair fraction.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1901_03088_b200 as pb  # noqa: E402
+from oracle import spcn_oracle as orc  # noqa: E402  (fixture generator only)
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--mpx", type=int, default=100)
+ap.add_argument("--iters", type=int, default=20)
+args = ap.parse_args()
+
+tile, _, _ = orc.render(2048, 2048, 1, tissue_fraction=0.6)
+reps = max(1, (args.mpx * 1_000_000) // (2048 * 2048))
+src = torch.from_numpy(tile).cuda().repeat(reps, 1, 1).contiguous()
+dst = torch.empty_like(src)
+npix = src.numel() // 3
+w = orc.he_basis()
+rot = np.array([[0.58, 0.12], [0.74, 0.93], [0.33, 0.35]])
+rot /= np.linalg.norm(rot, axis=0)
+for prec in ("fast", "exact", "strict"):
+    plan = pb.XformPlan([255.0] * 3, w, 0.0, [1.2, 0.85], rot, [250.0, 246.0, 240.0], prec)
+    for _ in range(3):
+        plan.run(src, dst, npix)
+    torch.cuda.synchronize()
+    iters = args.iters if prec != "strict" else 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        plan.run(src, dst, npix)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    rep = plan.repair_count() if prec == "exact" else 0
+    print(f"{prec:6s} npix={npix} {ms:.3f} ms  {npix / ms / 1e3:.1f} Mpx/s  "
+          f"{6 * npix / ms / 1e6:.1f} GB/s  repaired={rep} ({rep / npix:.4%})", flush=True)
