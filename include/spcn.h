@@ -146,6 +146,50 @@ int spcn_i0_from_hist(const int32_t* hist, int32_t nprob, double* i0, int32_t* e
 /* Per-problem OD tables lut[p][c][i] = ln(i0[p][c] / clip(i,1,i0[p][c])).   */
 int spcn_od_tables(const double* i0, int32_t nprob, double* lut, void* stream);
 
+/* ---- fit: sparse-NMF basis, density coding, p99 ------------------------ */
+typedef struct spcn_snmf_cfg {
+  double lam;            /* SnmfConfig.lam (src/stain_sep.py:50), 0.1 default  */
+  double rel_tol;        /* SnmfConfig.rel_tol, 1e-6                          */
+  double w_init[6];      /* initial basis (row-major 3x2): reference_basis() +
+                            default_rng(seed).uniform(0, 0.05), clamped and
+                            column-normalised (src/stain_sep.py:271-274)      */
+  int32_t max_outer;     /* SnmfConfig.max_outer_iters, 200                   */
+  int32_t cluster;       /* CTAs per problem (1 = batched, 8 = single slide)  */
+} spcn_snmf_cfg;
+
+/* Batched fit_basis (src/stain_sep.py:239-336).  Problem p's sample is the
+ * RGB8 pixels [offsets[p], offsets[p+1]) of `samples`, coded to OD through
+ * luts[p] (3x256 fp64).  Writes the ordered basis (nprob x 6, row-major),
+ * (or, when `od` is non-NULL, the fp64 OD columns od[c*total + i], c = 0..2,
+ * in which case `samples`/`luts` are ignored) and writes the objective history (nprob x (max_outer+1)) and info (nprob x 4:
+ * iterations, converged, warning flags bit0=no-convergence bit1=one-stain,
+ * history length).  hscratch: 2*total fp64.  All pointers device.          */
+int spcn_snmf_batched(const uint8_t* samples, const double* od, const int64_t* offsets,
+                      int32_t nprob,
+                      const double* luts, const spcn_snmf_cfg* cfg, double* hscratch,
+                      int64_t total, double* basis_out, double* history_out,
+                      int32_t* info_out, void* stream);
+
+/* Batched code_densities of the fit samples (src/pipeline.py:226): h[j*total
+ * + i] for the pixels of every problem with its own table and basis.        */
+int spcn_code_samples(const uint8_t* samples, const int64_t* offsets, int32_t nprob,
+                      int64_t max_m, const double* luts, const double* bases, double lam,
+                      int32_t max_sweeps, double* h, int64_t total, void* stream);
+
+/* Per-segment, per-stain percentile p of densities h (2 x total, fp64):
+ * stain_stats src/normalize.py:83-100 with percentile src/order_stats.py:11-36
+ * computed by exact radix select.  out[s*2+j]; absent[s*2+j] = 1 when the
+ * segment is empty or its max is <= 0 (StainAbsentError).  Scratch: qbuf of
+ * 6*nseg*32 bytes, selbuf of 6*nseg doubles (device).                      */
+int spcn_percentile_segments(const double* h, int64_t total, const int64_t* seg_offsets,
+                             int32_t nseg, double p, void* qbuf, double* selbuf, double* out,
+                             int32_t* absent, void* stream);
+
+/* Generic exact k-th smallest (0-based) of values[begin, end) for nq queries
+ * given as device arrays; out[q] (device).                                  */
+int spcn_select_kth(const double* values, const int64_t* begin, const int64_t* end,
+                    const int64_t* k, int32_t nq, void* qbuf, double* out, void* stream);
+
 /* Thread-local description of the last error ("" if none).                 */
 const char* spcn_last_error(void);
 

@@ -19,6 +19,10 @@ from .optics import beer_lambert, estimate_max_intensity, inverse_beer_lambert  
 from .stain_sep import (  # noqa: F401
     SnmfConfig, SnmfFit, code_densities, fit_basis, order_stains, reference_basis,
 )
+from .order_stats import median, percentile  # noqa: F401
+from .pipeline import (  # noqa: F401
+    BufferGauge, PixelSample, RunStats, SamplePlan, fit, normalize, sample_pixels, transform,
+)
 from .xform import XformPlan, process_strip  # noqa: F401
 
 __version__ = "0.1.0"

@@ -310,3 +310,124 @@ int spcn_inverse_beer_lambert(const double* od, uint8_t* out, int64_t n, const d
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ fit entry points
+#include "sample.h"
+#include "select.h"
+#include "snmf.h"
+
+extern "C" {
+
+int spcn_sample_count(const uint8_t* img, const spcn_patch* patches, int32_t npatches,
+                      int32_t max_chunks, int32_t white_threshold, int32_t* counts,
+                      void* stream) {
+  g_err.clear();
+  if (npatches < 0 || max_chunks < 0) return fail(SPCN_EINVAL, "negative size");
+  if (npatches == 0) return SPCN_OK;
+  if (!img || !patches || !counts) return fail(SPCN_EINVAL, "NULL argument");
+  cudaError_t e = launch_sample_count(img, patches, npatches, max_chunks, white_threshold, counts,
+                                      static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "sample_count");
+}
+
+int spcn_sample_compact(const uint8_t* img, const spcn_patch* patches, int32_t npatches,
+                        int32_t max_chunks, int32_t white_threshold, const int32_t* counts,
+                        const spcn_patch_take* takes, uint8_t* out_px, int32_t* bright_hist,
+                        void* stream) {
+  g_err.clear();
+  if (npatches < 0 || max_chunks < 0) return fail(SPCN_EINVAL, "negative size");
+  if (npatches == 0) return SPCN_OK;
+  if (!img || !patches || !counts || !takes || !bright_hist) return fail(SPCN_EINVAL, "NULL argument");
+  cudaError_t e = launch_sample_compact(img, patches, npatches, max_chunks, white_threshold, counts,
+                                        takes, out_px, bright_hist,
+                                        static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "sample_compact");
+}
+
+int spcn_i0_from_hist(const int32_t* hist, int32_t nprob, double* i0, int32_t* empty,
+                      void* stream) {
+  g_err.clear();
+  if (nprob < 0) return fail(SPCN_EINVAL, "negative size");
+  if (nprob == 0) return SPCN_OK;
+  if (!hist || !i0 || !empty) return fail(SPCN_EINVAL, "NULL argument");
+  cudaError_t e = launch_i0_from_hist(hist, nprob, i0, empty, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "i0_from_hist");
+}
+
+int spcn_od_tables(const double* i0, int32_t nprob, double* lut, void* stream) {
+  g_err.clear();
+  if (nprob < 0) return fail(SPCN_EINVAL, "negative size");
+  if (nprob == 0) return SPCN_OK;
+  if (!i0 || !lut) return fail(SPCN_EINVAL, "NULL argument");
+  cudaError_t e = launch_od_tables(i0, nprob, lut, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "od_tables");
+}
+
+int spcn_snmf_batched(const uint8_t* samples, const double* od, const int64_t* offsets,
+                      int32_t nprob,
+                      const double* luts, const spcn_snmf_cfg* cfg, double* hscratch,
+                      int64_t total, double* basis_out, double* history_out, int32_t* info_out,
+                      void* stream) {
+  g_err.clear();
+  if (!cfg) return fail(SPCN_EINVAL, "cfg is NULL");
+  if (nprob < 0 || total < 0) return fail(SPCN_EINVAL, "negative size");
+  if (!(cfg->lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
+  if (cfg->max_outer < 1) return fail(SPCN_EINVAL, "max_outer_iters must be >= 1");
+  if (!(cfg->rel_tol > 0.0)) return fail(SPCN_EINVAL, "rel_tol must be > 0");
+  if (cfg->cluster < 1 || cfg->cluster > 8) return fail(SPCN_EINVAL, "cluster must be in [1, 8]");
+  if (nprob == 0) return SPCN_OK;
+  if ((!od && (!samples || !luts)) || !offsets || !hscratch || !basis_out || !history_out || !info_out)
+    return fail(SPCN_EINVAL, "NULL argument");
+  SnmfArgs a;
+  a.lam = cfg->lam;
+  a.rel_tol = cfg->rel_tol;
+  for (int i = 0; i < 6; ++i) a.w_init[i] = cfg->w_init[i];
+  a.max_outer = cfg->max_outer;
+  a.pad_ = 0;
+  cudaError_t e = launch_snmf(samples, od, offsets, nprob, luts, a, hscratch, total, basis_out,
+                              history_out, info_out, cfg->cluster,
+                              static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "snmf");
+}
+
+int spcn_code_samples(const uint8_t* samples, const int64_t* offsets, int32_t nprob,
+                      int64_t max_m, const double* luts, const double* bases, double lam,
+                      int32_t max_sweeps, double* h, int64_t total, void* stream) {
+  g_err.clear();
+  if (nprob < 0 || total < 0) return fail(SPCN_EINVAL, "negative size");
+  if (!(lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
+  if (max_sweeps < 0) return fail(SPCN_EINVAL, "max_sweeps must be >= 0");
+  if (nprob == 0 || total == 0) return SPCN_OK;
+  if (!samples || !offsets || !luts || !bases || !h) return fail(SPCN_EINVAL, "NULL argument");
+  cudaError_t e = launch_code_samples(samples, offsets, nprob, max_m, luts, bases, lam, max_sweeps,
+                                      h, total, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "code_samples");
+}
+
+int spcn_percentile_segments(const double* h, int64_t total, const int64_t* seg_offsets,
+                             int32_t nseg, double p, void* qbuf, double* selbuf, double* out,
+                             int32_t* absent, void* stream) {
+  g_err.clear();
+  if (nseg < 0 || total < 0) return fail(SPCN_EINVAL, "negative size");
+  if (!(p >= 0.0 && p <= 100.0)) return fail(SPCN_EINVAL, "percentile p must be in [0, 100]");
+  if (nseg == 0) return SPCN_OK;
+  if (!h || !seg_offsets || !qbuf || !selbuf || !out || !absent)
+    return fail(SPCN_EINVAL, "NULL argument");
+  cudaError_t e = launch_p99(h, total, seg_offsets, nseg, p, static_cast<SelQuery*>(qbuf), selbuf,
+                             out, absent, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "percentile_segments");
+}
+
+int spcn_select_kth(const double* values, const int64_t* begin, const int64_t* end,
+                    const int64_t* k, int32_t nq, void* qbuf, double* out, void* stream) {
+  g_err.clear();
+  if (nq < 0) return fail(SPCN_EINVAL, "negative size");
+  if (nq == 0) return SPCN_OK;
+  if (!values || !begin || !end || !k || !qbuf || !out) return fail(SPCN_EINVAL, "NULL argument");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_build_queries(begin, end, k, nq, static_cast<SelQuery*>(qbuf), st);
+  if (e == cudaSuccess) e = launch_select(values, static_cast<SelQuery*>(qbuf), nq, out, st);
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "select_kth");
+}
+
+}  // extern "C"

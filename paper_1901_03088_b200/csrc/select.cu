@@ -1,0 +1,168 @@
+// select.cu — exact order statistics on the device (K3/K7b).
+//
+// Reference: percentile src/order_stats.py:11-36 (sorted[lo] + (sorted[hi] -
+// sorted[lo]) * frac, rank = p/100*(n-1)) as used by stain_stats
+// src/normalize.py:83-100.  A sort is not needed: each query is an MSD radix
+// select over the fp64 bit patterns (mapped to order-preserving uint64),
+// 11-bit digits, shared-memory histograms, one CTA per query.  Exact by
+// construction (integer counting), so percentile-histogram counts are
+// bit-exact given identical densities.
+#include "select.h"
+#include "spcn_device.cuh"
+
+namespace spcn {
+
+constexpr int kSelThreads = 512;
+constexpr int kDigit = 11;
+constexpr int kBins = 1 << kDigit;
+
+__device__ __forceinline__ uint64_t key_of(double x) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double val_of(uint64_t k) {
+  const uint64_t b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+// keys: values[stride*j + i] for i in [begin, end) — j = component (stain) picked per query
+__global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict__ values,
+                                                       const SelQuery* __restrict__ qs,
+                                                       double* __restrict__ out) {
+  const SelQuery q = qs[blockIdx.x];
+  __shared__ uint32_t hist[kBins];
+  __shared__ uint32_t s_scan[kSelThreads];
+  __shared__ uint64_t s_prefix;
+  __shared__ int64_t s_k;
+  if (threadIdx.x == 0) {
+    s_prefix = 0;
+    s_k = q.k;
+  }
+  const double* v = values + q.offset;
+  int used = 0;  // bits of the prefix fixed so far
+  while (used < 64) {
+    const int dbits = (64 - used) < kDigit ? (64 - used) : kDigit;
+    const int shift = 64 - used - dbits;
+    for (int i = threadIdx.x; i < kBins; i += kSelThreads) hist[i] = 0;
+    __syncthreads();
+    const uint64_t prefix = s_prefix;
+    for (int64_t i = q.begin + threadIdx.x; i < q.end; i += kSelThreads) {
+      const uint64_t key = key_of(v[i]);
+      if (used == 0 || (key >> (64 - used)) == prefix) {
+        atomicAdd(&hist[(key >> shift) & ((1u << dbits) - 1u)], 1u);
+      }
+    }
+    __syncthreads();
+    // locate the digit holding rank k: per-thread chunk sums + block scan
+    constexpr int kPer = kBins / kSelThreads;  // 4 bins per thread
+    uint32_t loc = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) loc += hist[threadIdx.x * kPer + j];
+    s_scan[threadIdx.x] = loc;
+    __syncthreads();
+    for (int off = 1; off < kSelThreads; off <<= 1) {
+      const uint32_t y = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0u;
+      __syncthreads();
+      s_scan[threadIdx.x] += y;
+      __syncthreads();
+    }
+    const int64_t k = s_k;
+    const int64_t incl = s_scan[threadIdx.x];
+    const int64_t excl = incl - loc;
+    __syncthreads();
+    if (k >= excl && k < incl) {
+      int64_t c = excl;
+      for (int j = 0; j < kPer; ++j) {
+        const int bin = threadIdx.x * kPer + j;
+        if (k < c + hist[bin]) {
+          s_prefix = (prefix << dbits) | (uint64_t)bin;
+          s_k = k - c;
+          break;
+        }
+        c += hist[bin];
+      }
+    }
+    __syncthreads();
+    used += dbits;
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = val_of(s_prefix);
+}
+
+// Queries for per-segment percentiles of both stains: for segment s and
+// stain j, ranks lo, hi (p/100*(n-1)) and n-1 (the max).
+__global__ void k_p99_queries(const int64_t* __restrict__ seg, int nseg, int64_t total, double p,
+                              SelQuery* __restrict__ qs) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nseg * 2) return;
+  const int s = idx >> 1, j = idx & 1;
+  const int64_t b = seg[s], e = seg[s + 1], n = e - b;
+  const double rank = __dmul_rn(p / 100.0, (double)(n > 0 ? n - 1 : 0));
+  const int64_t lo = (int64_t)floor(rank), hi = (int64_t)ceil(rank);
+  SelQuery* q = qs + 3 * idx;
+  for (int t = 0; t < 3; ++t) {
+    q[t].offset = j * total;
+    q[t].begin = b;
+    q[t].end = e;
+  }
+  q[0].k = lo;
+  q[1].k = hi;
+  q[2].k = n > 0 ? n - 1 : 0;
+}
+
+__global__ void k_p99_combine(const int64_t* __restrict__ seg, int nseg, double p,
+                              const double* __restrict__ sel, double* __restrict__ p99,
+                              int32_t* __restrict__ absent) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nseg * 2) return;
+  const int s = idx >> 1;
+  const int64_t n = seg[s + 1] - seg[s];
+  if (n <= 0) {
+    p99[idx] = 0.0;
+    absent[idx] = 1;
+    return;
+  }
+  const double a = sel[3 * idx], b = sel[3 * idx + 1], mx = sel[3 * idx + 2];
+  const double rank = __dmul_rn(p / 100.0, (double)(n - 1));
+  const double frac = __dsub_rn(rank, floor(rank));
+  p99[idx] = __dadd_rn(a, __dmul_rn(__dsub_rn(b, a), frac));
+  absent[idx] = (mx <= 0.0) ? 1 : 0;   // s.max(initial=0) <= 0 (src/normalize.py:91)
+}
+
+__global__ void k_build_queries(const int64_t* __restrict__ b, const int64_t* __restrict__ e,
+                                const int64_t* __restrict__ k, int nq, SelQuery* __restrict__ qs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq) return;
+  qs[i].offset = 0;
+  qs[i].begin = b[i];
+  qs[i].end = e[i];
+  qs[i].k = k[i];
+}
+
+cudaError_t launch_build_queries(const int64_t* b, const int64_t* e, const int64_t* k, int nq,
+                                 SelQuery* qs, cudaStream_t st) {
+  if (nq <= 0) return cudaSuccess;
+  k_build_queries<<<(nq + 127) / 128, 128, 0, st>>>(b, e, k, nq, qs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const double* values, const SelQuery* qs, int nq, double* out,
+                          cudaStream_t st) {
+  if (nq <= 0) return cudaSuccess;
+  k_select<<<nq, kSelThreads, 0, st>>>(values, qs, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p99(const double* h, int64_t total, const int64_t* seg, int nseg, double p,
+                       SelQuery* qbuf, double* selbuf, double* p99, int32_t* absent,
+                       cudaStream_t st) {
+  if (nseg <= 0) return cudaSuccess;
+  const int n2 = nseg * 2;
+  k_p99_queries<<<(n2 + 127) / 128, 128, 0, st>>>(seg, nseg, total, p, qbuf);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if ((e = launch_select(h, qbuf, 3 * n2, selbuf, st)) != cudaSuccess) return e;
+  k_p99_combine<<<(n2 + 127) / 128, 128, 0, st>>>(seg, nseg, p, selbuf, p99, absent);
+  return cudaGetLastError();
+}
+
+}  // namespace spcn

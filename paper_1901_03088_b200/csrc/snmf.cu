@@ -1,0 +1,329 @@
+// snmf.cu — batched sparse-NMF stain-basis fit (K6) and batched density
+// coding of the fit samples (K7a).
+//
+// Reference: fit_basis src/stain_sep.py:239-336 (+ _w_step :210-236,
+// snmf_objective :204-207, order_stains :104-116) and code_densities
+// src/stain_sep.py:168-201 as used by fit src/pipeline.py:225-226.
+//
+// One thread-block CLUSTER per problem (cluster size 1 for the 4096-patch
+// batch, 8 for a single whole-slide fit).  Each CTA owns a contiguous slice
+// of the problem's sampled pixels; OD values are re-read through the
+// problem's 256-entry table from the 3-byte RGB sample (24 B/px of fp64 OD
+// never touch HBM); stain densities H live in a global scratch array.
+// Every reduction (objective, V H^T, H H^T, sum H) is a fixed-order
+// warp-shuffle → CTA → DSMEM cluster tree, and every CTA of the cluster
+// combines the partials in the same rank order, so all CTAs hold bitwise
+// identical totals and take identical control decisions (W-step accept,
+// convergence) without a broadcast.  Scalar arithmetic that numpy routes
+// through BLAS (3-vector dots, the K=2 matmul element) uses the same FMA
+// chain numpy/OpenBLAS uses; long reductions differ from BLAS only in
+// summation order (basis within cosine 1e-3, measured
+// ~1e-15).
+#include <cooperative_groups.h>
+
+#include "snmf.h"
+#include "spcn_device.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace spcn {
+
+constexpr int kSnThreads = 512;
+constexpr int kNStat = 12;  // rr, s0, s1, vht[3][2], hht00, hht01, hht11
+
+__device__ __forceinline__ double fma_dot3(double a0, double a1, double a2, double b0, double b1,
+                                           double b2) {
+  // numpy 1-D @ 1-D of length 3 on OpenBLAS: fma(a2,b2, fma(a1,b1, a0*b0))
+  return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
+}
+
+template <int N>
+__device__ __forceinline__ void cta_reduce(double (&v)[N], double* warp_part,
+                                           double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], off);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < N; ++q) warp_part[warp * N + q] = v[q];
+  __syncthreads();
+  if (threadIdx.x < N) {
+    double s = 0.0;
+    for (int w = 0; w < kSnThreads / 32; ++w) s += warp_part[w * N + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+struct SnmfShared {
+  double lut[3 * 256];
+  double w[6];            // current basis, row-major [c][j]
+  double cand[6];
+  double part[2][kNStat]; // double-buffered CTA partials (read by the cluster)
+  double tot[kNStat];     // cluster totals (identical in every CTA)
+  double warp_part[kSnThreads / 32][kNStat];
+  double g[4];            // g00, g01, g11, det
+  int flag;
+};
+
+__global__ void __launch_bounds__(kSnThreads) k_snmf(
+    const uint8_t* __restrict__ samples, const double* __restrict__ od,
+    const int64_t* __restrict__ offsets, int nprob, const double* __restrict__ luts,
+    const __grid_constant__ SnmfArgs a, double* __restrict__ hbuf,
+    int64_t total, double* __restrict__ basis_out, double* __restrict__ hist_out,
+    int32_t* __restrict__ info_out) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int ncl = gridDim.x / cs;
+  const int cid = blockIdx.x / cs;
+  __shared__ SnmfShared sh;
+  const int tid = threadIdx.x;
+  int phase = 0;
+
+  // cluster-wide sum of a CTA partial: every CTA reads all ranks in order
+  auto cluster_total = [&](int nstat) {
+    cluster.sync();
+    if (tid < nstat) {
+      double s = 0.0;
+      for (int r = 0; r < cs; ++r) {
+        const double* rp = cluster.map_shared_rank(&sh.part[phase & 1][0], r);
+        s += rp[tid];
+      }
+      sh.tot[tid] = s;
+    }
+    ++phase;
+    __syncthreads();
+  };
+
+  for (int p = cid; p < nprob; p += ncl) {
+    const int64_t o0 = offsets[p], m = offsets[p + 1] - offsets[p];
+    const int64_t lo = o0 + (m * rank) / cs, hi = o0 + (m * (rank + 1)) / cs;
+    if (!od)
+      for (int i = tid; i < 3 * 256; i += kSnThreads) sh.lut[i] = luts[(int64_t)p * 768 + i];
+    if (tid < 6) sh.w[tid] = a.w_init[tid];
+    __syncthreads();
+    const double lam = a.lam, code_lam = a.lam / 2.0;
+    auto load_od = [&](int64_t i, double& v0, double& v1, double& v2) {
+      if (od) {
+        v0 = od[i]; v1 = od[total + i]; v2 = od[2 * total + i];
+      } else {
+        const uint8_t* px = samples + 3 * i;
+        v0 = sh.lut[px[0]]; v1 = sh.lut[256 + px[1]]; v2 = sh.lut[512 + px[2]];
+      }
+    };
+    double* hist = hist_out + (int64_t)p * (a.max_outer + 1);
+
+    // --- H-step + objective + sufficient statistics (one fused pass)
+    auto hstep = [&]() {
+      if (tid == 0) {
+        const double* w = sh.w;
+        const double g00 = fma_dot3(w[0], w[2], w[4], w[0], w[2], w[4]);
+        const double g11 = fma_dot3(w[1], w[3], w[5], w[1], w[3], w[5]);
+        const double g01 = fma_dot3(w[0], w[2], w[4], w[1], w[3], w[5]);
+        sh.g[0] = g00; sh.g[1] = g01; sh.g[2] = g11;
+        sh.g[3] = __dsub_rn(__dmul_rn(g00, g11), __dmul_rn(g01, g01));
+      }
+      __syncthreads();
+      const double w00 = sh.w[0], w01 = sh.w[1], w10 = sh.w[2], w11 = sh.w[3], w20 = sh.w[4],
+                   w21 = sh.w[5];
+      const double g00 = sh.g[0], g01 = sh.g[1], g11 = sh.g[2], det = sh.g[3];
+      double st[kNStat];
+#pragma unroll
+      for (int q = 0; q < kNStat; ++q) st[q] = 0.0;
+      for (int64_t i = lo + tid; i < hi; i += kSnThreads) {
+        double v0, v1, v2;
+        load_od(i, v0, v1, v2);
+        const double b0 = strict_dot3(w00, w10, w20, v0, v1, v2);
+        const double b1 = strict_dot3(w01, w11, w21, v0, v1, v2);
+        double h0, h1;
+        strict_nnls(b0, b1, g00, g01, g11, det, code_lam, 500, 1e-9, h0, h1);
+        hbuf[i] = h0;
+        hbuf[total + i] = h1;
+        const double r0 = v0 - __fma_rn(w01, h1, __dmul_rn(w00, h0));
+        const double r1 = v1 - __fma_rn(w11, h1, __dmul_rn(w10, h0));
+        const double r2 = v2 - __fma_rn(w21, h1, __dmul_rn(w20, h0));
+        st[0] += r0 * r0 + r1 * r1 + r2 * r2;
+        st[1] += h0;
+        st[2] += h1;
+        st[3] += v0 * h0; st[4] += v0 * h1;
+        st[5] += v1 * h0; st[6] += v1 * h1;
+        st[7] += v2 * h0; st[8] += v2 * h1;
+        st[9] += h0 * h0; st[10] += h0 * h1; st[11] += h1 * h1;
+      }
+      cta_reduce<kNStat>(st, &sh.warp_part[0][0], sh.part[phase & 1]);
+      cluster_total(kNStat);
+      return sh.tot[0] + lam * (sh.tot[1] + sh.tot[2]);
+    };
+
+    // --- objective of a candidate basis with the current H
+    auto cand_objective = [&]() {
+      const double c00 = sh.cand[0], c01 = sh.cand[1], c10 = sh.cand[2], c11 = sh.cand[3],
+                   c20 = sh.cand[4], c21 = sh.cand[5];
+      double st[1] = {0.0};
+      for (int64_t i = lo + tid; i < hi; i += kSnThreads) {
+        double v0, v1, v2;
+        load_od(i, v0, v1, v2);
+        const double h0 = hbuf[i], h1 = hbuf[total + i];
+        const double r0 = v0 - __fma_rn(c01, h1, __dmul_rn(c00, h0));
+        const double r1 = v1 - __fma_rn(c11, h1, __dmul_rn(c10, h0));
+        const double r2 = v2 - __fma_rn(c21, h1, __dmul_rn(c20, h0));
+        st[0] += r0 * r0 + r1 * r1 + r2 * r2;
+      }
+      cta_reduce<1>(st, &sh.warp_part[0][0], sh.part[phase & 1]);
+      cluster_total(1);
+      return sh.tot[0];
+    };
+
+    double f = hstep();
+    double sumh = sh.tot[1] + sh.tot[2];
+    double row0 = sh.tot[1], row1 = sh.tot[2];
+    double vht[3][2], hht[2][2];
+    auto grab_stats = [&]() {
+      for (int c = 0; c < 3; ++c) {
+        vht[c][0] = sh.tot[3 + 2 * c];
+        vht[c][1] = sh.tot[4 + 2 * c];
+      }
+      hht[0][0] = sh.tot[9]; hht[0][1] = hht[1][0] = sh.tot[10]; hht[1][1] = sh.tot[11];
+    };
+    grab_stats();
+    if (rank == 0 && tid == 0) hist[0] = f;
+    int it = 0, converged = 0;
+    double f_rec = f;
+    const double floor_f = 1e-12 * (double)m;
+    for (it = 1; it <= a.max_outer; ++it) {
+      // _w_step (src/stain_sep.py:221-235)
+      for (int j = 0; j < 2; ++j) {
+        const int k = 1 - j;
+        if (hht[j][j] <= 0.0) continue;
+        double u[3];
+        for (int c = 0; c < 3; ++c) {
+          u[c] = __dsub_rn(vht[c][j], __dmul_rn(sh.w[c * 2 + k], hht[k][j]));
+          u[c] = u[c] < 0.0 ? 0.0 : u[c];   // np.maximum(u, 0.0)
+        }
+        const double nrm = sqrt(fma_dot3(u[0], u[1], u[2], u[0], u[1], u[2]));
+        if (nrm <= 1e-15) continue;
+        __syncthreads();
+        if (tid < 6) {
+          const int c = tid >> 1, jj = tid & 1;
+          sh.cand[tid] = (jj == j) ? __ddiv_rn(u[c], nrm) : sh.w[tid];
+        }
+        __syncthreads();
+        const double ft = cand_objective() + lam * sumh;
+        if (ft <= f) {
+          __syncthreads();
+          if (tid < 6) sh.w[tid] = sh.cand[tid];
+          f = ft;
+        }
+        __syncthreads();
+      }
+      f = hstep();
+      sumh = sh.tot[1] + sh.tot[2];
+      row0 = sh.tot[1];
+      row1 = sh.tot[2];
+      grab_stats();
+      if (rank == 0 && tid == 0) hist[it] = f;
+      const double last = f_rec;   // history[-2]
+      f_rec = f;
+      if (fabs(last - f) <= a.rel_tol * fmax(fabs(last), 1e-12)) { converged = 1; break; }
+      if (f <= floor_f) { converged = 1; break; }
+    }
+    if (it > a.max_outer) it = a.max_outer;
+    // flags and ordering (src/stain_sep.py:315-336)
+    if (rank == 0 && tid == 0) {
+      int flags = 0;
+      if (!converged) flags |= 1;
+      const double tot = row0 + row1;
+      if (tot > 0 && fmin(row0, row1) <= 1e-9 * tot) flags |= 2;
+      const double* w = sh.w;
+      const double rb0 = w[0] - w[4], rb1 = w[1] - w[5];
+      double* bo = basis_out + (int64_t)p * 6;
+      if (rb1 > rb0) {
+        for (int c = 0; c < 3; ++c) { bo[2 * c] = w[2 * c + 1]; bo[2 * c + 1] = w[2 * c]; }
+      } else {
+        for (int c = 0; c < 6; ++c) bo[c] = w[c];
+      }
+      int32_t* inf = info_out + (int64_t)p * 4;
+      inf[0] = it;
+      inf[1] = converged;
+      inf[2] = flags;
+      inf[3] = it + 1;  // history length
+    }
+    cluster.sync();   // before the next problem reuses shared state
+  }
+}
+
+// Batched code_densities over the fit samples: problem p's pixels
+// [off[p], off[p+1]) through its own OD table and basis.
+__global__ void __launch_bounds__(256) k_code_samples(
+    const uint8_t* __restrict__ samples, const int64_t* __restrict__ offsets, int nprob,
+    const double* __restrict__ luts, const double* __restrict__ bases, double lam, int max_sweeps,
+    double* __restrict__ h, int64_t total) {
+  const int p = blockIdx.y;
+  const int64_t o0 = offsets[p], o1 = offsets[p + 1];
+  __shared__ double lut[768];
+  __shared__ double w[6], g[4];
+  for (int i = threadIdx.x; i < 768; i += 256) lut[i] = luts[(int64_t)p * 768 + i];
+  if (threadIdx.x < 6) w[threadIdx.x] = bases[(int64_t)p * 6 + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // code_densities' scalar Gram order (src/stain_sep.py:197-199): plain mul/add
+    g[0] = __dadd_rn(__dadd_rn(__dmul_rn(w[0], w[0]), __dmul_rn(w[2], w[2])), __dmul_rn(w[4], w[4]));
+    g[2] = __dadd_rn(__dadd_rn(__dmul_rn(w[1], w[1]), __dmul_rn(w[3], w[3])), __dmul_rn(w[5], w[5]));
+    g[1] = __dadd_rn(__dadd_rn(__dmul_rn(w[0], w[1]), __dmul_rn(w[2], w[3])), __dmul_rn(w[4], w[5]));
+    g[3] = __dsub_rn(__dmul_rn(g[0], g[2]), __dmul_rn(g[1], g[1]));
+  }
+  __syncthreads();
+  for (int64_t i = o0 + blockIdx.x * 256ll + threadIdx.x; i < o1; i += 256ll * gridDim.x) {
+    const uint8_t* px = samples + 3 * i;
+    const double v0 = lut[px[0]], v1 = lut[256 + px[1]], v2 = lut[512 + px[2]];
+    const double b0 = strict_dot3(w[0], w[2], w[4], v0, v1, v2);
+    const double b1 = strict_dot3(w[1], w[3], w[5], v0, v1, v2);
+    double h0, h1;
+    strict_nnls(b0, b1, g[0], g[1], g[2], g[3], lam, max_sweeps, 0.0, h0, h1);
+    h[i] = h0;
+    h[total + i] = h1;
+  }
+}
+
+cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t* offsets, int nprob,
+                        const double* luts, const SnmfArgs& a, double* hbuf, int64_t total,
+                        double* basis_out, double* hist_out, int32_t* info_out, int cluster,
+                        cudaStream_t st) {
+  if (nprob <= 0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int nclusters = nprob;
+  const int max_clusters = (sms * 2) / cluster;
+  if (nclusters > max_clusters) nclusters = max_clusters;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nclusters * cluster);
+  cfg.blockDim = dim3(kSnThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_snmf, samples, od, offsets, nprob, luts, a, hbuf, total,
+                            basis_out, hist_out, info_out);
+}
+
+cudaError_t launch_code_samples(const uint8_t* samples, const int64_t* offsets, int nprob,
+                                int64_t max_m, const double* luts, const double* bases,
+                                double lam, int max_sweeps, double* h, int64_t total,
+                                cudaStream_t st) {
+  if (nprob <= 0 || max_m <= 0) return cudaSuccess;
+  int64_t gx = (max_m + 255) / 256;
+  if (gx > 64) gx = 64;
+  k_code_samples<<<dim3((unsigned)gx, nprob), 256, 0, st>>>(samples, offsets, nprob, luts, bases,
+                                                            lam, max_sweeps, h, total);
+  return cudaGetLastError();
+}
+
+}  // namespace spcn

@@ -173,6 +173,12 @@ class ArrayWriter(StripWriter):
     def rows(self, y, h):
         return self.pixels[y:y + h]
 
+    def mark_written(self, y, h):
+        """Advance the in-order cursor for rows the transform copied in directly."""
+        if y != self._rows_written:
+            raise ValueError(f"out-of-order strip: expected y={self._rows_written}, got y={y}")
+        self._rows_written += h
+
     def _write(self, rows):
         y = self._rows_written
         if hasattr(rows, "cpu"):

@@ -1,0 +1,487 @@
+"""Whole-slide orchestration on the device: sample → i0 → SNMF → p99 → transform.
+
+Mirrors src/pipeline.py:1-345 (same functions, arguments, defaults, errors
+and stage labels).  The per-pixel work is libspcn (CUDA); the host keeps the
+reference's sequential control logic where it is O(patches): the seeded patch
+visit order (numpy PCG64, identical to src/pipeline.py:138-142) and the
+visit/stop rules (src/pipeline.py:156-184), replayed on per-patch counts the
+GPU produced.
+"""
+from __future__ import annotations
+
+import os
+import time
+from collections import deque
+from dataclasses import dataclass
+from threading import Lock
+
+import numpy as np
+
+from . import _dev, _lib, optics, snmf
+from .errors import BlankSlideError, DegenerateStainError, InsufficientPixelsError, SlideNormError
+from .image_io import (DEFAULT_STRIP_HEIGHT, ArraySource, ArrayWriter, DeviceSource, DeviceWriter,
+                       PixelBlock, plan_strips)
+from .normalize import FitParams, StainStats, config_hash, scale_factors, stain_stats
+from .optics import SAMPLE_CAP, WHITE_THRESHOLD
+from .stain_sep import SnmfConfig
+from .xform import XformPlan
+
+PATCH_DT = np.dtype([("base", "<i8"), ("width", "<i4"), ("height", "<i4"), ("row_stride", "<i8")])
+TAKE_DT = np.dtype([("take_nonwhite", "<i8"), ("out_base", "<i8"), ("take_bright", "<i4", (3,)),
+                    ("problem", "<i4")])
+CHUNK = 4096  # SPCN_SAMPLE_CHUNK
+
+
+@dataclass(frozen=True)
+class SamplePlan:
+    """How to gather the fitting sample from a slide (src/pipeline.py:39-59)."""
+
+    max_patches: int = 20
+    patch_size: int = 1000
+    target_pixels: int = 100_000
+    background_fraction_cutoff: float = 0.95
+    seed: int = 0
+    white_threshold: int = WHITE_THRESHOLD
+    sample_cap: int = SAMPLE_CAP
+
+    def __post_init__(self):
+        if self.max_patches < 1:
+            raise ValueError("max_patches must be >= 1")
+        if self.target_pixels < 1:
+            raise ValueError("target_pixels must be >= 1")
+        if not 0.0 < self.background_fraction_cutoff <= 1.0:
+            raise ValueError("background_fraction_cutoff must be in (0, 1]")
+        if self.patch_size < 1:
+            raise ValueError("patch_size must be >= 1")
+
+
+@dataclass
+class PixelSample:
+    """Pixels gathered by :func:`sample_pixels` (src/pipeline.py:62-70)."""
+
+    non_white: object              # (M, 3) uint8 (numpy from sample_pixels; CUDA inside fit)
+    patch_counts: list
+    bright: tuple                  # three 1-D arrays (sample_pixels) or None (device path)
+    patches_visited: int = 0
+    patches_used: int = 0
+    bright_hist: np.ndarray = None  # (3, 256) counts of the bright pools
+
+
+@dataclass
+class RunStats:
+    """Per-stage wall times and counters (src/pipeline.py:73-99)."""
+
+    sampling_s: float = 0.0
+    basis_fit_s: float = 0.0
+    transform_s: float = 0.0
+    total_s: float = 0.0
+    sampled_pixels: int = 0
+    transformed_pixels: int = 0
+    patches: int = 0
+    peak_strip_pixels: int = 0
+
+    CSV_HEADER = "stage,seconds,pixels,patches"
+
+    def csv_rows(self):
+        return [("sampling", self.sampling_s, self.sampled_pixels, self.patches),
+                ("basis_fit", self.basis_fit_s, self.sampled_pixels, self.patches),
+                ("transform", self.transform_s, self.transformed_pixels, self.patches),
+                ("total", self.total_s, self.transformed_pixels, self.patches)]
+
+    def write_csv(self, fh):
+        fh.write(self.CSV_HEADER + "\n")
+        for stage, seconds, pixels, patches in self.csv_rows():
+            fh.write(f"{stage},{seconds:.6f},{pixels},{patches}\n")
+
+
+class BufferGauge:
+    """Thread-safe gauge of pixels held in in-flight strip buffers (src/pipeline.py:102-118)."""
+
+    def __init__(self):
+        self._lock = Lock()
+        self.current = 0
+        self.peak = 0
+
+    def add(self, pixels: int):
+        with self._lock:
+            self.current += pixels
+            self.peak = max(self.peak, self.current)
+
+    def release(self, pixels: int):
+        with self._lock:
+            self.current -= pixels
+
+
+def _stage(label, fn, *args, **kwargs):
+    """src/pipeline.py:121-125: prefix domain errors with the stage label."""
+    try:
+        return fn(*args, **kwargs)
+    except SlideNormError as exc:
+        raise type(exc)(f"{label}: {exc}") from exc
+
+
+# ----------------------------------------------------------------------------- sampling
+def _lib_sample():
+    L = _lib.lib()
+    if not getattr(L, "_spcn_sample_declared", False):
+        P, I32 = _lib.P, _lib.I32
+        _lib.declare("spcn_sample_count", _lib.ctypes.c_int, [P, P, I32, I32, I32, P, P])
+        _lib.declare("spcn_sample_compact", _lib.ctypes.c_int, [P, P, I32, I32, I32, P, P, P, P, P])
+        _lib.declare("spcn_i0_from_hist", _lib.ctypes.c_int, [P, I32, P, P, P])
+        _lib.declare("spcn_od_tables", _lib.ctypes.c_int, [P, I32, P, P])
+        L._spcn_sample_declared = True
+    return L
+
+
+class _PatchImage:
+    """Device view of the slide regions the sampler may visit."""
+
+    def __init__(self, slide, rects):
+        t = _dev.torch()
+        self.rects = rects
+        if isinstance(slide, DeviceSource):
+            self.img = slide.tensor
+            width = slide.width
+            self.desc = np.array([(y * width + x, w, h, width) for (x, y, w, h) in rects],
+                                 dtype=PATCH_DT)
+        else:
+            # host slide: upload only the candidate regions (≤ 10 x max_patches of them)
+            parts, desc, base = [], [], 0
+            for (x, y, w, h) in rects:
+                px = slide.read_region(x, y, w, h).pixels
+                parts.append(np.ascontiguousarray(px).reshape(-1))
+                desc.append((base, w, h, w))
+                base += w * h
+            host = np.concatenate(parts) if parts else np.zeros(3, np.uint8)
+            self.img = t.from_numpy(host).to("cuda")
+            self.desc = np.array(desc, dtype=PATCH_DT)
+
+
+def _count(L, pimg, sel, thr):
+    """Per-chunk counts for the patches `sel` (indices into pimg.desc) → (n, chunks, 4)."""
+    t = _dev.torch()
+    desc = pimg.desc[sel]
+    npx = desc["width"].astype(np.int64) * desc["height"]
+    chunks = int(max(1, -(-int(npx.max()) // CHUNK)))
+    d = t.from_numpy(desc.view(np.uint8).copy()).cuda()
+    out = t.empty((len(sel), chunks, 4), dtype=t.int32, device="cuda")
+    _lib.check(L.spcn_sample_count(_lib.ptr(pimg.img), _lib.ptr(d), len(sel), chunks, thr,
+                                   _lib.ptr(out), _lib.stream_handle()), "sample_count")
+    return out, chunks
+
+
+def _visit(plan, order, rects, counts_of):
+    """Replay src/pipeline.py:156-184 on per-patch totals.  counts_of(i) → (nw, bR, bG, bB)."""
+    limit = 10 * plan.max_patches
+    min_frac = 1.0 - plan.background_fraction_cutoff
+    collected = visited = used = 0
+    bright_n = [0, 0, 0]
+    takes, used_counts = [], []
+    for k, idx in enumerate(order):
+        if visited >= limit or used >= plan.max_patches:
+            break
+        if collected >= plan.target_pixels:
+            break
+        nw, b0, b1, b2 = counts_of(k)
+        x, y, w, h = rects[k]
+        visited += 1
+        tb = [0, 0, 0]
+        for c, bc in enumerate((b0, b1, b2)):
+            if bright_n[c] < plan.sample_cap:
+                tb[c] = int(min(bc, plan.sample_cap - bright_n[c]))
+                bright_n[c] += tb[c]
+        if nw < min_frac * (w * h):
+            takes.append((k, 0, 0, tb))
+            continue
+        used += 1
+        take = int(min(nw, plan.target_pixels - collected))
+        takes.append((k, take, collected, tb))
+        used_counts.append(take)
+        collected += take
+    return takes, used_counts, collected, visited, used
+
+
+def _sample_device(slide, plan: SamplePlan):
+    """Device sampling; returns (sample CUDA uint8 (M,3), PixelSample meta)."""
+    t = _dev.torch()
+    L = _lib_sample()
+    rng = np.random.default_rng(plan.seed)
+    xs = range(0, slide.width, plan.patch_size)
+    ys = range(0, slide.height, plan.patch_size)
+    origins = [(x, y) for y in ys for x in xs]
+    order = rng.permutation(len(origins))
+    ncand = min(len(order), 10 * plan.max_patches)
+    rects = [(origins[i][0], origins[i][1], min(plan.patch_size, slide.width - origins[i][0]),
+              min(plan.patch_size, slide.height - origins[i][1])) for i in order[:ncand]]
+    pimg = _PatchImage(slide, rects)
+    thr = int(plan.white_threshold)
+    # counts in growing batches (most slides stop after one or two patches)
+    tot = np.zeros((0, 4), dtype=np.int64)
+    dev_counts = []
+    batch = min(ncand, max(2, min(plan.max_patches, 8)))
+
+    def counts_of(k):
+        nonlocal tot, batch
+        while k >= tot.shape[0]:
+            lo = tot.shape[0]
+            hi = min(ncand, lo + batch)
+            c, chunks = _count(L, pimg, np.arange(lo, hi), thr)
+            dev_counts.append((lo, hi, c, chunks))
+            tot = np.concatenate([tot, c.sum(dim=1).cpu().numpy().astype(np.int64)])
+            batch *= 2
+        return tuple(int(v) for v in tot[k])
+
+    takes, used_counts, collected, visited, used = _visit(plan, order[:ncand], rects, counts_of)
+    if collected == 0:
+        raise BlankSlideError("blank slide: no non-white pixels found in any sampled patch")
+    sample = t.empty((collected, 3), dtype=t.uint8, device="cuda")
+    hist = t.zeros((1, 3, 256), dtype=t.int32, device="cuda")
+    for lo, hi, c, chunks in dev_counts:
+        sel = [tk for tk in takes if lo <= tk[0] < hi and (tk[1] > 0 or any(tk[3]))]
+        if not sel:
+            continue
+        idx = np.array([tk[0] - lo for tk in sel], dtype=np.int64)
+        desc = pimg.desc[lo:hi][idx]
+        tk = np.zeros(len(sel), dtype=TAKE_DT)
+        tk["take_nonwhite"] = [s[1] for s in sel]
+        tk["out_base"] = [s[2] for s in sel]
+        tk["take_bright"] = [s[3] for s in sel]
+        tk["problem"] = 0
+        cnt = c[t.from_numpy(idx).cuda()].contiguous()
+        d = t.from_numpy(desc.view(np.uint8).copy()).cuda()
+        dt = t.from_numpy(tk.view(np.uint8).copy()).cuda()
+        _lib.check(L.spcn_sample_compact(_lib.ptr(pimg.img), _lib.ptr(d), len(sel), chunks, thr,
+                                         _lib.ptr(cnt), _lib.ptr(dt), _lib.ptr(sample),
+                                         _lib.ptr(hist), _lib.stream_handle()), "sample_compact")
+    bh = hist.cpu().numpy()[0].astype(np.int64)
+    meta = PixelSample(non_white=sample, patch_counts=used_counts, bright=None,
+                       patches_visited=visited, patches_used=used, bright_hist=bh)
+    return sample, meta
+
+
+def sample_pixels(slide, plan: SamplePlan = SamplePlan()) -> PixelSample:
+    """src/pipeline.py:128-200 (device sampling; numpy result like the reference).
+
+    ``bright`` holds the pools as value-sorted arrays (the multiset the
+    reference keeps; i0 only depends on it through an order statistic)."""
+    sample, meta = _sample_device(slide, plan)
+    meta.non_white = sample.cpu().numpy()
+    meta.bright = tuple(np.repeat(np.arange(256, dtype=np.uint8), meta.bright_hist[c])
+                        for c in range(3))
+    return meta
+
+
+# ----------------------------------------------------------------------------- fit
+def _cfg_fields(plan, cfg, code_lam, per_patch_stats):
+    return {"lambda": cfg.lam, "code_lambda": code_lam, "rel_tol": cfg.rel_tol,
+            "max_outer_iters": cfg.max_outer_iters, "snmf_seed": cfg.seed,
+            "sample_seed": plan.seed, "white_threshold": plan.white_threshold,
+            "sample_cap": plan.sample_cap, "target_pixels": plan.target_pixels,
+            "max_patches": plan.max_patches, "patch_size": plan.patch_size,
+            "background_fraction_cutoff": plan.background_fraction_cutoff,
+            "per_patch_stats": per_patch_stats}
+
+
+def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), *,
+        code_lam: float = 0.0, per_patch_stats: bool = False, source_label: str = "",
+        stats: RunStats | None = None) -> FitParams:
+    """src/pipeline.py:203-257 on the device."""
+    t = _dev.torch()
+    stats = stats if stats is not None else RunStats()
+    if isinstance(slide, np.ndarray):
+        slide = ArraySource(slide)
+    elif _dev.is_tensor(slide):
+        slide = DeviceSource(slide)
+    t0 = time.perf_counter()
+    sample, meta = _stage("sampling", _sample_device, slide, plan)
+    stats.sampling_s += time.perf_counter() - t0
+    m = int(sample.shape[0])
+    stats.sampled_pixels = m
+    stats.patches = meta.patches_used
+
+    t0 = time.perf_counter()
+    i0 = _stage("background estimation", optics.i0_from_counts, meta.bright_hist)
+    lut = t.from_numpy(optics.od_table(i0)).cuda().reshape(1, 3, 256)
+    if m < 10:
+        raise InsufficientPixelsError(
+            f"basis fit: insufficient pixels: need at least 10 OD samples, got {m}")
+    offsets = t.tensor([0, m], dtype=t.int64, device="cuda")
+    flat = sample.reshape(-1)
+    r = snmf.snmf_batched(flat, offsets, lut, cfg, cluster=8 if m >= 20_000 else 1)
+    info = r.info.cpu().numpy()[0]
+    basis = r.basis.cpu().numpy()[0]
+    snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
+    h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
+    if per_patch_stats:
+        from . import stats as dstats
+
+        counts = [c for c in meta.patch_counts if c > 0]
+        seg = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        vals, _ = dstats.segment_percentiles(h, seg, 99.0)
+        pairs = [tuple(v) for v in vals.cpu().numpy()]
+        st = _stage("density stats", stain_stats, patch_p99s=pairs, sample_count=m)
+    else:
+        st = _stage("density stats", stain_stats, h)
+    stats.basis_fit_s += time.perf_counter() - t0
+    provenance = {"source": str(source_label),
+                  "config_hash": config_hash(_cfg_fields(plan, cfg, code_lam, per_patch_stats))}
+    return FitParams(i0=i0, basis=basis, stats=st, provenance=provenance)
+
+
+# ----------------------------------------------------------------------------- transform
+def _pinned(a: np.ndarray) -> bool:
+    t = _dev.torch()
+    try:
+        return bool(t.from_numpy(a).is_pinned())
+    except Exception:  # pragma: no cover
+        return False
+
+
+def transform(slide, source: FitParams, target: FitParams, sink, *,
+              strip_height: int = DEFAULT_STRIP_HEIGHT, workers: int | None = None,
+              code_lam: float = 0.0, stats: RunStats | None = None,
+              gauge: BufferGauge | None = None, progress=None,
+              precision: str = "exact") -> RunStats:
+    """src/pipeline.py:275-345 on the device.
+
+    Output is byte-identical for any strip height / worker count (and, with
+    precision="exact", to the reference).  Device source + DeviceWriter: one
+    launch over the resident slide.  Host source: strips stream through
+    ``workers`` (default 2) CUDA streams — H2D, recolor, D2H overlap — and
+    are committed to the sink in order; pinned host arrays are copied
+    directly without a staging copy.
+    """
+    t = _dev.torch()
+    stats = stats if stats is not None else RunStats()
+    gauge = gauge if gauge is not None else BufferGauge()
+    factors = scale_factors(source.stats, target.stats)
+    if np.any(factors <= 0):
+        raise DegenerateStainError("degenerate stain density: target p99 is zero for a stain")
+    strips = plan_strips(slide.height, strip_height)
+    width = slide.width
+    plan = XformPlan(source.i0, source.basis, code_lam, factors, target.basis, target.i0,
+                     precision=precision)
+    t0 = time.perf_counter()
+
+    if isinstance(slide, DeviceSource):
+        src = slide.tensor
+        if isinstance(sink, DeviceWriter):
+            plan.run(src, sink.pixels, width * slide.height)
+            for y, h in strips:
+                gauge.add(h * width)
+                sink.mark_written(y, h)
+                gauge.release(h * width)
+                if progress is not None:
+                    progress(y + h, slide.height)
+            t.cuda.current_stream().synchronize()
+        else:
+            out = t.empty_like(src)
+            plan.run(src, out, width * slide.height)
+            host = out.cpu().numpy()
+            for y, h in strips:
+                gauge.add(h * width)
+                sink.write_strip(PixelBlock(0, y, host[y:y + h]))
+                gauge.release(h * width)
+                if progress is not None:
+                    progress(y + h, slide.height)
+    else:
+        _transform_streamed(slide, sink, plan, strips, width, workers or 2, gauge, progress)
+
+    stats.transform_s += time.perf_counter() - t0
+    stats.transformed_pixels = slide.width * slide.height
+    stats.peak_strip_pixels = max(stats.peak_strip_pixels, gauge.peak)
+    stats.total_s = stats.sampling_s + stats.basis_fit_s + stats.transform_s
+    return stats
+
+
+def _transform_streamed(slide, sink, plan, strips, width, nslots, gauge, progress):
+    """Host-resident slide: bounded in-flight window of strips, in-order commit
+    (src/pipeline.py:298-339), each slot its own stream + device/pinned buffers."""
+    t = _dev.torch()
+    max_h = max(h for _, h in strips)
+    nslots = max(1, min(nslots, len(strips)))
+    src_arr = slide.array if isinstance(slide, ArraySource) else None
+    direct_in = src_arr is not None and _pinned(src_arr)
+    direct_out = isinstance(sink, ArrayWriter) and _pinned(sink.pixels)
+    slots = []
+    for _ in range(nslots):
+        slots.append(dict(
+            stream=t.cuda.Stream(),
+            dsrc=t.empty((max_h, width, 3), dtype=t.uint8, device="cuda"),
+            ddst=t.empty((max_h, width, 3), dtype=t.uint8, device="cuda"),
+            hin=None if direct_in else t.empty((max_h, width, 3), dtype=t.uint8, pin_memory=True),
+            hout=None if direct_out else t.empty((max_h, width, 3), dtype=t.uint8,
+                                                 pin_memory=True),
+            ev=None, job=None))
+    pending = deque()
+
+    def commit():
+        slot = pending.popleft()
+        y, h = slot["job"]
+        slot["ev"].synchronize()
+        if direct_out:
+            sink.mark_written(y, h)
+        else:
+            sink.write_strip(PixelBlock(0, y, slot["hout"][:h].numpy()))
+        gauge.release(h * width)
+        if progress is not None:
+            progress(y + h, slide.height)
+
+    for i, (y, h) in enumerate(strips):
+        slot = slots[i % nslots]
+        while len(pending) >= nslots:
+            commit()
+        gauge.add(h * width)
+        s = slot["stream"]
+        with t.cuda.stream(s):
+            if direct_in:
+                hsrc = t.from_numpy(src_arr[y:y + h])
+            else:
+                block = slide.read_region(0, y, width, h).pixels
+                slot["hin"][:h].numpy()[...] = block
+                hsrc = slot["hin"][:h]
+            slot["dsrc"][:h].copy_(hsrc, non_blocking=True)
+            plan.run(slot["dsrc"], slot["ddst"], h * width, stream=s)
+            if direct_out:
+                t.from_numpy(sink.pixels[y:y + h]).copy_(slot["ddst"][:h], non_blocking=True)
+            else:
+                slot["hout"][:h].copy_(slot["ddst"][:h], non_blocking=True)
+            ev = t.cuda.Event()
+            ev.record(s)
+        slot["ev"] = ev
+        slot["job"] = (y, h)
+        pending.append(slot)
+    while pending:
+        commit()
+
+
+def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
+              cfg: SnmfConfig = SnmfConfig(), code_lam: float = 0.0,
+              per_patch_stats: bool = False, strip_height: int = DEFAULT_STRIP_HEIGHT,
+              precision: str = "exact", stats: RunStats | None = None):
+    """The drop-in entry: fit(source), fit(target) (or use a FitParams / profile
+    for the target), then transform — exactly the reference's _normalize_one
+    (src/cli.py:220-244).  numpy in → numpy out; CUDA tensor in → CUDA tensor out."""
+    from .normalize import load_profile
+
+    t = _dev.torch()
+    stats = stats if stats is not None else RunStats()
+    host = not _dev.is_tensor(source)
+    src = ArraySource(source) if host else DeviceSource(source)
+    if isinstance(target, FitParams):
+        tp = target
+    elif isinstance(target, (str, os.PathLike)):
+        tp = load_profile(target)
+    else:
+        tsrc = ArraySource(target) if not _dev.is_tensor(target) else DeviceSource(target)
+        tp = fit(tsrc, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats)
+    sp = fit(src, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats, stats=stats)
+    if host:
+        sink = ArrayWriter(src.width, src.height)
+        transform(src, sp, tp, sink, strip_height=strip_height, code_lam=code_lam, stats=stats,
+                  precision=precision)
+        return sink.pixels
+    sink = DeviceWriter(src.width, src.height, device=source.device)
+    transform(src, sp, tp, sink, strip_height=strip_height, code_lam=code_lam, stats=stats,
+              precision=precision)
+    return sink.pixels
