@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the SPCN hot path on B200 (contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[3], the north-star case): a synthetic
+100000 x 100000 (10 Gpixel) H&E whole-slide image, rendered on the GPU
+(model of src/synthetic.py), sharded into equal row bands across N GPUs
+(strong scaling: total work fixed).  One step = ``fit`` of the source slide
+(seeded patch sampling → i0 → sparse-NMF basis → density p99, all on the
+device) + ``transform`` of every pixel against a fixed target profile (the
+target is fitted once before timing, as with a --profile target).  Input and
+output (30 GB each) stay resident in HBM; they are >> the 126 MB L2, so no
+flush is needed between steps.
+
+    python bench.py                          # N=1, defaults
+    python bench.py --impl reference         # the reference's CPU path (oracle port)
+    torchrun --nproc-per-node N bench.py --gpus N
+
+Extra keys: roofline (dominant kernel = the
+fused recolor launch, 6 algorithmic bytes/pixel), cpu_baseline (oracle port
+on the host cores, bounded sample, extrapolated), e2e (public API with
+pinned host buffers, H2D+D2H inside the timed region), gpu_launches,
+clocks (NVML sampled during the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mpixels/sec normalized (whole box, 1/2/4/8 B200) + % of HBM/MUFU roofline"
+BYTES_PER_PX = 6          # pass 2: 3 read + 3 write
+
+
+def parse():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--width", type=int, default=100_000)
+    ap.add_argument("--height", type=int, default=100_000)
+    ap.add_argument("--tissue", type=float, default=0.6)
+    ap.add_argument("--layout", default="scatter")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--precision", default="exact", choices=("exact", "fast", "strict"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the CPU-baseline band")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class Clocks(threading.Thread):
+    """NVML sampler (SM clock, throttle reasons) for the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int, period: float = 0.01):
+        super().__init__(daemon=True)
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._halt = threading.Event()
+        self.ok = True
+
+    def run(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._halt.is_set():
+                self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+                time.sleep(self.period)
+        except Exception as exc:  # pragma: no cover - NVML missing
+            self.ok = False
+            self.reasons.add(f"nvml-unavailable: {exc}")
+
+    def stop(self):
+        self._halt.set()
+        self.join(timeout=2)
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- distributed
+def dist_setup(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def band_of(height, rank, world):
+    per = height // world
+    r0 = rank * per
+    rows = per if rank < world - 1 else height - r0
+    return r0, rows
+
+
+# --------------------------------------------------------------------------- CPU baseline
+def cpu_reference_run(band: np.ndarray, target: dict, cores: int, repeats: int = 1):
+    """Time the reference algorithm (oracle port) on a host band: fit + transform."""
+    from oracle import spcn_oracle as orc
+
+    t_fit, t_x = [], []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        fp = orc.fit_params(band)
+        t1 = time.perf_counter()
+        orc.run_transform(band, fp, target, strip_height=64, workers=cores)
+        t2 = time.perf_counter()
+        t_fit.append(t1 - t0)
+        t_x.append(t2 - t1)
+    return min(t_fit), min(t_x)
+
+
+def extrapolated_mpx(total_px, band_px, t_fit, t_x):
+    """Whole-slide Mpx/s from a band: one fit + linear-in-pixels transform
+    (linearity: criterion 10, tests/test_acceptance.py:286-289)."""
+    return total_px / (t_fit + t_x * total_px / band_px) / 1e6
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import spcn_oracle as orc
+
+    cores = os.cpu_count() or 1
+    rows = max(16, args.cpu_rows)
+    band, _, _ = orc.render(args.width, rows, args.seed, tissue_fraction=args.tissue,
+                            layout=args.layout)
+    tgt_px, _, _ = orc.render(1024, 1024, args.seed + 1, tissue_fraction=0.6)
+    target = orc.fit_params(tgt_px)
+    total = args.width * args.height
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_reference_run(band, target, cores)
+    times = []
+    for _ in range(args.steps if args.steps < 5 else 3):
+        tf, tx = cpu_reference_run(band, target, cores)
+        times.append((tf, tx))
+    tf = statistics.median(t[0] for t in times)
+    tx = statistics.median(t[1] for t in times)
+    value = extrapolated_mpx(total, band.shape[0] * band.shape[1], tf, tx)
+    step_ms = (tf + tx * total / (band.shape[0] * band.shape[1])) * 1e3
+    sample = (f"{rows} x {args.width} band ({rows * args.width / 1e6:.1f} Mpx) of the same "
+              f"synthetic model rendered by the oracle; per step fit(band) "
+              f"{tf:.3f} s + transform(band, workers={cores}, strip 64) {tx:.3f} s, "
+              f"extrapolated linearly to {total / 1e9:.0f} Gpx")
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpx/s", "n_gpus": world,
+            "steps": len(times), "warmup": 1, "ms_per_step": round(step_ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": workload_config(args, world),
+            "cpu_baseline": {"value": round(value, 3), "unit": "Mpx/s", "cores": cores,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "Mpx/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, world):
+    return {"workload": f"C4: {args.width}x{args.height} synthetic H&E WSI "
+                        f"({args.width * args.height / 1e9:.2f} Gpx, tissue {args.tissue} "
+                        f"{args.layout}); step = fit(source) + transform(all pixels) vs a "
+                        "fixed target profile",
+            "width": args.width, "height": args.height, "precision": args.precision,
+            "parallelism": f"row-band x{world}", "p99_mode": "sample",
+            "l2": "input+output 60 GB per step >> 126 MB L2 (no flush needed)"}
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local):
+    import torch
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200 import _lib, synthetic
+
+    dev = torch.device("cuda", local if world > 1 else 0)
+    r0, rows = band_of(args.height, rank, world)
+    W = args.width
+    slide = torch.empty((rows, W, 3), dtype=torch.uint8, device=dev)
+    synthetic.render_rows(slide, W, args.height, r0, rows, args.seed, tissue_fraction=args.tissue,
+                          layout=args.layout)
+    out = torch.empty_like(slide)
+    tgt = synthetic.render_slide(2048, 2048, args.seed + 1, tissue_fraction=0.6)
+    target = pb.fit(pb.DeviceSource(tgt))
+    del tgt
+    src = pb.DeviceSource(slide)
+    group = None
+    if world > 1:
+        from paper_1901_03088_b200 import distributed
+
+        group = distributed.RowBandGroup(args.width, args.height, r0, rows)
+
+    xform_ms = []
+
+    def step(record=False):
+        if group is None:
+            fp = pb.fit(src)
+        else:
+            fp = group.fit(src)
+        sink = pb.DeviceWriter(W, rows, out=out)
+        if record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        pb.transform(src, fp, target, sink, precision=args.precision)
+        if record:
+            e1.record()
+            xform_ms.append((e0, e1))
+        return fp
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = Clocks(dev.index if dev.index is not None else 0)
+    clocks.start()
+    time.sleep(0.05)
+    L = _lib.lib()
+    launches0 = L.spcn_launch_count()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step(record=True)
+    t1.record()
+    torch.cuda.synchronize()
+    launches = L.spcn_launch_count() - launches0
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    total = args.width * args.height
+    value = total / (ms * 1e-3) / 1e6
+    x_ms = statistics.mean(a.elapsed_time(b) for a, b in xform_ms)
+    npx_rank = rows * W
+    achieved = BYTES_PER_PX * npx_rank / (x_ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "xform_traffic.json")))
+        traffic = prof.get("bytes_per_px")
+    except Exception:
+        pass
+
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpx/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (on-GPU generator, model of src/synthetic.py)",
+            "config": workload_config(args, world),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "kernel": "spcn_xform_rgb8 (k_xform_tma + repair)",
+                         "kernel_ms": round(x_ms, 4), "share_of_step": round(x_ms / ms, 4),
+                         "algorithmic_bytes_per_px": BYTES_PER_PX,
+                         "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
+            "gpu_launches": int(launches), "clocks": clk}
+
+    # ---- end-to-end through the public API with pinned host buffers
+    if not args.no_e2e:
+        try:
+            line["e2e"] = e2e(args, pb, slide, target, rank, world)
+        except Exception as exc:  # pragma: no cover
+            line["e2e"] = {"value": None, "unit": "Mpx/s", "error": repr(exc)[:200]}
+    # ---- CPU baseline (rank 0, N = 1 only)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args, slide, target)
+        except Exception as exc:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def e2e(args, pb, slide, target, rank, world):
+    """Same metric through pb.fit/pb.transform with host (pinned) input and output."""
+    import torch
+
+    rows, W = slide.shape[0], slide.shape[1]
+    nbytes = slide.numel()
+    avail = 0
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable"):
+                avail = int(ln.split()[1]) * 1024
+    except Exception:
+        pass
+    use_rows = rows
+    if avail and 2.3 * nbytes > avail / max(1, world):
+        use_rows = max(1024, int(rows * (avail / max(1, world)) / (2.5 * nbytes)))
+    h_src = torch.empty((use_rows, W, 3), dtype=torch.uint8, pin_memory=True)
+    h_src.copy_(slide[:use_rows])
+    h_dst = torch.empty_like(h_src).pin_memory()
+    src = pb.ArraySource(h_src.numpy())
+    times = []
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fp = pb.fit(src)
+        sink = pb.ArrayWriter(W, use_rows, out=h_dst.numpy())
+        pb.transform(src, fp, target, sink, precision=args.precision, workers=3)
+        torch.cuda.synchronize()
+        if i:                       # first run = warm-up
+            times.append(time.perf_counter() - t0)
+    sec = min(times)
+    if world > 1:
+        tt = torch.tensor([sec], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        sec = float(tt.item())
+    px = use_rows * W * world
+    res = {"value": round(px / sec / 1e6, 3), "unit": "Mpx/s",
+           "h2d_bytes_per_step": int(use_rows * W * 3), "d2h_bytes_per_step": int(use_rows * W * 3),
+           "rows_per_gpu": use_rows, "seconds_per_step": round(sec, 4),
+           "path": "pb.fit(ArraySource(pinned)) + pb.transform(→ ArrayWriter(pinned)), 3 streams"}
+    del h_src, h_dst
+    return res
+
+
+def cpu_baseline(args, slide, target):
+    """Oracle port of the reference path on the host cores (bounded band)."""
+    cores = os.cpu_count() or 1
+    rows = max(16, args.cpu_rows)
+    band = slide[:rows].cpu().numpy()
+    tgt = dict(i0=np.asarray(target.i0), basis=np.asarray(target.basis),
+               p99=np.asarray(target.stats.p99))
+    tf, tx = cpu_reference_run(band, tgt, cores)
+    total = args.width * args.height
+    v = extrapolated_mpx(total, band.shape[0] * band.shape[1], tf, tx)
+    return {"value": round(v, 3), "unit": "Mpx/s", "cores": cores, "kind": "port",
+            "sample": (f"{rows} x {args.width} band ({rows * args.width / 1e6:.1f} Mpx) of the "
+                       f"same slide; fit {tf:.3f} s + transform {tx:.3f} s (oracle port = "
+                       f"reference algorithm in NumPy, {cores} threads, strip 64), "
+                       f"extrapolated linearly to {total / 1e9:.0f} Gpx")}
+
+
+def main():
+    args = parse()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    rank, world, local = dist_setup(args) if args.impl == "ours" else (
+        int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -190,11 +190,32 @@ int spcn_percentile_segments(const double* h, int64_t total, const int64_t* seg_
 int spcn_select_kth(const double* values, const int64_t* begin, const int64_t* end,
                     const int64_t* k, int32_t nq, void* qbuf, double* out, void* stream);
 
+/* ---- measurement input: synthetic H&E slides --------------------------- */
+typedef struct spcn_synth_params {
+  float i0[3];             /* background intensity per channel              */
+  float basis[6];          /* mixing basis, row-major 3x2 (reference H&E)   */
+  float tissue_fraction;
+  int32_t layout;          /* 0 = scatter, 1 = block (src/synthetic.py:75-89) */
+  int32_t dense;           /* 0 = sparse_densities, 1 = dense_densities     */
+} spcn_synth_params;
+
+/* Render rows [row0, row0+rows) of a width x height synthetic slide into
+ * `out` (packed RGB8, 16-byte aligned).  Model of src/synthetic.py:26-121
+ * with a counter-based RNG (pixel content depends only on seed and the
+ * pixel's absolute position).  Not part of the reference's API: it is the
+ * input generator for 400-Mpx..10-Gpx measurements.                        */
+int spcn_render_synthetic(uint8_t* out, int64_t width, int64_t row0, int64_t rows,
+                          int64_t height, uint64_t seed, const spcn_synth_params* p,
+                          void* stream);
+
 /* Thread-local description of the last error ("" if none).                 */
 const char* spcn_last_error(void);
 
 /* Library version string.                                                   */
 const char* spcn_version(void);
+
+/* Number of kernels libspcn has launched in this process (diagnostics).     */
+uint64_t spcn_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -29,7 +29,10 @@ PREC = {"exact": 0, "fast": 1, "strict": 2}
 EXPORTS = (
     "spcn_xform_workspace_bytes", "spcn_xform_rgb8", "spcn_xform_repair_count",
     "spcn_code_densities", "spcn_normalize_block", "spcn_beer_lambert",
-    "spcn_inverse_beer_lambert", "spcn_last_error", "spcn_version",
+    "spcn_inverse_beer_lambert", "spcn_sample_count", "spcn_sample_compact",
+    "spcn_i0_from_hist", "spcn_od_tables", "spcn_snmf_batched", "spcn_code_samples",
+    "spcn_percentile_segments", "spcn_select_kth", "spcn_render_synthetic",
+    "spcn_last_error", "spcn_version", "spcn_launch_count",
 )
 
 
@@ -66,6 +69,7 @@ _SIGS = {
     "spcn_inverse_beer_lambert": (ctypes.c_int, [P, P, I64, P, P]),
     "spcn_last_error": (ctypes.c_char_p, []),
     "spcn_version": (ctypes.c_char_p, []),
+    "spcn_launch_count": (ctypes.c_uint64, []),
 }
 
 

@@ -14,6 +14,12 @@
 #include "spcn_device.cuh"
 #include "xform.h"
 
+#include "launch_count.h"
+
+namespace spcn {
+std::atomic<unsigned long long> g_launches{0};
+}
+
 using namespace spcn;
 
 namespace {
@@ -154,6 +160,8 @@ extern "C" {
 const char* spcn_last_error(void) { return g_err.c_str(); }
 
 const char* spcn_version(void) { return "spcn-b200 0.1.0 (sm_100a)"; }
+
+uint64_t spcn_launch_count(void) { return spcn::g_launches.load(std::memory_order_relaxed); }
 
 size_t spcn_xform_workspace_bytes(int64_t npix) {
   const int64_t cap = 65536 + (npix > 0 ? npix / 32 : 0);
@@ -431,3 +439,22 @@ int spcn_select_kth(const double* values, const int64_t* begin, const int64_t* e
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ synthetic input
+#include "synth.h"
+
+extern "C" int spcn_render_synthetic(uint8_t* out, int64_t width, int64_t row0, int64_t rows,
+                                     int64_t height, uint64_t seed, const spcn_synth_params* p,
+                                     void* stream) {
+  g_err.clear();
+  if (!p) return fail(SPCN_EINVAL, "params is NULL");
+  if (width < 1 || rows < 0 || row0 < 0 || row0 + rows > height)
+    return fail(SPCN_EINVAL, "bad slide geometry");
+  if (rows == 0) return SPCN_OK;
+  if (!out) return fail(SPCN_EINVAL, "out is NULL");
+  if ((reinterpret_cast<uintptr_t>(out) & 15u) != 0)
+    return fail(SPCN_EINVAL, "out must be 16-byte aligned");
+  cudaError_t e = launch_render(out, width, row0, rows, height, seed, *p,
+                                static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "render_synthetic");
+}

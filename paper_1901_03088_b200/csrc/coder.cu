@@ -4,6 +4,7 @@
 //   beer_lambert    (src/optics.py:71-94, through the 256-entry OD table)
 // These are the building blocks the reference exposes publicly; the fused
 // transform (xform.cu) is what the hot path runs.
+#include "launch_count.h"
 #include "spcn_device.cuh"
 #include "xform.h"
 
@@ -69,28 +70,28 @@ cudaError_t launch_code_densities(const double* od, double* h, int64_t n, const 
                                   cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_code_densities<<<grid_for(n), 256, 0, st>>>(od, h, n, sp);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_normalize_block(const double* h, uint8_t* out, int64_t n, const StrictP& sp,
                                    cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_normalize_block<<<grid_for(n), 256, 0, st>>>(h, out, n, sp);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_beer_lambert(const uint8_t* px, double* od, int64_t n, const StrictP& sp,
                                 cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_beer_lambert<<<grid_for(n), 256, 0, st>>>(px, od, n, sp);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_inverse_bl(const double* od, uint8_t* out, int64_t n, const StrictP& sp,
                               cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_inverse_bl<<<grid_for(n), 256, 0, st>>>(od, out, n, sp);
-  return cudaGetLastError();
+  return launched();
 }
 
 }  // namespace spcn

@@ -16,6 +16,7 @@
 //                    so "first N in raster order" is reproduced exactly; the
 //                    taken bright values go straight into 256-bin histograms.
 //   k_i0_from_hist   exact 80th percentile of the bright pools from the counts.
+#include "launch_count.h"
 #include "spcn_device.cuh"
 #include "spcn.h"
 #include "sample.h"
@@ -221,7 +222,7 @@ cudaError_t launch_sample_count(const uint8_t* img, const spcn_patch* patches, i
   if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;
   k_sample_count<<<dim3(max_chunks, npatches), kSThreads, 0, st>>>(img, patches, max_chunks, thr,
                                                                    counts);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches, int npatches,
@@ -231,21 +232,21 @@ cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches,
   if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;
   k_sample_compact<<<dim3(max_chunks, npatches), kSThreads, 0, st>>>(
       img, patches, max_chunks, thr, counts, takes, out_px, bright_hist);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_i0_from_hist(const int32_t* hist, int nprob, double* i0, int32_t* empty,
                                 cudaStream_t st) {
   if (nprob <= 0) return cudaSuccess;
   k_i0_from_hist<<<(nprob * 3 + 127) / 128, 128, 0, st>>>(hist, nprob, i0, empty);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_od_tables(const double* i0, int nprob, double* lut, cudaStream_t st) {
   if (nprob <= 0) return cudaSuccess;
   const int64_t n = (int64_t)nprob * 3 * 256;
   k_od_tables<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(i0, nprob, lut);
-  return cudaGetLastError();
+  return launched();
 }
 
 }  // namespace spcn

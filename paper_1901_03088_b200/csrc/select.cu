@@ -8,6 +8,7 @@
 // construction (integer counting), so percentile-histogram counts are
 // bit-exact given identical densities.
 #include "select.h"
+#include "launch_count.h"
 #include "spcn_device.cuh"
 
 namespace spcn {
@@ -142,14 +143,14 @@ cudaError_t launch_build_queries(const int64_t* b, const int64_t* e, const int64
                                  SelQuery* qs, cudaStream_t st) {
   if (nq <= 0) return cudaSuccess;
   k_build_queries<<<(nq + 127) / 128, 128, 0, st>>>(b, e, k, nq, qs);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_select(const double* values, const SelQuery* qs, int nq, double* out,
                           cudaStream_t st) {
   if (nq <= 0) return cudaSuccess;
   k_select<<<nq, kSelThreads, 0, st>>>(values, qs, out);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_p99(const double* h, int64_t total, const int64_t* seg, int nseg, double p,
@@ -158,11 +159,11 @@ cudaError_t launch_p99(const double* h, int64_t total, const int64_t* seg, int n
   if (nseg <= 0) return cudaSuccess;
   const int n2 = nseg * 2;
   k_p99_queries<<<(n2 + 127) / 128, 128, 0, st>>>(seg, nseg, total, p, qbuf);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launched();
   if (e != cudaSuccess) return e;
   if ((e = launch_select(h, qbuf, 3 * n2, selbuf, st)) != cudaSuccess) return e;
   k_p99_combine<<<(n2 + 127) / 128, 128, 0, st>>>(seg, nseg, p, selbuf, p99, absent);
-  return cudaGetLastError();
+  return launched();
 }
 
 }  // namespace spcn

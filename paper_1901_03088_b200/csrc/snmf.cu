@@ -21,6 +21,7 @@
 // ~1e-15).
 #include <cooperative_groups.h>
 
+#include "launch_count.h"
 #include "snmf.h"
 #include "spcn_device.cuh"
 
@@ -310,8 +311,9 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_snmf, samples, od, offsets, nprob, luts, a, hbuf, total,
-                            basis_out, hist_out, info_out);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_snmf, samples, od, offsets, nprob, luts, a,
+                                           hbuf, total, basis_out, hist_out, info_out);
+  return e != cudaSuccess ? e : launched();
 }
 
 cudaError_t launch_code_samples(const uint8_t* samples, const int64_t* offsets, int nprob,
@@ -323,7 +325,7 @@ cudaError_t launch_code_samples(const uint8_t* samples, const int64_t* offsets, 
   if (gx > 64) gx = 64;
   k_code_samples<<<dim3((unsigned)gx, nprob), 256, 0, st>>>(samples, offsets, nprob, luts, bases,
                                                             lam, max_sweeps, h, total);
-  return cudaGetLastError();
+  return launched();
 }
 
 }  // namespace spcn

@@ -16,6 +16,7 @@
 //   k_xform_repair      fp64 reference-order recompute of the listed pixels.
 //   k_xform_strict      fp64 reference-order path for every pixel (STRICT mode,
 //                       head/tail pixels, unaligned buffers).
+#include "launch_count.h"
 #include "spcn_device.cuh"
 #include "xform.h"
 
@@ -269,7 +270,7 @@ cudaError_t launch_xform_tma(int mode, const uint8_t* src, uint8_t* dst, int64_t
     k_xform_tma<0><<<grid, kThreads, kXformSmem, st>>>(src, dst, npix, fp, sp, rl);
   else
     k_xform_tma<1><<<grid, kThreads, kXformSmem, st>>>(src, dst, npix, fp, sp, rl);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_xform_repair(uint8_t* dst, const StrictP& sp, unsigned long long* count,
@@ -279,7 +280,7 @@ cudaError_t launch_xform_repair(uint8_t* dst, const StrictP& sp, unsigned long l
   if (e != cudaSuccess) return e;
   RepairList rl{count, items, cap};
   k_xform_repair<<<g_sm_count * 2, 256, 0, st>>>(dst, sp, rl);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_xform_strict(const uint8_t* src, uint8_t* dst, int64_t npix,
@@ -290,7 +291,7 @@ cudaError_t launch_xform_strict(const uint8_t* src, uint8_t* dst, int64_t npix,
   const int64_t want = (npix + 255) / 256;
   const int grid = static_cast<int>(min64(want, (int64_t)g_sm_count * 16));
   k_xform_strict<<<grid, 256, 0, st>>>(src, dst, npix, sp);
-  return cudaGetLastError();
+  return launched();
 }
 
 int xform_tile_pixels() { return kTilePx; }

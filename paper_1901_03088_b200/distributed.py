@@ -1,0 +1,181 @@
+"""Row-band sharding of one whole-slide image across GPUs.
+
+Every rank holds a contiguous band of full-width rows [r0, r0 + rows) of a
+W x H slide.  The transform needs no exchange (it is pointwise-pure: output
+is bit-identical for any strip partition, src/pipeline.py:275-345).  The
+sample-mode fit (src/pipeline.py:128-257) is made distributed without moving
+pixels except the ≤100 k sampled ones:
+
+  1. every rank derives the same seeded patch visit order (numpy PCG64);
+  2. each rank counts (non-white, bright R/G/B) on its slice of every
+     candidate patch; an all-gather of those per-rank totals (ranks x
+     candidates x 4 int64) gives every rank the global per-patch counts and
+     the per-rank prefix inside each patch's raster order;
+  3. every rank replays the reference's visit loop on the global counts
+     (identical decisions everywhere), converts the global takes into its own
+     local takes (clip by the prefix of lower ranks), and compacts its
+     pixels into their global positions of the sample buffer;
+  4. one all-reduce(sum) of the sample bytes (disjoint writers) and of the
+     3 x 256 bright histogram completes the sample on every rank;
+  5. every rank runs the (deterministic) i0 → SNMF → coding → p99 chain on
+     the identical sample, so all ranks hold identical FitParams with no
+     broadcast.
+
+Collectives: one all-gather (KBs) and two all-reduces (~300 KB) per fit over
+NCCL/NVLink.  The host-side pieces (``local_parts``, ``split_takes``) are
+pure functions tested on CPU with gloo, world size 2.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _dev, _lib
+
+CHUNK = 4096
+
+
+def local_parts(rects, r0: int, rows: int, width: int):
+    """Intersect global candidate rects (x, y, w, h) with the band.
+
+    Returns a list aligned with ``rects`` of (base_px, w, h_local, row_offset)
+    or None when the patch has no rows in this band.  ``base_px`` is the pixel
+    offset of the slice's first pixel inside the band buffer, ``row_offset``
+    the first patch row the slice covers (its raster rank start is
+    row_offset * w).
+    """
+    out = []
+    for (x, y, w, h) in rects:
+        a, b = max(y, r0), min(y + h, r0 + rows)
+        if a >= b:
+            out.append(None)
+        else:
+            out.append(((a - r0) * width + x, w, b - a, a - y))
+    return out
+
+
+def split_takes(takes, per_rank_totals, rank: int):
+    """Global takes → this rank's takes.
+
+    takes: list of (cand, take_nonwhite, out_base, [tb_r, tb_g, tb_b]) from the
+    visit loop; per_rank_totals: (world, ncand, 4) local counts of every rank
+    (ranks are ordered by band, i.e. by raster order inside a patch).
+    Returns list of (cand, take_nonwhite, out_base, [tb...]) for this rank,
+    omitting entries with nothing to take.
+    """
+    prefix = per_rank_totals[:rank].sum(axis=0)        # (ncand, 4) counts of lower ranks
+    mine = per_rank_totals[rank]
+    res = []
+    for cand, tnw, base, tb in takes:
+        pre, loc = prefix[cand], mine[cand]
+        lnw = int(np.clip(tnw - pre[0], 0, loc[0]))
+        ltb = [int(np.clip(tb[c] - pre[1 + c], 0, loc[1 + c])) for c in range(3)]
+        if lnw or any(ltb):
+            res.append((cand, lnw, int(base + min(pre[0], tnw)), ltb))
+    return res
+
+
+class RowBandGroup:
+    """Sample-mode fit of a row-band-sharded slide (one instance per rank)."""
+
+    def __init__(self, width: int, height: int, r0: int, rows: int, group=None):
+        self.width, self.height, self.r0, self.rows = width, height, r0, rows
+        self.group = group
+
+    def fit(self, band_source, plan=None, cfg=None, *, code_lam: float = 0.0,
+            per_patch_stats: bool = False, source_label: str = ""):
+        import torch
+        import torch.distributed as dist
+
+        from . import optics, snmf
+        from .errors import BlankSlideError, InsufficientPixelsError
+        from .normalize import FitParams, config_hash, stain_stats
+        from .pipeline import (PATCH_DT, TAKE_DT, SamplePlan, _cfg_fields, _lib_sample, _stage,
+                               _visit)
+        from .stain_sep import SnmfConfig
+
+        plan = plan or SamplePlan()
+        cfg = cfg or SnmfConfig()
+        L = _lib_sample()
+        W, H = self.width, self.height
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        rng = np.random.default_rng(plan.seed)
+        origins = [(x, y) for y in range(0, H, plan.patch_size) for x in range(0, W, plan.patch_size)]
+        order = rng.permutation(len(origins))
+        ncand = min(len(order), 10 * plan.max_patches)
+        rects = [(origins[i][0], origins[i][1], min(plan.patch_size, W - origins[i][0]),
+                  min(plan.patch_size, H - origins[i][1])) for i in order[:ncand]]
+        parts = local_parts(rects, self.r0, self.rows, W)
+        img = band_source.tensor
+        thr = int(plan.white_threshold)
+        dev = img.device
+        present = [i for i, p in enumerate(parts) if p is not None]
+        chunks = max([1] + [-(-(p[1] * p[2]) // CHUNK) for p in parts if p is not None])
+        local_tot = np.zeros((ncand, 4), dtype=np.int64)
+        cnt_dev = None
+        if present:
+            desc = np.array([(parts[i][0], parts[i][1], parts[i][2], W) for i in present],
+                            dtype=PATCH_DT)
+            d = torch.from_numpy(desc.view(np.uint8).copy()).to(dev)
+            cnt_dev = torch.empty((len(present), chunks, 4), dtype=torch.int32, device=dev)
+            _lib.check(L.spcn_sample_count(_lib.ptr(img), _lib.ptr(d), len(present), chunks, thr,
+                                           _lib.ptr(cnt_dev), _lib.stream_handle()), "sample_count")
+            local_tot[present] = cnt_dev.sum(dim=1).cpu().numpy()
+        # all-gather of per-rank totals (ranks in band order)
+        lt = torch.from_numpy(local_tot).to(dev)
+        gathered = [torch.empty_like(lt) for _ in range(world)]
+        dist.all_gather(gathered, lt, group=self.group)
+        per_rank = np.stack([g.cpu().numpy() for g in gathered])
+        glob = per_rank.sum(axis=0)
+        takes, used_counts, collected, visited, used = _visit(
+            plan, order[:ncand], rects, lambda k: tuple(int(v) for v in glob[k]))
+        if collected == 0:
+            raise BlankSlideError("sampling: blank slide: no non-white pixels found in any "
+                                  "sampled patch")
+        sample = torch.zeros((collected, 3), dtype=torch.uint8, device=dev)
+        hist = torch.zeros((1, 3, 256), dtype=torch.int32, device=dev)
+        mine = [tk for tk in split_takes(takes, per_rank, rank) if parts[tk[0]] is not None]
+        if mine:
+            pos = {c: j for j, c in enumerate(present)}
+            idx = np.array([pos[tk[0]] for tk in mine], dtype=np.int64)
+            desc = np.array([(parts[tk[0]][0], parts[tk[0]][1], parts[tk[0]][2], W)
+                             for tk in mine], dtype=PATCH_DT)
+            tk = np.zeros(len(mine), dtype=TAKE_DT)
+            tk["take_nonwhite"] = [m[1] for m in mine]
+            tk["out_base"] = [m[2] for m in mine]
+            tk["take_bright"] = [m[3] for m in mine]
+            cnt = cnt_dev[torch.from_numpy(idx).to(dev)].contiguous()
+            d = torch.from_numpy(desc.view(np.uint8).copy()).to(dev)
+            dt = torch.from_numpy(tk.view(np.uint8).copy()).to(dev)
+            _lib.check(L.spcn_sample_compact(_lib.ptr(img), _lib.ptr(d), len(mine), chunks, thr,
+                                             _lib.ptr(cnt), _lib.ptr(dt), _lib.ptr(sample),
+                                             _lib.ptr(hist), _lib.stream_handle()),
+                       "sample_compact")
+        dist.all_reduce(sample, group=self.group)     # disjoint writers: sum == gather
+        dist.all_reduce(hist, group=self.group)
+        # --- identical, deterministic fit on every rank
+        m = collected
+        i0 = _stage("background estimation", optics.i0_from_counts,
+                    hist.cpu().numpy()[0].astype(np.int64))
+        lut = torch.from_numpy(optics.od_table(i0)).to(dev).reshape(1, 3, 256)
+        if m < 10:
+            raise InsufficientPixelsError(
+                f"basis fit: insufficient pixels: need at least 10 OD samples, got {m}")
+        offsets = torch.tensor([0, m], dtype=torch.int64, device=dev)
+        flat = sample.reshape(-1)
+        r = snmf.snmf_batched(flat, offsets, lut, cfg, cluster=8 if m >= 20_000 else 1)
+        info = r.info.cpu().numpy()[0]
+        snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
+        h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
+        if per_patch_stats:
+            from . import stats as dstats
+
+            counts = [c for c in used_counts if c > 0]
+            seg = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+            vals, _ = dstats.segment_percentiles(h, seg, 99.0)
+            st = _stage("density stats", stain_stats,
+                        patch_p99s=[tuple(v) for v in vals.cpu().numpy()], sample_count=m)
+        else:
+            st = _stage("density stats", stain_stats, h)
+        prov = {"source": str(source_label),
+                "config_hash": config_hash(_cfg_fields(plan, cfg, code_lam, per_patch_stats))}
+        return FitParams(i0=i0, basis=r.basis.cpu().numpy()[0], stats=st, provenance=prov)

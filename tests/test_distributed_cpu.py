@@ -1,0 +1,124 @@
+"""Multi-process (gloo, world size 2, CPU) test of the row-band sharded fit logic.
+
+The device kernels are replaced by NumPy emulations of their contracts
+(per-chunk counts; ordered compaction), everything else is the product code:
+``distributed.local_parts``, ``distributed.split_takes``, the reference visit
+loop ``pipeline._visit``, and the all-gather / all-reduce(sum) exchange.  The
+assembled sample must equal the single-process reference sampling.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import spcn_oracle as orc
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _emulate_counts(band, part, thr):
+    base, w, h, _ = part
+    W = band.shape[1]
+    rows = np.stack([band.reshape(-1, 3)[base + r * W: base + r * W + w] for r in range(h)])
+    px = rows.reshape(-1, 3)
+    nw = ~np.all(px > thr, axis=1)
+    return np.array([nw.sum(), (px[:, 0] > thr).sum(), (px[:, 1] > thr).sum(),
+                     (px[:, 2] > thr).sum()], dtype=np.int64), px
+
+
+def _worker(rank, world, port, img, plan_kw, q):
+    import torch.distributed as dist
+    import torch
+
+    from paper_1901_03088_b200 import distributed as dd
+    from paper_1901_03088_b200.pipeline import SamplePlan, _visit
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        H, W = img.shape[:2]
+        per = H // world
+        r0 = rank * per
+        rows = per if rank < world - 1 else H - r0
+        band = np.ascontiguousarray(img[r0:r0 + rows])
+        plan = SamplePlan(**plan_kw)
+        rng = np.random.default_rng(plan.seed)
+        origins = [(x, y) for y in range(0, H, plan.patch_size) for x in range(0, W, plan.patch_size)]
+        order = rng.permutation(len(origins))
+        ncand = min(len(order), 10 * plan.max_patches)
+        rects = [(origins[i][0], origins[i][1], min(plan.patch_size, W - origins[i][0]),
+                  min(plan.patch_size, H - origins[i][1])) for i in order[:ncand]]
+        parts = dd.local_parts(rects, r0, rows, W)
+        thr = plan.white_threshold
+        local = np.zeros((ncand, 4), dtype=np.int64)
+        pix = {}
+        for i, p in enumerate(parts):
+            if p is not None:
+                local[i], pix[i] = _emulate_counts(band, p, thr)
+        lt = torch.from_numpy(local)
+        gathered = [torch.empty_like(lt) for _ in range(world)]
+        dist.all_gather(gathered, lt)
+        per_rank = np.stack([g.numpy() for g in gathered])
+        glob = per_rank.sum(axis=0)
+        takes, counts, collected, visited, used = _visit(
+            plan, order[:ncand], rects, lambda k: tuple(int(v) for v in glob[k]))
+        sample = np.zeros((collected, 3), dtype=np.int64)
+        hist = np.zeros((3, 256), dtype=np.int64)
+        for cand, tnw, base, tb in dd.split_takes(takes, per_rank, rank):
+            px = pix[cand]
+            nw = px[~np.all(px > thr, axis=1)][:tnw]
+            sample[base:base + len(nw)] = nw
+            for c in range(3):
+                vals = px[:, c][px[:, c] > thr][:tb[c]]
+                hist[c] += np.bincount(vals, minlength=256)
+        st = torch.from_numpy(sample)
+        ht = torch.from_numpy(hist)
+        dist.all_reduce(st)
+        dist.all_reduce(ht)
+        if rank == 0:
+            q.put((st.numpy().astype(np.uint8), ht.numpy(), counts, visited, used))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("plan_kw", [dict(patch_size=128, target_pixels=30_000, seed=3),
+                                     dict(patch_size=100, target_pixels=5_000, seed=1,
+                                          sample_cap=700, max_patches=4)])
+def test_row_band_fit_sample_equals_single_process(plan_kw):
+    import torch.multiprocessing as mp
+
+    img, _, _ = orc.render(300, 333, 5, tissue_fraction=0.5)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, img, plan_kw, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    sample, hist, counts, visited, used = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = orc.gather_sample(img, orc.Plan(**plan_kw))
+    assert np.array_equal(sample, ref["non_white"])
+    assert np.array_equal(hist, np.stack([np.bincount(b, minlength=256) for b in ref["bright"]]))
+    assert list(counts) == list(ref["counts"])
+    assert (visited, used) == (ref["visited"], ref["used"])
+
+
+def test_split_takes_partitions_global_takes():
+    from paper_1901_03088_b200.distributed import split_takes
+
+    per_rank = np.array([[[5, 3, 0, 9]], [[7, 4, 2, 1]], [[2, 2, 2, 2]]], dtype=np.int64)
+    takes = [(0, 10, 100, [6, 1, 10])]
+    got = [split_takes(takes, per_rank, r) for r in range(3)]
+    assert got[0] == [(0, 5, 100, [3, 0, 9])]
+    assert got[1] == [(0, 5, 105, [3, 1, 1])]
+    assert got[2] == []
