@@ -56,7 +56,18 @@ typedef struct spcn_xform_params {
                                (src/optics.py:89-94); NULL = computed with libm  */
   int32_t precision;        /* SPCN_PREC_*                                       */
   int32_t max_sweeps;       /* CD sweep cap, reference 2000 (src/stain_sep.py:168) */
+  double cert_alpha;        /* EXACT only: relative certification bound from
+                               spcn_xform_calibrate (> 0), or <= 0 for the
+                               analytic per-pixel bound                          */
 } spcn_xform_params;
+
+/* Exhaustive calibration of the EXACT certification bound for one parameter
+ * set: runs the fp32 path and the fp64 reference-order path on all 2^24 RGB
+ * colours and returns alpha = 1.5 * max relative error + 2^-22 (or -1 when
+ * the fast path is not applicable).  Valid by exhaustion for every input.
+ * Synchronizes `stream`; ~0.5 ms on a B200.  workspace >= 16 bytes.        */
+int spcn_xform_calibrate(const spcn_xform_params* p, void* workspace,
+                         size_t workspace_bytes, double* alpha_out, void* stream);
 
 /* Device workspace (bytes) needed by spcn_xform_rgb8 for `npix` pixels.     */
 size_t spcn_xform_workspace_bytes(int64_t npix);

@@ -28,6 +28,7 @@ PREC = {"exact": 0, "fast": 1, "strict": 2}
 # every symbol include/spcn.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "spcn_xform_workspace_bytes", "spcn_xform_rgb8", "spcn_xform_repair_count",
+    "spcn_xform_calibrate",
     "spcn_code_densities", "spcn_normalize_block", "spcn_beer_lambert",
     "spcn_inverse_beer_lambert", "spcn_sample_count", "spcn_sample_compact",
     "spcn_i0_from_hist", "spcn_od_tables", "spcn_snmf_batched", "spcn_code_samples",
@@ -47,6 +48,7 @@ class XformParams(ctypes.Structure):
         ("od_table", ctypes.POINTER(ctypes.c_double)),
         ("precision", ctypes.c_int32),
         ("max_sweeps", ctypes.c_int32),
+        ("cert_alpha", ctypes.c_double),
     ]
 
 
@@ -63,6 +65,8 @@ _SIGS = {
     "spcn_xform_workspace_bytes": (SZ, [I64]),
     "spcn_xform_rgb8": (ctypes.c_int, [P, P, I64, ctypes.POINTER(XformParams), P, SZ, P]),
     "spcn_xform_repair_count": (ctypes.c_int, [P, P, ctypes.POINTER(I64)]),
+    "spcn_xform_calibrate": (ctypes.c_int, [ctypes.POINTER(XformParams), P, SZ,
+                                            ctypes.POINTER(DBL), P]),
     "spcn_code_densities": (ctypes.c_int, [P, P, I64, P, DBL, I32, P]),
     "spcn_normalize_block": (ctypes.c_int, [P, P, I64, P, P, P, P]),
     "spcn_beer_lambert": (ctypes.c_int, [P, P, I64, P, P, P]),

@@ -108,8 +108,9 @@ bool fill_fast(FastP& fp, const StrictP& sp, bool exact) {
   fp.nlam = static_cast<float>(-sp.lam);
   const double A = g11 / det, C = g01 / det, E = 1.0 / g11, F = g01 / g11, G = 1.0 / g00,
                H = g01 / g00;
-  fp.A = (float)A; fp.C = (float)C; fp.E = (float)E;
-  fp.F = (float)F; fp.G = (float)G; fp.H = (float)H;
+  fp.A = (float)A; fp.nC = -(float)C; fp.E = (float)E;
+  fp.nF = -(float)F; fp.G = (float)G; fp.nH = -(float)H;
+  for (int c = 0; c < 3; ++c) fp.ilo[c] = fp.ihi[c] = 0.0f;
   const double log2e = 1.4426950408889634;
   double Kabs[3][2];
   for (int c = 0; c < 3; ++c)
@@ -168,6 +169,78 @@ size_t spcn_xform_workspace_bytes(int64_t npix) {
   return kWsHeader + static_cast<size_t>(cap) * 8;
 }
 
+}  // extern "C"
+
+namespace {
+// Validation shared by the transform entry points (see the file header).
+int check_xform_params(const spcn_xform_params* p) {
+  if (!p) return fail(SPCN_EINVAL, "params is NULL");
+  if (p->precision < 0 || p->precision > 2) return fail(SPCN_EINVAL, "unknown precision");
+  for (int c = 0; c < 3; ++c) {
+    if (!(p->src_i0[c] >= 1.0) || !std::isfinite(p->src_i0[c]))
+      return fail(SPCN_EINVAL, "i0 components must be >= 1");
+    if (!std::isfinite(p->tgt_i0[c])) return fail(SPCN_EINVAL, "target i0 must be finite");
+  }
+  int rc = check_basis(p->src_basis, "source");
+  if (rc) return rc;
+  if ((rc = check_basis(p->tgt_basis, "target"))) return rc;
+  if (!(p->code_lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
+  for (int j = 0; j < 2; ++j)
+    if (!(p->factors[j] > 0.0) || !std::isfinite(p->factors[j]))
+      return fail(SPCN_EINVAL, "factors must be positive and finite");
+  if (p->max_sweeps < 0) return fail(SPCN_EINVAL, "max_sweeps must be >= 0");
+  return SPCN_OK;
+}
+
+// Calibrated certification interval bounds (rounded outward in fp32).
+void set_calibrated(FastP& fp, double alpha) {
+  fp.a1 = 0.0f;
+  fp.a0 = static_cast<float>(alpha);
+  for (int c = 0; c < 3; ++c) {
+    const double i0 = static_cast<double>(fp.i0t[c]);
+    float lo = static_cast<float>(i0 * (1.0 - alpha));
+    float hi = static_cast<float>(i0 * (1.0 + alpha));
+    lo = std::nextafter(lo, 0.0f);
+    hi = std::nextafter(hi, 1e30f);
+    fp.ilo[c] = lo;
+    fp.ihi[c] = hi;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int spcn_xform_calibrate(const spcn_xform_params* p, void* workspace, size_t workspace_bytes,
+                         double* alpha_out, void* stream) {
+  g_err.clear();
+  int rc = check_xform_params(p);
+  if (rc) return rc;
+  if (!alpha_out) return fail(SPCN_EINVAL, "alpha_out is NULL");
+  if (!workspace || workspace_bytes < kWsHeader) return fail(SPCN_EINVAL, "workspace too small");
+  double lut[3][256];
+  od_table(p->src_i0, p->od_table, lut);
+  static thread_local StrictP sp;
+  static thread_local FastP fp;
+  fill_strict(sp, &lut[0][0], p->src_basis, p->tgt_basis, p->factors, p->tgt_i0, p->code_lam,
+              p->max_sweeps);
+  *alpha_out = -1.0;
+  if (!fill_fast(fp, sp, true)) return SPCN_OK;   // fast path not applicable: strict is used
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned int* bits = static_cast<unsigned int*>(workspace);
+  cudaError_t e = cudaMemsetAsync(bits, 0, sizeof(unsigned int), st);
+  if (e == cudaSuccess) e = launch_calibrate(fp, sp, bits, st);
+  unsigned int h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, bits, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "xform_calibrate");
+  float worst;
+  std::memcpy(&worst, &h, sizeof(worst));
+  const double alpha = 1.5 * static_cast<double>(worst) + std::ldexp(1.0, -22);
+  // a calibrated bound looser than the analytic one is never used
+  *alpha_out = alpha < 1e-3 ? alpha : -1.0;
+  return SPCN_OK;
+}
+
 int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_xform_params* p,
                     void* workspace, size_t workspace_bytes, void* stream) {
   g_err.clear();
@@ -199,6 +272,11 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool exact = p->precision == SPCN_PREC_EXACT;
   bool fast_ok = p->precision != SPCN_PREC_STRICT && fill_fast(fp, sp, exact);
+  int mode = exact ? 0 : 1;
+  if (exact && fast_ok && p->cert_alpha > 0.0 && p->cert_alpha < 1e-3) {
+    set_calibrated(fp, p->cert_alpha);
+    mode = 2;
+  }
 
   // 16-byte alignment of the vector body (both buffers must share the phase)
   const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
@@ -225,8 +303,7 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
   cudaError_t e;
   if (head > 0 && (e = launch_xform_strict(src, dst, head, sp, st)) != cudaSuccess)
     return cuda_fail(e, "xform_head");
-  e = launch_xform_tma(exact ? 0 : 1, src + 3 * head, dst + 3 * head, body, fp, sp, count, items,
-                       cap, st);
+  e = launch_xform_tma(mode, src + 3 * head, dst + 3 * head, body, fp, sp, count, items, cap, st);
   if (e != cudaSuccess) return cuda_fail(e, "xform_tma");
   if (exact && (e = launch_xform_repair(dst + 3 * head, sp, count, items, cap, st)) != cudaSuccess)
     return cuda_fail(e, "xform_repair");

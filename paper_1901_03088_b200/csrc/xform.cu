@@ -9,13 +9,19 @@
 //   k_xform_tma<MODE>   persistent, warp-specialised: one producer warp streams
 //                       12 KiB tiles (4096 px) into a 4-stage shared-memory ring
 //                       with 1-D TMA bulk copies; 8 compute warps run the fp32
-//                       path (16 px / thread, OD via a 16-way replicated
-//                       shared-memory table) and store with 128-bit STG.
-//                       EXACT mode certifies each rounding and appends the
-//                       uncertified pixels to a repair list.
+//                       path two pixels at a time (FFMA2/FMUL2), look OD up in
+//                       a 16-way replicated shared-memory table addressed with
+//                       one PRMT per channel, pack output bytes with PRMT and
+//                       store with 128-bit STG.  MODE: 0 = EXACT with the
+//                       analytic per-pixel bound, 1 = FAST, 2 = EXACT with a
+//                       calibrated constant bound.  EXACT appends uncertified
+//                       pixels to a repair list.
 //   k_xform_repair      fp64 reference-order recompute of the listed pixels.
 //   k_xform_strict      fp64 reference-order path for every pixel (STRICT mode,
 //                       head/tail pixels, unaligned buffers).
+//   k_calibrate         runs the fast path and the fp64 path on all 2^24 RGB
+//                       colours and returns the largest relative error of the
+//                       fast path: a certification bound valid by exhaustion.
 #include "launch_count.h"
 #include "spcn_device.cuh"
 #include "xform.h"
@@ -27,8 +33,10 @@ constexpr int kTileBytes = 3 * kTilePx;       // 12 KiB
 constexpr int kStages = 4;
 constexpr int kComputeWarps = 8;
 constexpr int kThreads = 32 * (kComputeWarps + 1);
-constexpr int kLutRep = 16;                   // table copies (bank-conflict bound 2)
-constexpr int kLutBytes = 3 * 256 * kLutRep * 4;
+// OD table: 256 rows of 256 B; row x = [ch0 x16 | ch1 x16 | ch2 x16 | pad],
+// copy (lane & 15) of channel c at byte x*256 + c*64 + (lane&15)*4, so one
+// PRMT of (input word, lane constant) yields the address (bank conflicts <= 2).
+constexpr int kLutBytes = 256 * 256;
 constexpr size_t kXformSmem = kLutBytes + kStages * kTileBytes + 2 * kStages * sizeof(uint64_t);
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -60,13 +68,72 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int idx) {
   return (w[idx >> 2] >> (8 * (idx & 3))) & 0xffu;
 }
 
+// OD of input byte `idx` (0..47) of the thread's 48-byte block, channel c.
+__device__ __forceinline__ float od_lookup(const uint8_t* lut, const uint32_t* w, int idx,
+                                           uint32_t lc) {
+  const uint32_t sel = 0x5504u | ((uint32_t)(idx & 3) << 4);
+  const uint32_t addr = __byte_perm(w[idx >> 2], lc, sel);  // x*256 + c*64 + (lane&15)*4
+  return *reinterpret_cast<const float*>(lut + addr);
+}
+
+// Recolor two pixels (k, k+1) of the block; writes their 6 output "bytes"
+// (low byte of each word) to ob[3k .. 3k+5].  EXACT: returns, in 2-bit fields
+// 2k and 2k+2, how many channels of each pixel failed certification
+// (r_hi - r_lo is 0 or 1 per channel since the interval is narrower than 1).
+template <int MODE>
+__device__ __forceinline__ uint32_t recolor_pair(const FastP& fp, const uint8_t* lut,
+                                                 const uint32_t* w, int k, const uint32_t* lc,
+                                                 uint32_t* ob) {
+  const int a = 3 * k, b = 3 * k + 3;
+  const float2 v0 = make_float2(od_lookup(lut, w, a, lc[0]), od_lookup(lut, w, b, lc[0]));
+  const float2 v1 = make_float2(od_lookup(lut, w, a + 1, lc[1]), od_lookup(lut, w, b + 1, lc[1]));
+  const float2 v2 = make_float2(od_lookup(lut, w, a + 2, lc[2]), od_lookup(lut, w, b + 2, lc[2]));
+  const FastPair fq = fast_pair(fp, v0, v1, v2);
+  const float e[3][2] = {{fq.e0.x, fq.e0.y}, {fq.e1.x, fq.e1.y}, {fq.e2.x, fq.e2.y}};
+  if (MODE == 1) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float2 pw = make_float2(ex2_approx(e[c][0]), ex2_approx(e[c][1]));
+      const float2 r = __ffma2_rn(bc2(fp.i0t[c]), pw, bc2(kMagic));
+      ob[a + c] = __float_as_uint(r.x);
+      ob[b + c] = __float_as_uint(r.y);
+    }
+    return 0u;
+  }
+  float2 alpha = bc2(0.f);
+  if (MODE == 0) alpha = __ffma2_rn(bc2(fp.a1), fq.T, bc2(fp.a0));
+  uint32_t da = 0, db = 0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float pa = ex2_approx(e[c][0]), pb = ex2_approx(e[c][1]);
+    float2 Ia, Ib;
+    if (MODE == 0) {
+      Ia = cert_interval(fp.i0t[c], alpha.x);
+      Ib = cert_interval(fp.i0t[c], alpha.y);
+    } else {
+      Ia = Ib = make_float2(fp.ilo[c], fp.ihi[c]);
+    }
+    const float2 ra = __ffma2_rn(Ia, bc2(pa), bc2(kMagic));
+    const float2 rb = __ffma2_rn(Ib, bc2(pb), bc2(kMagic));
+    ob[a + c] = __float_as_uint(ra.y);
+    ob[b + c] = __float_as_uint(rb.y);
+    da += __float_as_uint(ra.y) - __float_as_uint(ra.x);
+    db += __float_as_uint(rb.y) - __float_as_uint(rb.x);
+  }
+  return (da << (2 * k)) | (db << (2 * k + 2));
+}
+
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 2)
     k_xform_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
                 const __grid_constant__ FastP fp, const __grid_constant__ StrictP sp,
                 RepairList rl) {
   extern __shared__ __align__(128) uint8_t smem[];
-  float* lut = reinterpret_cast<float*>(smem);
+  const uint8_t* lut = smem;
   uint8_t* stages = smem + kLutBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kTileBytes);
   uint64_t* empty = full + kStages;
@@ -75,10 +142,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (npix + kTilePx - 1) / kTilePx;
 
-  // replicated OD table: entry (c, x) copy r at float index c*4096 + x*16 + r
-  for (int i = tid; i < 3 * 256 * kLutRep; i += kThreads) {
-    const int c = i >> 12, x = (i >> 4) & 255;
-    lut[i] = fp.lut[c][x];
+  for (int i = tid; i < 256 * 48; i += kThreads) {
+    const int x = i / 48, rem = i - 48 * (i / 48), c = rem >> 4, r = rem & 15;
+    *reinterpret_cast<float*>(smem + x * 256 + c * 64 + r * 4) = fp.lut[c][x];
   }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -108,7 +174,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   // ---------------- compute warps
   const int ct = tid;                        // 0..255
-  const char* lbase = reinterpret_cast<const char*>(lut) + (lane & 15) * 4;
+  const uint32_t lrep = (uint32_t)(lane & 15) * 4;
+  const uint32_t lc[3] = {lrep, 64u + lrep, 128u + lrep};
   int i = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
     const int s = i % kStages;
@@ -124,37 +191,19 @@ __global__ void __launch_bounds__(kThreads, 2)
       w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
       w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
     }
-    uint32_t o[12];
-#pragma unroll
-    for (int k = 0; k < 12; ++k) o[k] = 0;
-    uint32_t badmask = 0;
+    uint32_t ob[48], o[12];
+    uint32_t badacc = 0;  // EXACT: 2-bit failure count per pixel
     if (valid) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const uint32_t r = byte_of(w, 3 * k), g = byte_of(w, 3 * k + 1), b = byte_of(w, 3 * k + 2);
-      const float v0 = *reinterpret_cast<const float*>(lbase + (r << 6));
-      const float v1 = *reinterpret_cast<const float*>(lbase + 16384 + (g << 6));
-      const float v2 = *reinterpret_cast<const float*>(lbase + 32768 + (b << 6));
-      const FastCore fc = fast_core(fp, v0, v1, v2);
-      uint32_t c0, c1, c2;
-      if (MODE == 0) {
-        const float alpha = __fmaf_rn(fp.a1, fc.T, fp.a0);
-        uint32_t bad = 0;
-        c0 = cert_channel(fp.i0t[0], alpha, fc.e0, bad);
-        c1 = cert_channel(fp.i0t[1], alpha, fc.e1, bad);
-        c2 = cert_channel(fp.i0t[2], alpha, fc.e2, bad);
-        badmask |= (bad != 0u ? 1u : 0u) << k;
-      } else {
-        c0 = fast_channel(fp.i0t[0], fc.e0);
-        c1 = fast_channel(fp.i0t[1], fc.e1);
-        c2 = fast_channel(fp.i0t[2], fc.e2);
+      for (int q = 0; q < 8; ++q) {
+        badacc |= recolor_pair<MODE>(fp, lut, w, 2 * q, lc, ob);
+        // pack output words as soon as their 4 bytes exist (short live ranges)
+#pragma unroll
+        for (int j = 0; j < 12; ++j)
+          if (4 * j + 3 >= 6 * q && 4 * j + 3 < 6 * q + 6)
+            o[j] = pack4(ob[4 * j], ob[4 * j + 1], ob[4 * j + 2], ob[4 * j + 3]);
       }
-      const int bi = 3 * k;
-      o[bi >> 2] |= (c0 & 0xffu) << (8 * (bi & 3));
-      o[(bi + 1) >> 2] |= (c1 & 0xffu) << (8 * ((bi + 1) & 3));
-      o[(bi + 2) >> 2] |= (c2 & 0xffu) << (8 * ((bi + 2) & 3));
     }
-    }  // valid (compute)
     // Release the stage only after every loaded word has been consumed: the
     // arrive does not wait for in-flight LDS, and the next TMA write into this
     // stage is an async-proxy write (cross-proxy WAR), hence also the fence.
@@ -162,13 +211,18 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (valid) {
-    uint4* d = reinterpret_cast<uint4*>(dst + 3 * (tile0 + 16 * ct));
-    d[0] = make_uint4(o[0], o[1], o[2], o[3]);
-    d[1] = make_uint4(o[4], o[5], o[6], o[7]);
-    d[2] = make_uint4(o[8], o[9], o[10], o[11]);
-
-    if (MODE == 0) {
+      uint4* d = reinterpret_cast<uint4*>(dst + 3 * (tile0 + 16 * ct));
+      d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+      d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+      d[2] = make_uint4(o[8], o[9], o[10], o[11]);
+    }
+    if (MODE != 1) {
       // warp-aggregated append of uncertified pixels to the repair list
+      uint32_t badmask = 0;
+      if (badacc) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) badmask |= (((badacc >> (2 * k)) & 3u) ? 1u : 0u) << k;
+      }
       const unsigned active = __activemask();
       if (__any_sync(active, badmask != 0u)) {
         const uint32_t cnt = __popc(badmask);
@@ -199,7 +253,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
-    }  // valid
   }
 }
 
@@ -235,6 +288,56 @@ __global__ void __launch_bounds__(256) k_xform_strict(const uint8_t* __restrict_
   }
 }
 
+// Exhaustive calibration: for every RGB colour (two per thread-iteration,
+// through the same fast_pair as the transform) compare y_fast = i0 * 2^e
+// (the exact product the certification scales) with the fp64 reference
+// value y_ref = i0 * exp(-v') computed in the reference's operation order;
+// record max |y_ref - y_fast| / y_fast over colours with y_fast > 0.
+__global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP fp,
+                                                   const __grid_constant__ StrictP sp,
+                                                   unsigned int* __restrict__ max_bits) {
+  __shared__ double lut[3 * 256];
+  __shared__ float flut[3 * 256];
+  for (int i = threadIdx.x; i < 3 * 256; i += 256) {
+    lut[i] = sp.lut[i >> 8][i & 255];
+    flut[i] = fp.lut[i >> 8][i & 255];
+  }
+  __syncthreads();
+  float worst = 0.f;
+  for (uint32_t q = blockIdx.x * 256u + threadIdx.x; q < (1u << 23); q += 256u * gridDim.x) {
+    const uint32_t ca = 2u * q, cb = 2u * q + 1u;   // colours: r | g<<8 | b<<16
+    const float2 v0 = make_float2(flut[ca & 255], flut[cb & 255]);
+    const float2 v1 = make_float2(flut[256 + ((ca >> 8) & 255)], flut[256 + ((cb >> 8) & 255)]);
+    const float2 v2 = make_float2(flut[512 + (ca >> 16)], flut[512 + (cb >> 16)]);
+    const FastPair fq = fast_pair(fp, v0, v1, v2);
+    const float e[3][2] = {{fq.e0.x, fq.e0.y}, {fq.e1.x, fq.e1.y}, {fq.e2.x, fq.e2.y}};
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const uint32_t col = side ? cb : ca;
+      const double d0 = lut[col & 255], d1 = lut[256 + ((col >> 8) & 255)], d2 = lut[512 + (col >> 16)];
+      const double b0 = strict_dot3(sp.ws[0][0], sp.ws[1][0], sp.ws[2][0], d0, d1, d2);
+      const double b1 = strict_dot3(sp.ws[0][1], sp.ws[1][1], sp.ws[2][1], d0, d1, d2);
+      double h0, h1;
+      strict_nnls(b0, b1, sp.g00, sp.g01, sp.g11, sp.det, sp.lam, sp.max_sweeps, sp.tol, h0, h1);
+      const double s0 = __dmul_rn(sp.f[0], h0), s1 = __dmul_rn(sp.f[1], h1);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double od = __dadd_rn(__dmul_rn(sp.wt[c][0], s0), __dmul_rn(sp.wt[c][1], s1));
+        const double yref = __dmul_rn(sp.i0t[c], exp(-od));
+        const double yfast = (double)fp.i0t[c] * (double)ex2_approx(e[c][side]);
+        if (yfast > 0.0) {
+          const float rel = (float)(fabs(yref - yfast) / yfast);
+          worst = fmaxf(worst, rel);
+        } else if (yref >= 0.25) {
+          worst = 1.0f;  // cannot happen for finite inputs; forces the analytic path
+        }
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) worst = fmaxf(worst, __shfl_xor_sync(0xffffffffu, worst, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(max_bits, __float_as_uint(worst));
+}
+
 // ------------------------------------------------------------------ launchers
 static int g_sm_count = 0;
 static int g_tma_blocks_per_sm = 0;
@@ -246,11 +349,11 @@ cudaError_t xform_setup_device() {
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  for (auto fn : {k_xform_tma<0>, k_xform_tma<1>}) {
+  for (auto fn : {k_xform_tma<0>, k_xform_tma<1>, k_xform_tma<2>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXformSmem);
     if (e != cudaSuccess) return e;
   }
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_tma_blocks_per_sm, k_xform_tma<0>,
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_tma_blocks_per_sm, k_xform_tma<2>,
                                                     kThreads, kXformSmem);
   if (e != cudaSuccess) return e;
   if (g_tma_blocks_per_sm < 1) g_tma_blocks_per_sm = 1;
@@ -268,8 +371,10 @@ cudaError_t launch_xform_tma(int mode, const uint8_t* src, uint8_t* dst, int64_t
   RepairList rl{count, items, cap};
   if (mode == 0)
     k_xform_tma<0><<<grid, kThreads, kXformSmem, st>>>(src, dst, npix, fp, sp, rl);
-  else
+  else if (mode == 1)
     k_xform_tma<1><<<grid, kThreads, kXformSmem, st>>>(src, dst, npix, fp, sp, rl);
+  else
+    k_xform_tma<2><<<grid, kThreads, kXformSmem, st>>>(src, dst, npix, fp, sp, rl);
   return launched();
 }
 
@@ -279,7 +384,7 @@ cudaError_t launch_xform_repair(uint8_t* dst, const StrictP& sp, unsigned long l
   cudaError_t e = xform_setup_device();
   if (e != cudaSuccess) return e;
   RepairList rl{count, items, cap};
-  k_xform_repair<<<g_sm_count * 2, 256, 0, st>>>(dst, sp, rl);
+  k_xform_repair<<<g_sm_count * 4, 256, 0, st>>>(dst, sp, rl);
   return launched();
 }
 
@@ -291,6 +396,14 @@ cudaError_t launch_xform_strict(const uint8_t* src, uint8_t* dst, int64_t npix,
   const int64_t want = (npix + 255) / 256;
   const int grid = static_cast<int>(min64(want, (int64_t)g_sm_count * 16));
   k_xform_strict<<<grid, 256, 0, st>>>(src, dst, npix, sp);
+  return launched();
+}
+
+cudaError_t launch_calibrate(const FastP& fp, const StrictP& sp, unsigned int* max_bits,
+                             cudaStream_t st) {
+  cudaError_t e = xform_setup_device();
+  if (e != cudaSuccess) return e;
+  k_calibrate<<<g_sm_count * 8, 256, 0, st>>>(fp, sp, max_bits);
   return launched();
 }
 

@@ -22,5 +22,7 @@ cudaError_t launch_beer_lambert(const uint8_t* px, double* od, int64_t n, const 
                                 cudaStream_t st);
 cudaError_t launch_inverse_bl(const double* od, uint8_t* out, int64_t n, const StrictP& sp,
                               cudaStream_t st);
+cudaError_t launch_calibrate(const FastP& fp, const StrictP& sp, unsigned int* max_bits,
+                             cudaStream_t st);
 int xform_tile_pixels();
 }  // namespace spcn

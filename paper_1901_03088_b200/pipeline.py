@@ -362,6 +362,7 @@ def transform(slide, source: FitParams, target: FitParams, sink, *,
     plan = XformPlan(source.i0, source.basis, code_lam, factors, target.basis, target.i0,
                      precision=precision)
     t0 = time.perf_counter()
+    plan.maybe_calibrate(width * slide.height)
 
     if isinstance(slide, DeviceSource):
         src = slide.tensor
