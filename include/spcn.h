@@ -228,6 +228,9 @@ const char* spcn_version(void);
 /* Number of kernels libspcn has launched in this process (diagnostics).     */
 uint64_t spcn_launch_count(void);
 
+/* Launch shape of the recolor kernel on the current device (diagnostics).   */
+const char* spcn_xform_shape(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -109,14 +109,14 @@ bool fill_fast(FastP& fp, const StrictP& sp, bool exact) {
   const double A = g11 / det, C = g01 / det, E = 1.0 / g11, F = g01 / g11, G = 1.0 / g00,
                H = g01 / g00;
   fp.A = (float)A; fp.nC = -(float)C; fp.E = (float)E;
-  fp.nF = -(float)F; fp.G = (float)G; fp.nH = -(float)H;
+  fp.nF2 = -(float)F * 0.5f; fp.G = (float)G; fp.nH2 = -(float)H * 0.5f;
   for (int c = 0; c < 3; ++c) fp.ilo[c] = fp.ihi[c] = 0.0f;
   const double log2e = 1.4426950408889634;
   double Kabs[3][2];
   for (int c = 0; c < 3; ++c)
     for (int j = 0; j < 2; ++j) {
       const double k = -log2e * sp.wt[c][j] * sp.f[j];
-      fp.K[c][j] = static_cast<float>(k);
+      fp.K2[c][j] = static_cast<float>(k) * 0.5f;
       Kabs[c][j] = std::fabs(k);
     }
   for (int c = 0; c < 3; ++c) fp.i0t[c] = static_cast<float>(sp.i0t[c]);
@@ -163,6 +163,8 @@ const char* spcn_last_error(void) { return g_err.c_str(); }
 const char* spcn_version(void) { return "spcn-b200 0.1.0 (sm_100a)"; }
 
 uint64_t spcn_launch_count(void) { return spcn::g_launches.load(std::memory_order_relaxed); }
+
+const char* spcn_xform_shape(void) { return spcn::xform_shape_name(); }
 
 size_t spcn_xform_workspace_bytes(int64_t npix) {
   const int64_t cap = 65536 + (npix > 0 ? npix / 32 : 0);

@@ -26,18 +26,54 @@
 #include "spcn_device.cuh"
 #include "xform.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace spcn {
 
-constexpr int kTilePx = 4096;                 // pixels per tile
-constexpr int kTileBytes = 3 * kTilePx;       // 12 KiB
-constexpr int kStages = 4;
-constexpr int kComputeWarps = 8;
-constexpr int kThreads = 32 * (kComputeWarps + 1);
-// OD table: 256 rows of 256 B; row x = [ch0 x16 | ch1 x16 | ch2 x16 | pad],
-// copy (lane & 15) of channel c at byte x*256 + c*64 + (lane&15)*4, so one
-// PRMT of (input word, lane constant) yields the address (bank conflicts <= 2).
-constexpr int kLutBytes = 256 * 256;
-constexpr size_t kXformSmem = kLutBytes + kStages * kTileBytes + 2 * kStages * sizeof(uint64_t);
+// Kernel shape: CW compute warps (+1 producer warp), 16 px per thread, and an
+// OD table replicated REP times so a warp's 32 lookups hit distinct banks:
+//   REP 16: 64 KiB, rows of 256 B = [ch0 x16 | ch1 x16 | ch2 x16 | pad], copy
+//           (lane&15) of channel c at x*256 + c*64 + (lane&15)*4 (<= 2-way
+//           bank conflicts), two CTAs per SM;
+//   REP 32: 128 KiB, region 0 rows [ch0 x32 | ch1 x32], region 1 (+64 KiB)
+//           rows [ch2 x32 | pad], copy `lane` at x*256 + ... + lane*4
+//           (conflict-free), one CTA per SM.
+// Either way ONE PRMT of (input word, per-lane constant) forms the address:
+// byte 0 = the constant's low byte, byte 1 = the pixel byte x, byte 2 = the
+// constant's region byte.
+// STORE 0: each thread stores its 48 output bytes with 3 STG.128.  STORE 1:
+// the output is written back in place into the input stage and each warp
+// issues one 1-D TMA bulk store (cp.async.bulk S2G) of its 1536-byte slice.
+// BLK = CTAs per SM the shared-memory budget is sized for.
+template <int CW, int REP, int STORE, int BLK>
+struct XCfg {
+  static constexpr int kComputeWarps = CW;
+  static constexpr int kThreads = 32 * (CW + 1);
+  static constexpr int kTilePx = CW * 32 * 16;
+  static constexpr int kTileBytes = 3 * kTilePx;
+  static constexpr int kLutBytes = REP == 32 ? 2 * 65536 : 65536;
+  static constexpr int kBudget = BLK == 1 ? 224 * 1024 : 112 * 1024;
+  static constexpr int kStages = (kBudget - kLutBytes) / kTileBytes;
+  static constexpr size_t kSmem = kLutBytes + kStages * kTileBytes + 2 * kStages * 8;
+  static_assert(kStages >= 3, "need at least three stages");
+};
+
+// the production shape (see DESIGN.md §3 and profiles/)
+#ifndef SPCN_XFORM_CW
+#define SPCN_XFORM_CW 16
+#endif
+#ifndef SPCN_XFORM_REP
+#define SPCN_XFORM_REP 32
+#endif
+#ifndef SPCN_XFORM_STORE
+#define SPCN_XFORM_STORE 1
+#endif
+#ifndef SPCN_XFORM_BLK
+#define SPCN_XFORM_BLK 1
+#endif
+using Prod = XCfg<SPCN_XFORM_CW, SPCN_XFORM_REP, SPCN_XFORM_STORE, SPCN_XFORM_BLK>;
+constexpr int kTilePx = Prod::kTilePx;
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -57,11 +93,8 @@ struct SmemLut {
 };
 
 // Rare path (repair-list overflow): kept out of line so the hot loop stays small.
-__device__ __noinline__ void repair_inline(const StrictP& sp, uint8_t* dst, int64_t gp, uint32_t rgb) {
-  const uint32_t out = strict_pixel(sp, ConstLut{&sp}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
-  dst[3 * gp] = out & 255u;
-  dst[3 * gp + 1] = (out >> 8) & 255u;
-  dst[3 * gp + 2] = (out >> 16) & 255u;
+__device__ __noinline__ uint32_t strict_rgb(const StrictP& sp, uint32_t rgb) {
+  return strict_pixel(sp, ConstLut{&sp}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
 }
 
 __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int idx) {
@@ -71,8 +104,8 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int idx) {
 // OD of input byte `idx` (0..47) of the thread's 48-byte block, channel c.
 __device__ __forceinline__ float od_lookup(const uint8_t* lut, const uint32_t* w, int idx,
                                            uint32_t lc) {
-  const uint32_t sel = 0x5504u | ((uint32_t)(idx & 3) << 4);
-  const uint32_t addr = __byte_perm(w[idx >> 2], lc, sel);  // x*256 + c*64 + (lane&15)*4
+  const uint32_t sel = 0x7604u | ((uint32_t)(idx & 3) << 4);
+  const uint32_t addr = __byte_perm(w[idx >> 2], lc, sel);  // region*64K + x*256 + low byte
   return *reinterpret_cast<const float*>(lut + addr);
 }
 
@@ -127,14 +160,17 @@ __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, ui
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int MODE, int CW, int REP, int STORE, int BLK>
+__global__ void __launch_bounds__(XCfg<CW, REP, STORE, BLK>::kThreads, BLK)
     k_xform_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
                 const __grid_constant__ FastP fp, const __grid_constant__ StrictP sp,
                 RepairList rl) {
+  using C = XCfg<CW, REP, STORE, BLK>;
+  constexpr int kThreads = C::kThreads, kTilePx = C::kTilePx, kTileBytes = C::kTileBytes;
+  constexpr int kStages = C::kStages, kComputeWarps = C::kComputeWarps;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint8_t* lut = smem;
-  uint8_t* stages = smem + kLutBytes;
+  uint8_t* stages = smem + C::kLutBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kTileBytes);
   uint64_t* empty = full + kStages;
 
@@ -142,9 +178,17 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (npix + kTilePx - 1) / kTilePx;
 
-  for (int i = tid; i < 256 * 48; i += kThreads) {
-    const int x = i / 48, rem = i - 48 * (i / 48), c = rem >> 4, r = rem & 15;
-    *reinterpret_cast<float*>(smem + x * 256 + c * 64 + r * 4) = fp.lut[c][x];
+  if (REP == 16) {
+    for (int i = tid; i < 256 * 48; i += kThreads) {
+      const int x = i / 48, rem = i - 48 * (i / 48), c = rem >> 4, r = rem & 15;
+      *reinterpret_cast<float*>(smem + x * 256 + c * 64 + r * 4) = fp.lut[c][x];
+    }
+  } else {
+    for (int i = tid; i < 256 * 96; i += kThreads) {
+      const int x = i / 96, rem = i - 96 * (i / 96), c = rem >> 5, r = rem & 31;
+      const int off = (c == 2 ? 65536 : 0) + x * 256 + (c == 1 ? 128 : 0) + r * 4;
+      *reinterpret_cast<float*>(smem + off) = fp.lut[c][x];
+    }
   }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -173,9 +217,15 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 
   // ---------------- compute warps
-  const int ct = tid;                        // 0..255
-  const uint32_t lrep = (uint32_t)(lane & 15) * 4;
-  const uint32_t lc[3] = {lrep, 64u + lrep, 128u + lrep};
+  const int ct = tid;                        // 0 .. 32*CW-1
+  uint32_t lc[3];
+  if (REP == 16) {
+    const uint32_t lrep = (uint32_t)(lane & 15) * 4;
+    lc[0] = lrep; lc[1] = 64u + lrep; lc[2] = 128u + lrep;
+  } else {
+    const uint32_t lrep = (uint32_t)lane * 4;
+    lc[0] = lrep; lc[1] = 128u + lrep; lc[2] = 0x10000u | lrep;
+  }
   int i = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
     const int s = i % kStages;
@@ -183,9 +233,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int64_t tile0 = t * kTilePx;
     const int64_t n = min64(kTilePx, npix - tile0);
     const bool valid = 16 * ct < n;
+    uint8_t* slot = stages + s * kTileBytes + 48 * ct;
     uint32_t w[12];
     if (valid) {
-      const uint4* q = reinterpret_cast<const uint4*>(stages + s * kTileBytes + 48 * ct);
+      const uint4* q = reinterpret_cast<const uint4*>(slot);
       const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
       w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
       w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
@@ -194,66 +245,99 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t ob[48], o[12];
     uint32_t badacc = 0;  // EXACT: 2-bit failure count per pixel
     if (valid) {
+      if (MODE == 3) {    // identity (memory-path ceiling measurement only)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        badacc |= recolor_pair<MODE>(fp, lut, w, 2 * q, lc, ob);
-        // pack output words as soon as their 4 bytes exist (short live ranges)
+        for (int j = 0; j < 12; ++j) o[j] = w[j];
+      } else {
 #pragma unroll
-        for (int j = 0; j < 12; ++j)
-          if (4 * j + 3 >= 6 * q && 4 * j + 3 < 6 * q + 6)
-            o[j] = pack4(ob[4 * j], ob[4 * j + 1], ob[4 * j + 2], ob[4 * j + 3]);
+        for (int q = 0; q < 8; ++q) {
+          badacc |= recolor_pair<MODE>(fp, lut, w, 2 * q, lc, ob);
+          // pack output words as soon as their 4 bytes exist (short live ranges)
+#pragma unroll
+          for (int j = 0; j < 12; ++j)
+            if (4 * j + 3 >= 6 * q && 4 * j + 3 < 6 * q + 6)
+              o[j] = pack4(ob[4 * j], ob[4 * j + 1], ob[4 * j + 2], ob[4 * j + 3]);
+        }
       }
     }
-    // Release the stage only after every loaded word has been consumed: the
-    // arrive does not wait for in-flight LDS, and the next TMA write into this
-    // stage is an async-proxy write (cross-proxy WAR), hence also the fence.
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (valid) {
-      uint4* d = reinterpret_cast<uint4*>(dst + 3 * (tile0 + 16 * ct));
+    if (STORE == 0) {
+      // Release the stage once every loaded word has been consumed: the arrive
+      // does not wait for in-flight LDS, and the next TMA write into this stage
+      // is an async-proxy write (cross-proxy WAR), hence also the fence.
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (valid) {
+        uint4* d = reinterpret_cast<uint4*>(dst + 3 * (tile0 + 16 * ct));
+        d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        d[2] = make_uint4(o[8], o[9], o[10], o[11]);
+      }
+    } else if (valid) {
+      // in-place staging: the output overwrites the thread's own input bytes
+      uint4* d = reinterpret_cast<uint4*>(slot);
       d[0] = make_uint4(o[0], o[1], o[2], o[3]);
       d[1] = make_uint4(o[4], o[5], o[6], o[7]);
       d[2] = make_uint4(o[8], o[9], o[10], o[11]);
     }
-    if (MODE != 1) {
+    if (MODE == 0 || MODE == 2) {
       // warp-aggregated append of uncertified pixels to the repair list
       uint32_t badmask = 0;
       if (badacc) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) badmask |= (((badacc >> (2 * k)) & 3u) ? 1u : 0u) << k;
       }
-      const unsigned active = __activemask();
-      if (__any_sync(active, badmask != 0u)) {
+      if (__any_sync(0xffffffffu, badmask != 0u)) {
         const uint32_t cnt = __popc(badmask);
         uint32_t incl = cnt;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t y = __shfl_up_sync(active, incl, off);
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
           if (lane >= off) incl += y;
         }
-        const int leader = 31 - __clz(active);
-        const uint32_t total = __shfl_sync(active, incl, leader);
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         unsigned long long base = 0;
-        if (lane == leader) base = atomicAdd(rl.count, (unsigned long long)total);
-        base = __shfl_sync(active, base, leader);
-        unsigned long long slot = base + incl - cnt;
+        if (lane == 31) base = atomicAdd(rl.count, (unsigned long long)total);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        unsigned long long item = base + incl - cnt;
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           if (!((badmask >> k) & 1u)) continue;
           const uint32_t rgb = byte_of(w, 3 * k) | (byte_of(w, 3 * k + 1) << 8) |
                                (byte_of(w, 3 * k + 2) << 16);
           const int64_t gp = tile0 + 16 * ct + k;
-          if (slot < rl.cap) {
-            rl.items[slot] = (static_cast<unsigned long long>(gp) << 24) | rgb;
-          } else {  // list overflow: repair inline (same thread, ordered after the STG)
-            repair_inline(sp, dst, gp, rgb);
+          if (item < rl.cap) {
+            rl.items[item] = (static_cast<unsigned long long>(gp) << 24) | rgb;
+          } else {  // list overflow: recompute in fp64 now (ordered after our own store)
+            const uint32_t px = strict_rgb(sp, rgb);
+            uint8_t* o8 = STORE == 0 ? dst + 3 * gp : slot + 3 * k;
+            o8[0] = px & 255u;
+            o8[1] = (px >> 8) & 255u;
+            o8[2] = (px >> 16) & 255u;
           }
-          ++slot;
+          ++item;
         }
       }
     }
+    if (STORE == 1) {
+      // one 1-D TMA bulk store per warp of its contiguous 1536-byte slice, issued
+      // from the stage itself; the stage is released once the PREVIOUS tile's
+      // store has finished reading shared memory (delayed release).
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int64_t wn = min64(512, n - (int64_t)warp * 512);
+        if (wn > 0) {
+          bulk_s2g(dst + 3 * (tile0 + (int64_t)warp * 512), stages + s * kTileBytes + warp * 1536,
+                   static_cast<uint32_t>(3 * wn));
+        }
+        bulk_commit();
+        bulk_wait_read<1>();
+        if (i > 0) mbar_arrive(&empty[(i - 1) % kStages]);
+      }
+    }
   }
+  if (STORE == 1 && lane == 0) bulk_wait_all();
 }
 
 __global__ void __launch_bounds__(256) k_xform_repair(uint8_t* __restrict__ dst,
@@ -340,23 +424,58 @@ __global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP
 
 // ------------------------------------------------------------------ launchers
 static int g_sm_count = 0;
-static int g_tma_blocks_per_sm = 0;
+
+using XformFn = void (*)(const uint8_t*, uint8_t*, int64_t, FastP, StrictP, RepairList);
+
+struct Shape {
+  int cw, rep, store, blk, threads, tile_px, blocks_per_sm;
+  size_t smem;
+  XformFn fn[4];
+};
+
+template <int CW, int REP, int STORE, int BLK>
+Shape make_shape() {
+  using C = XCfg<CW, REP, STORE, BLK>;
+  return Shape{CW, REP, STORE, BLK, C::kThreads, C::kTilePx, 0, C::kSmem,
+               {k_xform_tma<0, CW, REP, STORE, BLK>, k_xform_tma<1, CW, REP, STORE, BLK>,
+                k_xform_tma<2, CW, REP, STORE, BLK>, k_xform_tma<3, CW, REP, STORE, BLK>}};
+}
+
+// Compiled shapes; SPCN_XFORM_SHAPE="CWxREPxSTORExBLK" selects one
+// (experiments), the default is the production shape Prod.
+// SPCN_XFORM_IDENTITY=1 makes the kernel copy input to output (memory-path
+// ceiling measurement only).
+static Shape g_shapes[] = {
+    make_shape<SPCN_XFORM_CW, SPCN_XFORM_REP, SPCN_XFORM_STORE, SPCN_XFORM_BLK>(),
+    make_shape<8, 16, 0, 2>(), make_shape<16, 32, 0, 1>(), make_shape<16, 16, 1, 1>(),
+    make_shape<8, 16, 1, 2>(), make_shape<12, 32, 1, 1>(), make_shape<20, 16, 1, 1>()};
+static Shape* g_shape = nullptr;
+static bool g_identity = false;
 
 cudaError_t xform_setup_device() {
-  if (g_sm_count) return cudaSuccess;
+  if (g_shape) return cudaSuccess;
   int dev;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  for (auto fn : {k_xform_tma<0>, k_xform_tma<1>, k_xform_tma<2>}) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXformSmem);
+  Shape* pick = &g_shapes[0];
+  if (const char* env = getenv("SPCN_XFORM_SHAPE")) {
+    int cw = 0, rep = 0, store = 0, blk = 0;
+    if (sscanf(env, "%dx%dx%dx%d", &cw, &rep, &store, &blk) == 4)
+      for (auto& s : g_shapes)
+        if (s.cw == cw && s.rep == rep && s.store == store && s.blk == blk) pick = &s;
+  }
+  if (const char* env = getenv("SPCN_XFORM_IDENTITY")) g_identity = env[0] == '1';
+  for (auto fn : pick->fn) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pick->smem);
     if (e != cudaSuccess) return e;
   }
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_tma_blocks_per_sm, k_xform_tma<2>,
-                                                    kThreads, kXformSmem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pick->blocks_per_sm, pick->fn[2],
+                                                    pick->threads, pick->smem);
   if (e != cudaSuccess) return e;
-  if (g_tma_blocks_per_sm < 1) g_tma_blocks_per_sm = 1;
+  if (pick->blocks_per_sm < 1) pick->blocks_per_sm = 1;
+  g_shape = pick;
   return cudaSuccess;
 }
 
@@ -366,16 +485,21 @@ cudaError_t launch_xform_tma(int mode, const uint8_t* src, uint8_t* dst, int64_t
                              cudaStream_t st) {
   cudaError_t e = xform_setup_device();
   if (e != cudaSuccess) return e;
-  const int64_t ntiles = (npix + kTilePx - 1) / kTilePx;
-  const int grid = static_cast<int>(min64(ntiles, (int64_t)g_sm_count * g_tma_blocks_per_sm));
+  const Shape& s = *g_shape;
+  const int64_t ntiles = (npix + s.tile_px - 1) / s.tile_px;
+  const int grid = static_cast<int>(min64(ntiles, (int64_t)g_sm_count * s.blocks_per_sm));
   RepairList rl{count, items, cap};
-  if (mode == 0)
-    k_xform_tma<0><<<grid, kThreads, kXformSmem, st>>>(src, dst, npix, fp, sp, rl);
-  else if (mode == 1)
-    k_xform_tma<1><<<grid, kThreads, kXformSmem, st>>>(src, dst, npix, fp, sp, rl);
-  else
-    k_xform_tma<2><<<grid, kThreads, kXformSmem, st>>>(src, dst, npix, fp, sp, rl);
+  s.fn[g_identity ? 3 : mode]<<<grid, s.threads, s.smem, st>>>(src, dst, npix, fp, sp, rl);
   return launched();
+}
+
+const char* xform_shape_name() {
+  static char buf[96];
+  if (xform_setup_device() != cudaSuccess || !g_shape) return "unavailable";
+  snprintf(buf, sizeof(buf), "%d compute warps, LUT x%d, %s stores, %d CTA/SM, %d px/tile",
+           g_shape->cw, g_shape->rep, g_shape->store ? "TMA" : "STG.128",
+           g_shape->blocks_per_sm, g_shape->tile_px);
+  return buf;
 }
 
 cudaError_t launch_xform_repair(uint8_t* dst, const StrictP& sp, unsigned long long* count,
@@ -407,6 +531,6 @@ cudaError_t launch_calibrate(const FastP& fp, const StrictP& sp, unsigned int* m
   return launched();
 }
 
-int xform_tile_pixels() { return kTilePx; }
+int xform_tile_pixels() { return g_shape ? g_shape->tile_px : kTilePx; }
 
 }  // namespace spcn

@@ -25,4 +25,5 @@ cudaError_t launch_inverse_bl(const double* od, uint8_t* out, int64_t n, const S
 cudaError_t launch_calibrate(const FastP& fp, const StrictP& sp, unsigned int* max_bits,
                              cudaStream_t st);
 int xform_tile_pixels();
+const char* xform_shape_name();
 }  // namespace spcn
