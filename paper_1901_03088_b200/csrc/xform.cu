@@ -97,6 +97,14 @@ __device__ __noinline__ uint32_t strict_rgb(const StrictP& sp, uint32_t rgb) {
   return strict_pixel(sp, ConstLut{&sp}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
 }
 
+// (a ^ b) | c as a single LOP3 (opaque to the optimiser, which would otherwise
+// turn the XOR into compare-and-select chains).
+__device__ __forceinline__ uint32_t lop3_xor_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xBE;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int idx) {
   return (w[idx >> 2] >> (8 * (idx & 3))) & 0xffu;
 }
@@ -110,9 +118,9 @@ __device__ __forceinline__ float od_lookup(const uint8_t* lut, const uint32_t* w
 }
 
 // Recolor two pixels (k, k+1) of the block; writes their 6 output "bytes"
-// (low byte of each word) to ob[3k .. 3k+5].  EXACT: returns, in 2-bit fields
-// 2k and 2k+2, how many channels of each pixel failed certification
-// (r_hi - r_lo is 0 or 1 per channel since the interval is narrower than 1).
+// (low byte of each word) to ob[3k .. 3k+5].  EXACT: returns non-zero when any
+// of the pair's six roundings is not certified (r_lo != r_hi); both pixels of
+// such a pair go to the fp64 repair list.
 template <int MODE>
 __device__ __forceinline__ uint32_t recolor_pair(const FastP& fp, const uint8_t* lut,
                                                  const uint32_t* w, int k, const uint32_t* lc,
@@ -135,7 +143,7 @@ __device__ __forceinline__ uint32_t recolor_pair(const FastP& fp, const uint8_t*
   }
   float2 alpha = bc2(0.f);
   if (MODE == 0) alpha = __ffma2_rn(bc2(fp.a1), fq.T, bc2(fp.a0));
-  uint32_t da = 0, db = 0;
+  uint32_t bad = 0;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const float pa = ex2_approx(e[c][0]), pb = ex2_approx(e[c][1]);
@@ -150,10 +158,10 @@ __device__ __forceinline__ uint32_t recolor_pair(const FastP& fp, const uint8_t*
     const float2 rb = __ffma2_rn(Ib, bc2(pb), bc2(kMagic));
     ob[a + c] = __float_as_uint(ra.y);
     ob[b + c] = __float_as_uint(rb.y);
-    da += __float_as_uint(ra.y) - __float_as_uint(ra.x);
-    db += __float_as_uint(rb.y) - __float_as_uint(rb.x);
+    bad = lop3_xor_or(__float_as_uint(ra.y), __float_as_uint(ra.x), bad);   // one LOP3 each
+    bad = lop3_xor_or(__float_as_uint(rb.y), __float_as_uint(rb.x), bad);
   }
-  return (da << (2 * k)) | (db << (2 * k + 2));
+  return bad;
 }
 
 __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -243,7 +251,7 @@ __global__ void __launch_bounds__(XCfg<CW, REP, STORE, BLK>::kThreads, BLK)
       w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
     }
     uint32_t ob[48], o[12];
-    uint32_t badacc = 0;  // EXACT: 2-bit failure count per pixel
+    uint32_t badpairs = 0;  // EXACT: bit q = pair q (pixels 2q, 2q+1) not certified
     if (valid) {
       if (MODE == 3) {    // identity (memory-path ceiling measurement only)
 #pragma unroll
@@ -251,7 +259,8 @@ __global__ void __launch_bounds__(XCfg<CW, REP, STORE, BLK>::kThreads, BLK)
       } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          badacc |= recolor_pair<MODE>(fp, lut, w, 2 * q, lc, ob);
+          const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * q, lc, ob);
+          if (MODE == 0 || MODE == 2) badpairs |= (bad != 0u ? 1u : 0u) << q;
           // pack output words as soon as their 4 bytes exist (short live ranges)
 #pragma unroll
           for (int j = 0; j < 12; ++j)
@@ -282,10 +291,10 @@ __global__ void __launch_bounds__(XCfg<CW, REP, STORE, BLK>::kThreads, BLK)
     }
     if (MODE == 0 || MODE == 2) {
       // warp-aggregated append of uncertified pixels to the repair list
-      uint32_t badmask = 0;
-      if (badacc) {
+      uint32_t badmask = 0;   // bit k = pixel k
+      if (badpairs) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) badmask |= (((badacc >> (2 * k)) & 3u) ? 1u : 0u) << k;
+        for (int q = 0; q < 8; ++q) badmask |= ((badpairs >> q) & 1u) * (3u << (2 * q));
       }
       if (__any_sync(0xffffffffu, badmask != 0u)) {
         const uint32_t cnt = __popc(badmask);
@@ -338,6 +347,161 @@ __global__ void __launch_bounds__(XCfg<CW, REP, STORE, BLK>::kThreads, BLK)
     }
   }
   if (STORE == 1 && lane == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
+// k_xform_warp: the same per-thread pipeline, but every warp owns its own
+// ring of NSW 1536-byte slots (512 px each) and is its own producer: lane 0
+// issues the 1-D TMA bulk load of the warp's next slices, the warp recolours a
+// slice in place in shared memory, and lane 0 issues the TMA bulk store from
+// the same slot; the slot is refilled as soon as that store has finished
+// reading it.  No CTA-wide stage coupling: a slow warp never holds back the
+// others' refills.  Work: 512-px slices, grid-strided over all warps.
+template <int CW, int REP, int NSW, int BLK>
+struct WCfg {
+  static constexpr int kThreads = 32 * CW;
+  static constexpr int kLutBytes = REP == 32 ? 2 * 65536 : 65536;
+  static constexpr size_t kSmem = kLutBytes + (size_t)CW * NSW * 1536 + CW * NSW * 8;
+  static_assert(kSmem <= (BLK == 1 ? 227 * 1024 : 113 * 1024), "shared memory budget");
+};
+
+template <int MODE, int CW, int REP, int NSW, int BLK>
+__global__ void __launch_bounds__(32 * CW, BLK)
+    k_xform_warp(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
+                 const __grid_constant__ FastP fp, const __grid_constant__ StrictP sp,
+                 RepairList rl) {
+  using C = WCfg<CW, REP, NSW, BLK>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint8_t* lut = smem;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint8_t* myslots = smem + C::kLutBytes + (size_t)warp * NSW * 1536;
+  uint64_t* mybar = reinterpret_cast<uint64_t*>(smem + C::kLutBytes + (size_t)CW * NSW * 1536) +
+                    warp * NSW;
+
+  if (REP == 16) {
+    for (int i = tid; i < 256 * 48; i += C::kThreads) {
+      const int x = i / 48, rem = i - 48 * (i / 48), c = rem >> 4, r = rem & 15;
+      *reinterpret_cast<float*>(smem + x * 256 + c * 64 + r * 4) = fp.lut[c][x];
+    }
+  } else {
+    for (int i = tid; i < 256 * 96; i += C::kThreads) {
+      const int x = i / 96, rem = i - 96 * (i / 96), c = rem >> 5, r = rem & 31;
+      const int off = (c == 2 ? 65536 : 0) + x * 256 + (c == 1 ? 128 : 0) + r * 4;
+      *reinterpret_cast<float*>(smem + off) = fp.lut[c][x];
+    }
+  }
+  if (lane == 0) {
+    for (int s = 0; s < NSW; ++s) mbar_init(&mybar[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  uint32_t lc[3];
+  if (REP == 16) {
+    const uint32_t lrep = (uint32_t)(lane & 15) * 4;
+    lc[0] = lrep; lc[1] = 64u + lrep; lc[2] = 128u + lrep;
+  } else {
+    const uint32_t lrep = (uint32_t)lane * 4;
+    lc[0] = lrep; lc[1] = 128u + lrep; lc[2] = 0x10000u | lrep;
+  }
+  const int64_t nslices = (npix + 511) / 512;
+  const int64_t gw = (int64_t)blockIdx.x * CW + warp, GW = (int64_t)gridDim.x * CW;
+  uint64_t pol = 0;
+  auto issue_load = [&](int64_t k) {   // lane 0 only
+    const int64_t j = gw + k * GW;
+    if (j >= nslices) return;
+    const int s = (int)(k % NSW);
+    const uint32_t bytes = static_cast<uint32_t>(3 * min64(512, npix - j * 512));
+    mbar_expect_tx(&mybar[s], bytes);
+    bulk_g2s(myslots + s * 1536, src + 3 * j * 512, bytes, &mybar[s], pol);
+  };
+  if (lane == 0) {
+    pol = policy_evict_first();
+    for (int k = 0; k < NSW; ++k) issue_load(k);
+  }
+
+  for (int64_t k = 0;; ++k) {
+    const int64_t j = gw + k * GW;
+    if (j >= nslices) break;
+    const int s = (int)(k % NSW);
+    mbar_wait(&mybar[s], (uint32_t)((k / NSW) & 1));
+    const int64_t n = min64(512, npix - j * 512);
+    const bool valid = 16 * lane < n;
+    uint8_t* slot = myslots + s * 1536 + 48 * lane;
+    uint32_t w[12], ob[48], o[12];
+    uint32_t badpairs = 0;
+    if (valid) {
+      const uint4* q = reinterpret_cast<const uint4*>(slot);
+      const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
+      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+      w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+      w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
+      if (MODE == 3) {
+#pragma unroll
+        for (int t = 0; t < 12; ++t) o[t] = w[t];
+      } else {
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+          const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * qq, lc, ob);
+          if (MODE == 0 || MODE == 2) badpairs |= (bad != 0u ? 1u : 0u) << qq;
+#pragma unroll
+          for (int t = 0; t < 12; ++t)
+            if (4 * t + 3 >= 6 * qq && 4 * t + 3 < 6 * qq + 6)
+              o[t] = pack4(ob[4 * t], ob[4 * t + 1], ob[4 * t + 2], ob[4 * t + 3]);
+        }
+      }
+      uint4* d = reinterpret_cast<uint4*>(slot);
+      d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+      d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+      d[2] = make_uint4(o[8], o[9], o[10], o[11]);
+    }
+    if (MODE == 0 || MODE == 2) {
+      if (__any_sync(0xffffffffu, badpairs != 0u)) {
+        uint32_t badmask = 0;
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) badmask |= ((badpairs >> qq) & 1u) * (3u << (2 * qq));
+        const uint32_t cnt = __popc(badmask);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(rl.count, (unsigned long long)total);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        unsigned long long item = base + incl - cnt;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          if (!((badmask >> kk) & 1u)) continue;
+          const uint32_t rgb = byte_of(w, 3 * kk) | (byte_of(w, 3 * kk + 1) << 8) |
+                               (byte_of(w, 3 * kk + 2) << 16);
+          const int64_t gp = j * 512 + 16 * lane + kk;
+          if (item < rl.cap) {
+            rl.items[item] = (static_cast<unsigned long long>(gp) << 24) | rgb;
+          } else {  // list overflow: fp64 recompute patched into the slot before the store
+            const uint32_t px = strict_rgb(sp, rgb);
+            slot[3 * kk] = px & 255u;
+            slot[3 * kk + 1] = (px >> 8) & 255u;
+            slot[3 * kk + 2] = (px >> 16) & 255u;
+          }
+          ++item;
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      bulk_s2g(dst + 3 * j * 512, myslots + s * 1536, static_cast<uint32_t>(3 * n));
+      bulk_commit();
+      if (k >= 1) {
+        bulk_wait_read<1>();          // the store of item k-1 has read its slot
+        issue_load(k - 1 + NSW);      // refill that slot
+      }
+    }
+  }
+  if (lane == 0) bulk_wait_all();
 }
 
 __global__ void __launch_bounds__(256) k_xform_repair(uint8_t* __restrict__ dst,
@@ -428,10 +592,18 @@ static int g_sm_count = 0;
 using XformFn = void (*)(const uint8_t*, uint8_t*, int64_t, FastP, StrictP, RepairList);
 
 struct Shape {
-  int cw, rep, store, blk, threads, tile_px, blocks_per_sm;
+  int cw, rep, store, blk, threads, tile_px, blocks_per_sm;   // store 2 = per-warp rings
   size_t smem;
   XformFn fn[4];
 };
+
+template <int CW, int REP, int NSW, int BLK>
+Shape make_wshape() {
+  using C = WCfg<CW, REP, NSW, BLK>;
+  return Shape{CW, REP, 2, BLK, C::kThreads, CW * 512, 0, C::kSmem,
+               {k_xform_warp<0, CW, REP, NSW, BLK>, k_xform_warp<1, CW, REP, NSW, BLK>,
+                k_xform_warp<2, CW, REP, NSW, BLK>, k_xform_warp<3, CW, REP, NSW, BLK>}};
+}
 
 template <int CW, int REP, int STORE, int BLK>
 Shape make_shape() {
@@ -446,9 +618,9 @@ Shape make_shape() {
 // SPCN_XFORM_IDENTITY=1 makes the kernel copy input to output (memory-path
 // ceiling measurement only).
 static Shape g_shapes[] = {
-    make_shape<SPCN_XFORM_CW, SPCN_XFORM_REP, SPCN_XFORM_STORE, SPCN_XFORM_BLK>(),
-    make_shape<8, 16, 0, 2>(), make_shape<16, 32, 0, 1>(), make_shape<16, 16, 1, 1>(),
-    make_shape<8, 16, 1, 2>(), make_shape<12, 32, 1, 1>(), make_shape<20, 16, 1, 1>()};
+    make_wshape<16, 32, 4, 1>(),   // production: per-warp rings, conflict-free table
+    make_shape<16, 32, 1, 1>(), make_shape<8, 16, 0, 2>(), make_shape<16, 32, 0, 1>(),
+    make_wshape<16, 16, 6, 1>(), make_wshape<8, 16, 4, 2>(), make_wshape<20, 16, 5, 1>()};
 static Shape* g_shape = nullptr;
 static bool g_identity = false;
 
