@@ -56,6 +56,11 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the CPU-baseline band")
+    ap.add_argument("--workload", choices=("wsi", "batch"), default="wsi",
+                    help="wsi = configs[3] (default); batch = configs[1] (4096 x 512^2 patches)")
+    ap.add_argument("--batch", type=int, default=4096)
+    ap.add_argument("--patch", type=int, default=512)
+    ap.add_argument("--cpu-patches", type=int, default=8, help="patches in the CPU-baseline sample")
     return ap.parse_args()
 
 
@@ -196,6 +201,177 @@ def workload_config(args, world):
             "l2": "input+output 60 GB per step >> 126 MB L2 (no flush needed)"}
 
 
+# --------------------------------------------------------------------------- batch (configs[1])
+def batch_config(args, world):
+    return {"workload": f"C2: batch of {args.batch} synthetic {args.patch}x{args.patch} H&E "
+                        "patches (8 groups of tissue fraction / background), each fitted and "
+                        "normalized against one fixed target profile; step = "
+                        "normalize_batch(all patches)",
+            "batch": args.batch, "patch": args.patch, "precision": args.precision,
+            "parallelism": f"independent batches x{world}",
+            "l2": f"input+output {2 * 3 * args.batch * args.patch ** 2 / 1e9:.1f} GB per step "
+                  ">> 126 MB L2 (no flush needed)"}
+
+
+def _batch_images(args, seed, n, dev):
+    import torch
+
+    from paper_1901_03088_b200 import synthetic
+
+    P = args.patch
+    imgs = torch.empty((n, P, P, 3), dtype=torch.uint8, device=dev)
+    groups = 8
+    per = -(-n // groups)
+    for g in range(groups):
+        a, b = g * per, min(n, (g + 1) * per)
+        if a >= b:
+            break
+        i0 = (255 - 3 * g, 252 - 2 * g, 255 - g)
+        synthetic.render_rows(imgs[a:b].view(-1), P, (b - a) * P, 0, (b - a) * P, seed + 97 * g,
+                              i0=i0, tissue_fraction=0.3 + 0.08 * g, dense=bool(g & 1))
+    return imgs
+
+
+def run_batch(args, rank, world, local):
+    import torch
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200 import _lib, synthetic
+
+    dev = torch.device("cuda", local if world > 1 else 0)
+    n, P = args.batch, args.patch
+    imgs = _batch_images(args, args.seed + 1000 * rank, n, dev)
+    out = torch.empty_like(imgs)
+    tgt = synthetic.render_slide(2048, 2048, args.seed + 1, tissue_fraction=0.6)
+    target = pb.fit(pb.DeviceSource(tgt))
+    del tgt
+    xform_ms = []
+
+    def step(record=False):
+        fits = pb.fit_batch(imgs)
+        if record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        _, errors = pb.transform_batch(imgs, fits, target, out, precision=args.precision)
+        if record:
+            e1.record()
+            xform_ms.append((e0, e1))
+        return errors
+
+    for _ in range(args.warmup):
+        errors = step()
+    failed = sum(e is not None for e in errors)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = Clocks(dev.index if dev.index is not None else 0)
+    clocks.start()
+    time.sleep(0.05)
+    L = _lib.lib()
+    launches0 = L.spcn_launch_count()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step(record=True)
+    t1.record()
+    torch.cuda.synchronize()
+    launches = L.spcn_launch_count() - launches0
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    npx = n * P * P
+    value = npx * world / (ms * 1e-3) / 1e6
+    x_ms = statistics.mean(a.elapsed_time(b) for a, b in xform_ms)
+    achieved = BYTES_PER_PX * npx / (x_ms * 1e-3) / 1e9
+    peak, peak_src = _hbm_peak()
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpx/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (on-GPU generator, model of src/synthetic.py)",
+            "config": batch_config(args, world),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "spcn_xform_batch (k_xform_batch + k_repair_batch)",
+                         "kernel_ms": round(x_ms, 4), "share_of_step": round(x_ms / ms, 4),
+                         "algorithmic_bytes_per_px": BYTES_PER_PX, "peak_source": peak_src},
+            "gpu_launches": int(launches), "clocks": clk, "failed_items": failed}
+    if not args.no_e2e:
+        h_in = torch.empty(imgs.shape, dtype=torch.uint8, pin_memory=True)
+        h_in.copy_(imgs)
+        h_out = torch.empty_like(h_in).pin_memory()
+        times = []
+        for i in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t_a = time.perf_counter()
+            d_in = h_in.to(dev, non_blocking=True)
+            fits = pb.fit_batch(d_in)
+            o, _ = pb.transform_batch(d_in, fits, target, precision=args.precision)
+            h_out.copy_(o, non_blocking=True)
+            torch.cuda.synchronize()
+            if i:
+                times.append(time.perf_counter() - t_a)
+            del d_in, o
+        sec = min(times)
+        line["e2e"] = {"value": round(npx * world / sec / 1e6, 3), "unit": "Mpx/s",
+                       "h2d_bytes_per_step": 3 * npx, "d2h_bytes_per_step": 3 * npx,
+                       "seconds_per_step": round(sec, 4),
+                       "path": "pinned host batch -> H2D -> pb.fit_batch + pb.transform_batch "
+                               "-> D2H into pinned host"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_batch_baseline(args, imgs, target)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def _cpu_patch_run(px, target):
+    from oracle import spcn_oracle as orc
+
+    fp = orc.fit_params(px)
+    return orc.run_transform(px, fp, target, strip_height=1024, workers=1)
+
+
+def cpu_batch_baseline(args, imgs, target, cores=None):
+    """Oracle port on a bounded number of patches, one patch per host core
+    (the reference's cmd_batch runs patches one after another; src/cli.py:270-301)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cores = cores or (os.cpu_count() or 1)
+    k = max(1, min(args.cpu_patches, imgs.shape[0]))
+    stride = max(1, imgs.shape[0] // k)
+    sample = [imgs[i * stride].cpu().numpy() for i in range(k)]
+    tgt = dict(i0=np.asarray(target.i0), basis=np.asarray(target.basis),
+               p99=np.asarray(target.stats.p99))
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=min(cores, k)) as pool:
+        list(pool.map(lambda p: _cpu_patch_run(p, tgt), sample))
+    sec = time.perf_counter() - t0
+    v = k * args.patch ** 2 / sec / 1e6
+    return {"value": round(v, 3), "unit": "Mpx/s", "cores": min(cores, k), "kind": "port",
+            "sample": f"{k} of the {imgs.shape[0]} patches (every {stride}th), fit + transform "
+                      f"each with the oracle port, {min(cores, k)} patches in parallel; "
+                      f"{sec:.2f} s"}
+
+
+def _hbm_peak():
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        peaks = {}
+    if "hbm_gbs" in peaks:
+        return float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
 # --------------------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local):
     import torch
@@ -290,7 +466,7 @@ def run_ours(args, rank, world, local):
             "config": workload_config(args, world),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "kernel": "spcn_xform_rgb8 (k_xform_tma + repair)",
+                         "traffic": traffic, "kernel": "spcn_xform_rgb8 (k_xform_warp + k_xform_repair)",
                          "kernel_ms": round(x_ms, 4), "share_of_step": round(x_ms / ms, 4),
                          "algorithmic_bytes_per_px": BYTES_PER_PX,
                          "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
@@ -384,6 +560,8 @@ def main():
         int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0)
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.workload == "batch":
+        return run_batch(args, rank, world, local)
     return run_ours(args, rank, world, local)
 
 

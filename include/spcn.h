@@ -201,6 +201,38 @@ int spcn_percentile_segments(const double* h, int64_t total, const int64_t* seg_
 int spcn_select_kth(const double* values, const int64_t* begin, const int64_t* end,
                     const int64_t* k, int32_t nq, void* qbuf, double* out, void* stream);
 
+/* ---- batched recolouring (many items, own source params, one target) --- */
+/* One batch = N independent `_normalize_one` (src/cli.py:220-244) transforms:
+ * item i's pixels are [off[i], off[i+1]) of the concatenated src/dst.       */
+typedef struct spcn_batch_target {
+  double i0[3];
+  double basis[6];          /* row-major 3x2 */
+  double p99[2];
+} spcn_batch_target;
+
+/* Byte sizes of the opaque per-item blocks spcn_batch_params writes.        */
+int spcn_batch_sizes(size_t* fast_scalar_bytes, size_t* strict_param_bytes);
+
+/* Build per-item parameter blocks ON THE DEVICE from batched fit results
+ * (i0 nx3, luts nx3x256 fp64, bases nx6, p99 nx2; all device): factors
+ * tgt_p99/src_p99 with the reference's degeneracy checks
+ * (src/normalize.py:103-112, src/pipeline.py:291-297).  status (device, in:
+ * 0 = fit ok / <0 = fit error code; out: 0 = fast path, 1 = strict path
+ * only, -SPCN_EDEGENERATE = degenerate stain).                              */
+int spcn_batch_params(int32_t nitems, const double* i0, const double* luts, const double* bases,
+                      const double* p99, const spcn_batch_target* tgt, double code_lam,
+                      int32_t max_sweeps, int32_t precision, void* fast_scalars, float* flut,
+                      void* strict_params, int32_t* status, void* stream);
+
+/* Recolour every item (status 0 via the fast kernel, status 1 via the fp64
+ * kernel, errors skipped).  off_host/off_dev: n+1 pixel offsets (multiples of
+ * 16); fast_scalars_host/status_host: host copies of the blocks above.       */
+int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int64_t* off_host,
+                     const int64_t* off_dev, const void* fast_scalars_host,
+                     const int32_t* status_host, const int32_t* status_dev, const float* flut,
+                     const void* strict_params, int32_t precision, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
 /* ---- measurement input: synthetic H&E slides --------------------------- */
 typedef struct spcn_synth_params {
   float i0[3];             /* background intensity per channel              */

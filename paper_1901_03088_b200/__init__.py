@@ -24,5 +24,6 @@ from .pipeline import (  # noqa: F401
     BufferGauge, PixelSample, RunStats, SamplePlan, fit, normalize, sample_pixels, transform,
 )
 from .xform import XformPlan, process_strip  # noqa: F401
+from .batch import BatchFit, fit_batch, normalize_batch, transform_batch  # noqa: F401
 
 __version__ = "0.1.0"

@@ -1,0 +1,258 @@
+"""Batched normalisation: many images, each with its own fit, one target.
+
+BASELINE configs[1] ("batch of 4096 synthetic 512x512 patches against one
+fixed target basis").  Per item this is exactly the reference's
+``_normalize_one`` (src/cli.py:220-244): fit(item) then transform(item)
+against the target; failures are collected per item and do not stop the
+batch, like ``cmd_batch`` (src/cli.py:270-301).  All items go through each
+stage together: one sampling launch, one i0 launch, one SNMF launch (a CTA
+per item), one coding launch, one p99 select launch, a device-side parameter
+build and ~n/148 recolour launches.
+"""
+from __future__ import annotations
+
+import ctypes
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev, _lib, optics, snmf
+from .errors import (BlankSlideError, DegenerateStainError, InsufficientPixelsError,
+                     StainAbsentError)
+from .normalize import FitParams, StainStats, config_hash
+from .pipeline import PATCH_DT, TAKE_DT, SamplePlan, _cfg_fields, _lib_sample, _visit
+from .stain_sep import SnmfConfig
+from .xform import XformPlan
+
+CHUNK = 4096
+_ERR = {-_lib.SPCN_EBLANK: BlankSlideError, -_lib.SPCN_EINSUFFICIENT: InsufficientPixelsError,
+        -_lib.SPCN_ESTAIN_ABSENT: StainAbsentError, -_lib.SPCN_EDEGENERATE: DegenerateStainError}
+_MSG = {-_lib.SPCN_EBLANK: "sampling: blank slide: no non-white pixels found in any sampled patch",
+        -_lib.SPCN_EINSUFFICIENT: "basis fit: insufficient pixels: need at least 10 OD samples",
+        -_lib.SPCN_ESTAIN_ABSENT: "density stats: stain absent",
+        -_lib.SPCN_EDEGENERATE: "degenerate stain density: p99 is zero for a stain"}
+
+
+class BatchTargetC(ctypes.Structure):
+    _fields_ = [("i0", ctypes.c_double * 3), ("basis", ctypes.c_double * 6),
+                ("p99", ctypes.c_double * 2)]
+
+
+def _sig():
+    L = _lib.lib()
+    if not getattr(L, "_spcn_batch_declared", False):
+        P, I32, DBL = _lib.P, _lib.I32, _lib.DBL
+        _lib.declare("spcn_batch_sizes", ctypes.c_int,
+                     [ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)])
+        _lib.declare("spcn_batch_params", ctypes.c_int,
+                     [I32, P, P, P, P, ctypes.POINTER(BatchTargetC), DBL, I32, I32, P, P, P, P, P])
+        _lib.declare("spcn_xform_batch", ctypes.c_int,
+                     [P, P, I32, P, P, P, P, P, P, P, I32, P, _lib.SZ, P])
+        L._spcn_batch_declared = True
+    return L
+
+
+@dataclass
+class BatchFit:
+    """Per-item fit results (device tensors) + host status."""
+
+    i0: object          # (n, 3) float64 CUDA
+    basis: object       # (n, 3, 2) float64 CUDA (ordered)
+    p99: object         # (n, 2) float64 CUDA
+    luts: object        # (n, 3, 256) float64 CUDA (exact reference OD tables)
+    count: np.ndarray   # (n,) sampled pixels
+    status: np.ndarray  # (n,) 0 = ok, <0 = -SPCN_E* error code
+    provenance: dict
+
+    def error(self, i):
+        st = int(self.status[i])
+        if st >= 0:
+            return None
+        return _ERR[st](_MSG[st])
+
+    def params(self, i) -> FitParams:
+        """FitParams of item i (raises the item's error, like fit() would)."""
+        err = self.error(i)
+        if err is not None:
+            raise err
+        return FitParams(i0=self.i0[i].cpu().numpy(), basis=self.basis[i].cpu().numpy(),
+                         stats=StainStats(p99=self.p99[i].cpu().numpy(),
+                                          sample_count=int(self.count[i])),
+                         provenance=dict(self.provenance))
+
+
+def _od_tables_exact(i0: np.ndarray) -> np.ndarray:
+    """(n,3,256) OD tables with the reference's numpy expression, computed once
+    per distinct (channel, i0) value (i0 are order statistics of u8 pools)."""
+    n = i0.shape[0]
+    out = np.empty((n, 3, 256))
+    ramp = np.arange(256, dtype=np.float64)
+    for c in range(3):
+        vals, inv = np.unique(i0[:, c], return_inverse=True)
+        rows = np.empty((vals.size, 256))
+        for k, v in enumerate(vals):
+            x = np.clip(ramp, 1.0, v)
+            rows[k] = np.log(v / x)
+        out[:, c, :] = rows[inv]
+    return out
+
+
+def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), *,
+              code_lam: float = 0.0) -> BatchFit:
+    """fit() of every image of a (n, H, W, 3) uint8 CUDA tensor, all on the device."""
+    t = _dev.torch()
+    L = _lib_sample()
+    if images.ndim != 4 or images.shape[3] != 3 or str(images.dtype) != "torch.uint8":
+        raise ValueError("images must be an (n, H, W, 3) uint8 tensor")
+    imgs = images.contiguous() if images.is_cuda else images.cuda().contiguous()
+    n, H, W = int(imgs.shape[0]), int(imgs.shape[1]), int(imgs.shape[2])
+    dev = imgs.device
+    # identical seeded visit order for every item (same grid, same seed)
+    origins = [(x, y) for y in range(0, H, plan.patch_size) for x in range(0, W, plan.patch_size)]
+    order = np.random.default_rng(plan.seed).permutation(len(origins))
+    ncand = min(len(order), 10 * plan.max_patches)
+    rects = [(origins[i][0], origins[i][1], min(plan.patch_size, W - origins[i][0]),
+              min(plan.patch_size, H - origins[i][1])) for i in order[:ncand]]
+    desc = np.zeros((n, ncand), dtype=PATCH_DT)
+    for k, (x, y, w, h) in enumerate(rects):
+        desc["base"][:, k] = np.arange(n, dtype=np.int64) * (H * W) + y * W + x
+        desc["width"][:, k] = w
+        desc["height"][:, k] = h
+        desc["row_stride"][:, k] = W
+    desc = desc.ravel()
+    chunks = max(1, -(-max(w * h for (_, _, w, h) in rects) // CHUNK))
+    d_desc = t.from_numpy(desc.view(np.uint8).copy()).to(dev)
+    counts = t.empty((n * ncand, chunks, 4), dtype=t.int32, device=dev)
+    thr = int(plan.white_threshold)
+    _lib.check(L.spcn_sample_count(_lib.ptr(imgs), _lib.ptr(d_desc), n * ncand, chunks, thr,
+                                   _lib.ptr(counts), _lib.stream_handle()), "sample_count")
+    tot = counts.sum(dim=1).cpu().numpy().astype(np.int64).reshape(n, ncand, 4)
+    # the reference's visit loop per item (vectorised for single-patch grids)
+    take_nw = np.zeros((n, ncand), np.int64)
+    take_b = np.zeros((n, ncand, 3), np.int64)
+    collected = np.zeros(n, np.int64)
+    patch_counts = [None] * n
+    if ncand == 1:
+        npx = rects[0][2] * rects[0][3]
+        min_frac = 1.0 - plan.background_fraction_cutoff
+        take_b[:, 0, :] = np.minimum(tot[:, 0, 1:], plan.sample_cap)
+        used = tot[:, 0, 0] >= min_frac * npx
+        take_nw[:, 0] = np.where(used, np.minimum(tot[:, 0, 0], plan.target_pixels), 0)
+        collected = take_nw[:, 0].copy()
+    else:
+        for i in range(n):
+            takes, uc, coll, _, _ = _visit(plan, order[:ncand], rects,
+                                           lambda k, i=i: tuple(int(v) for v in tot[i, k]))
+            for (k, tnw, _base, tb) in takes:
+                take_nw[i, k] = tnw
+                take_b[i, k] = tb
+            collected[i] = coll
+            patch_counts[i] = uc
+    offsets = np.concatenate([[0], np.cumsum(collected)]).astype(np.int64)
+    total = int(offsets[-1])
+    base_in_item = np.cumsum(take_nw, axis=1) - take_nw
+    tk = np.zeros((n, ncand), dtype=TAKE_DT)
+    tk["take_nonwhite"] = take_nw
+    tk["out_base"] = offsets[:-1, None] + base_in_item
+    tk["take_bright"] = take_b
+    tk["problem"] = np.arange(n, dtype=np.int32)[:, None]
+    sample = t.empty((max(total, 1), 3), dtype=t.uint8, device=dev)
+    hist = t.zeros((n, 3, 256), dtype=t.int32, device=dev)
+    d_tk = t.from_numpy(tk.ravel().view(np.uint8).copy()).to(dev)
+    _lib.check(L.spcn_sample_compact(_lib.ptr(imgs), _lib.ptr(d_desc), n * ncand, chunks, thr,
+                                     _lib.ptr(counts), _lib.ptr(d_tk), _lib.ptr(sample),
+                                     _lib.ptr(hist), _lib.stream_handle()), "sample_compact")
+    status = np.zeros(n, np.int32)
+    status[collected == 0] = -_lib.SPCN_EBLANK
+    status[(collected > 0) & (collected < 10)] = -_lib.SPCN_EINSUFFICIENT
+    # background i0 per item (exact order statistic of the 8-bit pools)
+    i0 = t.empty((n, 3), dtype=t.float64, device=dev)
+    empty = t.empty((n, 3), dtype=t.int32, device=dev)
+    _lib.check(L.spcn_i0_from_hist(_lib.ptr(hist), n, _lib.ptr(i0), _lib.ptr(empty),
+                                   _lib.stream_handle()), "i0_from_hist")
+    i0_h = i0.cpu().numpy()
+    if empty.any().item():
+        warnings.warn("some items had no pixels brighter than the white threshold in a "
+                      "channel; their i0 fell back to 255", optics.BackgroundEstimateWarning,
+                      stacklevel=2)
+    luts = t.from_numpy(_od_tables_exact(i0_h)).to(dev)
+    d_off = t.from_numpy(offsets).to(dev)
+    flat = sample.reshape(-1)
+    r = snmf.snmf_batched(flat, d_off, luts, cfg, cluster=1)
+    h = snmf.code_samples(flat, d_off, luts, r.basis, code_lam, int(collected.max(initial=0)))
+    from . import stats as dstats
+
+    p99, absent = dstats.segment_percentiles(h, d_off, 99.0)
+    absent_h = absent.cpu().numpy().any(axis=1)
+    status[(status == 0) & absent_h] = -_lib.SPCN_ESTAIN_ABSENT
+    prov = {"source": "", "config_hash": config_hash(_cfg_fields(plan, cfg, code_lam, False))}
+    return BatchFit(i0=i0, basis=r.basis, p99=p99, luts=luts, count=collected, status=status,
+                    provenance=prov)
+
+
+def transform_batch(images, fits: BatchFit, target: FitParams, out=None, *,
+                    code_lam: float = 0.0, precision: str = "exact", max_sweeps: int = 2000):
+    """Recolour every item against `target`.  Returns (out, errors) where
+    errors[i] is None or the exception the reference would have raised."""
+    t = _dev.torch()
+    L = _sig()
+    if precision not in _lib.PREC:
+        raise ValueError(f"precision must be one of {sorted(_lib.PREC)}")
+    imgs = images.contiguous()
+    n = int(imgs.shape[0])
+    per = int(imgs.shape[1]) * int(imgs.shape[2])
+    dev = imgs.device
+    out = out if out is not None else t.empty_like(imgs)
+    fs_b, sp_b = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    L.spcn_batch_sizes(ctypes.byref(fs_b), ctypes.byref(sp_b))
+    fast = t.empty(n * fs_b.value, dtype=t.uint8, device=dev)
+    strict = t.empty(n * sp_b.value, dtype=t.uint8, device=dev)
+    flut = t.empty((n, 3, 256), dtype=t.float32, device=dev)
+    status = t.from_numpy(fits.status.astype(np.int32)).to(dev)
+    tg = BatchTargetC()
+    tg.i0[:] = [float(x) for x in np.asarray(target.i0, dtype=np.float64)]
+    tg.basis[:] = [float(x) for x in np.asarray(target.basis, dtype=np.float64).ravel()]
+    tg.p99[:] = [float(x) for x in np.asarray(target.stats.p99, dtype=np.float64)]
+    _lib.check(L.spcn_batch_params(n, _lib.ptr(fits.i0), _lib.ptr(fits.luts),
+                                   _lib.ptr(fits.basis.contiguous()), _lib.ptr(fits.p99),
+                                   ctypes.byref(tg), float(code_lam), int(max_sweeps),
+                                   _lib.PREC[precision], _lib.ptr(fast), _lib.ptr(flut),
+                                   _lib.ptr(strict), _lib.ptr(status), _lib.stream_handle()),
+               "batch_params")
+    if precision == "strict":
+        status = t.where(status == 0, t.ones_like(status), status)
+    fast_h = fast.cpu().numpy()
+    status_h = status.cpu().numpy()
+    errors = [None if s >= 0 else _ERR[int(s)](_MSG[int(s)]) for s in status_h]
+    if per % 16:
+        # item boundaries not 16-pixel aligned: one aligned-head/tail launch per item
+        for i in range(n):
+            if status_h[i] < 0:
+                continue
+            fp = fits.params(i)
+            fac = np.asarray(target.stats.p99, dtype=np.float64) / fp.stats.p99
+            XformPlan(fp.i0, fp.basis, code_lam, fac, target.basis, target.i0,
+                      precision=precision).run(imgs[i], out[i], per)
+        return out, errors
+    off = np.arange(n + 1, dtype=np.int64) * per
+    d_off = t.from_numpy(off).to(dev)
+    ws_bytes = int(_lib.lib().spcn_xform_workspace_bytes(n * per))
+    ws = _dev.workspace(ws_bytes)
+    _lib.check(L.spcn_xform_batch(_lib.ptr(imgs), _lib.ptr(out), n, off.ctypes.data,
+                                  _lib.ptr(d_off), fast_h.ctypes.data, status_h.ctypes.data,
+                                  _lib.ptr(status), _lib.ptr(flut), _lib.ptr(strict),
+                                  _lib.PREC[precision], _lib.ptr(ws), ws_bytes,
+                                  _lib.stream_handle()), "xform_batch")
+    return out, errors
+
+
+def normalize_batch(images, target, *, plan: SamplePlan = SamplePlan(),
+                    cfg: SnmfConfig = SnmfConfig(), code_lam: float = 0.0,
+                    precision: str = "exact", out=None):
+    """fit_batch + transform_batch: the batch equivalent of ``normalize``.
+    ``target`` is a FitParams (e.g. a loaded profile)."""
+    fits = fit_batch(images, plan, cfg, code_lam=code_lam)
+    out, errors = transform_batch(images, fits, target, out, code_lam=code_lam,
+                                  precision=precision)
+    return out, errors, fits

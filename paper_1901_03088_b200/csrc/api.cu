@@ -12,6 +12,7 @@
 
 #include "spcn.h"
 #include "spcn_device.cuh"
+#include "params.cuh"
 #include "xform.h"
 
 #include "launch_count.h"
@@ -50,14 +51,6 @@ int check_basis(const double* w, const char* role) {
   return SPCN_OK;
 }
 
-// Gram entries in the reference's scalar order (src/stain_sep.py:197-199).
-// This file is compiled with -ffp-contract=off so no FMA is formed here.
-void gram(const double* w, double& g00, double& g01, double& g11) {
-  g00 = w[0] * w[0] + w[2] * w[2] + w[4] * w[4];
-  g11 = w[1] * w[1] + w[3] * w[3] + w[5] * w[5];
-  g01 = w[0] * w[1] + w[2] * w[3] + w[4] * w[5];
-}
-
 // OD table: ln(i0_c / clip(i, 1, i0_c)), src/optics.py:92-94.
 void od_table(const double* i0, const double* given, double lut[3][256]) {
   if (given) {
@@ -75,81 +68,12 @@ void od_table(const double* i0, const double* given, double lut[3][256]) {
 void fill_strict(StrictP& sp, const double* lut_src, const double* ws, const double* wt,
                  const double* f, const double* i0t, double lam, int max_sweeps) {
   std::memcpy(sp.lut, lut_src, sizeof(sp.lut));
-  for (int c = 0; c < 3; ++c)
-    for (int j = 0; j < 2; ++j) {
-      sp.ws[c][j] = ws ? ws[c * 2 + j] : 0.0;
-      sp.wt[c][j] = wt ? wt[c * 2 + j] : 0.0;
-    }
-  sp.f[0] = f ? f[0] : 1.0;
-  sp.f[1] = f ? f[1] : 1.0;
-  for (int c = 0; c < 3; ++c) sp.i0t[c] = i0t ? i0t[c] : 255.0;
-  if (ws) {
-    gram(ws, sp.g00, sp.g01, sp.g11);
-    sp.det = sp.g00 * sp.g11 - sp.g01 * sp.g01;
-  }
-  sp.lam = lam;
-  sp.tol = 0.0;
-  sp.max_sweeps = max_sweeps;
-  sp.pad_ = 0;
+  fill_strict_scalars(sp, ws, wt, f, i0t, lam, max_sweeps);
 }
 
-// fp32 coefficients + the certification bound (DESIGN.md §Certified rounding).
-// Returns false when the fast path must not be used (ill-conditioned basis,
-// target i0 outside [0,255], or a target i0 sitting on a rounding tie).
+// fp32 coefficients + certification bound (params.cuh, shared with the batch builder)
 bool fill_fast(FastP& fp, const StrictP& sp, bool exact) {
-  const double g00 = sp.g00, g01 = sp.g01, g11 = sp.g11, det = sp.det;
-  if (!(det > 1e-6 * g00 * g11) || !(g00 > 0) || !(g11 > 0)) return false;
-  for (int c = 0; c < 3; ++c)
-    if (!(sp.i0t[c] >= 0.0 && sp.i0t[c] <= 255.0)) return false;
-  for (int c = 0; c < 3; ++c)
-    for (int i = 0; i < 256; ++i) fp.lut[c][i] = static_cast<float>(sp.lut[c][i]);
-  for (int c = 0; c < 3; ++c)
-    for (int j = 0; j < 2; ++j) fp.w[c][j] = static_cast<float>(sp.ws[c][j]);
-  fp.nlam = static_cast<float>(-sp.lam);
-  const double A = g11 / det, C = g01 / det, E = 1.0 / g11, F = g01 / g11, G = 1.0 / g00,
-               H = g01 / g00;
-  fp.A = (float)A; fp.nC = -(float)C; fp.E = (float)E;
-  fp.nF2 = -(float)F * 0.5f; fp.G = (float)G; fp.nH2 = -(float)H * 0.5f;
-  for (int c = 0; c < 3; ++c) fp.ilo[c] = fp.ihi[c] = 0.0f;
-  const double log2e = 1.4426950408889634;
-  double Kabs[3][2];
-  for (int c = 0; c < 3; ++c)
-    for (int j = 0; j < 2; ++j) {
-      const double k = -log2e * sp.wt[c][j] * sp.f[j];
-      fp.K2[c][j] = static_cast<float>(k) * 0.5f;
-      Kabs[c][j] = std::fabs(k);
-    }
-  for (int c = 0; c < 3; ++c) fp.i0t[c] = static_cast<float>(sp.i0t[c]);
-  fp.lam4 = static_cast<float>(4.0 * sp.lam);
-  // error chain, per unit u*T (u = 2^-24, T = t0 + t1 + 4 lam)
-  const double P0 = A + C, D0 = 8.0 * (A + C);
-  const double D1 = 7.0 * E + F * D0 + 3.0 * F * P0;
-  const double P1 = E + F * P0;
-  const double Dh0 = 7.0 * G + H * D1 + 3.0 * H * P1;
-  const double H0 = G + H * P1;
-  double L = 0.0;
-  for (int c = 0; c < 3; ++c) {
-    const double l = Kabs[c][0] * Dh0 + Kabs[c][1] * D1 + 3.0 * (Kabs[c][0] * H0 + Kabs[c][1] * P1);
-    L = l > L ? l : L;
-  }
-  const double u = std::ldexp(1.0, -24), ln2 = 0.6931471805599453;
-  const double a1 = 1.25 * ln2 * u * L * 1.001;
-  const double a0 = 1.25 * (std::ldexp(1.0, -21) + std::ldexp(1.0, -21));
-  fp.a1 = static_cast<float>(a1 * (1.0 + 1e-6));
-  fp.a0 = static_cast<float>(a0 * (1.0 + 1e-6));
-  if (!exact) return true;
-  // worst-case T over all u8 inputs: OD is largest at i = 0
-  double tmax = 4.0 * sp.lam;
-  for (int c = 0; c < 3; ++c) tmax += (sp.ws[c][0] + sp.ws[c][1]) * sp.lut[c][0];
-  if (a1 * tmax + a0 > 1e-3) return false;
-  // zero-density pixels render exactly i0_t; the interval around an exact tie
-  // (i0_t = k + 0.5) can never certify, so such targets take the strict path
-  const double a_zero = a1 * 4.0 * sp.lam + a0;
-  for (int c = 0; c < 3; ++c) {
-    const double fr = sp.i0t[c] - std::floor(sp.i0t[c]);
-    if (std::fabs(fr - 0.5) <= 2.0 * a_zero * sp.i0t[c] + 1e-9) return false;
-  }
-  return true;
+  return fill_fast_scalars(fp, sp, exact, fp.lut);
 }
 
 constexpr size_t kWsHeader = 16;
@@ -537,3 +461,111 @@ extern "C" int spcn_render_synthetic(uint8_t* out, int64_t width, int64_t row0, 
                                 static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "render_synthetic");
 }
+
+// ------------------------------------------------------------------ batched recolouring
+#include "batch.h"
+
+extern "C" {
+
+int spcn_batch_sizes(size_t* fast_scalar_bytes, size_t* strict_param_bytes) {
+  if (fast_scalar_bytes) *fast_scalar_bytes = sizeof(FastS);
+  if (strict_param_bytes) *strict_param_bytes = sizeof(StrictP);
+  return SPCN_OK;
+}
+
+int spcn_batch_params(int32_t nitems, const double* i0, const double* luts, const double* bases,
+                      const double* p99, const spcn_batch_target* tgt, double code_lam,
+                      int32_t max_sweeps, int32_t precision, void* fast_scalars, float* flut,
+                      void* strict_params, int32_t* status, void* stream) {
+  g_err.clear();
+  if (nitems < 0) return fail(SPCN_EINVAL, "nitems must be >= 0");
+  if (!tgt) return fail(SPCN_EINVAL, "target is NULL");
+  int rc = check_basis(tgt->basis, "target");
+  if (rc) return rc;
+  if (!(code_lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
+  if (precision < 0 || precision > 2) return fail(SPCN_EINVAL, "unknown precision");
+  if (nitems == 0) return SPCN_OK;
+  if (!i0 || !luts || !bases || !p99 || !fast_scalars || !flut || !strict_params || !status)
+    return fail(SPCN_EINVAL, "NULL argument");
+  BatchTarget t;
+  for (int c = 0; c < 3; ++c) t.i0[c] = tgt->i0[c];
+  for (int k = 0; k < 6; ++k) t.basis[k] = tgt->basis[k];
+  t.p99[0] = tgt->p99[0];
+  t.p99[1] = tgt->p99[1];
+  cudaError_t e = launch_build_params(nitems, i0, luts, bases, p99, t, code_lam, max_sweeps,
+                                      precision == SPCN_PREC_EXACT ? 1 : 0,
+                                      static_cast<FastS*>(fast_scalars), flut,
+                                      static_cast<StrictP*>(strict_params), status,
+                                      static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "batch_params");
+}
+
+int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int64_t* off_host,
+                     const int64_t* off_dev, const void* fast_scalars_host,
+                     const int32_t* status_host, const int32_t* status_dev, const float* flut,
+                     const void* strict_params, int32_t precision, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (nitems < 0) return fail(SPCN_EINVAL, "nitems must be >= 0");
+  if (nitems == 0) return SPCN_OK;
+  if (!src || !dst || !off_host || !off_dev || !fast_scalars_host || !status_host || !status_dev ||
+      !flut || !strict_params)
+    return fail(SPCN_EINVAL, "NULL argument");
+  if (precision < 0 || precision > 2) return fail(SPCN_EINVAL, "unknown precision");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const FastS* fs = static_cast<const FastS*>(fast_scalars_host);
+  const StrictP* sps = static_cast<const StrictP*>(strict_params);
+  const bool strict_all = precision == SPCN_PREC_STRICT;
+  const bool exact = precision == SPCN_PREC_EXACT;
+  int64_t max_pix = 0;
+  bool any_strict = false;
+  for (int i = 0; i < nitems; ++i) {
+    const int64_t n = off_host[i + 1] - off_host[i];
+    if (n < 0) return fail(SPCN_EINVAL, "offsets must be non-decreasing");
+    if ((off_host[i] & 15) != 0 || (n & 15) != 0)
+      return fail(SPCN_EINVAL, "item pixel offsets and sizes must be multiples of 16");
+    max_pix = n > max_pix ? n : max_pix;
+    any_strict = any_strict || status_host[i] == 1 || (strict_all && status_host[i] == 0);
+  }
+  if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    return fail(SPCN_EINVAL, "src/dst must be 16-byte aligned");
+  unsigned long long* count = nullptr;
+  unsigned long long* items = nullptr;
+  unsigned long long cap = 0;
+  cudaError_t e = cudaSuccess;
+  if (exact) {
+    if (!workspace || workspace_bytes < kWsHeader + 8)
+      return fail(SPCN_EINVAL, "EXACT precision needs a workspace");
+    count = static_cast<unsigned long long*>(workspace);
+    items = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + kWsHeader);
+    cap = (workspace_bytes - kWsHeader) / 8;
+    if ((e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), st)) != cudaSuccess)
+      return cuda_fail(e, "memset");
+  }
+  if (!strict_all) {
+    static thread_local BatchArgs a;
+    for (int i0 = 0; i0 < nitems; i0 += kMaxBatch) {
+      const int n = nitems - i0 < kMaxBatch ? nitems - i0 : kMaxBatch;
+      a.n = n;
+      a.item0 = i0;
+      for (int i = 0; i <= n; ++i) a.off[i] = off_host[i0 + i];   // absolute pixel offsets
+      for (int i = 0; i < n; ++i) {
+        a.strict[i] = status_host[i0 + i] != 0 ? 1 : 0;
+        a.s[i] = fs[i0 + i];
+      }
+      e = launch_xform_batch(exact ? 0 : 1, src, dst, flut, sps, a, count, items, cap, st);
+      if (e != cudaSuccess) return cuda_fail(e, "xform_batch");
+    }
+    if (exact && (e = launch_repair_batch(dst, sps, off_dev, nitems, count, items, cap, st)) !=
+                     cudaSuccess)
+      return cuda_fail(e, "repair_batch");
+  }
+  if (any_strict) {
+    // strict items: status 1 (or every valid item in STRICT precision)
+    e = launch_strict_batch(src, dst, sps, off_dev, status_dev, nitems, max_pix, st);
+    if (e != cudaSuccess) return cuda_fail(e, "strict_batch");
+  }
+  return SPCN_OK;
+}
+
+}  // extern "C"

@@ -122,7 +122,7 @@ __device__ __forceinline__ float od_lookup(const uint8_t* lut, const uint32_t* w
 // of the pair's six roundings is not certified (r_lo != r_hi); both pixels of
 // such a pair go to the fp64 repair list.
 template <int MODE>
-__device__ __forceinline__ uint32_t recolor_pair(const FastP& fp, const uint8_t* lut,
+__device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t* lut,
                                                  const uint32_t* w, int k, const uint32_t* lc,
                                                  uint32_t* ob) {
   const int a = 3 * k, b = 3 * k + 3;
@@ -351,32 +351,38 @@ __global__ void __launch_bounds__(XCfg<CW, REP, STORE, BLK>::kThreads, BLK)
 
 // ---------------------------------------------------------------------------
 // k_xform_warp: the same per-thread pipeline, but every warp owns its own
-// ring of NSW 1536-byte slots (512 px each) and is its own producer: lane 0
-// issues the 1-D TMA bulk load of the warp's next slices, the warp recolours a
-// slice in place in shared memory, and lane 0 issues the TMA bulk store from
-// the same slot; the slot is refilled as soon as that store has finished
-// reading it.  No CTA-wide stage coupling: a slow warp never holds back the
-// others' refills.  Work: 512-px slices, grid-strided over all warps.
-template <int CW, int REP, int NSW, int BLK>
+// ring of NSW slots of NSUB x 512 px and is its own producer: lane 0 issues the
+// 1-D TMA bulk load of the warp's next slices, the warp recolours a slice in
+// place in shared memory (each lane: 16 px of each 512-px sub-slice, so the
+// 48-byte lane blocks stay bank-conflict-free), and lane 0 issues the TMA bulk
+// store from the same slot; the slot is refilled as soon as that store has
+// finished reading it.  No CTA-wide stage coupling: a slow warp never holds
+// back the others' refills.  Work: slices grid-strided over all warps; NSUB
+// amortises the per-slice bookkeeping (bulk ops, barrier waits) over more px.
+template <int CW, int REP, int NSW, int BLK, int NSUB>
 struct WCfg {
   static constexpr int kThreads = 32 * CW;
+  static constexpr int kSlicePx = 512 * NSUB;
+  static constexpr int kSlotBytes = 3 * kSlicePx;
   static constexpr int kLutBytes = REP == 32 ? 2 * 65536 : 65536;
-  static constexpr size_t kSmem = kLutBytes + (size_t)CW * NSW * 1536 + CW * NSW * 8;
+  static constexpr size_t kSmem = kLutBytes + (size_t)CW * NSW * kSlotBytes + CW * NSW * 8;
   static_assert(kSmem <= (BLK == 1 ? 227 * 1024 : 113 * 1024), "shared memory budget");
+  static_assert(REP == 16 || REP == 32, "table layouts exist for 16 and 32 replicas");
 };
 
-template <int MODE, int CW, int REP, int NSW, int BLK>
+template <int MODE, int CW, int REP, int NSW, int BLK, int NSUB>
 __global__ void __launch_bounds__(32 * CW, BLK)
     k_xform_warp(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
                  const __grid_constant__ FastP fp, const __grid_constant__ StrictP sp,
                  RepairList rl) {
-  using C = WCfg<CW, REP, NSW, BLK>;
+  using C = WCfg<CW, REP, NSW, BLK, NSUB>;
+  constexpr int kSlicePx = C::kSlicePx, kSlotBytes = C::kSlotBytes;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint8_t* lut = smem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint8_t* myslots = smem + C::kLutBytes + (size_t)warp * NSW * 1536;
-  uint64_t* mybar = reinterpret_cast<uint64_t*>(smem + C::kLutBytes + (size_t)CW * NSW * 1536) +
-                    warp * NSW;
+  uint8_t* myslots = smem + C::kLutBytes + (size_t)warp * NSW * kSlotBytes;
+  uint64_t* mybar =
+      reinterpret_cast<uint64_t*>(smem + C::kLutBytes + (size_t)CW * NSW * kSlotBytes) + warp * NSW;
 
   if (REP == 16) {
     for (int i = tid; i < 256 * 48; i += C::kThreads) {
@@ -404,16 +410,16 @@ __global__ void __launch_bounds__(32 * CW, BLK)
     const uint32_t lrep = (uint32_t)lane * 4;
     lc[0] = lrep; lc[1] = 128u + lrep; lc[2] = 0x10000u | lrep;
   }
-  const int64_t nslices = (npix + 511) / 512;
+  const int64_t nslices = (npix + kSlicePx - 1) / kSlicePx;
   const int64_t gw = (int64_t)blockIdx.x * CW + warp, GW = (int64_t)gridDim.x * CW;
   uint64_t pol = 0;
   auto issue_load = [&](int64_t k) {   // lane 0 only
     const int64_t j = gw + k * GW;
     if (j >= nslices) return;
     const int s = (int)(k % NSW);
-    const uint32_t bytes = static_cast<uint32_t>(3 * min64(512, npix - j * 512));
+    const uint32_t bytes = static_cast<uint32_t>(3 * min64(kSlicePx, npix - j * kSlicePx));
     mbar_expect_tx(&mybar[s], bytes);
-    bulk_g2s(myslots + s * 1536, src + 3 * j * 512, bytes, &mybar[s], pol);
+    bulk_g2s(myslots + s * kSlotBytes, src + 3 * j * kSlicePx, bytes, &mybar[s], pol);
   };
   if (lane == 0) {
     pol = policy_evict_first();
@@ -425,75 +431,79 @@ __global__ void __launch_bounds__(32 * CW, BLK)
     if (j >= nslices) break;
     const int s = (int)(k % NSW);
     mbar_wait(&mybar[s], (uint32_t)((k / NSW) & 1));
-    const int64_t n = min64(512, npix - j * 512);
-    const bool valid = 16 * lane < n;
-    uint8_t* slot = myslots + s * 1536 + 48 * lane;
-    uint32_t w[12], ob[48], o[12];
-    uint32_t badpairs = 0;
-    if (valid) {
-      const uint4* q = reinterpret_cast<const uint4*>(slot);
-      const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
-      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-      w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-      w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
-      if (MODE == 3) {
+    const int n = (int)min64(kSlicePx, npix - j * kSlicePx);
+    uint8_t* sbase = myslots + s * kSlotBytes;
 #pragma unroll
-        for (int t = 0; t < 12; ++t) o[t] = w[t];
-      } else {
+    for (int u = 0; u < NSUB; ++u) {
+      const bool valid = u * 512 + 16 * lane < n;
+      uint8_t* slot = sbase + u * 1536 + 48 * lane;
+      uint32_t w[12], ob[48], o[12];
+      uint32_t badpairs = 0;
+      if (valid) {
+        const uint4* q = reinterpret_cast<const uint4*>(slot);
+        const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
+        w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+        w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+        w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
+        if (MODE == 3) {
 #pragma unroll
-        for (int qq = 0; qq < 8; ++qq) {
-          const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * qq, lc, ob);
-          if (MODE == 0 || MODE == 2) badpairs |= (bad != 0u ? 1u : 0u) << qq;
+          for (int t = 0; t < 12; ++t) o[t] = w[t];
+        } else {
 #pragma unroll
-          for (int t = 0; t < 12; ++t)
-            if (4 * t + 3 >= 6 * qq && 4 * t + 3 < 6 * qq + 6)
-              o[t] = pack4(ob[4 * t], ob[4 * t + 1], ob[4 * t + 2], ob[4 * t + 3]);
-        }
-      }
-      uint4* d = reinterpret_cast<uint4*>(slot);
-      d[0] = make_uint4(o[0], o[1], o[2], o[3]);
-      d[1] = make_uint4(o[4], o[5], o[6], o[7]);
-      d[2] = make_uint4(o[8], o[9], o[10], o[11]);
-    }
-    if (MODE == 0 || MODE == 2) {
-      if (__any_sync(0xffffffffu, badpairs != 0u)) {
-        uint32_t badmask = 0;
+          for (int qq = 0; qq < 8; ++qq) {
+            const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * qq, lc, ob);
+            if (MODE == 0 || MODE == 2) badpairs |= (bad != 0u ? 1u : 0u) << qq;
 #pragma unroll
-        for (int qq = 0; qq < 8; ++qq) badmask |= ((badpairs >> qq) & 1u) * (3u << (2 * qq));
-        const uint32_t cnt = __popc(badmask);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl += y;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned long long base = 0;
-        if (lane == 31) base = atomicAdd(rl.count, (unsigned long long)total);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        unsigned long long item = base + incl - cnt;
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          if (!((badmask >> kk) & 1u)) continue;
-          const uint32_t rgb = byte_of(w, 3 * kk) | (byte_of(w, 3 * kk + 1) << 8) |
-                               (byte_of(w, 3 * kk + 2) << 16);
-          const int64_t gp = j * 512 + 16 * lane + kk;
-          if (item < rl.cap) {
-            rl.items[item] = (static_cast<unsigned long long>(gp) << 24) | rgb;
-          } else {  // list overflow: fp64 recompute patched into the slot before the store
-            const uint32_t px = strict_rgb(sp, rgb);
-            slot[3 * kk] = px & 255u;
-            slot[3 * kk + 1] = (px >> 8) & 255u;
-            slot[3 * kk + 2] = (px >> 16) & 255u;
+            for (int t = 0; t < 12; ++t)
+              if (4 * t + 3 >= 6 * qq && 4 * t + 3 < 6 * qq + 6)
+                o[t] = pack4(ob[4 * t], ob[4 * t + 1], ob[4 * t + 2], ob[4 * t + 3]);
           }
-          ++item;
+        }
+        uint4* d = reinterpret_cast<uint4*>(slot);
+        d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        d[2] = make_uint4(o[8], o[9], o[10], o[11]);
+      }
+      if (MODE == 0 || MODE == 2) {
+        if (__any_sync(0xffffffffu, badpairs != 0u)) {
+          uint32_t badmask = 0;
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq) badmask |= ((badpairs >> qq) & 1u) * (3u << (2 * qq));
+          const uint32_t cnt = __popc(badmask);
+          uint32_t incl = cnt;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+          }
+          const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+          unsigned long long base = 0;
+          if (lane == 31) base = atomicAdd(rl.count, (unsigned long long)total);
+          base = __shfl_sync(0xffffffffu, base, 31);
+          unsigned long long item = base + incl - cnt;
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) {
+            if (!((badmask >> kk) & 1u)) continue;
+            const uint32_t rgb = byte_of(w, 3 * kk) | (byte_of(w, 3 * kk + 1) << 8) |
+                                 (byte_of(w, 3 * kk + 2) << 16);
+            const int64_t gp = j * kSlicePx + u * 512 + 16 * lane + kk;
+            if (item < rl.cap) {
+              rl.items[item] = (static_cast<unsigned long long>(gp) << 24) | rgb;
+            } else {  // list overflow: fp64 recompute patched into the slot before the store
+              const uint32_t px = strict_rgb(sp, rgb);
+              slot[3 * kk] = px & 255u;
+              slot[3 * kk + 1] = (px >> 8) & 255u;
+              slot[3 * kk + 2] = (px >> 16) & 255u;
+            }
+            ++item;
+          }
         }
       }
     }
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      bulk_s2g(dst + 3 * j * 512, myslots + s * 1536, static_cast<uint32_t>(3 * n));
+      bulk_s2g(dst + 3 * j * kSlicePx, sbase, static_cast<uint32_t>(3 * n));
       bulk_commit();
       if (k >= 1) {
         bulk_wait_read<1>();          // the store of item k-1 has read its slot
@@ -597,12 +607,13 @@ struct Shape {
   XformFn fn[4];
 };
 
-template <int CW, int REP, int NSW, int BLK>
+template <int CW, int REP, int NSW, int BLK, int NSUB>
 Shape make_wshape() {
-  using C = WCfg<CW, REP, NSW, BLK>;
-  return Shape{CW, REP, 2, BLK, C::kThreads, CW * 512, 0, C::kSmem,
-               {k_xform_warp<0, CW, REP, NSW, BLK>, k_xform_warp<1, CW, REP, NSW, BLK>,
-                k_xform_warp<2, CW, REP, NSW, BLK>, k_xform_warp<3, CW, REP, NSW, BLK>}};
+  using C = WCfg<CW, REP, NSW, BLK, NSUB>;
+  return Shape{CW, REP, 1 + NSUB, BLK, C::kThreads, CW * C::kSlicePx, 0, C::kSmem,
+               {k_xform_warp<0, CW, REP, NSW, BLK, NSUB>, k_xform_warp<1, CW, REP, NSW, BLK, NSUB>,
+                k_xform_warp<2, CW, REP, NSW, BLK, NSUB>,
+                k_xform_warp<3, CW, REP, NSW, BLK, NSUB>}};
 }
 
 template <int CW, int REP, int STORE, int BLK>
@@ -618,9 +629,10 @@ Shape make_shape() {
 // SPCN_XFORM_IDENTITY=1 makes the kernel copy input to output (memory-path
 // ceiling measurement only).
 static Shape g_shapes[] = {
-    make_wshape<16, 32, 4, 1>(),   // production: per-warp rings, conflict-free table
-    make_shape<16, 32, 1, 1>(), make_shape<8, 16, 0, 2>(), make_shape<16, 32, 0, 1>(),
-    make_wshape<16, 16, 6, 1>(), make_wshape<8, 16, 4, 2>(), make_wshape<20, 16, 5, 1>()};
+    make_wshape<16, 16, 3, 1, 2>(),   // production: per-warp rings of 2x512-px slots
+    make_wshape<16, 32, 4, 1, 1>(), make_shape<16, 32, 1, 1>(),
+    make_wshape<16, 16, 2, 1, 3>(), make_wshape<12, 16, 3, 1, 3>(), make_wshape<16, 16, 4, 1, 1>(),
+    make_wshape<8, 16, 2, 2, 2>(), make_wshape<8, 16, 3, 2, 1>()};
 static Shape* g_shape = nullptr;
 static bool g_identity = false;
 

@@ -1,0 +1,154 @@
+"""GPU parity of the batched path (configs[1]: many patches, one target).
+
+Each item must give exactly what the single-image path and the reference
+give for it: fit parameters (i0 exact, basis/p99 as in test_fit_gpu), output
+bytes bit-identical in exact/strict precision, per-item errors of the same
+class as the reference's (src/cli.py:220-244, 270-301) without disturbing the
+other items.
+"""
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import spcn_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _pb():
+    import paper_1901_03088_b200 as pb
+
+    return pb
+
+
+def _items(h, w, n, seed=0):
+    rng = np.random.default_rng(seed)
+    out = []
+    for k in range(n):
+        i0 = tuple(int(v) for v in rng.integers(228, 256, size=3))
+        frac = float(rng.uniform(0.3, 0.9))
+        sampler = orc.sparse_pairs if k % 2 == 0 else orc.dense_pairs
+        px, _, _ = orc.render(w, h, seed * 1000 + k, i0=i0, tissue_fraction=frac,
+                              sampler=sampler)
+        out.append(px)
+    return out
+
+
+def _target(pb, seed=77):
+    px, _, _ = orc.render(256, 192, seed, i0=(246, 242, 250))
+    ft = orc.fit_params(px)
+    return pb.FitParams(i0=ft["i0"], basis=ft["basis"],
+                        stats=pb.StainStats(p99=np.asarray(ft["p99"]), sample_count=ft["count"]))
+
+
+def _oracle_item(px, plan, tgt, code_lam=0.0):
+    """(fit dict, output) or (error kind, None) for one item."""
+    try:
+        src = orc.fit_params(px, plan)
+    except orc.OracleError as e:
+        return e.kind, None
+    t = {"i0": tgt.i0, "basis": tgt.basis, "p99": tgt.stats.p99}
+    try:
+        out = orc.run_transform(px, src, t, workers=1, code_lam=code_lam)
+    except orc.OracleError as e:
+        return e.kind, None
+    return src, out
+
+
+def _run(pb, imgs, plan, tgt, precision="exact"):
+    import torch
+
+    x = torch.from_numpy(np.stack(imgs)).cuda()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        out, errors, fits = pb.normalize_batch(x, tgt, plan=plan, precision=precision)
+    return out.cpu().numpy(), errors, fits
+
+
+@pytest.mark.parametrize("shape,plan_kw", [
+    ((96, 160), {}),                                                   # one patch per item
+    ((128, 192), dict(patch_size=64, max_patches=2, target_pixels=3000)),  # visit loop
+    ((33, 37), {}),                                                    # unaligned item size
+])
+def test_batch_matches_reference_per_item(shape, plan_kw):
+    pb = _pb()
+    h, w = shape
+    imgs = _items(h, w, 9, seed=h)
+    imgs[3] = np.full((h, w, 3), 255, np.uint8)                 # blank item
+    tgt = _target(pb)
+    plan = pb.SamplePlan(**plan_kw)
+    oplan = orc.Plan(**plan_kw)
+    out, errors, fits = _run(pb, imgs, plan, tgt)
+    for i, px in enumerate(imgs):
+        src, ref = _oracle_item(px, oplan, tgt)
+        if ref is None:
+            assert errors[i] is not None and type(errors[i]).__name__ == src, (i, errors[i], src)
+            continue
+        assert errors[i] is None, (i, errors[i])
+        fp = fits.params(i)
+        assert np.array_equal(fp.i0, src["i0"]), i
+        np.testing.assert_allclose(fp.basis, src["basis"], atol=1e-9, err_msg=str(i))
+        np.testing.assert_allclose(fp.stats.p99, src["p99"], rtol=1e-9, err_msg=str(i))
+        assert fp.stats.sample_count == src["count"], i
+        assert np.array_equal(out[i], ref), (i, int((out[i] != ref).sum()))
+
+
+def test_batch_equals_single_item_path():
+    import torch
+
+    pb = _pb()
+    imgs = _items(112, 144, 6, seed=5)
+    tgt = _target(pb, 3)
+    plan = pb.SamplePlan()
+    out, errors, fits = _run(pb, imgs, plan, tgt)
+    for i, px in enumerate(imgs):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            fp = pb.fit(torch.from_numpy(px).cuda(), plan)
+        bp = fits.params(i)
+        assert np.array_equal(bp.i0, fp.i0)
+        assert np.array_equal(bp.basis, fp.basis)
+        assert np.array_equal(bp.stats.p99, fp.stats.p99)
+        sink = pb.DeviceWriter(px.shape[1], px.shape[0])
+        pb.transform(pb.DeviceSource(torch.from_numpy(px).cuda()), fp, tgt, sink)
+        assert np.array_equal(sink.pixels.cpu().numpy(), out[i])
+
+
+@pytest.mark.parametrize("precision", ["strict", "fast"])
+def test_batch_precisions(precision):
+    pb = _pb()
+    imgs = _items(64, 96, 5, seed=11)
+    tgt = _target(pb, 4)
+    exact, _, _ = _run(pb, imgs, pb.SamplePlan(), tgt, "exact")
+    out, errors, _ = _run(pb, imgs, pb.SamplePlan(), tgt, precision)
+    assert all(e is None for e in errors)
+    if precision == "strict":
+        assert np.array_equal(out, exact)
+    else:
+        d = np.abs(out.astype(np.int16) - exact.astype(np.int16))
+        assert d.max() <= 1 and (d > 0).mean() <= 1e-3
+
+
+def test_batch_degenerate_target_reports_every_item():
+    pb = _pb()
+    imgs = _items(64, 64, 4, seed=2)
+    tgt = _target(pb)
+    tgt = pb.FitParams(i0=tgt.i0, basis=tgt.basis,
+                       stats=pb.StainStats(p99=np.array([tgt.stats.p99[0], 0.0])))
+    _, errors, _ = _run(pb, imgs, pb.SamplePlan(), tgt)
+    assert all(isinstance(e, pb.DegenerateStainError) for e in errors)
+
+
+def test_batch_many_items_one_launch_per_148():
+    """A batch larger than one launch (148 items) keeps item order and results."""
+    pb = _pb()
+    base = _items(48, 64, 4, seed=9)
+    imgs = [base[k % 4] for k in range(300)]
+    tgt = _target(pb, 8)
+    out, errors, _ = _run(pb, imgs, pb.SamplePlan(), tgt)
+    assert all(e is None for e in errors)
+    for k in range(300):
+        assert np.array_equal(out[k], out[k % 4]), k
+    _, ref = _oracle_item(base[1], orc.Plan(), tgt)
+    assert np.array_equal(out[1], ref)

@@ -28,6 +28,10 @@ npix = src.numel() // 3
 w = orc.he_basis()
 rot = np.array([[0.58, 0.12], [0.74, 0.93], [0.33, 0.35]])
 rot /= np.linalg.norm(rot, axis=0)
+ref = torch.empty_like(src)
+pb.XformPlan([255.0] * 3, w, 0.0, [1.2, 0.85], np.array([[0.58, 0.12], [0.74, 0.93], [0.33, 0.35]])
+             / np.linalg.norm([[0.58, 0.12], [0.74, 0.93], [0.33, 0.35]], axis=0),
+             [250.0, 246.0, 240.0], "strict").run(src, ref, npix)
 for prec, cal in (("fast", False), ("exact", False), ("exact", True), ("strict", False)):
     plan = pb.XformPlan([255.0] * 3, w, 0.0, [1.2, 0.85], rot, [250.0, 246.0, 240.0], prec)
     if cal:
@@ -48,5 +52,8 @@ for prec, cal in (("fast", False), ("exact", False), ("exact", True), ("strict",
     ms = e0.elapsed_time(e1) / iters
     rep = plan.repair_count() if prec == "exact" else 0
     tag = prec + ("+cal" if cal else "")
+    diff = int((dst != ref).sum().item())
+    if prec != "fast" and diff:
+        print(f"MISMATCH {tag}: {diff} bytes differ from the fp64 path", flush=True)
     print(f"{tag:10s} npix={npix} {ms:.3f} ms  {npix / ms / 1e3:.1f} Mpx/s  "
           f"{6 * npix / ms / 1e6:.1f} GB/s  repaired={rep} ({rep / npix:.5%})", flush=True)
