@@ -170,11 +170,12 @@ typedef struct spcn_snmf_cfg {
 
 /* Batched fit_basis (src/stain_sep.py:239-336).  Problem p's sample is the
  * RGB8 pixels [offsets[p], offsets[p+1]) of `samples`, coded to OD through
- * luts[p] (3x256 fp64).  Writes the ordered basis (nprob x 6, row-major),
- * (or, when `od` is non-NULL, the fp64 OD columns od[c*total + i], c = 0..2,
- * in which case `samples`/`luts` are ignored) and writes the objective history (nprob x (max_outer+1)) and info (nprob x 4:
- * iterations, converged, warning flags bit0=no-convergence bit1=one-stain,
- * history length).  hscratch: 2*total fp64.  All pointers device.          */
+ * luts[p] (3x256 fp64) (or, when `od` is non-NULL, the fp64 OD columns
+ * od[c*total + i], c = 0..2, in which case `samples`/`luts` are ignored).
+ * Writes the ordered basis (nprob x 6, row-major), the objective history
+ * (nprob x (max_outer+1)) and info (nprob x 4: iterations, converged, warning
+ * flags bit0=no-convergence bit1=one-stain, history length).  hscratch is
+ * unused (kept for ABI stability; may be NULL).  All pointers device.      */
 int spcn_snmf_batched(const uint8_t* samples, const double* od, const int64_t* offsets,
                       int32_t nprob,
                       const double* luts, const spcn_snmf_cfg* cfg, double* hscratch,
@@ -226,9 +227,11 @@ int spcn_batch_params(int32_t nitems, const double* i0, const double* luts, cons
 
 /* Recolour every item (status 0 via the fast kernel, status 1 via the fp64
  * kernel, errors skipped).  off_host/off_dev: n+1 pixel offsets (multiples of
- * 16); fast_scalars_host/status_host: host copies of the blocks above.       */
+ * 16); fast_scalars/flut/strict_params: the device blocks spcn_batch_params
+ * wrote; status_host: host copy of its status output.  EXACT needs a
+ * workspace of spcn_xform_workspace_bytes(total pixels).                     */
 int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int64_t* off_host,
-                     const int64_t* off_dev, const void* fast_scalars_host,
+                     const int64_t* off_dev, const void* fast_scalars,
                      const int32_t* status_host, const int32_t* status_dev, const float* flut,
                      const void* strict_params, int32_t precision, void* workspace,
                      size_t workspace_bytes, void* stream);

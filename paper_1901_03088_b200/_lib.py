@@ -12,7 +12,7 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspcn.so")
+LIB_PATH = os.environ.get("SPCN_LIB_PATH") or os.path.join(_HERE, "libspcn.so")   # override: A/B tools
 
 SPCN_OK = 0
 SPCN_EINVAL = 1

@@ -229,9 +229,10 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
   cudaError_t e;
   if (head > 0 && (e = launch_xform_strict(src, dst, head, sp, st)) != cudaSuccess)
     return cuda_fail(e, "xform_head");
-  e = launch_xform_tma(mode, src + 3 * head, dst + 3 * head, body, fp, sp, count, items, cap, st);
+  e = launch_xform_main(mode, src + 3 * head, dst + 3 * head, body, fp, sp, count, items, cap, st);
   if (e != cudaSuccess) return cuda_fail(e, "xform_tma");
-  if (exact && (e = launch_xform_repair(dst + 3 * head, sp, count, items, cap, st)) != cudaSuccess)
+  if (exact && (e = launch_xform_repair(src + 3 * head, dst + 3 * head, body, sp, count, items, cap,
+                                        st)) != cudaSuccess)
     return cuda_fail(e, "xform_repair");
   const int64_t tail0 = head + body;
   if (tail0 < npix &&
@@ -387,7 +388,7 @@ int spcn_snmf_batched(const uint8_t* samples, const double* od, const int64_t* o
   if (!(cfg->rel_tol > 0.0)) return fail(SPCN_EINVAL, "rel_tol must be > 0");
   if (cfg->cluster < 1 || cfg->cluster > 8) return fail(SPCN_EINVAL, "cluster must be in [1, 8]");
   if (nprob == 0) return SPCN_OK;
-  if ((!od && (!samples || !luts)) || !offsets || !hscratch || !basis_out || !history_out || !info_out)
+  if ((!od && (!samples || !luts)) || !offsets || !basis_out || !history_out || !info_out)
     return fail(SPCN_EINVAL, "NULL argument");
   SnmfArgs a;
   a.lam = cfg->lam;
@@ -501,24 +502,23 @@ int spcn_batch_params(int32_t nitems, const double* i0, const double* luts, cons
 }
 
 int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int64_t* off_host,
-                     const int64_t* off_dev, const void* fast_scalars_host,
-                     const int32_t* status_host, const int32_t* status_dev, const float* flut,
-                     const void* strict_params, int32_t precision, void* workspace,
-                     size_t workspace_bytes, void* stream) {
+                     const int64_t* off_dev, const void* fast_scalars, const int32_t* status_host,
+                     const int32_t* status_dev, const float* flut, const void* strict_params,
+                     int32_t precision, void* workspace, size_t workspace_bytes, void* stream) {
   g_err.clear();
   if (nitems < 0) return fail(SPCN_EINVAL, "nitems must be >= 0");
   if (nitems == 0) return SPCN_OK;
-  if (!src || !dst || !off_host || !off_dev || !fast_scalars_host || !status_host || !status_dev ||
+  if (!src || !dst || !off_host || !off_dev || !fast_scalars || !status_host || !status_dev ||
       !flut || !strict_params)
     return fail(SPCN_EINVAL, "NULL argument");
   if (precision < 0 || precision > 2) return fail(SPCN_EINVAL, "unknown precision");
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const FastS* fs = static_cast<const FastS*>(fast_scalars_host);
+  const FastS* fs = static_cast<const FastS*>(fast_scalars);
   const StrictP* sps = static_cast<const StrictP*>(strict_params);
   const bool strict_all = precision == SPCN_PREC_STRICT;
   const bool exact = precision == SPCN_PREC_EXACT;
   int64_t max_pix = 0;
-  bool any_strict = false;
+  bool any_strict = false, any_fast = false;
   for (int i = 0; i < nitems; ++i) {
     const int64_t n = off_host[i + 1] - off_host[i];
     if (n < 0) return fail(SPCN_EINVAL, "offsets must be non-decreasing");
@@ -526,6 +526,7 @@ int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int
       return fail(SPCN_EINVAL, "item pixel offsets and sizes must be multiples of 16");
     max_pix = n > max_pix ? n : max_pix;
     any_strict = any_strict || status_host[i] == 1 || (strict_all && status_host[i] == 0);
+    any_fast = any_fast || status_host[i] == 0;
   }
   if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
     return fail(SPCN_EINVAL, "src/dst must be 16-byte aligned");
@@ -542,22 +543,13 @@ int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int
     if ((e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), st)) != cudaSuccess)
       return cuda_fail(e, "memset");
   }
-  if (!strict_all) {
-    static thread_local BatchArgs a;
-    for (int i0 = 0; i0 < nitems; i0 += kMaxBatch) {
-      const int n = nitems - i0 < kMaxBatch ? nitems - i0 : kMaxBatch;
-      a.n = n;
-      a.item0 = i0;
-      for (int i = 0; i <= n; ++i) a.off[i] = off_host[i0 + i];   // absolute pixel offsets
-      for (int i = 0; i < n; ++i) {
-        a.strict[i] = status_host[i0 + i] != 0 ? 1 : 0;
-        a.s[i] = fs[i0 + i];
-      }
-      e = launch_xform_batch(exact ? 0 : 1, src, dst, flut, sps, a, count, items, cap, st);
-      if (e != cudaSuccess) return cuda_fail(e, "xform_batch");
-    }
-    if (exact && (e = launch_repair_batch(dst, sps, off_dev, nitems, count, items, cap, st)) !=
-                     cudaSuccess)
+  if (!strict_all && any_fast) {
+    // one persistent launch over every fast-path item (status 0)
+    e = launch_xform_batch(exact ? 0 : 1, src, dst, nitems, off_dev, status_dev, fs, flut, count,
+                           items, cap, st);
+    if (e != cudaSuccess) return cuda_fail(e, "xform_batch");
+    if (exact && (e = launch_repair_batch(src, dst, sps, off_dev, status_dev, nitems, count, items,
+                                          cap, st)) != cudaSuccess)
       return cuda_fail(e, "repair_batch");
   }
   if (any_strict) {

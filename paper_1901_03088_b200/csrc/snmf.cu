@@ -140,8 +140,6 @@ __global__ void __launch_bounds__(kSnThreads) k_snmf(
         const double b1 = strict_dot3(w01, w11, w21, v0, v1, v2);
         double h0, h1;
         strict_nnls(b0, b1, g00, g01, g11, det, code_lam, 500, 1e-9, h0, h1);
-        hbuf[i] = h0;
-        hbuf[total + i] = h1;
         const double r0 = v0 - __fma_rn(w01, h1, __dmul_rn(w00, h0));
         const double r1 = v1 - __fma_rn(w11, h1, __dmul_rn(w10, h0));
         const double r2 = v2 - __fma_rn(w21, h1, __dmul_rn(w20, h0));
@@ -158,27 +156,7 @@ __global__ void __launch_bounds__(kSnThreads) k_snmf(
       return sh.tot[0] + lam * (sh.tot[1] + sh.tot[2]);
     };
 
-    // --- objective of a candidate basis with the current H
-    auto cand_objective = [&]() {
-      const double c00 = sh.cand[0], c01 = sh.cand[1], c10 = sh.cand[2], c11 = sh.cand[3],
-                   c20 = sh.cand[4], c21 = sh.cand[5];
-      double st[1] = {0.0};
-      for (int64_t i = lo + tid; i < hi; i += kSnThreads) {
-        double v0, v1, v2;
-        load_od(i, v0, v1, v2);
-        const double h0 = hbuf[i], h1 = hbuf[total + i];
-        const double r0 = v0 - __fma_rn(c01, h1, __dmul_rn(c00, h0));
-        const double r1 = v1 - __fma_rn(c11, h1, __dmul_rn(c10, h0));
-        const double r2 = v2 - __fma_rn(c21, h1, __dmul_rn(c20, h0));
-        st[0] += r0 * r0 + r1 * r1 + r2 * r2;
-      }
-      cta_reduce<1>(st, &sh.warp_part[0][0], sh.part[phase & 1]);
-      cluster_total(1);
-      return sh.tot[0];
-    };
-
     double f = hstep();
-    double sumh = sh.tot[1] + sh.tot[2];
     double row0 = sh.tot[1], row1 = sh.tot[2];
     double vht[3][2], hht[2][2];
     auto grab_stats = [&]() {
@@ -194,33 +172,42 @@ __global__ void __launch_bounds__(kSnThreads) k_snmf(
     double f_rec = f;
     const double floor_f = 1e-12 * (double)m;
     for (it = 1; it <= a.max_outer; ++it) {
-      // _w_step (src/stain_sep.py:221-235)
-      for (int j = 0; j < 2; ++j) {
-        const int k = 1 - j;
-        if (hht[j][j] <= 0.0) continue;
-        double u[3];
-        for (int c = 0; c < 3; ++c) {
-          u[c] = __dsub_rn(vht[c][j], __dmul_rn(sh.w[c * 2 + k], hht[k][j]));
-          u[c] = u[c] < 0.0 ? 0.0 : u[c];   // np.maximum(u, 0.0)
+      // _w_step (src/stain_sep.py:210-236).  The candidate's objective with H
+      // fixed follows from the sufficient statistics of the H-step pass:
+      // replacing column j by c = w_j + d changes ||V - WH||^2 by
+      // -2 d.(VH^T_j - W HH^T_j) + |d|^2 HH^T_jj (lam*sum(H) is unchanged),
+      // so no pass over the samples is needed.  f is the explicit objective of
+      // the current (W, H); each accepted candidate's value carries over to the
+      // next column's test, as in the reference.
+      if (tid == 0) {
+        double* w = sh.w;
+        for (int j = 0; j < 2; ++j) {
+          const int k = 1 - j;
+          if (hht[j][j] <= 0.0) continue;
+          double u[3];
+          for (int c = 0; c < 3; ++c) {
+            u[c] = __dsub_rn(vht[c][j], __dmul_rn(w[c * 2 + k], hht[k][j]));
+            u[c] = u[c] < 0.0 ? 0.0 : u[c];   // np.maximum(u, 0.0)
+          }
+          const double nrm = sqrt(fma_dot3(u[0], u[1], u[2], u[0], u[1], u[2]));
+          if (nrm <= 1e-15) continue;
+          double cand[3], dg = 0.0, dd = 0.0;
+          for (int c = 0; c < 3; ++c) {
+            cand[c] = __ddiv_rn(u[c], nrm);
+            const double d = cand[c] - w[c * 2 + j];
+            const double g = vht[c][j] - (w[c * 2] * hht[0][j] + w[c * 2 + 1] * hht[1][j]);
+            dg += d * g;
+            dd += d * d;
+          }
+          const double ft = f + (dd * hht[j][j] - 2.0 * dg);
+          if (ft <= f) {
+            for (int c = 0; c < 3; ++c) w[c * 2 + j] = cand[c];
+            f = ft;
+          }
         }
-        const double nrm = sqrt(fma_dot3(u[0], u[1], u[2], u[0], u[1], u[2]));
-        if (nrm <= 1e-15) continue;
-        __syncthreads();
-        if (tid < 6) {
-          const int c = tid >> 1, jj = tid & 1;
-          sh.cand[tid] = (jj == j) ? __ddiv_rn(u[c], nrm) : sh.w[tid];
-        }
-        __syncthreads();
-        const double ft = cand_objective() + lam * sumh;
-        if (ft <= f) {
-          __syncthreads();
-          if (tid < 6) sh.w[tid] = sh.cand[tid];
-          f = ft;
-        }
-        __syncthreads();
       }
+      __syncthreads();
       f = hstep();
-      sumh = sh.tot[1] + sh.tot[2];
       row0 = sh.tot[1];
       row1 = sh.tot[2];
       grab_stats();

@@ -6,23 +6,26 @@
 // (src/normalize.py:115-151) → inverse_beer_lambert (src/optics.py:97-110).
 //
 // Kernels:
-//   k_xform_tma<MODE>   persistent, warp-specialised: one producer warp streams
-//                       12 KiB tiles (4096 px) into a 4-stage shared-memory ring
-//                       with 1-D TMA bulk copies; 8 compute warps run the fp32
-//                       path two pixels at a time (FFMA2/FMUL2), look OD up in
-//                       a 16-way replicated shared-memory table addressed with
-//                       one PRMT per channel, pack output bytes with PRMT and
-//                       store with 128-bit STG.  MODE: 0 = EXACT with the
-//                       analytic per-pixel bound, 1 = FAST, 2 = EXACT with a
-//                       calibrated constant bound.  EXACT appends uncertified
-//                       pixels to a repair list.
-//   k_xform_repair      fp64 reference-order recompute of the listed pixels.
+//   k_xform_warp<MODE>  persistent; every warp owns a ring of shared-memory
+//                       slots fed and drained by 1-D TMA bulk copies
+//                       (cp.async.bulk G2S / S2G, mbarrier completion) and
+//                       recolours 16 px per lane per 512-px sub-slice in place:
+//                       fp32 path two pixels at a time (FFMA2/FMUL2), OD from a
+//                       replicated shared-memory table addressed with one PRMT
+//                       per channel, output bytes packed with PRMT.  MODE: 0 =
+//                       EXACT with the analytic per-pixel bound, 1 = FAST, 2 =
+//                       EXACT with a calibrated constant bound, 3 = identity
+//                       (memory-path ceiling).  EXACT appends uncertified pixels
+//                       to a repair list.
+//   k_xform_repair      fp64 reference-order recompute of the listed pixels (or
+//                       of every pixel if the list overflowed).
 //   k_xform_strict      fp64 reference-order path for every pixel (STRICT mode,
 //                       head/tail pixels, unaligned buffers).
 //   k_calibrate         runs the fast path and the fp64 path on all 2^24 RGB
 //                       colours and returns the largest relative error of the
 //                       fast path: a certification bound valid by exhaustion.
 #include "launch_count.h"
+#include "recolor.cuh"
 #include "spcn_device.cuh"
 #include "xform.h"
 
@@ -31,57 +34,7 @@
 
 namespace spcn {
 
-// Kernel shape: CW compute warps (+1 producer warp), 16 px per thread, and an
-// OD table replicated REP times so a warp's 32 lookups hit distinct banks:
-//   REP 16: 64 KiB, rows of 256 B = [ch0 x16 | ch1 x16 | ch2 x16 | pad], copy
-//           (lane&15) of channel c at x*256 + c*64 + (lane&15)*4 (<= 2-way
-//           bank conflicts), two CTAs per SM;
-//   REP 32: 128 KiB, region 0 rows [ch0 x32 | ch1 x32], region 1 (+64 KiB)
-//           rows [ch2 x32 | pad], copy `lane` at x*256 + ... + lane*4
-//           (conflict-free), one CTA per SM.
-// Either way ONE PRMT of (input word, per-lane constant) forms the address:
-// byte 0 = the constant's low byte, byte 1 = the pixel byte x, byte 2 = the
-// constant's region byte.
-// STORE 0: each thread stores its 48 output bytes with 3 STG.128.  STORE 1:
-// the output is written back in place into the input stage and each warp
-// issues one 1-D TMA bulk store (cp.async.bulk S2G) of its 1536-byte slice.
-// BLK = CTAs per SM the shared-memory budget is sized for.
-template <int CW, int REP, int STORE, int BLK>
-struct XCfg {
-  static constexpr int kComputeWarps = CW;
-  static constexpr int kThreads = 32 * (CW + 1);
-  static constexpr int kTilePx = CW * 32 * 16;
-  static constexpr int kTileBytes = 3 * kTilePx;
-  static constexpr int kLutBytes = REP == 32 ? 2 * 65536 : 65536;
-  static constexpr int kBudget = BLK == 1 ? 224 * 1024 : 112 * 1024;
-  static constexpr int kStages = (kBudget - kLutBytes) / kTileBytes;
-  static constexpr size_t kSmem = kLutBytes + kStages * kTileBytes + 2 * kStages * 8;
-  static_assert(kStages >= 3, "need at least three stages");
-};
-
-// the production shape (see DESIGN.md §3 and profiles/)
-#ifndef SPCN_XFORM_CW
-#define SPCN_XFORM_CW 16
-#endif
-#ifndef SPCN_XFORM_REP
-#define SPCN_XFORM_REP 32
-#endif
-#ifndef SPCN_XFORM_STORE
-#define SPCN_XFORM_STORE 1
-#endif
-#ifndef SPCN_XFORM_BLK
-#define SPCN_XFORM_BLK 1
-#endif
-using Prod = XCfg<SPCN_XFORM_CW, SPCN_XFORM_REP, SPCN_XFORM_STORE, SPCN_XFORM_BLK>;
-constexpr int kTilePx = Prod::kTilePx;
-
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
-
-struct RepairList {
-  unsigned long long* count;   // device counter
-  unsigned long long* items;   // (pixel index << 24) | rgb
-  unsigned long long cap;
-};
 
 struct ConstLut {              // fp64 table read from kernel parameters
   const StrictP* p;
@@ -91,263 +44,6 @@ struct SmemLut {
   const double* t;
   __device__ double operator()(int c, uint32_t i) const { return t[c * 256 + i]; }
 };
-
-// Rare path (repair-list overflow): kept out of line so the hot loop stays small.
-__device__ __noinline__ uint32_t strict_rgb(const StrictP& sp, uint32_t rgb) {
-  return strict_pixel(sp, ConstLut{&sp}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
-}
-
-// (a ^ b) | c as a single LOP3 (opaque to the optimiser, which would otherwise
-// turn the XOR into compare-and-select chains).
-__device__ __forceinline__ uint32_t lop3_xor_or(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("lop3.b32 %0, %1, %2, %3, 0xBE;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-
-__device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int idx) {
-  return (w[idx >> 2] >> (8 * (idx & 3))) & 0xffu;
-}
-
-// OD of input byte `idx` (0..47) of the thread's 48-byte block, channel c.
-__device__ __forceinline__ float od_lookup(const uint8_t* lut, const uint32_t* w, int idx,
-                                           uint32_t lc) {
-  const uint32_t sel = 0x7604u | ((uint32_t)(idx & 3) << 4);
-  const uint32_t addr = __byte_perm(w[idx >> 2], lc, sel);  // region*64K + x*256 + low byte
-  return *reinterpret_cast<const float*>(lut + addr);
-}
-
-// Recolor two pixels (k, k+1) of the block; writes their 6 output "bytes"
-// (low byte of each word) to ob[3k .. 3k+5].  EXACT: returns non-zero when any
-// of the pair's six roundings is not certified (r_lo != r_hi); both pixels of
-// such a pair go to the fp64 repair list.
-template <int MODE>
-__device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t* lut,
-                                                 const uint32_t* w, int k, const uint32_t* lc,
-                                                 uint32_t* ob) {
-  const int a = 3 * k, b = 3 * k + 3;
-  const float2 v0 = make_float2(od_lookup(lut, w, a, lc[0]), od_lookup(lut, w, b, lc[0]));
-  const float2 v1 = make_float2(od_lookup(lut, w, a + 1, lc[1]), od_lookup(lut, w, b + 1, lc[1]));
-  const float2 v2 = make_float2(od_lookup(lut, w, a + 2, lc[2]), od_lookup(lut, w, b + 2, lc[2]));
-  const FastPair fq = fast_pair(fp, v0, v1, v2);
-  const float e[3][2] = {{fq.e0.x, fq.e0.y}, {fq.e1.x, fq.e1.y}, {fq.e2.x, fq.e2.y}};
-  if (MODE == 1) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const float2 pw = make_float2(ex2_approx(e[c][0]), ex2_approx(e[c][1]));
-      const float2 r = __ffma2_rn(bc2(fp.i0t[c]), pw, bc2(kMagic));
-      ob[a + c] = __float_as_uint(r.x);
-      ob[b + c] = __float_as_uint(r.y);
-    }
-    return 0u;
-  }
-  float2 alpha = bc2(0.f);
-  if (MODE == 0) alpha = __ffma2_rn(bc2(fp.a1), fq.T, bc2(fp.a0));
-  uint32_t bad = 0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const float pa = ex2_approx(e[c][0]), pb = ex2_approx(e[c][1]);
-    float2 Ia, Ib;
-    if (MODE == 0) {
-      Ia = cert_interval(fp.i0t[c], alpha.x);
-      Ib = cert_interval(fp.i0t[c], alpha.y);
-    } else {
-      Ia = Ib = make_float2(fp.ilo[c], fp.ihi[c]);
-    }
-    const float2 ra = __ffma2_rn(Ia, bc2(pa), bc2(kMagic));
-    const float2 rb = __ffma2_rn(Ib, bc2(pb), bc2(kMagic));
-    ob[a + c] = __float_as_uint(ra.y);
-    ob[b + c] = __float_as_uint(rb.y);
-    bad = lop3_xor_or(__float_as_uint(ra.y), __float_as_uint(ra.x), bad);   // one LOP3 each
-    bad = lop3_xor_or(__float_as_uint(rb.y), __float_as_uint(rb.x), bad);
-  }
-  return bad;
-}
-
-__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
-}
-
-template <int MODE, int CW, int REP, int STORE, int BLK>
-__global__ void __launch_bounds__(XCfg<CW, REP, STORE, BLK>::kThreads, BLK)
-    k_xform_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
-                const __grid_constant__ FastP fp, const __grid_constant__ StrictP sp,
-                RepairList rl) {
-  using C = XCfg<CW, REP, STORE, BLK>;
-  constexpr int kThreads = C::kThreads, kTilePx = C::kTilePx, kTileBytes = C::kTileBytes;
-  constexpr int kStages = C::kStages, kComputeWarps = C::kComputeWarps;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const uint8_t* lut = smem;
-  uint8_t* stages = smem + C::kLutBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kTileBytes);
-  uint64_t* empty = full + kStages;
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int64_t ntiles = (npix + kTilePx - 1) / kTilePx;
-
-  if (REP == 16) {
-    for (int i = tid; i < 256 * 48; i += kThreads) {
-      const int x = i / 48, rem = i - 48 * (i / 48), c = rem >> 4, r = rem & 15;
-      *reinterpret_cast<float*>(smem + x * 256 + c * 64 + r * 4) = fp.lut[c][x];
-    }
-  } else {
-    for (int i = tid; i < 256 * 96; i += kThreads) {
-      const int x = i / 96, rem = i - 96 * (i / 96), c = rem >> 5, r = rem & 31;
-      const int off = (c == 2 ? 65536 : 0) + x * 256 + (c == 1 ? 128 : 0) + r * 4;
-      *reinterpret_cast<float*>(smem + off) = fp.lut[c][x];
-    }
-  }
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kComputeWarps);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  if (warp == kComputeWarps) {
-    // ---------------- producer warp: TMA bulk loads into the stage ring
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int i = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-        const int s = i % kStages;
-        if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-        const int64_t n = min64(kTilePx, npix - t * kTilePx);
-        const uint32_t bytes = static_cast<uint32_t>(3 * n);
-        mbar_expect_tx(&full[s], bytes);
-        bulk_g2s(stages + s * kTileBytes, src + 3 * t * kTilePx, bytes, &full[s], pol);
-      }
-    }
-    return;
-  }
-
-  // ---------------- compute warps
-  const int ct = tid;                        // 0 .. 32*CW-1
-  uint32_t lc[3];
-  if (REP == 16) {
-    const uint32_t lrep = (uint32_t)(lane & 15) * 4;
-    lc[0] = lrep; lc[1] = 64u + lrep; lc[2] = 128u + lrep;
-  } else {
-    const uint32_t lrep = (uint32_t)lane * 4;
-    lc[0] = lrep; lc[1] = 128u + lrep; lc[2] = 0x10000u | lrep;
-  }
-  int i = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-    const int s = i % kStages;
-    mbar_wait(&full[s], (i / kStages) & 1);
-    const int64_t tile0 = t * kTilePx;
-    const int64_t n = min64(kTilePx, npix - tile0);
-    const bool valid = 16 * ct < n;
-    uint8_t* slot = stages + s * kTileBytes + 48 * ct;
-    uint32_t w[12];
-    if (valid) {
-      const uint4* q = reinterpret_cast<const uint4*>(slot);
-      const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
-      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-      w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-      w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
-    }
-    uint32_t ob[48], o[12];
-    uint32_t badpairs = 0;  // EXACT: bit q = pair q (pixels 2q, 2q+1) not certified
-    if (valid) {
-      if (MODE == 3) {    // identity (memory-path ceiling measurement only)
-#pragma unroll
-        for (int j = 0; j < 12; ++j) o[j] = w[j];
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * q, lc, ob);
-          if (MODE == 0 || MODE == 2) badpairs |= (bad != 0u ? 1u : 0u) << q;
-          // pack output words as soon as their 4 bytes exist (short live ranges)
-#pragma unroll
-          for (int j = 0; j < 12; ++j)
-            if (4 * j + 3 >= 6 * q && 4 * j + 3 < 6 * q + 6)
-              o[j] = pack4(ob[4 * j], ob[4 * j + 1], ob[4 * j + 2], ob[4 * j + 3]);
-        }
-      }
-    }
-    if (STORE == 0) {
-      // Release the stage once every loaded word has been consumed: the arrive
-      // does not wait for in-flight LDS, and the next TMA write into this stage
-      // is an async-proxy write (cross-proxy WAR), hence also the fence.
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (valid) {
-        uint4* d = reinterpret_cast<uint4*>(dst + 3 * (tile0 + 16 * ct));
-        d[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        d[1] = make_uint4(o[4], o[5], o[6], o[7]);
-        d[2] = make_uint4(o[8], o[9], o[10], o[11]);
-      }
-    } else if (valid) {
-      // in-place staging: the output overwrites the thread's own input bytes
-      uint4* d = reinterpret_cast<uint4*>(slot);
-      d[0] = make_uint4(o[0], o[1], o[2], o[3]);
-      d[1] = make_uint4(o[4], o[5], o[6], o[7]);
-      d[2] = make_uint4(o[8], o[9], o[10], o[11]);
-    }
-    if (MODE == 0 || MODE == 2) {
-      // warp-aggregated append of uncertified pixels to the repair list
-      uint32_t badmask = 0;   // bit k = pixel k
-      if (badpairs) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) badmask |= ((badpairs >> q) & 1u) * (3u << (2 * q));
-      }
-      if (__any_sync(0xffffffffu, badmask != 0u)) {
-        const uint32_t cnt = __popc(badmask);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl += y;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned long long base = 0;
-        if (lane == 31) base = atomicAdd(rl.count, (unsigned long long)total);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        unsigned long long item = base + incl - cnt;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          if (!((badmask >> k) & 1u)) continue;
-          const uint32_t rgb = byte_of(w, 3 * k) | (byte_of(w, 3 * k + 1) << 8) |
-                               (byte_of(w, 3 * k + 2) << 16);
-          const int64_t gp = tile0 + 16 * ct + k;
-          if (item < rl.cap) {
-            rl.items[item] = (static_cast<unsigned long long>(gp) << 24) | rgb;
-          } else {  // list overflow: recompute in fp64 now (ordered after our own store)
-            const uint32_t px = strict_rgb(sp, rgb);
-            uint8_t* o8 = STORE == 0 ? dst + 3 * gp : slot + 3 * k;
-            o8[0] = px & 255u;
-            o8[1] = (px >> 8) & 255u;
-            o8[2] = (px >> 16) & 255u;
-          }
-          ++item;
-        }
-      }
-    }
-    if (STORE == 1) {
-      // one 1-D TMA bulk store per warp of its contiguous 1536-byte slice, issued
-      // from the stage itself; the stage is released once the PREVIOUS tile's
-      // store has finished reading shared memory (delayed release).
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        const int64_t wn = min64(512, n - (int64_t)warp * 512);
-        if (wn > 0) {
-          bulk_s2g(dst + 3 * (tile0 + (int64_t)warp * 512), stages + s * kTileBytes + warp * 1536,
-                   static_cast<uint32_t>(3 * wn));
-        }
-        bulk_commit();
-        bulk_wait_read<1>();
-        if (i > 0) mbar_arrive(&empty[(i - 1) % kStages]);
-      }
-    }
-  }
-  if (STORE == 1 && lane == 0) bulk_wait_all();
-}
 
 // ---------------------------------------------------------------------------
 // k_xform_warp: the same per-thread pipeline, but every warp owns its own
@@ -364,10 +60,9 @@ struct WCfg {
   static constexpr int kThreads = 32 * CW;
   static constexpr int kSlicePx = 512 * NSUB;
   static constexpr int kSlotBytes = 3 * kSlicePx;
-  static constexpr int kLutBytes = REP == 32 ? 2 * 65536 : 65536;
+  static constexpr int kLutBytes = LutLayout<REP>::kBytes;
   static constexpr size_t kSmem = kLutBytes + (size_t)CW * NSW * kSlotBytes + CW * NSW * 8;
   static_assert(kSmem <= (BLK == 1 ? 227 * 1024 : 113 * 1024), "shared memory budget");
-  static_assert(REP == 16 || REP == 32, "table layouts exist for 16 and 32 replicas");
 };
 
 template <int MODE, int CW, int REP, int NSW, int BLK, int NSUB>
@@ -384,18 +79,7 @@ __global__ void __launch_bounds__(32 * CW, BLK)
   uint64_t* mybar =
       reinterpret_cast<uint64_t*>(smem + C::kLutBytes + (size_t)CW * NSW * kSlotBytes) + warp * NSW;
 
-  if (REP == 16) {
-    for (int i = tid; i < 256 * 48; i += C::kThreads) {
-      const int x = i / 48, rem = i - 48 * (i / 48), c = rem >> 4, r = rem & 15;
-      *reinterpret_cast<float*>(smem + x * 256 + c * 64 + r * 4) = fp.lut[c][x];
-    }
-  } else {
-    for (int i = tid; i < 256 * 96; i += C::kThreads) {
-      const int x = i / 96, rem = i - 96 * (i / 96), c = rem >> 5, r = rem & 31;
-      const int off = (c == 2 ? 65536 : 0) + x * 256 + (c == 1 ? 128 : 0) + r * 4;
-      *reinterpret_cast<float*>(smem + off) = fp.lut[c][x];
-    }
-  }
+  LutLayout<REP>::fill(smem, &fp.lut[0][0], tid, C::kThreads);
   if (lane == 0) {
     for (int s = 0; s < NSW; ++s) mbar_init(&mybar[s], 1);
     mbar_fence_init();
@@ -403,13 +87,7 @@ __global__ void __launch_bounds__(32 * CW, BLK)
   __syncthreads();
 
   uint32_t lc[3];
-  if (REP == 16) {
-    const uint32_t lrep = (uint32_t)(lane & 15) * 4;
-    lc[0] = lrep; lc[1] = 64u + lrep; lc[2] = 128u + lrep;
-  } else {
-    const uint32_t lrep = (uint32_t)lane * 4;
-    lc[0] = lrep; lc[1] = 128u + lrep; lc[2] = 0x10000u | lrep;
-  }
+  LutLayout<REP>::lane_consts(lane, lc);
   const int64_t nslices = (npix + kSlicePx - 1) / kSlicePx;
   const int64_t gw = (int64_t)blockIdx.x * CW + warp, GW = (int64_t)gridDim.x * CW;
   uint64_t pol = 0;
@@ -434,72 +112,9 @@ __global__ void __launch_bounds__(32 * CW, BLK)
     const int n = (int)min64(kSlicePx, npix - j * kSlicePx);
     uint8_t* sbase = myslots + s * kSlotBytes;
 #pragma unroll
-    for (int u = 0; u < NSUB; ++u) {
-      const bool valid = u * 512 + 16 * lane < n;
-      uint8_t* slot = sbase + u * 1536 + 48 * lane;
-      uint32_t w[12], ob[48], o[12];
-      uint32_t badpairs = 0;
-      if (valid) {
-        const uint4* q = reinterpret_cast<const uint4*>(slot);
-        const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
-        w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-        w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-        w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
-        if (MODE == 3) {
-#pragma unroll
-          for (int t = 0; t < 12; ++t) o[t] = w[t];
-        } else {
-#pragma unroll
-          for (int qq = 0; qq < 8; ++qq) {
-            const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * qq, lc, ob);
-            if (MODE == 0 || MODE == 2) badpairs |= (bad != 0u ? 1u : 0u) << qq;
-#pragma unroll
-            for (int t = 0; t < 12; ++t)
-              if (4 * t + 3 >= 6 * qq && 4 * t + 3 < 6 * qq + 6)
-                o[t] = pack4(ob[4 * t], ob[4 * t + 1], ob[4 * t + 2], ob[4 * t + 3]);
-          }
-        }
-        uint4* d = reinterpret_cast<uint4*>(slot);
-        d[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        d[1] = make_uint4(o[4], o[5], o[6], o[7]);
-        d[2] = make_uint4(o[8], o[9], o[10], o[11]);
-      }
-      if (MODE == 0 || MODE == 2) {
-        if (__any_sync(0xffffffffu, badpairs != 0u)) {
-          uint32_t badmask = 0;
-#pragma unroll
-          for (int qq = 0; qq < 8; ++qq) badmask |= ((badpairs >> qq) & 1u) * (3u << (2 * qq));
-          const uint32_t cnt = __popc(badmask);
-          uint32_t incl = cnt;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += y;
-          }
-          const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-          unsigned long long base = 0;
-          if (lane == 31) base = atomicAdd(rl.count, (unsigned long long)total);
-          base = __shfl_sync(0xffffffffu, base, 31);
-          unsigned long long item = base + incl - cnt;
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) {
-            if (!((badmask >> kk) & 1u)) continue;
-            const uint32_t rgb = byte_of(w, 3 * kk) | (byte_of(w, 3 * kk + 1) << 8) |
-                                 (byte_of(w, 3 * kk + 2) << 16);
-            const int64_t gp = j * kSlicePx + u * 512 + 16 * lane + kk;
-            if (item < rl.cap) {
-              rl.items[item] = (static_cast<unsigned long long>(gp) << 24) | rgb;
-            } else {  // list overflow: fp64 recompute patched into the slot before the store
-              const uint32_t px = strict_rgb(sp, rgb);
-              slot[3 * kk] = px & 255u;
-              slot[3 * kk + 1] = (px >> 8) & 255u;
-              slot[3 * kk + 2] = (px >> 16) & 255u;
-            }
-            ++item;
-          }
-        }
-      }
-    }
+    for (int u = 0; u < NSUB; ++u)
+      recolor_block<MODE>(fp, lut, lc, sbase + u * 1536 + 48 * lane, u * 512 + 16 * lane < n,
+                          j * kSlicePx + u * 512 + 16 * lane, rl, lane);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -514,10 +129,25 @@ __global__ void __launch_bounds__(32 * CW, BLK)
   if (lane == 0) bulk_wait_all();
 }
 
-__global__ void __launch_bounds__(256) k_xform_repair(uint8_t* __restrict__ dst,
+// fp64 recompute of the listed pixels; if the list overflowed (count > cap)
+// every pixel of the body is recomputed instead.
+__global__ void __launch_bounds__(256) k_xform_repair(const uint8_t* __restrict__ src,
+                                                      uint8_t* __restrict__ dst, int64_t npix,
                                                       const __grid_constant__ StrictP sp,
                                                       RepairList rl) {
-  const unsigned long long n = min(*rl.count, rl.cap);
+  const unsigned long long n = *rl.count;
+  if (n > rl.cap) {
+    __shared__ double lut[3 * 256];
+    for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < npix; i += 256ll * gridDim.x) {
+      const uint32_t out = strict_pixel(sp, SmemLut{lut}, src[3 * i], src[3 * i + 1], src[3 * i + 2]);
+      dst[3 * i] = out & 255u;
+      dst[3 * i + 1] = (out >> 8) & 255u;
+      dst[3 * i + 2] = (out >> 16) & 255u;
+    }
+    return;
+  }
   for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n;
        i += 256ull * gridDim.x) {
     const unsigned long long it = rl.items[i];
@@ -602,7 +232,7 @@ static int g_sm_count = 0;
 using XformFn = void (*)(const uint8_t*, uint8_t*, int64_t, FastP, StrictP, RepairList);
 
 struct Shape {
-  int cw, rep, store, blk, threads, tile_px, blocks_per_sm;   // store 2 = per-warp rings
+  int cw, rep, nsub, blk, threads, tile_px, blocks_per_sm;
   size_t smem;
   XformFn fn[4];
 };
@@ -610,27 +240,19 @@ struct Shape {
 template <int CW, int REP, int NSW, int BLK, int NSUB>
 Shape make_wshape() {
   using C = WCfg<CW, REP, NSW, BLK, NSUB>;
-  return Shape{CW, REP, 1 + NSUB, BLK, C::kThreads, CW * C::kSlicePx, 0, C::kSmem,
+  return Shape{CW, REP, NSUB, BLK, C::kThreads, CW * C::kSlicePx, 0, C::kSmem,
                {k_xform_warp<0, CW, REP, NSW, BLK, NSUB>, k_xform_warp<1, CW, REP, NSW, BLK, NSUB>,
                 k_xform_warp<2, CW, REP, NSW, BLK, NSUB>,
                 k_xform_warp<3, CW, REP, NSW, BLK, NSUB>}};
 }
 
-template <int CW, int REP, int STORE, int BLK>
-Shape make_shape() {
-  using C = XCfg<CW, REP, STORE, BLK>;
-  return Shape{CW, REP, STORE, BLK, C::kThreads, C::kTilePx, 0, C::kSmem,
-               {k_xform_tma<0, CW, REP, STORE, BLK>, k_xform_tma<1, CW, REP, STORE, BLK>,
-                k_xform_tma<2, CW, REP, STORE, BLK>, k_xform_tma<3, CW, REP, STORE, BLK>}};
-}
-
-// Compiled shapes; SPCN_XFORM_SHAPE="CWxREPxSTORExBLK" selects one
-// (experiments), the default is the production shape Prod.
+// Compiled shapes; SPCN_XFORM_SHAPE="CWxREPxNSUBxBLK" selects one
+// (experiments); the first entry is the production shape.
 // SPCN_XFORM_IDENTITY=1 makes the kernel copy input to output (memory-path
 // ceiling measurement only).
 static Shape g_shapes[] = {
     make_wshape<16, 16, 3, 1, 2>(),   // production: per-warp rings of 2x512-px slots
-    make_wshape<16, 32, 4, 1, 1>(), make_shape<16, 32, 1, 1>(),
+    make_wshape<16, 32, 4, 1, 1>(),
     make_wshape<16, 16, 2, 1, 3>(), make_wshape<12, 16, 3, 1, 3>(), make_wshape<16, 16, 4, 1, 1>(),
     make_wshape<8, 16, 2, 2, 2>(), make_wshape<8, 16, 3, 2, 1>()};
 static Shape* g_shape = nullptr;
@@ -645,10 +267,10 @@ cudaError_t xform_setup_device() {
   if (e != cudaSuccess) return e;
   Shape* pick = &g_shapes[0];
   if (const char* env = getenv("SPCN_XFORM_SHAPE")) {
-    int cw = 0, rep = 0, store = 0, blk = 0;
-    if (sscanf(env, "%dx%dx%dx%d", &cw, &rep, &store, &blk) == 4)
+    int cw = 0, rep = 0, nsub = 0, blk = 0;
+    if (sscanf(env, "%dx%dx%dx%d", &cw, &rep, &nsub, &blk) == 4)
       for (auto& s : g_shapes)
-        if (s.cw == cw && s.rep == rep && s.store == store && s.blk == blk) pick = &s;
+        if (s.cw == cw && s.rep == rep && s.nsub == nsub && s.blk == blk) pick = &s;
   }
   if (const char* env = getenv("SPCN_XFORM_IDENTITY")) g_identity = env[0] == '1';
   for (auto fn : pick->fn) {
@@ -663,7 +285,7 @@ cudaError_t xform_setup_device() {
   return cudaSuccess;
 }
 
-cudaError_t launch_xform_tma(int mode, const uint8_t* src, uint8_t* dst, int64_t npix,
+cudaError_t launch_xform_main(int mode, const uint8_t* src, uint8_t* dst, int64_t npix,
                              const FastP& fp, const StrictP& sp, unsigned long long* count,
                              unsigned long long* items, unsigned long long cap,
                              cudaStream_t st) {
@@ -680,19 +302,18 @@ cudaError_t launch_xform_tma(int mode, const uint8_t* src, uint8_t* dst, int64_t
 const char* xform_shape_name() {
   static char buf[96];
   if (xform_setup_device() != cudaSuccess || !g_shape) return "unavailable";
-  snprintf(buf, sizeof(buf), "%d compute warps, LUT x%d, %s stores, %d CTA/SM, %d px/tile",
-           g_shape->cw, g_shape->rep, g_shape->store ? "TMA" : "STG.128",
-           g_shape->blocks_per_sm, g_shape->tile_px);
+  snprintf(buf, sizeof(buf), "k_xform_warp: %d warps/CTA, LUT x%d, %d x 512-px sub-slices/slot, "
+           "%d CTA/SM", g_shape->cw, g_shape->rep, g_shape->nsub, g_shape->blocks_per_sm);
   return buf;
 }
 
-cudaError_t launch_xform_repair(uint8_t* dst, const StrictP& sp, unsigned long long* count,
-                                unsigned long long* items, unsigned long long cap,
-                                cudaStream_t st) {
+cudaError_t launch_xform_repair(const uint8_t* src, uint8_t* dst, int64_t npix, const StrictP& sp,
+                                unsigned long long* count, unsigned long long* items,
+                                unsigned long long cap, cudaStream_t st) {
   cudaError_t e = xform_setup_device();
   if (e != cudaSuccess) return e;
   RepairList rl{count, items, cap};
-  k_xform_repair<<<g_sm_count * 4, 256, 0, st>>>(dst, sp, rl);
+  k_xform_repair<<<g_sm_count * 4, 256, 0, st>>>(src, dst, npix, sp, rl);
   return launched();
 }
 
@@ -715,6 +336,6 @@ cudaError_t launch_calibrate(const FastP& fp, const StrictP& sp, unsigned int* m
   return launched();
 }
 
-int xform_tile_pixels() { return g_shape ? g_shape->tile_px : kTilePx; }
+int xform_tile_pixels() { return g_shape ? g_shape->tile_px : 16 * 512 * 2; }
 
 }  // namespace spcn

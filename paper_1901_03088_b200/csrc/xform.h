@@ -6,12 +6,12 @@
 
 namespace spcn {
 cudaError_t xform_setup_device();
-cudaError_t launch_xform_tma(int mode, const uint8_t* src, uint8_t* dst, int64_t npix,
-                             const FastP& fp, const StrictP& sp, unsigned long long* count,
-                             unsigned long long* items, unsigned long long cap, cudaStream_t st);
-cudaError_t launch_xform_repair(uint8_t* dst, const StrictP& sp, unsigned long long* count,
-                                unsigned long long* items, unsigned long long cap,
-                                cudaStream_t st);
+cudaError_t launch_xform_main(int mode, const uint8_t* src, uint8_t* dst, int64_t npix,
+                              const FastP& fp, const StrictP& sp, unsigned long long* count,
+                              unsigned long long* items, unsigned long long cap, cudaStream_t st);
+cudaError_t launch_xform_repair(const uint8_t* src, uint8_t* dst, int64_t npix, const StrictP& sp,
+                                unsigned long long* count, unsigned long long* items,
+                                unsigned long long cap, cudaStream_t st);
 cudaError_t launch_xform_strict(const uint8_t* src, uint8_t* dst, int64_t npix,
                                 const StrictP& sp, cudaStream_t st);
 cudaError_t launch_code_densities(const double* od, double* h, int64_t n, const StrictP& sp,

@@ -70,7 +70,6 @@ def snmf_batched(samples, offsets, luts, cfg, cluster: int = 1, od=None) -> Batc
     nprob = offsets.numel() - 1
     total = (od.shape[1] if od is not None else samples.numel() // 3)
     dev = offsets.device
-    h = t.empty(2 * max(total, 1), dtype=t.float64, device=dev)
     basis = t.empty((nprob, 6), dtype=t.float64, device=dev)
     hist = t.zeros((nprob, cfg.max_outer_iters + 1), dtype=t.float64, device=dev)
     info = t.zeros((nprob, 4), dtype=t.int32, device=dev)
@@ -78,7 +77,7 @@ def snmf_batched(samples, offsets, luts, cfg, cluster: int = 1, od=None) -> Batc
     _lib.check(L.spcn_snmf_batched(
         _lib.ptr(samples) if samples is not None else None,
         _lib.ptr(od) if od is not None else None, _lib.ptr(offsets), nprob,
-        _lib.ptr(luts) if luts is not None else None, ctypes.byref(c), _lib.ptr(h), total,
+        _lib.ptr(luts) if luts is not None else None, ctypes.byref(c), None, total,
         _lib.ptr(basis), _lib.ptr(hist), _lib.ptr(info), _lib.stream_handle()), "snmf_batched")
     return BatchFit(basis.reshape(nprob, 3, 2), hist, info)
 
