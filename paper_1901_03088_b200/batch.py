@@ -64,6 +64,9 @@ class BatchFit:
     count: np.ndarray   # (n,) sampled pixels
     status: np.ndarray  # (n,) 0 = ok, <0 = -SPCN_E* error code
     provenance: dict
+    iterations: np.ndarray = None   # (n,) SNMF outer iterations (SnmfFit.iterations)
+    converged: np.ndarray = None    # (n,) SnmfFit.converged
+    warn_flags: np.ndarray = None   # (n,) bit0 no convergence, bit1 one stain (warnings)
 
     def error(self, i):
         st = int(self.status[i])
@@ -187,8 +190,10 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
     absent_h = absent.cpu().numpy().any(axis=1)
     status[(status == 0) & absent_h] = -_lib.SPCN_ESTAIN_ABSENT
     prov = {"source": "", "config_hash": config_hash(_cfg_fields(plan, cfg, code_lam, False))}
+    info = r.info.cpu().numpy()
     return BatchFit(i0=i0, basis=r.basis, p99=p99, luts=luts, count=collected, status=status,
-                    provenance=prov)
+                    provenance=prov, iterations=info[:, 0].copy(), converged=info[:, 1] != 0,
+                    warn_flags=info[:, 2].copy())
 
 
 def transform_batch(images, fits: BatchFit, target: FitParams, out=None, *,

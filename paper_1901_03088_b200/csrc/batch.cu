@@ -179,8 +179,9 @@ __global__ void __launch_bounds__(256) k_repair_batch(const uint8_t* __restrict_
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
       if (status[it] != 0) continue;
       const StrictP& sp = sps[it];
+      const NnlsGram G = gram_of(sp);
       for (int64_t i = off[it] + threadIdx.x; i < off[it + 1]; i += 256) {
-        const uint32_t out = strict_pixel(sp, GlobalLut{&sp}, src[3 * i], src[3 * i + 1],
+        const uint32_t out = strict_pixel(sp, G, GlobalLut{&sp}, src[3 * i], src[3 * i + 1],
                                           src[3 * i + 2]);
         dst[3 * i] = out & 255u;
         dst[3 * i + 1] = (out >> 8) & 255u;
@@ -217,9 +218,10 @@ __global__ void __launch_bounds__(256) k_strict_batch(const uint8_t* __restrict_
   if (item >= nitems || status[item] != 1) return;
   const StrictP& sp = sps[item];
   const GlobalLut gl{sps + item};
+  const NnlsGram G = gram_of(sp);
   for (int64_t i = off[item] + blockIdx.x * 256ll + threadIdx.x; i < off[item + 1];
        i += 256ll * gridDim.x) {
-    const uint32_t out = strict_pixel(sp, gl, src[3 * i], src[3 * i + 1], src[3 * i + 2]);
+    const uint32_t out = strict_pixel(sp, G, gl, src[3 * i], src[3 * i + 1], src[3 * i + 2]);
     dst[3 * i] = out & 255u;
     dst[3 * i + 1] = (out >> 8) & 255u;
     dst[3 * i + 2] = (out >> 16) & 255u;

@@ -13,12 +13,13 @@ namespace spcn {
 __global__ void __launch_bounds__(256) k_code_densities(const double* __restrict__ od,
                                                         double* __restrict__ h, int64_t n,
                                                         const __grid_constant__ StrictP sp) {
+  const NnlsGram G = gram_of(sp);
   for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) {
     const double v0 = od[i], v1 = od[n + i], v2 = od[2 * n + i];
     const double b0 = strict_dot3(sp.ws[0][0], sp.ws[1][0], sp.ws[2][0], v0, v1, v2);
     const double b1 = strict_dot3(sp.ws[0][1], sp.ws[1][1], sp.ws[2][1], v0, v1, v2);
     double h0, h1;
-    strict_nnls(b0, b1, sp.g00, sp.g01, sp.g11, sp.det, sp.lam, sp.max_sweeps, sp.tol, h0, h1);
+    strict_nnls(b0, b1, G, sp.lam, sp.max_sweeps, sp.tol, h0, h1);
     h[i] = h0;
     h[n + i] = h1;
   }

@@ -29,7 +29,7 @@ namespace cg = cooperative_groups;
 
 namespace spcn {
 
-constexpr int kSnThreads = 512;
+constexpr int kSnMaxThreads = 512;
 constexpr int kNStat = 12;  // rr, s0, s1, vht[3][2], hht00, hht01, hht11
 
 __device__ __forceinline__ double fma_dot3(double a0, double a1, double a2, double b0, double b1,
@@ -38,7 +38,7 @@ __device__ __forceinline__ double fma_dot3(double a0, double a1, double a2, doub
   return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
 }
 
-template <int N>
+template <int NT, int N>
 __device__ __forceinline__ void cta_reduce(double (&v)[N], double* warp_part,
                                            double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -52,7 +52,7 @@ __device__ __forceinline__ void cta_reduce(double (&v)[N], double* warp_part,
   __syncthreads();
   if (threadIdx.x < N) {
     double s = 0.0;
-    for (int w = 0; w < kSnThreads / 32; ++w) s += warp_part[w * N + threadIdx.x];
+    for (int w = 0; w < NT / 32; ++w) s += warp_part[w * N + threadIdx.x];
     out[threadIdx.x] = s;
   }
 }
@@ -63,15 +63,18 @@ struct SnmfShared {
   double cand[6];
   double part[2][kNStat]; // double-buffered CTA partials (read by the cluster)
   double tot[kNStat];     // cluster totals (identical in every CTA)
-  double warp_part[kSnThreads / 32][kNStat];
+  double warp_part[kSnMaxThreads / 32][kNStat];
   double g[4];            // g00, g01, g11, det
   int flag;
 };
 
-__global__ void __launch_bounds__(kSnThreads) k_snmf(
+// NT threads per CTA, MINB CTAs per SM (512 x 1 measured best for both the
+// cluster fit of one slide and the one-CTA-per-problem batch).
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_snmf(
     const uint8_t* __restrict__ samples, const double* __restrict__ od,
     const int64_t* __restrict__ offsets, int nprob, const double* __restrict__ luts,
-    const __grid_constant__ SnmfArgs a, double* __restrict__ hbuf,
+    const __grid_constant__ SnmfArgs a, int* __restrict__ ticket,
     int64_t total, double* __restrict__ basis_out, double* __restrict__ hist_out,
     int32_t* __restrict__ info_out) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -98,11 +101,22 @@ __global__ void __launch_bounds__(kSnThreads) k_snmf(
     __syncthreads();
   };
 
-  for (int p = cid; p < nprob; p += ncl) {
+  // problem scheduling: clusters take p = cid, cid + ncl, ...; single CTAs
+  // pull problems from a global ticket counter (problems differ a lot in
+  // outer-iteration count, so static assignment leaves SMs idle)
+  __shared__ int s_ticket;
+  auto next_problem = [&](int p) {
+    if (cs > 1 || !ticket) return p < 0 ? cid : p + ncl;
+    __syncthreads();   // everyone has read the previous ticket
+    if (tid == 0) s_ticket = atomicAdd(ticket, 1);
+    __syncthreads();
+    return s_ticket;
+  };
+  for (int p = next_problem(-1); p < nprob; p = next_problem(p)) {
     const int64_t o0 = offsets[p], m = offsets[p + 1] - offsets[p];
     const int64_t lo = o0 + (m * rank) / cs, hi = o0 + (m * (rank + 1)) / cs;
     if (!od)
-      for (int i = tid; i < 3 * 256; i += kSnThreads) sh.lut[i] = luts[(int64_t)p * 768 + i];
+      for (int i = tid; i < 3 * 256; i += NT) sh.lut[i] = luts[(int64_t)p * 768 + i];
     if (tid < 6) sh.w[tid] = a.w_init[tid];
     __syncthreads();
     const double lam = a.lam, code_lam = a.lam / 2.0;
@@ -129,17 +143,11 @@ __global__ void __launch_bounds__(kSnThreads) k_snmf(
       __syncthreads();
       const double w00 = sh.w[0], w01 = sh.w[1], w10 = sh.w[2], w11 = sh.w[3], w20 = sh.w[4],
                    w21 = sh.w[5];
-      const double g00 = sh.g[0], g01 = sh.g[1], g11 = sh.g[2], det = sh.g[3];
+      const NnlsGram G = make_nnls_gram(sh.g[0], sh.g[1], sh.g[2], sh.g[3]);
       double st[kNStat];
 #pragma unroll
       for (int q = 0; q < kNStat; ++q) st[q] = 0.0;
-      for (int64_t i = lo + tid; i < hi; i += kSnThreads) {
-        double v0, v1, v2;
-        load_od(i, v0, v1, v2);
-        const double b0 = strict_dot3(w00, w10, w20, v0, v1, v2);
-        const double b1 = strict_dot3(w01, w11, w21, v0, v1, v2);
-        double h0, h1;
-        strict_nnls(b0, b1, g00, g01, g11, det, code_lam, 500, 1e-9, h0, h1);
+      auto accumulate = [&](double v0, double v1, double v2, double h0, double h1) {
         const double r0 = v0 - __fma_rn(w01, h1, __dmul_rn(w00, h0));
         const double r1 = v1 - __fma_rn(w11, h1, __dmul_rn(w10, h0));
         const double r2 = v2 - __fma_rn(w21, h1, __dmul_rn(w20, h0));
@@ -150,8 +158,25 @@ __global__ void __launch_bounds__(kSnThreads) k_snmf(
         st[5] += v1 * h0; st[6] += v1 * h1;
         st[7] += v2 * h0; st[8] += v2 * h1;
         st[9] += h0 * h0; st[10] += h0 * h1; st[11] += h1 * h1;
+      };
+      // two independent pixels per thread per step: their division chains
+      // interleave (the fp64 pipe is latency-bound with one)
+      for (int64_t i = lo + tid; i < hi; i += 2 * NT) {
+        const bool two = i + NT < hi;
+        const int64_t i2 = two ? i + NT : i;
+        double a0, a1, a2, c0, c1, c2;
+        load_od(i, a0, a1, a2);
+        load_od(i2, c0, c1, c2);
+        NnlsState sa = nnls_seed(strict_dot3(w00, w10, w20, a0, a1, a2),
+                                 strict_dot3(w01, w11, w21, a0, a1, a2), G, code_lam, 1e-9);
+        NnlsState sc = nnls_seed(strict_dot3(w00, w10, w20, c0, c1, c2),
+                                 strict_dot3(w01, w11, w21, c0, c1, c2), G, code_lam, 1e-9);
+        nnls_finish(sa, G, 500, 1e-9);
+        nnls_finish(sc, G, 500, 1e-9);
+        accumulate(a0, a1, a2, sa.x0, sa.x1);
+        if (two) accumulate(c0, c1, c2, sc.x0, sc.x1);
       }
-      cta_reduce<kNStat>(st, &sh.warp_part[0][0], sh.part[phase & 1]);
+      cta_reduce<NT, kNStat>(st, &sh.warp_part[0][0], sh.part[phase & 1]);
       cluster_total(kNStat);
       return sh.tot[0] + lam * (sh.tot[1] + sh.tot[2]);
     };
@@ -263,13 +288,14 @@ __global__ void __launch_bounds__(256) k_code_samples(
     g[3] = __dsub_rn(__dmul_rn(g[0], g[2]), __dmul_rn(g[1], g[1]));
   }
   __syncthreads();
+  const NnlsGram G = make_nnls_gram(g[0], g[1], g[2], g[3]);
   for (int64_t i = o0 + blockIdx.x * 256ll + threadIdx.x; i < o1; i += 256ll * gridDim.x) {
     const uint8_t* px = samples + 3 * i;
     const double v0 = lut[px[0]], v1 = lut[256 + px[1]], v2 = lut[512 + px[2]];
     const double b0 = strict_dot3(w[0], w[2], w[4], v0, v1, v2);
     const double b1 = strict_dot3(w[1], w[3], w[5], v0, v1, v2);
     double h0, h1;
-    strict_nnls(b0, b1, g[0], g[1], g[2], g[3], lam, max_sweeps, 0.0, h0, h1);
+    strict_nnls(b0, b1, G, lam, max_sweeps, 0.0, h0, h1);
     h[i] = h0;
     h[total + i] = h1;
   }
@@ -280,15 +306,32 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
                         double* basis_out, double* hist_out, int32_t* info_out, int cluster,
                         cudaStream_t st) {
   if (nprob <= 0) return cudaSuccess;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static int sms = 0, occ1 = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_snmf<512, 1>, 512, 0);
+    if (e != cudaSuccess) {
+      sms = 0;
+      return e;
+    }
+    if (occ1 < 1) occ1 = 1;
+  }
+  const bool single = cluster == 1;
+  int* ticket = nullptr;
+  if (single && nprob > 1) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ticket), sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+  }
   int nclusters = nprob;
-  const int max_clusters = (sms * 2) / cluster;
+  const int max_clusters = single ? sms * occ1 : (sms * 2) / cluster;   // occ1: resident CTAs/SM
   if (nclusters > max_clusters) nclusters = max_clusters;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nclusters * cluster);
-  cfg.blockDim = dim3(kSnThreads);
+  cfg.blockDim = dim3(512);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -298,8 +341,12 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_snmf, samples, od, offsets, nprob, luts, a,
-                                           hbuf, total, basis_out, hist_out, info_out);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_snmf<512, 1>, samples, od, offsets, nprob, luts, a,
+                                     ticket, total, basis_out, hist_out, info_out);
+  if (ticket) {
+    const cudaError_t e2 = cudaFreeAsync(ticket, st);
+    if (e == cudaSuccess) e = e2;
+  }
   return e != cudaSuccess ? e : launched();
 }
 

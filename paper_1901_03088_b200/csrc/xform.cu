@@ -140,21 +140,24 @@ __global__ void __launch_bounds__(256) k_xform_repair(const uint8_t* __restrict_
     __shared__ double lut[3 * 256];
     for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
     __syncthreads();
+    const NnlsGram G = gram_of(sp);
     for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < npix; i += 256ll * gridDim.x) {
-      const uint32_t out = strict_pixel(sp, SmemLut{lut}, src[3 * i], src[3 * i + 1], src[3 * i + 2]);
+      const uint32_t out =
+          strict_pixel(sp, G, SmemLut{lut}, src[3 * i], src[3 * i + 1], src[3 * i + 2]);
       dst[3 * i] = out & 255u;
       dst[3 * i + 1] = (out >> 8) & 255u;
       dst[3 * i + 2] = (out >> 16) & 255u;
     }
     return;
   }
+  const NnlsGram G = gram_of(sp);
   for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n;
        i += 256ull * gridDim.x) {
     const unsigned long long it = rl.items[i];
     const uint32_t rgb = static_cast<uint32_t>(it & 0xffffffu);
     const int64_t gp = static_cast<int64_t>(it >> 24);
     const uint32_t out =
-        strict_pixel(sp, ConstLut{&sp}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
+        strict_pixel(sp, G, ConstLut{&sp}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
     dst[3 * gp] = out & 255u;
     dst[3 * gp + 1] = (out >> 8) & 255u;
     dst[3 * gp + 2] = (out >> 16) & 255u;
@@ -167,9 +170,10 @@ __global__ void __launch_bounds__(256) k_xform_strict(const uint8_t* __restrict_
   __shared__ double lut[3 * 256];
   for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
   __syncthreads();
+  const NnlsGram G = gram_of(sp);
   for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < npix; i += 256ll * gridDim.x) {
     const uint32_t r = src[3 * i], g = src[3 * i + 1], b = src[3 * i + 2];
-    const uint32_t out = strict_pixel(sp, SmemLut{lut}, r, g, b);
+    const uint32_t out = strict_pixel(sp, G, SmemLut{lut}, r, g, b);
     dst[3 * i] = out & 255u;
     dst[3 * i + 1] = (out >> 8) & 255u;
     dst[3 * i + 2] = (out >> 16) & 255u;
@@ -192,6 +196,7 @@ __global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP
   }
   __syncthreads();
   float worst = 0.f;
+  const NnlsGram G = gram_of(sp);
   for (uint32_t q = blockIdx.x * 256u + threadIdx.x; q < (1u << 23); q += 256u * gridDim.x) {
     const uint32_t ca = 2u * q, cb = 2u * q + 1u;   // colours: r | g<<8 | b<<16
     const float2 v0 = make_float2(flut[ca & 255], flut[cb & 255]);
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP
       const double b0 = strict_dot3(sp.ws[0][0], sp.ws[1][0], sp.ws[2][0], d0, d1, d2);
       const double b1 = strict_dot3(sp.ws[0][1], sp.ws[1][1], sp.ws[2][1], d0, d1, d2);
       double h0, h1;
-      strict_nnls(b0, b1, sp.g00, sp.g01, sp.g11, sp.det, sp.lam, sp.max_sweeps, sp.tol, h0, h1);
+      strict_nnls(b0, b1, G, sp.lam, sp.max_sweeps, sp.tol, h0, h1);
       const double s0 = __dmul_rn(sp.f[0], h0), s1 = __dmul_rn(sp.f[1], h1);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
