@@ -83,7 +83,7 @@ __host__ __device__ inline bool fill_fast_scalars(FastS& fp, const StrictP& sp, 
   fp.nF2 = -(float)F * 0.5f;
   fp.G = (float)G;
   fp.nH2 = -(float)H * 0.5f;
-  for (int c = 0; c < 3; ++c) fp.ilo[c] = fp.ihi[c] = 0.0f;
+  for (int c = 0; c < 3; ++c) fp.I[c].x = fp.I[c].y = 0.0f;
   const double log2e = 1.4426950408889634;
   double Kabs[3][2];
   for (int c = 0; c < 3; ++c)

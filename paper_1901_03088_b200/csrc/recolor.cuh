@@ -107,7 +107,7 @@ __device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t*
       Ia = cert_interval(fp.i0t[c], alpha.x);
       Ib = cert_interval(fp.i0t[c], alpha.y);
     } else {
-      Ia = Ib = make_float2(fp.ilo[c], fp.ihi[c]);
+      Ia = Ib = fp.I[c];
     }
     const float2 ra = __ffma2_rn(Ia, bc2(pa), bc2(kMagic));
     const float2 rb = __ffma2_rn(Ib, bc2(pb), bc2(kMagic));

@@ -36,10 +36,6 @@ namespace spcn {
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
-struct ConstLut {              // fp64 table read from kernel parameters
-  const StrictP* p;
-  __device__ double operator()(int c, uint32_t i) const { return p->lut[c][i]; }
-};
 struct SmemLut {
   const double* t;
   __device__ double operator()(int c, uint32_t i) const { return t[c * 256 + i]; }
@@ -130,17 +126,20 @@ __global__ void __launch_bounds__(32 * CW, BLK)
 }
 
 // fp64 recompute of the listed pixels; if the list overflowed (count > cap)
-// every pixel of the body is recomputed instead.
+// every pixel of the body is recomputed instead.  The fp64 table is staged in
+// shared memory (per-thread table indices differ, so reading it from the
+// kernel-parameter bank would serialise).
 __global__ void __launch_bounds__(256) k_xform_repair(const uint8_t* __restrict__ src,
                                                       uint8_t* __restrict__ dst, int64_t npix,
                                                       const __grid_constant__ StrictP sp,
                                                       RepairList rl) {
   const unsigned long long n = *rl.count;
+  if (n == 0) return;
+  __shared__ double lut[3 * 256];
+  for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
+  __syncthreads();
+  const NnlsGram G = gram_of(sp);
   if (n > rl.cap) {
-    __shared__ double lut[3 * 256];
-    for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
-    __syncthreads();
-    const NnlsGram G = gram_of(sp);
     for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < npix; i += 256ll * gridDim.x) {
       const uint32_t out =
           strict_pixel(sp, G, SmemLut{lut}, src[3 * i], src[3 * i + 1], src[3 * i + 2]);
@@ -150,14 +149,13 @@ __global__ void __launch_bounds__(256) k_xform_repair(const uint8_t* __restrict_
     }
     return;
   }
-  const NnlsGram G = gram_of(sp);
   for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n;
        i += 256ull * gridDim.x) {
     const unsigned long long it = rl.items[i];
     const uint32_t rgb = static_cast<uint32_t>(it & 0xffffffu);
     const int64_t gp = static_cast<int64_t>(it >> 24);
     const uint32_t out =
-        strict_pixel(sp, G, ConstLut{&sp}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
+        strict_pixel(sp, G, SmemLut{lut}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
     dst[3 * gp] = out & 255u;
     dst[3 * gp + 1] = (out >> 8) & 255u;
     dst[3 * gp + 2] = (out >> 16) & 255u;
