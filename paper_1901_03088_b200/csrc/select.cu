@@ -110,6 +110,185 @@ __global__ void k_p99_queries(const int64_t* __restrict__ seg, int nseg, int64_t
   q[2].k = n > 0 ? n - 1 : 0;
 }
 
+// ---------------------------------------------------------------------------
+// k_p99_seg: one CTA per (segment, stain) producing the three order
+// statistics k_p99_combine needs (ranks lo, hi and the max).  The 99th
+// percentile sits just below the maximum, so: pass 1 finds the max key; pass 2
+// histograms only the keys within a window below it (bin = (max - key) >>
+// kWinShift, i.e. 2^-12-relative bins over two octaves — few values, spread
+// over many bins, so the shared-memory atomics do not collide); pass 3
+// gathers the keys of the bins holding ranks lo..hi into shared memory, where
+// an MSD radix select resolves them exactly.  If the window or the candidate
+// list is too small/large for a pathological distribution, the CTA falls back
+// to the all-global radix select.  Exact integer counting throughout: the
+// same order statistics as a sort.
+constexpr int kTop = 13;
+constexpr int kTopBins = 1 << kTop;
+constexpr int kCand = 8192;
+constexpr int kWinShift = 40;   // 2^52 key units per octave -> 2^12 bins per octave
+
+struct SegShared {
+  uint32_t hist[kTopBins];
+  unsigned long long cand[kCand];
+  uint32_t scan[kSelThreads];
+  unsigned long long red[kSelThreads / 32];
+  int loc_bin;
+  long long loc_rank;
+  uint32_t ncand;
+};
+
+// Block-wide: the bin of hist[0..nb) holding rank k -> sh.loc_bin, and k's
+// rank inside that bin -> sh.loc_rank.
+__device__ void hist_locate(SegShared& sh, int nb, int64_t k) {
+  const int per = nb / kSelThreads;
+  uint32_t loc = 0;
+  for (int j = 0; j < per; ++j) loc += sh.hist[threadIdx.x * per + j];
+  sh.scan[threadIdx.x] = loc;
+  __syncthreads();
+  for (int off = 1; off < kSelThreads; off <<= 1) {
+    const uint32_t y = threadIdx.x >= off ? sh.scan[threadIdx.x - off] : 0u;
+    __syncthreads();
+    sh.scan[threadIdx.x] += y;
+    __syncthreads();
+  }
+  const int64_t incl = sh.scan[threadIdx.x], excl = incl - loc;
+  if (k >= excl && k < incl) {
+    int64_t c = excl;
+    for (int j = 0; j < per; ++j) {
+      const int bin = threadIdx.x * per + j;
+      if (k < c + sh.hist[bin]) {
+        sh.loc_bin = bin;
+        sh.loc_rank = k - c;
+        break;
+      }
+      c += sh.hist[bin];
+    }
+  }
+  __syncthreads();
+}
+
+// MSD radix select of rank k among cnt keys src(i), i in [0, cnt).
+template <class Src>
+__device__ uint64_t radix_select(SegShared& sh, const Src& src, int64_t cnt, int64_t k) {
+  uint64_t prefix = 0;
+  int used = 0;
+  while (used < 64) {
+    const int dbits = (64 - used) < kDigit ? (64 - used) : kDigit;
+    const int shift = 64 - used - dbits;
+    for (int i = threadIdx.x; i < kBins; i += kSelThreads) sh.hist[i] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < cnt; i += kSelThreads) {
+      const uint64_t key = src(i);
+      if (used == 0 || (key >> (64 - used)) == prefix)
+        atomicAdd(&sh.hist[(key >> shift) & ((1u << dbits) - 1u)], 1u);
+    }
+    __syncthreads();
+    hist_locate(sh, kBins, k);
+    prefix = (prefix << dbits) | (uint64_t)sh.loc_bin;
+    k = sh.loc_rank;
+    used += dbits;
+    __syncthreads();
+  }
+  return prefix;
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_p99_seg(const double* __restrict__ h,
+                                                        int64_t total,
+                                                        const int64_t* __restrict__ seg,
+                                                        double p, double* __restrict__ sel) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  SegShared& sh = *reinterpret_cast<SegShared*>(smem_raw);
+  const int idx = blockIdx.x, s = idx >> 1, j = idx & 1;
+  const int64_t b = seg[s], e = seg[s + 1], n = e - b;
+  if (n <= 0) {
+    if (threadIdx.x < 3) sel[3 * idx + threadIdx.x] = 0.0;
+    return;
+  }
+  const double rank = __dmul_rn(p / 100.0, (double)(n - 1));
+  const int64_t klo = (int64_t)floor(rank), khi = (int64_t)ceil(rank);
+  const double* v = h + j * total + b;
+  // pass 1: the max key
+  uint64_t mx = 0;
+  for (int64_t i = threadIdx.x; i < n; i += kSelThreads) {
+    const uint64_t key = key_of(v[i]);
+    mx = key > mx ? key : mx;
+  }
+  for (int off = 16; off; off >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, mx, off);
+    mx = o > mx ? o : mx;
+  }
+  if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5] = mx;
+  for (int i = threadIdx.x; i < kTopBins; i += kSelThreads) sh.hist[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kSelThreads / 32; ++w) mx = sh.red[w] > mx ? sh.red[w] : mx;
+    sh.red[0] = mx;
+  }
+  __syncthreads();
+  mx = sh.red[0];
+  // pass 2: histogram of the window below the max (bin 0 = the largest keys)
+  constexpr uint64_t kWin = (uint64_t)(kTopBins - 1) << kWinShift;
+  for (int64_t i = threadIdx.x; i < n; i += kSelThreads) {
+    const uint64_t d = mx - key_of(v[i]);
+    if (d < kWin) atomicAdd(&sh.hist[d >> kWinShift], 1u);
+  }
+  __syncthreads();
+  // ranks counted from the top: rt = n - 1 - k
+  const int64_t rt_hi = n - 1 - khi, rt_lo = n - 1 - klo;   // rt_hi <= rt_lo
+  uint32_t inwin = 0;
+  for (int i = threadIdx.x; i < kTopBins; i += kSelThreads) inwin += sh.hist[i];
+  for (int off = 16; off; off >>= 1) inwin += __shfl_xor_sync(0xffffffffu, inwin, off);
+  if ((threadIdx.x & 31) == 0) sh.scan[threadIdx.x >> 5] = inwin;
+  __syncthreads();
+  inwin = 0;
+  for (int w = 0; w < kSelThreads / 32; ++w) inwin += sh.scan[w];
+  __syncthreads();
+  uint64_t klo_key = 0, khi_key = 0;
+  bool done = false;
+  if ((int64_t)inwin > rt_lo) {
+    hist_locate(sh, kTopBins, rt_hi);
+    const int b1 = sh.loc_bin;
+    const int64_t r1 = sh.loc_rank;
+    __syncthreads();
+    hist_locate(sh, kTopBins, rt_lo);
+    const int b2 = sh.loc_bin;
+    const int64_t r2 = sh.loc_rank;
+    int64_t ncand = 0, before2 = 0;
+    for (int t = b1; t <= b2; ++t) {
+      if (t == b2) before2 = ncand;
+      ncand += sh.hist[t];
+    }
+    if (ncand <= kCand) {
+      // pass 3: gather the keys of bins b1..b2
+      if (threadIdx.x == 0) sh.ncand = 0;
+      __syncthreads();
+      const uint64_t dlo = (uint64_t)b1 << kWinShift, dhi = ((uint64_t)(b2 + 1) << kWinShift);
+      for (int64_t i = threadIdx.x; i < n; i += kSelThreads) {
+        const uint64_t key = key_of(v[i]);
+        const uint64_t d = mx - key;
+        if (d >= dlo && d < dhi) sh.cand[atomicAdd(&sh.ncand, 1u)] = key;
+      }
+      __syncthreads();
+      const auto src = [&](int64_t i) -> uint64_t { return sh.cand[i]; };
+      // top-rank r within the candidates -> bottom rank ncand - 1 - r
+      khi_key = radix_select(sh, src, ncand, ncand - 1 - r1);
+      klo_key = radix_select(sh, src, ncand, ncand - 1 - (before2 + r2));
+      done = true;
+    }
+  }
+  if (!done) {
+    const auto src = [&](int64_t i) -> uint64_t { return key_of(v[i]); };
+    __syncthreads();
+    klo_key = radix_select(sh, src, n, klo);
+    khi_key = radix_select(sh, src, n, khi);
+  }
+  if (threadIdx.x == 0) {
+    sel[3 * idx] = val_of(klo_key);
+    sel[3 * idx + 1] = val_of(khi_key);
+    sel[3 * idx + 2] = val_of(mx);
+  }
+}
+
 __global__ void k_p99_combine(const int64_t* __restrict__ seg, int nseg, double p,
                               const double* __restrict__ sel, double* __restrict__ p99,
                               int32_t* __restrict__ absent) {
@@ -158,10 +337,17 @@ cudaError_t launch_p99(const double* h, int64_t total, const int64_t* seg, int n
                        cudaStream_t st) {
   if (nseg <= 0) return cudaSuccess;
   const int n2 = nseg * 2;
-  k_p99_queries<<<(n2 + 127) / 128, 128, 0, st>>>(seg, nseg, total, p, qbuf);
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e0 = cudaFuncSetAttribute(k_p99_seg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)sizeof(SegShared));
+    if (e0 != cudaSuccess) return e0;
+    attr = true;
+  }
+  (void)qbuf;
+  k_p99_seg<<<n2, kSelThreads, sizeof(SegShared), st>>>(h, total, seg, p, selbuf);
   cudaError_t e = launched();
   if (e != cudaSuccess) return e;
-  if ((e = launch_select(h, qbuf, 3 * n2, selbuf, st)) != cudaSuccess) return e;
   k_p99_combine<<<(n2 + 127) / 128, 128, 0, st>>>(seg, nseg, p, selbuf, p99, absent);
   return launched();
 }

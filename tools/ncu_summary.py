@@ -7,8 +7,11 @@ and an ncu launch-list CSV into per-kernel shares.  Output goes to profiles/.
 import collections
 import csv
 import io
+import signal
 import subprocess
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 
 KEYS = [
     "gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
