@@ -452,10 +452,11 @@ def run_ours(args, rank, world, local):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    traffic = None
+    traffic, traffic_px = None, None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "xform_traffic.json")))
-        traffic = prof.get("bytes_per_px")
+        traffic_px = float(prof["bytes_per_px"])
+        traffic = round(traffic_px * npx_rank)       # DRAM bytes per launch (ncu, scaled)
     except Exception:
         pass
 
@@ -466,7 +467,9 @@ def run_ours(args, rank, world, local):
             "config": workload_config(args, world),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "kernel": "spcn_xform_rgb8 (k_xform_warp + k_xform_repair)",
+                         "traffic": traffic, "traffic_bytes_per_px": traffic_px,
+                         "traffic_source": "profiles/xform_traffic.json (ncu --set full)",
+                         "kernel": "spcn_xform_rgb8 (k_xform_warp + k_xform_repair)",
                          "kernel_ms": round(x_ms, 4), "share_of_step": round(x_ms / ms, 4),
                          "algorithmic_bytes_per_px": BYTES_PER_PX,
                          "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
