@@ -134,38 +134,44 @@ def _lib_sample():
 
 
 class _PatchImage:
-    """Device view of the slide regions the sampler may visit."""
+    """Device view of the slide regions the sampler may visit.  A device slide
+    is addressed in place; for a host slide only the regions of the batches
+    the visit loop actually counts are uploaded (usually the first few of the
+    10 x max_patches candidates)."""
 
     def __init__(self, slide, rects):
-        t = _dev.torch()
         self.rects = rects
-        if isinstance(slide, DeviceSource):
-            self.img = slide.tensor
+        self.slide = slide
+        self.device = isinstance(slide, DeviceSource)
+        if self.device:
             width = slide.width
+            self.img = slide.tensor
             self.desc = np.array([(y * width + x, w, h, width) for (x, y, w, h) in rects],
                                  dtype=PATCH_DT)
-        else:
-            # host slide: upload only the candidate regions (≤ 10 x max_patches of them)
-            parts, desc, base = [], [], 0
-            for (x, y, w, h) in rects:
-                px = slide.read_region(x, y, w, h).pixels
-                parts.append(np.ascontiguousarray(px).reshape(-1))
-                desc.append((base, w, h, w))
-                base += w * h
-            host = np.concatenate(parts) if parts else np.zeros(3, np.uint8)
-            self.img = t.from_numpy(host).to("cuda")
-            self.desc = np.array(desc, dtype=PATCH_DT)
+
+    def batch(self, lo, hi):
+        """(device image, descriptors) of candidates [lo, hi)."""
+        if self.device:
+            return self.img, self.desc[lo:hi]
+        t = _dev.torch()
+        parts, desc, base = [], [], 0
+        for (x, y, w, h) in self.rects[lo:hi]:
+            px = self.slide.read_region(x, y, w, h).pixels
+            parts.append(np.ascontiguousarray(px).reshape(-1))
+            desc.append((base, w, h, w))
+            base += w * h
+        host = np.concatenate(parts) if parts else np.zeros(3, np.uint8)
+        return t.from_numpy(host).to("cuda"), np.array(desc, dtype=PATCH_DT)
 
 
-def _count(L, pimg, sel, thr):
-    """Per-chunk counts for the patches `sel` (indices into pimg.desc) → (n, chunks, 4)."""
+def _count(L, img, desc, thr):
+    """Per-chunk counts for the patches `desc` of `img` → (n, chunks, 4)."""
     t = _dev.torch()
-    desc = pimg.desc[sel]
     npx = desc["width"].astype(np.int64) * desc["height"]
     chunks = int(max(1, -(-int(npx.max()) // CHUNK)))
     d = t.from_numpy(desc.view(np.uint8).copy()).cuda()
-    out = t.empty((len(sel), chunks, 4), dtype=t.int32, device="cuda")
-    _lib.check(L.spcn_sample_count(_lib.ptr(pimg.img), _lib.ptr(d), len(sel), chunks, thr,
+    out = t.empty((len(desc), chunks, 4), dtype=t.int32, device="cuda")
+    _lib.check(L.spcn_sample_count(_lib.ptr(img), _lib.ptr(d), len(desc), chunks, thr,
                                    _lib.ptr(out), _lib.stream_handle()), "sample_count")
     return out, chunks
 
@@ -225,8 +231,9 @@ def _sample_device(slide, plan: SamplePlan):
         while k >= tot.shape[0]:
             lo = tot.shape[0]
             hi = min(ncand, lo + batch)
-            c, chunks = _count(L, pimg, np.arange(lo, hi), thr)
-            dev_counts.append((lo, hi, c, chunks))
+            img, desc = pimg.batch(lo, hi)
+            c, chunks = _count(L, img, desc, thr)
+            dev_counts.append((lo, hi, c, chunks, img, desc))
             tot = np.concatenate([tot, c.sum(dim=1).cpu().numpy().astype(np.int64)])
             batch *= 2
         return tuple(int(v) for v in tot[k])
@@ -236,12 +243,12 @@ def _sample_device(slide, plan: SamplePlan):
         raise BlankSlideError("blank slide: no non-white pixels found in any sampled patch")
     sample = t.empty((collected, 3), dtype=t.uint8, device="cuda")
     hist = t.zeros((1, 3, 256), dtype=t.int32, device="cuda")
-    for lo, hi, c, chunks in dev_counts:
+    for lo, hi, c, chunks, img, bdesc in dev_counts:
         sel = [tk for tk in takes if lo <= tk[0] < hi and (tk[1] > 0 or any(tk[3]))]
         if not sel:
             continue
         idx = np.array([tk[0] - lo for tk in sel], dtype=np.int64)
-        desc = pimg.desc[lo:hi][idx]
+        desc = bdesc[idx]
         tk = np.zeros(len(sel), dtype=TAKE_DT)
         tk["take_nonwhite"] = [s[1] for s in sel]
         tk["out_base"] = [s[2] for s in sel]
@@ -250,7 +257,7 @@ def _sample_device(slide, plan: SamplePlan):
         cnt = c[t.from_numpy(idx).cuda()].contiguous()
         d = t.from_numpy(desc.view(np.uint8).copy()).cuda()
         dt = t.from_numpy(tk.view(np.uint8).copy()).cuda()
-        _lib.check(L.spcn_sample_compact(_lib.ptr(pimg.img), _lib.ptr(d), len(sel), chunks, thr,
+        _lib.check(L.spcn_sample_compact(_lib.ptr(img), _lib.ptr(d), len(sel), chunks, thr,
                                          _lib.ptr(cnt), _lib.ptr(dt), _lib.ptr(sample),
                                          _lib.ptr(hist), _lib.stream_handle()), "sample_compact")
     bh = hist.cpu().numpy()[0].astype(np.int64)
