@@ -84,6 +84,38 @@ __host__ __device__ inline bool fill_fast_scalars(FastS& fp, const StrictP& sp, 
   fp.G = (float)G;
   fp.nH2 = -(float)H * 0.5f;
   for (int c = 0; c < 3; ++c) fp.I[c].x = fp.I[c].y = 0.0f;
+  // Background skip: a byte x >= i0_c has OD exactly 0, so a
+  // pixel with every channel there has h = 0 and renders floor(i0_t + 0.5)
+  // (src/optics.py:89-94, src/normalize.py:146-150).  T = the smallest byte
+  // value with OD 0 in every channel; the kernel tests "all bits of wmask set"
+  // for every byte, i.e. x >= 256 - 2^k >= T (conservative).
+  {
+    int T = 0;
+    for (int c = 0; c < 3; ++c) {
+      int x = 255;
+      while (x > 0 && sp.lut[c][x - 1] == 0.0) --x;
+      if (!(sp.lut[c][255] == 0.0)) x = 256;   // no background byte in this channel
+      T = x > T ? x : T;
+    }
+    fp.wmask = 0;
+    if (T <= 255) {
+      int k = 0;
+      while ((2 << k) <= 256 - T) ++k;          // 2^k <= 256 - T < 2^(k+1)
+      const uint32_t mb = (~((1u << k) - 1u)) & 0xffu;
+      fp.wmask = mb * 0x01010101u;
+    }
+    uint32_t ob[3];
+    for (int c = 0; c < 3; ++c) {
+      double y = floor(p_add(static_cast<double>(sp.i0t[c]), 0.5));
+      y = y < 0.0 ? 0.0 : (y > 255.0 ? 255.0 : y);
+      ob[c] = static_cast<uint32_t>(y);
+    }
+    for (int wd = 0; wd < 3; ++wd) {
+      uint32_t v = 0;
+      for (int b = 0; b < 4; ++b) v |= ob[(4 * wd + b) % 3] << (8 * b);
+      fp.wout[wd] = v;
+    }
+  }
   const double log2e = 1.4426950408889634;
   double Kabs[3][2];
   for (int c = 0; c < 3; ++c)

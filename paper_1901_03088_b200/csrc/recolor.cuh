@@ -134,6 +134,26 @@ __device__ __forceinline__ void recolor_block(const FastS& fp, const uint8_t* lu
     w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
     w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
     w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
+  }
+  if (MODE != 3 && fp.wmask) {
+    // background blocks (every byte >= the OD-zero threshold) render the
+    // constant target background; skip the math when the whole warp has them
+    uint32_t acc = 0xffffffffu;
+    if (valid) {
+#pragma unroll
+      for (int t = 0; t < 12; ++t) acc &= w[t];
+    }
+    if (__all_sync(0xffffffffu, (acc & fp.wmask) == fp.wmask)) {
+      if (valid) {
+        uint4* d = reinterpret_cast<uint4*>(blk);
+        d[0] = make_uint4(fp.wout[0], fp.wout[1], fp.wout[2], fp.wout[0]);
+        d[1] = make_uint4(fp.wout[1], fp.wout[2], fp.wout[0], fp.wout[1]);
+        d[2] = make_uint4(fp.wout[2], fp.wout[0], fp.wout[1], fp.wout[2]);
+      }
+      return;
+    }
+  }
+  if (valid) {
     if (MODE == 3) {
 #pragma unroll
       for (int t = 0; t < 12; ++t) o[t] = w[t];
