@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-workers", type=int, default=3, help="CUDA streams of the host transform")
     ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the CPU-baseline band")
+    ap.add_argument("--p99-mode", choices=("sample", "global"), default="sample",
+                    help="sample = reference semantics (default); global = whole-slide p99 passes")
     ap.add_argument("--workload", choices=("wsi", "batch"), default="wsi",
                     help="wsi = configs[3] (default); batch = configs[1] (4096 x 512^2 patches)")
     ap.add_argument("--batch", type=int, default=4096)
@@ -198,7 +200,7 @@ def workload_config(args, world):
                         f"{args.layout}); step = fit(source) + transform(all pixels) vs a "
                         "fixed target profile",
             "width": args.width, "height": args.height, "precision": args.precision,
-            "parallelism": f"row-band x{world}", "p99_mode": "sample",
+            "parallelism": f"row-band x{world}", "p99_mode": args.p99_mode,
             "l2": "input+output 60 GB per step >> 126 MB L2 (no flush needed)"}
 
 
@@ -401,9 +403,9 @@ def run_ours(args, rank, world, local):
 
     def step(record=False):
         if group is None:
-            fp = pb.fit(src)
+            fp = pb.fit(src, p99_mode=args.p99_mode)
         else:
-            fp = group.fit(src)
+            fp = group.fit(src, p99_mode=args.p99_mode)
         sink = pb.DeviceWriter(W, rows, out=out)
         if record:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

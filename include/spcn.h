@@ -236,6 +236,30 @@ int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int
                      const void* strict_params, int32_t precision, void* workspace,
                      size_t workspace_bytes, void* stream);
 
+/* ---- whole-slide ("global") percentile mode --
+ * Extension of stain_stats (src/normalize.py:58-100): the p99 of the
+ * densities of EVERY non-white pixel (not all channels > white_threshold,
+ * src/pipeline.py:176), coded like code_densities (src/stain_sep.py:168-201)
+ * with p->src_i0 / src_basis / code_lam / max_sweeps (target fields unused).
+ * spcn_stats_hist: fp32 densities binned into hist[j*nbins + bin], bin =
+ * (float_bits(h_j) - base[j]) >> shift[j] (keys below base are counted in
+ * counts[1+j]; counts[0] += non-white pixels; h = 0 counts into bin 0 when
+ * base[j] == 0).  Approximate: it only places the refine window.
+ * spcn_stats_refine: exact classification against [lo[j], hi[j]): densities
+ * that may lie in the window are recomputed in fp64 in the reference's order;
+ * counts[j] += exact count below lo[j], counts[2+j] += count in the window
+ * (the first `cap` values listed in cand[j*cap + i]), counts[4] += fp64
+ * evaluations.  All buffers device; hist/counts accumulate (caller zeroes);
+ * src 16-byte aligned.  Multi-GPU: sum hist/counts across ranks, gather cand. */
+int spcn_stats_hist(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
+                    int32_t white_threshold, const uint32_t* base, const uint32_t* shift,
+                    int32_t nbins, unsigned long long* hist, unsigned long long* counts,
+                    void* stream);
+int spcn_stats_refine(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
+                      int32_t white_threshold, const double* lo, const double* hi,
+                      unsigned long long* counts, double* cand, unsigned long long cap,
+                      void* stream);
+
 /* ---- measurement input: synthetic H&E slides --------------------------- */
 typedef struct spcn_synth_params {
   float i0[3];             /* background intensity per channel              */

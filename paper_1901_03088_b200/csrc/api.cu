@@ -448,6 +448,95 @@ int spcn_select_kth(const double* values, const int64_t* begin, const int64_t* e
 
 }  // extern "C"
 
+// ------------------------------------------------------------------ global stats
+#include "stats.h"
+
+namespace {
+// Strict + fast parameter blocks of the density coder alone (source side).
+int stats_setup(const spcn_xform_params* p, int32_t white, StatsArgs& a, StrictP& sp) {
+  if (!p) return fail(SPCN_EINVAL, "params is NULL");
+  for (int c = 0; c < 3; ++c)
+    if (!(p->src_i0[c] >= 1.0) || !std::isfinite(p->src_i0[c]))
+      return fail(SPCN_EINVAL, "i0 components must be >= 1");
+  int rc = check_basis(p->src_basis, "source");
+  if (rc) return rc;
+  if (!(p->code_lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
+  if (white < 0 || white > 255) return fail(SPCN_EINVAL, "white threshold must be in [0, 255]");
+  double lut[3][256];
+  od_table(p->src_i0, p->od_table, lut);
+  const double one[2] = {1.0, 1.0}, i0t[3] = {255.0, 255.0, 255.0};
+  fill_strict(sp, &lut[0][0], p->src_basis, p->src_basis, one, i0t, p->code_lam, p->max_sweeps);
+  static thread_local FastP fp;
+  const bool ok = fill_fast_scalars(fp, sp, false, fp.lut);
+  a.fs = fp;
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 256; ++i) a.lut[c][i] = static_cast<float>(lut[c][i]);
+  double coef[2];
+  density_error_coeffs(sp, coef);
+  for (int j = 0; j < 2; ++j)   // ill-conditioned basis: every candidate goes through fp64
+    a.coef[j] = ok ? static_cast<float>(coef[j] * (1.0 + 1e-6)) : INFINITY;
+  a.white = static_cast<uint32_t>(white);
+  return SPCN_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int spcn_stats_hist(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
+                    int32_t white_threshold, const uint32_t* base, const uint32_t* shift,
+                    int32_t nbins, unsigned long long* hist, unsigned long long* counts,
+                    void* stream) {
+  g_err.clear();
+  if (npix < 0) return fail(SPCN_EINVAL, "npix must be >= 0");
+  if (nbins < 1 || nbins > 8192) return fail(SPCN_EINVAL, "nbins must be in [1, 8192]");
+  if (!base || !shift || !hist || !counts) return fail(SPCN_EINVAL, "NULL argument");
+  if (npix > 0 && !src) return fail(SPCN_EINVAL, "src is NULL");
+  if (npix > 0 && (reinterpret_cast<uintptr_t>(src) & 15))
+    return fail(SPCN_EINVAL, "src must be 16-byte aligned");
+  static thread_local StatsArgs a;
+  static thread_local StrictP sp;
+  int rc = stats_setup(p, white_threshold, a, sp);
+  if (rc) return rc;
+  for (int j = 0; j < 2; ++j) {
+    if (shift[j] > 31) return fail(SPCN_EINVAL, "shift must be <= 31");
+    a.base[j] = base[j];
+    a.shift[j] = shift[j];
+    a.a[j] = a.b[j] = 0.0;
+  }
+  a.nbins = nbins;
+  const cudaError_t e = launch_stats_hist(src, npix, a, hist, counts,
+                                          static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_hist");
+}
+
+int spcn_stats_refine(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
+                      int32_t white_threshold, const double* lo, const double* hi,
+                      unsigned long long* counts, double* cand, unsigned long long cap,
+                      void* stream) {
+  g_err.clear();
+  if (npix < 0) return fail(SPCN_EINVAL, "npix must be >= 0");
+  if (!lo || !hi || !counts || (cap > 0 && !cand)) return fail(SPCN_EINVAL, "NULL argument");
+  if (npix > 0 && !src) return fail(SPCN_EINVAL, "src is NULL");
+  if (npix > 0 && (reinterpret_cast<uintptr_t>(src) & 15))
+    return fail(SPCN_EINVAL, "src must be 16-byte aligned");
+  static thread_local StatsArgs a;
+  static thread_local StrictP sp;
+  int rc = stats_setup(p, white_threshold, a, sp);
+  if (rc) return rc;
+  for (int j = 0; j < 2; ++j) {
+    a.base[j] = 0;
+    a.shift[j] = 0;
+    a.a[j] = lo[j];
+    a.b[j] = hi[j];
+  }
+  a.nbins = 1;
+  const cudaError_t e = launch_stats_refine(src, npix, a, sp, counts, cand, cap,
+                                            static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_refine");
+}
+
+}  // extern "C"
+
 // ------------------------------------------------------------------ synthetic input
 #include "synth.h"
 

@@ -157,4 +157,21 @@ __host__ __device__ inline bool fill_fast_scalars(FastS& fp, const StrictP& sp, 
   return true;
 }
 
+// Per-pixel error bound of the fp32 densities (fast_density) against the
+// reference's fp64 coder: |h_j - h_ref,j| <= coef[j] * T + 1e-30, T the
+// pixel's t0 + t1 + 4 lam.  Same instruction-by-instruction chain and safety
+// factor as the certification bound in fill_fast_scalars (h0 <- Dh0, h1 <- D1).
+__host__ __device__ inline void density_error_coeffs(const StrictP& sp, double coef[2]) {
+  const double g00 = sp.g00, g01 = sp.g01, g11 = sp.g11, det = sp.det;
+  const double A = g11 / det, C = g01 / det, E = 1.0 / g11, F = g01 / g11, G = 1.0 / g00,
+               H = g01 / g00;
+  const double P0 = A + C, D0 = 8.0 * (A + C);
+  const double D1 = 7.0 * E + F * D0 + 3.0 * F * P0;
+  const double P1 = E + F * P0;
+  const double Dh0 = 7.0 * G + H * D1 + 3.0 * H * P1;
+  const double u = 5.9604644775390625e-08;   // 2^-24
+  coef[0] = 1.25 * 1.001 * u * Dh0;
+  coef[1] = 1.25 * 1.001 * u * D1;
+}
+
 }  // namespace spcn

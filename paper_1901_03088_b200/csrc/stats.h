@@ -1,0 +1,24 @@
+// stats.h — whole-slide percentile passes (internal launch interface).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "spcn_device.cuh"
+
+namespace spcn {
+struct StatsArgs {
+  FastS fs;                 // density coefficients of the source basis
+  float lut[3][256];        // fp32 OD table
+  float coef[2];            // density error bound per unit T (params.cuh density_error_coeffs)
+  uint32_t white;           // white threshold: non-white = not all channels > white
+  uint32_t base[2];         // histogram window start (fp32 key) per stain
+  uint32_t shift[2];        // bin = (key - base) >> shift
+  int32_t nbins;            // <= 8192
+  double a[2], b[2];        // refine window [a, b) per stain
+};
+cudaError_t launch_stats_hist(const uint8_t* src, int64_t npix, const StatsArgs& a,
+                              unsigned long long* hist, unsigned long long* counts,
+                              cudaStream_t st);
+cudaError_t launch_stats_refine(const uint8_t* src, int64_t npix, const StatsArgs& a,
+                                const StrictP& sp, unsigned long long* counts, double* cand,
+                                unsigned long long cap, cudaStream_t st);
+}  // namespace spcn

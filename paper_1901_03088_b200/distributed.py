@@ -74,6 +74,37 @@ def split_takes(takes, per_rank_totals, rank: int):
     return res
 
 
+class TorchComm:
+    """Sum all-reduce and variable-size all-gather over a torch.distributed
+    group (NCCL on GPUs, gloo in the CPU tests) — the collectives of the
+    global-p99 passes."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def allreduce(self, t):
+        import torch.distributed as dist
+
+        dist.all_reduce(t, group=self.group)
+        return t
+
+    def allgather(self, t):
+        import torch
+        import torch.distributed as dist
+
+        world = dist.get_world_size(self.group)
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+        sizes = [torch.empty_like(n) for _ in range(world)]
+        dist.all_gather(sizes, n, group=self.group)
+        sizes = [int(x.item()) for x in sizes]
+        m = max(sizes + [1])
+        pad = torch.zeros(m, dtype=t.dtype, device=t.device)
+        pad[:t.numel()] = t.reshape(-1)
+        out = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(out, pad, group=self.group)
+        return [o[:k] for o, k in zip(out, sizes)]
+
+
 class RowBandGroup:
     """Sample-mode fit of a row-band-sharded slide (one instance per rank)."""
 
@@ -82,7 +113,7 @@ class RowBandGroup:
         self.group = group
 
     def fit(self, band_source, plan=None, cfg=None, *, code_lam: float = 0.0,
-            per_patch_stats: bool = False, source_label: str = ""):
+            per_patch_stats: bool = False, source_label: str = "", p99_mode: str = "sample"):
         import torch
         import torch.distributed as dist
 
@@ -166,7 +197,16 @@ class RowBandGroup:
         info = r.info.cpu().numpy()[0]
         snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
         h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
-        if per_patch_stats:
+        if p99_mode == "global":
+            from .global_stats import global_p99
+            from .normalize import StainStats
+            from .pipeline import slide_chunks
+
+            p99, nonwhite, _ = _stage("density stats", global_p99, slide_chunks(band_source), i0,
+                                      r.basis.cpu().numpy()[0], code_lam, thr,
+                                      comm=TorchComm(self.group))
+            st = StainStats(p99=p99, sample_count=int(nonwhite))
+        elif per_patch_stats:
             from . import stats as dstats
 
             counts = [c for c in used_counts if c > 0]
@@ -176,6 +216,8 @@ class RowBandGroup:
                         patch_p99s=[tuple(v) for v in vals.cpu().numpy()], sample_count=m)
         else:
             st = _stage("density stats", stain_stats, h)
-        prov = {"source": str(source_label),
-                "config_hash": config_hash(_cfg_fields(plan, cfg, code_lam, per_patch_stats))}
+        fields = _cfg_fields(plan, cfg, code_lam, per_patch_stats)
+        if p99_mode != "sample":
+            fields["p99_mode"] = p99_mode
+        prov = {"source": str(source_label), "config_hash": config_hash(fields)}
         return FitParams(i0=i0, basis=r.basis.cpu().numpy()[0], stats=st, provenance=prov)

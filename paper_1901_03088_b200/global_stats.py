@@ -1,0 +1,219 @@
+"""Whole-slide ("global") per-stain 99th percentile — ``p99_mode="global"``.
+
+The reference's stain_stats (src/normalize.py:58-100) pools the densities of
+the <= 100 k *sampled* non-white pixels (src/pipeline.py:226,238); that stays
+the default (``p99_mode="sample"``).  Global mode (SURVEY.md §8(0).3, §8(a)
+a7) pools the densities of every non-white pixel of the slide (non-white = not
+all channels > white threshold, src/pipeline.py:176), coded with the fitted
+basis exactly as code_densities (src/stain_sep.py:168-201) would, and returns
+exactly ``percentile(those densities, 99)`` (src/order_stats.py:11-36).
+
+Passes over the slide (csrc/stats.cu):
+  1. coarse histogram of fp32 densities (8192 bins of fp32 keys)   — K2
+  2. fine histogram around the bins holding ranks lo / hi          — K2
+  3. exact refine: fp64 reference-order densities for the pixels that may
+     fall in the final window, exact counts below it, the in-window values
+     listed, then an exact select of the two ranks                  — K3
+Across GPUs the histograms/counts are summed (``allreduce``, NCCL) and the
+candidate lists gathered (``allgather``), SURVEY §8(e).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _dev, _lib
+from .errors import StainAbsentError
+from .order_stats import interpolate
+
+NBINS = 8192
+SHIFT0 = 19              # fp32 key >> 19: 8192 bins over all non-negative floats
+CAND_CAP = 1 << 20       # in-window values listed per stain per rank
+
+_U32x2 = ctypes.c_uint32 * 2
+_F64x2 = ctypes.c_double * 2
+
+
+def _sig():
+    L = _lib.lib()
+    if not getattr(L, "_spcn_gstats_declared", False):
+        P, I32, I64 = _lib.P, _lib.I32, _lib.I64
+        _lib.declare("spcn_stats_hist", ctypes.c_int,
+                     [P, I64, ctypes.POINTER(_lib.XformParams), I32, P, P, I32, P, P, P])
+        _lib.declare("spcn_stats_refine", ctypes.c_int,
+                     [P, I64, ctypes.POINTER(_lib.XformParams), I32, P, P, P, P, ctypes.c_uint64,
+                      P])
+        L._spcn_gstats_declared = True
+    return L
+
+
+def _key_value(key: int) -> float:
+    """fp32 whose bit pattern is `key` (non-negative floats), as a double."""
+    if key >= 0x7F800000:
+        return math.inf
+    return float(np.array([key], dtype=np.uint32).view(np.float32)[0])
+
+
+def _locate(hist: np.ndarray, rank: int):
+    """Bin holding `rank` (0-based) of a histogram, or None past the end."""
+    c = np.cumsum(hist, dtype=np.int64)
+    b = int(np.searchsorted(c, rank, side="right"))
+    return b if b < hist.size else None
+
+
+class _Local:
+    """Single-process reductions (identity)."""
+
+    @staticmethod
+    def allreduce(t):
+        return t
+
+    @staticmethod
+    def allgather(t):
+        return [t]
+
+
+class DeviceEngine:
+    """The two device passes (csrc/stats.cu) over a rank's part of the slide."""
+
+    def __init__(self, chunks, src_i0, basis, code_lam, white_threshold, max_sweeps=2000):
+        from .xform import XformPlan
+
+        self.t = _dev.torch()
+        self.L = _sig()
+        self.chunks = chunks
+        basis = np.asarray(basis, dtype=np.float64)
+        self.plan = XformPlan(src_i0, basis, code_lam, [1.0, 1.0], basis, [255.0] * 3,
+                              precision="exact", max_sweeps=max_sweeps)
+        self.thr = int(white_threshold)
+
+    def hist(self, base, shift):
+        t, L = self.t, self.L
+        hist = t.zeros((2, NBINS), dtype=t.int64, device="cuda")
+        counts = t.zeros(3, dtype=t.int64, device="cuda")
+        b, s = _U32x2(*base), _U32x2(*shift)
+        for x in self.chunks():
+            _lib.check(L.spcn_stats_hist(_lib.ptr(x), x.numel() // 3, ctypes.byref(self.plan.params),
+                                         self.thr, ctypes.byref(b), ctypes.byref(s), NBINS,
+                                         _lib.ptr(hist), _lib.ptr(counts), _lib.stream_handle()),
+                       "stats_hist")
+        return hist, counts
+
+    def refine(self, lo, hi, cap):
+        t, L = self.t, self.L
+        counts = t.zeros(5, dtype=t.int64, device="cuda")
+        cand = t.empty((2, max(cap, 1)), dtype=t.float64, device="cuda")
+        a, b = _F64x2(*lo), _F64x2(*hi)
+        for x in self.chunks():
+            _lib.check(L.spcn_stats_refine(_lib.ptr(x), x.numel() // 3,
+                                           ctypes.byref(self.plan.params), self.thr,
+                                           ctypes.byref(a), ctypes.byref(b), _lib.ptr(counts),
+                                           _lib.ptr(cand), cap, _lib.stream_handle()),
+                       "stats_refine")
+        return counts, cand
+
+    def select(self, values, ks):
+        from . import stats as dstats
+
+        return dstats.select_kth(values, ks).cpu().numpy()
+
+
+def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: int = 220,
+               p: float = 99.0, *, comm=None, max_sweeps: int = 2000, engine=None):
+    """Exact whole-slide percentile of both stains.
+
+    chunks   : callable returning an iterable of flat CUDA uint8 tensors (RGB8
+               pixel runs, 16-byte aligned) that together cover this rank's
+               part of the slide; called once per pass.
+    comm     : object with ``allreduce(tensor) -> tensor`` (sum) and
+               ``allgather(tensor) -> list`` for multi-GPU; None = one process.
+    engine   : the pass implementation (default: the CUDA kernels; the CPU
+               tests substitute an emulation of their contracts).
+    Returns (p99 ndarray(2), non-white pixel count, info dict).
+    """
+    comm = comm or _Local()
+    eng = engine or DeviceEngine(chunks, src_i0, basis, code_lam, white_threshold, max_sweeps)
+    info = {"passes": 0}
+    import torch as t   # tensor plumbing only (the engine does the compute)
+
+    def hist_pass(base, shift):
+        hist, counts = eng.hist(base, shift)
+        info["passes"] += 1
+        hist, counts = comm.allreduce(hist), comm.allreduce(counts)
+        return hist.cpu().numpy(), counts.cpu().numpy()
+
+    def refine_pass(lo, hi, cap):
+        counts, cand = eng.refine(lo, hi, cap)
+        info["passes"] += 1
+        local = counts.cpu().numpy()
+        lists = []
+        for j in range(2):
+            m = int(min(local[2 + j], cap))
+            parts = comm.allgather(cand[j, :m].contiguous())
+            lists.append(t.cat(parts) if len(parts) > 1 else parts[0])
+        total = comm.allreduce(counts).cpu().numpy()
+        overflow = bool(local[2] > cap or local[3] > cap)
+        return total, lists, overflow
+
+    # pass 1: coarse
+    h0, c0 = hist_pass((0, 0), (SHIFT0, SHIFT0))
+    n = int(c0[0])
+    if n == 0:
+        raise StainAbsentError("stain absent: no non-white pixels in the slide")
+    rank = (p / 100.0) * (n - 1)
+    klo, khi = int(math.floor(rank)), int(math.ceil(rank))
+    # pass 2: fine window around the coarse bins of ranks lo..hi (+1 bin margin)
+    base, shift, coarse = [0, 0], [0, 0], []
+    for j in range(2):
+        blo, bhi = _locate(h0[j], klo), _locate(h0[j], khi)
+        blo = max(0, blo - 1)
+        bhi = bhi + 2
+        coarse.append((blo << SHIFT0, bhi << SHIFT0))
+        width = (bhi - blo) << SHIFT0
+        s = 0
+        while (width >> s) > NBINS:
+            s += 1
+        base[j], shift[j] = blo << SHIFT0, s
+    h1, c1 = hist_pass(base, shift)
+    lo_w, hi_w = [0.0, 0.0], [0.0, 0.0]
+    for j in range(2):
+        below = int(c1[1 + j])
+        flo = _locate(h1[j], klo - below) if klo >= below else None
+        fhi = _locate(h1[j], khi - below) if khi >= below else None
+        if flo is None or fhi is None:          # fine level missed: use the coarse window
+            ka, kb = coarse[j]
+        else:
+            ka = base[j] + (max(0, flo - 1) << shift[j])
+            kb = base[j] + ((fhi + 2) << shift[j])
+        lo_w[j] = -math.inf if ka == 0 else _key_value(ka)
+        hi_w[j] = _key_value(kb)
+    # pass 3: exact refine + select
+    total, cands, overflow = refine_pass(lo_w, hi_w, CAND_CAP)
+    ok = not overflow and all(int(total[j]) <= klo and khi < int(total[j] + total[2 + j])
+                              for j in range(2))
+    if not ok:                                   # widen to the coarse windows once
+        lo_w = [-math.inf if c[0] == 0 else _key_value(c[0]) for c in coarse]
+        hi_w = [_key_value(c[1]) for c in coarse]
+        total, cands, overflow = refine_pass(lo_w, hi_w, 1 << 26)
+        ok = not overflow and all(int(total[j]) <= klo and khi < int(total[j] + total[2 + j])
+                                  for j in range(2))
+        if not ok:
+            raise RuntimeError("global p99: the refine window does not contain the ranks")
+    p99 = np.empty(2)
+    for j in range(2):
+        below = int(total[j])
+        vals = eng.select(cands[j], [klo - below, khi - below])
+        p99[j] = interpolate(vals[0], vals[1], rank)
+    info.update(nonwhite=n, fp64_evaluations=int(total[4]), window=(lo_w, hi_w),
+                candidates=[int(total[2]), int(total[3])])
+    # stain absent (src/normalize.py:91-94): max <= 0, i.e. no positive density
+    for j in range(2):
+        if p99[j] <= 0.0:
+            tot, _, _ = refine_pass([5e-324, 5e-324], [math.inf, math.inf], 0)
+            if int(tot[2 + j]) == 0:
+                names = ("hematoxylin", "eosin")
+                raise StainAbsentError(f"stain absent: no {names[j]} density observed")
+            break
+    return p99, n, info

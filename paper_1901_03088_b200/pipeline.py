@@ -289,10 +289,37 @@ def _cfg_fields(plan, cfg, code_lam, per_patch_stats):
             "per_patch_stats": per_patch_stats}
 
 
+def slide_chunks(slide, rows: int = 2048):
+    """Callable yielding the slide as flat CUDA uint8 runs (for whole-slide
+    passes): a device slide in one piece, a host slide strip by strip through
+    one reusable device buffer (stream-ordered reuse)."""
+    t = _dev.torch()
+
+    def gen():
+        if isinstance(slide, DeviceSource):
+            x = slide.tensor.reshape(-1)
+            if not x.is_contiguous() or x.data_ptr() % 16:
+                x = x.contiguous().clone()
+            yield x
+            return
+        buf = t.empty(rows * slide.width * 3, dtype=t.uint8, device="cuda")
+        for y in range(0, slide.height, rows):
+            h = min(rows, slide.height - y)
+            px = np.ascontiguousarray(slide.read_region(0, y, slide.width, h).pixels).reshape(-1)
+            buf[:px.size].copy_(t.from_numpy(px), non_blocking=_pinned(px))
+            yield buf[:px.size]
+    return gen
+
+
 def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), *,
         code_lam: float = 0.0, per_patch_stats: bool = False, source_label: str = "",
-        stats: RunStats | None = None) -> FitParams:
-    """src/pipeline.py:203-257 on the device."""
+        stats: RunStats | None = None, p99_mode: str = "sample") -> FitParams:
+    """src/pipeline.py:203-257 on the device.
+
+    p99_mode="sample" (default) is the reference; "global" takes the p99 over
+    the densities of every non-white pixel of the slide (global_stats.py)."""
+    if p99_mode not in ("sample", "global"):
+        raise ValueError("p99_mode must be 'sample' or 'global'")
     t = _dev.torch()
     stats = stats if stats is not None else RunStats()
     if isinstance(slide, np.ndarray):
@@ -319,7 +346,13 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
     basis = r.basis.cpu().numpy()[0]
     snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
     h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
-    if per_patch_stats:
+    if p99_mode == "global":
+        from .global_stats import global_p99
+
+        p99, nonwhite, _ = _stage("density stats", global_p99, slide_chunks(slide), i0, basis,
+                                  code_lam, plan.white_threshold)
+        st = StainStats(p99=p99, sample_count=int(nonwhite))
+    elif per_patch_stats:
         from . import stats as dstats
 
         counts = [c for c in meta.patch_counts if c > 0]
@@ -330,8 +363,10 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
     else:
         st = _stage("density stats", stain_stats, h)
     stats.basis_fit_s += time.perf_counter() - t0
-    provenance = {"source": str(source_label),
-                  "config_hash": config_hash(_cfg_fields(plan, cfg, code_lam, per_patch_stats))}
+    fields = _cfg_fields(plan, cfg, code_lam, per_patch_stats)
+    if p99_mode != "sample":
+        fields["p99_mode"] = p99_mode
+    provenance = {"source": str(source_label), "config_hash": config_hash(fields)}
     return FitParams(i0=i0, basis=basis, stats=st, provenance=provenance)
 
 

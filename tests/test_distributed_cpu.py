@@ -122,3 +122,86 @@ def test_split_takes_partitions_global_takes():
     assert got[0] == [(0, 5, 100, [3, 0, 9])]
     assert got[1] == [(0, 5, 105, [3, 1, 1])]
     assert got[2] == []
+
+
+# ---------------------------------------------------------------------------
+# global p99 across ranks: window logic + TorchComm (gloo), passes emulated
+class _NumpyEngine:
+    """Contract of the stats passes on exact densities (fp32 keys for the
+    histograms, exact values for the refine), as the kernels provide them."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def hist(self, base, shift):
+        import torch
+
+        from paper_1901_03088_b200.global_stats import NBINS
+
+        hist = np.zeros((2, NBINS), np.int64)
+        counts = np.zeros(3, np.int64)
+        counts[0] = self.h.shape[1]
+        for j in range(2):
+            keys = self.h[j].astype(np.float32).view(np.uint32).astype(np.int64)
+            counts[1 + j] = int((keys < base[j]).sum())
+            d = (keys[keys >= base[j]] - base[j]) >> shift[j]
+            d = d[d < NBINS]
+            hist[j] += np.bincount(d, minlength=NBINS)[:NBINS]
+        return torch.from_numpy(hist), torch.from_numpy(counts)
+
+    def refine(self, lo, hi, cap):
+        import torch
+
+        counts = np.zeros(5, np.int64)
+        cand = np.zeros((2, max(cap, 1)))
+        for j in range(2):
+            x = self.h[j]
+            counts[j] = int((x < lo[j]).sum())
+            w = x[(x >= lo[j]) & (x < hi[j])]
+            counts[2 + j] = w.size
+            cand[j, :min(cap, w.size)] = w[:cap]
+        return torch.from_numpy(counts), torch.from_numpy(cand)
+
+    def select(self, values, ks):
+        return np.sort(values.numpy())[ks]
+
+
+def _global_worker(rank, world, port, hs, q):
+    import torch.distributed as dist
+
+    from paper_1901_03088_b200 import distributed as dd
+    from paper_1901_03088_b200.global_stats import global_p99
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p99, n, info = global_p99(None, None, None, comm=dd.TorchComm(),
+                                  engine=_NumpyEngine(hs[rank]))
+        q.put((rank, p99.tolist(), n))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_global_p99_two_ranks_gloo():
+    import multiprocessing as mp
+
+    rng = np.random.default_rng(4)
+    n = 50_000
+    h = np.zeros((2, n))
+    h[0] = rng.gamma(2.0, 0.4, n)
+    h[1] = rng.gamma(1.5, 0.3, n)
+    h[:, rng.random(n) < 0.3] = 0.0                   # many exact zeros (clamped densities)
+    hs = [h[:, :20_000], h[:, 20_000:]]              # unequal bands
+    ref = [orc.pct(h[0], 99.0), orc.pct(h[1], 99.0)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_global_worker, args=(r, 2, port, hs, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, p99, cnt in out:
+        assert cnt == n
+        assert p99 == ref, (rank, p99, ref)

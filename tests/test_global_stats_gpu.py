@@ -1,0 +1,76 @@
+"""Whole-slide ("global") p99 mode on the GPU.
+
+Oracle: the reference's percentile (src/order_stats.py:11-36) over the
+reference-order fp64 densities (code_densities, src/stain_sep.py:168-201) of
+every non-white pixel (src/pipeline.py:176).  The result must be identical.
+"""
+import numpy as np
+import pytest
+
+from oracle import spcn_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_global(px, i0, basis, code_lam=0.0, thr=220):
+    flat = px.reshape(-1, 3)
+    nw = ~np.all(flat > thr, axis=1)
+    v = np.ascontiguousarray(orc.od_of(flat[nw], i0).T)
+    h = orc.densities(v, basis, code_lam)
+    return np.array([orc.pct(h[0], 99.0), orc.pct(h[1], 99.0)]), int(nw.sum())
+
+
+@pytest.mark.parametrize("seed,i0,code_lam,layout", [
+    (3, (255, 255, 255), 0.0, "scatter"),
+    (4, (250, 243, 230), 0.0, "block"),
+    (5, (252, 249, 246), 0.05, "scatter"),
+])
+def test_global_p99_matches_reference(seed, i0, code_lam, layout):
+    import torch
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200.global_stats import global_p99
+    from paper_1901_03088_b200.pipeline import slide_chunks
+
+    px, _, _ = orc.render(700, 520, seed, i0=i0, tissue_fraction=0.55, layout=layout)
+    fitp = orc.fit_params(px)
+    ref, n = _oracle_global(px, fitp["i0"], fitp["basis"], code_lam)
+    src = pb.DeviceSource(torch.from_numpy(px).cuda())
+    p99, nw, info = global_p99(slide_chunks(src), fitp["i0"], fitp["basis"], code_lam)
+    assert nw == n
+    assert np.array_equal(p99, ref), (p99, ref, info)
+    assert info["fp64_evaluations"] < 0.05 * n          # only the window is recomputed
+
+
+def test_fit_global_mode_host_and_device_slides():
+    import torch
+
+    import paper_1901_03088_b200 as pb
+
+    px, _, _ = orc.render(1100, 900, 11, i0=(248, 246, 250), tissue_fraction=0.6)
+    for src in (pb.ArraySource(px), pb.DeviceSource(torch.from_numpy(px).cuda())):
+        fp = pb.fit(src, p99_mode="global")
+        ref, n = _oracle_global(px, fp.i0, fp.basis)
+        assert np.array_equal(fp.stats.p99, ref)
+        assert fp.stats.sample_count == n
+    with pytest.raises(ValueError):
+        pb.fit(pb.ArraySource(px), p99_mode="everything")
+
+
+def test_global_p99_large_slide_window_logic():
+    """4 Mpx GPU-rendered slide: the fine window must hold both ranks."""
+    import torch
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200 import synthetic
+    from paper_1901_03088_b200.global_stats import global_p99
+    from paper_1901_03088_b200.pipeline import slide_chunks
+
+    dev = synthetic.render_slide(2048, 2048, 21, tissue_fraction=0.6)
+    px = dev.cpu().numpy()
+    basis = orc.he_basis()
+    i0 = np.array([255.0, 255.0, 255.0])
+    ref, n = _oracle_global(px, i0, basis)
+    p99, nw, info = global_p99(slide_chunks(pb.DeviceSource(dev)), i0, basis)
+    assert nw == n and np.array_equal(p99, ref), (p99, ref, info)
+    assert max(info["candidates"]) < 1 << 20
