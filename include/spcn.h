@@ -246,19 +246,21 @@ int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int
  * counts[1+j]; counts[0] += non-white pixels; h = 0 counts into bin 0 when
  * base[j] == 0).  Approximate: it only places the refine window.
  * spcn_stats_refine: exact classification against [lo[j], hi[j]): densities
- * that may lie in the window are recomputed in fp64 in the reference's order;
- * counts[j] += exact count below lo[j], counts[2+j] += count in the window
- * (the first `cap` values listed in cand[j*cap + i]), counts[4] += fp64
- * evaluations.  All buffers device; hist/counts accumulate (caller zeroes);
- * src 16-byte aligned.  Multi-GPU: sum hist/counts across ranks, gather cand. */
+ * that may lie in the window are recomputed in fp64 in the reference's order
+ * (once per colour per CTA); counts[j] += exact count below lo[j],
+ * counts[2+j] += pixels in the window, listed as counts[5+j] (value, pixel
+ * count) pairs cand[j*cap + i] / cand_count[j*cap + i] (the first `cap`),
+ * counts[4] += fp64 evaluations.  All buffers device; hist/counts accumulate
+ * (caller zeroes; counts has 7 entries); src 16-byte aligned.  Multi-GPU: sum
+ * hist/counts across ranks, gather the (value, count) lists.                */
 int spcn_stats_hist(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
                     int32_t white_threshold, const uint32_t* base, const uint32_t* shift,
                     int32_t nbins, unsigned long long* hist, unsigned long long* counts,
                     void* stream);
 int spcn_stats_refine(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
                       int32_t white_threshold, const double* lo, const double* hi,
-                      unsigned long long* counts, double* cand, unsigned long long cap,
-                      void* stream);
+                      unsigned long long* counts, double* cand, unsigned long long* cand_count,
+                      unsigned long long cap, void* stream);
 
 /* ---- measurement input: synthetic H&E slides --------------------------- */
 typedef struct spcn_synth_params {

@@ -511,11 +511,12 @@ int spcn_stats_hist(const uint8_t* src, int64_t npix, const spcn_xform_params* p
 
 int spcn_stats_refine(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
                       int32_t white_threshold, const double* lo, const double* hi,
-                      unsigned long long* counts, double* cand, unsigned long long cap,
-                      void* stream) {
+                      unsigned long long* counts, double* cand, unsigned long long* cand_count,
+                      unsigned long long cap, void* stream) {
   g_err.clear();
   if (npix < 0) return fail(SPCN_EINVAL, "npix must be >= 0");
-  if (!lo || !hi || !counts || (cap > 0 && !cand)) return fail(SPCN_EINVAL, "NULL argument");
+  if (!lo || !hi || !counts || (cap > 0 && (!cand || !cand_count)))
+    return fail(SPCN_EINVAL, "NULL argument");
   if (npix > 0 && !src) return fail(SPCN_EINVAL, "src is NULL");
   if (npix > 0 && (reinterpret_cast<uintptr_t>(src) & 15))
     return fail(SPCN_EINVAL, "src must be 16-byte aligned");
@@ -530,7 +531,7 @@ int spcn_stats_refine(const uint8_t* src, int64_t npix, const spcn_xform_params*
     a.b[j] = hi[j];
   }
   a.nbins = 1;
-  const cudaError_t e = launch_stats_refine(src, npix, a, sp, counts, cand, cap,
+  const cudaError_t e = launch_stats_refine(src, npix, a, sp, counts, cand, cand_count, cap,
                                             static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_refine");
 }

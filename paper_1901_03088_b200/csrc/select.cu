@@ -49,9 +49,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
     const uint64_t prefix = s_prefix;
     for (int64_t i = q.begin + threadIdx.x; i < q.end; i += kSelThreads) {
       const uint64_t key = key_of(v[i]);
-      if (used == 0 || (key >> (64 - used)) == prefix) {
-        atomicAdd(&hist[(key >> shift) & ((1u << dbits) - 1u)], 1u);
-      }
+      if (used == 0 || (key >> (64 - used)) == prefix)
+        hist_add_agg(hist, (uint32_t)((key >> shift) & ((1u << dbits) - 1u)));
     }
     __syncthreads();
     // locate the digit holding rank k: per-thread chunk sums + block scan
@@ -180,7 +179,7 @@ __device__ uint64_t radix_select(SegShared& sh, const Src& src, int64_t cnt, int
     for (int64_t i = threadIdx.x; i < cnt; i += kSelThreads) {
       const uint64_t key = src(i);
       if (used == 0 || (key >> (64 - used)) == prefix)
-        atomicAdd(&sh.hist[(key >> shift) & ((1u << dbits) - 1u)], 1u);
+        hist_add_agg(sh.hist, (uint32_t)((key >> shift) & ((1u << dbits) - 1u)));
     }
     __syncthreads();
     hist_locate(sh, kBins, k);
@@ -230,7 +229,7 @@ __global__ void __launch_bounds__(kSelThreads) k_p99_seg(const double* __restric
   constexpr uint64_t kWin = (uint64_t)(kTopBins - 1) << kWinShift;
   for (int64_t i = threadIdx.x; i < n; i += kSelThreads) {
     const uint64_t d = mx - key_of(v[i]);
-    if (d < kWin) atomicAdd(&sh.hist[d >> kWinShift], 1u);
+    if (d < kWin) hist_add_agg(sh.hist, (uint32_t)(d >> kWinShift));
   }
   __syncthreads();
   // ranks counted from the top: rt = n - 1 - k

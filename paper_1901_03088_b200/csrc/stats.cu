@@ -19,9 +19,10 @@
 //                   the final window [a, b) with its analytic fp32 error bound
 //                   (params.cuh density_error_coeffs); only densities that may
 //                   lie in the window are recomputed in fp64 in the reference's
-//                   operation order (strict_nnls), counted exactly, and the
-//                   in-window ones listed.  The host checks that the ranks fall
-//                   inside the window and selects them from the list exactly.
+//                   operation order (strict_nnls) — once per colour per CTA —
+//                   counted exactly, and the in-window values listed as
+//                   (value, pixel count) pairs.  The host checks that the ranks
+//                   fall inside the window and selects them exactly.
 //
 // Multi-GPU: histograms and counts are summed across ranks (NCCL all-reduce,
 // SURVEY §8(e)); the candidate lists are all-gathered.
@@ -103,10 +104,20 @@ __global__ void __launch_bounds__(kStThreads, 1)
   LutLayout<kStRep>::lane_consts(threadIdx.x & 31, lc);
   unsigned long long nonwhite = 0, below[2] = {0, 0}, zero[2] = {0, 0};
   const int64_t nblk = (npix + 15) / 16, full = npix / 16;
-  for (int64_t blk = blockIdx.x * (int64_t)kStThreads + threadIdx.x; blk < nblk;
-       blk += (int64_t)gridDim.x * kStThreads) {
+  const int64_t stride = (int64_t)gridDim.x * kStThreads;
+  uint32_t nxt[12];   // software prefetch: the next block is in flight while this one computes
+  int64_t blk = blockIdx.x * (int64_t)kStThreads + threadIdx.x;
+  if (blk < nblk) {
+    if (blk < full) st_load(src, blk, nxt); else st_load_tail(src, blk, npix, nxt);
+  }
+  for (; blk < nblk; blk += stride) {
     uint32_t w[12];
-    if (blk < full) st_load(src, blk, w); else st_load_tail(src, blk, npix, w);
+#pragma unroll
+    for (int t = 0; t < 12; ++t) w[t] = nxt[t];
+    if (blk + stride < nblk) {
+      if (blk + stride < full) st_load(src, blk + stride, nxt);
+      else st_load_tail(src, blk + stride, npix, nxt);
+    }
     float h0[16], h1[16], T[16];
     const uint32_t nw = st_block(a, lut, lc, w, h0, h1, T);
     nonwhite += __popc(nw);
@@ -119,7 +130,7 @@ __global__ void __launch_bounds__(kStThreads, 1)
         if (key == 0u && a.base[j] == 0u) { ++zero[j]; continue; }   // h = 0: bin 0, no atomics
         if (key < a.base[j]) { ++below[j]; continue; }
         const uint32_t d = (key - a.base[j]) >> a.shift[j];
-        if (d < (uint32_t)a.nbins) atomicAdd(&sh[j * kStBins + d], 1u);
+        if (d < (uint32_t)a.nbins) hist_add_agg(sh + j * kStBins, d);
       }
     }
   }
@@ -146,26 +157,70 @@ __global__ void __launch_bounds__(kStThreads, 1)
   }
 }
 
+// Per-CTA colour cache of the refine pass: a density is a function of the
+// pixel's RGB only, and the pixels that can fall in the narrow window share
+// few colours, so each CTA evaluates a colour in fp64 once and keeps in-window
+// pixel counts per colour; at the end it lists (value, count) pairs.
+constexpr int kSlots = 2048;
+constexpr uint32_t kEmpty = 0xffffffffu;
+struct ColourSlot {
+  uint32_t key;        // rgb, or kEmpty
+  uint32_t ready;      // x valid
+  uint32_t cnt[2];     // in-window pixels per stain
+  double x[2];         // exact densities
+};
+constexpr size_t kStSmemRefine =
+    LutLayout<kStRep>::kBytes + 3 * 256 * sizeof(double) + kSlots * sizeof(ColourSlot);
+
+__device__ __forceinline__ uint32_t colour_hash(uint32_t rgb) {
+  return (rgb * 2654435761u) >> (32 - 11);
+}
+
 __global__ void __launch_bounds__(kStThreads, 1)
     k_stats_refine(const uint8_t* __restrict__ src, int64_t npix,
                    const __grid_constant__ StatsArgs a, const __grid_constant__ StrictP sp,
                    unsigned long long* __restrict__ counts, double* __restrict__ cand,
-                   unsigned long long cap) {
+                   unsigned long long* __restrict__ wcnt, unsigned long long cap) {
   extern __shared__ __align__(128) uint8_t smem[];
   const uint8_t* lut = smem;
   double* dlut = reinterpret_cast<double*>(smem + LutLayout<kStRep>::kBytes);
+  ColourSlot* tab = reinterpret_cast<ColourSlot*>(smem + LutLayout<kStRep>::kBytes +
+                                                  3 * 256 * sizeof(double));
   LutLayout<kStRep>::fill(smem, &a.lut[0][0], threadIdx.x, kStThreads);
   for (int i = threadIdx.x; i < 3 * 256; i += kStThreads) dlut[i] = sp.lut[i >> 8][i & 255];
+  for (int i = threadIdx.x; i < kSlots; i += kStThreads) {
+    tab[i].key = kEmpty;
+    tab[i].ready = 0;
+    tab[i].cnt[0] = tab[i].cnt[1] = 0;
+  }
   __syncthreads();
   uint32_t lc[3];
   LutLayout<kStRep>::lane_consts(threadIdx.x & 31, lc);
   const NnlsGram G = gram_of(sp);
   unsigned long long below[2] = {0, 0}, exact_evals = 0;
   const int64_t nblk = (npix + 15) / 16, full = npix / 16;
-  for (int64_t blk = blockIdx.x * (int64_t)kStThreads + threadIdx.x; blk < nblk;
-       blk += (int64_t)gridDim.x * kStThreads) {
+  auto list = [&](int j, double x, unsigned long long c) {   // one (value, count) entry
+    atomicAdd(&counts[2 + j], c);
+    const unsigned long long idx = atomicAdd(&counts[5 + j], 1ull);
+    if (idx < cap) {
+      cand[j * cap + idx] = x;
+      wcnt[j * cap + idx] = c;
+    }
+  };
+  const int64_t stride = (int64_t)gridDim.x * kStThreads;
+  uint32_t nxt[12];   // software prefetch: the next block is in flight while this one computes
+  int64_t blk = blockIdx.x * (int64_t)kStThreads + threadIdx.x;
+  if (blk < nblk) {
+    if (blk < full) st_load(src, blk, nxt); else st_load_tail(src, blk, npix, nxt);
+  }
+  for (; blk < nblk; blk += stride) {
     uint32_t w[12];
-    if (blk < full) st_load(src, blk, w); else st_load_tail(src, blk, npix, w);
+#pragma unroll
+    for (int t = 0; t < 12; ++t) w[t] = nxt[t];
+    if (blk + stride < nblk) {
+      if (blk + stride < full) st_load(src, blk + stride, nxt);
+      else st_load_tail(src, blk + stride, npix, nxt);
+    }
     float h0[16], h1[16], T[16];
     const uint32_t nw = st_block(a, lut, lc, w, h0, h1, T);
 #pragma unroll
@@ -179,27 +234,66 @@ __global__ void __launch_bounds__(kStThreads, 1)
         if (h + eps < a.a[j]) ++below[j];          // surely below the window
         else if (!(h - eps >= a.b[j])) need |= 1u << j;   // may lie in [a, b)
       }
-      if (need) {
+      if (!need) continue;
+      const uint32_t rgb = st_byte(w, 3 * k) | (st_byte(w, 3 * k + 1) << 8) |
+                           (st_byte(w, 3 * k + 2) << 16);
+      // colour cache: find or claim a slot; a slot claimed but not yet filled
+      // by another thread is simply recomputed here (no waiting)
+      int slot = -1;
+      double x[2];
+      bool have = false;
+      uint32_t s = colour_hash(rgb);
+      for (int probe = 0; probe < 8; ++probe, s = (s + 1) & (kSlots - 1)) {
+        uint32_t key = *(volatile uint32_t*)&tab[s].key;
+        if (key == kEmpty) key = atomicCAS(&tab[s].key, kEmpty, rgb) == kEmpty ? kEmpty - 1 : tab[s].key;
+        if (key == kEmpty - 1) {                   // claimed by us: fill it below
+          slot = (int)s;
+          break;
+        }
+        if (key == rgb) {
+          slot = (int)s;
+          if (*(volatile uint32_t*)&tab[s].ready) {
+            x[0] = tab[s].x[0];
+            x[1] = tab[s].x[1];
+            have = true;
+          }
+          break;
+        }
+      }
+      if (!have) {
         ++exact_evals;
-        const double v0 = dlut[st_byte(w, 3 * k)], v1 = dlut[256 + st_byte(w, 3 * k + 1)],
-                     v2 = dlut[512 + st_byte(w, 3 * k + 2)];
+        const double v0 = dlut[rgb & 255u], v1 = dlut[256 + ((rgb >> 8) & 255u)],
+                     v2 = dlut[512 + (rgb >> 16)];
         const double b0 = strict_dot3(sp.ws[0][0], sp.ws[1][0], sp.ws[2][0], v0, v1, v2);
         const double b1 = strict_dot3(sp.ws[0][1], sp.ws[1][1], sp.ws[2][1], v0, v1, v2);
-        double x[2];
         strict_nnls(b0, b1, G, sp.lam, sp.max_sweeps, sp.tol, x[0], x[1]);
+        if (slot >= 0 && tab[slot].key == rgb && !tab[slot].ready) {
+          tab[slot].x[0] = x[0];
+          tab[slot].x[1] = x[1];
+          __threadfence_block();
+          atomicExch(&tab[slot].ready, 1u);
+        }
+      }
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (!((need >> j) & 1u)) continue;
-          if (x[j] < a.a[j]) {
-            ++below[j];
-          } else if (x[j] < a.b[j]) {
-            const unsigned long long idx = atomicAdd(&counts[2 + j], 1ull);
-            if (idx < cap) cand[j * cap + idx] = x[j];
-          }
+      for (int j = 0; j < 2; ++j) {
+        if (!((need >> j) & 1u)) continue;
+        if (x[j] < a.a[j]) {
+          ++below[j];
+        } else if (x[j] < a.b[j]) {
+          if (slot >= 0) atomicAdd(&tab[slot].cnt[j], 1u);
+          else list(j, x[j], 1ull);                // cache full: list the pixel itself
         }
       }
     }
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSlots; i += kStThreads)
+    for (int j = 0; j < 2; ++j)
+      if (tab[i].cnt[j]) {
+        // counted only by threads that knew the value; its owner set it
+        // (and `ready`) before this barrier
+        list(j, tab[i].x[j], tab[i].cnt[j]);
+      }
   for (int off = 16; off; off >>= 1) {
     exact_evals += __shfl_xor_sync(0xffffffffu, exact_evals, off);
     for (int j = 0; j < 2; ++j) below[j] += __shfl_xor_sync(0xffffffffu, below[j], off);
@@ -242,8 +336,9 @@ cudaError_t launch_stats_hist(const uint8_t* src, int64_t npix, const StatsArgs&
 
 cudaError_t launch_stats_refine(const uint8_t* src, int64_t npix, const StatsArgs& a,
                                 const StrictP& sp, unsigned long long* counts, double* cand,
-                                unsigned long long cap, cudaStream_t st) {
-  constexpr size_t smem = LutLayout<kStRep>::kBytes + 3 * 256 * sizeof(double);
+                                unsigned long long* wcnt, unsigned long long cap,
+                                cudaStream_t st) {
+  constexpr size_t smem = kStSmemRefine;
   static bool attr = false;
   if (!attr) {
     const cudaError_t e = cudaFuncSetAttribute(k_stats_refine, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -255,7 +350,7 @@ cudaError_t launch_stats_refine(const uint8_t* src, int64_t npix, const StatsArg
   const int64_t nblk = (npix + 15) / 16;
   int64_t grid = (nblk + kStThreads - 1) / kStThreads;
   if (grid > st_grid()) grid = st_grid();
-  k_stats_refine<<<(int)grid, kStThreads, smem, st>>>(src, npix, a, sp, counts, cand, cap);
+  k_stats_refine<<<(int)grid, kStThreads, smem, st>>>(src, npix, a, sp, counts, cand, wcnt, cap);
   return launched();
 }
 

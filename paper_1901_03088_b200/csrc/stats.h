@@ -20,5 +20,6 @@ cudaError_t launch_stats_hist(const uint8_t* src, int64_t npix, const StatsArgs&
                               cudaStream_t st);
 cudaError_t launch_stats_refine(const uint8_t* src, int64_t npix, const StatsArgs& a,
                                 const StrictP& sp, unsigned long long* counts, double* cand,
-                                unsigned long long cap, cudaStream_t st);
+                                unsigned long long* wcnt, unsigned long long cap,
+                                cudaStream_t st);
 }  // namespace spcn

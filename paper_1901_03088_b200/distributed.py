@@ -202,9 +202,15 @@ class RowBandGroup:
             from .normalize import StainStats
             from .pipeline import slide_chunks
 
+            from .errors import SlideNormError
+
+            try:
+                guess = stain_stats(h).p99
+            except SlideNormError:
+                guess = None
             p99, nonwhite, _ = _stage("density stats", global_p99, slide_chunks(band_source), i0,
                                       r.basis.cpu().numpy()[0], code_lam, thr,
-                                      comm=TorchComm(self.group))
+                                      comm=TorchComm(self.group), guess=guess)
             st = StainStats(p99=p99, sample_count=int(nonwhite))
         elif per_patch_stats:
             from . import stats as dstats

@@ -30,7 +30,8 @@ from .order_stats import interpolate
 
 NBINS = 8192
 SHIFT0 = 19              # fp32 key >> 19: 8192 bins over all non-negative floats
-CAND_CAP = 1 << 20       # in-window values listed per stain per rank
+CAND_CAP = 1 << 20       # in-window values listed per stain per rank (grown as needed)
+MIN_SHIFT = 6            # finest bins: 64 fp32 ulps, > 2x the fp32 density error
 
 _U32x2 = ctypes.c_uint32 * 2
 _F64x2 = ctypes.c_double * 2
@@ -43,8 +44,8 @@ def _sig():
         _lib.declare("spcn_stats_hist", ctypes.c_int,
                      [P, I64, ctypes.POINTER(_lib.XformParams), I32, P, P, I32, P, P, P])
         _lib.declare("spcn_stats_refine", ctypes.c_int,
-                     [P, I64, ctypes.POINTER(_lib.XformParams), I32, P, P, P, P, ctypes.c_uint64,
-                      P])
+                     [P, I64, ctypes.POINTER(_lib.XformParams), I32, P, P, P, P, P,
+                      ctypes.c_uint64, P])
         L._spcn_gstats_declared = True
     return L
 
@@ -54,6 +55,11 @@ def _key_value(key: int) -> float:
     if key >= 0x7F800000:
         return math.inf
     return float(np.array([key], dtype=np.uint32).view(np.float32)[0])
+
+
+def _key_of(x: float) -> int:
+    """fp32 bit pattern (as int) of a non-negative value."""
+    return int(np.array([x], dtype=np.float32).view(np.uint32)[0])
 
 
 def _locate(hist: np.ndarray, rank: int):
@@ -102,26 +108,33 @@ class DeviceEngine:
         return hist, counts
 
     def refine(self, lo, hi, cap):
+        """-> counts (7: below[2], in-window pixels[2], fp64 evals, list sizes[2]),
+        values (2, cap), pixel counts (2, cap)."""
         t, L = self.t, self.L
-        counts = t.zeros(5, dtype=t.int64, device="cuda")
+        counts = t.zeros(7, dtype=t.int64, device="cuda")
         cand = t.empty((2, max(cap, 1)), dtype=t.float64, device="cuda")
+        wcnt = t.empty((2, max(cap, 1)), dtype=t.int64, device="cuda")
         a, b = _F64x2(*lo), _F64x2(*hi)
         for x in self.chunks():
             _lib.check(L.spcn_stats_refine(_lib.ptr(x), x.numel() // 3,
                                            ctypes.byref(self.plan.params), self.thr,
                                            ctypes.byref(a), ctypes.byref(b), _lib.ptr(counts),
-                                           _lib.ptr(cand), cap, _lib.stream_handle()),
-                       "stats_refine")
-        return counts, cand
+                                           _lib.ptr(cand), _lib.ptr(wcnt), cap,
+                                           _lib.stream_handle()), "stats_refine")
+        return counts, cand, wcnt
 
-    def select(self, values, ks):
-        from . import stats as dstats
 
-        return dstats.select_kth(values, ks).cpu().numpy()
+def weighted_select(values: np.ndarray, weights: np.ndarray, ks):
+    """Order statistics of the multiset {values[i] repeated weights[i] times}
+    (exact: a stable sort of the distinct values and integer cumulative
+    counts)."""
+    order = np.argsort(values, kind="stable")
+    v, c = values[order], np.cumsum(weights[order].astype(np.int64))
+    return [float(v[int(np.searchsorted(c, k, side="right"))]) for k in ks]
 
 
 def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: int = 220,
-               p: float = 99.0, *, comm=None, max_sweeps: int = 2000, engine=None):
+               p: float = 99.0, *, comm=None, max_sweeps: int = 2000, engine=None, guess=None):
     """Exact whole-slide percentile of both stains.
 
     chunks   : callable returning an iterable of flat CUDA uint8 tensors (RGB8
@@ -131,6 +144,8 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
                ``allgather(tensor) -> list`` for multi-GPU; None = one process.
     engine   : the pass implementation (default: the CUDA kernels; the CPU
                tests substitute an emulation of their contracts).
+    guess    : optional estimate of the two percentiles (the sample p99): the
+               first histogram level then spans +-2 octaves around it.
     Returns (p99 ndarray(2), non-white pixel count, info dict).
     """
     comm = comm or _Local()
@@ -145,66 +160,89 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
         return hist.cpu().numpy(), counts.cpu().numpy()
 
     def refine_pass(lo, hi, cap):
-        counts, cand = eng.refine(lo, hi, cap)
+        counts, cand, wcnt = eng.refine(lo, hi, cap)
         info["passes"] += 1
         local = counts.cpu().numpy()
         lists = []
         for j in range(2):
-            m = int(min(local[2 + j], cap))
-            parts = comm.allgather(cand[j, :m].contiguous())
-            lists.append(t.cat(parts) if len(parts) > 1 else parts[0])
+            m = int(min(local[5 + j], cap))
+            vals = comm.allgather(cand[j, :m].contiguous())
+            cnts = comm.allgather(wcnt[j, :m].contiguous())
+            lists.append((t.cat(vals).cpu().numpy(), t.cat(cnts).cpu().numpy()))
         total = comm.allreduce(counts).cpu().numpy()
-        overflow = bool(local[2] > cap or local[3] > cap)
+        overflow = bool(local[5] > cap or local[6] > cap)
         return total, lists, overflow
 
-    # pass 1: coarse
-    h0, c0 = hist_pass((0, 0), (SHIFT0, SHIFT0))
-    n = int(c0[0])
+    # histogram levels: start over all fp32 keys, then zoom into the bins
+    # holding ranks lo..hi (one bin of margin each side) until the window is
+    # small enough to list, or its bins reach the fp32 error scale
+    base, shift = [0, 0], [SHIFT0, SHIFT0]
+    if guess is not None and all(g > 0 and math.isfinite(g) for g in guess):
+        # start from +-2 octaves around an estimate (e.g. the sample p99); a
+        # miss falls back to the full-range level below
+        for j in range(2):
+            k0 = _key_of(guess[j] / 4.0)
+            base[j], shift[j] = k0, max(MIN_SHIFT, ((_key_of(guess[j] * 4.0) - k0) // NBINS)
+                                         .bit_length())
+    h, c = hist_pass(base, shift)
+    n = int(c[0])
     if n == 0:
         raise StainAbsentError("stain absent: no non-white pixels in the slide")
     rank = (p / 100.0) * (n - 1)
     klo, khi = int(math.floor(rank)), int(math.ceil(rank))
-    # pass 2: fine window around the coarse bins of ranks lo..hi (+1 bin margin)
-    base, shift, coarse = [0, 0], [0, 0], []
-    for j in range(2):
-        blo, bhi = _locate(h0[j], klo), _locate(h0[j], khi)
-        blo = max(0, blo - 1)
-        bhi = bhi + 2
-        coarse.append((blo << SHIFT0, bhi << SHIFT0))
-        width = (bhi - blo) << SHIFT0
-        s = 0
-        while (width >> s) > NBINS:
-            s += 1
-        base[j], shift[j] = blo << SHIFT0, s
-    h1, c1 = hist_pass(base, shift)
-    lo_w, hi_w = [0.0, 0.0], [0.0, 0.0]
-    for j in range(2):
-        below = int(c1[1 + j])
-        flo = _locate(h1[j], klo - below) if klo >= below else None
-        fhi = _locate(h1[j], khi - below) if khi >= below else None
-        if flo is None or fhi is None:          # fine level missed: use the coarse window
-            ka, kb = coarse[j]
-        else:
-            ka = base[j] + (max(0, flo - 1) << shift[j])
-            kb = base[j] + ((fhi + 2) << shift[j])
-        lo_w[j] = -math.inf if ka == 0 else _key_value(ka)
-        hi_w[j] = _key_value(kb)
-    # pass 3: exact refine + select
-    total, cands, overflow = refine_pass(lo_w, hi_w, CAND_CAP)
-    ok = not overflow and all(int(total[j]) <= klo and khi < int(total[j] + total[2 + j])
-                              for j in range(2))
-    if not ok:                                   # widen to the coarse windows once
-        lo_w = [-math.inf if c[0] == 0 else _key_value(c[0]) for c in coarse]
-        hi_w = [_key_value(c[1]) for c in coarse]
-        total, cands, overflow = refine_pass(lo_w, hi_w, 1 << 26)
+    if guess is not None and base != [0, 0]:
+        inside = all(int(c[1 + j]) <= klo and khi < int(c[1 + j] + h[j].sum()) for j in range(2))
+        if not inside:
+            base, shift = [0, 0], [SHIFT0, SHIFT0]
+            h, c = hist_pass(base, shift)
+    windows = []                          # key windows of every level, outermost first
+    while True:
+        win, est = [], []
+        for j in range(2):
+            below = int(c[1 + j])
+            flo = _locate(h[j], klo - below) if klo >= below else None
+            fhi = _locate(h[j], khi - below) if khi >= below else None
+            if flo is None or fhi is None:   # lost the ranks: keep the previous window
+                win = None
+                break
+            f0, f1 = max(0, flo - 1), min(NBINS, fhi + 2)
+            win.append((base[j] + (f0 << shift[j]), base[j] + (f1 << shift[j])))
+            est.append(int(h[j][f0:f1].sum()))
+        if win is None:
+            break
+        windows.append((win, max(est)))
+        if max(est) <= CAND_CAP // 4 or min(shift) < MIN_SHIFT + 1:
+            break
+        for j in range(2):
+            width = win[j][1] - win[j][0]
+            s_ = 0
+            while (width >> s_) > NBINS:
+                s_ += 1
+            base[j], shift[j] = win[j][0], max(s_, MIN_SHIFT)
+        h, c = hist_pass(base, shift)
+    info["levels"] = len(windows)
+
+    def keys_to_values(win):
+        return ([-math.inf if k[0] == 0 else _key_value(k[0]) for k in win],
+                [_key_value(k[1]) for k in win])
+
+    # pass: exact refine of the innermost window (widen outward if it misses)
+    for win, est in reversed(windows):
+        lo_w, hi_w = keys_to_values(win)
+        cap = max(CAND_CAP, 2 * est + 4096)
+        total, cands, overflow = refine_pass(lo_w, hi_w, cap)
+        info.setdefault("refines", []).append(dict(window=(lo_w, hi_w), below=total[:2].tolist(),
+                                                   inwin=total[2:4].tolist(), overflow=overflow))
         ok = not overflow and all(int(total[j]) <= klo and khi < int(total[j] + total[2 + j])
                                   for j in range(2))
-        if not ok:
-            raise RuntimeError("global p99: the refine window does not contain the ranks")
+        if ok:
+            break
+    else:
+        raise RuntimeError(f"global p99: no refine window contains the ranks ({info})")
     p99 = np.empty(2)
     for j in range(2):
         below = int(total[j])
-        vals = eng.select(cands[j], [klo - below, khi - below])
+        vals = weighted_select(cands[j][0], cands[j][1], [klo - below, khi - below])
         p99[j] = interpolate(vals[0], vals[1], rank)
     info.update(nonwhite=n, fp64_evaluations=int(total[4]), window=(lo_w, hi_w),
                 candidates=[int(total[2]), int(total[3])])

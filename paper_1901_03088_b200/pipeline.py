@@ -349,8 +349,12 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
     if p99_mode == "global":
         from .global_stats import global_p99
 
+        try:                              # the sample p99 seeds the first histogram level
+            guess = stain_stats(h).p99
+        except SlideNormError:
+            guess = None
         p99, nonwhite, _ = _stage("density stats", global_p99, slide_chunks(slide), i0, basis,
-                                  code_lam, plan.white_threshold)
+                                  code_lam, plan.white_threshold, guess=guess)
         st = StainStats(p99=p99, sample_count=int(nonwhite))
     elif per_patch_stats:
         from . import stats as dstats

@@ -152,18 +152,19 @@ class _NumpyEngine:
     def refine(self, lo, hi, cap):
         import torch
 
-        counts = np.zeros(5, np.int64)
+        counts = np.zeros(7, np.int64)
         cand = np.zeros((2, max(cap, 1)))
+        wcnt = np.zeros((2, max(cap, 1)), np.int64)
         for j in range(2):
             x = self.h[j]
             counts[j] = int((x < lo[j]).sum())
             w = x[(x >= lo[j]) & (x < hi[j])]
             counts[2 + j] = w.size
-            cand[j, :min(cap, w.size)] = w[:cap]
-        return torch.from_numpy(counts), torch.from_numpy(cand)
-
-    def select(self, values, ks):
-        return np.sort(values.numpy())[ks]
+            u, c = np.unique(w, return_counts=True)        # (value, count) pairs
+            counts[5 + j] = u.size
+            cand[j, :min(cap, u.size)] = u[:cap]
+            wcnt[j, :min(cap, u.size)] = c[:cap]
+        return torch.from_numpy(counts), torch.from_numpy(cand), torch.from_numpy(wcnt)
 
 
 def _global_worker(rank, world, port, hs, q):

