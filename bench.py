@@ -59,8 +59,9 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the CPU-baseline band")
     ap.add_argument("--p99-mode", choices=("sample", "global"), default="sample",
                     help="sample = reference semantics (default); global = whole-slide p99 passes")
-    ap.add_argument("--workload", choices=("wsi", "batch"), default="wsi",
-                    help="wsi = configs[3] (default); batch = configs[1] (4096 x 512^2 patches)")
+    ap.add_argument("--workload", choices=("wsi", "batch", "tile"), default="wsi",
+                    help="wsi = configs[3] (default); batch = configs[1] (4096 x 512^2 "
+                         "patches); tile = configs[0] (2048^2 tile vs 2048^2 target)")
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--patch", type=int, default=512)
     ap.add_argument("--cpu-patches", type=int, default=8, help="patches in the CPU-baseline sample")
@@ -375,6 +376,82 @@ def _hbm_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# --------------------------------------------------------------------------- tile (configs[0])
+def run_tile(args, rank, world, local):
+    """C1: one 2048^2 tile normalized to a 2048^2 target — pb.normalize (fit
+    source + fit target + transform), the reference's _normalize_one."""
+    import torch
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200 import _lib, synthetic
+
+    side = 2048
+    dev = torch.device("cuda", local if world > 1 else 0)
+    src = synthetic.render_slide(side, side, args.seed + 10 * rank, tissue_fraction=0.6)
+    tgt = synthetic.render_slide(side, side, args.seed + 1, tissue_fraction=0.6)
+    for _ in range(args.warmup):
+        pb.normalize(src, tgt, precision=args.precision, p99_mode=args.p99_mode)
+    torch.cuda.synchronize()
+    L = _lib.lib()
+    launches0 = L.spcn_launch_count()
+    clocks = Clocks(dev.index if dev.index is not None else 0)
+    clocks.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        pb.normalize(src, tgt, precision=args.precision, p99_mode=args.p99_mode)
+    t1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = L.spcn_launch_count() - launches0
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    npx = side * side
+    line = {"metric": METRIC, "value": round(npx * world / (ms * 1e-3) / 1e6, 3), "unit": "Mpx/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (on-GPU generator, model of src/synthetic.py)",
+            "config": {"workload": "C1: 2048x2048 tile normalized to a 2048x2048 target "
+                                   "(fit both + transform, reference defaults)",
+                       "precision": args.precision, "p99_mode": args.p99_mode,
+                       "l2": "per-step working set 25 MB fits L2 (fit-dominated step)"},
+            "gpu_launches": int(launches), "clocks": clk}
+    if not args.no_e2e:
+        s_np, t_np = src.cpu().numpy(), tgt.cpu().numpy()
+        times = []
+        for i in range(args.e2e_steps + 1):
+            a = time.perf_counter()
+            pb.normalize(s_np, t_np, precision=args.precision, p99_mode=args.p99_mode)
+            if i:
+                times.append(time.perf_counter() - a)
+        sec = min(times)
+        line["e2e"] = {"value": round(npx * world / sec / 1e6, 3), "unit": "Mpx/s",
+                       "h2d_bytes_per_step": 2 * 3 * npx, "d2h_bytes_per_step": 3 * npx,
+                       "seconds_per_step": round(sec, 4),
+                       "path": "pb.normalize(numpy source, numpy target) -> numpy"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import spcn_oracle as orc
+
+        s_np, t_np = src.cpu().numpy(), tgt.cpu().numpy()
+        a = time.perf_counter()
+        fs, ft = orc.fit_params(s_np), orc.fit_params(t_np)
+        orc.run_transform(s_np, fs, ft, strip_height=64, workers=os.cpu_count() or 1)
+        sec = time.perf_counter() - a
+        line["cpu_baseline"] = {"value": round(npx / sec / 1e6, 3), "unit": "Mpx/s",
+                                "cores": os.cpu_count() or 1, "kind": "port",
+                                "sample": f"the whole C1 step (fit source + fit target + "
+                                          f"transform, strip 64) with the oracle port: {sec:.2f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 # --------------------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local):
     import torch
@@ -573,6 +650,8 @@ def main():
         return run_reference(args, rank, world)
     if args.workload == "batch":
         return run_batch(args, rank, world, local)
+    if args.workload == "tile":
+        return run_tile(args, rank, world, local)
     return run_ours(args, rank, world, local)
 
 

@@ -505,7 +505,8 @@ def _transform_streamed(slide, sink, plan, strips, width, nslots, gauge, progres
 def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
               cfg: SnmfConfig = SnmfConfig(), code_lam: float = 0.0,
               per_patch_stats: bool = False, strip_height: int = DEFAULT_STRIP_HEIGHT,
-              precision: str = "exact", stats: RunStats | None = None):
+              precision: str = "exact", stats: RunStats | None = None,
+              p99_mode: str = "sample"):
     """The drop-in entry: fit(source), fit(target) (or use a FitParams / profile
     for the target), then transform — exactly the reference's _normalize_one
     (src/cli.py:220-244).  numpy in → numpy out; CUDA tensor in → CUDA tensor out."""
@@ -521,8 +522,10 @@ def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
         tp = load_profile(target)
     else:
         tsrc = ArraySource(target) if not _dev.is_tensor(target) else DeviceSource(target)
-        tp = fit(tsrc, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats)
-    sp = fit(src, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats, stats=stats)
+        tp = fit(tsrc, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats,
+                 p99_mode=p99_mode)
+    sp = fit(src, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats, stats=stats,
+             p99_mode=p99_mode)
     if host:
         sink = ArrayWriter(src.width, src.height)
         transform(src, sp, tp, sink, strip_height=strip_height, code_lam=code_lam, stats=stats,
