@@ -227,6 +227,22 @@ def c1_fixture():
     return out
 
 
+def make_profile_fixture(out_dir):
+    """A profile file written by the reference's own save_profile
+    (src/normalize.py:160-190), for the byte-compatibility test."""
+    import importlib
+
+    import numpy as np
+
+    rn = importlib.import_module("slidenorm.normalize")
+    rs = importlib.import_module("slidenorm.stain_sep")
+    w = rn.FitParams(i0=np.array([250., 244., 251.5]), basis=rs.reference_basis(),
+                     stats=rn.StainStats(p99=np.array([1.2534567890123456, 0.5]),
+                                         sample_count=1234),
+                     provenance={"source": "slide_7.tif", "config_hash": "0f1e2d"})
+    rn.save_profile(os.path.join(out_dir, "profile_ref.txt"), w)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     for name, fn in [("optics", optics_fixture), ("coder", coder_fixture),
@@ -236,7 +252,9 @@ def main():
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)
         print(f"{path}: {os.path.getsize(path) / 1e6:.2f} MB")
+    make_profile_fixture(OUT)
 
 
 if __name__ == "__main__":
     main()
+

@@ -107,3 +107,19 @@ def test_profile_round_trip(tmp_path):
     assert np.array_equal(back.i0, p.i0) and np.array_equal(back.basis, p.basis)
     assert np.array_equal(back.stats.p99, p.stats.p99)
     assert back.provenance == p.provenance
+
+
+def test_profile_files_byte_compatible_with_reference(tmp_path):
+    """A profile written by the reference's save_profile (fixture made by
+    oracle/make_golden.py) loads, and is written back byte for byte."""
+    from conftest import GOLDEN as GOLDEN_DIR
+
+    import paper_1901_03088_b200.normalize as nz
+
+    ref_path = os.path.join(GOLDEN_DIR, "profile_ref.txt")
+    p = nz.load_profile(ref_path)
+    assert p.stats.sample_count == 1234 and p.provenance["source"] == "slide_7.tif"
+    assert p.i0.tolist() == [250.0, 244.0, 251.5]
+    out = tmp_path / "ours.txt"
+    nz.save_profile(out, p)
+    assert out.read_bytes() == open(ref_path, "rb").read()
