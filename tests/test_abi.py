@@ -112,9 +112,11 @@ def test_profile_round_trip(tmp_path):
 def test_profile_files_byte_compatible_with_reference(tmp_path):
     """A profile written by the reference's save_profile (fixture made by
     oracle/make_golden.py) loads, and is written back byte for byte."""
+    import importlib
+
     from conftest import GOLDEN as GOLDEN_DIR
 
-    import paper_1901_03088_b200.normalize as nz
+    nz = importlib.import_module("paper_1901_03088_b200.normalize")
 
     ref_path = os.path.join(GOLDEN_DIR, "profile_ref.txt")
     p = nz.load_profile(ref_path)
