@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-workers", type=int, default=3, help="CUDA streams of the host transform")
     ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the CPU-baseline band")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="gloo: functional check of the N>1 path on one GPU (not a measurement)")
     ap.add_argument("--p99-mode", choices=("sample", "global"), default="sample",
                     help="sample = reference semantics (default); global = whole-slide p99 passes")
     ap.add_argument("--workload", choices=("wsi", "batch", "tile"), default="wsi",
@@ -116,13 +118,28 @@ def dist_setup(args):
     import torch
 
     if world > 1:
+        local = local % max(1, torch.cuda.device_count())   # gloo checks may share one GPU
         torch.cuda.set_device(local)
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:   # code-path check only (host-staged collectives); never for timing
+            dist.init_process_group("gloo")
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
+
+
+def _max_over_ranks(x: float, dev) -> float:
+    """Max of a host scalar over ranks (device tensor under NCCL, host under gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+    tt = torch.tensor([x], device=on, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
 
 
 def band_of(height, rank, world):
@@ -287,9 +304,7 @@ def run_batch(args, rank, world, local):
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / args.steps
     if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = _max_over_ranks(ms, dev)
     npx = n * P * P
     value = npx * world / (ms * 1e-3) / 1e6
     x_ms = statistics.mean(a.elapsed_time(b) for a, b in xform_ms)
@@ -406,9 +421,7 @@ def run_tile(args, rank, world, local):
     launches = L.spcn_launch_count() - launches0
     ms = t0.elapsed_time(t1) / args.steps
     if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = _max_over_ranks(ms, dev)
     npx = side * side
     line = {"metric": METRIC, "value": round(npx * world / (ms * 1e-3) / 1e6, 3), "unit": "Mpx/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -517,9 +530,7 @@ def run_ours(args, rank, world, local):
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / args.steps
     if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = _max_over_ranks(ms, dev)
     total = args.width * args.height
     value = total / (ms * 1e-3) / 1e6
     x_ms = statistics.mean(a.elapsed_time(b) for a, b in xform_ms)
@@ -609,9 +620,7 @@ def e2e(args, pb, slide, target, rank, world):
             fit_s.append(t1 - t0)
     sec = min(times)
     if world > 1:
-        tt = torch.tensor([sec], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        sec = float(tt.item())
+        sec = _max_over_ranks(sec, torch.device("cuda", torch.cuda.current_device()))
     px = use_rows * W * world
     res = {"value": round(px / sec / 1e6, 3), "unit": "Mpx/s",
            "h2d_bytes_per_step": int(use_rows * W * 3), "d2h_bytes_per_step": int(use_rows * W * 3),

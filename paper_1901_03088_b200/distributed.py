@@ -74,6 +74,43 @@ def split_takes(takes, per_rank_totals, rank: int):
     return res
 
 
+def _host_staged(group) -> bool:
+    """gloo moves CUDA tensors only for some collectives: stage through host."""
+    import torch.distributed as dist
+
+    return dist.get_backend(group) == "gloo"
+
+
+def all_reduce_sum(t, group=None):
+    """In-place sum all-reduce of a tensor on any device (NCCL: device-direct)."""
+    import torch.distributed as dist
+
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
+    return t
+
+
+def all_gather_list(t, group=None):
+    """All-gather of equal-shape tensors → list (host-staged under gloo)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    src = t.cpu() if (t.is_cuda and _host_staged(group)) else t
+    out = [torch_empty_like(src) for _ in range(world)]
+    dist.all_gather(out, src, group=group)
+    return [o.to(t.device) for o in out]
+
+
+def torch_empty_like(t):
+    import torch
+
+    return torch.empty_like(t)
+
+
 class TorchComm:
     """Sum all-reduce and variable-size all-gather over a torch.distributed
     group (NCCL on GPUs, gloo in the CPU tests) — the collectives of the
@@ -83,26 +120,17 @@ class TorchComm:
         self.group = group
 
     def allreduce(self, t):
-        import torch.distributed as dist
-
-        dist.all_reduce(t, group=self.group)
-        return t
+        return all_reduce_sum(t, self.group)
 
     def allgather(self, t):
         import torch
-        import torch.distributed as dist
 
-        world = dist.get_world_size(self.group)
         n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
-        sizes = [torch.empty_like(n) for _ in range(world)]
-        dist.all_gather(sizes, n, group=self.group)
-        sizes = [int(x.item()) for x in sizes]
+        sizes = [int(x.item()) for x in all_gather_list(n, self.group)]
         m = max(sizes + [1])
         pad = torch.zeros(m, dtype=t.dtype, device=t.device)
         pad[:t.numel()] = t.reshape(-1)
-        out = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(out, pad, group=self.group)
-        return [o[:k] for o, k in zip(out, sizes)]
+        return [o[:k] for o, k in zip(all_gather_list(pad, self.group), sizes)]
 
 
 class RowBandGroup:
@@ -153,8 +181,7 @@ class RowBandGroup:
             local_tot[present] = cnt_dev.sum(dim=1).cpu().numpy()
         # all-gather of per-rank totals (ranks in band order)
         lt = torch.from_numpy(local_tot).to(dev)
-        gathered = [torch.empty_like(lt) for _ in range(world)]
-        dist.all_gather(gathered, lt, group=self.group)
+        gathered = all_gather_list(lt, self.group)
         per_rank = np.stack([g.cpu().numpy() for g in gathered])
         glob = per_rank.sum(axis=0)
         takes, used_counts, collected, visited, used = _visit(
@@ -181,8 +208,8 @@ class RowBandGroup:
                                              _lib.ptr(cnt), _lib.ptr(dt), _lib.ptr(sample),
                                              _lib.ptr(hist), _lib.stream_handle()),
                        "sample_compact")
-        dist.all_reduce(sample, group=self.group)     # disjoint writers: sum == gather
-        dist.all_reduce(hist, group=self.group)
+        all_reduce_sum(sample, self.group)     # disjoint writers: sum == gather
+        all_reduce_sum(hist, self.group)
         # --- identical, deterministic fit on every rank
         m = collected
         i0 = _stage("background estimation", optics.i0_from_counts,
