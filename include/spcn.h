@@ -174,8 +174,10 @@ typedef struct spcn_snmf_cfg {
  * od[c*total + i], c = 0..2, in which case `samples`/`luts` are ignored).
  * Writes the ordered basis (nprob x 6, row-major), the objective history
  * (nprob x (max_outer+1)) and info (nprob x 4: iterations, converged, warning
- * flags bit0=no-convergence bit1=one-stain, history length).  hscratch is
- * unused (kept for ABI stability; may be NULL).  All pointers device.      */
+ * flags bit0=no-convergence bit1=one-stain, history length).  hscratch
+ * (optional, >= total + nprob/2 + 1 fp64 words) holds a per-problem table of
+ * distinct sample colours with pixel counts, so each SNMF pass visits every
+ * colour once with its weight; NULL = one visit per sample.  Device pointers. */
 int spcn_snmf_batched(const uint8_t* samples, const double* od, const int64_t* offsets,
                       int32_t nprob,
                       const double* luts, const spcn_snmf_cfg* cfg, double* hscratch,

@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(NT, MINB) k_snmf(
     const int64_t* __restrict__ offsets, int nprob, const double* __restrict__ luts,
     const __grid_constant__ SnmfArgs a, int* __restrict__ ticket,
     int64_t total, double* __restrict__ basis_out, double* __restrict__ hist_out,
-    int32_t* __restrict__ info_out) {
+    int32_t* __restrict__ info_out, const uint32_t* __restrict__ ukey,
+    const uint32_t* __restrict__ ucnt, const int32_t* __restrict__ ucount) {
   cg::cluster_group cluster = cg::this_cluster();
   const int cs = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -114,19 +115,29 @@ __global__ void __launch_bounds__(NT, MINB) k_snmf(
   };
   for (int p = next_problem(-1); p < nprob; p = next_problem(p)) {
     const int64_t o0 = offsets[p], m = offsets[p + 1] - offsets[p];
-    const int64_t lo = o0 + (m * rank) / cs, hi = o0 + (m * (rank + 1)) / cs;
+    // with the colour table: entries [o0, o0 + ucount[p]) of (rgb, pixel count)
+    const int64_t me = ukey ? (int64_t)ucount[p] : m;
+    const int64_t lo = o0 + (me * rank) / cs, hi = o0 + (me * (rank + 1)) / cs;
     if (!od)
       for (int i = tid; i < 3 * 256; i += NT) sh.lut[i] = luts[(int64_t)p * 768 + i];
     if (tid < 6) sh.w[tid] = a.w_init[tid];
     __syncthreads();
     const double lam = a.lam, code_lam = a.lam / 2.0;
-    auto load_od = [&](int64_t i, double& v0, double& v1, double& v2) {
+    // OD of entry i and its weight (pixels of that colour; 1 without the table)
+    auto load_od = [&](int64_t i, double& v0, double& v1, double& v2) -> double {
       if (od) {
         v0 = od[i]; v1 = od[total + i]; v2 = od[2 * total + i];
-      } else {
-        const uint8_t* px = samples + 3 * i;
-        v0 = sh.lut[px[0]]; v1 = sh.lut[256 + px[1]]; v2 = sh.lut[512 + px[2]];
+        return 1.0;
       }
+      if (ukey) {
+        const uint32_t rgb = ukey[i];
+        v0 = sh.lut[rgb & 255u]; v1 = sh.lut[256 + ((rgb >> 8) & 255u)];
+        v2 = sh.lut[512 + (rgb >> 16)];
+        return (double)ucnt[i];
+      }
+      const uint8_t* px = samples + 3 * i;
+      v0 = sh.lut[px[0]]; v1 = sh.lut[256 + px[1]]; v2 = sh.lut[512 + px[2]];
+      return 1.0;
     };
     double* hist = hist_out + (int64_t)p * (a.max_outer + 1);
 
@@ -147,17 +158,21 @@ __global__ void __launch_bounds__(NT, MINB) k_snmf(
       double st[kNStat];
 #pragma unroll
       for (int q = 0; q < kNStat; ++q) st[q] = 0.0;
-      auto accumulate = [&](double v0, double v1, double v2, double h0, double h1) {
+      // weighted sums over colours; with weight 1 every update is the same
+      // single-rounding fma as the unweighted per-pixel sum
+      auto accumulate = [&](double wt, double v0, double v1, double v2, double h0, double h1) {
         const double r0 = v0 - __fma_rn(w01, h1, __dmul_rn(w00, h0));
         const double r1 = v1 - __fma_rn(w11, h1, __dmul_rn(w10, h0));
         const double r2 = v2 - __fma_rn(w21, h1, __dmul_rn(w20, h0));
-        st[0] += r0 * r0 + r1 * r1 + r2 * r2;
-        st[1] += h0;
-        st[2] += h1;
-        st[3] += v0 * h0; st[4] += v0 * h1;
-        st[5] += v1 * h0; st[6] += v1 * h1;
-        st[7] += v2 * h0; st[8] += v2 * h1;
-        st[9] += h0 * h0; st[10] += h0 * h1; st[11] += h1 * h1;
+        st[0] = __fma_rn(wt, __fma_rn(r2, r2, __fma_rn(r1, r1, __dmul_rn(r0, r0))), st[0]);
+        st[1] = __fma_rn(wt, h0, st[1]);
+        st[2] = __fma_rn(wt, h1, st[2]);
+        const double wh0 = __dmul_rn(wt, h0), wh1 = __dmul_rn(wt, h1);
+        st[3] = __fma_rn(v0, wh0, st[3]); st[4] = __fma_rn(v0, wh1, st[4]);
+        st[5] = __fma_rn(v1, wh0, st[5]); st[6] = __fma_rn(v1, wh1, st[6]);
+        st[7] = __fma_rn(v2, wh0, st[7]); st[8] = __fma_rn(v2, wh1, st[8]);
+        st[9] = __fma_rn(h0, wh0, st[9]); st[10] = __fma_rn(h0, wh1, st[10]);
+        st[11] = __fma_rn(h1, wh1, st[11]);
       };
       // two independent pixels per thread per step: their division chains
       // interleave (the fp64 pipe is latency-bound with one)
@@ -165,16 +180,16 @@ __global__ void __launch_bounds__(NT, MINB) k_snmf(
         const bool two = i + NT < hi;
         const int64_t i2 = two ? i + NT : i;
         double a0, a1, a2, c0, c1, c2;
-        load_od(i, a0, a1, a2);
-        load_od(i2, c0, c1, c2);
+        const double wa = load_od(i, a0, a1, a2);
+        const double wc = load_od(i2, c0, c1, c2);
         NnlsState sa = nnls_seed(strict_dot3(w00, w10, w20, a0, a1, a2),
                                  strict_dot3(w01, w11, w21, a0, a1, a2), G, code_lam, 1e-9);
         NnlsState sc = nnls_seed(strict_dot3(w00, w10, w20, c0, c1, c2),
                                  strict_dot3(w01, w11, w21, c0, c1, c2), G, code_lam, 1e-9);
         nnls_finish(sa, G, 500, 1e-9);
         nnls_finish(sc, G, 500, 1e-9);
-        accumulate(a0, a1, a2, sa.x0, sa.x1);
-        if (two) accumulate(c0, c1, c2, sc.x0, sc.x1);
+        accumulate(wa, a0, a1, a2, sa.x0, sa.x1);
+        if (two) accumulate(wc, c0, c1, c2, sc.x0, sc.x1);
       }
       cta_reduce<NT, kNStat>(st, &sh.warp_part[0][0], sh.part[phase & 1]);
       cluster_total(kNStat);
@@ -301,6 +316,120 @@ __global__ void __launch_bounds__(256) k_code_samples(
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_colour_table: the fit samples are 8-bit RGB and repeat heavily (a 100 k
+// sample of an H&E patch holds ~10 k distinct colours), while every SNMF
+// quantity is a function of the colour.  One CTA per problem counts the
+// distinct colours of the problem's samples in a shared-memory hash table and
+// writes them as (rgb, pixel count) entries at the problem's sample offset;
+// the SNMF passes then iterate over ~10x fewer entries with weights.  If the
+// table fills up, the problem's samples are listed one by one with count 1.
+constexpr int kTabBits = 14;
+constexpr int kTabSlots = 1 << kTabBits;
+constexpr uint32_t kTabEmpty = 0xffffffffu;
+
+__global__ void __launch_bounds__(512) k_colour_table(const uint8_t* __restrict__ samples,
+                                                      const int64_t* __restrict__ offsets,
+                                                      int nprob, uint32_t* __restrict__ ukey,
+                                                      uint32_t* __restrict__ ucnt,
+                                                      int32_t* __restrict__ ucount) {
+  extern __shared__ __align__(16) uint32_t tab[];   // keys [kTabSlots], counts [kTabSlots]
+  uint32_t* key = tab;
+  uint32_t* cnt = tab + kTabSlots;
+  __shared__ int s_full, s_used;   // table too full (or a probe failed) -> list the samples
+  __shared__ uint32_t s_scan[512];
+  const int tid = threadIdx.x;
+  for (int p = blockIdx.x; p < nprob; p += gridDim.x) {
+    const int64_t o0 = offsets[p], m = offsets[p + 1] - o0;
+    for (int i = tid; i < kTabSlots; i += 512) {
+      key[i] = kTabEmpty;
+      cnt[i] = 0;
+    }
+    if (tid == 0) s_full = s_used = 0;
+    __syncthreads();
+    for (int64_t i = tid; i < m; i += 512) {
+      const uint8_t* px = samples + 3 * (o0 + i);
+      const uint32_t rgb = px[0] | (px[1] << 8) | (px[2] << 16);
+      // lanes holding the same colour insert once
+      const unsigned peers = __match_any_sync(__activemask(), rgb);
+      if ((int)(tid & 31) != __ffs(peers) - 1) continue;
+      const uint32_t add = __popc(peers);
+      uint32_t slot = (rgb * 2654435761u) >> (32 - kTabBits);
+      bool done = false;
+      for (int probe = 0; probe < 64 && !done; ++probe, slot = (slot + 1) & (kTabSlots - 1)) {
+        uint32_t k = key[slot];
+        if (k == kTabEmpty) {
+          k = atomicCAS(&key[slot], kTabEmpty, rgb);
+          if (k == kTabEmpty && atomicAdd(&s_used, 1) >= (3 * kTabSlots) / 4) s_full = 1;
+        }
+        if (k == kTabEmpty || k == rgb) {
+          atomicAdd(&cnt[slot], add);
+          done = true;
+        }
+      }
+      if (!done) s_full = 1;
+    }
+    __syncthreads();
+    if (!s_full) {
+      // With linear probing the SET of occupied slots, hence every cluster
+      // (maximal run of occupied slots) and its key set, does not depend on
+      // insertion order — only the order inside a cluster does.  Sorting each
+      // cluster by colour makes the entry order, and every later
+      // floating-point summation order, deterministic.
+      for (int s0 = tid; s0 < kTabSlots; s0 += 512) {
+        if (key[s0] == kTabEmpty || key[(s0 - 1) & (kTabSlots - 1)] != kTabEmpty) continue;
+        int len = 1;                                     // this thread owns the cluster at s0
+        while (len < kTabSlots && key[(s0 + len) & (kTabSlots - 1)] != kTabEmpty) ++len;
+        for (int x = 1; x < len; ++x) {                  // insertion sort, clusters are short
+          const int sx = (s0 + x) & (kTabSlots - 1);
+          const uint32_t kx = key[sx], cx = cnt[sx];
+          int y = x - 1;
+          while (y >= 0 && key[(s0 + y) & (kTabSlots - 1)] > kx) {
+            const int sy = (s0 + y) & (kTabSlots - 1), sy1 = (s0 + y + 1) & (kTabSlots - 1);
+            key[sy1] = key[sy];
+            cnt[sy1] = cnt[sy];
+            --y;
+          }
+          const int sd = (s0 + y + 1) & (kTabSlots - 1);
+          key[sd] = kx;
+          cnt[sd] = cx;
+        }
+      }
+      __syncthreads();
+      // compact in slot order (block scan)
+      constexpr int kPer = kTabSlots / 512;
+      uint32_t occ = 0;
+      for (int j = 0; j < kPer; ++j) occ += key[tid * kPer + j] != kTabEmpty;
+      s_scan[tid] = occ;
+      __syncthreads();
+      for (int off = 1; off < 512; off <<= 1) {
+        const uint32_t y = tid >= off ? s_scan[tid - off] : 0u;
+        __syncthreads();
+        s_scan[tid] += y;
+        __syncthreads();
+      }
+      uint32_t pos = s_scan[tid] - occ;
+      for (int j = 0; j < kPer; ++j) {
+        const int sl = tid * kPer + j;
+        if (key[sl] != kTabEmpty) {
+          ukey[o0 + pos] = key[sl];
+          ucnt[o0 + pos] = cnt[sl];
+          ++pos;
+        }
+      }
+      if (tid == 511) ucount[p] = (int32_t)s_scan[511];
+    } else {
+      for (int64_t i = tid; i < m; i += 512) {
+        const uint8_t* px = samples + 3 * (o0 + i);
+        ukey[o0 + i] = px[0] | (px[1] << 8) | (px[2] << 16);
+        ucnt[o0 + i] = 1u;
+      }
+      if (tid == 0) ucount[p] = (int32_t)m;
+    }
+    __syncthreads();
+  }
+}
+
 cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t* offsets, int nprob,
                         const double* luts, const SnmfArgs& a, double* hbuf, int64_t total,
                         double* basis_out, double* hist_out, int32_t* info_out, int cluster,
@@ -320,6 +449,30 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
     if (occ1 < 1) occ1 = 1;
   }
   const bool single = cluster == 1;
+  // colour table in the caller's scratch: keys | counts (total each) | per-problem sizes
+  uint32_t* ukey = nullptr;
+  uint32_t* ucnt = nullptr;
+  int32_t* ucount = nullptr;
+  // (batches only: a single slide's fit runs on a cluster of CTAs, while the
+  // table of one problem is built by one CTA and would cost more than it saves)
+  if (hbuf && !od && samples && single) {
+    static bool attr = false;
+    constexpr int kTabSmem = 2 * kTabSlots * sizeof(uint32_t);
+    if (!attr) {
+      const cudaError_t e0 = cudaFuncSetAttribute(k_colour_table,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kTabSmem);
+      if (e0 != cudaSuccess) return e0;
+      attr = true;
+    }
+    ukey = reinterpret_cast<uint32_t*>(hbuf);
+    ucnt = ukey + total;
+    ucount = reinterpret_cast<int32_t*>(ucnt + total);
+    int g = nprob < 4 * sms ? nprob : 4 * sms;
+    k_colour_table<<<g, 512, kTabSmem, st>>>(samples, offsets, nprob, ukey, ucnt, ucount);
+    const cudaError_t e1 = launched();
+    if (e1 != cudaSuccess) return e1;
+  }
   int* ticket = nullptr;
   if (single && nprob > 1) {
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ticket), sizeof(int), st);
@@ -341,8 +494,11 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const uint32_t* ck = ukey;
+  const uint32_t* cc = ucnt;
+  const int32_t* cu = ucount;
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_snmf<512, 1>, samples, od, offsets, nprob, luts, a,
-                                     ticket, total, basis_out, hist_out, info_out);
+                                     ticket, total, basis_out, hist_out, info_out, ck, cc, cu);
   if (ticket) {
     const cudaError_t e2 = cudaFreeAsync(ticket, st);
     if (e == cudaSuccess) e = e2;

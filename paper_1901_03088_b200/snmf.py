@@ -74,10 +74,14 @@ def snmf_batched(samples, offsets, luts, cfg, cluster: int = 1, od=None) -> Batc
     hist = t.zeros((nprob, cfg.max_outer_iters + 1), dtype=t.float64, device=dev)
     info = t.zeros((nprob, 4), dtype=t.int32, device=dev)
     c = make_cfg(cfg, cluster)
+    # colour-table scratch (keys | counts | per-problem sizes): RGB8 samples only
+    scratch = (t.empty(total + nprob // 2 + 1, dtype=t.float64, device=dev)
+               if od is None and samples is not None else None)
     _lib.check(L.spcn_snmf_batched(
         _lib.ptr(samples) if samples is not None else None,
         _lib.ptr(od) if od is not None else None, _lib.ptr(offsets), nprob,
-        _lib.ptr(luts) if luts is not None else None, ctypes.byref(c), None, total,
+        _lib.ptr(luts) if luts is not None else None, ctypes.byref(c),
+        _lib.ptr(scratch) if scratch is not None else None, total,
         _lib.ptr(basis), _lib.ptr(hist), _lib.ptr(info), _lib.stream_handle()), "snmf_batched")
     return BatchFit(basis.reshape(nprob, 3, 2), hist, info)
 
