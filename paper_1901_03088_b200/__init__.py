@@ -24,6 +24,8 @@ from .pipeline import (  # noqa: F401
     BufferGauge, PixelSample, RunStats, SamplePlan, fit, normalize, sample_pixels, transform,
 )
 from .xform import XformPlan, process_strip  # noqa: F401
-from .batch import BatchFit, fit_batch, normalize_batch, transform_batch  # noqa: F401
+from .batch import (  # noqa: F401
+    BatchFit, fit_batch, normalize_batch, normalize_batch_host, transform_batch,
+)
 
 __version__ = "0.1.0"

@@ -85,20 +85,19 @@ class BatchFit:
                          provenance=dict(self.provenance))
 
 
-def _od_tables_exact(i0: np.ndarray) -> np.ndarray:
-    """(n,3,256) OD tables with the reference's numpy expression, computed once
-    per distinct (channel, i0) value (i0 are order statistics of u8 pools)."""
-    n = i0.shape[0]
-    out = np.empty((n, 3, 256))
+def _od_tables_exact(i0: np.ndarray, device):
+    """(n, 3, 256) fp64 OD tables (CUDA) with the reference's numpy expression
+    (src/optics.py:89-94), evaluated once per distinct (channel, i0) value on
+    the host — i0 are order statistics of 8-bit pools, so there are few — and
+    expanded to the items on the device."""
+    t = _dev.torch()
     ramp = np.arange(256, dtype=np.float64)
+    per_channel = []
     for c in range(3):
         vals, inv = np.unique(i0[:, c], return_inverse=True)
-        rows = np.empty((vals.size, 256))
-        for k, v in enumerate(vals):
-            x = np.clip(ramp, 1.0, v)
-            rows[k] = np.log(v / x)
-        out[:, c, :] = rows[inv]
-    return out
+        rows = np.log(vals[:, None] / np.clip(ramp[None, :], 1.0, vals[:, None]))
+        per_channel.append(t.from_numpy(rows).to(device)[t.from_numpy(inv.ravel()).to(device)])
+    return t.stack(per_channel, dim=1).contiguous()
 
 
 def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), *,
@@ -179,7 +178,7 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
         warnings.warn("some items had no pixels brighter than the white threshold in a "
                       "channel; their i0 fell back to 255", optics.BackgroundEstimateWarning,
                       stacklevel=2)
-    luts = t.from_numpy(_od_tables_exact(i0_h)).to(dev)
+    luts = _od_tables_exact(i0_h, dev)
     d_off = t.from_numpy(offsets).to(dev)
     flat = sample.reshape(-1)
     r = snmf.snmf_batched(flat, d_off, luts, cfg, cluster=1)
@@ -263,3 +262,57 @@ def normalize_batch(images, target, *, plan: SamplePlan = SamplePlan(),
     out, errors = transform_batch(images, fits, target, out, code_lam=code_lam,
                                   precision=precision)
     return out, errors, fits
+
+
+def normalize_batch_host(images, target, out=None, *, chunk: int = 512, streams: int = 3,
+                         plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(),
+                         code_lam: float = 0.0, precision: str = "exact"):
+    """normalize_batch for a host-resident batch ((n, H, W, 3) uint8 numpy array
+    or CPU tensor; pinned memory gives asynchronous copies): chunks of
+    ``chunk`` items rotate over ``streams`` CUDA streams so the H2D copy of one
+    chunk, the fit + recolour of another and the D2H copy of a third overlap —
+    cmd_batch's loop over files (src/cli.py:270-301) as a pipeline.  Returns
+    (out, errors) with errors in item order."""
+    t = _dev.torch()
+    host = images if _dev.is_tensor(images) else t.from_numpy(np.ascontiguousarray(images))
+    if host.ndim != 4 or host.shape[3] != 3:
+        raise ValueError("images must be an (n, H, W, 3) uint8 batch")
+    n = int(host.shape[0])
+    if out is None:
+        out = t.empty(host.shape, dtype=t.uint8, pin_memory=host.is_pinned())
+    elif not _dev.is_tensor(out):
+        out = t.from_numpy(out)
+    pinned = host.is_pinned() and out.is_pinned()
+    starts = list(range(0, n, chunk))
+    slots = [dict(stream=t.cuda.Stream(), done=None, d_in=None) for _ in range(max(2, streams))]
+
+    def upload(k):                       # H2D of chunk k on its slot's stream
+        slot = slots[k % len(slots)]
+        if slot["done"] is not None:
+            slot["done"].synchronize()   # the chunk that used this slot has left the GPU
+        a, b = starts[k], min(n, starts[k] + chunk)
+        with t.cuda.stream(slot["stream"]):
+            slot["d_in"] = host[a:b].to("cuda", non_blocking=pinned)
+
+    errors = [None] * n
+    if starts:
+        upload(0)
+    for k, a in enumerate(starts):
+        b = min(n, a + chunk)
+        if k + 1 < len(starts):
+            upload(k + 1)                # next chunk's copy overlaps this chunk's compute
+        slot = slots[k % len(slots)]
+        with t.cuda.stream(slot["stream"]):
+            d_in = slot["d_in"]
+            fits = fit_batch(d_in, plan, cfg, code_lam=code_lam)
+            d_out, errs = transform_batch(d_in, fits, target, code_lam=code_lam,
+                                          precision=precision)
+            out[a:b].copy_(d_out, non_blocking=pinned)
+            ev = t.cuda.Event()
+            ev.record(slot["stream"])
+        slot["done"] = ev
+        errors[a:b] = errs
+    for slot in slots:
+        if slot["done"] is not None:
+            slot["done"].synchronize()
+    return out, errors

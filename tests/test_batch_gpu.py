@@ -152,3 +152,18 @@ def test_batch_many_items_one_launch_per_148():
         assert np.array_equal(out[k], out[k % 4]), k
     _, ref = _oracle_item(base[1], orc.Plan(), tgt)
     assert np.array_equal(out[1], ref)
+
+
+def test_normalize_batch_host_matches_device_batch():
+    import torch
+
+    pb = _pb()
+    imgs = _items(64, 80, 11, seed=13)
+    tgt = _target(pb, 5)
+    dev_out, dev_err, _ = _run(pb, imgs, pb.SamplePlan(), tgt)
+    host = torch.from_numpy(np.stack(imgs)).pin_memory()
+    with __import__("warnings").catch_warnings():
+        __import__("warnings").simplefilter("ignore")
+        out, errs = pb.normalize_batch_host(host, tgt, chunk=4, streams=3)
+    assert np.array_equal(out.numpy(), dev_out)
+    assert [type(e) for e in errs] == [type(e) for e in dev_err]
