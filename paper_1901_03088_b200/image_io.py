@@ -225,3 +225,126 @@ class DeviceWriter(StripWriter):
         if self._rows_written != self.height:
             raise ValueError("incomplete image")
         self._closed = True
+
+
+# ----------------------------------------------------------------------------- files
+# Image files for the CLI (src/image_io.py:110-466).  PNG goes through Pillow
+# (decoded once, as the reference does: PNG has no random access); `.npy`
+# (H, W, 3) uint8 arrays are memory-mapped, so large slides stream without a
+# full load.  8-bit RGB TIFF needs `tifffile`, which this image does not ship:
+# it is reported as an unsupported format rather than half-supported.
+_PNG_MAGIC = b"\x89PNG\r\n\x1a\n"
+_NPY_MAGIC = b"\x93NUMPY"
+_TIFF_MAGIC = (b"II*\x00", b"MM\x00*", b"II+\x00", b"MM\x00+")
+
+
+def _decode_png(path) -> np.ndarray:
+    from PIL import Image, UnidentifiedImageError
+
+    from .errors import CorruptImageError, UnsupportedFormatError
+
+    try:
+        with Image.open(path) as img:
+            if img.mode != "RGB":
+                raise UnsupportedFormatError(f"{path}: only 8-bit RGB PNG is supported "
+                                             f"(mode {img.mode})")
+            return np.asarray(img, dtype=np.uint8)
+    except UnidentifiedImageError as exc:
+        raise CorruptImageError(f"{path}: cannot decode PNG: {exc}") from exc
+    except (OSError, SyntaxError, ValueError) as exc:
+        raise CorruptImageError(f"{path}: truncated or corrupt PNG: {exc}") from exc
+
+
+def open_slide(path) -> SlideSource:
+    """Image file → SlideSource, dispatching on the magic bytes."""
+    from .errors import CorruptImageError, UnsupportedFormatError
+
+    with open(path, "rb") as fh:
+        head = fh.read(8)
+    if head == _PNG_MAGIC:
+        return ArraySource(_decode_png(path))
+    if head[:6] == _NPY_MAGIC:
+        try:
+            arr = np.load(path, mmap_mode="r")
+        except ValueError as exc:
+            raise CorruptImageError(f"{path}: corrupt .npy: {exc}") from exc
+        if arr.ndim != 3 or arr.shape[2] != 3 or arr.dtype != np.uint8:
+            raise UnsupportedFormatError(f"{path}: .npy must hold (H, W, 3) uint8")
+        return ArraySource(arr)
+    if head[:4] in _TIFF_MAGIC:
+        try:
+            import tifffile
+        except ImportError:
+            raise UnsupportedFormatError(f"{path}: TIFF input needs the tifffile package, "
+                                         "which is not installed") from None
+        try:
+            arr = tifffile.imread(path)
+        except Exception as exc:   # tifffile raises many types
+            raise CorruptImageError(f"{path}: cannot decode TIFF: {exc}") from exc
+        if arr.ndim != 3 or arr.shape[2] != 3 or arr.dtype != np.uint8:
+            raise UnsupportedFormatError(f"{path}: only 8-bit RGB TIFF is supported")
+        return ArraySource(np.ascontiguousarray(arr))
+    raise UnsupportedFormatError(f"{path}: not a supported image format (PNG, .npy, "
+                                 "8-bit RGB TIFF)")
+
+
+class FileWriter(ArrayWriter):
+    """Output file fed in-order strips; encoded on close (PNG) or written
+    through a memory map (.npy).  A failed or incomplete image leaves no file."""
+
+    def __init__(self, path, width, height):
+        from .errors import UnsupportedFormatError
+
+        self.path = str(path)
+        low = self.path.lower()
+        if low.endswith(".npy"):
+            self.kind = "npy"
+            out = np.lib.format.open_memmap(self.path, mode="w+", dtype=np.uint8,
+                                            shape=(height, width, 3))
+        elif low.endswith(".png"):
+            self.kind = "png"
+            out = None
+        elif low.endswith((".tif", ".tiff")):
+            try:
+                import tifffile  # noqa: F401
+            except ImportError:
+                raise UnsupportedFormatError(f"{path}: TIFF output needs the tifffile "
+                                             "package, which is not installed") from None
+            self.kind = "tiff"
+            out = None
+        else:
+            raise UnsupportedFormatError(f"{path}: output must be .png, .npy or .tif(f)")
+        super().__init__(width, height, out=out)
+
+    def close(self):
+        if self._closed:
+            return
+        try:
+            super().close()
+        except ValueError:
+            self.abort()
+            raise
+        if self.kind == "png":
+            from PIL import Image
+
+            Image.fromarray(self.pixels, mode="RGB").save(self.path, compress_level=6)
+        elif self.kind == "tiff":
+            import tifffile
+
+            tifffile.imwrite(self.path, self.pixels, photometric="rgb")
+        else:
+            self.pixels.flush()
+
+    def abort(self):
+        import os
+
+        self._closed = True
+        if self.kind == "npy":
+            del self.pixels
+        if os.path.exists(self.path):
+            os.remove(self.path)
+
+
+def open_writer(path, width: int, height: int) -> StripWriter:
+    """src/image_io.py:457-466: a StripWriter for an output file."""
+    return FileWriter(path, width, height)
