@@ -230,9 +230,9 @@ class DeviceWriter(StripWriter):
 # ----------------------------------------------------------------------------- files
 # Image files for the CLI (src/image_io.py:110-466).  PNG goes through Pillow
 # (decoded once, as the reference does: PNG has no random access); `.npy`
-# (H, W, 3) uint8 arrays are memory-mapped, so large slides stream without a
-# full load.  8-bit RGB TIFF needs `tifffile`, which this image does not ship:
-# it is reported as an unsupported format rather than half-supported.
+# (H, W, 3) uint8 arrays are memory-mapped; tiled/striped RGB8 (Big)TIFF goes
+# through the package's own codec (tiff.py: per-segment random access in, tiled
+# deflate out), so whole-slide files stream without a full load.
 _PNG_MAGIC = b"\x89PNG\r\n\x1a\n"
 _NPY_MAGIC = b"\x93NUMPY"
 _TIFF_MAGIC = (b"II*\x00", b"MM\x00*", b"II+\x00", b"MM\x00+")
@@ -272,20 +272,55 @@ def open_slide(path) -> SlideSource:
             raise UnsupportedFormatError(f"{path}: .npy must hold (H, W, 3) uint8")
         return ArraySource(arr)
     if head[:4] in _TIFF_MAGIC:
-        try:
-            import tifffile
-        except ImportError:
-            raise UnsupportedFormatError(f"{path}: TIFF input needs the tifffile package, "
-                                         "which is not installed") from None
-        try:
-            arr = tifffile.imread(path)
-        except Exception as exc:   # tifffile raises many types
-            raise CorruptImageError(f"{path}: cannot decode TIFF: {exc}") from exc
-        if arr.ndim != 3 or arr.shape[2] != 3 or arr.dtype != np.uint8:
-            raise UnsupportedFormatError(f"{path}: only 8-bit RGB TIFF is supported")
-        return ArraySource(np.ascontiguousarray(arr))
+        return TiffSource(path)
     raise UnsupportedFormatError(f"{path}: not a supported image format (PNG, .npy, "
                                  "8-bit RGB TIFF)")
+
+
+class TiffSource(SlideSource):
+    """Tiled or striped RGB8 (Big)TIFF (src/image_io.py:132-227)."""
+
+    def __init__(self, path):
+        from .tiff import TiffReader
+
+        self._reader = TiffReader(path)
+        self.width, self.height = self._reader.width, self._reader.height
+
+    def read_region(self, x, y, w, h):
+        self._check_bounds(x, y, w, h)
+        return PixelBlock(x, y, self._reader.read_region(x, y, w, h))
+
+    def close(self):
+        self._reader.close()
+
+
+class TiffStripWriter(StripWriter):
+    """Tiled deflate TIFF output, written band by band (src/image_io.py:361-454)."""
+
+    def __init__(self, path, width, height, compression="deflate"):
+        from .tiff import TiffTileWriter
+
+        super().__init__(width, height)
+        self._tw = TiffTileWriter(path, width, height, compression=compression)
+
+    def _write(self, rows):
+        if hasattr(rows, "cpu"):
+            rows = rows.cpu().numpy()
+        self._tw.write(np.asarray(rows))
+
+    def close(self):
+        if self._closed:
+            return
+        if self._rows_written != self.height:
+            self.abort()
+            raise ValueError(f"incomplete image: {self._rows_written} of {self.height} rows")
+        self._tw.close()
+        self._closed = True
+
+    def abort(self):
+        if not self._closed:
+            self._closed = True
+            self._tw.abort()
 
 
 class FileWriter(ArrayWriter):
@@ -304,16 +339,8 @@ class FileWriter(ArrayWriter):
         elif low.endswith(".png"):
             self.kind = "png"
             out = None
-        elif low.endswith((".tif", ".tiff")):
-            try:
-                import tifffile  # noqa: F401
-            except ImportError:
-                raise UnsupportedFormatError(f"{path}: TIFF output needs the tifffile "
-                                             "package, which is not installed") from None
-            self.kind = "tiff"
-            out = None
         else:
-            raise UnsupportedFormatError(f"{path}: output must be .png, .npy or .tif(f)")
+            raise UnsupportedFormatError(f"{path}: output must be .png, .npy or .tif(f)")  # noqa
         super().__init__(width, height, out=out)
 
     def close(self):
@@ -328,10 +355,6 @@ class FileWriter(ArrayWriter):
             from PIL import Image
 
             Image.fromarray(self.pixels, mode="RGB").save(self.path, compress_level=6)
-        elif self.kind == "tiff":
-            import tifffile
-
-            tifffile.imwrite(self.path, self.pixels, photometric="rgb")
         else:
             self.pixels.flush()
 
@@ -347,4 +370,6 @@ class FileWriter(ArrayWriter):
 
 def open_writer(path, width: int, height: int) -> StripWriter:
     """src/image_io.py:457-466: a StripWriter for an output file."""
+    if str(path).lower().endswith((".tif", ".tiff")):
+        return TiffStripWriter(path, width, height)
     return FileWriter(path, width, height)

@@ -92,3 +92,71 @@ def test_file_io_roundtrip(tmp_path):
     assert not os.path.exists(tmp_path / "b.png")
     with pytest.raises(cli.E.UnsupportedFormatError):
         io.open_writer(tmp_path / "c.jpg", 30, 20)
+
+
+@pytest.mark.parametrize("comp,big", [("deflate", False), ("none", False), ("deflate", True)])
+def test_tiff_codec_roundtrip_and_pillow(tmp_path, comp, big):
+    import numpy as np
+    from PIL import Image
+
+    from paper_1901_03088_b200 import image_io as io
+    from paper_1901_03088_b200 import tiff
+
+    rng = np.random.default_rng(1)
+    a = rng.integers(0, 256, size=(600, 530, 3), dtype=np.uint8)
+    p = tmp_path / "t.tif"
+    w = tiff.TiffTileWriter(p, 530, 600, compression=comp, bigtiff=big)
+    for y in range(0, 600, 250):
+        w.write(a[y:y + 250])
+    w.close()
+    with io.open_slide(p) as s:
+        assert (s.width, s.height) == (530, 600)
+        assert np.array_equal(s.read_region(0, 0, 530, 600).pixels, a)
+        assert np.array_equal(s.read_region(97, 255, 300, 211).pixels, a[255:466, 97:397])
+    if not big:                                   # libtiff (through Pillow) reads ours
+        with Image.open(p) as im:
+            assert np.array_equal(np.asarray(im.convert("RGB")), a)
+
+
+def test_tiff_reads_pillow_strips_and_rejects_unsupported(tmp_path):
+    import numpy as np
+    from PIL import Image
+
+    from paper_1901_03088_b200 import image_io as io
+
+    a = np.random.default_rng(2).integers(0, 256, size=(300, 200, 3), dtype=np.uint8)
+    for comp in ("raw", "tiff_adobe_deflate"):
+        p = tmp_path / f"{comp}.tif"
+        Image.fromarray(a).save(p, compression=comp)
+        with io.open_slide(p) as s:
+            assert np.array_equal(s.read_region(0, 0, 200, 300).pixels, a)
+    p = tmp_path / "lzw.tif"
+    Image.fromarray(a).save(p, compression="tiff_lzw")
+    with pytest.raises(cli.E.UnsupportedFormatError):
+        io.open_slide(p)
+    p = tmp_path / "gray.tif"
+    Image.fromarray(a[..., 0]).save(p)
+    with pytest.raises(cli.E.UnsupportedFormatError):
+        io.open_slide(p)
+    good = tmp_path / "raw.tif"
+    bad = tmp_path / "cut.tif"
+    bad.write_bytes(good.read_bytes()[:5000])
+    with pytest.raises(cli.E.CorruptImageError):
+        io.open_slide(bad)
+
+
+def test_tiff_strip_writer_through_open_writer(tmp_path):
+    import numpy as np
+
+    from paper_1901_03088_b200 import image_io as io
+
+    a = np.random.default_rng(3).integers(0, 256, size=(513, 300, 3), dtype=np.uint8)
+    with io.open_writer(tmp_path / "o.tiff", 300, 513) as w:
+        for y in range(0, 513, 100):
+            w.write_strip(io.PixelBlock(0, y, a[y:y + 100]))
+    with io.open_slide(tmp_path / "o.tiff") as s:
+        assert np.array_equal(s.read_region(0, 0, 300, 513).pixels, a)
+    with pytest.raises(ValueError):
+        with io.open_writer(tmp_path / "p.tif", 300, 513) as w:
+            w.write_strip(io.PixelBlock(0, 0, a[:100]))
+    assert not os.path.exists(tmp_path / "p.tif")

@@ -43,6 +43,18 @@ def test_cli_fit_normalize_batch(tmp_path, capsys):
                      "--stats-csv", str(tmp_path / "s.csv")]) == 0
     assert np.array_equal(_read(out), ref)
     assert (tmp_path / "s.csv").read_text().count("\n") >= 2
+    from paper_1901_03088_b200 import tiff
+
+    tw = tiff.TiffTileWriter(tmp_path / "src.tif", src.shape[1], src.shape[0])
+    tw.write(src)
+    tw.close()
+    out_t = tmp_path / "out.tif"
+    assert cli.main(["normalize", str(tmp_path / "src.tif"), "--target",
+                     str(tmp_path / "tgt.png"), "--out", str(out_t)]) == 0
+    from paper_1901_03088_b200 import image_io
+
+    with image_io.open_slide(out_t) as s:
+        assert np.array_equal(s.read_region(0, 0, s.width, s.height).pixels, ref)
     out2 = tmp_path / "out2.npy"
     assert cli.main(["normalize", str(tmp_path / "src.png"), "--profile", str(prof),
                      "--out", str(out2)]) == 0
