@@ -43,6 +43,11 @@ extern "C" {
 /* Parameters of one source→target recoloring (src/pipeline.py:260
  * `_process_strip(pixels, src_i0, src_basis, code_lam, factors, tgt_basis,
  * tgt_i0)`).  Bases are row-major 3x2 (basis[c*2+j], channel c, stain j). */
+/* spcn_xform_params.cert_alpha: 0 = analytic per-pixel bound; (0, 1e-3) =
+ * a calibrated bound from spcn_xform_calibrate; SPCN_CALIBRATE_INLINE =
+ * calibrate on the device inside spcn_xform_rgb8 (no host round trip).     */
+#define SPCN_CALIBRATE_INLINE (-1.0)
+
 typedef struct spcn_xform_params {
   double src_i0[3];
   double src_basis[6];
@@ -147,6 +152,24 @@ int spcn_sample_compact(const uint8_t* img, const spcn_patch* patches, int32_t n
                         int32_t max_chunks, int32_t white_threshold, const int32_t* counts,
                         const spcn_patch_take* takes, uint8_t* out_px, int32_t* bright_hist,
                         void* stream);
+
+/* The reference's patch visit loop (src/pipeline.py:156-184) on the device,
+ * for candidates [k0, k0 + n) of the visit order (one thread, sequential like
+ * the reference), continuing `state` across calls:
+ *   state (int64[8], zero before the first call): collected, visited, used,
+ *   bright_n[3], stopped, need_more (set when the batch ran out before a stop
+ *   rule fired and more candidates exist: call again with the next batch).
+ * counts: spcn_sample_count output for the n candidates; dims[k] = {w, h} of
+ * candidate k0+k; takes[k] receives its decision (take 0 when not visited);
+ * offsets[1] = collected (the sample's end offset).                        */
+typedef struct spcn_visit_plan {
+  int64_t target_pixels, sample_cap;
+  int32_t max_patches, ncand;   /* ncand = candidates in the visit order (<= 10*max_patches) */
+  double background_cutoff;     /* SamplePlan.background_fraction_cutoff */
+} spcn_visit_plan;
+int spcn_sample_visit(const int32_t* counts, int32_t n, int32_t max_chunks, int32_t k0,
+                      const int32_t* dims, const spcn_visit_plan* plan, int64_t* state,
+                      spcn_patch_take* takes, int64_t* offsets, void* stream);
 
 /* Background i0 per problem and channel: exact 80th percentile of the bright
  * pool given as 256-bin counts (estimate_max_intensity src/optics.py:35-68).

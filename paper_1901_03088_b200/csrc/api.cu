@@ -203,10 +203,14 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
   const bool exact = p->precision == SPCN_PREC_EXACT;
   bool fast_ok = p->precision != SPCN_PREC_STRICT && fill_fast(fp, sp, exact);
   int mode = exact ? 0 : 1;
+  // cert_alpha == SPCN_CALIBRATE_INLINE: calibrate on the device right before
+  // the main kernel, which reads the result itself (no host round trip)
+  const bool inline_cal = exact && fast_ok && p->cert_alpha == SPCN_CALIBRATE_INLINE;
   if (exact && fast_ok && p->cert_alpha > 0.0 && p->cert_alpha < 1e-3) {
     set_calibrated(fp, p->cert_alpha);
     mode = 2;
   }
+  if (inline_cal) mode = 2;
 
   // 16-byte alignment of the vector body (both buffers must share the phase)
   const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
@@ -227,13 +231,20 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
     count = static_cast<unsigned long long*>(workspace);
     items = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + kWsHeader);
     cap = (workspace_bytes - kWsHeader) / 8;
-    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+    cudaError_t e = cudaMemsetAsync(count, 0, kWsHeader, st);   // count + calibration word
     if (e != cudaSuccess) return cuda_fail(e, "memset");
   }
   cudaError_t e;
+  const unsigned int* alpha_bits = nullptr;
+  if (inline_cal) {
+    unsigned int* bits = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + 8);
+    if ((e = launch_calibrate(fp, sp, bits, st)) != cudaSuccess) return cuda_fail(e, "calibrate");
+    alpha_bits = bits;
+  }
   if (head > 0 && (e = launch_xform_strict(src, dst, head, sp, st)) != cudaSuccess)
     return cuda_fail(e, "xform_head");
-  e = launch_xform_main(mode, src + 3 * head, dst + 3 * head, body, fp, sp, count, items, cap, st);
+  e = launch_xform_main(mode, src + 3 * head, dst + 3 * head, body, fp, sp, count, items, cap,
+                        alpha_bits, st);
   if (e != cudaSuccess) return cuda_fail(e, "xform_tma");
   if (exact && (e = launch_xform_repair(src + 3 * head, dst + 3 * head, body, sp, count, items, cap,
                                         st)) != cudaSuccess)
@@ -358,6 +369,20 @@ int spcn_sample_compact(const uint8_t* img, const spcn_patch* patches, int32_t n
                                         takes, out_px, bright_hist,
                                         static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "sample_compact");
+}
+
+int spcn_sample_visit(const int32_t* counts, int32_t n, int32_t max_chunks, int32_t k0,
+                      const int32_t* dims, const spcn_visit_plan* plan, int64_t* state,
+                      spcn_patch_take* takes, int64_t* offsets, void* stream) {
+  g_err.clear();
+  if (n < 1 || n > 4096 || max_chunks < 1 || k0 < 0) return fail(SPCN_EINVAL, "bad batch");
+  if (!counts || !dims || !plan || !state || !takes || !offsets)
+    return fail(SPCN_EINVAL, "NULL argument");
+  if (plan->max_patches < 1 || plan->target_pixels < 1 || plan->sample_cap < 0)
+    return fail(SPCN_EINVAL, "bad sample plan");
+  const cudaError_t e = launch_visit(counts, n, max_chunks, k0, dims, *plan, state, takes, offsets,
+                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "sample_visit");
 }
 
 int spcn_i0_from_hist(const int32_t* hist, int32_t nprob, double* i0, int32_t* empty,

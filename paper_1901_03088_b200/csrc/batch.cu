@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(32 * kBW, 1)
 #pragma unroll
       for (int u = 0; u < kBNSub; ++u)
         recolor_block<MODE>(fp, lut, lc, sbase + u * 1536 + 48 * lane, u * 512 + 16 * lane < n,
-                            base + j * kBSlicePx + u * 512 + 16 * lane, rl, lane);
+                            base + j * kBSlicePx + u * 512 + 16 * lane, rl, lane, fp.I);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {

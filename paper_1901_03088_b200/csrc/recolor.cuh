@@ -76,10 +76,11 @@ __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, ui
 // per-pixel bound), 1 = FAST, 2 = EXACT (calibrated constant bound).  EXACT:
 // returns non-zero when any of the pair's six roundings is not certified
 // (r_lo != r_hi); both pixels of such a pair go to the fp64 repair list.
+// I: the calibrated {I_lo, I_hi} per channel (MODE 2).
 template <int MODE>
 __device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t* lut,
                                                  const uint32_t* w, int k, const uint32_t* lc,
-                                                 uint32_t* ob) {
+                                                 uint32_t* ob, const float2* I) {
   const int a = 3 * k, b = 3 * k + 3;
   const float2 v0 = make_float2(od_lookup(lut, w, a, lc[0]), od_lookup(lut, w, b, lc[0]));
   const float2 v1 = make_float2(od_lookup(lut, w, a + 1, lc[1]), od_lookup(lut, w, b + 1, lc[1]));
@@ -107,7 +108,7 @@ __device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t*
       Ia = cert_interval(fp.i0t[c], alpha.x);
       Ib = cert_interval(fp.i0t[c], alpha.y);
     } else {
-      Ia = Ib = fp.I[c];
+      Ia = Ib = I[c];
     }
     const float2 ra = __ffma2_rn(Ia, bc2(pa), bc2(kMagic));
     const float2 rb = __ffma2_rn(Ib, bc2(pb), bc2(kMagic));
@@ -125,7 +126,8 @@ __device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t*
 template <int MODE>
 __device__ __forceinline__ void recolor_block(const FastS& fp, const uint8_t* lut,
                                               const uint32_t* lc, uint8_t* blk, bool valid,
-                                              int64_t gp0, const RepairList& rl, int lane) {
+                                              int64_t gp0, const RepairList& rl, int lane,
+                                              const float2* I) {
   uint32_t w[12], ob[48], o[12];
   uint32_t badpairs = 0;
   if (valid) {
@@ -160,7 +162,7 @@ __device__ __forceinline__ void recolor_block(const FastS& fp, const uint8_t* lu
     } else {
 #pragma unroll
       for (int qq = 0; qq < 8; ++qq) {
-        const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * qq, lc, ob);
+        const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * qq, lc, ob, I);
         if (MODE == 0 || MODE == 2) badpairs |= (bad != 0u ? 1u : 0u) << qq;
 #pragma unroll
         for (int t = 0; t < 12; ++t)

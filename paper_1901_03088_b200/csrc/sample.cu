@@ -249,4 +249,78 @@ cudaError_t launch_od_tables(const double* i0, int nprob, double* lut, cudaStrea
   return launched();
 }
 
+// ---------------------------------------------------------------------------
+// k_visit: the reference's visit loop (src/pipeline.py:156-184) over one batch
+// of candidates, on the device so the sampler needs no host round trip in the
+// common case.  Block-wide: chunk totals of every candidate, then thread 0
+// replays the sequential decisions exactly like pipeline._visit.
+__global__ void __launch_bounds__(256) k_visit(const int32_t* __restrict__ counts, int n,
+                                               int max_chunks, int k0,
+                                               const int32_t* __restrict__ dims,
+                                               spcn_visit_plan plan, int64_t* __restrict__ state,
+                                               spcn_patch_take* __restrict__ takes,
+                                               int64_t* __restrict__ offsets) {
+  extern __shared__ int64_t tot[];   // n x 4 totals
+  for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) {
+    const int k = i >> 2, q = i & 3;
+    int64_t t = 0;
+    for (int c = 0; c < max_chunks; ++c) t += counts[(k * max_chunks + c) * 4 + q];
+    tot[i] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int64_t collected = state[0], visited = state[1], used = state[2];
+  int64_t bright_n[3] = {state[3], state[4], state[5]};
+  int64_t stopped = state[6];
+  const int64_t limit = 10 * (int64_t)plan.max_patches;
+  const double min_frac = 1.0 - plan.background_cutoff;
+  int k = 0;
+  for (; k < n; ++k) {
+    spcn_patch_take& tk = takes[k];
+    tk.take_nonwhite = 0;
+    tk.out_base = 0;
+    tk.take_bright[0] = tk.take_bright[1] = tk.take_bright[2] = 0;
+    tk.problem = 0;
+    if (stopped) continue;
+    if (visited >= limit || used >= plan.max_patches || collected >= plan.target_pixels) {
+      stopped = 1;
+      continue;
+    }
+    const int64_t nw = tot[4 * k];
+    const int64_t npx = (int64_t)dims[2 * k] * dims[2 * k + 1];
+    ++visited;
+    for (int c = 0; c < 3; ++c) {
+      if (bright_n[c] < plan.sample_cap) {
+        const int64_t room = plan.sample_cap - bright_n[c];
+        const int64_t t = tot[4 * k + 1 + c] < room ? tot[4 * k + 1 + c] : room;
+        tk.take_bright[c] = (int32_t)t;
+        bright_n[c] += t;
+      }
+    }
+    if ((double)nw < min_frac * (double)npx) continue;   // background patch
+    ++used;
+    const int64_t room = plan.target_pixels - collected;
+    const int64_t take = nw < room ? nw : room;
+    tk.take_nonwhite = take;
+    tk.out_base = collected;
+    collected += take;
+  }
+  state[0] = collected;
+  state[1] = visited;
+  state[2] = used;
+  for (int c = 0; c < 3; ++c) state[3 + c] = bright_n[c];
+  state[6] = stopped;
+  state[7] = (!stopped && k0 + n < plan.ncand) ? 1 : 0;   // need more candidates
+  offsets[0] = 0;
+  offsets[1] = collected;
+}
+
+cudaError_t launch_visit(const int32_t* counts, int n, int max_chunks, int k0, const int32_t* dims,
+                         const spcn_visit_plan& plan, int64_t* state, spcn_patch_take* takes,
+                         int64_t* offsets, cudaStream_t st) {
+  k_visit<<<1, 256, 4 * n * sizeof(int64_t), st>>>(counts, n, max_chunks, k0, dims, plan, state,
+                                                  takes, offsets);
+  return launched();
+}
+
 }  // namespace spcn

@@ -14,4 +14,7 @@ cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches,
 cudaError_t launch_i0_from_hist(const int32_t* hist, int nprob, double* i0, int32_t* empty,
                                 cudaStream_t st);
 cudaError_t launch_od_tables(const double* i0, int nprob, double* lut, cudaStream_t st);
+cudaError_t launch_visit(const int32_t* counts, int n, int max_chunks, int k0, const int32_t* dims,
+                         const spcn_visit_plan& plan, int64_t* state, spcn_patch_take* takes,
+                         int64_t* offsets, cudaStream_t st);
 }  // namespace spcn

@@ -84,6 +84,11 @@ __global__ void __launch_bounds__(32 * CW, BLK)
 
   uint32_t lc[3];
   LutLayout<REP>::lane_consts(lane, lc);
+  float2 I[3];   // calibrated interval: from the host, or from the on-device calibration
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    I[c] = (MODE == 2 && rl.alpha_bits) ? calibrated_interval(fp.i0t[c], __uint_as_float(*rl.alpha_bits))
+                                        : fp.I[c];
   const int64_t nslices = (npix + kSlicePx - 1) / kSlicePx;
   const int64_t gw = (int64_t)blockIdx.x * CW + warp, GW = (int64_t)gridDim.x * CW;
   uint64_t pol = 0;
@@ -110,7 +115,7 @@ __global__ void __launch_bounds__(32 * CW, BLK)
 #pragma unroll
     for (int u = 0; u < NSUB; ++u)
       recolor_block<MODE>(fp, lut, lc, sbase + u * 1536 + 48 * lane, u * 512 + 16 * lane < n,
-                          j * kSlicePx + u * 512 + 16 * lane, rl, lane);
+                          j * kSlicePx + u * 512 + 16 * lane, rl, lane, I);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -291,13 +296,13 @@ cudaError_t xform_setup_device() {
 cudaError_t launch_xform_main(int mode, const uint8_t* src, uint8_t* dst, int64_t npix,
                              const FastP& fp, const StrictP& sp, unsigned long long* count,
                              unsigned long long* items, unsigned long long cap,
-                             cudaStream_t st) {
+                             const unsigned int* alpha_bits, cudaStream_t st) {
   cudaError_t e = xform_setup_device();
   if (e != cudaSuccess) return e;
   const Shape& s = *g_shape;
   const int64_t ntiles = (npix + s.tile_px - 1) / s.tile_px;
   const int grid = static_cast<int>(min64(ntiles, (int64_t)g_sm_count * s.blocks_per_sm));
-  RepairList rl{count, items, cap};
+  RepairList rl{count, items, cap, alpha_bits};
   s.fn[g_identity ? 3 : mode]<<<grid, s.threads, s.smem, st>>>(src, dst, npix, fp, sp, rl);
   return launched();
 }

@@ -8,7 +8,8 @@ namespace spcn {
 cudaError_t xform_setup_device();
 cudaError_t launch_xform_main(int mode, const uint8_t* src, uint8_t* dst, int64_t npix,
                               const FastP& fp, const StrictP& sp, unsigned long long* count,
-                              unsigned long long* items, unsigned long long cap, cudaStream_t st);
+                              unsigned long long* items, unsigned long long cap,
+                              const unsigned int* alpha_bits, cudaStream_t st);
 cudaError_t launch_xform_repair(const uint8_t* src, uint8_t* dst, int64_t npix, const StrictP& sp,
                                 unsigned long long* count, unsigned long long* items,
                                 unsigned long long cap, cudaStream_t st);

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import os
 import time
+import warnings
 from collections import deque
 from dataclasses import dataclass
 from threading import Lock
@@ -18,7 +19,8 @@ from threading import Lock
 import numpy as np
 
 from . import _dev, _lib, optics, snmf
-from .errors import BlankSlideError, DegenerateStainError, InsufficientPixelsError, SlideNormError
+from .errors import (BlankSlideError, DegenerateStainError, InsufficientPixelsError,
+                     SlideNormError, StainAbsentError)
 from .image_io import (DEFAULT_STRIP_HEIGHT, ArraySource, ArrayWriter, DeviceSource, DeviceWriter,
                        PixelBlock, plan_strips)
 from .normalize import FitParams, StainStats, config_hash, scale_factors, stain_stats
@@ -207,18 +209,110 @@ def _visit(plan, order, rects, counts_of):
     return takes, used_counts, collected, visited, used
 
 
+def _candidates(width: int, height: int, plan: SamplePlan):
+    """The seeded visit order of the patch grid (src/pipeline.py:138-142):
+    (order, ncand, rects of the first ncand candidates)."""
+    ps = plan.patch_size
+    ncols, nrows = -(-width // ps), -(-height // ps)
+    order = np.random.default_rng(plan.seed).permutation(ncols * nrows)
+    ncand = min(len(order), 10 * plan.max_patches)
+    first = order[:ncand]
+    xs, ys = (first % ncols) * ps, (first // ncols) * ps
+    rects = [(int(x), int(y), int(min(ps, width - x)), int(min(ps, height - y)))
+             for x, y in zip(xs, ys)]
+    return order, ncand, rects
+
+
+_VISIT_PLAN = None
+
+
+def _visit_plan_type():
+    global _VISIT_PLAN
+    if _VISIT_PLAN is None:
+        import ctypes
+
+        class VisitPlan(ctypes.Structure):
+            _fields_ = [("target_pixels", ctypes.c_int64), ("sample_cap", ctypes.c_int64),
+                        ("max_patches", ctypes.c_int32), ("ncand", ctypes.c_int32),
+                        ("background_cutoff", ctypes.c_double)]
+
+        _VISIT_PLAN = VisitPlan
+        P, I32 = _lib.P, _lib.I32
+        _lib.declare("spcn_sample_visit", _lib.ctypes.c_int,
+                     [P, I32, I32, I32, P, _lib.ctypes.POINTER(VisitPlan), P, P, P, P])
+    return _VISIT_PLAN
+
+
+def _fit_sample_resident(slide: DeviceSource, plan: SamplePlan, need_counts: bool = False):
+    """Sampling + i0 for a device-resident slide with one host round trip in
+    the common case: count → visit loop (k_visit, on the device) → ordered
+    compaction → i0, then a single read of the results.  A further candidate
+    batch is only needed when the first ran out before a stop rule fired.
+    Returns (sample (target_pixels, 3) CUDA buffer, m, i0, PixelSample meta, empty)."""
+    import ctypes
+
+    t = _dev.torch()
+    L = _lib_sample()
+    VisitPlan = _visit_plan_type()
+    order, ncand, rects = _candidates(slide.width, slide.height, plan)
+    W = slide.width
+    desc = np.array([(y * W + x, w, h, W) for (x, y, w, h) in rects], dtype=PATCH_DT)
+    dims = np.array([(w, h) for (_, _, w, h) in rects], dtype=np.int32)
+    d_desc = t.from_numpy(desc.view(np.uint8).copy()).cuda()
+    d_dims = t.from_numpy(dims).cuda()
+    vp = VisitPlan(plan.target_pixels, plan.sample_cap, plan.max_patches, ncand,
+                   float(plan.background_fraction_cutoff))
+    thr = int(plan.white_threshold)
+    state = t.zeros(8, dtype=t.int64, device="cuda")
+    offsets = t.zeros(2, dtype=t.int64, device="cuda")
+    sample = t.empty((max(plan.target_pixels, 1), 3), dtype=t.uint8, device="cuda")
+    hist = t.zeros((1, 3, 256), dtype=t.int32, device="cuda")
+    i0 = t.empty(3, dtype=t.float64, device="cuda")
+    empty = t.empty(3, dtype=t.int32, device="cuda")
+    takes_all = t.zeros(ncand * TAKE_DT.itemsize, dtype=t.uint8, device="cuda")
+    img, stream = slide.tensor, _lib.stream_handle()
+    k0, batch = 0, min(ncand, max(2, min(plan.max_patches, 8)))
+    while True:
+        n = min(batch, ncand - k0)
+        npx = dims[k0:k0 + n, 0].astype(np.int64) * dims[k0:k0 + n, 1]
+        chunks = int(max(1, -(-int(npx.max()) // CHUNK)))
+        counts = t.empty((n, chunks, 4), dtype=t.int32, device="cuda")
+        dsl = d_desc[k0 * PATCH_DT.itemsize:(k0 + n) * PATCH_DT.itemsize]
+        tks = takes_all[k0 * TAKE_DT.itemsize:(k0 + n) * TAKE_DT.itemsize]
+        _lib.check(L.spcn_sample_count(_lib.ptr(img), _lib.ptr(dsl), n, chunks, thr,
+                                       _lib.ptr(counts), stream), "sample_count")
+        _lib.check(L.spcn_sample_visit(_lib.ptr(counts), n, chunks, k0,
+                                       _lib.ptr(d_dims[k0:]), ctypes.byref(vp), _lib.ptr(state),
+                                       _lib.ptr(tks), _lib.ptr(offsets), stream), "sample_visit")
+        _lib.check(L.spcn_sample_compact(_lib.ptr(img), _lib.ptr(dsl), n, chunks, thr,
+                                         _lib.ptr(counts), _lib.ptr(tks), _lib.ptr(sample),
+                                         _lib.ptr(hist), stream), "sample_compact")
+        _lib.check(L.spcn_i0_from_hist(_lib.ptr(hist), 1, _lib.ptr(i0), _lib.ptr(empty), stream),
+                   "i0_from_hist")
+        # one read: state (8 int64) | i0 (3 f64) | empty flags (3 int32 widened)
+        packed = t.cat([state.view(t.float64), i0, empty.to(t.float64)]).cpu().numpy()
+        st = packed[:8].view(np.int64)
+        if st[7]:                                  # the batch ran out: next candidates
+            k0 += n
+            batch *= 2
+            continue
+        break
+    m = int(st[0])
+    used_counts = []
+    if need_counts:                                # per-patch stats only (one more read)
+        tk = np.frombuffer(takes_all[:(k0 + n) * TAKE_DT.itemsize].cpu().numpy().tobytes(),
+                           dtype=TAKE_DT)
+        used_counts = [int(v) for v in tk["take_nonwhite"] if v > 0]
+    meta = PixelSample(non_white=sample[:m], patch_counts=used_counts, bright=None,
+                       patches_visited=int(st[1]), patches_used=int(st[2]), bright_hist=None)
+    return sample, m, packed[8:11].copy(), meta, packed[11:14].astype(bool)
+
+
 def _sample_device(slide, plan: SamplePlan):
     """Device sampling; returns (sample CUDA uint8 (M,3), PixelSample meta)."""
     t = _dev.torch()
     L = _lib_sample()
-    rng = np.random.default_rng(plan.seed)
-    xs = range(0, slide.width, plan.patch_size)
-    ys = range(0, slide.height, plan.patch_size)
-    origins = [(x, y) for y in ys for x in xs]
-    order = rng.permutation(len(origins))
-    ncand = min(len(order), 10 * plan.max_patches)
-    rects = [(origins[i][0], origins[i][1], min(plan.patch_size, slide.width - origins[i][0]),
-              min(plan.patch_size, slide.height - origins[i][1])) for i in order[:ncand]]
+    order, ncand, rects = _candidates(slide.width, slide.height, plan)
     pimg = _PatchImage(slide, rects)
     thr = int(plan.white_threshold)
     # counts in growing batches (most slides stop after one or two patches)
@@ -327,14 +421,28 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
     elif _dev.is_tensor(slide):
         slide = DeviceSource(slide)
     t0 = time.perf_counter()
-    sample, meta = _stage("sampling", _sample_device, slide, plan)
-    stats.sampling_s += time.perf_counter() - t0
-    m = int(sample.shape[0])
+    if isinstance(slide, DeviceSource):
+        # resident slide: visit loop + i0 on the device, one host round trip
+        sample, m, i0, meta, empty = _stage("sampling", _fit_sample_resident, slide, plan,
+                                            per_patch_stats)
+        if m == 0:
+            raise BlankSlideError("sampling: blank slide: no non-white pixels found in any "
+                                  "sampled patch")
+        sample = sample[:m]
+        for c in np.flatnonzero(empty):
+            warnings.warn(f"no pixels brighter than the white threshold in the "
+                          f"{('red', 'green', 'blue')[c]} channel; falling back to 255",
+                          optics.BackgroundEstimateWarning, stacklevel=2)
+        stats.sampling_s += time.perf_counter() - t0
+        t0 = time.perf_counter()
+    else:
+        sample, meta = _stage("sampling", _sample_device, slide, plan)
+        stats.sampling_s += time.perf_counter() - t0
+        m = int(sample.shape[0])
+        t0 = time.perf_counter()
+        i0 = _stage("background estimation", optics.i0_from_counts, meta.bright_hist)
     stats.sampled_pixels = m
     stats.patches = meta.patches_used
-
-    t0 = time.perf_counter()
-    i0 = _stage("background estimation", optics.i0_from_counts, meta.bright_hist)
     lut = t.from_numpy(optics.od_table(i0)).cuda().reshape(1, 3, 256)
     if m < 10:
         raise InsufficientPixelsError(
@@ -342,10 +450,32 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
     offsets = t.tensor([0, m], dtype=t.int64, device="cuda")
     flat = sample.reshape(-1)
     r = snmf.snmf_batched(flat, offsets, lut, cfg, cluster=8 if m >= 20_000 else 1)
+    h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
+    if p99_mode == "sample" and not per_patch_stats:
+        # basis, SNMF info, pooled p99 and the absent flags in ONE read
+        from . import stats as dstats
+        from .normalize import _STAIN_NAMES
+
+        vals, absent = dstats.segment_percentiles(h, offsets, 99.0)
+        packed = t.cat([r.basis.reshape(-1), r.info.reshape(-1).to(t.float64),
+                        vals.reshape(-1), absent.reshape(-1).to(t.float64)]).cpu().numpy()
+        basis, info = packed[:6].reshape(3, 2).copy(), packed[6:10].astype(np.int64)
+        snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
+        for j in range(2):
+            if packed[12 + j]:
+                raise StainAbsentError(f"density stats: stain absent: no {_STAIN_NAMES[j]} "
+                                       "density observed")
+        p99 = packed[10:12].copy()
+        if not (np.isfinite(p99).all() and (p99 >= 0).all()):
+            raise ValueError(f"density stats: p99 must be finite and non-negative, got {p99}")
+        st = StainStats(p99=p99, sample_count=m)
+        stats.basis_fit_s += time.perf_counter() - t0
+        fields = _cfg_fields(plan, cfg, code_lam, per_patch_stats)
+        provenance = {"source": str(source_label), "config_hash": config_hash(fields)}
+        return FitParams(i0=i0, basis=basis, stats=st, provenance=provenance)
     info = r.info.cpu().numpy()[0]
     basis = r.basis.cpu().numpy()[0]
     snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
-    h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
     if p99_mode == "global":
         from .global_stats import global_p99
 
@@ -408,7 +538,8 @@ def transform(slide, source: FitParams, target: FitParams, sink, *,
     plan = XformPlan(source.i0, source.basis, code_lam, factors, target.basis, target.i0,
                      precision=precision)
     t0 = time.perf_counter()
-    plan.maybe_calibrate(width * slide.height)
+    one_launch = isinstance(slide, DeviceSource)
+    plan.maybe_calibrate(width * slide.height, inline=one_launch)
 
     if isinstance(slide, DeviceSource):
         src = slide.tensor

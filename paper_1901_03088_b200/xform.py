@@ -16,6 +16,9 @@ from . import _dev, _lib
 from .optics import od_table
 
 
+CALIBRATE_INLINE = -1.0   # include/spcn.h SPCN_CALIBRATE_INLINE
+
+
 class XformPlan:
     """Packed spcn_xform_params for one recoloring (host-side, reusable)."""
 
@@ -56,9 +59,16 @@ class XformPlan:
             self.params.cert_alpha = self.alpha if self.alpha > 0 else 0.0
         return self.alpha
 
-    def maybe_calibrate(self, npix: int, stream=None) -> None:
+    def maybe_calibrate(self, npix: int, stream=None, inline: bool = False) -> None:
+        """Use the calibrated bound for large images.  inline=True leaves the
+        calibration to the next run (on the device, no host round trip) —
+        for a single launch over the whole image; many launches (streamed
+        strips) should calibrate once up front instead."""
         if self.precision == "exact" and npix >= self.CALIBRATE_MIN_PIXELS:
-            self.calibrate(stream)
+            if inline:
+                self.params.cert_alpha = CALIBRATE_INLINE
+            else:
+                self.calibrate(stream)
 
     def run(self, src, dst, npix: int, stream=None) -> None:
         """src/dst: CUDA uint8 tensors (or raw device pointers) holding npix RGB pixels."""
