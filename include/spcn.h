@@ -267,9 +267,9 @@ int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int
  * src/pipeline.py:176), coded like code_densities (src/stain_sep.py:168-201)
  * with p->src_i0 / src_basis / code_lam / max_sweeps (target fields unused).
  * spcn_stats_hist: fp32 densities binned into hist[j*nbins + bin], bin =
- * (float_bits(h_j) - base[j]) >> shift[j] (keys below base are counted in
- * counts[1+j]; counts[0] += non-white pixels; h = 0 counts into bin 0 when
- * base[j] == 0).  Approximate: it only places the refine window.
+ * (float_bits(h_j) - base[j]) >> shift[j], shift <= 23 (keys below base are
+ * counted in counts[1+j]; counts[0] += non-white pixels; h = 0 counts into
+ * bin 0 when base[j] == 0).  Approximate: it only places the refine window.
  * spcn_stats_refine: exact classification against [lo[j], hi[j]): densities
  * that may lie in the window are recomputed in fp64 in the reference's order
  * (once per colour per CTA); counts[j] += exact count below lo[j],

@@ -499,8 +499,18 @@ int stats_setup(const spcn_xform_params* p, int32_t white, StatsArgs& a, StrictP
   double coef[2];
   density_error_coeffs(sp, coef);
   for (int j = 0; j < 2; ++j)   // ill-conditioned basis: every candidate goes through fp64
-    a.coef[j] = ok ? static_cast<float>(coef[j] * (1.0 + 1e-6)) : INFINITY;
+    a.coef[j] = ok ? std::nextafter(static_cast<float>(coef[j] * (1.0 + 2e-6)), INFINITY)
+                   : INFINITY;
   a.white = static_cast<uint32_t>(white);
+  // the OD table is strictly decreasing across [white, white + 1] when
+  // 1 <= white < i0 (clip(x, 1, i0) grows there), so "x > white" is "OD(x) <
+  // OD(white)" and the white test can run on the looked-up OD values
+  bool by_od = white >= 1 && white <= 254;
+  for (int c = 0; c < 3; ++c) {
+    by_od = by_od && p->src_i0[c] > white && a.lut[c][white + (white < 255)] < a.lut[c][white];
+    a.nwod[c] = by_od ? -a.lut[c][white] : 0.0f;
+  }
+  a.white_by_od = by_od ? 1u : 0u;
   return SPCN_OK;
 }
 }  // namespace
@@ -523,7 +533,7 @@ int spcn_stats_hist(const uint8_t* src, int64_t npix, const spcn_xform_params* p
   int rc = stats_setup(p, white_threshold, a, sp);
   if (rc) return rc;
   for (int j = 0; j < 2; ++j) {
-    if (shift[j] > 31) return fail(SPCN_EINVAL, "shift must be <= 31");
+    if (shift[j] > 23) return fail(SPCN_EINVAL, "shift must be <= 23");
     a.base[j] = base[j];
     a.shift[j] = shift[j];
     a.a[j] = a.b[j] = 0.0;

@@ -34,125 +34,250 @@
 
 namespace spcn {
 
-constexpr int kStThreads = 512;
-constexpr int kStRep = 16;
 constexpr int kStBins = 8192;
-constexpr size_t kStSmemHist = LutLayout<kStRep>::kBytes + 2 * kStBins * sizeof(uint32_t);
+constexpr int kSlicePx = 512;            // one TMA bulk load: 512 px = 1536 B
+constexpr int kSliceBytes = 3 * kSlicePx;
+
+// Ring geometry: CW warps per CTA, NSW slots per warp.
+template <int CW, int NSW>
+struct StRing {
+  static constexpr int kThreads = 32 * CW;
+  static constexpr size_t kBytes = (size_t)CW * NSW * kSliceBytes + (size_t)CW * NSW * 8;
+};
+// histogram pass: 32 warps (<= 64 registers), 2 slots each
+#ifndef SPCN_HIST_CW
+#define SPCN_HIST_CW 32
+#endif
+constexpr int kHistCW = SPCN_HIST_CW, kHistNSW = kHistCW == 32 ? 2 : 3;
+// refine pass
+#ifndef SPCN_REF_CW
+#define SPCN_REF_CW 32
+#endif
+constexpr int kRefCW = SPCN_REF_CW, kRefNSW = kRefCW == 32 ? 2 : 3;
+constexpr size_t kStSmemHist = LutLayout<16>::kBytes + 2 * (kStBins + 8) * sizeof(uint32_t) +
+                               StRing<kHistCW, kHistNSW>::kBytes;
 
 __device__ __forceinline__ uint32_t st_byte(const uint32_t* w, int idx) {
   return (w[idx >> 2] >> (8 * (idx & 3))) & 0xffu;
 }
 
-// 16 pixels of a lane: non-white flags (bit k = pixel k) and fp32 densities.
-__device__ __forceinline__ uint32_t st_block(const StatsArgs& a, const uint8_t* lut,
-                                             const uint32_t* lc, const uint32_t* w, float* h0,
-                                             float* h1, float* T) {
-  uint32_t nonwhite = 0;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const uint32_t r = st_byte(w, 3 * k), g = st_byte(w, 3 * k + 1), b = st_byte(w, 3 * k + 2);
-    if (!(r > a.white && g > a.white && b > a.white)) nonwhite |= 1u << k;
+// Every warp streams its share of the 512-px slices of the 16-px-aligned body
+// [0, nbody) through a private ring of NSW shared-memory slots (1-D TMA bulk
+// loads, mbarrier completion; lane 0 refills a slot as soon as the warp has
+// read it) and calls body(w, 16, inv, blk) with each lane's 16 pixels (48
+// bytes, also readable at blk until body returns; inv = all ones for a lane
+// past the end of a short slice, whose pixels must all be ignored).  The
+// < 16-px tail is read from global memory by one lane: body(w, nvalid, 0, w).
+template <int CW, int NSW, class Body>
+__device__ __forceinline__ void st_scan(const uint8_t* __restrict__ src, int64_t npix,
+                                        uint8_t* ring, Body&& body) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* myslots = ring + (size_t)warp * NSW * kSliceBytes;
+  uint64_t* mybar = reinterpret_cast<uint64_t*>(ring + (size_t)CW * NSW * kSliceBytes) + warp * NSW;
+  const int64_t nbody = npix & ~int64_t(15);
+  const int64_t nsl = (nbody + kSlicePx - 1) / kSlicePx;
+  const int64_t gw = (int64_t)blockIdx.x * CW + warp, GW = (int64_t)gridDim.x * CW;
+  uint64_t pol = 0;
+  auto issue = [&](int64_t k) {   // lane 0 only
+    const int64_t j = gw + k * GW;
+    if (j >= nsl) return;
+    const int s = (int)(k % NSW);
+    const int64_t left = nbody - j * kSlicePx;
+    const uint32_t bytes = static_cast<uint32_t>(3 * (left < kSlicePx ? left : kSlicePx));
+    mbar_expect_tx(&mybar[s], bytes);
+    bulk_g2s(myslots + s * kSliceBytes, src + 3 * j * kSlicePx, bytes, &mybar[s], pol);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < NSW; ++s) mbar_init(&mybar[s], 1);
+    mbar_fence_init();
+    pol = policy_evict_first();
+    for (int k = 0; k < NSW; ++k) issue(k);
   }
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int ia = 6 * q, ib = 6 * q + 3;
-    const float2 v0 = make_float2(od_lookup(lut, w, ia, lc[0]), od_lookup(lut, w, ib, lc[0]));
-    const float2 v1 = make_float2(od_lookup(lut, w, ia + 1, lc[1]), od_lookup(lut, w, ib + 1, lc[1]));
-    const float2 v2 = make_float2(od_lookup(lut, w, ia + 2, lc[2]), od_lookup(lut, w, ib + 2, lc[2]));
-    const FastDensity d = fast_density(a.fs, v0, v1, v2);
-    h0[2 * q] = 0.5f * d.h0x2.x;
-    h0[2 * q + 1] = 0.5f * d.h0x2.y;
-    h1[2 * q] = 0.5f * d.h1x2.x;
-    h1[2 * q + 1] = 0.5f * d.h1x2.y;
-    T[2 * q] = d.T.x;
-    T[2 * q + 1] = d.T.y;
-  }
-  return nonwhite;
-}
-
-__device__ __forceinline__ void st_load(const uint8_t* src, int64_t blk, uint32_t* w) {
-  const uint4* q = reinterpret_cast<const uint4*>(src + 48 * blk);
-  const uint4 q0 = __ldcs(q), q1 = __ldcs(q + 1), q2 = __ldcs(q + 2);
-  w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-  w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-  w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
-}
-
-// tail pixels (npix % 16) as a partial block: missing pixels read as white
-__device__ __forceinline__ void st_load_tail(const uint8_t* src, int64_t blk, int64_t npix,
-                                             uint32_t* w) {
-  for (int t = 0; t < 12; ++t) w[t] = 0xffffffffu;
-  const int64_t p0 = 16 * blk;
-  for (int k = 0; k < 16 && p0 + k < npix; ++k)
-    for (int c = 0; c < 3; ++c) {
-      const int idx = 3 * k + c;
-      const uint32_t byte = src[3 * (p0 + k) + c];
-      w[idx >> 2] = (w[idx >> 2] & ~(0xffu << (8 * (idx & 3)))) | (byte << (8 * (idx & 3)));
+  __syncwarp();
+  for (int64_t k = 0;; ++k) {
+    const int64_t j = gw + k * GW;
+    if (j >= nsl) break;
+    const int s = (int)(k % NSW);
+    mbar_wait(&mybar[s], (uint32_t)((k / NSW) & 1));
+    const int64_t left = nbody - j * kSlicePx;
+    {   // no divergent branch: lanes past the end of a short slice run on
+        // stale slot bytes with every pixel masked (body's `all_invalid`)
+      const uint4* q = reinterpret_cast<const uint4*>(myslots + s * kSliceBytes + 48 * lane);
+      const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
+      const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y,
+                              q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+      body(w, 16, 16 * lane < left ? 0u : ~0u,
+           myslots + s * kSliceBytes + 48 * lane);
     }
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async_smem();   // the warp's reads of slot s precede its refill
+      issue(k + NSW);
+    }
+  }
+  if (npix > nbody && blockIdx.x == 0 && threadIdx.x == 0) {
+    uint32_t w[12];
+    for (int t = 0; t < 12; ++t) w[t] = 0;
+    for (int64_t p = nbody; p < npix; ++p)
+      for (int c = 0; c < 3; ++c) {
+        const int idx = 3 * (int)(p - nbody) + c;
+        w[idx >> 2] |= (uint32_t)src[3 * p + c] << (8 * (idx & 3));
+      }
+    body(w, (int)(npix - nbody), 0u, reinterpret_cast<const uint8_t*>(w));
+  }
 }
 
-__global__ void __launch_bounds__(kStThreads, 1)
+// Two pixels (2q, 2q+1) of a lane's block: fp32 densities and non-white flags
+// (bit 0: pixel 2q, bit 1: pixel 2q+1).
+struct StPair {
+  float2 h0x2, h1x2, T;   // 2*h0, 2*h1 (the halving is folded into the consumers' constants)
+  uint32_t wx, wy;        // all ones if the pixel is white, else 0
+};
+
+// od_lookup through an explicit shared-window address (lets the table base
+// ride in the load's uniform-register operand)
+__device__ __forceinline__ float st_od(uint32_t lut_s, const uint32_t* w, int idx, uint32_t lc) {
+  const uint32_t sel = 0x7604u | ((uint32_t)(idx & 3) << 4);
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lut_s + __byte_perm(w[idx >> 2], lc, sel)));
+  return v;
+}
+
+template <bool OD>
+__device__ __forceinline__ StPair st_pair(const StatsArgs& a, const uint8_t* lut,
+                                          const uint32_t* lc, const uint32_t* w, int q) {
+  const int ia = 6 * q, ib = 6 * q + 3;
+  const uint32_t ls = smem_u32(lut);
+  const float2 v0 = make_float2(st_od(ls, w, ia, lc[0]), st_od(ls, w, ib, lc[0]));
+  const float2 v1 = make_float2(st_od(ls, w, ia + 1, lc[1]), st_od(ls, w, ib + 1, lc[1]));
+  const float2 v2 = make_float2(st_od(ls, w, ia + 2, lc[2]), st_od(ls, w, ib + 2, lc[2]));
+  const FastDensity d = fast_density(a.fs, v0, v1, v2);
+  StPair o;
+  o.h0x2 = d.h0x2;
+  o.h1x2 = d.h1x2;
+  o.T = d.T;
+  if (OD) {
+    // v - OD(white) < 0 (sign bit; RN subtraction keeps the sign) <=> channel > white
+    const float2 s0 = __fadd2_rn(v0, bc2(a.nwod[0]));
+    const float2 s1 = __fadd2_rn(v1, bc2(a.nwod[1]));
+    const float2 s2 = __fadd2_rn(v2, bc2(a.nwod[2]));
+    const uint32_t wx = __float_as_uint(s0.x) & __float_as_uint(s1.x) & __float_as_uint(s2.x);
+    const uint32_t wy = __float_as_uint(s0.y) & __float_as_uint(s1.y) & __float_as_uint(s2.y);
+    o.wx = (uint32_t)((int32_t)wx >> 31);
+    o.wy = (uint32_t)((int32_t)wy >> 31);
+  } else {
+    uint32_t m[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int k = 2 * q + p;
+      const bool white = st_byte(w, 3 * k) > a.white && st_byte(w, 3 * k + 1) > a.white &&
+                         st_byte(w, 3 * k + 2) > a.white;
+      m[p] = white ? ~0u : 0u;
+    }
+    o.wx = m[0];
+    o.wy = m[1];
+  }
+  return o;
+}
+
+// fp32 density of one pixel (the fast path's arithmetic, bit-identical to
+// st_pair's for that pixel), bytes read from a lane block in memory.
+__device__ __forceinline__ FastDensity st_one(const StatsArgs& a, const uint8_t* lut,
+                                              const uint32_t* lc, const uint8_t* px) {
+  const float v0 = *reinterpret_cast<const float*>(lut + (((uint32_t)px[0] << 8) | lc[0]));
+  const float v1 = *reinterpret_cast<const float*>(lut + (((uint32_t)px[1] << 8) | lc[1]));
+  const float v2 = *reinterpret_cast<const float*>(lut + (((uint32_t)px[2] << 8) | lc[2]));
+  return fast_density(a.fs, bc2(v0), bc2(v1), bc2(v2));
+}
+
+// Histogram layout per stain in shared memory: [0] = below the window or
+// white (not read), [1 .. nbins] = the bins, [nbins + 1] = above the window.
+constexpr int kHistStride = kStBins + 8;
+
+template <bool OD>
+__global__ void __launch_bounds__(32 * kHistCW, 1)
     k_stats_hist(const uint8_t* __restrict__ src, int64_t npix, const __grid_constant__ StatsArgs a,
                  unsigned long long* __restrict__ hist, unsigned long long* __restrict__ counts) {
+  constexpr int kThreads = 32 * kHistCW;
   extern __shared__ __align__(128) uint8_t smem[];
-  const uint8_t* lut = smem;
-  uint32_t* sh = reinterpret_cast<uint32_t*>(smem + LutLayout<kStRep>::kBytes);
-  LutLayout<kStRep>::fill(smem, &a.lut[0][0], threadIdx.x, kStThreads);
-  for (int i = threadIdx.x; i < 2 * kStBins; i += kStThreads) sh[i] = 0;
+  uint32_t* sh = reinterpret_cast<uint32_t*>(smem + LutLayout<16>::kBytes);
+  uint8_t* ring = smem + LutLayout<16>::kBytes + 2 * kHistStride * sizeof(uint32_t);
+  LutLayout<16>::fill(smem, &a.lut[0][0], threadIdx.x, kThreads);
+  for (int i = threadIdx.x; i < 2 * kHistStride; i += kThreads) sh[i] = 0;
   __syncthreads();
   uint32_t lc[3];
-  LutLayout<kStRep>::lane_consts(threadIdx.x & 31, lc);
-  unsigned long long nonwhite = 0, below[2] = {0, 0}, zero[2] = {0, 0};
-  const int64_t nblk = (npix + 15) / 16, full = npix / 16;
-  const int64_t stride = (int64_t)gridDim.x * kStThreads;
-  uint32_t nxt[12];   // software prefetch: the next block is in flight while this one computes
-  int64_t blk = blockIdx.x * (int64_t)kStThreads + threadIdx.x;
-  if (blk < nblk) {
-    if (blk < full) st_load(src, blk, nxt); else st_load_tail(src, blk, npix, nxt);
-  }
-  for (; blk < nblk; blk += stride) {
-    uint32_t w[12];
+  LutLayout<16>::lane_consts(threadIdx.x & 31, lc);
+  // Keys are taken of 2h: key(2h) = key(h) + 2^23 over the normal range, so
+  // the window start moves instead of every density being halved (the
+  // histogram only places the refine window; subnormal h may land a bin off).
+  // Slot of a key: min((max(key, lo) - lo) >> shift, nbins + 1) with lo one
+  // bin below the window start, so below-the-window keys (and white pixels,
+  // whose key is zeroed) land in slot 0 without a branch.  Every pixel does
+  // one shared atomic per stain (cheaper here than compacting the few
+  // in-window pixels: the kernel is ALU-bound and a divergent loop over
+  // candidates costs more than the atomics); "below" = non-white - slots
+  // 1..nbins+1, per CTA at the end (with base 0 that is h = 0, i.e. bin 0).
+  constexpr uint32_t kTwo = 1u << 23;
+  const uint32_t s0 = a.shift[0], s1 = a.shift[1];
+  const uint32_t lo0 = a.base[0] + kTwo - (1u << s0), lo1 = a.base[1] + kTwo - (1u << s1);
+  const uint32_t top = (uint32_t)a.nbins + 1u;
+  uint32_t* hs0 = reinterpret_cast<uint32_t*>(smem + LutLayout<16>::kBytes);
+  uint32_t* hs1 = hs0 + kHistStride;
+  int32_t nonwhite = 0;
+  st_scan<kHistCW, kHistNSW>(src, npix, ring,
+                             [&](const uint32_t* w, int nv, uint32_t inv, const uint8_t*) {
 #pragma unroll
-    for (int t = 0; t < 12; ++t) w[t] = nxt[t];
-    if (blk + stride < nblk) {
-      if (blk + stride < full) st_load(src, blk + stride, nxt);
-      else st_load_tail(src, blk + stride, npix, nxt);
-    }
-    float h0[16], h1[16], T[16];
-    const uint32_t nw = st_block(a, lut, lc, w, h0, h1, T);
-    nonwhite += __popc(nw);
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      if (!((nw >> k) & 1u)) continue;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint32_t key = __float_as_uint(j ? h1[k] : h0[k]);
-        if (key == 0u && a.base[j] == 0u) { ++zero[j]; continue; }   // h = 0: bin 0, no atomics
-        if (key < a.base[j]) { ++below[j]; continue; }
-        const uint32_t d = (key - a.base[j]) >> a.shift[j];
-        if (d < (uint32_t)a.nbins) hist_add_agg(sh + j * kStBins, d);
+    for (int q = 0; q < 8; ++q) {
+      const StPair d = st_pair<OD>(a, smem, lc, w, q);
+      uint32_t wx = d.wx | inv, wy = d.wy | inv;
+      if (nv < 16) {
+        if (2 * q >= nv) wx = ~0u;
+        if (2 * q + 1 >= nv) wy = ~0u;
       }
+      nonwhite += 2 + (int32_t)wx + (int32_t)wy;
+      const uint32_t k0x = __float_as_uint(d.h0x2.x) & ~wx, k1x = __float_as_uint(d.h1x2.x) & ~wx;
+      const uint32_t k0y = __float_as_uint(d.h0x2.y) & ~wy, k1y = __float_as_uint(d.h1x2.y) & ~wy;
+      atomicAdd(hs0 + min((max(k0x, lo0) - lo0) >> s0, top), 1u);
+      atomicAdd(hs1 + min((max(k1x, lo1) - lo1) >> s1, top), 1u);
+      atomicAdd(hs0 + min((max(k0y, lo0) - lo0) >> s0, top), 1u);
+      atomicAdd(hs1 + min((max(k1y, lo1) - lo1) >> s1, top), 1u);
     }
+  });
+  __syncthreads();
+  // flush the bins; count this CTA's binned pixels (incl. above) per stain
+  const int nb = a.nbins;
+  unsigned long long binned0 = 0, binned1 = 0;
+  for (int i = 1 + threadIdx.x; i <= nb + 1; i += kThreads) {
+    const uint32_t c0 = sh[i], c1 = sh[kHistStride + i];
+    binned0 += c0;
+    binned1 += c1;
+    if (i <= nb) {
+      if (c0) atomicAdd(&hist[i - 1], (unsigned long long)c0);
+      if (c1) atomicAdd(&hist[nb + i - 1], (unsigned long long)c1);
+    }
+  }
+  __shared__ unsigned long long red[32][3];
+  unsigned long long nwl = nonwhite;
+  for (int off = 16; off; off >>= 1) {
+    nwl += __shfl_xor_sync(0xffffffffu, nwl, off);
+    binned0 += __shfl_xor_sync(0xffffffffu, binned0, off);
+    binned1 += __shfl_xor_sync(0xffffffffu, binned1, off);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[warp][0] = nwl;
+    red[warp][1] = binned0;
+    red[warp][2] = binned1;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < a.nbins; i += kStThreads)
+  if (threadIdx.x == 0) {
+    unsigned long long t[3] = {0, 0, 0};
+    for (int k = 0; k < kHistCW; ++k)
+      for (int c = 0; c < 3; ++c) t[c] += red[k][c];
+    if (t[0]) atomicAdd(&counts[0], t[0]);
     for (int j = 0; j < 2; ++j) {
-      uint32_t c = sh[j * kStBins + i];
-      if (c) atomicAdd(&hist[j * a.nbins + i], (unsigned long long)c);
-    }
-  // zeros belong to bin 0 of a window starting at key 0
-  for (int off = 16; off; off >>= 1) {
-    nonwhite += __shfl_xor_sync(0xffffffffu, nonwhite, off);
-    for (int j = 0; j < 2; ++j) {
-      below[j] += __shfl_xor_sync(0xffffffffu, below[j], off);
-      zero[j] += __shfl_xor_sync(0xffffffffu, zero[j], off);
-    }
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (nonwhite) atomicAdd(&counts[0], nonwhite);
-    for (int j = 0; j < 2; ++j) {
-      if (below[j]) atomicAdd(&counts[1 + j], below[j]);
-      if (zero[j]) atomicAdd(&hist[j * a.nbins], zero[j]);
+      const unsigned long long below = t[0] - t[1 + j];
+      if (below) atomicAdd(a.base[j] ? &counts[1 + j] : &hist[j * nb], below);
     }
   }
 }
@@ -161,7 +286,7 @@ __global__ void __launch_bounds__(kStThreads, 1)
 // pixel's RGB only, and the pixels that can fall in the narrow window share
 // few colours, so each CTA evaluates a colour in fp64 once and keeps in-window
 // pixel counts per colour; at the end it lists (value, count) pairs.
-constexpr int kSlots = 2048;
+constexpr int kSlots = kRefCW == 32 ? 1024 : 2048;   // fits next to the ring
 constexpr uint32_t kEmpty = 0xffffffffu;
 struct ColourSlot {
   uint32_t key;        // rgb, or kEmpty
@@ -169,139 +294,199 @@ struct ColourSlot {
   uint32_t cnt[2];     // in-window pixels per stain
   double x[2];         // exact densities
 };
-constexpr size_t kStSmemRefine =
-    LutLayout<kStRep>::kBytes + 3 * 256 * sizeof(double) + kSlots * sizeof(ColourSlot);
+constexpr size_t kStSmemRefine = LutLayout<16>::kBytes + 3 * 256 * sizeof(double) +
+                                 kSlots * sizeof(ColourSlot) + StRing<kRefCW, kRefNSW>::kBytes;
 
 __device__ __forceinline__ uint32_t colour_hash(uint32_t rgb) {
-  return (rgb * 2654435761u) >> (32 - 11);
+  return (rgb * 2654435761u) >> (32 - (kSlots == 1024 ? 10 : 11));
 }
 
-__global__ void __launch_bounds__(kStThreads, 1)
-    k_stats_refine(const uint8_t* __restrict__ src, int64_t npix,
-                   const __grid_constant__ StatsArgs a, const __grid_constant__ StrictP sp,
-                   unsigned long long* __restrict__ counts, double* __restrict__ cand,
-                   unsigned long long* __restrict__ wcnt, unsigned long long cap) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const uint8_t* lut = smem;
-  double* dlut = reinterpret_cast<double*>(smem + LutLayout<kStRep>::kBytes);
-  ColourSlot* tab = reinterpret_cast<ColourSlot*>(smem + LutLayout<kStRep>::kBytes +
-                                                  3 * 256 * sizeof(double));
-  LutLayout<kStRep>::fill(smem, &a.lut[0][0], threadIdx.x, kStThreads);
-  for (int i = threadIdx.x; i < 3 * 256; i += kStThreads) dlut[i] = sp.lut[i >> 8][i & 255];
-  for (int i = threadIdx.x; i < kSlots; i += kStThreads) {
-    tab[i].key = kEmpty;
-    tab[i].ready = 0;
-    tab[i].cnt[0] = tab[i].cnt[1] = 0;
-  }
-  __syncthreads();
-  uint32_t lc[3];
-  LutLayout<kStRep>::lane_consts(threadIdx.x & 31, lc);
-  const NnlsGram G = gram_of(sp);
-  unsigned long long below[2] = {0, 0}, exact_evals = 0;
-  const int64_t nblk = (npix + 15) / 16, full = npix / 16;
-  auto list = [&](int j, double x, unsigned long long c) {   // one (value, count) entry
+struct RefineCtx {
+  const StatsArgs& a;
+  const StrictP& sp;
+  const NnlsGram& G;
+  const double* dlut;
+  ColourSlot* tab;
+  unsigned long long* counts;
+  double* cand;
+  unsigned long long* wcnt;
+  unsigned long long cap;
+
+  __device__ void list(int j, double x, unsigned long long c) const {   // one (value, count) entry
     atomicAdd(&counts[2 + j], c);
     const unsigned long long idx = atomicAdd(&counts[5 + j], 1ull);
     if (idx < cap) {
       cand[j * cap + idx] = x;
       wcnt[j * cap + idx] = c;
     }
-  };
-  const int64_t stride = (int64_t)gridDim.x * kStThreads;
-  uint32_t nxt[12];   // software prefetch: the next block is in flight while this one computes
-  int64_t blk = blockIdx.x * (int64_t)kStThreads + threadIdx.x;
-  if (blk < nblk) {
-    if (blk < full) st_load(src, blk, nxt); else st_load_tail(src, blk, npix, nxt);
   }
-  for (; blk < nblk; blk += stride) {
-    uint32_t w[12];
-#pragma unroll
-    for (int t = 0; t < 12; ++t) w[t] = nxt[t];
-    if (blk + stride < nblk) {
-      if (blk + stride < full) st_load(src, blk + stride, nxt);
-      else st_load_tail(src, blk + stride, npix, nxt);
-    }
-    float h0[16], h1[16], T[16];
-    const uint32_t nw = st_block(a, lut, lc, w, h0, h1, T);
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      if (!((nw >> k) & 1u)) continue;
-      uint32_t need = 0;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const double h = (double)(j ? h1[k] : h0[k]);
-        const double eps = (double)a.coef[j] * (double)T[k] * (1.0 + 1e-6) + 1e-30;
-        if (h + eps < a.a[j]) ++below[j];          // surely below the window
-        else if (!(h - eps >= a.b[j])) need |= 1u << j;   // may lie in [a, b)
+
+  // fp64 density of a colour that may lie in the window (bit j of `need`),
+  // through the colour cache; updates the exact below counts
+  // returns bit 0/1: NOT below the window (stain 0/1, among `need`), bit 2:
+  // an fp64 evaluation was made
+  __device__ __noinline__ uint32_t exact(uint32_t rgb, uint32_t need) const {
+    uint32_t r = 0;
+    // find or claim a slot; a slot claimed but not yet filled by another
+    // thread is simply recomputed here (no waiting)
+    int slot = -1;
+    double x[2];
+    bool have = false;
+    uint32_t s = colour_hash(rgb);
+    for (int probe = 0; probe < 8; ++probe, s = (s + 1) & (kSlots - 1)) {
+      uint32_t key = *(volatile uint32_t*)&tab[s].key;
+      if (key == kEmpty) key = atomicCAS(&tab[s].key, kEmpty, rgb) == kEmpty ? kEmpty - 1 : tab[s].key;
+      if (key == kEmpty - 1) {                   // claimed by us: fill it below
+        slot = (int)s;
+        break;
       }
-      if (!need) continue;
-      const uint32_t rgb = st_byte(w, 3 * k) | (st_byte(w, 3 * k + 1) << 8) |
-                           (st_byte(w, 3 * k + 2) << 16);
-      // colour cache: find or claim a slot; a slot claimed but not yet filled
-      // by another thread is simply recomputed here (no waiting)
-      int slot = -1;
-      double x[2];
-      bool have = false;
-      uint32_t s = colour_hash(rgb);
-      for (int probe = 0; probe < 8; ++probe, s = (s + 1) & (kSlots - 1)) {
-        uint32_t key = *(volatile uint32_t*)&tab[s].key;
-        if (key == kEmpty) key = atomicCAS(&tab[s].key, kEmpty, rgb) == kEmpty ? kEmpty - 1 : tab[s].key;
-        if (key == kEmpty - 1) {                   // claimed by us: fill it below
-          slot = (int)s;
-          break;
+      if (key == rgb) {
+        slot = (int)s;
+        if (*(volatile uint32_t*)&tab[s].ready) {
+          x[0] = tab[s].x[0];
+          x[1] = tab[s].x[1];
+          have = true;
         }
-        if (key == rgb) {
-          slot = (int)s;
-          if (*(volatile uint32_t*)&tab[s].ready) {
-            x[0] = tab[s].x[0];
-            x[1] = tab[s].x[1];
-            have = true;
-          }
-          break;
-        }
-      }
-      if (!have) {
-        ++exact_evals;
-        const double v0 = dlut[rgb & 255u], v1 = dlut[256 + ((rgb >> 8) & 255u)],
-                     v2 = dlut[512 + (rgb >> 16)];
-        const double b0 = strict_dot3(sp.ws[0][0], sp.ws[1][0], sp.ws[2][0], v0, v1, v2);
-        const double b1 = strict_dot3(sp.ws[0][1], sp.ws[1][1], sp.ws[2][1], v0, v1, v2);
-        strict_nnls(b0, b1, G, sp.lam, sp.max_sweeps, sp.tol, x[0], x[1]);
-        if (slot >= 0 && tab[slot].key == rgb && !tab[slot].ready) {
-          tab[slot].x[0] = x[0];
-          tab[slot].x[1] = x[1];
-          __threadfence_block();
-          atomicExch(&tab[slot].ready, 1u);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        if (!((need >> j) & 1u)) continue;
-        if (x[j] < a.a[j]) {
-          ++below[j];
-        } else if (x[j] < a.b[j]) {
-          if (slot >= 0) atomicAdd(&tab[slot].cnt[j], 1u);
-          else list(j, x[j], 1ull);                // cache full: list the pixel itself
-        }
+        break;
       }
     }
+    if (!have) {
+      r |= 4u;
+      const double v0 = dlut[rgb & 255u], v1 = dlut[256 + ((rgb >> 8) & 255u)],
+                   v2 = dlut[512 + (rgb >> 16)];
+      const double b0 = strict_dot3(sp.ws[0][0], sp.ws[1][0], sp.ws[2][0], v0, v1, v2);
+      const double b1 = strict_dot3(sp.ws[0][1], sp.ws[1][1], sp.ws[2][1], v0, v1, v2);
+      strict_nnls(b0, b1, G, sp.lam, sp.max_sweeps, sp.tol, x[0], x[1]);
+      if (slot >= 0 && tab[slot].key == rgb && !tab[slot].ready) {
+        tab[slot].x[0] = x[0];
+        tab[slot].x[1] = x[1];
+        __threadfence_block();
+        atomicExch(&tab[slot].ready, 1u);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (!((need >> j) & 1u)) continue;
+      if (x[j] < a.a[j]) continue;
+      r |= 1u << j;
+      if (x[j] < a.b[j]) {
+        if (slot >= 0) atomicAdd(&tab[slot].cnt[j], 1u);
+        else list(j, x[j], 1ull);                // cache full: list the pixel itself
+      }
+    }
+    return r;
+  }
+
+  // Full classification of one non-white candidate pixel (bytes at px):
+  // returns bit 0/1: not below the window (stain 0/1), bit 2: an fp64
+  // evaluation was made.  Same bounds as the kernel's fast test.
+  __device__ __forceinline__ uint32_t pixel(const uint8_t* lut, const uint32_t* lc,
+                                            const uint8_t* px) const {
+    const FastDensity d = st_one(a, lut, lc, px);
+    const float T = d.T.x;
+    float up[2], dn[2];
+    up[0] = __fadd_ru(d.h0x2.x, __fmaf_ru(2.0f * a.coef[0], T, 2e-30f));
+    up[1] = __fadd_ru(d.h1x2.x, __fmaf_ru(2.0f * a.coef[1], T, 2e-30f));
+    dn[0] = __fadd_rd(d.h0x2.x, __fmaf_rd(-2.0f * a.coef[0], T, -2e-30f));
+    dn[1] = __fadd_rd(d.h1x2.x, __fmaf_rd(-2.0f * a.coef[1], T, -2e-30f));
+    uint32_t r = 0, need = 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (up[j] < 2.0f * __double2float_rd(a.a[j])) continue;         // surely below
+      if (dn[j] >= 2.0f * __double2float_ru(a.b[j])) r |= 1u << j;    // surely at/above b
+      else need |= 1u << j;
+    }
+    if (need) r |= exact((uint32_t)px[0] | ((uint32_t)px[1] << 8) | ((uint32_t)px[2] << 16), need);
+    return r;
+  }
+};
+
+template <bool OD>
+__global__ void __launch_bounds__(32 * kRefCW, 1)
+    k_stats_refine(const uint8_t* __restrict__ src, int64_t npix,
+                   const __grid_constant__ StatsArgs a, const __grid_constant__ StrictP sp,
+                   unsigned long long* __restrict__ counts, double* __restrict__ cand,
+                   unsigned long long* __restrict__ wcnt, unsigned long long cap) {
+  constexpr int kThreads = 32 * kRefCW;
+  extern __shared__ __align__(128) uint8_t smem[];
+  double* dlut = reinterpret_cast<double*>(smem + LutLayout<16>::kBytes);
+  ColourSlot* tab = reinterpret_cast<ColourSlot*>(smem + LutLayout<16>::kBytes +
+                                                  3 * 256 * sizeof(double));
+  uint8_t* ring = reinterpret_cast<uint8_t*>(tab + kSlots);
+  LutLayout<16>::fill(smem, &a.lut[0][0], threadIdx.x, kThreads);
+  for (int i = threadIdx.x; i < 3 * 256; i += kThreads) dlut[i] = sp.lut[i >> 8][i & 255];
+  for (int i = threadIdx.x; i < kSlots; i += kThreads) {
+    tab[i].key = kEmpty;
+    tab[i].ready = 0;
+    tab[i].cnt[0] = tab[i].cnt[1] = 0;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kSlots; i += kStThreads)
+  uint32_t lc[3];
+  LutLayout<16>::lane_consts(threadIdx.x & 31, lc);
+  const NnlsGram G = gram_of(sp);
+  const RefineCtx ctx{a, sp, G, dlut, tab, counts, cand, wcnt, cap};
+  // Classification in fp32 with directed rounding: with e >= the density
+  // error bound, h + e (rounded up) < a (rounded down) proves x < a, and
+  // h - e (rounded down) >= b (rounded up) proves x >= b.  Evaluated on 2h
+  // against 2e, 2a, 2b (scaling by 2 is exact).  The sign of (h + e) - a
+  // (RN keeps the sign of a difference) is the "surely below" flag; a pair
+  // whose four flags are set (white pixels count as set) costs no more.
+  // Below counts are derived at the end: below = non-white - not-below.
+  const float2 ea0 = bc2(2.0f * a.coef[0]), ea1 = bc2(2.0f * a.coef[1]), tiny = bc2(2e-30f);
+  const float2 nlo0 = bc2(-2.0f * __double2float_rd(a.a[0])), nlo1 = bc2(-2.0f * __double2float_rd(a.a[1]));
+  int32_t nonwhite = 0;
+  uint32_t nb0 = 0, nb1 = 0, evals = 0;   // not below, fp64 evaluations
+  st_scan<kRefCW, kRefNSW>(src, npix, ring,
+                           [&](const uint32_t* w, int nv, uint32_t inv, const uint8_t* blk) {
+    // pass 1, branch-free: non-white count and the candidates = non-white
+    // pixels not surely below the window in both stains
+    uint32_t cand = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const StPair d = st_pair<OD>(a, smem, lc, w, q);
+      uint32_t wx = d.wx | inv, wy = d.wy | inv;
+      if (nv < 16) {
+        if (2 * q >= nv) wx = ~0u;
+        if (2 * q + 1 >= nv) wy = ~0u;
+      }
+      nonwhite += 2 + (int32_t)wx + (int32_t)wy;
+      const float2 e0 = __ffma2_ru(ea0, d.T, tiny), e1 = __ffma2_ru(ea1, d.T, tiny);
+      const float2 eb0 = __fadd2_rn(__fadd2_ru(d.h0x2, e0), nlo0);
+      const float2 eb1 = __fadd2_rn(__fadd2_ru(d.h1x2, e1), nlo1);
+      const uint32_t sx = (__float_as_uint(eb0.x) & __float_as_uint(eb1.x)) | wx;
+      const uint32_t sy = (__float_as_uint(eb0.y) & __float_as_uint(eb1.y)) | wy;
+      cand |= (~sx >> 31) << (2 * q);
+      cand |= (~sy >> 31) << (2 * q + 1);
+    }
+    // pass 2: each lane pops one candidate per iteration
+    while (cand) {
+      const int k = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const uint32_t r = ctx.pixel(smem, lc, blk + 3 * k);
+      nb0 += r & 1u;
+      nb1 += (r >> 1) & 1u;
+      evals += r >> 2;
+    }
+  });
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSlots; i += kThreads)
     for (int j = 0; j < 2; ++j)
       if (tab[i].cnt[j]) {
         // counted only by threads that knew the value; its owner set it
         // (and `ready`) before this barrier
-        list(j, tab[i].x[j], tab[i].cnt[j]);
+        ctx.list(j, tab[i].x[j], tab[i].cnt[j]);
       }
+  unsigned long long b0 = (unsigned long long)(nonwhite - (int32_t)nb0),
+                     b1 = (unsigned long long)(nonwhite - (int32_t)nb1), ev = evals;
   for (int off = 16; off; off >>= 1) {
-    exact_evals += __shfl_xor_sync(0xffffffffu, exact_evals, off);
-    for (int j = 0; j < 2; ++j) below[j] += __shfl_xor_sync(0xffffffffu, below[j], off);
+    ev += __shfl_xor_sync(0xffffffffu, ev, off);
+    b0 += __shfl_xor_sync(0xffffffffu, b0, off);
+    b1 += __shfl_xor_sync(0xffffffffu, b1, off);
   }
   if ((threadIdx.x & 31) == 0) {
-    for (int j = 0; j < 2; ++j)
-      if (below[j]) atomicAdd(&counts[j], below[j]);
-    if (exact_evals) atomicAdd(&counts[4], exact_evals);
+    if (b0) atomicAdd(&counts[0], b0);
+    if (b1) atomicAdd(&counts[1], b1);
+    if (ev) atomicAdd(&counts[4], ev);
   }
 }
 
@@ -321,16 +506,19 @@ cudaError_t launch_stats_hist(const uint8_t* src, int64_t npix, const StatsArgs&
                               cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_stats_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)kStSmemHist);
-    if (e != cudaSuccess) return e;
+    for (auto k : {k_stats_hist<true>, k_stats_hist<false>}) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStSmemHist);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
   if (npix <= 0) return cudaSuccess;
-  const int64_t nblk = (npix + 15) / 16;
-  int64_t grid = (nblk + kStThreads - 1) / kStThreads;
+  const int64_t nsl = (npix + kSlicePx - 1) / kSlicePx;
+  int64_t grid = (nsl + kHistCW - 1) / kHistCW;
   if (grid > st_grid()) grid = st_grid();
-  k_stats_hist<<<(int)grid, kStThreads, kStSmemHist, st>>>(src, npix, a, hist, counts);
+  (a.white_by_od ? k_stats_hist<true> : k_stats_hist<false>)<<<(int)grid, 32 * kHistCW,
+                                                               kStSmemHist, st>>>(src, npix, a, hist, counts);
   return launched();
 }
 
@@ -341,16 +529,19 @@ cudaError_t launch_stats_refine(const uint8_t* src, int64_t npix, const StatsArg
   constexpr size_t smem = kStSmemRefine;
   static bool attr = false;
   if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_stats_refine, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem);
-    if (e != cudaSuccess) return e;
+    for (auto k : {k_stats_refine<true>, k_stats_refine<false>}) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
   if (npix <= 0) return cudaSuccess;
-  const int64_t nblk = (npix + 15) / 16;
-  int64_t grid = (nblk + kStThreads - 1) / kStThreads;
+  const int64_t nsl = (npix + kSlicePx - 1) / kSlicePx;
+  int64_t grid = (nsl + kRefCW - 1) / kRefCW;
   if (grid > st_grid()) grid = st_grid();
-  k_stats_refine<<<(int)grid, kStThreads, smem, st>>>(src, npix, a, sp, counts, cand, wcnt, cap);
+  (a.white_by_od ? k_stats_refine<true> : k_stats_refine<false>)<<<(int)grid, 32 * kRefCW, smem, st>>>(
+      src, npix, a, sp, counts, cand, wcnt, cap);
   return launched();
 }
 

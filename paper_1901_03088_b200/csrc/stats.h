@@ -10,6 +10,8 @@ struct StatsArgs {
   float lut[3][256];        // fp32 OD table
   float coef[2];            // density error bound per unit T (params.cuh density_error_coeffs)
   uint32_t white;           // white threshold: non-white = not all channels > white
+  uint32_t white_by_od;     // 1: channel > white  <=>  lut[c][x] < lut[c][white] (see stats.cu)
+  float nwod[3];            // -lut[c][white]
   uint32_t base[2];         // histogram window start (fp32 key) per stain
   uint32_t shift[2];        // bin = (key - base) >> shift
   int32_t nbins;            // <= 8192

@@ -225,16 +225,11 @@ class RowBandGroup:
         snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
         h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
         if p99_mode == "global":
-            from .global_stats import global_p99
+            from .global_stats import global_p99, sample_bracket
             from .normalize import StainStats
             from .pipeline import slide_chunks
 
-            from .errors import SlideNormError
-
-            try:
-                guess = stain_stats(h).p99
-            except SlideNormError:
-                guess = None
+            guess = sample_bracket(h)
             p99, nonwhite, _ = _stage("density stats", global_p99, slide_chunks(band_source), i0,
                                       r.basis.cpu().numpy()[0], code_lam, thr,
                                       comm=TorchComm(self.group), guess=guess)

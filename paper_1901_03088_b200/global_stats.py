@@ -9,8 +9,10 @@ basis exactly as code_densities (src/stain_sep.py:168-201) would, and returns
 exactly ``percentile(those densities, 99)`` (src/order_stats.py:11-36).
 
 Passes over the slide (csrc/stats.cu):
-  1. coarse histogram of fp32 densities (8192 bins of fp32 keys)   — K2
-  2. fine histogram around the bins holding ranks lo / hi          — K2
+  1. histogram of fp32 densities (8192 bins of fp32 keys) over the bracket
+     the sampled densities give (``sample_bracket``), else over all keys — K2
+  2. (only if the bins are still too wide) a finer histogram around the bins
+     holding ranks lo / hi                                          — K2
   3. exact refine: fp64 reference-order densities for the pixels that may
      fall in the final window, exact counts below it, the in-window values
      listed, then an exact select of the two ranks                  — K3
@@ -31,6 +33,8 @@ from .order_stats import interpolate
 NBINS = 8192
 SHIFT0 = 19              # fp32 key >> 19: 8192 bins over all non-negative floats
 CAND_CAP = 1 << 20       # in-window values listed per stain per rank (grown as needed)
+REFINE_MAX = 1 << 22     # refine a window once it holds <= this many pixels: its
+                         # pixels cost one colour-cache probe each, a zoom level a pass
 MIN_SHIFT = 6            # finest bins: 64 fp32 ulps, > 2x the fp32 density error
 
 _U32x2 = ctypes.c_uint32 * 2
@@ -124,6 +128,23 @@ class DeviceEngine:
         return counts, cand, wcnt
 
 
+def sample_bracket(h, p: float = 99.0):
+    """[lo, hi] per stain around the p-th percentile of the sampled densities
+    `h` ((2, m) device tensor, one row per stain): the sample quantiles
+    p -+ d, d = max(0.5, 600 * sqrt(p (1 - p) / m)) percent (6 standard errors
+    of the quantile at a 100x smaller effective sample).  One device sort, one
+    host read; None when the sample is empty."""
+    m = int(h.shape[1])
+    if m == 0:
+        return None
+    q = p / 100.0
+    d = max(0.005, 6.0 * math.sqrt(q * (1.0 - q) / m) * 10.0)
+    idx = [int(math.floor(max(0.0, q - d) * (m - 1))), int(math.ceil(min(1.0, q + d) * (m - 1)))]
+    t = _dev.torch()
+    srt = t.sort(h, dim=1).values
+    return srt[:, t.tensor(idx, device=h.device)].cpu().numpy()
+
+
 def weighted_select(values: np.ndarray, weights: np.ndarray, ks):
     """Order statistics of the multiset {values[i] repeated weights[i] times}
     (exact: a stable sort of the distinct values and integer cumulative
@@ -144,8 +165,12 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
                ``allgather(tensor) -> list`` for multi-GPU; None = one process.
     engine   : the pass implementation (default: the CUDA kernels; the CPU
                tests substitute an emulation of their contracts).
-    guess    : optional estimate of the two percentiles (the sample p99): the
-               first histogram level then spans +-2 octaves around it.
+    guess    : optional estimate of the two percentiles: a point (2,) (the
+               first histogram level then spans +-2 octaves around it) or a
+               bracket (2, 2) of [lo, hi] per stain (``sample_bracket``: the
+               first level spans the bracket, usually fine enough to refine
+               directly — two passes in all).  A miss costs one full-range
+               level.
     Returns (p99 ndarray(2), non-white pixel count, info dict).
     """
     comm = comm or _Local()
@@ -177,20 +202,23 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
     # holding ranks lo..hi (one bin of margin each side) until the window is
     # small enough to list, or its bins reach the fp32 error scale
     base, shift = [0, 0], [SHIFT0, SHIFT0]
-    if guess is not None and all(g > 0 and math.isfinite(g) for g in guess):
-        # start from +-2 octaves around an estimate (e.g. the sample p99); a
-        # miss falls back to the full-range level below
+    g = None if guess is None else np.asarray(guess, dtype=np.float64)
+    if g is not None and g.shape == (2,) and all(x > 0 and math.isfinite(x) for x in g):
+        g = np.stack([g / 4.0, g * 4.0], axis=1)       # +-2 octaves around a point
+    if g is not None and g.shape == (2, 2) and np.isfinite(g).all() and (g >= 0).all() \
+            and (g[:, 1] >= g[:, 0]).all():
+        # start from the estimated bracket; a miss falls back to the
+        # full-range level below
         for j in range(2):
-            k0 = _key_of(guess[j] / 4.0)
-            base[j], shift[j] = k0, max(MIN_SHIFT, ((_key_of(guess[j] * 4.0) - k0) // NBINS)
-                                         .bit_length())
+            k0, k1 = _key_of(g[j, 0]), _key_of(g[j, 1]) + 1
+            base[j], shift[j] = k0, max(MIN_SHIFT, ((k1 - k0 - 1) // NBINS).bit_length())
     h, c = hist_pass(base, shift)
     n = int(c[0])
     if n == 0:
         raise StainAbsentError("stain absent: no non-white pixels in the slide")
     rank = (p / 100.0) * (n - 1)
     klo, khi = int(math.floor(rank)), int(math.ceil(rank))
-    if guess is not None and base != [0, 0]:
+    if g is not None and shift != [SHIFT0, SHIFT0]:
         inside = all(int(c[1 + j]) <= klo and khi < int(c[1 + j] + h[j].sum()) for j in range(2))
         if not inside:
             base, shift = [0, 0], [SHIFT0, SHIFT0]
@@ -211,7 +239,10 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
         if win is None:
             break
         windows.append((win, max(est)))
-        if max(est) <= CAND_CAP // 4 or min(shift) < MIN_SHIFT + 1:
+        # refine now if the window is small, or if a zoom (<= 4x finer bins)
+        # could not split it much (slides repeat colours: a bin can hold one value)
+        if max(est) <= REFINE_MAX or min(shift) < MIN_SHIFT + 1 or \
+                (max(shift) < MIN_SHIFT + 3 and max(est) <= 8 * REFINE_MAX):
             break
         for j in range(2):
             width = win[j][1] - win[j][0]

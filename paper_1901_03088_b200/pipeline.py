@@ -477,12 +477,9 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
     basis = r.basis.cpu().numpy()[0]
     snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
     if p99_mode == "global":
-        from .global_stats import global_p99
+        from .global_stats import global_p99, sample_bracket
 
-        try:                              # the sample p99 seeds the first histogram level
-            guess = stain_stats(h).p99
-        except SlideNormError:
-            guess = None
+        guess = sample_bracket(h)         # the sampled densities seed the first level
         p99, nonwhite, _ = _stage("density stats", global_p99, slide_chunks(slide), i0, basis,
                                   code_lam, plan.white_threshold, guess=guess)
         st = StainStats(p99=p99, sample_count=int(nonwhite))

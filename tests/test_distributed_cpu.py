@@ -183,6 +183,26 @@ def _global_worker(rank, world, port, hs, q):
         dist.destroy_process_group()
 
 
+def test_global_p99_bracket_window_logic():
+    """Window logic seeded with a bracket (hit: one histogram level + one
+    refine; miss: full-range fallback), single process."""
+    from paper_1901_03088_b200.global_stats import global_p99
+
+    rng = np.random.default_rng(9)
+    n = 200_000
+    h = np.zeros((2, n))
+    h[0] = rng.gamma(2.0, 0.4, n)
+    h[1] = rng.gamma(1.5, 0.3, n)
+    h[:, rng.random(n) < 0.2] = 0.0
+    ref = np.array([orc.pct(h[0], 99.0), orc.pct(h[1], 99.0)])
+    good = np.stack([ref * 0.97, ref * 1.02], axis=1)
+    for guess, passes in ((good, 2), (np.array([[9.0, 9.5], [9.0, 9.5]]), None), (ref, None)):
+        p99, cnt, info = global_p99(None, None, None, engine=_NumpyEngine(h), guess=guess)
+        assert cnt == n and np.array_equal(p99, ref), (guess, info)
+        if passes:
+            assert info["passes"] == passes, info
+
+
 def test_global_p99_two_ranks_gloo():
     import multiprocessing as mp
 

@@ -42,6 +42,62 @@ def test_global_p99_matches_reference(seed, i0, code_lam, layout):
     assert info["fp64_evaluations"] < 0.25 * n          # only the window is recomputed
 
 
+@pytest.mark.parametrize("thr,i0", [
+    (220, (255, 255, 255)),   # white test on the OD values
+    (0, (255, 255, 255)),     # threshold 0: byte test (OD(0) == OD(1))
+    (248, (250, 243, 230)),   # threshold >= an i0 component: byte test
+    (255, (252, 249, 246)),   # nothing is white
+])
+def test_global_p99_white_thresholds_and_tail(thr, i0):
+    """Odd pixel count (a < 16-px tail after the TMA-streamed body) and
+    every branch of the white test."""
+    import torch
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200.global_stats import global_p99
+    from paper_1901_03088_b200.pipeline import slide_chunks
+
+    px, _, _ = orc.render(701, 523, 7, i0=i0, tissue_fraction=0.5)
+    fitp = orc.fit_params(px)
+    src = pb.DeviceSource(torch.from_numpy(px).cuda())
+    if thr == 0 and px.min(axis=2).min() > 0:        # every pixel is white
+        with pytest.raises(pb.StainAbsentError):
+            global_p99(slide_chunks(src), fitp["i0"], fitp["basis"], 0.0, thr)
+        return
+    ref, n = _oracle_global(px, fitp["i0"], fitp["basis"], 0.0, thr)
+    p99, nw, info = global_p99(slide_chunks(src), fitp["i0"], fitp["basis"], 0.0, thr)
+    assert nw == n
+    assert np.array_equal(p99, ref), (p99, ref, info)
+
+
+def test_global_p99_sample_bracket_two_passes():
+    """Seeded with the bracket of the sampled densities, the search is one
+    histogram + one refine, and a wrong bracket still gives the exact answer."""
+    import torch
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200 import synthetic
+    from paper_1901_03088_b200.global_stats import global_p99, sample_bracket
+    from paper_1901_03088_b200.pipeline import slide_chunks
+
+    dev = synthetic.render_slide(2048, 1536, 5, tissue_fraction=0.6)
+    px = dev.cpu().numpy()
+    basis, i0 = orc.he_basis(), np.array([255.0, 255.0, 255.0])
+    ref, n = _oracle_global(px, i0, basis)
+    flat = px.reshape(-1, 3)
+    nw = ~np.all(flat > 220, axis=1)
+    sub = flat[nw][::97]
+    h = orc.densities(np.ascontiguousarray(orc.od_of(sub, i0).T), basis, 0.0)
+    br = sample_bracket(torch.from_numpy(np.ascontiguousarray(h)).cuda())
+    assert br.shape == (2, 2) and (br[:, 0] <= ref).all() and (ref <= br[:, 1]).all()
+    p99, nw_, info = global_p99(slide_chunks(pb.DeviceSource(dev)), i0, basis, guess=br)
+    assert nw_ == n and np.array_equal(p99, ref), (p99, ref, info)
+    assert info["passes"] == 2, info
+    wrong = np.array([[5.0, 6.0], [5.0, 6.0]])
+    p99, _, info = global_p99(slide_chunks(pb.DeviceSource(dev)), i0, basis, guess=wrong)
+    assert np.array_equal(p99, ref) and info["passes"] >= 3, info
+
+
 def test_fit_global_mode_host_and_device_slides():
     import torch
 
@@ -73,4 +129,4 @@ def test_global_p99_large_slide_window_logic():
     ref, n = _oracle_global(px, i0, basis)
     p99, nw, info = global_p99(slide_chunks(pb.DeviceSource(dev)), i0, basis)
     assert nw == n and np.array_equal(p99, ref), (p99, ref, info)
-    assert max(info["candidates"]) < 1 << 20
+    assert max(info["candidates"]) < 1 << 23

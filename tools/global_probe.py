@@ -53,3 +53,28 @@ ms = timed(lambda: eng.hist((gs._key_of(1.9), gs._key_of(1.9)), (8, 8)))
 print(f"hist zoom   {ms:.2f} ms  {npx / ms / 1e6:.1f} Mpx/s")
 ms = timed(lambda: eng.refine([1.95476, 1.94631], [1.95479, 1.94634], 1 << 20))
 print(f"refine      {ms:.2f} ms  {npx / ms / 1e6:.1f} Mpx/s")
+
+# whole fit, sample vs global mode (global seeded with the sample bracket)
+_orig = gs.global_p99
+
+
+def _traced(*a, **k):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = _orig(*a, **k)
+    torch.cuda.synchronize()
+    print(f"  global_p99 {1e3 * (time.perf_counter() - t0):.2f} ms passes {r[2]['passes']} "
+          f"levels {r[2]['levels']} guess {k.get('guess')}")
+    return r
+
+
+gs.global_p99 = _traced
+for mode in ("sample", "global"):
+    src = pb.DeviceSource(dev)
+    pb.fit(src, p99_mode=mode)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        pb.fit(src, p99_mode=mode)
+    torch.cuda.synchronize()
+    print(f"fit {mode}: {(time.perf_counter() - t0) / 3 * 1e3:.2f} ms")
