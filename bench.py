@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the CPU-baseline band")
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
                     help="gloo: functional check of the N>1 path on one GPU (not a measurement)")
+    ap.add_argument("--no-global-line", action="store_true",
+                    help="wsi: skip the extra global-p99 measurement")
     ap.add_argument("--p99-mode", choices=("sample", "global"), default="sample",
                     help="sample = reference semantics (default); global = whole-slide p99 passes")
     ap.add_argument("--workload", choices=("wsi", "batch", "tile"), default="wsi",
@@ -582,6 +584,33 @@ def run_ours(args, rank, world, local):
                          "mufu": mufu_roofline(npx_rank, x_ms, clk)},
             "gpu_launches": int(launches), "clocks": clk}
 
+    # ---- the same step with whole-slide percentiles (configs[3]: histogram
+    # all-reduce across the row bands), a few steps, same timing rules
+    if args.p99_mode == "sample" and not args.no_global_line:
+        gsteps = max(3, args.steps // 5)
+        args.p99_mode = "global"
+        try:
+            step()
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            for _ in range(gsteps):
+                step()
+            g1.record()
+            torch.cuda.synchronize()
+            gms = g0.elapsed_time(g1) / gsteps
+            if world > 1:
+                gms = _max_over_ranks(gms, dev)
+            line["global_p99_mode"] = {
+                "value": round(total / (gms * 1e-3) / 1e6, 3), "unit": "Mpx/s",
+                "ms_per_step": round(gms, 4), "steps": gsteps, "warmup": 1,
+                "note": "same step with fit(p99_mode='global'): exact p99 of every non-white "
+                        "pixel (k_stats_hist + k_stats_refine, histograms all-reduced over "
+                        + ("NCCL" if world > 1 else "one rank") + ")"}
+        finally:
+            args.p99_mode = "sample"
     # ---- end-to-end through the public API with pinned host buffers
     if not args.no_e2e:
         try:
