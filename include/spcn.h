@@ -286,6 +286,23 @@ int spcn_stats_refine(const uint8_t* src, int64_t npix, const spcn_xform_params*
                       int32_t white_threshold, const double* lo, const double* hi,
                       unsigned long long* counts, double* cand, unsigned long long* cand_count,
                       unsigned long long cap, void* stream);
+/* One-pass exact mode.  spcn_stats_table: every non-white pixel whose
+ * density is not surely below lo[j] (fp32 bound, as in the refine) for some
+ * stain j is counted in table[rgb] (2^24 u64 counters, r | g<<8 | b<<16;
+ * accumulates; caller zeroes); counts[0] += non-white pixels.  Pixels off the
+ * table have exact densities < lo[j] in both stains.  Multi-GPU: sum the
+ * tables and counts across ranks.
+ * spcn_stats_table_scan: for every colour with table[rgb] > 0, the exact
+ * fp64 densities in the reference's order (x[2i], x[2i+1]) and its count w[i]
+ * (the first `cap`, in no particular order); n_out[0] += present colours,
+ * n_out[1] += their pixels.  The p-th percentile follows from a weighted
+ * select over the entries with x >= lo (see global_stats.py).            */
+int spcn_stats_table(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
+                     int32_t white_threshold, const double* lo, unsigned long long* table,
+                     unsigned long long* counts, void* stream);
+int spcn_stats_table_scan(const spcn_xform_params* p, const unsigned long long* table,
+                          double* x, unsigned long long* w, unsigned long long cap,
+                          unsigned long long* n_out, void* stream);
 
 /* ---- measurement input: synthetic H&E slides --------------------------- */
 typedef struct spcn_synth_params {

@@ -34,7 +34,8 @@ EXPORTS = (
     "spcn_i0_from_hist", "spcn_od_tables", "spcn_snmf_batched", "spcn_code_samples",
     "spcn_percentile_segments", "spcn_select_kth", "spcn_render_synthetic",
     "spcn_batch_sizes", "spcn_batch_params", "spcn_xform_batch",
-    "spcn_stats_hist", "spcn_stats_refine", "spcn_sample_visit",
+    "spcn_stats_hist", "spcn_stats_refine", "spcn_stats_table", "spcn_stats_table_scan",
+    "spcn_sample_visit",
     "spcn_last_error", "spcn_version", "spcn_launch_count", "spcn_xform_shape",
 )
 

@@ -571,6 +571,45 @@ int spcn_stats_refine(const uint8_t* src, int64_t npix, const spcn_xform_params*
   return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_refine");
 }
 
+int spcn_stats_table(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
+                     int32_t white_threshold, const double* lo, unsigned long long* table,
+                     unsigned long long* counts, void* stream) {
+  g_err.clear();
+  if (npix < 0) return fail(SPCN_EINVAL, "npix must be >= 0");
+  if (!lo || !table || !counts) return fail(SPCN_EINVAL, "NULL argument");
+  if (npix > 0 && !src) return fail(SPCN_EINVAL, "src is NULL");
+  if (npix > 0 && (reinterpret_cast<uintptr_t>(src) & 15))
+    return fail(SPCN_EINVAL, "src must be 16-byte aligned");
+  static thread_local StatsArgs a;
+  static thread_local StrictP sp;
+  int rc = stats_setup(p, white_threshold, a, sp);
+  if (rc) return rc;
+  for (int j = 0; j < 2; ++j) {
+    a.base[j] = 0;
+    a.shift[j] = 0;
+    a.a[j] = lo[j];
+    a.b[j] = INFINITY;
+  }
+  a.nbins = 1;
+  const cudaError_t e = launch_stats_table(src, npix, a, table, counts,
+                                           static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_table");
+}
+
+int spcn_stats_table_scan(const spcn_xform_params* p, const unsigned long long* table,
+                          double* x, unsigned long long* w, unsigned long long cap,
+                          unsigned long long* n_out, void* stream) {
+  g_err.clear();
+  if (!table || !n_out || (cap > 0 && (!x || !w))) return fail(SPCN_EINVAL, "NULL argument");
+  static thread_local StatsArgs a;
+  static thread_local StrictP sp;
+  int rc = stats_setup(p, 220, a, sp);
+  if (rc) return rc;
+  const cudaError_t e = launch_table_scan(table, sp, x, w, cap, n_out,
+                                          static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_table_scan");
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------------ synthetic input

@@ -490,6 +490,122 @@ __global__ void __launch_bounds__(32 * kRefCW, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// One-pass exact mode (colour table).  A pixel's density depends only on its
+// RGB, so the pixels that are not surely below a lower bound a_j (from the
+// sample) in some stain are counted per colour in a direct-mapped table of
+// 2^24 counters (per-CTA shared-memory cache in front of the global
+// atomics).  k_table_scan then evaluates every present colour in fp64 in the
+// reference's operation order: pixels off the table are < a_j for sure, so
+// the order statistics at or above a_j are exactly those of the table
+// entries with x_j >= a_j (the host checks the ranks land there).
+constexpr int kTabSlots = 4096;
+constexpr size_t kStSmemTable = LutLayout<16>::kBytes + kTabSlots * 8 + StRing<kRefCW, kRefNSW>::kBytes;
+
+template <bool OD>
+__global__ void __launch_bounds__(32 * kRefCW, 1)
+    k_stats_table(const uint8_t* __restrict__ src, int64_t npix, const __grid_constant__ StatsArgs a,
+                  unsigned long long* __restrict__ table, unsigned long long* __restrict__ counts) {
+  constexpr int kThreads = 32 * kRefCW;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* ckey = reinterpret_cast<uint32_t*>(smem + LutLayout<16>::kBytes);
+  uint32_t* ccnt = ckey + kTabSlots;
+  uint8_t* ring = smem + LutLayout<16>::kBytes + kTabSlots * 8;
+  LutLayout<16>::fill(smem, &a.lut[0][0], threadIdx.x, kThreads);
+  for (int i = threadIdx.x; i < kTabSlots; i += kThreads) {
+    ckey[i] = kEmpty;
+    ccnt[i] = 0;
+  }
+  __syncthreads();
+  uint32_t lc[3];
+  LutLayout<16>::lane_consts(threadIdx.x & 31, lc);
+  const float2 ea0 = bc2(2.0f * a.coef[0]), ea1 = bc2(2.0f * a.coef[1]), tiny = bc2(2e-30f);
+  const float2 nlo0 = bc2(-2.0f * __double2float_rd(a.a[0])), nlo1 = bc2(-2.0f * __double2float_rd(a.a[1]));
+  int32_t nonwhite = 0;
+  st_scan<kRefCW, kRefNSW>(src, npix, ring,
+                           [&](const uint32_t* w, int nv, uint32_t inv, const uint8_t* blk) {
+    uint32_t cand = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const StPair d = st_pair<OD>(a, smem, lc, w, q);
+      uint32_t wx = d.wx | inv, wy = d.wy | inv;
+      if (nv < 16) {
+        if (2 * q >= nv) wx = ~0u;
+        if (2 * q + 1 >= nv) wy = ~0u;
+      }
+      nonwhite += 2 + (int32_t)wx + (int32_t)wy;
+      const float2 e0 = __ffma2_ru(ea0, d.T, tiny), e1 = __ffma2_ru(ea1, d.T, tiny);
+      const float2 eb0 = __fadd2_rn(__fadd2_ru(d.h0x2, e0), nlo0);
+      const float2 eb1 = __fadd2_rn(__fadd2_ru(d.h1x2, e1), nlo1);
+      const uint32_t sx = (__float_as_uint(eb0.x) & __float_as_uint(eb1.x)) | wx;
+      const uint32_t sy = (__float_as_uint(eb0.y) & __float_as_uint(eb1.y)) | wy;
+      cand |= (~sx >> 31) << (2 * q);
+      cand |= (~sy >> 31) << (2 * q + 1);
+    }
+    while (cand) {   // each lane counts one candidate colour per iteration
+      const int k = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const uint8_t* px = blk + 3 * k;
+      const uint32_t rgb = (uint32_t)px[0] | ((uint32_t)px[1] << 8) | ((uint32_t)px[2] << 16);
+      uint32_t sl = (rgb * 2654435761u) >> 20;   // 12-bit hash
+      bool done = false;
+      for (int probe = 0; probe < 8 && !done; ++probe, sl = (sl + 1) & (kTabSlots - 1)) {
+        uint32_t key = ckey[sl];
+        if (key == kEmpty) {
+          const uint32_t prev = atomicCAS(&ckey[sl], kEmpty, rgb);
+          key = prev == kEmpty ? rgb : prev;
+        }
+        if (key == rgb) {
+          atomicAdd(&ccnt[sl], 1u);
+          done = true;
+        }
+      }
+      if (!done) atomicAdd(&table[rgb], 1ull);    // cache full around this hash
+    }
+  });
+  __syncthreads();
+  for (int i = threadIdx.x; i < kTabSlots; i += kThreads)
+    if (ccnt[i]) atomicAdd(&table[ckey[i]], (unsigned long long)ccnt[i]);
+  unsigned long long nwl = (unsigned long long)nonwhite;
+  for (int off = 16; off; off >>= 1) nwl += __shfl_xor_sync(0xffffffffu, nwl, off);
+  if ((threadIdx.x & 31) == 0 && nwl) atomicAdd(&counts[0], nwl);
+}
+
+// Every present colour of the table: exact fp64 densities (reference order)
+// and its pixel count, compacted to (x[2*i], x[2*i+1], w[i]); n_out[0] = the
+// number of present colours (entries past `cap` are dropped), n_out[1] = the
+// pixels they hold.
+__global__ void __launch_bounds__(256) k_table_scan(const unsigned long long* __restrict__ table,
+                                                    const __grid_constant__ StrictP sp,
+                                                    double* __restrict__ x,
+                                                    unsigned long long* __restrict__ w,
+                                                    unsigned long long cap,
+                                                    unsigned long long* __restrict__ n_out) {
+  __shared__ double dlut[3 * 256];
+  for (int i = threadIdx.x; i < 3 * 256; i += 256) dlut[i] = sp.lut[i >> 8][i & 255];
+  __syncthreads();
+  const NnlsGram G = gram_of(sp);
+  unsigned long long pix = 0;
+  for (uint32_t c = blockIdx.x * 256u + threadIdx.x; c < (1u << 24); c += 256u * gridDim.x) {
+    const unsigned long long n = table[c];
+    if (!n) continue;
+    pix += n;
+    const double v0 = dlut[c & 255u], v1 = dlut[256 + ((c >> 8) & 255u)], v2 = dlut[512 + (c >> 16)];
+    const double b0 = strict_dot3(sp.ws[0][0], sp.ws[1][0], sp.ws[2][0], v0, v1, v2);
+    const double b1 = strict_dot3(sp.ws[0][1], sp.ws[1][1], sp.ws[2][1], v0, v1, v2);
+    double h0, h1;
+    strict_nnls(b0, b1, G, sp.lam, sp.max_sweeps, sp.tol, h0, h1);
+    const unsigned long long i = atomicAdd(&n_out[0], 1ull);
+    if (i < cap) {
+      x[2 * i] = h0;
+      x[2 * i + 1] = h1;
+      w[i] = n;
+    }
+  }
+  for (int off = 16; off; off >>= 1) pix += __shfl_xor_sync(0xffffffffu, pix, off);
+  if ((threadIdx.x & 31) == 0 && pix) atomicAdd(&n_out[1], pix);
+}
+
 static int st_grid() {
   static int sms = 0;
   if (!sms) {
@@ -545,4 +661,35 @@ cudaError_t launch_stats_refine(const uint8_t* src, int64_t npix, const StatsArg
   return launched();
 }
 
+}  // namespace spcn
+
+namespace spcn {
+cudaError_t launch_stats_table(const uint8_t* src, int64_t npix, const StatsArgs& a,
+                               unsigned long long* table, unsigned long long* counts,
+                               cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    for (auto k : {k_stats_table<true>, k_stats_table<false>}) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStSmemTable);
+      if (e != cudaSuccess) return e;
+    }
+    attr = true;
+  }
+  if (npix <= 0) return cudaSuccess;
+  const int64_t nsl = (npix + kSlicePx - 1) / kSlicePx;
+  int64_t grid = (nsl + kRefCW - 1) / kRefCW;
+  if (grid > st_grid()) grid = st_grid();
+  (a.white_by_od ? k_stats_table<true> : k_stats_table<false>)<<<(int)grid, 32 * kRefCW,
+                                                                 kStSmemTable, st>>>(
+      src, npix, a, table, counts);
+  return launched();
+}
+
+cudaError_t launch_table_scan(const unsigned long long* table, const StrictP& sp, double* x,
+                              unsigned long long* w, unsigned long long cap,
+                              unsigned long long* n_out, cudaStream_t st) {
+  k_table_scan<<<4 * st_grid(), 256, 0, st>>>(table, sp, x, w, cap, n_out);
+  return launched();
+}
 }  // namespace spcn

@@ -24,4 +24,10 @@ cudaError_t launch_stats_refine(const uint8_t* src, int64_t npix, const StatsArg
                                 const StrictP& sp, unsigned long long* counts, double* cand,
                                 unsigned long long* wcnt, unsigned long long cap,
                                 cudaStream_t st);
+cudaError_t launch_stats_table(const uint8_t* src, int64_t npix, const StatsArgs& a,
+                               unsigned long long* table, unsigned long long* counts,
+                               cudaStream_t st);
+cudaError_t launch_table_scan(const unsigned long long* table, const StrictP& sp, double* x,
+                              unsigned long long* w, unsigned long long cap,
+                              unsigned long long* n_out, cudaStream_t st);
 }  // namespace spcn

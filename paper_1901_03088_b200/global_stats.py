@@ -128,6 +128,81 @@ class DeviceEngine:
         return counts, cand, wcnt
 
 
+def _table_sig():
+    L = _sig()
+    if not getattr(L, "_spcn_table_declared", False):
+        P, I32, I64 = _lib.P, _lib.I32, _lib.I64
+        _lib.declare("spcn_stats_table", ctypes.c_int,
+                     [P, I64, ctypes.POINTER(_lib.XformParams), I32, P, P, P, P])
+        _lib.declare("spcn_stats_table_scan", ctypes.c_int,
+                     [ctypes.POINTER(_lib.XformParams), P, P, P, ctypes.c_uint64, P, P])
+        L._spcn_table_declared = True
+    return L
+
+
+TABLE_CAP = 1 << 22      # present colours handled by the one-pass mode (else: histogram path)
+
+
+def _device_table(self, lo):
+    """One pass: colour counts (2^24, int64 view of u64) of the pixels not
+    surely below lo, and the non-white count."""
+    t, L = self.t, _table_sig()
+    table = t.zeros(1 << 24, dtype=t.int64, device="cuda")
+    counts = t.zeros(1, dtype=t.int64, device="cuda")
+    a = _F64x2(*lo)
+    for x in self.chunks():
+        _lib.check(L.spcn_stats_table(_lib.ptr(x), x.numel() // 3, ctypes.byref(self.plan.params),
+                                      self.thr, ctypes.byref(a), _lib.ptr(table),
+                                      _lib.ptr(counts), _lib.stream_handle()), "stats_table")
+    return table, counts
+
+
+def _device_scan(self, table, cap=TABLE_CAP):
+    """Present colours of a (reduced) table: exact densities (m, 2) and pixel
+    counts (m,), or None when there are more than `cap` colours."""
+    t, L = self.t, _table_sig()
+    x = t.empty((cap, 2), dtype=t.float64, device="cuda")
+    w = t.empty(cap, dtype=t.int64, device="cuda")
+    n_out = t.zeros(2, dtype=t.int64, device="cuda")
+    _lib.check(L.spcn_stats_table_scan(ctypes.byref(self.plan.params), _lib.ptr(table),
+                                       _lib.ptr(x), _lib.ptr(w), cap, _lib.ptr(n_out),
+                                       _lib.stream_handle()), "stats_table_scan")
+    m = int(n_out[0].item())
+    if m > cap:
+        return None
+    return x[:m], w[:m]
+
+
+DeviceEngine.table = _device_table
+DeviceEngine.scan = _device_scan
+
+
+def _table_select(x, w, n: int, lo, ks):
+    """Order statistics `ks` (0-based ranks among the n non-white pixels) of
+    both stains from the colour table: pixels off the table are < lo[j], so
+    rank k is the (k - below_j)-th of the entries with x_j >= lo[j], below_j =
+    pixels off the table + table pixels with x_j < lo[j].  Returns (values
+    (2, len(ks)), below list) or None when a rank falls below lo."""
+    import torch as t   # tensor plumbing on the tables' device
+    vals, belows = [], []
+    total = w.sum()
+    for j in range(2):
+        keep = x[:, j] >= lo[j]
+        below = n - total + w[~keep].sum()
+        xs, order = t.sort(x[keep, j])
+        c = t.cumsum(w[keep][order], 0)
+        kk = t.tensor(ks, dtype=t.int64, device=x.device) - below
+        idx = t.searchsorted(c, kk, right=True).clamp_(max=max(int(xs.numel()) - 1, 0))
+        vals.append(xs[idx] if xs.numel() else t.zeros(len(ks), dtype=x.dtype, device=x.device))
+        belows.append(below.reshape(1))
+    packed = t.cat([vals[0], vals[1], t.cat(belows).to(x.dtype)]).cpu().numpy()
+    below = [int(packed[2 * len(ks)]), int(packed[2 * len(ks) + 1])]
+    if any(min(ks) < b for b in below) or int(total.item()) == 0:
+        return None
+    k = len(ks)
+    return np.stack([packed[:k], packed[k:2 * k]]), below
+
+
 def sample_bracket(h, p: float = 99.0):
     """[lo, hi] per stain around the p-th percentile of the sampled densities
     `h` ((2, m) device tensor, one row per stain): the sample quantiles
@@ -198,11 +273,34 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
         overflow = bool(local[5] > cap or local[6] > cap)
         return total, lists, overflow
 
+    # one-pass mode: colour table of the pixels not surely below the
+    # bracket's lower ends (needs positive lower ends and a table engine)
+    g = None if guess is None else np.asarray(guess, dtype=np.float64)
+    if g is not None and g.shape == (2, 2) and np.isfinite(g).all() and (g[:, 0] > 0).all() \
+            and hasattr(eng, "table"):
+        lo_t = [float(g[0, 0]), float(g[1, 0])]
+        tab, cnt = eng.table(lo_t)
+        info["passes"] += 1
+        tab, cnt = comm.allreduce(tab), comm.allreduce(cnt)
+        n = int(cnt.reshape(-1)[0].item())
+        if n == 0:
+            raise StainAbsentError("stain absent: no non-white pixels in the slide")
+        rank = (p / 100.0) * (n - 1)
+        klo, khi = int(math.floor(rank)), int(math.ceil(rank))
+        sc = eng.scan(tab)
+        res = None if sc is None else _table_select(sc[0], sc[1], n, lo_t, [klo, khi])
+        if res is not None:
+            vals, below = res
+            p99 = np.array([interpolate(vals[j][0], vals[j][1], rank) for j in range(2)])
+            info.update(mode="table", nonwhite=n, colours=int(sc[1].numel()), below=below,
+                        fp64_evaluations=int(sc[1].numel()), levels=0)
+            return p99, n, info
+        info["table_miss"] = True
+
     # histogram levels: start over all fp32 keys, then zoom into the bins
     # holding ranks lo..hi (one bin of margin each side) until the window is
     # small enough to list, or its bins reach the fp32 error scale
     base, shift = [0, 0], [SHIFT0, SHIFT0]
-    g = None if guess is None else np.asarray(guess, dtype=np.float64)
     if g is not None and g.shape == (2,) and all(x > 0 and math.isfinite(x) for x in g):
         g = np.stack([g / 4.0, g * 4.0], axis=1)       # +-2 octaves around a point
     if g is not None and g.shape == (2, 2) and np.isfinite(g).all() and (g >= 0).all() \

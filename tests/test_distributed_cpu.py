@@ -167,6 +167,93 @@ class _NumpyEngine:
         return torch.from_numpy(counts), torch.from_numpy(cand), torch.from_numpy(wcnt)
 
 
+class _TableEngine(_NumpyEngine):
+    """Adds the one-pass colour-table contract: `ids` maps each pixel to a
+    colour of the shared palette `pal` (2, C) of exact densities."""
+
+    def __init__(self, h, ids, pal):
+        super().__init__(h)
+        self.ids, self.pal = ids, pal
+
+    def table(self, lo):
+        import torch
+
+        cand = (self.h[0] >= lo[0]) | (self.h[1] >= lo[1])   # superset of "not surely below"
+        tab = np.bincount(self.ids[cand], minlength=self.pal.shape[1]).astype(np.int64)
+        return torch.from_numpy(tab), torch.tensor([self.h.shape[1]], dtype=torch.int64)
+
+    def scan(self, tab):
+        import torch
+
+        present = torch.nonzero(tab).reshape(-1)
+        x = torch.from_numpy(np.ascontiguousarray(self.pal.T))[present]
+        return x, tab[present]
+
+
+def _palette_slide(n, seed):
+    """Densities drawn from a palette of 3000 colours (as a slide's are)."""
+    rng = np.random.default_rng(seed)
+    pal = np.zeros((2, 3000))
+    pal[0] = rng.gamma(2.0, 0.4, 3000)
+    pal[1] = rng.gamma(1.5, 0.3, 3000)
+    pal[:, :300] = 0.0
+    ids = rng.integers(0, 3000, n)
+    return pal[:, ids], ids, pal
+
+
+def test_global_p99_table_mode():
+    from paper_1901_03088_b200.global_stats import global_p99
+
+    h, ids, pal = _palette_slide(100_000, 3)
+    ref = np.array([orc.pct(h[0], 99.0), orc.pct(h[1], 99.0)])
+    good = np.stack([ref * 0.9, ref * 1.1], axis=1)
+    p99, n, info = global_p99(None, None, None, engine=_TableEngine(h, ids, pal), guess=good)
+    assert n == h.shape[1] and np.array_equal(p99, ref), info
+    assert info["passes"] == 1 and info["mode"] == "table", info
+    high = np.stack([ref * 1.2, ref * 1.3], axis=1)              # lower end above p99: miss
+    p99, _, info = global_p99(None, None, None, engine=_TableEngine(h, ids, pal), guess=high)
+    assert np.array_equal(p99, ref) and info.get("table_miss") and info["passes"] >= 2, info
+
+
+def _table_worker(rank, world, port, parts, pal, q):
+    import torch.distributed as dist
+
+    from paper_1901_03088_b200 import distributed as dd
+    from paper_1901_03088_b200.global_stats import global_p99
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        h, ids = parts[rank]
+        ref = [0.5, 0.5]
+        p99, n, info = global_p99(None, None, None, comm=dd.TorchComm(),
+                                  engine=_TableEngine(h, ids, pal),
+                                  guess=np.array([[r * 0.5, r * 4] for r in ref]))
+        q.put((rank, p99.tolist(), n, info.get("mode")))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_global_p99_table_mode_two_ranks_gloo():
+    import multiprocessing as mp
+
+    h, ids, pal = _palette_slide(60_000, 8)
+    parts = [(h[:, :25_000], ids[:25_000]), (h[:, 25_000:], ids[25_000:])]
+    ref = [orc.pct(h[0], 99.0), orc.pct(h[1], 99.0)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_table_worker, args=(r, 2, port, parts, pal, q)) for r in range(2)]
+    for pr in ps:
+        pr.start()
+    got = [q.get(timeout=120) for _ in ps]
+    for pr in ps:
+        pr.join(timeout=60)
+    for rank, p99, n, mode in got:
+        assert n == h.shape[1] and mode == "table"
+        assert p99 == ref, (rank, p99, ref)
+
+
 def _global_worker(rank, world, port, hs, q):
     import torch.distributed as dist
 

@@ -68,11 +68,16 @@ def test_global_p99_white_thresholds_and_tail(thr, i0):
     p99, nw, info = global_p99(slide_chunks(src), fitp["i0"], fitp["basis"], 0.0, thr)
     assert nw == n
     assert np.array_equal(p99, ref), (p99, ref, info)
+    # one-pass colour-table mode (bracket around the answer)
+    br = np.stack([ref * 0.8, ref * 1.2], axis=1)
+    p99, nw, info = global_p99(slide_chunks(src), fitp["i0"], fitp["basis"], 0.0, thr, guess=br)
+    assert nw == n and info.get("mode") == "table", info
+    assert np.array_equal(p99, ref), (p99, ref, info)
 
 
 def test_global_p99_sample_bracket_two_passes():
     """Seeded with the bracket of the sampled densities, the search is one
-    histogram + one refine, and a wrong bracket still gives the exact answer."""
+    pass (colour table), and a wrong bracket still gives the exact answer."""
     import torch
 
     import paper_1901_03088_b200 as pb
@@ -92,7 +97,7 @@ def test_global_p99_sample_bracket_two_passes():
     assert br.shape == (2, 2) and (br[:, 0] <= ref).all() and (ref <= br[:, 1]).all()
     p99, nw_, info = global_p99(slide_chunks(pb.DeviceSource(dev)), i0, basis, guess=br)
     assert nw_ == n and np.array_equal(p99, ref), (p99, ref, info)
-    assert info["passes"] == 2, info
+    assert info["passes"] == 1 and info["mode"] == "table", info
     wrong = np.array([[5.0, 6.0], [5.0, 6.0]])
     p99, _, info = global_p99(slide_chunks(pb.DeviceSource(dev)), i0, basis, guess=wrong)
     assert np.array_equal(p99, ref) and info["passes"] >= 3, info
