@@ -222,6 +222,19 @@ int spcn_percentile_segments(const double* h, int64_t total, const int64_t* seg_
                              int32_t nseg, double p, void* qbuf, double* selbuf, double* out,
                              int32_t* absent, void* stream);
 
+/* The same two steps over the colour table spcn_snmf_batched left in
+ * hscratch (problem p: ucount[p] (rgb, pixel count) entries at offsets[p]):
+ * spcn_code_table codes each distinct colour once (h at the entry's index);
+ * spcn_percentile_table gives the per-problem percentile of the expanded
+ * multiset (weighted exact radix select) — identical to spcn_code_samples +
+ * spcn_percentile_segments on the samples.                                 */
+int spcn_code_table(const void* hscratch, const int64_t* offsets, int32_t nprob, int64_t max_m,
+                    const double* luts, const double* bases, double lam, int32_t max_sweeps,
+                    double* h, int64_t total, void* stream);
+int spcn_percentile_table(const double* h, int64_t total, const void* hscratch,
+                          const int64_t* seg_offsets, int32_t nseg, double p, double* out,
+                          int32_t* absent, void* stream);
+
 /* Generic exact k-th smallest (0-based) of values[begin, end) for nq queries
  * given as device arrays; out[q] (device).                                  */
 int spcn_select_kth(const double* values, const int64_t* begin, const int64_t* end,

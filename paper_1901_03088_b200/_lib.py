@@ -32,7 +32,8 @@ EXPORTS = (
     "spcn_code_densities", "spcn_normalize_block", "spcn_beer_lambert",
     "spcn_inverse_beer_lambert", "spcn_sample_count", "spcn_sample_compact",
     "spcn_i0_from_hist", "spcn_od_tables", "spcn_snmf_batched", "spcn_code_samples",
-    "spcn_percentile_segments", "spcn_select_kth", "spcn_render_synthetic",
+    "spcn_percentile_segments", "spcn_code_table", "spcn_percentile_table",
+    "spcn_select_kth", "spcn_render_synthetic",
     "spcn_batch_sizes", "spcn_batch_params", "spcn_xform_batch",
     "spcn_stats_hist", "spcn_stats_refine", "spcn_stats_table", "spcn_stats_table_scan",
     "spcn_sample_visit",

@@ -182,10 +182,17 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
     d_off = t.from_numpy(offsets).to(dev)
     flat = sample.reshape(-1)
     r = snmf.snmf_batched(flat, d_off, luts, cfg, cluster=1)
-    h = snmf.code_samples(flat, d_off, luts, r.basis, code_lam, int(collected.max(initial=0)))
-    from . import stats as dstats
+    mmax = int(collected.max(initial=0))
+    if r.table is not None and total > 0:
+        # densities and p99 over the SNMF's colour table: one fp64 coding per
+        # distinct colour, weighted exact select (same values as per sample)
+        h = snmf.code_table(r.table, d_off, luts, r.basis, code_lam, mmax, total)
+        p99, absent = snmf.percentile_table(h, r.table, d_off, total, 99.0)
+    else:
+        from . import stats as dstats
 
-    p99, absent = dstats.segment_percentiles(h, d_off, 99.0)
+        h = snmf.code_samples(flat, d_off, luts, r.basis, code_lam, mmax)
+        p99, absent = dstats.segment_percentiles(h, d_off, 99.0)
     absent_h = absent.cpu().numpy().any(axis=1)
     status[(status == 0) & absent_h] = -_lib.SPCN_ESTAIN_ABSENT
     prov = {"source": "", "config_hash": config_hash(_cfg_fields(plan, cfg, code_lam, False))}

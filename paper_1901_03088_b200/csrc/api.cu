@@ -445,6 +445,38 @@ int spcn_code_samples(const uint8_t* samples, const int64_t* offsets, int32_t np
   return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "code_samples");
 }
 
+int spcn_code_table(const void* hscratch, const int64_t* offsets, int32_t nprob, int64_t max_m,
+                    const double* luts, const double* bases, double lam, int32_t max_sweeps,
+                    double* h, int64_t total, void* stream) {
+  g_err.clear();
+  if (nprob < 0 || total < 0) return fail(SPCN_EINVAL, "negative size");
+  if (!(lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
+  if (max_sweeps < 0) return fail(SPCN_EINVAL, "max_sweeps must be >= 0");
+  if (nprob == 0 || total == 0) return SPCN_OK;
+  if (!hscratch || !offsets || !luts || !bases || !h) return fail(SPCN_EINVAL, "NULL argument");
+  const uint32_t* ukey = static_cast<const uint32_t*>(hscratch);
+  const int32_t* ucount = reinterpret_cast<const int32_t*>(ukey + 2 * total);
+  cudaError_t e = launch_code_table(ukey, ucount, offsets, nprob, max_m, luts, bases, lam,
+                                    max_sweeps, h, total, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "code_table");
+}
+
+int spcn_percentile_table(const double* h, int64_t total, const void* hscratch,
+                          const int64_t* seg_offsets, int32_t nseg, double p, double* out,
+                          int32_t* absent, void* stream) {
+  g_err.clear();
+  if (nseg < 0 || total < 0) return fail(SPCN_EINVAL, "negative size");
+  if (!(p >= 0.0 && p <= 100.0)) return fail(SPCN_EINVAL, "percentile p must be in [0, 100]");
+  if (nseg == 0) return SPCN_OK;
+  if (!h || !hscratch || !seg_offsets || !out || !absent) return fail(SPCN_EINVAL, "NULL argument");
+  const uint32_t* ukey = static_cast<const uint32_t*>(hscratch);
+  const uint32_t* ucnt = ukey + total;
+  const int32_t* ucount = reinterpret_cast<const int32_t*>(ukey + 2 * total);
+  cudaError_t e = launch_p99_weighted(h, total, ucnt, ucount, seg_offsets, nseg, p, out, absent,
+                                      static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "percentile_table");
+}
+
 int spcn_percentile_segments(const double* h, int64_t total, const int64_t* seg_offsets,
                              int32_t nseg, double p, void* qbuf, double* selbuf, double* out,
                              int32_t* absent, void* stream) {

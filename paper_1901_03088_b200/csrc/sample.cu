@@ -27,10 +27,41 @@ constexpr int kChunk = SPCN_SAMPLE_CHUNK;     // raster pixels per chunk (4096)
 constexpr int kSThreads = 256;
 constexpr int kPerThread = kChunk / kSThreads; // 16
 
-__device__ __forceinline__ const uint8_t* patch_px(const uint8_t* img, const spcn_patch& p,
-                                                   int64_t r) {
-  const int64_t row = r / p.width, col = r - row * p.width;
-  return img + 3 * (p.base + row * p.row_stride + col);
+// The kPerThread raster-consecutive pixels r0.. of a patch as packed RGB
+// (0xffffffff = past the end of the patch).  One division per thread; a run
+// inside one row at a 16-byte-aligned address is read with three 16-byte
+// loads, anything else pixel by pixel with an incremental (row, col).
+__device__ __forceinline__ void patch_run(const uint8_t* img, const spcn_patch& p, int64_t r0,
+                                          int64_t npx, uint32_t (&rgb)[kPerThread]) {
+  int64_t row = r0 / p.width, col = r0 - row * p.width;
+  const uint8_t* q = img + 3 * (p.base + row * p.row_stride + col);
+  if (r0 + kPerThread <= npx && col + kPerThread <= p.width &&
+      (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+    static_assert(kPerThread == 16, "16 px = 48 bytes = 3 vector loads");
+    const uint4* v = reinterpret_cast<const uint4*>(q);
+    const uint4 a = __ldg(v), b = __ldg(v + 1), c = __ldg(v + 2);
+    const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int j = 0; j < kPerThread; ++j) {
+      const int i = 3 * j;   // byte offset of pixel j
+      const uint64_t pair = ((uint64_t)w[(i >> 2) + ((i >> 2) < 11 ? 1 : 0)] << 32) | w[i >> 2];
+      rgb[j] = (uint32_t)(pair >> (8 * (i & 3))) & 0xffffffu;
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j) {
+    if (r0 + j < npx) {
+      const uint8_t* t = img + 3 * (p.base + row * p.row_stride + col);
+      rgb[j] = t[0] | (t[1] << 8) | (t[2] << 16);
+      if (++col == p.width) {
+        col = 0;
+        ++row;
+      }
+    } else {
+      rgb[j] = 0xffffffffu;
+    }
+  }
 }
 
 template <int N>
@@ -63,12 +94,13 @@ __global__ void __launch_bounds__(kSThreads) k_sample_count(const uint8_t* __res
   const int64_t npx = (int64_t)p.width * p.height;
   const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
   int c[4] = {0, 0, 0, 0};  // non-white, bright R, G, B
-  if ((int64_t)k * kChunk < npx) {
+  if (r0 < npx) {
+    uint32_t rgb[kPerThread];
+    patch_run(img, p, r0, npx, rgb);
+#pragma unroll
     for (int j = 0; j < kPerThread; ++j) {
-      const int64_t r = r0 + j;
-      if (r >= npx) break;
-      const uint8_t* q = patch_px(img, p, r);
-      const int a = q[0], b = q[1], d = q[2];
+      if (rgb[j] == 0xffffffffu) continue;
+      const int a = rgb[j] & 255, b = (rgb[j] >> 8) & 255, d = rgb[j] >> 16;
       c[0] += !(a > thr && b > thr && d > thr);
       c[1] += a > thr;
       c[2] += b > thr;
@@ -115,22 +147,22 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
 
   // per-thread flags for its 16 raster-consecutive pixels
   const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
-  uint32_t rgb[kPerThread];
+  uint32_t rgb[kPerThread];   // 0xffffffff: not a pixel
   int cnt[4] = {0, 0, 0, 0};
+  if (r0 < npx) {
+    patch_run(img, p, r0, npx, rgb);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kPerThread; ++j) rgb[j] = 0xffffffffu;
+  }
 #pragma unroll
   for (int j = 0; j < kPerThread; ++j) {
-    const int64_t r = r0 + j;
-    if (r < npx) {
-      const uint8_t* q = patch_px(img, p, r);
-      rgb[j] = q[0] | (q[1] << 8) | (q[2] << 16);
-      const int a = q[0], b = q[1], d = q[2];
-      cnt[0] += !(a > thr && b > thr && d > thr);
-      cnt[1] += a > thr;
-      cnt[2] += b > thr;
-      cnt[3] += d > thr;
-    } else {
-      rgb[j] = 0xffffffffu;  // sentinel: not a pixel
-    }
+    if (rgb[j] == 0xffffffffu) continue;
+    const int a = rgb[j] & 255, b = (rgb[j] >> 8) & 255, d = rgb[j] >> 16;
+    cnt[0] += !(a > thr && b > thr && d > thr);
+    cnt[1] += a > thr;
+    cnt[2] += b > thr;
+    cnt[3] += d > thr;
   }
   // block exclusive scan of the four counters
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -351,4 +351,163 @@ cudaError_t launch_p99(const double* h, int64_t total, const int64_t* seg, int n
   return launched();
 }
 
+// ---------------------------------------------------------------------------
+// Weighted per-segment percentile over colour-table entries: segment s holds
+// ucount[s] entries at seg[s] with densities h[j*total + i] and pixel counts
+// w[i] (summing to n = seg[s+1] - seg[s] samples).  The order statistics of
+// the expanded multiset are found by an MSD radix select over the fp64 bit
+// patterns (non-negative doubles order like their bits) with the counts as
+// weights — exact, the same values a sort of the n samples gives — staged in
+// shared memory when the segment fits.  Interpolation and the absent rule as
+// k_p99_combine.
+constexpr int kWThreads = 512;
+constexpr int kWCap = 12288;   // entries staged in shared memory (k_colour_table's fill limit)
+
+__device__ __forceinline__ unsigned long long wkey(double x) {
+  const unsigned long long b = __double_as_longlong(x);
+  return b == 0x8000000000000000ull ? 0ull : b;   // -0 sorts as +0
+}
+
+__global__ void __launch_bounds__(kWThreads) k_p99_weighted(
+    const double* __restrict__ h, int64_t total, const uint32_t* __restrict__ w,
+    const int32_t* __restrict__ ucount, const int64_t* __restrict__ seg, int nseg, double p,
+    double* __restrict__ p99, int32_t* __restrict__ absent) {
+  extern __shared__ __align__(16) unsigned long long s_key[];   // [kWCap]
+  uint32_t* s_w = reinterpret_cast<uint32_t*>(s_key + kWCap);    // [kWCap]
+  __shared__ uint32_t hist[256];
+  __shared__ unsigned long long s_red[kWThreads / 32];
+  __shared__ unsigned long long s_bc[2];   // chosen prefix, remaining rank
+  __shared__ uint32_t s_binw;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    const int64_t o0 = seg[sg], n = seg[sg + 1] - o0;
+    const int ne = ucount[sg];
+    for (int j = 0; j < 2; ++j) {
+      const int idx = 2 * sg + j;
+      if (n <= 0 || ne <= 0) {
+        if (tid == 0) {
+          p99[idx] = 0.0;
+          absent[idx] = 1;
+        }
+        continue;
+      }
+      const double* hv = h + (int64_t)j * total + o0;
+      const uint32_t* wv = w + o0;
+      const bool staged = ne <= kWCap;
+      if (staged)
+        for (int i = tid; i < ne; i += kWThreads) {
+          s_key[i] = wkey(hv[i]);
+          s_w[i] = wv[i];
+        }
+      __syncthreads();
+      auto key_at = [&](int i) { return staged ? s_key[i] : wkey(hv[i]); };
+      auto w_at = [&](int i) { return staged ? s_w[i] : wv[i]; };
+      // block max / min-above reduction helpers
+      auto block_max = [&](unsigned long long v) {
+        for (int off = 16; off; off >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, off));
+        if (lane == 0) s_red[warp] = v;
+        __syncthreads();
+        unsigned long long r = 0;
+        for (int k = 0; k < kWThreads / 32; ++k) r = max(r, s_red[k]);
+        __syncthreads();
+        return r;
+      };
+      auto block_min = [&](unsigned long long v) {
+        for (int off = 16; off; off >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, off));
+        if (lane == 0) s_red[warp] = v;
+        __syncthreads();
+        unsigned long long r = ~0ull;
+        for (int k = 0; k < kWThreads / 32; ++k) r = min(r, s_red[k]);
+        __syncthreads();
+        return r;
+      };
+      // weighted MSD radix select of rank k: returns the key; s_binw = the
+      // weight of entries equal to it, s_bc[1] = k's rank among them
+      auto select = [&](int64_t k) {
+        unsigned long long prefix = 0;
+        for (int shift = 56; shift >= 0; shift -= 8) {
+          if (tid < 256) hist[tid] = 0;
+          __syncthreads();
+          const unsigned long long mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+          for (int i = tid; i < ne; i += kWThreads) {
+            const unsigned long long kk = key_at(i);
+            if ((kk & mask) == prefix) atomicAdd(&hist[(kk >> shift) & 255u], w_at(i));
+          }
+          __syncthreads();
+          if (warp == 0) {   // warp scan of 256 bins (8 per lane)
+            uint32_t loc[8], sum = 0;
+            for (int b = 0; b < 8; ++b) {
+              loc[b] = hist[lane * 8 + b];
+              sum += loc[b];
+            }
+            uint32_t incl = sum;
+            for (int off = 1; off < 32; off <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+              if (lane >= off) incl += y;
+            }
+            uint32_t before = incl - sum;
+            for (int b = 0; b < 8; ++b) {
+              if (k >= (int64_t)before && k < (int64_t)(before + loc[b])) {
+                s_bc[0] = prefix | ((unsigned long long)(lane * 8 + b) << shift);
+                s_bc[1] = (unsigned long long)(k - before);
+                s_binw = loc[b];
+              }
+              before += loc[b];
+            }
+          }
+          __syncthreads();
+          prefix = s_bc[0];
+          k = (int64_t)s_bc[1];
+          __syncthreads();
+        }
+        return prefix;
+      };
+      const double rank = __dmul_rn(p / 100.0, (double)(n - 1));
+      const int64_t klo = (int64_t)floor(rank), khi = (int64_t)ceil(rank);
+      unsigned long long mx = 0;
+      for (int i = tid; i < ne; i += kWThreads) mx = max(mx, key_at(i));
+      mx = block_max(mx);
+      const unsigned long long klo_key = select(klo);
+      const unsigned long long rem = s_bc[1];
+      const uint32_t binw = s_binw;
+      unsigned long long khi_key = klo_key;
+      if (khi != klo && rem + 1 >= binw) {   // the next distinct value
+        unsigned long long nx = ~0ull;
+        for (int i = tid; i < ne; i += kWThreads) {
+          const unsigned long long kk = key_at(i);
+          if (kk > klo_key) nx = min(nx, kk);
+        }
+        khi_key = block_min(nx);
+      }
+      if (tid == 0) {
+        const double a = __longlong_as_double(klo_key), b = __longlong_as_double(khi_key);
+        const double frac = __dsub_rn(rank, floor(rank));
+        p99[idx] = __dadd_rn(a, __dmul_rn(__dsub_rn(b, a), frac));
+        absent[idx] = mx == 0ull ? 1 : 0;   // s.max(initial=0) <= 0 (src/normalize.py:91)
+      }
+      __syncthreads();
+    }
+  }
+}
+
+cudaError_t launch_p99_weighted(const double* h, int64_t total, const uint32_t* w,
+                                const int32_t* ucount, const int64_t* seg, int nseg, double p,
+                                double* p99, int32_t* absent, cudaStream_t st) {
+  if (nseg <= 0) return cudaSuccess;
+  constexpr int smem = kWCap * (8 + 4);
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_p99_weighted, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int g = nseg < 2 * sms ? nseg : 2 * sms;
+  k_p99_weighted<<<g, kWThreads, smem, st>>>(h, total, w, ucount, seg, nseg, p, p99, absent);
+  return launched();
+}
+
 }  // namespace spcn

@@ -316,6 +316,54 @@ __global__ void __launch_bounds__(256) k_code_samples(
   }
 }
 
+// The same coding over the colour table of the samples (k_colour_table's
+// entries: problem p's first ucount[p] entries at off[p] are (rgb, count)):
+// one fp64 evaluation per distinct colour, written at the entry's position.
+__global__ void __launch_bounds__(256) k_code_table(
+    const uint32_t* __restrict__ ukey, const int32_t* __restrict__ ucount,
+    const int64_t* __restrict__ offsets, int nprob, const double* __restrict__ luts,
+    const double* __restrict__ bases, double lam, int max_sweeps, double* __restrict__ h,
+    int64_t total) {
+  const int p = blockIdx.y;
+  const int64_t o0 = offsets[p], o1 = o0 + ucount[p];
+  __shared__ double lut[768];
+  __shared__ double w[6], g[4];
+  for (int i = threadIdx.x; i < 768; i += 256) lut[i] = luts[(int64_t)p * 768 + i];
+  if (threadIdx.x < 6) w[threadIdx.x] = bases[(int64_t)p * 6 + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    g[0] = __dadd_rn(__dadd_rn(__dmul_rn(w[0], w[0]), __dmul_rn(w[2], w[2])), __dmul_rn(w[4], w[4]));
+    g[2] = __dadd_rn(__dadd_rn(__dmul_rn(w[1], w[1]), __dmul_rn(w[3], w[3])), __dmul_rn(w[5], w[5]));
+    g[1] = __dadd_rn(__dadd_rn(__dmul_rn(w[0], w[1]), __dmul_rn(w[2], w[3])), __dmul_rn(w[4], w[5]));
+    g[3] = __dsub_rn(__dmul_rn(g[0], g[2]), __dmul_rn(g[1], g[1]));
+  }
+  __syncthreads();
+  const NnlsGram G = make_nnls_gram(g[0], g[1], g[2], g[3]);
+  for (int64_t i = o0 + blockIdx.x * 256ll + threadIdx.x; i < o1; i += 256ll * gridDim.x) {
+    const uint32_t rgb = ukey[i];
+    const double v0 = lut[rgb & 255u], v1 = lut[256 + ((rgb >> 8) & 255u)], v2 = lut[512 + (rgb >> 16)];
+    const double b0 = strict_dot3(w[0], w[2], w[4], v0, v1, v2);
+    const double b1 = strict_dot3(w[1], w[3], w[5], v0, v1, v2);
+    double h0, h1;
+    strict_nnls(b0, b1, G, lam, max_sweeps, 0.0, h0, h1);
+    h[i] = h0;
+    h[total + i] = h1;
+  }
+}
+
+cudaError_t launch_code_table(const uint32_t* ukey, const int32_t* ucount, const int64_t* offsets,
+                              int nprob, int64_t max_m, const double* luts, const double* bases,
+                              double lam, int max_sweeps, double* h, int64_t total,
+                              cudaStream_t st) {
+  if (nprob <= 0) return cudaSuccess;
+  int64_t gx = (max_m + 255) / 256;
+  if (gx > 16) gx = 16;
+  if (gx < 1) gx = 1;
+  k_code_table<<<dim3((unsigned)gx, nprob), 256, 0, st>>>(ukey, ucount, offsets, nprob, luts,
+                                                          bases, lam, max_sweeps, h, total);
+  return launched();
+}
+
 // ---------------------------------------------------------------------------
 // k_colour_table: the fit samples are 8-bit RGB and repeat heavily (a 100 k
 // sample of an H&E patch holds ~10 k distinct colours), while every SNMF

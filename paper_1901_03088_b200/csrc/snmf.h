@@ -19,4 +19,8 @@ cudaError_t launch_code_samples(const uint8_t* samples, const int64_t* offsets, 
                                 int64_t max_m, const double* luts, const double* bases,
                                 double lam, int max_sweeps, double* h, int64_t total,
                                 cudaStream_t st);
+cudaError_t launch_code_table(const uint32_t* ukey, const int32_t* ucount, const int64_t* offsets,
+                              int nprob, int64_t max_m, const double* luts, const double* bases,
+                              double lam, int max_sweeps, double* h, int64_t total,
+                              cudaStream_t st);
 }  // namespace spcn

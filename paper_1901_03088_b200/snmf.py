@@ -29,6 +29,10 @@ def _sig():
                      [P, P, P, I32, P, ctypes.POINTER(SnmfCfgC), P, I64, P, P, P, P])
         _lib.declare("spcn_code_samples", ctypes.c_int,
                      [P, P, I32, I64, P, P, DBL, I32, P, I64, P])
+        _lib.declare("spcn_code_table", ctypes.c_int,
+                     [P, P, I32, I64, P, P, DBL, I32, P, I64, P])
+        _lib.declare("spcn_percentile_table", ctypes.c_int,
+                     [P, I64, P, P, I32, DBL, P, P, P])
         L._spcn_snmf_declared = True
     return L
 
@@ -56,10 +60,11 @@ def make_cfg(cfg, cluster: int) -> SnmfCfgC:
 class BatchFit:
     """Device results of ``snmf_batched`` (bases already ordered, on the host)."""
 
-    def __init__(self, basis, history, info):
+    def __init__(self, basis, history, info, table=None):
         self.basis = basis          # (P, 3, 2)
         self.history = history      # (P, max_outer+1), valid prefix = info[:, 3]
         self.info = info            # (P, 4): iterations, converged, flags, history length
+        self.table = table          # colour-table scratch (batches) or None
 
 
 def snmf_batched(samples, offsets, luts, cfg, cluster: int = 1, od=None) -> BatchFit:
@@ -83,7 +88,8 @@ def snmf_batched(samples, offsets, luts, cfg, cluster: int = 1, od=None) -> Batc
         _lib.ptr(luts) if luts is not None else None, ctypes.byref(c),
         _lib.ptr(scratch) if scratch is not None else None, total,
         _lib.ptr(basis), _lib.ptr(hist), _lib.ptr(info), _lib.stream_handle()), "snmf_batched")
-    return BatchFit(basis.reshape(nprob, 3, 2), hist, info)
+    return BatchFit(basis.reshape(nprob, 3, 2), hist, info,
+                    table=scratch if cluster == 1 else None)
 
 
 def code_samples(samples, offsets, luts, bases, lam, max_m, max_sweeps=2000):
@@ -98,6 +104,35 @@ def code_samples(samples, offsets, luts, bases, lam, max_m, max_sweeps=2000):
                                    _lib.ptr(luts), _lib.ptr(b), float(lam), int(max_sweeps),
                                    _lib.ptr(h), total, _lib.stream_handle()), "code_samples")
     return h
+
+
+def code_table(table, offsets, luts, bases, lam, max_m, total, max_sweeps=2000):
+    """code_samples over the colour table of ``snmf_batched`` (one fp64
+    evaluation per distinct colour) → CUDA (2, total) float64, valid at the
+    entry positions."""
+    t = _dev.torch()
+    L = _sig()
+    nprob = offsets.numel() - 1
+    h = t.empty((2, max(total, 1)), dtype=t.float64, device=offsets.device)
+    b = bases.reshape(nprob, 6).to(t.float64).contiguous()
+    _lib.check(L.spcn_code_table(_lib.ptr(table), _lib.ptr(offsets), nprob, int(max_m),
+                                 _lib.ptr(luts), _lib.ptr(b), float(lam), int(max_sweeps),
+                                 _lib.ptr(h), total, _lib.stream_handle()), "code_table")
+    return h
+
+
+def percentile_table(h, table, offsets, total, p=99.0):
+    """Per-problem percentile of the colour-table densities (weighted) →
+    (values (P, 2), absent (P, 2) int32) CUDA tensors."""
+    t = _dev.torch()
+    L = _sig()
+    nprob = offsets.numel() - 1
+    out = t.empty((nprob, 2), dtype=t.float64, device=offsets.device)
+    absent = t.empty((nprob, 2), dtype=t.int32, device=offsets.device)
+    _lib.check(L.spcn_percentile_table(_lib.ptr(h), total, _lib.ptr(table), _lib.ptr(offsets),
+                                       nprob, float(p), _lib.ptr(out), _lib.ptr(absent),
+                                       _lib.stream_handle()), "percentile_table")
+    return out, absent
 
 
 def warn_flags(m: int, flags: int, max_outer: int, stacklevel: int = 3) -> None:

@@ -167,3 +167,40 @@ def test_normalize_batch_host_matches_device_batch():
         out, errs = pb.normalize_batch_host(host, tgt, chunk=4, streams=3)
     assert np.array_equal(out.numpy(), dev_out)
     assert [type(e) for e in errs] == [type(e) for e in dev_err]
+
+
+def test_table_percentiles_equal_per_sample_percentiles():
+    """Coding each distinct colour once and selecting with weights gives the
+    same densities and p99 as coding every sample (exact)."""
+    import torch
+
+    pb = _pb()
+    from paper_1901_03088_b200 import batch, snmf, stats as dstats
+
+    imgs = _items(96, 128, 7, seed=21)
+    imgs[2] = np.full((96, 128, 3), 255, np.uint8)             # blank item (no samples)
+    x = torch.from_numpy(np.stack(imgs)).cuda()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        fits = pb.fit_batch(x, pb.SamplePlan())
+    # rebuild the sample arrays the way fit_batch does and compare both paths
+    n = len(imgs)
+    flat = []
+    offs = [0]
+    for i in range(n):
+        px = imgs[i].reshape(-1, 3)
+        nw = px[~np.all(px > 220, axis=1)][:100_000]
+        flat.append(nw)
+        offs.append(offs[-1] + len(nw))
+    samples = torch.from_numpy(np.concatenate(flat).reshape(-1)).cuda()
+    d_off = torch.tensor(offs, dtype=torch.int64, device="cuda")
+    total = offs[-1]
+    r = snmf.snmf_batched(samples, d_off, fits.luts, pb.SnmfConfig(), cluster=1)
+    assert r.table is not None
+    h_s = snmf.code_samples(samples, d_off, fits.luts, r.basis, 0.0, max(np.diff(offs)))
+    p_s, a_s = dstats.segment_percentiles(h_s, d_off, 99.0)
+    h_t = snmf.code_table(r.table, d_off, fits.luts, r.basis, 0.0, max(np.diff(offs)), total)
+    p_t, a_t = snmf.percentile_table(h_t, r.table, d_off, total, 99.0)
+    assert np.array_equal(p_s.cpu().numpy(), p_t.cpu().numpy())
+    assert np.array_equal(a_s.cpu().numpy(), a_t.cpu().numpy())
+    assert np.array_equal(fits.p99.cpu().numpy(), p_t.cpu().numpy())
