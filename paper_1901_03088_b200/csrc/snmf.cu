@@ -376,7 +376,9 @@ constexpr int kTabBits = 14;
 constexpr int kTabSlots = 1 << kTabBits;
 constexpr uint32_t kTabEmpty = 0xffffffffu;
 
-__global__ void __launch_bounds__(512) k_colour_table(const uint8_t* __restrict__ samples,
+constexpr int kCT = 1024;   // threads of k_colour_table
+
+__global__ void __launch_bounds__(kCT) k_colour_table(const uint8_t* __restrict__ samples,
                                                       const int64_t* __restrict__ offsets,
                                                       int nprob, uint32_t* __restrict__ ukey,
                                                       uint32_t* __restrict__ ucnt,
@@ -385,37 +387,70 @@ __global__ void __launch_bounds__(512) k_colour_table(const uint8_t* __restrict_
   uint32_t* key = tab;
   uint32_t* cnt = tab + kTabSlots;
   __shared__ int s_full, s_used;   // table too full (or a probe failed) -> list the samples
-  __shared__ uint32_t s_scan[512];
-  const int tid = threadIdx.x;
+  __shared__ uint32_t s_scan[kCT];
+  const int tid = threadIdx.x, lane = tid & 31;
+  constexpr uint32_t kNone = 0xffffffffu;   // not a sample
+  // one colour per lane (kNone: none): lanes holding the same colour insert once
+  auto insert = [&](uint32_t rgb) {
+    const unsigned peers = __match_any_sync(0xffffffffu, rgb);
+    if (rgb == kNone || lane != __ffs(peers) - 1) return;
+    const uint32_t add = __popc(peers);
+    uint32_t slot = (rgb * 2654435761u) >> (32 - kTabBits);
+    for (int probe = 0; probe < 64; ++probe, slot = (slot + 1) & (kTabSlots - 1)) {
+      uint32_t k = key[slot];
+      if (k == kTabEmpty) {
+        k = atomicCAS(&key[slot], kTabEmpty, rgb);
+        if (k == kTabEmpty && atomicAdd(&s_used, 1) >= (3 * kTabSlots) / 4) s_full = 1;
+      }
+      if (k == kTabEmpty || k == rgb) {
+        atomicAdd(&cnt[slot], add);
+        return;
+      }
+    }
+    s_full = 1;
+  };
   for (int p = blockIdx.x; p < nprob; p += gridDim.x) {
     const int64_t o0 = offsets[p], m = offsets[p + 1] - o0;
-    for (int i = tid; i < kTabSlots; i += 512) {
+    for (int i = tid; i < kTabSlots; i += kCT) {
       key[i] = kTabEmpty;
       cnt[i] = 0;
     }
     if (tid == 0) s_full = s_used = 0;
     __syncthreads();
-    for (int64_t i = tid; i < m; i += 512) {
-      const uint8_t* px = samples + 3 * (o0 + i);
-      const uint32_t rgb = px[0] | (px[1] << 8) | (px[2] << 16);
-      // lanes holding the same colour insert once
-      const unsigned peers = __match_any_sync(__activemask(), rgb);
-      if ((int)(tid & 31) != __ffs(peers) - 1) continue;
-      const uint32_t add = __popc(peers);
-      uint32_t slot = (rgb * 2654435761u) >> (32 - kTabBits);
-      bool done = false;
-      for (int probe = 0; probe < 64 && !done; ++probe, slot = (slot + 1) & (kTabSlots - 1)) {
-        uint32_t k = key[slot];
-        if (k == kTabEmpty) {
-          k = atomicCAS(&key[slot], kTabEmpty, rgb);
-          if (k == kTabEmpty && atomicAdd(&s_used, 1) >= (3 * kTabSlots) / 4) s_full = 1;
+    // samples [a, a + 16 nb) in 16-sample groups at 16-byte-aligned addresses
+    // (three vector loads each); the few before and after one by one
+    const int64_t a0 = (16 - (o0 & 15)) & 15, a = m < a0 ? m : a0;
+    const int64_t nb = (m - a) / 16, rest0 = a + 16 * nb;
+    const int64_t rounds = (nb + kCT - 1) / kCT;
+    for (int64_t r = 0; r < rounds; ++r) {
+      const int64_t g = r * kCT + tid;
+      uint32_t rgb[16];
+      if (g < nb) {
+        const uint4* v = reinterpret_cast<const uint4*>(samples + 3 * (o0 + a + 16 * g));
+        const uint4 q0 = __ldg(v), q1 = __ldg(v + 1), q2 = __ldg(v + 2);
+        const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int i = 3 * j;
+          const uint64_t pr = ((uint64_t)w[(i >> 2) + ((i >> 2) < 11 ? 1 : 0)] << 32) | w[i >> 2];
+          rgb[j] = (uint32_t)(pr >> (8 * (i & 3))) & 0xffffffu;
         }
-        if (k == kTabEmpty || k == rgb) {
-          atomicAdd(&cnt[slot], add);
-          done = true;
-        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) rgb[j] = kNone;
       }
-      if (!done) s_full = 1;
+#pragma unroll 1
+      for (int j = 0; j < 16; ++j) insert(rgb[j]);
+    }
+    // head [0, a) and tail [rest0, m): < 32 samples, one warp
+    if (tid < 32) {
+      const int64_t i = tid < a ? tid : rest0 + (tid - a);
+      uint32_t rgb = kNone;
+      if ((tid < a) || (tid >= a && i < m)) {
+        const uint8_t* px = samples + 3 * (o0 + i);
+        rgb = px[0] | (px[1] << 8) | (px[2] << 16);
+      }
+      insert(rgb);
     }
     __syncthreads();
     if (!s_full) {
@@ -424,7 +459,7 @@ __global__ void __launch_bounds__(512) k_colour_table(const uint8_t* __restrict_
       // insertion order — only the order inside a cluster does.  Sorting each
       // cluster by colour makes the entry order, and every later
       // floating-point summation order, deterministic.
-      for (int s0 = tid; s0 < kTabSlots; s0 += 512) {
+      for (int s0 = tid; s0 < kTabSlots; s0 += kCT) {
         if (key[s0] == kTabEmpty || key[(s0 - 1) & (kTabSlots - 1)] != kTabEmpty) continue;
         int len = 1;                                     // this thread owns the cluster at s0
         while (len < kTabSlots && key[(s0 + len) & (kTabSlots - 1)] != kTabEmpty) ++len;
@@ -445,12 +480,12 @@ __global__ void __launch_bounds__(512) k_colour_table(const uint8_t* __restrict_
       }
       __syncthreads();
       // compact in slot order (block scan)
-      constexpr int kPer = kTabSlots / 512;
+      constexpr int kPer = kTabSlots / kCT;
       uint32_t occ = 0;
       for (int j = 0; j < kPer; ++j) occ += key[tid * kPer + j] != kTabEmpty;
       s_scan[tid] = occ;
       __syncthreads();
-      for (int off = 1; off < 512; off <<= 1) {
+      for (int off = 1; off < kCT; off <<= 1) {
         const uint32_t y = tid >= off ? s_scan[tid - off] : 0u;
         __syncthreads();
         s_scan[tid] += y;
@@ -465,9 +500,9 @@ __global__ void __launch_bounds__(512) k_colour_table(const uint8_t* __restrict_
           ++pos;
         }
       }
-      if (tid == 511) ucount[p] = (int32_t)s_scan[511];
+      if (tid == kCT - 1) ucount[p] = (int32_t)s_scan[kCT - 1];
     } else {
-      for (int64_t i = tid; i < m; i += 512) {
+      for (int64_t i = tid; i < m; i += kCT) {
         const uint8_t* px = samples + 3 * (o0 + i);
         ukey[o0 + i] = px[0] | (px[1] << 8) | (px[2] << 16);
         ucnt[o0 + i] = 1u;
@@ -517,7 +552,7 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
     ucnt = ukey + total;
     ucount = reinterpret_cast<int32_t*>(ucnt + total);
     int g = nprob < 4 * sms ? nprob : 4 * sms;
-    k_colour_table<<<g, 512, kTabSmem, st>>>(samples, offsets, nprob, ukey, ucnt, ucount);
+    k_colour_table<<<g, kCT, kTabSmem, st>>>(samples, offsets, nprob, ukey, ucnt, ucount);
     const cudaError_t e1 = launched();
     if (e1 != cudaSuccess) return e1;
   }
