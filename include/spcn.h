@@ -200,7 +200,8 @@ typedef struct spcn_snmf_cfg {
  * flags bit0=no-convergence bit1=one-stain, history length).  hscratch
  * (optional, >= total + nprob/2 + 1 fp64 words) holds a per-problem table of
  * distinct sample colours with pixel counts, so each SNMF pass visits every
- * colour once with its weight; NULL = one visit per sample.  Device pointers. */
+ * colour once with its weight, and the work-queue ticket; NULL = one visit
+ * per sample.  Device pointers.                                            */
 int spcn_snmf_batched(const uint8_t* samples, const double* od, const int64_t* offsets,
                       int32_t nprob,
                       const double* luts, const spcn_snmf_cfg* cfg, double* hscratch,

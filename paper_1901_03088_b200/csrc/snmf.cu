@@ -556,9 +556,19 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
     const cudaError_t e1 = launched();
     if (e1 != cudaSuccess) return e1;
   }
+  // work ticket of the dynamic problem queue: in the caller's scratch right
+  // after the table (no stream-ordered allocation per call: a pool that
+  // returns memory to the driver makes every call re-map it)
   int* ticket = nullptr;
+  bool own_ticket = false;
   if (single && nprob > 1) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ticket), sizeof(int), st);
+    cudaError_t e = cudaSuccess;
+    if (hbuf) {
+      ticket = reinterpret_cast<int*>(reinterpret_cast<uint32_t*>(hbuf) + 2 * total + nprob);
+    } else {
+      e = cudaMallocAsync(reinterpret_cast<void**>(&ticket), sizeof(int), st);
+      own_ticket = true;
+    }
     if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
   }
@@ -582,7 +592,7 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
   const int32_t* cu = ucount;
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_snmf<512, 1>, samples, od, offsets, nprob, luts, a,
                                      ticket, total, basis_out, hist_out, info_out, ck, cc, cu);
-  if (ticket) {
+  if (own_ticket) {
     const cudaError_t e2 = cudaFreeAsync(ticket, st);
     if (e == cudaSuccess) e = e2;
   }
