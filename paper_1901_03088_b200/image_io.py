@@ -166,7 +166,8 @@ class ArrayWriter(StripWriter):
 
     def __init__(self, width, height, out=None):
         super().__init__(width, height)
-        self.pixels = out if out is not None else np.zeros((height, width, 3), np.uint8)
+        # every row is written before close() succeeds: no need to zero-fill
+        self.pixels = out if out is not None else np.empty((height, width, 3), np.uint8)
         if self.pixels.shape != (height, width, 3) or self.pixels.dtype != np.uint8:
             raise ValueError("ArrayWriter storage must be (height, width, 3) uint8")
 

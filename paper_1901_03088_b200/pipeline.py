@@ -14,6 +14,7 @@ import time
 import warnings
 from collections import deque
 from dataclasses import dataclass
+import threading
 from threading import Lock
 
 import numpy as np
@@ -155,15 +156,21 @@ class _PatchImage:
         """(device image, descriptors) of candidates [lo, hi)."""
         if self.device:
             return self.img, self.desc[lo:hi]
-        t = _dev.torch()
-        parts, desc, base = [], [], 0
+        desc, base = [], 0
         for (x, y, w, h) in self.rects[lo:hi]:
-            px = self.slide.read_region(x, y, w, h).pixels
-            parts.append(np.ascontiguousarray(px).reshape(-1))
             desc.append((base, w, h, w))
             base += w * h
-        host = np.concatenate(parts) if parts else np.zeros(3, np.uint8)
-        return t.from_numpy(host).to("cuda"), np.array(desc, dtype=PATCH_DT)
+        arr = self.slide.array if isinstance(self.slide, ArraySource) else None
+
+        def fill(stage):   # each region straight into the pinned buffer (one copy)
+            off = 0
+            for (x, y, w, h) in self.rects[lo:hi]:
+                dst = stage[3 * off:3 * (off + w * h)].reshape(h, w, 3)
+                _pcopy(dst, arr[y:y + h, x:x + w] if arr is not None else
+                       self.slide.read_region(x, y, w, h).pixels)
+                off += w * h
+
+        return _STAGING.to_device_fill(max(3 * base, 3), fill), np.array(desc, dtype=PATCH_DT)
 
 
 def _count(L, img, desc, thr):
@@ -315,10 +322,11 @@ def _sample_device(slide, plan: SamplePlan):
     order, ncand, rects = _candidates(slide.width, slide.height, plan)
     pimg = _PatchImage(slide, rects)
     thr = int(plan.white_threshold)
-    # counts in growing batches (most slides stop after one or two patches)
+    # counts in growing batches (most slides stop after one or two patches; a
+    # host slide uploads only the batches it counts, so it starts with one)
     tot = np.zeros((0, 4), dtype=np.int64)
     dev_counts = []
-    batch = min(ncand, max(2, min(plan.max_patches, 8)))
+    batch = min(ncand, max(2, min(plan.max_patches, 8))) if pimg.device else 1
 
     def counts_of(k):
         nonlocal tot, batch
@@ -502,6 +510,94 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
 
 
 # ----------------------------------------------------------------------------- transform
+class _Staging(threading.local):
+    """Per-thread reusable stream + device/pinned buffers of the streamed
+    transform's slots (and the host fit's upload buffer): allocating pinned
+    memory and streams on every call costs more than a 2048^2 tile's work."""
+
+    def __init__(self):
+        self.slots = []       # dicts: stream, dsrc, ddst, hin, hout (flat uint8, grow-only)
+        self.upload = None    # pinned flat uint8
+        self.upload_ev = None
+
+    @staticmethod
+    def _grow(buf, nbytes, pinned):
+        t = _dev.torch()
+        if buf is not None and buf.numel() >= nbytes:
+            return buf
+        if pinned:
+            return t.empty(nbytes, dtype=t.uint8, pin_memory=True)
+        return t.empty(nbytes, dtype=t.uint8, device="cuda")
+
+    def slot(self, k, nbytes, want_hin, want_hout):
+        t = _dev.torch()
+        while len(self.slots) <= k:
+            self.slots.append(dict(stream=t.cuda.Stream(), dsrc=None, ddst=None, hin=None,
+                                   hout=None))
+        sl = self.slots[k]
+        if sl["stream"].device != t.device("cuda", t.cuda.current_device()):
+            sl.update(stream=t.cuda.Stream(), dsrc=None, ddst=None)
+        sl["dsrc"] = self._grow(sl["dsrc"], nbytes, False)
+        sl["ddst"] = self._grow(sl["ddst"], nbytes, False)
+        if want_hin:
+            sl["hin"] = self._grow(sl["hin"], nbytes, True)
+        if want_hout:
+            sl["hout"] = self._grow(sl["hout"], nbytes, True)
+        return sl
+
+    def to_device_fill(self, nbytes: int, fill):
+        """Upload nbytes written by fill(pinned flat numpy view)."""
+        t = _dev.torch()
+        if self.upload_ev is not None:
+            self.upload_ev.synchronize()      # the previous upload has left the buffer
+        self.upload = self._grow(self.upload, nbytes, True)
+        stage = self.upload[:nbytes]
+        fill(stage.numpy())
+        out = stage.to("cuda", non_blocking=True)
+        self.upload_ev = t.cuda.Event()
+        self.upload_ev.record()
+        return out
+
+    def to_device(self, host: np.ndarray):
+        """Upload a contiguous uint8 array through the reusable pinned buffer."""
+        t = _dev.torch()
+        flat = host.reshape(-1)
+        if self.upload_ev is not None:
+            self.upload_ev.synchronize()      # the previous upload has left the buffer
+        self.upload = self._grow(self.upload, flat.size, True)
+        stage = self.upload[:flat.size]
+        stage.numpy()[...] = flat
+        out = stage.to("cuda", non_blocking=True)
+        self.upload_ev = t.cuda.Event()
+        self.upload_ev.record()
+        return out
+
+
+_STAGING = _Staging()
+_COPY_POOL = None
+
+
+def _pcopy(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[...] = src, split across 4 threads for multi-MB blocks (numpy
+    releases the GIL while copying; one core's memcpy is the bottleneck of a
+    host-resident tile's staging)."""
+    global _COPY_POOL
+    if dst.nbytes < (4 << 20) or dst.shape[0] < 8:
+        dst[...] = src
+        return
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _COPY_POOL = ThreadPoolExecutor(max_workers=4)
+    n = dst.shape[0]
+    cuts = [n * i // 4 for i in range(5)]
+
+    def part(i):
+        dst[cuts[i]:cuts[i + 1]] = src[cuts[i]:cuts[i + 1]]
+
+    list(_COPY_POOL.map(part, range(4)))
+
+
 def _pinned(a: np.ndarray) -> bool:
     t = _dev.torch()
     try:
@@ -579,15 +675,13 @@ def _transform_streamed(slide, sink, plan, strips, width, nslots, gauge, progres
     direct_in = src_arr is not None and _pinned(src_arr)
     direct_out = isinstance(sink, ArrayWriter) and _pinned(sink.pixels)
     slots = []
-    for _ in range(nslots):
-        slots.append(dict(
-            stream=t.cuda.Stream(),
-            dsrc=t.empty((max_h, width, 3), dtype=t.uint8, device="cuda"),
-            ddst=t.empty((max_h, width, 3), dtype=t.uint8, device="cuda"),
-            hin=None if direct_in else t.empty((max_h, width, 3), dtype=t.uint8, pin_memory=True),
-            hout=None if direct_out else t.empty((max_h, width, 3), dtype=t.uint8,
-                                                 pin_memory=True),
-            ev=None, job=None))
+    nbytes = max_h * width * 3
+    for k in range(nslots):
+        st = _STAGING.slot(k, nbytes, not direct_in, not direct_out)
+        view = lambda b: None if b is None else b[:nbytes].view(max_h, width, 3)  # noqa: E731
+        slots.append(dict(stream=st["stream"], dsrc=view(st["dsrc"]), ddst=view(st["ddst"]),
+                          hin=None if direct_in else view(st["hin"]),
+                          hout=None if direct_out else view(st["hout"]), ev=None, job=None))
     pending = deque()
 
     def commit():
@@ -597,7 +691,11 @@ def _transform_streamed(slide, sink, plan, strips, width, nslots, gauge, progres
         if direct_out:
             sink.mark_written(y, h)
         else:
-            sink.write_strip(PixelBlock(0, y, slot["hout"][:h].numpy()))
+            if isinstance(sink, ArrayWriter):
+                _pcopy(sink.rows(y, h), slot["hout"][:h].numpy())
+                sink.mark_written(y, h)
+            else:
+                sink.write_strip(PixelBlock(0, y, slot["hout"][:h].numpy()))
         gauge.release(h * width)
         if progress is not None:
             progress(y + h, slide.height)
@@ -612,8 +710,9 @@ def _transform_streamed(slide, sink, plan, strips, width, nslots, gauge, progres
             if direct_in:
                 hsrc = t.from_numpy(src_arr[y:y + h])
             else:
-                block = slide.read_region(0, y, width, h).pixels
-                slot["hin"][:h].numpy()[...] = block
+                block = src_arr[y:y + h] if src_arr is not None else \
+                    slide.read_region(0, y, width, h).pixels
+                _pcopy(slot["hin"][:h].numpy(), block)
                 hsrc = slot["hin"][:h]
             slot["dsrc"][:h].copy_(hsrc, non_blocking=True)
             plan.run(slot["dsrc"], slot["ddst"], h * width, stream=s)
