@@ -203,7 +203,7 @@ def run_reference(args, rank, world):
     sample = (f"{rows} x {args.width} band ({rows * args.width / 1e6:.1f} Mpx) of the same "
               f"synthetic model rendered by the oracle; per step fit(band) "
               f"{tf:.3f} s + transform(band, workers={cores}, strip 64) {tx:.3f} s, "
-              f"extrapolated linearly to {total / 1e9:.0f} Gpx")
+              f"extrapolated linearly to {total / 1e9:.2f} Gpx")
     line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpx/s", "n_gpus": world,
             "steps": len(times), "warmup": 1, "ms_per_step": round(step_ms, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -218,13 +218,16 @@ def run_reference(args, rank, world):
 
 
 def workload_config(args, world):
-    return {"workload": f"C4: {args.width}x{args.height} synthetic H&E WSI "
-                        f"({args.width * args.height / 1e9:.2f} Gpx, tissue {args.tissue} "
+    npx = args.width * args.height
+    tag = ("C3" if npx == 20000 * 20000 else
+           "C5" if args.tissue <= 0.35 else "C4" if npx == 100000 * 100000 else "WSI")
+    return {"workload": f"{tag}: {args.width}x{args.height} synthetic H&E WSI "
+                        f"({npx / 1e9:.2f} Gpx, tissue {args.tissue} "
                         f"{args.layout}); step = fit(source) + transform(all pixels) vs a "
                         "fixed target profile",
             "width": args.width, "height": args.height, "precision": args.precision,
             "parallelism": f"row-band x{world}", "p99_mode": args.p99_mode,
-            "l2": "input+output 60 GB per step >> 126 MB L2 (no flush needed)"}
+            "l2": f"input+output {6 * npx / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)"}
 
 
 # --------------------------------------------------------------------------- batch (configs[1])
@@ -691,7 +694,7 @@ def cpu_baseline(args, slide, target):
             "sample": (f"{rows} x {args.width} band ({rows * args.width / 1e6:.1f} Mpx) of the "
                        f"same slide; fit {tf:.3f} s + transform {tx:.3f} s (oracle port = "
                        f"reference algorithm in NumPy, {cores} threads, strip 64), "
-                       f"extrapolated linearly to {total / 1e9:.0f} Gpx")}
+                       f"extrapolated linearly to {total / 1e9:.2f} Gpx")}
 
 
 def main():
