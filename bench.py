@@ -68,7 +68,7 @@ def parse():
                          "patches); tile = configs[0] (2048^2 tile vs 2048^2 target)")
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--patch", type=int, default=512)
-    ap.add_argument("--batch-chunk", type=int, default=1024,
+    ap.add_argument("--batch-chunk", type=int, default=256,
                     help="items per pipelined chunk of the host-batch e2e leg")
     ap.add_argument("--cpu-patches", type=int, default=max(8, os.cpu_count() or 1),
                     help="patches in the CPU-baseline sample (one per host core)")
@@ -338,7 +338,7 @@ def run_batch(args, rank, world, local):
         for i in range(args.e2e_steps + 1):
             torch.cuda.synchronize()
             t_a = time.perf_counter()
-            pb.normalize_batch_host(h_in, target, h_out, chunk=args.batch_chunk,
+            pb.normalize_batch_host(h_in, target, h_out, chunk=args.batch_chunk, streams=6,
                                     precision=args.precision)
             torch.cuda.synchronize()
             if i:
@@ -348,7 +348,7 @@ def run_batch(args, rank, world, local):
                        "h2d_bytes_per_step": 3 * npx, "d2h_bytes_per_step": 3 * npx,
                        "seconds_per_step": round(sec, 4),
                        "path": f"pb.normalize_batch_host(pinned host batch -> pinned host), "
-                               f"{args.batch_chunk}-item chunks pipelined over 3 streams"}
+                               f"{args.batch_chunk}-item chunks pipelined over 6 streams"}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_batch_baseline(args, imgs, target)
     if rank == 0:

@@ -336,6 +336,13 @@ int spcn_render_synthetic(uint8_t* out, int64_t width, int64_t row0, int64_t row
                           int64_t height, uint64_t seed, const spcn_synth_params* p,
                           void* stream);
 
+/* Copy `bytes` of device memory into pinned host memory with a small kernel
+ * (stores through the host mapping) rather than a copy engine, stream-ordered;
+ * for small read-backs that must not wait behind large transfers queued on
+ * the copy engine by other streams.  Falls back to cudaMemcpyAsync when the
+ * buffer is not mapped or not 4-byte aligned.                               */
+int spcn_readback(const void* src, void* host_pinned, int64_t bytes, void* stream);
+
 /* Thread-local description of the last error ("" if none).                 */
 const char* spcn_last_error(void);
 

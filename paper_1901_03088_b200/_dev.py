@@ -43,17 +43,32 @@ def to_device(x, dtype=None, device=None):
     return y.to(dev, non_blocking=False)
 
 
-def workspace(nbytes: int, device=None):
-    """Per-(device, thread) cached byte buffer for the repair list."""
+def workspace(nbytes: int, device=None, stream: int | None = None):
+    """Cached byte buffer for the repair list, one per (device, thread,
+    stream): launches in flight on different streams (the streamed strips,
+    the pipelined batch chunks) must not share a repair list."""
     t = torch()
     dev = device if device is not None else t.cuda.current_device()
-    key = (int(dev), threading.get_ident())
+    if stream is None:
+        stream = int(t.cuda.current_stream().cuda_stream)
+    key = (int(dev), threading.get_ident(), int(stream))
     with _ws_lock:
-        buf = _ws_cache.get(key)
+        buf = _ws_cache.pop(key, None)
         if buf is None or buf.numel() < nbytes:
-            buf = t.empty(int(nbytes), dtype=t.uint8, device=dev)
-            _ws_cache[key] = buf
+            with t.cuda.stream(t.cuda.ExternalStream(int(stream))) if stream else _null():
+                buf = t.empty(int(nbytes), dtype=t.uint8, device=dev)
+        _ws_cache[key] = buf            # most recently used last
+        if len(_ws_cache) > 64:         # bound the cache (callers with transient streams);
+            _ws_cache.pop(next(iter(_ws_cache)))   # freed into its own stream's pool: safe
     return buf
+
+
+class _null:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
 
 
 def f64_array(x, n, name):
@@ -61,3 +76,31 @@ def f64_array(x, n, name):
     if a.size != n:
         raise ValueError(f"{name} must have {n} entries, got {a.size}")
     return np.ascontiguousarray(a)
+
+
+_rb = threading.local()
+
+
+def readback(x) -> np.ndarray:
+    """Small CUDA tensor → numpy through a reusable pinned buffer written by a
+    kernel (libspcn spcn_readback), synchronising only the current stream —
+    not queued behind large copies other streams have on the copy engine."""
+    import ctypes
+
+    from . import _lib
+
+    t = torch()
+    x = x.contiguous()
+    nbytes = x.numel() * x.element_size()
+    buf = getattr(_rb, "buf", None)
+    if buf is None or buf.numel() < max(nbytes, 4):
+        buf = t.empty(max(4096, 2 * nbytes), dtype=t.uint8, pin_memory=True)
+        _rb.buf = buf
+    L = _lib.lib()
+    if not getattr(L, "_spcn_rb_declared", False):
+        _lib.declare("spcn_readback", ctypes.c_int, [_lib.P, _lib.P, _lib.I64, _lib.P])
+        L._spcn_rb_declared = True
+    _lib.check(L.spcn_readback(_lib.ptr(x), _lib.ptr(buf), nbytes, _lib.stream_handle()),
+               "readback")
+    t.cuda.current_stream().synchronize()
+    return buf[:nbytes].view(x.dtype).reshape(x.shape).numpy().copy()

@@ -37,7 +37,7 @@ EXPORTS = (
     "spcn_batch_sizes", "spcn_batch_params", "spcn_xform_batch",
     "spcn_stats_hist", "spcn_stats_refine", "spcn_stats_table", "spcn_stats_table_scan",
     "spcn_sample_visit",
-    "spcn_last_error", "spcn_version", "spcn_launch_count", "spcn_xform_shape",
+    "spcn_readback", "spcn_last_error", "spcn_version", "spcn_launch_count", "spcn_xform_shape",
 )
 
 

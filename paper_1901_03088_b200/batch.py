@@ -12,6 +12,7 @@ build and one persistent recolour launch (+ the fp64 repair launch).
 from __future__ import annotations
 
 import ctypes
+import threading
 import warnings
 from dataclasses import dataclass
 
@@ -129,7 +130,7 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
     thr = int(plan.white_threshold)
     _lib.check(L.spcn_sample_count(_lib.ptr(imgs), _lib.ptr(d_desc), n * ncand, chunks, thr,
                                    _lib.ptr(counts), _lib.stream_handle()), "sample_count")
-    tot = counts.sum(dim=1).cpu().numpy().astype(np.int64).reshape(n, ncand, 4)
+    tot = _dev.readback(counts.sum(dim=1)).astype(np.int64).reshape(n, ncand, 4)
     # the reference's visit loop per item (vectorised for single-patch grids)
     take_nw = np.zeros((n, ncand), np.int64)
     take_b = np.zeros((n, ncand, 3), np.int64)
@@ -173,8 +174,8 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
     empty = t.empty((n, 3), dtype=t.int32, device=dev)
     _lib.check(L.spcn_i0_from_hist(_lib.ptr(hist), n, _lib.ptr(i0), _lib.ptr(empty),
                                    _lib.stream_handle()), "i0_from_hist")
-    i0_h = i0.cpu().numpy()
-    if empty.any().item():
+    i0_h = _dev.readback(i0)
+    if _dev.readback(empty).any():
         warnings.warn("some items had no pixels brighter than the white threshold in a "
                       "channel; their i0 fell back to 255", optics.BackgroundEstimateWarning,
                       stacklevel=2)
@@ -193,10 +194,10 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
 
         h = snmf.code_samples(flat, d_off, luts, r.basis, code_lam, mmax)
         p99, absent = dstats.segment_percentiles(h, d_off, 99.0)
-    absent_h = absent.cpu().numpy().any(axis=1)
+    absent_h = _dev.readback(absent).any(axis=1)
     status[(status == 0) & absent_h] = -_lib.SPCN_ESTAIN_ABSENT
     prov = {"source": "", "config_hash": config_hash(_cfg_fields(plan, cfg, code_lam, False))}
-    info = r.info.cpu().numpy()
+    info = _dev.readback(r.info)
     return BatchFit(i0=i0, basis=r.basis, p99=p99, luts=luts, count=collected, status=status,
                     provenance=prov, iterations=info[:, 0].copy(), converged=info[:, 1] != 0,
                     warn_flags=info[:, 2].copy())
@@ -233,7 +234,7 @@ def transform_batch(images, fits: BatchFit, target: FitParams, out=None, *,
                "batch_params")
     if precision == "strict":
         status = t.where(status == 0, t.ones_like(status), status)
-    status_h = status.cpu().numpy()
+    status_h = _dev.readback(status)
     errors = [None if s >= 0 else _ERR[int(s)](_MSG[int(s)]) for s in status_h]
     if per % 16:
         # item boundaries not 16-pixel aligned: one aligned-head/tail launch per item
@@ -271,7 +272,21 @@ def normalize_batch(images, target, *, plan: SamplePlan = SamplePlan(),
     return out, errors, fits
 
 
-def normalize_batch_host(images, target, out=None, *, chunk: int = 512, streams: int = 3,
+_HOST_STREAMS = threading.local()
+_SLICE_BYTES = 64 << 20
+
+
+def _sliced_copy(dst, src, non_blocking):
+    """dst.copy_(src) as <= 64 MB pieces: a copy engine serves its queue in
+    order, so one 800 MB transfer would hold up the fit's small read-backs
+    (issued from another stream) until it finished; between pieces they
+    interleave."""
+    per = max(1, _SLICE_BYTES // max(1, src[0].numel())) if src.shape[0] else 1
+    for i in range(0, src.shape[0], per):
+        dst[i:i + per].copy_(src[i:i + per], non_blocking=non_blocking)
+
+
+def normalize_batch_host(images, target, out=None, *, chunk: int = 256, streams: int = 6,
                          plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(),
                          code_lam: float = 0.0, precision: str = "exact"):
     """normalize_batch for a host-resident batch ((n, H, W, 3) uint8 numpy array
@@ -291,7 +306,13 @@ def normalize_batch_host(images, target, out=None, *, chunk: int = 512, streams:
         out = t.from_numpy(out)
     pinned = host.is_pinned() and out.is_pinned()
     starts = list(range(0, n, chunk))
-    slots = [dict(stream=t.cuda.Stream(), done=None, d_in=None) for _ in range(max(2, streams))]
+    # streams persist per thread: the caching allocator keeps freed blocks per
+    # stream, so fresh streams on every call would cudaMalloc (synchronously)
+    # every buffer again and never reuse the cached ones
+    pool = _HOST_STREAMS.__dict__.setdefault("streams", [])
+    while len(pool) < max(2, streams):
+        pool.append(t.cuda.Stream())
+    slots = [dict(stream=pool[i], done=None, d_in=None) for i in range(max(2, streams))]
 
     def upload(k):                       # H2D of chunk k on its slot's stream
         slot = slots[k % len(slots)]
@@ -299,7 +320,9 @@ def normalize_batch_host(images, target, out=None, *, chunk: int = 512, streams:
             slot["done"].synchronize()   # the chunk that used this slot has left the GPU
         a, b = starts[k], min(n, starts[k] + chunk)
         with t.cuda.stream(slot["stream"]):
-            slot["d_in"] = host[a:b].to("cuda", non_blocking=pinned)
+            d = t.empty(host[a:b].shape, dtype=t.uint8, device="cuda")
+            _sliced_copy(d, host[a:b], pinned)
+            slot["d_in"] = d
 
     errors = [None] * n
     if starts:
@@ -314,7 +337,7 @@ def normalize_batch_host(images, target, out=None, *, chunk: int = 512, streams:
             fits = fit_batch(d_in, plan, cfg, code_lam=code_lam)
             d_out, errs = transform_batch(d_in, fits, target, code_lam=code_lam,
                                           precision=precision)
-            out[a:b].copy_(d_out, non_blocking=pinned)
+            _sliced_copy(out[a:b], d_out, pinned)
             ev = t.cuda.Event()
             ev.record(slot["stream"])
         slot["done"] = ev

@@ -647,6 +647,42 @@ int spcn_stats_table_scan(const spcn_xform_params* p, const unsigned long long* 
 // ------------------------------------------------------------------ synthetic input
 #include "synth.h"
 
+// ------------------------------------------------------------------ small read-backs
+namespace {
+__global__ void k_copy_to_host(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                               int64_t words) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+}  // namespace
+
+// Device -> pinned host through the SMs (stores over PCIe into the mapped
+// allocation) instead of a copy engine: a read-back of a few KB never queues
+// behind multi-hundred-MB transfers another stream has on the copy engine.
+extern "C" int spcn_readback(const void* src, void* host_pinned, int64_t bytes, void* stream) {
+  g_err.clear();
+  if (bytes < 0) return fail(SPCN_EINVAL, "bytes must be >= 0");
+  if (bytes == 0) return SPCN_OK;
+  if (!src || !host_pinned) return fail(SPCN_EINVAL, "NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* dptr = nullptr;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(host_pinned) |
+                         static_cast<uintptr_t>(bytes)) & 3) == 0;
+  if (aligned && cudaHostGetDevicePointer(&dptr, host_pinned, 0) == cudaSuccess && dptr) {
+    const int64_t words = bytes / 4;
+    int grid = static_cast<int>((words + 255) / 256);
+    if (grid > 64) grid = 64;
+    k_copy_to_host<<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(src),
+                                         static_cast<uint32_t*>(dptr), words);
+    const cudaError_t e = launched();
+    return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "readback");
+  }
+  cudaGetLastError();   // not mapped / unaligned: plain async copy
+  const cudaError_t e = cudaMemcpyAsync(host_pinned, src, bytes, cudaMemcpyDeviceToHost, st);
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "readback");
+}
+
 extern "C" int spcn_render_synthetic(uint8_t* out, int64_t width, int64_t row0, int64_t rows,
                                      int64_t height, uint64_t seed, const spcn_synth_params* p,
                                      void* stream) {

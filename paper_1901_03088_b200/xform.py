@@ -50,7 +50,7 @@ class XformPlan:
         bound measured on all 2^24 colours (fewer fp64 repairs, same bytes)."""
         if self.alpha is None:
             L = _lib.lib()
-            ws = _dev.workspace(64)
+            ws = _dev.workspace(64, stream=_lib.stream_handle(stream))
             out = ctypes.c_double(-1.0)
             _lib.check(L.spcn_xform_calibrate(ctypes.byref(self.params), _lib.ptr(ws), 64,
                                               ctypes.byref(out), _lib.stream_handle(stream)),
@@ -74,7 +74,7 @@ class XformPlan:
         """src/dst: CUDA uint8 tensors (or raw device pointers) holding npix RGB pixels."""
         L = _lib.lib()
         ws_bytes = int(L.spcn_xform_workspace_bytes(int(npix)))
-        ws = _dev.workspace(ws_bytes)
+        ws = _dev.workspace(ws_bytes, stream=_lib.stream_handle(stream))
         sp = src if isinstance(src, int) else _lib.ptr(src)
         dp = dst if isinstance(dst, int) else _lib.ptr(dst)
         _lib.check(L.spcn_xform_rgb8(sp, dp, int(npix), ctypes.byref(self.params), _lib.ptr(ws),
@@ -83,7 +83,7 @@ class XformPlan:
     def repair_count(self, stream=None) -> int:
         """Pixels sent to the fp64 repair path by the last EXACT run (synchronizes)."""
         L = _lib.lib()
-        ws = _dev.workspace(16)
+        ws = _dev.workspace(16, stream=_lib.stream_handle(stream))
         out = ctypes.c_int64(0)
         _lib.check(L.spcn_xform_repair_count(_lib.ptr(ws), _lib.stream_handle(stream),
                                              ctypes.byref(out)), "repair_count")

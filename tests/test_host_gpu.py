@@ -54,3 +54,25 @@ def test_numpy_path_concurrent_threads():
     assert not errs, errs
     for i in range(6):
         assert np.array_equal(got[i], ref[i % 3]), i
+
+
+def test_streamed_strips_in_flight_keep_their_repair_lists():
+    """Many short strips on several streams at once (each with its own fp64
+    repair list): byte-identical to one device launch and to the oracle."""
+    import torch
+
+    import paper_1901_03088_b200 as pb
+
+    warnings.simplefilter("ignore")
+    s, t = _pair(21)
+    sp = pb.fit(pb.ArraySource(s))
+    tp = pb.fit(pb.ArraySource(t))
+    ref = pb.DeviceWriter(s.shape[1], s.shape[0])
+    pb.transform(pb.DeviceSource(torch.from_numpy(s).cuda()), sp, tp, ref)
+    for workers in (2, 4):
+        sink = pb.ArrayWriter(s.shape[1], s.shape[0])
+        pb.transform(pb.ArraySource(s), sp, tp, sink, strip_height=48, workers=workers)
+        assert np.array_equal(sink.pixels, ref.pixels.cpu().numpy()), workers
+    want = orc.run_transform(s, dict(i0=sp.i0, basis=sp.basis, p99=sp.stats.p99),
+                             dict(i0=tp.i0, basis=tp.basis, p99=tp.stats.p99), workers=4)
+    assert np.array_equal(sink.pixels, want)
