@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 
 #include "launch_count.h"
+#include "ctable.cuh"
 #include "snmf.h"
 #include "spcn_device.cuh"
 
@@ -372,9 +373,6 @@ cudaError_t launch_code_table(const uint32_t* ukey, const int32_t* ucount, const
 // writes them as (rgb, pixel count) entries at the problem's sample offset;
 // the SNMF passes then iterate over ~10x fewer entries with weights.  If the
 // table fills up, the problem's samples are listed one by one with count 1.
-constexpr int kTabBits = 14;
-constexpr int kTabSlots = 1 << kTabBits;
-constexpr uint32_t kTabEmpty = 0xffffffffu;
 
 constexpr int kCT = 1024;   // threads of k_colour_table
 
@@ -388,27 +386,7 @@ __global__ void __launch_bounds__(kCT) k_colour_table(const uint8_t* __restrict_
   uint32_t* cnt = tab + kTabSlots;
   __shared__ int s_full, s_used;   // table too full (or a probe failed) -> list the samples
   __shared__ uint32_t s_scan[kCT];
-  const int tid = threadIdx.x, lane = tid & 31;
-  constexpr uint32_t kNone = 0xffffffffu;   // not a sample
-  // one colour per lane (kNone: none): lanes holding the same colour insert once
-  auto insert = [&](uint32_t rgb) {
-    const unsigned peers = __match_any_sync(0xffffffffu, rgb);
-    if (rgb == kNone || lane != __ffs(peers) - 1) return;
-    const uint32_t add = __popc(peers);
-    uint32_t slot = (rgb * 2654435761u) >> (32 - kTabBits);
-    for (int probe = 0; probe < 64; ++probe, slot = (slot + 1) & (kTabSlots - 1)) {
-      uint32_t k = key[slot];
-      if (k == kTabEmpty) {
-        k = atomicCAS(&key[slot], kTabEmpty, rgb);
-        if (k == kTabEmpty && atomicAdd(&s_used, 1) >= (3 * kTabSlots) / 4) s_full = 1;
-      }
-      if (k == kTabEmpty || k == rgb) {
-        atomicAdd(&cnt[slot], add);
-        return;
-      }
-    }
-    s_full = 1;
-  };
+  const int tid = threadIdx.x;
   for (int p = blockIdx.x; p < nprob; p += gridDim.x) {
     const int64_t o0 = offsets[p], m = offsets[p + 1] - o0;
     for (int i = tid; i < kTabSlots; i += kCT) {
@@ -437,70 +415,24 @@ __global__ void __launch_bounds__(kCT) k_colour_table(const uint8_t* __restrict_
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) rgb[j] = kNone;
+        for (int j = 0; j < 16; ++j) rgb[j] = kNoColour;
       }
 #pragma unroll 1
-      for (int j = 0; j < 16; ++j) insert(rgb[j]);
+      for (int j = 0; j < 16; ++j) ct_insert(key, cnt, &s_used, &s_full, rgb[j]);
     }
     // head [0, a) and tail [rest0, m): < 32 samples, one warp
     if (tid < 32) {
       const int64_t i = tid < a ? tid : rest0 + (tid - a);
-      uint32_t rgb = kNone;
+      uint32_t rgb = kNoColour;
       if ((tid < a) || (tid >= a && i < m)) {
         const uint8_t* px = samples + 3 * (o0 + i);
         rgb = px[0] | (px[1] << 8) | (px[2] << 16);
       }
-      insert(rgb);
+      ct_insert(key, cnt, &s_used, &s_full, rgb);
     }
     __syncthreads();
     if (!s_full) {
-      // With linear probing the SET of occupied slots, hence every cluster
-      // (maximal run of occupied slots) and its key set, does not depend on
-      // insertion order — only the order inside a cluster does.  Sorting each
-      // cluster by colour makes the entry order, and every later
-      // floating-point summation order, deterministic.
-      for (int s0 = tid; s0 < kTabSlots; s0 += kCT) {
-        if (key[s0] == kTabEmpty || key[(s0 - 1) & (kTabSlots - 1)] != kTabEmpty) continue;
-        int len = 1;                                     // this thread owns the cluster at s0
-        while (len < kTabSlots && key[(s0 + len) & (kTabSlots - 1)] != kTabEmpty) ++len;
-        for (int x = 1; x < len; ++x) {                  // insertion sort, clusters are short
-          const int sx = (s0 + x) & (kTabSlots - 1);
-          const uint32_t kx = key[sx], cx = cnt[sx];
-          int y = x - 1;
-          while (y >= 0 && key[(s0 + y) & (kTabSlots - 1)] > kx) {
-            const int sy = (s0 + y) & (kTabSlots - 1), sy1 = (s0 + y + 1) & (kTabSlots - 1);
-            key[sy1] = key[sy];
-            cnt[sy1] = cnt[sy];
-            --y;
-          }
-          const int sd = (s0 + y + 1) & (kTabSlots - 1);
-          key[sd] = kx;
-          cnt[sd] = cx;
-        }
-      }
-      __syncthreads();
-      // compact in slot order (block scan)
-      constexpr int kPer = kTabSlots / kCT;
-      uint32_t occ = 0;
-      for (int j = 0; j < kPer; ++j) occ += key[tid * kPer + j] != kTabEmpty;
-      s_scan[tid] = occ;
-      __syncthreads();
-      for (int off = 1; off < kCT; off <<= 1) {
-        const uint32_t y = tid >= off ? s_scan[tid - off] : 0u;
-        __syncthreads();
-        s_scan[tid] += y;
-        __syncthreads();
-      }
-      uint32_t pos = s_scan[tid] - occ;
-      for (int j = 0; j < kPer; ++j) {
-        const int sl = tid * kPer + j;
-        if (key[sl] != kTabEmpty) {
-          ukey[o0 + pos] = key[sl];
-          ucnt[o0 + pos] = cnt[sl];
-          ++pos;
-        }
-      }
-      if (tid == kCT - 1) ucount[p] = (int32_t)s_scan[kCT - 1];
+      ct_finish<kCT>(key, cnt, s_scan, ukey, ucnt, o0, &ucount[p]);
     } else {
       for (int64_t i = tid; i < m; i += kCT) {
         const uint8_t* px = samples + 3 * (o0 + i);
@@ -508,8 +440,8 @@ __global__ void __launch_bounds__(kCT) k_colour_table(const uint8_t* __restrict_
         ucnt[o0 + i] = 1u;
       }
       if (tid == 0) ucount[p] = (int32_t)m;
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
