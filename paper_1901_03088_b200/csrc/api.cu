@@ -5,6 +5,7 @@
 // beer_lambert's i0 check (src/optics.py:90-91), code_densities' lam check
 // (src/stain_sep.py:188-189), normalize_block's factor check
 // (src/normalize.py:141-142).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -545,6 +546,40 @@ int stats_setup(const spcn_xform_params* p, int32_t white, StatsArgs& a, StrictP
   a.white_by_od = by_od ? 1u : 0u;
   return SPCN_OK;
 }
+// The table pass's four linear upper-bound forms (stats.cu k_stats_table):
+// stain 0: u0 - a0 = (g11 t0 - g01 t1)/det - a0 and t0/g00 - a0; stain 1:
+// (g00 t1 - g01 t0)/det - a1 and t1/g11 - a1, with t_j = sum_c w_cj v_c - lam,
+// as k.v + b in fp64, then fp32 with the evaluation error bound added to b:
+// |fp32(k.v + b) - (k.v + b)| <= 2^-21 (sum|k| V + |b|) for V = max OD (the
+// fp32 table, the fp32 coefficients and three FMAs); 8x that is added.  An
+// ill-conditioned basis (or no positive lower bound) makes every non-white
+// pixel a candidate.
+void stats_linear_forms(const StrictP& sp, const double* lo, StatsArgs& a) {
+  const double g00 = sp.g00, g01 = sp.g01, g11 = sp.g11, det = sp.det, lam = sp.lam;
+  double V = 0.0;
+  for (int c = 0; c < 3; ++c)
+    for (int x = 0; x < 256; ++x) V = std::max(V, std::fabs(sp.lut[c][x]));
+  const bool ok = det > 1e-6 * g00 * g11 && g00 > 0.0 && g11 > 0.0;
+  double k[4][3], b[4];
+  for (int c = 0; c < 3; ++c) {
+    const double w0 = sp.ws[c][0], w1 = sp.ws[c][1];
+    k[0][c] = ok ? (g11 * w0 - g01 * w1) / det : 0.0;
+    k[1][c] = ok ? w0 / g00 : 0.0;
+    k[2][c] = ok ? (g00 * w1 - g01 * w0) / det : 0.0;
+    k[3][c] = ok ? w1 / g11 : 0.0;
+  }
+  b[0] = ok ? (-g11 * lam + g01 * lam) / det - lo[0] : 1.0;
+  b[1] = ok ? -lam / g00 - lo[0] : 1.0;
+  b[2] = ok ? (-g00 * lam + g01 * lam) / det - lo[1] : 1.0;
+  b[3] = ok ? -lam / g11 - lo[1] : 1.0;
+  for (int i = 0; i < 4; ++i) {
+    double sk = 0.0;
+    for (int c = 0; c < 3; ++c) sk += std::fabs(k[i][c]);
+    const double margin = 8.0 * std::ldexp(sk * V + std::fabs(b[i]), -21);
+    for (int c = 0; c < 3; ++c) a.lf[i][c] = static_cast<float>(k[i][c]);
+    a.lf[i][3] = std::nextafter(static_cast<float>(b[i] + margin), INFINITY);
+  }
+}
 }  // namespace
 
 extern "C" {
@@ -621,8 +656,10 @@ int spcn_stats_table(const uint8_t* src, int64_t npix, const spcn_xform_params* 
     a.shift[j] = 0;
     a.a[j] = lo[j];
     a.b[j] = INFINITY;
+    if (!(lo[j] > 0.0)) return fail(SPCN_EINVAL, "table pass needs lo > 0");
   }
   a.nbins = 1;
+  stats_linear_forms(sp, lo, a);
   const cudaError_t e = launch_stats_table(src, npix, a, table, counts,
                                            static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_table");

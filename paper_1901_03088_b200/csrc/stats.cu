@@ -500,7 +500,24 @@ __global__ void __launch_bounds__(32 * kRefCW, 1)
 // the order statistics at or above a_j are exactly those of the table
 // entries with x_j >= a_j (the host checks the ranks land there).
 constexpr int kTabSlots = 4096;
-constexpr size_t kStSmemTable = LutLayout<16>::kBytes + kTabSlots * 8 + StRing<kRefCW, kRefNSW>::kBytes;
+// Shared-memory layout of the table pass: the OD table sits at the ABSOLUTE
+// shared-window address 0x10000, so the PRMT that forms an entry's offset
+// (pixel byte << 8 | lane byte, region byte 1) is already its address and
+// the load needs no base add (the compiler would otherwise add the window
+// base per lookup: 3 instructions per pixel).  Colour cache below it, the
+// TMA ring above it.
+constexpr uint32_t kTabLutAbs = 0x10000;
+constexpr size_t kStSmemTable = kTabLutAbs + LutLayout<16>::kBytes + StRing<kRefCW, kRefNSW>::kBytes;
+
+__device__ __forceinline__ float lds_abs(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float od_abs(const uint32_t* w, int idx, uint32_t lc) {
+  const uint32_t sel = 0x7604u | ((uint32_t)(idx & 3) << 4);
+  return lds_abs(__byte_perm(w[idx >> 2], lc, sel));
+}
 
 template <bool OD>
 __global__ void __launch_bounds__(32 * kRefCW, 1)
@@ -508,10 +525,13 @@ __global__ void __launch_bounds__(32 * kRefCW, 1)
                   unsigned long long* __restrict__ table, unsigned long long* __restrict__ counts) {
   constexpr int kThreads = 32 * kRefCW;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* ckey = reinterpret_cast<uint32_t*>(smem + LutLayout<16>::kBytes);
+  const uint32_t base = smem_u32(smem);
+  if (base + kTabSlots * 8 > kTabLutAbs) __trap();   // layout assumption (window base <= 32 KB)
+  uint8_t* lut = smem + (kTabLutAbs - base);
+  uint32_t* ckey = reinterpret_cast<uint32_t*>(smem);
   uint32_t* ccnt = ckey + kTabSlots;
-  uint8_t* ring = smem + LutLayout<16>::kBytes + kTabSlots * 8;
-  LutLayout<16>::fill(smem, &a.lut[0][0], threadIdx.x, kThreads);
+  uint8_t* ring = lut + LutLayout<16>::kBytes;
+  LutLayout<16>::fill(lut, &a.lut[0][0], threadIdx.x, kThreads);
   for (int i = threadIdx.x; i < kTabSlots; i += kThreads) {
     ckey[i] = kEmpty;
     ccnt[i] = 0;
@@ -519,26 +539,59 @@ __global__ void __launch_bounds__(32 * kRefCW, 1)
   __syncthreads();
   uint32_t lc[3];
   LutLayout<16>::lane_consts(threadIdx.x & 31, lc);
-  const float2 ea0 = bc2(2.0f * a.coef[0]), ea1 = bc2(2.0f * a.coef[1]), tiny = bc2(2e-30f);
-  const float2 nlo0 = bc2(-2.0f * __double2float_rd(a.a[0])), nlo1 = bc2(-2.0f * __double2float_rd(a.a[1]));
+  for (int c = 0; c < 3; ++c) lc[c] |= kTabLutAbs;   // region byte = 1: absolute address
+  // Candidates without solving the NNLS: for two stains the solution has
+  // h_j in {0, u_j, t_j/g_jj} (u = G^-1 t, t = W^T v - lam: the three
+  // active sets), so h_j <= max(u_j, t_j/g_jj, 0) and a pixel is surely below
+  // a_j > 0 when both linear forms u_j - a_j and t_j/g_jj - a_j are negative.
+  // The four forms k.v + b are evaluated in fp32 with their rounding bound
+  // folded into b (host, stats_linear_forms); a pixel with every form < 0 is
+  // off the table.
   int32_t nonwhite = 0;
   st_scan<kRefCW, kRefNSW>(src, npix, ring,
                            [&](const uint32_t* w, int nv, uint32_t inv, const uint8_t* blk) {
     uint32_t cand = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const StPair d = st_pair<OD>(a, smem, lc, w, q);
-      uint32_t wx = d.wx | inv, wy = d.wy | inv;
+      const int ia = 6 * q, ib = 6 * q + 3;
+      const float2 v0 = make_float2(od_abs(w, ia, lc[0]), od_abs(w, ib, lc[0]));
+      const float2 v1 = make_float2(od_abs(w, ia + 1, lc[1]), od_abs(w, ib + 1, lc[1]));
+      const float2 v2 = make_float2(od_abs(w, ia + 2, lc[2]), od_abs(w, ib + 2, lc[2]));
+      uint32_t wx, wy;
+      if (OD) {
+        const float2 s0 = __fadd2_rn(v0, bc2(a.nwod[0]));
+        const float2 s1 = __fadd2_rn(v1, bc2(a.nwod[1]));
+        const float2 s2 = __fadd2_rn(v2, bc2(a.nwod[2]));
+        wx = (uint32_t)((int32_t)(__float_as_uint(s0.x) & __float_as_uint(s1.x) & __float_as_uint(s2.x)) >> 31);
+        wy = (uint32_t)((int32_t)(__float_as_uint(s0.y) & __float_as_uint(s1.y) & __float_as_uint(s2.y)) >> 31);
+      } else {
+        uint32_t m[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const int k = 2 * q + p;
+          const bool white = st_byte(w, 3 * k) > a.white && st_byte(w, 3 * k + 1) > a.white &&
+                             st_byte(w, 3 * k + 2) > a.white;
+          m[p] = white ? ~0u : 0u;
+        }
+        wx = m[0];
+        wy = m[1];
+      }
+      wx |= inv;
+      wy |= inv;
       if (nv < 16) {
         if (2 * q >= nv) wx = ~0u;
         if (2 * q + 1 >= nv) wy = ~0u;
       }
       nonwhite += 2 + (int32_t)wx + (int32_t)wy;
-      const float2 e0 = __ffma2_ru(ea0, d.T, tiny), e1 = __ffma2_ru(ea1, d.T, tiny);
-      const float2 eb0 = __fadd2_rn(__fadd2_ru(d.h0x2, e0), nlo0);
-      const float2 eb1 = __fadd2_rn(__fadd2_ru(d.h1x2, e1), nlo1);
-      const uint32_t sx = (__float_as_uint(eb0.x) & __float_as_uint(eb1.x)) | wx;
-      const uint32_t sy = (__float_as_uint(eb0.y) & __float_as_uint(eb1.y)) | wy;
+      float2 f[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        f[i] = __ffma2_rn(bc2(a.lf[i][0]), v0,
+                          __ffma2_rn(bc2(a.lf[i][1]), v1, __ffma2_rn(bc2(a.lf[i][2]), v2, bc2(a.lf[i][3]))));
+      const uint32_t sx = (__float_as_uint(f[0].x) & __float_as_uint(f[1].x) &
+                           __float_as_uint(f[2].x) & __float_as_uint(f[3].x)) | wx;
+      const uint32_t sy = (__float_as_uint(f[0].y) & __float_as_uint(f[1].y) &
+                           __float_as_uint(f[2].y) & __float_as_uint(f[3].y)) | wy;
       cand |= (~sx >> 31) << (2 * q);
       cand |= (~sy >> 31) << (2 * q + 1);
     }

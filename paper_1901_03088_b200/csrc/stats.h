@@ -16,6 +16,7 @@ struct StatsArgs {
   uint32_t shift[2];        // bin = (key - base) >> shift
   int32_t nbins;            // <= 8192
   double a[2], b[2];        // refine window [a, b) per stain
+  float lf[4][4];           // table pass: linear upper-bound forms k.v + b (see stats.cu)
 };
 cudaError_t launch_stats_hist(const uint8_t* src, int64_t npix, const StatsArgs& a,
                               unsigned long long* hist, unsigned long long* counts,

@@ -293,6 +293,7 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
             vals, below = res
             p99 = np.array([interpolate(vals[j][0], vals[j][1], rank) for j in range(2)])
             info.update(mode="table", nonwhite=n, colours=int(sc[1].numel()), below=below,
+                        table_pixels=int(sc[1].sum().item()),
                         fp64_evaluations=int(sc[1].numel()), levels=0)
             return p99, n, info
         info["table_miss"] = True
