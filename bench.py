@@ -520,7 +520,10 @@ def run_ours(args, rank, world, local):
         if record:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-        pb.transform(src, fp, target, sink, precision=args.precision)
+        if group is None:
+            pb.transform(src, fp, target, sink, precision=args.precision)
+        else:   # calibration split across the ranks (one max all-reduce)
+            group.transform(src, fp, target, sink, precision=args.precision)
         if record:
             e1.record()
             xform_ms.append((e0, e1))

@@ -47,6 +47,11 @@ extern "C" {
  * a calibrated bound from spcn_xform_calibrate; SPCN_CALIBRATE_INLINE =
  * calibrate on the device inside spcn_xform_rgb8 (no host round trip).     */
 #define SPCN_CALIBRATE_INLINE (-1.0)
+/* SPCN_CALIBRATE_DEVICE: the bound is already in the workspace's calibration
+ * word — multi-GPU: every rank runs spcn_xform_calibrate_part on its share
+ * of the colours, then the words are all-reduced with max (uint32: the bits
+ * of a non-negative float order like the float).                           */
+#define SPCN_CALIBRATE_DEVICE (-2.0)
 
 typedef struct spcn_xform_params {
   double src_i0[3];
@@ -342,6 +347,13 @@ int spcn_render_synthetic(uint8_t* out, int64_t width, int64_t row0, int64_t row
  * the copy engine by other streams.  Falls back to cudaMemcpyAsync when the
  * buffer is not mapped or not 4-byte aligned.                               */
 int spcn_readback(const void* src, void* host_pinned, int64_t bytes, void* stream);
+
+/* Exhaustive calibration of part `part` of `nparts` of the 2^24 colours into
+ * the workspace's calibration word (zeroed first; stream-ordered).  With
+ * every part's word max-reduced, cert_alpha = SPCN_CALIBRATE_DEVICE makes the
+ * transform use it — the same bound as one full calibration.               */
+int spcn_xform_calibrate_part(const spcn_xform_params* p, int32_t part, int32_t nparts,
+                              void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Thread-local description of the last error ("" if none).                 */
 const char* spcn_last_error(void);

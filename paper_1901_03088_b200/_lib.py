@@ -28,7 +28,7 @@ PREC = {"exact": 0, "fast": 1, "strict": 2}
 # every symbol include/spcn.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "spcn_xform_workspace_bytes", "spcn_xform_rgb8", "spcn_xform_repair_count",
-    "spcn_xform_calibrate",
+    "spcn_xform_calibrate", "spcn_xform_calibrate_part",
     "spcn_code_densities", "spcn_normalize_block", "spcn_beer_lambert",
     "spcn_inverse_beer_lambert", "spcn_sample_count", "spcn_sample_compact",
     "spcn_i0_from_hist", "spcn_od_tables", "spcn_snmf_batched", "spcn_code_samples",

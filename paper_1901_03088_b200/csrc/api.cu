@@ -207,11 +207,14 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
   // cert_alpha == SPCN_CALIBRATE_INLINE: calibrate on the device right before
   // the main kernel, which reads the result itself (no host round trip)
   const bool inline_cal = exact && fast_ok && p->cert_alpha == SPCN_CALIBRATE_INLINE;
+  // SPCN_CALIBRATE_DEVICE: the calibration word is already in the workspace
+  // (spcn_xform_calibrate_part on every rank + an all-reduce max)
+  const bool device_cal = exact && fast_ok && p->cert_alpha == SPCN_CALIBRATE_DEVICE;
   if (exact && fast_ok && p->cert_alpha > 0.0 && p->cert_alpha < 1e-3) {
     set_calibrated(fp, p->cert_alpha);
     mode = 2;
   }
-  if (inline_cal) mode = 2;
+  if (inline_cal || device_cal) mode = 2;
 
   // 16-byte alignment of the vector body (both buffers must share the phase)
   const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
@@ -232,7 +235,8 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
     count = static_cast<unsigned long long*>(workspace);
     items = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + kWsHeader);
     cap = (workspace_bytes - kWsHeader) / 8;
-    cudaError_t e = cudaMemsetAsync(count, 0, kWsHeader, st);   // count + calibration word
+    // count + calibration word (kept when it was computed beforehand)
+    cudaError_t e = cudaMemsetAsync(count, 0, device_cal ? 8 : kWsHeader, st);
     if (e != cudaSuccess) return cuda_fail(e, "memset");
   }
   cudaError_t e;
@@ -242,6 +246,8 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
     if ((e = launch_calibrate(fp, sp, bits, st)) != cudaSuccess) return cuda_fail(e, "calibrate");
     alpha_bits = bits;
   }
+  if (device_cal)
+    alpha_bits = reinterpret_cast<const unsigned int*>(static_cast<char*>(workspace) + 8);
   if (head > 0 && (e = launch_xform_strict(src, dst, head, sp, st)) != cudaSuccess)
     return cuda_fail(e, "xform_head");
   e = launch_xform_main(mode, src + 3 * head, dst + 3 * head, body, fp, sp, count, items, cap,
@@ -255,6 +261,33 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
       (e = launch_xform_strict(src + 3 * tail0, dst + 3 * tail0, npix - tail0, sp, st)) != cudaSuccess)
     return cuda_fail(e, "xform_tail");
   return SPCN_OK;
+}
+
+int spcn_xform_calibrate_part(const spcn_xform_params* p, int32_t part, int32_t nparts,
+                              void* workspace, int64_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!p) return fail(SPCN_EINVAL, "params is NULL");
+  if (nparts < 1 || part < 0 || part >= nparts) return fail(SPCN_EINVAL, "bad part");
+  if (!workspace || workspace_bytes < kWsHeader) return fail(SPCN_EINVAL, "workspace too small");
+  int rc = check_basis(p->src_basis, "source");
+  if (!rc) rc = check_basis(p->tgt_basis, "target");
+  if (rc) return rc;
+  double lut[3][256];
+  od_table(p->src_i0, p->od_table, lut);
+  static thread_local StrictP sp;
+  static thread_local FastP fp;
+  fill_strict(sp, &lut[0][0], p->src_basis, p->tgt_basis, p->factors, p->tgt_i0, p->code_lam,
+              p->max_sweeps);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned int* bits = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + 8);
+  cudaError_t e = cudaMemsetAsync(bits, 0, 4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  if (!fill_fast(fp, sp, true)) return SPCN_OK;   // no fast path: the word stays 0 (unused)
+  const uint32_t n = 1u << 23;
+  const uint32_t q0 = static_cast<uint32_t>((uint64_t)n * part / nparts),
+                 q1 = static_cast<uint32_t>((uint64_t)n * (part + 1) / nparts);
+  e = launch_calibrate(fp, sp, bits, st, q0, q1);
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "calibrate_part");
 }
 
 int spcn_xform_repair_count(const void* workspace, void* stream, int64_t* count) {

@@ -190,7 +190,8 @@ __global__ void __launch_bounds__(256) k_xform_strict(const uint8_t* __restrict_
 // record max |y_ref - y_fast| / y_fast over colours with y_fast > 0.
 __global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP fp,
                                                    const __grid_constant__ StrictP sp,
-                                                   unsigned int* __restrict__ max_bits) {
+                                                   unsigned int* __restrict__ max_bits,
+                                                   uint32_t q0, uint32_t q1) {
   __shared__ double lut[3 * 256];
   __shared__ float flut[3 * 256];
   for (int i = threadIdx.x; i < 3 * 256; i += 256) {
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP
   __syncthreads();
   float worst = 0.f;
   const NnlsGram G = gram_of(sp);
-  for (uint32_t q = blockIdx.x * 256u + threadIdx.x; q < (1u << 23); q += 256u * gridDim.x) {
+  for (uint32_t q = q0 + blockIdx.x * 256u + threadIdx.x; q < q1; q += 256u * gridDim.x) {
     const uint32_t ca = 2u * q, cb = 2u * q + 1u;   // colours: r | g<<8 | b<<16
     const float2 v0 = make_float2(flut[ca & 255], flut[cb & 255]);
     const float2 v1 = make_float2(flut[256 + ((ca >> 8) & 255)], flut[256 + ((cb >> 8) & 255)]);
@@ -337,10 +338,15 @@ cudaError_t launch_xform_strict(const uint8_t* src, uint8_t* dst, int64_t npix,
 }
 
 cudaError_t launch_calibrate(const FastP& fp, const StrictP& sp, unsigned int* max_bits,
-                             cudaStream_t st) {
+                             cudaStream_t st, uint32_t q0, uint32_t q1) {
   cudaError_t e = xform_setup_device();
   if (e != cudaSuccess) return e;
-  k_calibrate<<<g_sm_count * 8, 256, 0, st>>>(fp, sp, max_bits);
+  if (q1 <= q0) return cudaSuccess;
+  // colour pairs [q0, q1); a share of the 2^23 pairs gets a proportional grid
+  const int64_t full = (int64_t)g_sm_count * 8;
+  int64_t grid = (full * (int64_t)(q1 - q0) + (1 << 23) - 1) >> 23;
+  if (grid < 1) grid = 1;
+  k_calibrate<<<(int)grid, 256, 0, st>>>(fp, sp, max_bits, q0, q1);
   return launched();
 }
 

@@ -24,7 +24,7 @@ cudaError_t launch_beer_lambert(const uint8_t* px, double* od, int64_t n, const 
 cudaError_t launch_inverse_bl(const double* od, uint8_t* out, int64_t n, const StrictP& sp,
                               cudaStream_t st);
 cudaError_t launch_calibrate(const FastP& fp, const StrictP& sp, unsigned int* max_bits,
-                             cudaStream_t st);
+                             cudaStream_t st, uint32_t q0 = 0, uint32_t q1 = 1u << 23);
 int xform_tile_pixels();
 const char* xform_shape_name();
 }  // namespace spcn

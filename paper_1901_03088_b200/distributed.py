@@ -94,6 +94,19 @@ def all_reduce_sum(t, group=None):
     return t
 
 
+def all_reduce_max(t, group=None):
+    """In-place max all-reduce (NCCL: device-direct; gloo: host-staged)."""
+    import torch.distributed as dist
+
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
+
+
 def all_gather_list(t, group=None):
     """All-gather of equal-shape tensors → list (host-staged under gloo)."""
     import torch.distributed as dist
@@ -134,11 +147,29 @@ class TorchComm:
 
 
 class RowBandGroup:
-    """Sample-mode fit of a row-band-sharded slide (one instance per rank)."""
+    """Fit and transform of a row-band-sharded slide (one instance per rank;
+    both methods are collectives)."""
 
     def __init__(self, width: int, height: int, r0: int, rows: int, group=None):
         self.width, self.height, self.r0, self.rows = width, height, r0, rows
         self.group = group
+
+    def transform(self, band_source, source, target, sink, **kw):
+        """pipeline.transform of this rank's band.  EXACT on a resident band:
+        the exhaustive certification calibration is split across the ranks
+        (each evaluates 1/N of the 2^24 colours, then a max all-reduce of one
+        word) instead of every rank evaluating all of it."""
+        import torch.distributed as dist
+
+        from .pipeline import transform
+
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+
+        def calibrate(plan, npix):
+            plan.calibrate_shared(self.width * self.height, npix, rank, world,
+                                  lambda w: all_reduce_max(w, self.group))
+
+        return transform(band_source, source, target, sink, _calibrate=calibrate, **kw)
 
     def fit(self, band_source, plan=None, cfg=None, *, code_lam: float = 0.0,
             per_patch_stats: bool = False, source_label: str = "", p99_mode: str = "sample"):

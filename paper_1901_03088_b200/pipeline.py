@@ -610,7 +610,7 @@ def transform(slide, source: FitParams, target: FitParams, sink, *,
               strip_height: int = DEFAULT_STRIP_HEIGHT, workers: int | None = None,
               code_lam: float = 0.0, stats: RunStats | None = None,
               gauge: BufferGauge | None = None, progress=None,
-              precision: str = "exact") -> RunStats:
+              precision: str = "exact", _calibrate=None) -> RunStats:
     """src/pipeline.py:275-345 on the device.
 
     Output is byte-identical for any strip height / worker count (and, with
@@ -632,7 +632,10 @@ def transform(slide, source: FitParams, target: FitParams, sink, *,
                      precision=precision)
     t0 = time.perf_counter()
     one_launch = isinstance(slide, DeviceSource)
-    plan.maybe_calibrate(width * slide.height, inline=one_launch)
+    if _calibrate is not None and one_launch:
+        _calibrate(plan, width * slide.height)      # collective (distributed.RowBandGroup)
+    else:
+        plan.maybe_calibrate(width * slide.height, inline=one_launch)
 
     if isinstance(slide, DeviceSource):
         src = slide.tensor

@@ -17,6 +17,7 @@ from .optics import od_table
 
 
 CALIBRATE_INLINE = -1.0   # include/spcn.h SPCN_CALIBRATE_INLINE
+CALIBRATE_DEVICE = -2.0   # include/spcn.h SPCN_CALIBRATE_DEVICE
 
 
 class XformPlan:
@@ -69,6 +70,29 @@ class XformPlan:
                 self.params.cert_alpha = CALIBRATE_INLINE
             else:
                 self.calibrate(stream)
+
+    def calibrate_shared(self, total_pixels: int, npix: int, part: int, nparts: int, reduce_max,
+                         stream=None) -> None:
+        """Multi-GPU calibration: this rank evaluates part `part` of `nparts`
+        of the colours into the calibration word of the workspace the next
+        run(npix) on this stream uses; reduce_max(int32 tensor) max-reduces the
+        word across ranks (a collective: every rank must call this with the
+        same total_pixels, which decides whether to calibrate at all)."""
+        if not (self.precision == "exact" and total_pixels >= self.CALIBRATE_MIN_PIXELS):
+            return
+        L = _lib.lib()
+        if not getattr(L, "_spcn_calpart_declared", False):
+            _lib.declare("spcn_xform_calibrate_part", ctypes.c_int,
+                         [ctypes.POINTER(_lib.XformParams), _lib.I32, _lib.I32, _lib.P, _lib.I64,
+                          _lib.P])
+            L._spcn_calpart_declared = True
+        ws_bytes = int(L.spcn_xform_workspace_bytes(int(npix)))
+        ws = _dev.workspace(ws_bytes, stream=_lib.stream_handle(stream))
+        _lib.check(L.spcn_xform_calibrate_part(ctypes.byref(self.params), int(part), int(nparts),
+                                               _lib.ptr(ws), ws_bytes, _lib.stream_handle(stream)),
+                   "xform_calibrate_part")
+        reduce_max(ws[8:12].view(_dev.torch().int32))
+        self.params.cert_alpha = CALIBRATE_DEVICE
 
     def run(self, src, dst, npix: int, stream=None) -> None:
         """src/dst: CUDA uint8 tensors (or raw device pointers) holding npix RGB pixels."""

@@ -69,3 +69,71 @@ def test_rowband_fit_equals_single_process(mode):
         assert np.array_equal(np.array(basis), ref.basis), rank
         assert p99 == ref.stats.p99.tolist(), rank
         assert count == ref.stats.sample_count, rank
+
+
+def _xform_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200 import distributed as dd, synthetic
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        W, H = 4096, 4096                      # >= 2^24 px: the EXACT bound is calibrated
+        full = synthetic.render_slide(W, H, 5, tissue_fraction=0.6)
+        tgt = pb.fit(pb.DeviceSource(synthetic.render_slide(1024, 1024, 6, tissue_fraction=0.6)))
+        src_fp = pb.fit(pb.DeviceSource(full))
+        r0, rows = rank * (H // world), H // world
+        band = full[r0:r0 + rows].contiguous()
+        g = dd.RowBandGroup(W, H, r0, rows)
+        sink = pb.DeviceWriter(W, rows)
+        g.transform(pb.DeviceSource(band), src_fp, tgt, sink)
+        ref = pb.DeviceWriter(W, H)
+        pb.transform(pb.DeviceSource(full), src_fp, tgt, ref)   # one full calibration
+        q.put((rank, bool(torch.equal(sink.pixels, ref.pixels[r0:r0 + rows]))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rowband_transform_with_split_calibration():
+    """Each rank calibrates 1/N of the colours, one max all-reduce: the bands
+    are byte-identical to the single-process transform."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_xform_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(ok for _, ok in out), out
+
+
+def test_calibration_parts_max_equals_full():
+    import ctypes
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200 import _dev, _lib
+    from paper_1901_03088_b200.xform import XformPlan
+    from oracle import spcn_oracle as orc
+
+    w = orc.he_basis()
+    plan = XformPlan([250.0, 243.0, 247.0], w, 0.0, [1.1, 0.9], w, [255.0, 255.0, 255.0])
+    full = plan.calibrate()
+    words = []
+    for part in range(3):
+        box = {}
+
+        def grab(word, box=box):
+            box["w"] = int(word.cpu()[0])
+        p2 = XformPlan([250.0, 243.0, 247.0], w, 0.0, [1.1, 0.9], w, [255.0, 255.0, 255.0])
+        p2.calibrate_shared(1 << 24, 1 << 20, part, 3, grab)
+        words.append(box["w"])
+    worst = np.array([max(words)], dtype=np.uint32).view(np.float32)[0]
+    assert float(worst) * (1.0 + 2.0 ** -20) == full, (worst, full)   # spcn_xform_calibrate's alpha
