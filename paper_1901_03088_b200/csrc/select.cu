@@ -8,6 +8,8 @@
 // construction (integer counting), so percentile-histogram counts are
 // bit-exact given identical densities.
 #include "select.h"
+
+#include <cooperative_groups.h>
 #include "launch_count.h"
 #include "spcn_device.cuh"
 
@@ -288,6 +290,149 @@ __global__ void __launch_bounds__(kSelThreads) k_p99_seg(const double* __restric
   }
 }
 
+// k_p99_seg_cluster: the same three passes for ONE large segment (the
+// single-slide fit's 100 k samples) on a cluster of kCl CTAs per stain: every
+// CTA streams 1/kCl of the values; the max, the window histogram (each CTA
+// sums 1/kCl of the bins across the cluster through distributed shared
+// memory) and the candidate list are combined in CTA 0's shared memory, which
+// then runs the radix select.  Same bins, same candidates, same select as
+// k_p99_seg — with kCl times the streaming parallelism.
+constexpr int kCl = 8;
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads)
+    k_p99_seg_cluster(const double* __restrict__ h, int64_t total,
+                      const int64_t* __restrict__ seg, double p, double* __restrict__ sel) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  SegShared& sh = *reinterpret_cast<SegShared*>(smem_raw);
+  __shared__ unsigned long long s_mx;
+  __shared__ int s_go, s_b1, s_b2;
+  __shared__ long long s_r1, s_r2;
+  const int cr = (int)cl.block_rank();
+  const int idx = blockIdx.x / kCl, s = idx >> 1, j = idx & 1;
+  const int64_t b = seg[s], e = seg[s + 1], n = e - b;
+  if (n <= 0) {                                    // uniform over the cluster
+    if (cr == 0 && threadIdx.x < 3) sel[3 * idx + threadIdx.x] = 0.0;
+    return;
+  }
+  const double* v = h + j * total + b;
+  SegShared& sh0 = *cl.map_shared_rank(&sh, 0);
+  const int64_t i0 = (int64_t)cr * kSelThreads + threadIdx.x, step = (int64_t)kCl * kSelThreads;
+  // pass 1: the max key (per CTA, then across the cluster)
+  uint64_t mx = 0;
+  for (int64_t i = i0; i < n; i += step) {
+    const uint64_t key = key_of(v[i]);
+    mx = key > mx ? key : mx;
+  }
+  for (int off = 16; off; off >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, mx, off);
+    mx = o > mx ? o : mx;
+  }
+  if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5] = mx;
+  for (int i = threadIdx.x; i < kTopBins; i += kSelThreads) sh.hist[i] = 0;
+  if (threadIdx.x == 0) sh.ncand = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kSelThreads / 32; ++w) mx = sh.red[w] > mx ? sh.red[w] : mx;
+    s_mx = mx;
+  }
+  cl.sync();
+  mx = 0;
+  for (int r = 0; r < kCl; ++r) {
+    const uint64_t o = *cl.map_shared_rank(&s_mx, r);
+    mx = o > mx ? o : mx;
+  }
+  // pass 2: window histogram, per CTA, then summed bin-slice by bin-slice into
+  // CTA 0's candidate area (free until pass 3) and copied to its histogram
+  constexpr uint64_t kWin = (uint64_t)(kTopBins - 1) << kWinShift;
+  for (int64_t i = i0; i < n; i += step) {
+    const uint64_t d = mx - key_of(v[i]);
+    if (d < kWin) atomicAdd(&sh.hist[(uint32_t)(d >> kWinShift)], 1u);
+  }
+  cl.sync();
+  uint32_t* sum0 = reinterpret_cast<uint32_t*>(sh0.cand);
+  for (int bin = cr * kSelThreads + threadIdx.x; bin < kTopBins; bin += kCl * kSelThreads) {
+    uint32_t c = 0;
+    for (int r = 0; r < kCl; ++r) c += cl.map_shared_rank(sh.hist, r)[bin];
+    sum0[bin] = c;
+  }
+  cl.sync();
+  const double rank = __dmul_rn(p / 100.0, (double)(n - 1));
+  const int64_t klo = (int64_t)floor(rank), khi = (int64_t)ceil(rank);
+  const int64_t rt_hi = n - 1 - khi, rt_lo = n - 1 - klo;   // ranks from the top
+  if (cr == 0) {
+    const uint32_t* sum = reinterpret_cast<const uint32_t*>(sh.cand);
+    uint32_t inwin = 0;
+    for (int i = threadIdx.x; i < kTopBins; i += kSelThreads) {
+      sh.hist[i] = sum[i];
+      inwin += sum[i];
+    }
+    for (int off = 16; off; off >>= 1) inwin += __shfl_xor_sync(0xffffffffu, inwin, off);
+    if ((threadIdx.x & 31) == 0) sh.scan[threadIdx.x >> 5] = inwin;
+    __syncthreads();
+    inwin = 0;
+    for (int w = 0; w < kSelThreads / 32; ++w) inwin += sh.scan[w];
+    __syncthreads();
+    int go = 0;
+    if ((int64_t)inwin > rt_lo) {
+      hist_locate(sh, kTopBins, rt_hi);
+      const int b1 = sh.loc_bin;
+      const int64_t r1 = sh.loc_rank;
+      __syncthreads();
+      hist_locate(sh, kTopBins, rt_lo);
+      const int b2 = sh.loc_bin;
+      const int64_t r2 = sh.loc_rank;
+      int64_t ncand = 0, before2 = 0;
+      for (int t = b1; t <= b2; ++t) {
+        if (t == b2) before2 = ncand;
+        ncand += sh.hist[t];
+      }
+      if (ncand <= kCand) {
+        go = 1;
+        if (threadIdx.x == 0) {
+          s_b1 = b1;
+          s_b2 = b2;
+          s_r1 = r1;
+          s_r2 = before2 + r2;
+          sh.ncand = 0;
+        }
+      }
+    }
+    if (threadIdx.x == 0) s_go = go;
+  }
+  cl.sync();
+  const int go = *cl.map_shared_rank(&s_go, 0);
+  if (go) {
+    // pass 3: every CTA appends the keys of bins b1..b2 to CTA 0's list
+    const int b1 = *cl.map_shared_rank(&s_b1, 0), b2 = *cl.map_shared_rank(&s_b2, 0);
+    const uint64_t dlo = (uint64_t)b1 << kWinShift, dhi = ((uint64_t)(b2 + 1) << kWinShift);
+    for (int64_t i = i0; i < n; i += step) {
+      const uint64_t key = key_of(v[i]);
+      const uint64_t d = mx - key;
+      if (d >= dlo && d < dhi) sh0.cand[atomicAdd(&sh0.ncand, 1u)] = key;
+    }
+  }
+  cl.sync();
+  if (cr != 0) return;
+  uint64_t klo_key, khi_key;
+  if (go) {
+    const int64_t ncand = sh.ncand;
+    const auto src = [&](int64_t i) -> uint64_t { return sh.cand[i]; };
+    khi_key = radix_select(sh, src, ncand, ncand - 1 - s_r1);
+    klo_key = radix_select(sh, src, ncand, ncand - 1 - s_r2);
+  } else {
+    const auto src = [&](int64_t i) -> uint64_t { return key_of(v[i]); };
+    klo_key = radix_select(sh, src, n, klo);
+    khi_key = radix_select(sh, src, n, khi);
+  }
+  if (threadIdx.x == 0) {
+    sel[3 * idx] = val_of(klo_key);
+    sel[3 * idx + 1] = val_of(khi_key);
+    sel[3 * idx + 2] = val_of(mx);
+  }
+}
+
 __global__ void k_p99_combine(const int64_t* __restrict__ seg, int nseg, double p,
                               const double* __restrict__ sel, double* __restrict__ p99,
                               int32_t* __restrict__ absent) {
@@ -344,7 +489,21 @@ cudaError_t launch_p99(const double* h, int64_t total, const int64_t* seg, int n
     attr = true;
   }
   (void)qbuf;
-  k_p99_seg<<<n2, kSelThreads, sizeof(SegShared), st>>>(h, total, seg, p, selbuf);
+  static bool attr_cl = false;
+  if (!attr_cl) {
+    const cudaError_t e0 = cudaFuncSetAttribute(k_p99_seg_cluster,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)sizeof(SegShared));
+    if (e0 != cudaSuccess) return e0;
+    attr_cl = true;
+  }
+  // a single large segment (one slide's sample) is latency-bound on one CTA
+  // per stain: spread it over a cluster; many segments keep one CTA each
+  if (nseg == 1) {
+    k_p99_seg_cluster<<<n2 * kCl, kSelThreads, sizeof(SegShared), st>>>(h, total, seg, p, selbuf);
+  } else {
+    k_p99_seg<<<n2, kSelThreads, sizeof(SegShared), st>>>(h, total, seg, p, selbuf);
+  }
   cudaError_t e = launched();
   if (e != cudaSuccess) return e;
   k_p99_combine<<<(n2 + 127) / 128, 128, 0, st>>>(seg, nseg, p, selbuf, p99, absent);
