@@ -211,30 +211,54 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
 
 // Exact 80th percentile of 8-bit pools from their 256-bin counts
 // (percentile src/order_stats.py:27-36 on the expanded multiset).
+// One warp per (problem, channel): 8 bins per lane, a warp prefix sum finds
+// the bins holding ranks lo and hi (exact integer counting).
 __global__ void k_i0_from_hist(const int32_t* __restrict__ hist, int nprob,
                                double* __restrict__ i0, int32_t* __restrict__ empty) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= nprob * 3) return;
-  const int32_t* h = hist + (int64_t)idx * 256;
-  int64_t n = 0;
-  for (int v = 0; v < 256; ++v) n += h[v];
+  const int idx = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (idx >= nprob * 3) return;                       // whole warps
+  const int32_t* h = hist + (int64_t)idx * 256 + lane * 8;
+  int64_t c[8], tot = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    c[b] = h[b];
+    tot += c[b];
+  }
+  int64_t incl = tot;
+  for (int off = 1; off < 32; off <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  const int64_t n = __shfl_sync(0xffffffffu, incl, 31);
   if (n == 0) {
-    i0[idx] = 255.0;
-    empty[idx] = 1;
+    if (lane == 0) {
+      i0[idx] = 255.0;
+      empty[idx] = 1;
+    }
     return;
   }
-  empty[idx] = 0;
   const double rank = __dmul_rn(80.0 / 100.0, (double)(n - 1));
   const int64_t lo = (int64_t)floor(rank), hi = (int64_t)ceil(rank);
-  int64_t cum = 0;
-  int lov = -1, hiv = -1;
-  for (int v = 0; v < 256 && hiv < 0; ++v) {
-    cum += h[v];
-    if (lov < 0 && cum > lo) lov = v;
-    if (cum > hi) hiv = v;
+  // the first value whose cumulative count exceeds the rank
+  int lov = 256, hiv = 256;
+  int64_t cum = incl - tot;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const int64_t before = cum;
+    cum += c[b];
+    if (before <= lo && cum > lo) lov = lane * 8 + b;
+    if (before <= hi && cum > hi) hiv = lane * 8 + b;
   }
-  const double frac = __dsub_rn(rank, (double)lo);
-  i0[idx] = __dadd_rn((double)lov, __dmul_rn(__dsub_rn((double)hiv, (double)lov), frac));
+  for (int off = 16; off; off >>= 1) {
+    lov = min(lov, __shfl_xor_sync(0xffffffffu, lov, off));
+    hiv = min(hiv, __shfl_xor_sync(0xffffffffu, hiv, off));
+  }
+  if (lane == 0) {
+    empty[idx] = 0;
+    const double frac = __dsub_rn(rank, (double)lo);
+    i0[idx] = __dadd_rn((double)lov, __dmul_rn(__dsub_rn((double)hiv, (double)lov), frac));
+  }
 }
 
 // Per-problem OD tables ln(i0_c / clip(i, 1, i0_c)) (src/optics.py:92-94).
@@ -270,7 +294,7 @@ cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches,
 cudaError_t launch_i0_from_hist(const int32_t* hist, int nprob, double* i0, int32_t* empty,
                                 cudaStream_t st) {
   if (nprob <= 0) return cudaSuccess;
-  k_i0_from_hist<<<(nprob * 3 + 127) / 128, 128, 0, st>>>(hist, nprob, i0, empty);
+  k_i0_from_hist<<<(nprob * 3 + 3) / 4, 128, 0, st>>>(hist, nprob, i0, empty);   // warp per pool
   return launched();
 }
 
