@@ -29,7 +29,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _dev, _lib
+from . import _lib
 
 CHUNK = 4096
 

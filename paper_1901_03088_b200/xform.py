@@ -10,7 +10,6 @@ from __future__ import annotations
 
 import ctypes
 
-import numpy as np
 
 from . import _dev, _lib
 from .optics import od_table
