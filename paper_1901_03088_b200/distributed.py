@@ -252,9 +252,32 @@ class RowBandGroup:
         offsets = torch.tensor([0, m], dtype=torch.int64, device=dev)
         flat = sample.reshape(-1)
         r = snmf.snmf_batched(flat, offsets, lut, cfg, cluster=8 if m >= 20_000 else 1)
+        h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
+        if p99_mode == "sample" and not per_patch_stats:
+            # basis, SNMF info, pooled p99 and the absent flags in ONE read
+            # (as pipeline.fit)
+            from . import stats as dstats
+            from .errors import StainAbsentError
+            from .normalize import _STAIN_NAMES, StainStats
+
+            vals, absent = dstats.segment_percentiles(h, offsets, 99.0)
+            packed = torch.cat([r.basis.reshape(-1), r.info.reshape(-1).to(torch.float64),
+                                vals.reshape(-1), absent.reshape(-1).to(torch.float64)]).cpu().numpy()
+            basis, info = packed[:6].reshape(3, 2).copy(), packed[6:10].astype(np.int64)
+            snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
+            for j in range(2):
+                if packed[12 + j]:
+                    raise StainAbsentError(f"density stats: stain absent: no {_STAIN_NAMES[j]} "
+                                           "density observed")
+            p99 = packed[10:12].copy()
+            if not (np.isfinite(p99).all() and (p99 >= 0).all()):
+                raise ValueError(f"density stats: p99 must be finite and non-negative, got {p99}")
+            fields = _cfg_fields(plan, cfg, code_lam, per_patch_stats)
+            prov = {"source": str(source_label), "config_hash": config_hash(fields)}
+            return FitParams(i0=i0, basis=basis, stats=StainStats(p99=p99, sample_count=m),
+                             provenance=prov)
         info = r.info.cpu().numpy()[0]
         snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
-        h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
         if p99_mode == "global":
             from .global_stats import global_p99, sample_bracket
             from .normalize import StainStats
