@@ -200,7 +200,7 @@ class RowBandGroup:
         dev = img.device
         present = [i for i, p in enumerate(parts) if p is not None]
         chunks = max([1] + [-(-(p[1] * p[2]) // CHUNK) for p in parts if p is not None])
-        local_tot = np.zeros((ncand, 4), dtype=np.int64)
+        lt = torch.zeros((ncand, 4), dtype=torch.int64, device=dev)
         cnt_dev = None
         if present:
             desc = np.array([(parts[i][0], parts[i][1], parts[i][2], W) for i in present],
@@ -209,11 +209,10 @@ class RowBandGroup:
             cnt_dev = torch.empty((len(present), chunks, 4), dtype=torch.int32, device=dev)
             _lib.check(L.spcn_sample_count(_lib.ptr(img), _lib.ptr(d), len(present), chunks, thr,
                                            _lib.ptr(cnt_dev), _lib.stream_handle()), "sample_count")
-            local_tot[present] = cnt_dev.sum(dim=1).cpu().numpy()
-        # all-gather of per-rank totals (ranks in band order)
-        lt = torch.from_numpy(local_tot).to(dev)
+            lt[torch.tensor(present, dtype=torch.int64, device=dev)] = cnt_dev.sum(dim=1).to(torch.int64)
+        # all-gather of per-rank totals (ranks in band order), one host read
         gathered = all_gather_list(lt, self.group)
-        per_rank = np.stack([g.cpu().numpy() for g in gathered])
+        per_rank = torch.stack([g.to(dev) for g in gathered]).cpu().numpy()
         glob = per_rank.sum(axis=0)
         takes, used_counts, collected, visited, used = _visit(
             plan, order[:ncand], rects, lambda k: tuple(int(v) for v in glob[k]))
