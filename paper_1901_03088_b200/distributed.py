@@ -219,8 +219,12 @@ class RowBandGroup:
         if collected == 0:
             raise BlankSlideError("sampling: blank slide: no non-white pixels found in any "
                                   "sampled patch")
-        sample = torch.zeros((collected, 3), dtype=torch.uint8, device=dev)
-        hist = torch.zeros((1, 3, 256), dtype=torch.int32, device=dev)
+        # sample bytes and bright histograms in ONE int32 buffer, one all-reduce:
+        # each sample byte has a single writer, so word sums are byte sums
+        nw = -(-3 * collected // 4)
+        buf = torch.zeros(nw + 3 * 256, dtype=torch.int32, device=dev)
+        sample = buf[:nw].view(torch.uint8)[:3 * collected].view(collected, 3)
+        hist = buf[nw:].view(1, 3, 256)
         mine = [tk for tk in split_takes(takes, per_rank, rank) if parts[tk[0]] is not None]
         if mine:
             pos = {c: j for j, c in enumerate(present)}
@@ -238,8 +242,7 @@ class RowBandGroup:
                                              _lib.ptr(cnt), _lib.ptr(dt), _lib.ptr(sample),
                                              _lib.ptr(hist), _lib.stream_handle()),
                        "sample_compact")
-        all_reduce_sum(sample, self.group)     # disjoint writers: sum == gather
-        all_reduce_sum(hist, self.group)
+        all_reduce_sum(buf, self.group)        # disjoint sample writers: sum == gather
         # --- identical, deterministic fit on every rank
         m = collected
         i0 = _stage("background estimation", optics.i0_from_counts,
