@@ -215,7 +215,7 @@ def sample_bracket(h, p: float = 99.0):
     q = p / 100.0
     d = max(0.005, 6.0 * math.sqrt(q * (1.0 - q) / m) * 10.0)
     idx = [int(math.floor(max(0.0, q - d) * (m - 1))), int(math.ceil(min(1.0, q + d) * (m - 1)))]
-    t = _dev.torch()
+    import torch as t   # tensor plumbing on h's device
     srt = t.sort(h, dim=1).values
     return srt[:, t.tensor(idx, device=h.device)].cpu().numpy()
 

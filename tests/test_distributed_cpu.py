@@ -313,3 +313,19 @@ def test_global_p99_two_ranks_gloo():
     for rank, p99, cnt in out:
         assert cnt == n
         assert p99 == ref, (rank, p99, ref)
+
+
+def test_sample_bracket_contains_the_percentile():
+    import torch
+
+    from paper_1901_03088_b200.global_stats import sample_bracket
+
+    rng = np.random.default_rng(5)
+    h = np.stack([rng.gamma(2.0, 0.4, 100_000), rng.gamma(1.5, 0.3, 100_000)])
+    br = sample_bracket(torch.from_numpy(h))
+    assert br.shape == (2, 2)
+    for j in range(2):
+        p = orc.pct(h[j], 99.0)
+        assert br[j, 0] <= p <= br[j, 1]
+        assert br[j, 0] > 0
+    assert sample_bracket(torch.zeros((2, 0), dtype=torch.float64)) is None
