@@ -41,12 +41,12 @@ def tb(*a, **k):
 
 
 batch.fit_batch, batch.transform_batch = fb, tb
-for chunk in (512, 512, 512, 1024, 1024, 1024):
+for chunk in (256, 256, 256):
     torch.cuda.synchronize()
     log.clear()
     m0 = torch.cuda.memory_stats()
     t0[0] = time.perf_counter()
-    pb.normalize_batch_host(host, target, out, chunk=chunk, streams=4)
+    pb.normalize_batch_host(host, target, out, chunk=chunk, streams=6)
     torch.cuda.synchronize()
     m1 = torch.cuda.memory_stats()
     print(f"chunk {chunk}: total {(time.perf_counter() - t0[0]) * 1e3:.1f} ms  cudaMalloc "
