@@ -174,8 +174,9 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
     empty = t.empty((n, 3), dtype=t.int32, device=dev)
     _lib.check(L.spcn_i0_from_hist(_lib.ptr(hist), n, _lib.ptr(i0), _lib.ptr(empty),
                                    _lib.stream_handle()), "i0_from_hist")
-    i0_h = _dev.readback(i0)
-    if _dev.readback(empty).any():
+    ie = _dev.readback(t.cat([i0.reshape(-1), empty.reshape(-1).to(t.float64)]))   # one read
+    i0_h = ie[:3 * n].reshape(n, 3)
+    if ie[3 * n:].any():
         warnings.warn("some items had no pixels brighter than the white threshold in a "
                       "channel; their i0 fell back to 255", optics.BackgroundEstimateWarning,
                       stacklevel=2)
@@ -194,10 +195,11 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
 
         h = snmf.code_samples(flat, d_off, luts, r.basis, code_lam, mmax)
         p99, absent = dstats.segment_percentiles(h, d_off, 99.0)
-    absent_h = _dev.readback(absent).any(axis=1)
+    ai = _dev.readback(t.cat([absent.reshape(-1), r.info.reshape(-1)]))   # one read
+    absent_h = ai[:2 * n].reshape(n, 2).any(axis=1)
+    info = ai[2 * n:].reshape(n, -1)
     status[(status == 0) & absent_h] = -_lib.SPCN_ESTAIN_ABSENT
     prov = {"source": "", "config_hash": config_hash(_cfg_fields(plan, cfg, code_lam, False))}
-    info = _dev.readback(r.info)
     return BatchFit(i0=i0, basis=r.basis, p99=p99, luts=luts, count=collected, status=status,
                     provenance=prov, iterations=info[:, 0].copy(), converged=info[:, 1] != 0,
                     warn_flags=info[:, 2].copy())
