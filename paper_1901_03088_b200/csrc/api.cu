@@ -449,7 +449,7 @@ int spcn_snmf_batched(const uint8_t* samples, const double* od, const int64_t* o
   if (!(cfg->lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
   if (cfg->max_outer < 1) return fail(SPCN_EINVAL, "max_outer_iters must be >= 1");
   if (!(cfg->rel_tol > 0.0)) return fail(SPCN_EINVAL, "rel_tol must be > 0");
-  if (cfg->cluster < 1 || cfg->cluster > 8) return fail(SPCN_EINVAL, "cluster must be in [1, 8]");
+  if (cfg->cluster < 1 || cfg->cluster > 16) return fail(SPCN_EINVAL, "cluster must be in [1, 16]");
   if (nprob == 0) return SPCN_OK;
   if ((!od && (!samples || !luts)) || !offsets || !basis_out || !history_out || !info_out)
     return fail(SPCN_EINVAL, "NULL argument");

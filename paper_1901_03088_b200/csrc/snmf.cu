@@ -457,6 +457,9 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_snmf<512, 1>, 512, 0);
+    // clusters of up to 16 CTAs (non-portable size) for one slide's fit
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_snmf<512, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) {
       sms = 0;
       return e;

@@ -253,7 +253,7 @@ class RowBandGroup:
                 f"basis fit: insufficient pixels: need at least 10 OD samples, got {m}")
         offsets = torch.tensor([0, m], dtype=torch.int64, device=dev)
         flat = sample.reshape(-1)
-        r = snmf.snmf_batched(flat, offsets, lut, cfg, cluster=8 if m >= 20_000 else 1)
+        r = snmf.fit_slide(flat, offsets, lut, cfg, m)
         h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
         if p99_mode == "sample" and not per_patch_stats:
             # basis, SNMF info, pooled p99 and the absent flags in ONE read

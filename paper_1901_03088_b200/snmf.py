@@ -106,6 +106,25 @@ def code_samples(samples, offsets, luts, bases, lam, max_m, max_sweeps=2000):
     return h
 
 
+_BIG_CLUSTER = [16]   # one slide's fit: clusters of 16 CTAs (non-portable), else 8
+
+
+def fit_slide(samples, offsets, luts, cfg, m: int, od=None) -> BatchFit:
+    """snmf_batched for ONE slide's sample: a thread-block cluster of 16 CTAs
+    (8 if the device cannot schedule 16) from 20 k samples, else one CTA.
+    The cluster size fixes the reduction order, so every caller (single
+    process, row-band ranks) uses this rule."""
+    if m < 20_000:
+        return snmf_batched(samples, offsets, luts, cfg, cluster=1, od=od)
+    while True:
+        try:
+            return snmf_batched(samples, offsets, luts, cfg, cluster=_BIG_CLUSTER[0], od=od)
+        except RuntimeError:
+            if _BIG_CLUSTER[0] == 8:
+                raise
+            _BIG_CLUSTER[0] = 8      # 16-CTA clusters unavailable here
+
+
 def code_table(table, offsets, luts, bases, lam, max_m, total, max_sweeps=2000):
     """code_samples over the colour table of ``snmf_batched`` (one fp64
     evaluation per distinct colour) → CUDA (2, total) float64, valid at the
@@ -163,7 +182,7 @@ def fit_basis(od_sample, cfg):
     if m < 10:
         raise InsufficientPixelsError(f"insufficient pixels: need at least 10 OD samples, got {m}")
     offsets = t.tensor([0, m], dtype=t.int64, device=v.device)
-    r = snmf_batched(None, offsets, None, cfg, cluster=8 if m >= 20_000 else 1, od=v.contiguous())
+    r = fit_slide(None, offsets, None, cfg, m, od=v.contiguous())
     info = r.info.cpu().numpy()[0]
     hist = r.history.cpu().numpy()[0][: int(info[3])]
     warn_flags(m, int(info[2]), cfg.max_outer_iters)
