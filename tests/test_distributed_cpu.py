@@ -329,3 +329,24 @@ def test_sample_bracket_contains_the_percentile():
         assert br[j, 0] <= p <= br[j, 1]
         assert br[j, 0] > 0
     assert sample_bracket(torch.zeros((2, 0), dtype=torch.float64)) is None
+
+
+def test_fit_slide_cluster_choice_and_fallback(monkeypatch):
+    """One slide's SNMF: one CTA below 20 k samples, a 16-CTA cluster above,
+    and a sticky fall-back to 8 when 16-CTA clusters cannot be launched."""
+    from paper_1901_03088_b200 import snmf
+
+    calls = []
+
+    def fake(samples, offsets, luts, cfg, cluster=1, od=None):
+        calls.append(cluster)
+        if cluster == 16:
+            raise RuntimeError("cluster too large")
+        return cluster
+
+    monkeypatch.setattr(snmf, "snmf_batched", fake)
+    monkeypatch.setattr(snmf, "_BIG_CLUSTER", [16])
+    assert snmf.fit_slide(None, None, None, None, 1_000) == 1
+    assert snmf.fit_slide(None, None, None, None, 50_000) == 8
+    assert snmf.fit_slide(None, None, None, None, 50_000) == 8
+    assert calls == [1, 16, 8, 8]
