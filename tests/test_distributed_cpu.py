@@ -350,3 +350,30 @@ def test_fit_slide_cluster_choice_and_fallback(monkeypatch):
     assert snmf.fit_slide(None, None, None, None, 50_000) == 8
     assert snmf.fit_slide(None, None, None, None, 50_000) == 8
     assert calls == [1, 16, 8, 8]
+
+
+def test_host_copy_helpers():
+    """pipeline._pcopy (threaded multi-MB copies) and batch._sliced_copy
+    (copies in <= 64 MB pieces) are plain copies."""
+    import torch
+
+    from paper_1901_03088_b200 import batch, pipeline
+
+    rng = np.random.default_rng(3)
+    src = rng.integers(0, 256, (1500, 1200, 3), dtype=np.uint8)     # 5.4 MB: threaded path
+    dst = np.empty_like(src)
+    pipeline._pcopy(dst, src)
+    assert np.array_equal(dst, src)
+    small = src[:10]
+    d2 = np.empty_like(small)
+    pipeline._pcopy(d2, small)
+    assert np.array_equal(d2, small)
+    t_src = torch.from_numpy(rng.integers(0, 256, (37, 64, 64, 3), dtype=np.uint8))
+    t_dst = torch.empty_like(t_src)
+    old = batch._SLICE_BYTES
+    try:
+        batch._SLICE_BYTES = 5 * 64 * 64 * 3          # pieces of 5 items
+        batch._sliced_copy(t_dst, t_src, False)
+    finally:
+        batch._SLICE_BYTES = old
+    assert torch.equal(t_dst, t_src)
