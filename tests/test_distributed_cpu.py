@@ -377,3 +377,36 @@ def test_host_copy_helpers():
     finally:
         batch._SLICE_BYTES = old
     assert torch.equal(t_dst, t_src)
+
+
+def _max_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1901_03088_b200 import distributed as dd
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # the calibration word: bits of a non-negative float, max-reduced as int32
+        w = torch.tensor(np.array([0.5e-6 * (rank + 1)], dtype=np.float32).view(np.int32))
+        dd.all_reduce_max(w)
+        q.put((rank, float(w.numpy().view(np.float32)[0])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_all_reduce_max_of_float_bits_two_ranks():
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_max_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in ps:
+        pr.start()
+    got = [q.get(timeout=120) for _ in ps]
+    for pr in ps:
+        pr.join(timeout=60)
+    want = float(np.float32(1.0e-6))
+    assert all(v == want for _, v in got), got
