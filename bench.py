@@ -28,7 +28,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -56,7 +55,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-workers", type=int, default=3, help="CUDA streams of the host transform")
-    ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the CPU-baseline band")
+    ap.add_argument("--cpu-rows", type=int, default=0,
+                    help="rows of the CPU-baseline band (default: 4 strips of 64 rows per core)")
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
                     help="gloo: functional check of the N>1 path on one GPU (not a measurement)")
     ap.add_argument("--no-global-line", action="store_true",
@@ -76,43 +76,57 @@ def parse():
 
 
 # --------------------------------------------------------------------------- clocks
-class Clocks(threading.Thread):
-    """NVML sampler (SM clock, throttle reasons) for the timed region."""
+_REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+            0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
-               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index: int, period: float = 0.01):
-        super().__init__(daemon=True)
+def _clock_loop(index, period, halt, q):
+    """NVML sampling loop (child process: never starved by the parent's GIL)."""
+    samples, reasons, max_mhz = [], set(), None
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not halt.is_set():
+            samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for bit, name in _REASONS.items():
+                if mask & bit:
+                    reasons.add(name)
+            time.sleep(period)
+    except Exception as exc:  # pragma: no cover - NVML missing
+        reasons.add(f"nvml-unavailable: {exc}")
+    q.put((samples, sorted(reasons), max_mhz))
+
+
+class Clocks:
+    """NVML sampler (SM clock, throttle reasons) over the timed region, in a
+    forked child process sampling every `period` seconds."""
+
+    def __init__(self, index: int, period: float = 0.005):
+        import multiprocessing as mp
+
         self.index, self.period = index, period
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._halt = threading.Event()
-        self.ok = True
+        self._ctx = mp.get_context("fork")
+        self._halt, self._q, self._p = self._ctx.Event(), self._ctx.Queue(), None
 
-    def run(self):
-        try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            while not self._halt.is_set():
-                self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
-                mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit:
-                        self.reasons.add(name)
-                time.sleep(self.period)
-        except Exception as exc:  # pragma: no cover - NVML missing
-            self.ok = False
-            self.reasons.add(f"nvml-unavailable: {exc}")
+    def start(self):
+        self._p = self._ctx.Process(target=_clock_loop,
+                                    args=(self.index, self.period, self._halt, self._q),
+                                    daemon=True)
+        self._p.start()
 
     def stop(self):
         self._halt.set()
-        self.join(timeout=2)
-        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+        try:
+            samples, reasons, max_mhz = self._q.get(timeout=10)
+        except Exception:  # pragma: no cover
+            samples, reasons, max_mhz = [], ["sampler-lost"], None
+        self._p.join(timeout=5)
+        return {"sm_mhz": float(statistics.median(samples)) if samples else None,
+                "sm_max_mhz": max_mhz, "reasons": reasons, "samples": len(samples)}
 
 
 # --------------------------------------------------------------------------- distributed
@@ -155,20 +169,39 @@ def band_of(height, rank, world):
 
 
 # --------------------------------------------------------------------------- CPU baseline
-def cpu_reference_run(band: np.ndarray, target: dict, cores: int, repeats: int = 1):
-    """Time the reference algorithm (oracle port) on a host band: fit + transform."""
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def cpu_band_rows(cores: int, strip: int = 64, per_core: int = 4) -> int:
+    """Rows of the CPU-baseline band: per_core strips of `strip` rows per host
+    core, so every worker of the reference's pool stays busy (src/pipeline.py
+    :311-315 keeps at most `workers` strips in flight)."""
+    return per_core * cores * strip
+
+
+def cpu_reference_run(band: np.ndarray, target: dict, cores: int, strips=(64,)):
+    """Time the reference algorithm (oracle port) on a host band: one fit, then
+    one transform per strip height.  Returns (t_fit, {strip: t_transform})."""
     from oracle import spcn_oracle as orc
 
-    t_fit, t_x = [], []
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        fp = orc.fit_params(band)
+    t0 = time.perf_counter()
+    fp = orc.fit_params(band)
+    t_fit = time.perf_counter() - t0
+    t_x = {}
+    for sh in strips:
         t1 = time.perf_counter()
-        orc.run_transform(band, fp, target, strip_height=64, workers=cores)
-        t2 = time.perf_counter()
-        t_fit.append(t1 - t0)
-        t_x.append(t2 - t1)
-    return min(t_fit), min(t_x)
+        orc.run_transform(band, fp, target, strip_height=sh, workers=cores)
+        t_x[sh] = time.perf_counter() - t1
+    return t_fit, t_x
 
 
 def extrapolated_mpx(total_px, band_px, t_fit, t_x):
@@ -177,40 +210,56 @@ def extrapolated_mpx(total_px, band_px, t_fit, t_x):
     return total_px / (t_fit + t_x * total_px / band_px) / 1e6
 
 
+def cpu_sample_desc(rows, width, cores, t_fit, t_x, total):
+    band_px = rows * width
+    parts = ", ".join(f"strip {sh}: {band_px / t / 1e6:.1f} Mpx/s ({t:.2f} s, "
+                      f"{-(-rows // sh)} strips)" for sh, t in sorted(t_x.items()))
+    return (f"{rows} x {width} band ({band_px / 1e6:.0f} Mpx) of the same synthetic model, "
+            f"reference algorithm (oracle port, NumPy) on {cores} threads of "
+            f"'{cpu_model()}': fit {t_fit:.3f} s; transform {parts}; value = one fit + the "
+            f"strip-64 transform (the faster CPU setting) extrapolated linearly in pixels "
+            f"(criterion 10) to the whole {total / 1e9:.2f} Gpx: "
+            f"{t_fit + t_x[64] * total / band_px:.0f} s")
+
+
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
+    """The reference's CPU path on the box's host cores: each step = fit + transform
+    (strip 64, all cores) of a bounded band of the workload (4 strips per core);
+    one extra strip-1024 transform (the reference default) is reported beside it."""
     if rank != 0:
         return 0
     from oracle import spcn_oracle as orc
 
     cores = os.cpu_count() or 1
-    rows = max(16, args.cpu_rows)
-    band, _, _ = orc.render(args.width, rows, args.seed, tissue_fraction=args.tissue,
-                            layout=args.layout)
+    rows = min(args.height, max(64, args.cpu_rows or cpu_band_rows(cores)))
+    band = orc.render_band(args.width, args.height, args.seed, rows, tissue_fraction=args.tissue,
+                           layout=args.layout)
     tgt_px, _, _ = orc.render(1024, 1024, args.seed + 1, tissue_fraction=0.6)
     target = orc.fit_params(tgt_px)
     total = args.width * args.height
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        cpu_reference_run(band, target, cores)
+    if args.warmup:            # warm thread pools / allocator on a small piece
+        cpu_reference_run(band[:min(rows, 4 * 64)], target, cores)
+    steps = max(1, min(args.steps, 2))
     times = []
-    for _ in range(args.steps if args.steps < 5 else 3):
+    for _ in range(steps):
         tf, tx = cpu_reference_run(band, target, cores)
-        times.append((tf, tx))
-    tf = statistics.median(t[0] for t in times)
-    tx = statistics.median(t[1] for t in times)
-    value = extrapolated_mpx(total, band.shape[0] * band.shape[1], tf, tx)
-    step_ms = (tf + tx * total / (band.shape[0] * band.shape[1])) * 1e3
-    sample = (f"{rows} x {args.width} band ({rows * args.width / 1e6:.1f} Mpx) of the same "
-              f"synthetic model rendered by the oracle; per step fit(band) "
-              f"{tf:.3f} s + transform(band, workers={cores}, strip 64) {tx:.3f} s, "
-              f"extrapolated linearly to {total / 1e9:.2f} Gpx")
+        times.append(tf + tx[64])
+    _, tx1024 = cpu_reference_run(band, target, cores, strips=(1024,))
+    sec = statistics.median(times)
+    band_px = rows * args.width
+    value = extrapolated_mpx(total, band_px, tf, tx[64])
+    sample = cpu_sample_desc(rows, args.width, cores, tf, {64: tx[64], 1024: tx1024[1024]},
+                             total)
     line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpx/s", "n_gpus": world,
-            "steps": len(times), "warmup": 1, "ms_per_step": round(step_ms, 3),
+            "steps": steps, "warmup": 1 if args.warmup else 0, "ms_per_step": round(sec * 1e3, 1),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": workload_config(args, world),
             "cpu_baseline": {"value": round(value, 3), "unit": "Mpx/s", "cores": cores,
-                             "kind": "port", "sample": sample},
+                             "kind": "port", "cpu": cpu_model(), "sample": sample,
+                             "strip1024_value": round(extrapolated_mpx(total, band_px, tf,
+                                                                       tx1024[1024]), 3)},
             "e2e": {"value": round(value, 3), "unit": "Mpx/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -321,7 +370,8 @@ def run_batch(args, rank, world, local):
     line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpx/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic (on-GPU generator, model of src/synthetic.py)",
+            "dtype": dtype_label(args.precision),
+            "data": "synthetic (on-GPU generator, model of src/synthetic.py)",
             "config": batch_config(args, world),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
@@ -401,6 +451,14 @@ def mufu_roofline(npx, kernel_ms, clk):
             "peak_source": f"{sms} SM x 16/clk x {mhz:.0f} MHz (measured clock)"}
 
 
+def dtype_label(precision: str) -> str:
+    """What the path computes in: EXACT = fp32 arithmetic certified per pixel,
+    fp64 (reference operation order) for the uncertified ones — output bytes
+    identical to the fp64 reference; STRICT = fp64 throughout; FAST = fp32."""
+    return {"exact": "f64-exact (fp32 certified + fp64 repair; u8 out byte-identical)",
+            "strict": "f64", "fast": "f32 (+-1 LSB)"}[precision]
+
+
 def _hbm_peak():
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -446,7 +504,7 @@ def run_tile(args, rank, world, local):
     line = {"metric": METRIC, "value": round(npx * world / (ms * 1e-3) / 1e6, 3), "unit": "Mpx/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32",
+            "vs_baseline": None, "dtype": dtype_label(args.precision),
             "data": "synthetic (on-GPU generator, model of src/synthetic.py)",
             "config": {"workload": "C1: 2048x2048 tile normalized to a 2048x2048 target "
                                    "(fit both + transform, reference defaults)",
@@ -577,7 +635,8 @@ def run_ours(args, rank, world, local):
     line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpx/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic (on-GPU generator, model of src/synthetic.py)",
+            "dtype": dtype_label(args.precision),
+            "data": "synthetic (on-GPU generator, model of src/synthetic.py)",
             "config": workload_config(args, world),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -695,26 +754,69 @@ def e2e(args, pb, slide, target, rank, world):
 
 
 def cpu_baseline(args, slide, target):
-    """Oracle port of the reference path on the host cores (bounded band)."""
+    """Oracle port of the reference path on the host cores (bounded band of the
+    same slide, 4 strips of 64 rows per core), strip heights 64 and 1024."""
     cores = os.cpu_count() or 1
-    rows = max(16, args.cpu_rows)
+    rows = min(slide.shape[0], max(64, args.cpu_rows or cpu_band_rows(cores)))
     band = slide[:rows].cpu().numpy()
     tgt = dict(i0=np.asarray(target.i0), basis=np.asarray(target.basis),
                p99=np.asarray(target.stats.p99))
-    tf, tx = cpu_reference_run(band, tgt, cores)
+    tf, tx = cpu_reference_run(band, tgt, cores, strips=(64, 1024))
+    band_px = rows * args.width
     total = args.width * args.height
-    v = extrapolated_mpx(total, band.shape[0] * band.shape[1], tf, tx)
-    return {"value": round(v, 3), "unit": "Mpx/s", "cores": cores, "kind": "port",
-            "sample": (f"{rows} x {args.width} band ({rows * args.width / 1e6:.1f} Mpx) of the "
-                       f"same slide; fit {tf:.3f} s + transform {tx:.3f} s (oracle port = "
-                       f"reference algorithm in NumPy, {cores} threads, strip 64), "
-                       f"extrapolated linearly to {total / 1e9:.2f} Gpx")}
+    return {"value": round(extrapolated_mpx(total, band_px, tf, tx[64]), 3), "unit": "Mpx/s",
+            "cores": cores, "kind": "port", "cpu": cpu_model(),
+            "strip1024_value": round(extrapolated_mpx(total, band_px, tf, tx[1024]), 3),
+            "sample": cpu_sample_desc(rows, args.width, cores, tf, tx, total)}
+
+
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1, with NCCL's communicator logging on
+    (stderr); rank 0 prints the JSON line.  Exit code = the launcher's."""
+    import subprocess
+
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def check_world(args, world: int) -> None:
+    """--gpus must match the launched world (never measure N=1 under an N-GPU
+    command); the NCCL arm needs one GPU per rank."""
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "ours" and world > 1 and args.dist_backend == "nccl":
+        import torch
+
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench.py: --gpus {world} needs {world} GPUs, "
+                             f"{torch.cuda.device_count()} visible")
 
 
 def main():
     args = parse()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1 and args.impl == "ours":
+        return launch_ranks(args)
+    if world_env is not None or args.impl == "ours":
+        check_world(args, int(world_env or "1"))
     rank, world, local = dist_setup(args) if args.impl == "ours" else (
         int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0)
     if args.impl == "reference":

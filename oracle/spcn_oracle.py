@@ -441,35 +441,55 @@ def dense_pairs(n, rng, min_h=0.65, max_h=2.0, zero_e=0.3, max_e=1.2):
     return h
 
 
+def _render_block(width, height, y0, rows, seed, i0, tissue_fraction, layout, sampler):
+    """src/synthetic.py:69-99 (_render_rows): rows [y0, y0+rows) of one
+    256-row block; content depends only on (seed, y0 // 256)."""
+    w = he_basis()
+    rng = np.random.default_rng([seed, y0 // 256])
+    n = width * rows
+    if layout == "scatter":
+        tissue = rng.random(n) < tissue_fraction
+    elif layout == "block":
+        side = max(1, int(round((tissue_fraction * width * height) ** 0.5)))
+        bx, by = (width - side) // 2, (height - side) // 2
+        ys = y0 + np.arange(rows)
+        rin = (ys >= by) & (ys < by + side)
+        cin = np.zeros(width, dtype=bool)
+        cin[bx:bx + side] = True
+        tissue = (rin[:, None] & cin[None, :]).ravel()
+    else:
+        raise ValueError(layout)
+    h = np.zeros((2, n))
+    k = int(tissue.sum())
+    if k:
+        h[:, tissue] = sampler(k, rng)
+    od = (w @ h).T.reshape(rows, width, 3)
+    return rgb_of(od, i0), h, tissue.reshape(rows, width)
+
+
 def render(width, height, seed, i0=(255, 255, 255), tissue_fraction=0.6,
            layout="scatter", sampler=sparse_pairs):
     """src/synthetic.py:69-121 → (pixels u8 (H,W,3), densities (2,HW), mask)."""
     i0 = np.asarray(i0, dtype=np.float64)
-    w = he_basis()
-    px_parts, h_parts, m_parts = [], [], []
-    for y0 in range(0, height, 256):
-        rows = min(256, height - y0)
-        rng = np.random.default_rng([seed, y0 // 256])
-        n = width * rows
-        if layout == "scatter":
-            tissue = rng.random(n) < tissue_fraction
-        elif layout == "block":
-            side = max(1, int(round((tissue_fraction * width * height) ** 0.5)))
-            bx, by = (width - side) // 2, (height - side) // 2
-            ys = y0 + np.arange(rows)
-            rin = (ys >= by) & (ys < by + side)
-            cin = np.zeros(width, dtype=bool)
-            cin[bx:bx + side] = True
-            tissue = (rin[:, None] & cin[None, :]).ravel()
-        else:
-            raise ValueError(layout)
-        h = np.zeros((2, n))
-        k = int(tissue.sum())
-        if k:
-            h[:, tissue] = sampler(k, rng)
-        od = (w @ h).T.reshape(rows, width, 3)
-        px_parts.append(rgb_of(od, i0))
-        h_parts.append(h)
-        m_parts.append(tissue.reshape(rows, width))
-    return (np.concatenate(px_parts), np.concatenate(h_parts, axis=1),
-            np.concatenate(m_parts))
+    parts = [_render_block(width, height, y0, min(256, height - y0), seed, i0,
+                           tissue_fraction, layout, sampler) for y0 in range(0, height, 256)]
+    return (np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts], axis=1),
+            np.concatenate([p[2] for p in parts]))
+
+
+def render_band(width, height, seed, rows, i0=(255, 255, 255), tissue_fraction=0.6,
+                layout="scatter", workers=None):
+    """Pixels of the first ``rows`` rows of render(width, height, seed, ...)
+    (identical bytes), 256-row blocks rendered on a thread pool — the
+    CPU-baseline input of bench.py (fixture cost only)."""
+    i0 = np.asarray(i0, dtype=np.float64)
+    out = np.empty((rows, width, 3), np.uint8)
+
+    def one(y0):
+        keep = min(256, rows - y0)          # the block is drawn whole (same RNG stream)
+        out[y0:y0 + keep] = _render_block(width, height, y0, min(256, height - y0), seed, i0,
+                                          tissue_fraction, layout, sparse_pairs)[0][:keep]
+
+    with ThreadPoolExecutor(max_workers=workers or (os.cpu_count() or 1)) as pool:
+        list(pool.map(one, range(0, rows, 256)))
+    return out

@@ -29,3 +29,41 @@ def test_defaults_finish_quickly_flags():
     assert out.returncode == 0
     for flag in ("--gpus", "--steps", "--warmup", "--impl", "--workload", "--p99-mode"):
         assert flag in out.stdout, flag
+
+
+def test_gpus_flag_must_match_world():
+    """Under torchrun the world size and --gpus must agree (an N-GPU command
+    never measures fewer GPUs); non-zero ranks of the reference arm exit 0
+    silently."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="", WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    bad = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "1"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert bad.returncode != 0 and "WORLD_SIZE=2" in bad.stderr
+    env.update(RANK="1", LOCAL_RANK="1")
+    ok = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2"],
+                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert ok.returncode == 0 and ok.stdout.strip() == ""
+
+
+def test_launch_ranks_command(monkeypatch):
+    """--gpus N outside torchrun re-launches itself as N torch.distributed.run ranks."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    seen = {}
+
+    def fake_call(cmd, env):
+        seen.update(cmd=cmd, env=env)
+        return 0
+
+    monkeypatch.setattr(subprocess, "call", fake_call)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "5"])
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    assert bench.main() == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "5"]
+    assert seen["env"]["NCCL_DEBUG"]

@@ -1,7 +1,9 @@
 """Row-band sharded fit (distributed.RowBandGroup) equals the
-single-process fit — 2 ranks in 2 processes with gloo collectives, both on
+single-process fit — 2 ranks in 2 processes.  With gloo both ranks share
 cuda:0 (a functional check of the exchange logic; no kernel waits on another
-rank's kernel).  Sample mode and global-p99 mode."""
+rank's kernel); with NCCL (needs >= 2 GPUs, skipped otherwise) each rank owns
+its GPU and the collectives run device-direct.  Sample mode and global-p99
+mode."""
 import os
 import socket
 
@@ -19,17 +21,33 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, px, mode, q):
+BACKENDS = ["gloo", pytest.param("nccl", marks=pytest.mark.skipif(
+    "__import__('torch').cuda.device_count() < 2", reason="NCCL ranks need >= 2 GPUs"))]
+
+
+def _init(rank, world, port, backend):
     import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _worker(rank, world, port, px, mode, q, backend="gloo"):
     import torch.distributed as dist
 
     import paper_1901_03088_b200 as pb
     from paper_1901_03088_b200 import distributed as dd
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _init(rank, world, port, backend)
     try:
-        torch.cuda.set_device(0)
+        import torch
         H, W = px.shape[:2]
         r0 = rank * (H // world)
         rows = H // world if rank < world - 1 else H - r0
@@ -43,8 +61,9 @@ def _worker(rank, world, port, px, mode, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("backend", BACKENDS)
 @pytest.mark.parametrize("mode", ["sample", "global"])
-def test_rowband_fit_equals_single_process(mode):
+def test_rowband_fit_equals_single_process(mode, backend):
     import multiprocessing as mp
 
     import torch
@@ -58,7 +77,7 @@ def test_rowband_fit_equals_single_process(mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, px, mode, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, px, mode, q, backend)) for r in range(2)]
     for p in ps:
         p.start()
     out = [q.get(timeout=300) for _ in ps]
@@ -71,17 +90,15 @@ def test_rowband_fit_equals_single_process(mode):
         assert count == ref.stats.sample_count, rank
 
 
-def _xform_worker(rank, world, port, q):
+def _xform_worker(rank, world, port, q, backend="gloo"):
     import torch
     import torch.distributed as dist
 
     import paper_1901_03088_b200 as pb
     from paper_1901_03088_b200 import distributed as dd, synthetic
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _init(rank, world, port, backend)
     try:
-        torch.cuda.set_device(0)
         W, H = 4096, 4096                      # >= 2^24 px: the EXACT bound is calibrated
         full = synthetic.render_slide(W, H, 5, tissue_fraction=0.6)
         tgt = pb.fit(pb.DeviceSource(synthetic.render_slide(1024, 1024, 6, tissue_fraction=0.6)))
@@ -98,7 +115,8 @@ def _xform_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_rowband_transform_with_split_calibration():
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_rowband_transform_with_split_calibration(backend):
     """Each rank calibrates 1/N of the colours, one max all-reduce: the bands
     are byte-identical to the single-process transform."""
     import multiprocessing as mp
@@ -106,7 +124,7 @@ def test_rowband_transform_with_split_calibration():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_xform_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_xform_worker, args=(r, 2, port, q, backend)) for r in range(2)]
     for p in ps:
         p.start()
     out = [q.get(timeout=300) for _ in ps]
