@@ -7,6 +7,9 @@
 //   REP 16: 64 KiB, rows of 256 B = [ch0 x16 | ch1 x16 | ch2 x16 | pad], copy
 //           (lane&15) of channel c at x*256 + c*64 + (lane&15)*4 (<= 2-way
 //           bank conflicts);
+//   REP 24: 64 KiB, rows of 256 B = [ch0 x32 | ch1 x16 | ch2 x16]: channel 0
+//           conflict-free (copy `lane`), channels 1 and 2 as REP 16 — 5 instead
+//           of 6 shared-memory wavefronts per pixel's three lookups;
 //   REP 32: 128 KiB, region 0 rows [ch0 x32 | ch1 x32], region 1 (+64 KiB)
 //           rows [ch2 x32 | pad], copy `lane` at x*256 + ... + lane*4
 //           (conflict-free).
@@ -20,12 +23,20 @@ namespace spcn {
 
 template <int REP>
 struct LutLayout {
-  static_assert(REP == 16 || REP == 32, "table layouts exist for 16 and 32 replicas");
+  static_assert(REP == 16 || REP == 24 || REP == 32,
+                "table layouts exist for 16, 24 (mixed) and 32 replicas");
   static constexpr int kBytes = REP == 32 ? 2 * 65536 : 65536;
 
   // cooperative fill from a [3][256] fp32 table (any address space)
   __device__ static void fill(uint8_t* smem, const float* t, int tid, int nthreads) {
-    if (REP == 16) {
+    if (REP == 24) {
+      // rows of 256 B = [ch0 x32 | ch1 x16 | ch2 x16]
+      for (int i = tid; i < 256 * 64; i += nthreads) {
+        const int x = i >> 6, r = i & 63;
+        const int c = r < 32 ? 0 : (r < 48 ? 1 : 2);
+        *reinterpret_cast<float*>(smem + x * 256 + r * 4) = t[c * 256 + x];
+      }
+    } else if (REP == 16) {
       for (int i = tid; i < 256 * 48; i += nthreads) {
         const int x = i / 48, rem = i - 48 * x, c = rem >> 4, r = rem & 15;
         *reinterpret_cast<float*>(smem + x * 256 + c * 64 + r * 4) = t[c * 256 + x];
@@ -41,7 +52,10 @@ struct LutLayout {
 
   // per-lane PRMT constants of the three channels
   __device__ static void lane_consts(int lane, uint32_t (&lc)[3]) {
-    if (REP == 16) {
+    if (REP == 24) {
+      const uint32_t lrep = (uint32_t)(lane & 15) * 4;
+      lc[0] = (uint32_t)lane * 4; lc[1] = 128u + lrep; lc[2] = 192u + lrep;
+    } else if (REP == 16) {
       const uint32_t lrep = (uint32_t)(lane & 15) * 4;
       lc[0] = lrep; lc[1] = 64u + lrep; lc[2] = 128u + lrep;
     } else {
@@ -57,6 +71,30 @@ __device__ __forceinline__ uint32_t lop3_xor_or(uint32_t a, uint32_t b, uint32_t
   uint32_t d;
   asm("lop3.b32 %0, %1, %2, %3, 0xBE;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
+}
+
+// acc |= BIT if any of the three (lo, hi) float pairs differ: each pair is
+// reinterpreted as one 64-bit float (its register pair, no moves) and
+// compared with DSETP (fp64 pipe); the compares chain through one predicate
+// that guards a single OR.
+__device__ __forceinline__ double as_f64(float2 v) {
+  union {
+    float2 f;
+    double d;
+  } u;
+  u.f = v;
+  return u.d;
+}
+__device__ __forceinline__ void or_if_pairs_differ(uint32_t& acc, uint32_t bit,
+                                                   const float2 (&lo)[3], const float2 (&hi)[3]) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.neu.f64 p, %1, %2;\n\t"
+      "setp.neu.or.f64 p, %3, %4, p;\n\t"
+      "setp.neu.or.f64 p, %5, %6, p;\n\t"
+      "@p or.b32 %0, %0, %7;\n\t}"
+      : "+r"(acc)
+      : "d"(as_f64(lo[0])), "d"(as_f64(hi[0])), "d"(as_f64(lo[1])), "d"(as_f64(hi[1])),
+        "d"(as_f64(lo[2])), "d"(as_f64(hi[2])), "r"(bit));
 }
 
 // OD of input byte `idx` (0..47) of the thread's 48-byte block, channel c.
@@ -80,7 +118,8 @@ __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, ui
 template <int MODE>
 __device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t* lut,
                                                  const uint32_t* w, int k, const uint32_t* lc,
-                                                 uint32_t* ob, const float2* I) {
+                                                 uint32_t* ob, const float2* I,
+                                                 uint32_t* badpairs = nullptr) {
   const int a = 3 * k, b = 3 * k + 3;
   const float2 v0 = make_float2(od_lookup(lut, w, a, lc[0]), od_lookup(lut, w, b, lc[0]));
   const float2 v1 = make_float2(od_lookup(lut, w, a + 1, lc[1]), od_lookup(lut, w, b + 1, lc[1]));
@@ -95,6 +134,25 @@ __device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t*
       ob[a + c] = __float_as_uint(r.x);
       ob[b + c] = __float_as_uint(r.y);
     }
+    return 0u;
+  }
+  if (MODE == 2) {
+    // calibrated constant interval: {lo, hi} of BOTH pixels of the pair in two
+    // FFMA2 (pixel pair x one interval end), and the certification test of
+    // the pair's six roundings as three 64-bit compares of (lo_a, lo_b) with
+    // (hi_a, hi_b) accumulated in one predicate (DSETP on the fp64 pipe, off
+    // the saturated ALU/FMA issue).  Magic-number floats are never NaN or
+    // zero, so 64-bit float inequality is bit inequality.
+    float2 lo[3], hi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float2 pw = make_float2(ex2_approx(e[c][0]), ex2_approx(e[c][1]));
+      lo[c] = __ffma2_rn(bc2(I[c].x), pw, bc2(kMagic));
+      hi[c] = __ffma2_rn(bc2(I[c].y), pw, bc2(kMagic));
+      ob[a + c] = __float_as_uint(hi[c].x);
+      ob[b + c] = __float_as_uint(hi[c].y);
+    }
+    or_if_pairs_differ(*badpairs, 1u << (k >> 1), lo, hi);
     return 0u;
   }
   float2 alpha = bc2(0.f);
@@ -140,12 +198,18 @@ __device__ __forceinline__ void recolor_block(const FastS& fp, const uint8_t* lu
   if (MODE != 3 && fp.wmask) {
     // background blocks (every byte >= the OD-zero threshold) render the
     // constant target background; skip the math when the whole warp has them
-    uint32_t acc = 0xffffffffu;
-    if (valid) {
+    // (two stages: the first 4 pixels of every lane, then the rest — tissue
+    // warps leave after one LOP3 and one vote)
+    uint32_t acc = valid ? (w[0] & w[1] & w[2]) : 0xffffffffu;
+    bool bg = __all_sync(0xffffffffu, (acc & fp.wmask) == fp.wmask);
+    if (bg) {
+      if (valid) {
 #pragma unroll
-      for (int t = 0; t < 12; ++t) acc &= w[t];
+        for (int t = 3; t < 12; ++t) acc &= w[t];
+      }
+      bg = __all_sync(0xffffffffu, (acc & fp.wmask) == fp.wmask);
     }
-    if (__all_sync(0xffffffffu, (acc & fp.wmask) == fp.wmask)) {
+    if (bg) {
       if (valid) {
         uint4* d = reinterpret_cast<uint4*>(blk);
         d[0] = make_uint4(fp.wout[0], fp.wout[1], fp.wout[2], fp.wout[0]);
@@ -162,8 +226,8 @@ __device__ __forceinline__ void recolor_block(const FastS& fp, const uint8_t* lu
     } else {
 #pragma unroll
       for (int qq = 0; qq < 8; ++qq) {
-        const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * qq, lc, ob, I);
-        if (MODE == 0 || MODE == 2) badpairs |= (bad != 0u ? 1u : 0u) << qq;
+        const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * qq, lc, ob, I, &badpairs);
+        if (MODE == 0) badpairs |= (bad != 0u ? 1u : 0u) << qq;
 #pragma unroll
         for (int t = 0; t < 12; ++t)
           if (4 * t + 3 >= 6 * qq && 4 * t + 3 < 6 * qq + 6)

@@ -241,7 +241,7 @@ static int g_sm_count = 0;
 using XformFn = void (*)(const uint8_t*, uint8_t*, int64_t, FastP, StrictP, RepairList);
 
 struct Shape {
-  int cw, rep, nsub, blk, threads, tile_px, blocks_per_sm;
+  int cw, rep, nsub, blk, nsw, threads, tile_px, blocks_per_sm;
   size_t smem;
   XformFn fn[4];
 };
@@ -249,7 +249,7 @@ struct Shape {
 template <int CW, int REP, int NSW, int BLK, int NSUB>
 Shape make_wshape() {
   using C = WCfg<CW, REP, NSW, BLK, NSUB>;
-  return Shape{CW, REP, NSUB, BLK, C::kThreads, CW * C::kSlicePx, 0, C::kSmem,
+  return Shape{CW, REP, NSUB, BLK, NSW, C::kThreads, CW * C::kSlicePx, 0, C::kSmem,
                {k_xform_warp<0, CW, REP, NSW, BLK, NSUB>, k_xform_warp<1, CW, REP, NSW, BLK, NSUB>,
                 k_xform_warp<2, CW, REP, NSW, BLK, NSUB>,
                 k_xform_warp<3, CW, REP, NSW, BLK, NSUB>}};
@@ -260,10 +260,11 @@ Shape make_wshape() {
 // SPCN_XFORM_IDENTITY=1 makes the kernel copy input to output (memory-path
 // ceiling measurement only).
 static Shape g_shapes[] = {
-    make_wshape<16, 16, 3, 1, 2>(),   // production: per-warp rings of 2x512-px slots
-    make_wshape<16, 32, 4, 1, 1>(),
+    make_wshape<16, 24, 3, 1, 2>(),   // production: per-warp rings of 2x512-px slots, mixed table
+    make_wshape<16, 16, 3, 1, 2>(), make_wshape<16, 32, 4, 1, 1>(),
     make_wshape<16, 16, 2, 1, 3>(), make_wshape<12, 16, 3, 1, 3>(), make_wshape<16, 16, 4, 1, 1>(),
-    make_wshape<8, 16, 2, 2, 2>(), make_wshape<8, 16, 3, 2, 1>()};
+    make_wshape<8, 16, 2, 2, 2>(), make_wshape<8, 16, 3, 2, 1>(),
+    make_wshape<20, 16, 2, 1, 2>(), make_wshape<16, 32, 2, 1, 2>(), make_wshape<20, 24, 2, 1, 2>()};
 static Shape* g_shape = nullptr;
 static bool g_identity = false;
 
@@ -276,10 +277,15 @@ cudaError_t xform_setup_device() {
   if (e != cudaSuccess) return e;
   Shape* pick = &g_shapes[0];
   if (const char* env = getenv("SPCN_XFORM_SHAPE")) {
-    int cw = 0, rep = 0, nsub = 0, blk = 0;
-    if (sscanf(env, "%dx%dx%dx%d", &cw, &rep, &nsub, &blk) == 4)
+    int cw = 0, rep = 0, nsub = 0, blk = 0, nsw = 0;   // CWxREPxNSUBxBLK[xNSW]
+    const int nf = sscanf(env, "%dx%dx%dx%dx%d", &cw, &rep, &nsub, &blk, &nsw);
+    if (nf >= 4)
       for (auto& s : g_shapes)
-        if (s.cw == cw && s.rep == rep && s.nsub == nsub && s.blk == blk) pick = &s;
+        if (s.cw == cw && s.rep == rep && s.nsub == nsub && s.blk == blk &&
+            (nf == 4 || s.nsw == nsw)) {
+          pick = &s;
+          break;
+        }
   }
   if (const char* env = getenv("SPCN_XFORM_IDENTITY")) g_identity = env[0] == '1';
   for (auto fn : pick->fn) {
