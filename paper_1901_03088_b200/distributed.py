@@ -176,11 +176,10 @@ class RowBandGroup:
         import torch
         import torch.distributed as dist
 
-        from . import optics, snmf
-        from .errors import BlankSlideError, InsufficientPixelsError
-        from .normalize import FitParams, config_hash, stain_stats
-        from .pipeline import (PATCH_DT, TAKE_DT, SamplePlan, _cfg_fields, _lib_sample, _stage,
-                               _visit)
+        from . import fitcore, optics
+        from .errors import BlankSlideError
+        from .pipeline import (PATCH_DT, TAKE_DT, SamplePlan, _lib_sample, _stage, _visit,
+                               slide_chunks)
         from .stain_sep import SnmfConfig
 
         plan = plan or SamplePlan()
@@ -243,65 +242,14 @@ class RowBandGroup:
                                              _lib.ptr(hist), _lib.stream_handle()),
                        "sample_compact")
         all_reduce_sum(buf, self.group)        # disjoint sample writers: sum == gather
-        # --- identical, deterministic fit on every rank
+        # --- identical, deterministic fit on every rank (the single-process tail)
         m = collected
         i0 = _stage("background estimation", optics.i0_from_counts,
                     hist.cpu().numpy()[0].astype(np.int64))
-        lut = torch.from_numpy(optics.od_table(i0)).to(dev).reshape(1, 3, 256)
-        if m < 10:
-            raise InsufficientPixelsError(
-                f"basis fit: insufficient pixels: need at least 10 OD samples, got {m}")
-        offsets = torch.tensor([0, m], dtype=torch.int64, device=dev)
-        flat = sample.reshape(-1)
-        r = snmf.fit_slide(flat, offsets, lut, cfg, m)
-        h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
-        if p99_mode == "sample" and not per_patch_stats:
-            # basis, SNMF info, pooled p99 and the absent flags in ONE read
-            # (as pipeline.fit)
-            from . import stats as dstats
-            from .errors import StainAbsentError
-            from .normalize import _STAIN_NAMES, StainStats
-
-            vals, absent = dstats.segment_percentiles(h, offsets, 99.0)
-            packed = torch.cat([r.basis.reshape(-1), r.info.reshape(-1).to(torch.float64),
-                                vals.reshape(-1), absent.reshape(-1).to(torch.float64)]).cpu().numpy()
-            basis, info = packed[:6].reshape(3, 2).copy(), packed[6:10].astype(np.int64)
-            snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
-            for j in range(2):
-                if packed[12 + j]:
-                    raise StainAbsentError(f"density stats: stain absent: no {_STAIN_NAMES[j]} "
-                                           "density observed")
-            p99 = packed[10:12].copy()
-            if not (np.isfinite(p99).all() and (p99 >= 0).all()):
-                raise ValueError(f"density stats: p99 must be finite and non-negative, got {p99}")
-            fields = _cfg_fields(plan, cfg, code_lam, per_patch_stats)
-            prov = {"source": str(source_label), "config_hash": config_hash(fields)}
-            return FitParams(i0=i0, basis=basis, stats=StainStats(p99=p99, sample_count=m),
-                             provenance=prov)
-        info = r.info.cpu().numpy()[0]
-        snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
-        if p99_mode == "global":
-            from .global_stats import global_p99, sample_bracket
-            from .normalize import StainStats
-            from .pipeline import slide_chunks
-
-            guess = sample_bracket(h)
-            p99, nonwhite, _ = _stage("density stats", global_p99, slide_chunks(band_source), i0,
-                                      r.basis.cpu().numpy()[0], code_lam, thr,
-                                      comm=TorchComm(self.group), guess=guess)
-            st = StainStats(p99=p99, sample_count=int(nonwhite))
-        elif per_patch_stats:
-            from . import stats as dstats
-
-            counts = [c for c in used_counts if c > 0]
-            seg = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-            vals, _ = dstats.segment_percentiles(h, seg, 99.0)
-            st = _stage("density stats", stain_stats,
-                        patch_p99s=[tuple(v) for v in vals.cpu().numpy()], sample_count=m)
-        else:
-            st = _stage("density stats", stain_stats, h)
-        fields = _cfg_fields(plan, cfg, code_lam, per_patch_stats)
-        if p99_mode != "sample":
-            fields["p99_mode"] = p99_mode
-        prov = {"source": str(source_label), "config_hash": config_hash(fields)}
-        return FitParams(i0=i0, basis=r.basis.cpu().numpy()[0], stats=st, provenance=prov)
+        fb = fitcore.buffers(dev, plan.target_pixels, cfg.max_outer_iters)
+        fb.offsets().copy_(torch.tensor([0, m], dtype=torch.int64), non_blocking=False)
+        return fitcore.fit_tail(fb, sample.reshape(-1), m, i0, plan, cfg, code_lam=code_lam,
+                                per_patch_stats=per_patch_stats, p99_mode=p99_mode,
+                                used_counts=used_counts, source_label=source_label,
+                                chunks=slide_chunks(band_source) if p99_mode == "global" else None,
+                                comm=TorchComm(self.group), stage=_stage)

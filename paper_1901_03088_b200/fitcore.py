@@ -1,0 +1,251 @@
+"""Device fit core: reusable buffers and the fit tail shared by the
+single-process fit (pipeline.fit) and the row-band-sharded fit
+(distributed.RowBandGroup.fit) — src/pipeline.py:203-257.
+
+A fit is launch-bound (≈ 0.2 ms of kernels), so the host side is kept to two
+short round trips: one read after sampling (i0, which the host needs to build
+the OD table with numpy's own ``log`` — the reference's table, bit for bit)
+and one packed read of basis / SNMF info / p99 / absent flags at the end.
+Everything else — device buffers, the seeded candidate list of a slide
+geometry, the SNMF initial basis of a seed, the OD table of an i0 — is a pure
+function of its key and is memoised per thread, so a fit allocates nothing
+and runs no numpy beyond the table of a new i0.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from functools import lru_cache
+
+import numpy as np
+
+from . import _dev, _lib, optics, snmf
+from .errors import InsufficientPixelsError, StainAbsentError
+from .normalize import FitParams, StainStats, config_hash
+
+_STAIN_NAMES = ("hematoxylin", "eosin")
+_QBYTES = 32        # sizeof(SelQuery), stats.py
+
+# phase-1 arena (bytes): state i64[8] | offsets i64[2] | i0 f64[3] | empty i32[3] | pad | hist i32[768]
+A_STATE, A_OFFS, A_I0, A_EMPTY, A_HIST, A_BYTES, A_READ = 0, 64, 80, 104, 128, 128 + 3072, 116
+# phase-2 arena (bytes): basis f64[6] | p99 f64[2] | info i32[4] | absent i32[2]
+B_BASIS, B_P99, B_INFO, B_ABSENT, B_BYTES = 0, 48, 64, 80, 88
+
+
+@lru_cache(maxsize=64)
+def od_table_cached(i0_bytes: bytes) -> np.ndarray:
+    """optics.od_table of an i0 (memoised: a pure function of the 24 bytes)."""
+    return optics.od_table(np.frombuffer(i0_bytes, dtype=np.float64))
+
+
+@lru_cache(maxsize=32)
+def snmf_cfg_cached(lam, rel_tol, max_outer, seed, cluster) -> snmf.SnmfCfgC:
+    from .stain_sep import SnmfConfig
+
+    return snmf.make_cfg(SnmfConfig(lam=lam, rel_tol=rel_tol, max_outer_iters=max_outer,
+                                    seed=seed), cluster)
+
+
+def snmf_cluster(m: int) -> int:
+    """snmf.fit_slide's cluster rule (20 k samples → a 16-CTA cluster, else 1)."""
+    return snmf._BIG_CLUSTER[0] if m >= 20_000 else 1
+
+
+class FitBuffers:
+    """Device + pinned buffers of fits with one (target_pixels, max_outer) on
+    one device and stream (per thread: a fit is stream-ordered on the
+    caller's stream, so consecutive fits reuse them safely)."""
+
+    def __init__(self, device, target_pixels: int, max_outer: int):
+        t = _dev.torch()
+        self.device = device
+        self.target = max(int(target_pixels), 1)
+        self.arena_a = t.empty(A_BYTES, dtype=t.uint8, device=device)
+        self.arena_b = t.empty(B_BYTES, dtype=t.uint8, device=device)
+        self.sample = t.empty(3 * self.target, dtype=t.uint8, device=device)
+        self.lut = t.empty((1, 3, 256), dtype=t.float64, device=device)
+        self.history = t.empty(max_outer + 1, dtype=t.float64, device=device)
+        self.h = t.empty(2 * self.target, dtype=t.float64, device=device)
+        self.scratch = t.empty(self.target + 2, dtype=t.float64, device=device)
+        self.q = t.empty(6 * _QBYTES, dtype=t.uint8, device=device)
+        self.sel = t.empty(6, dtype=t.float64, device=device)
+        self.pin_a = t.empty(256, dtype=t.uint8, pin_memory=True)
+        self.pin_b = t.empty(256, dtype=t.uint8, pin_memory=True)
+        self.pin_lut = t.empty(768, dtype=t.float64, pin_memory=True)
+        self.lut_ev = None
+        self.cand = {}          # (W, H, plan) -> candidate descriptors on the device
+        L = _lib.lib()
+        if not getattr(L, "_spcn_rb_declared", False):
+            _lib.declare("spcn_readback", ctypes.c_int, [_lib.P, _lib.P, _lib.I64, _lib.P])
+            L._spcn_rb_declared = True
+
+    # views into the arenas
+    def state(self):
+        return self.arena_a[A_STATE:A_OFFS].view(_dev.torch().int64)
+
+    def offsets(self):
+        return self.arena_a[A_OFFS:A_I0].view(_dev.torch().int64)
+
+    def i0(self):
+        return self.arena_a[A_I0:A_EMPTY].view(_dev.torch().float64)
+
+    def empty(self):
+        return self.arena_a[A_EMPTY:A_EMPTY + 12].view(_dev.torch().int32)
+
+    def hist(self):
+        return self.arena_a[A_HIST:A_BYTES].view(_dev.torch().int32).view(1, 3, 256)
+
+    def basis(self):
+        return self.arena_b[B_BASIS:B_P99].view(_dev.torch().float64)
+
+    def p99(self):
+        return self.arena_b[B_P99:B_INFO].view(_dev.torch().float64)
+
+    def info(self):
+        return self.arena_b[B_INFO:B_ABSENT].view(_dev.torch().int32)
+
+    def absent(self):
+        return self.arena_b[B_ABSENT:B_BYTES].view(_dev.torch().int32)
+
+    def read(self, arena, pinned, nbytes: int) -> np.ndarray:
+        """Copy the first nbytes of a device arena to pinned memory with a
+        kernel (not queued behind other streams' bulk copies) and wait."""
+        t = _dev.torch()
+        _lib.check(_lib.lib().spcn_readback(_lib.ptr(arena), _lib.ptr(pinned), nbytes,
+                                            _lib.stream_handle()), "readback")
+        t.cuda.current_stream().synchronize()
+        return pinned[:nbytes].numpy().copy()
+
+    def upload_lut(self, i0: np.ndarray):
+        """The host OD table of i0 → self.lut (async from pinned memory)."""
+        t = _dev.torch()
+        if self.lut_ev is not None:
+            self.lut_ev.synchronize()          # previous upload has left the staging buffer
+        self.pin_lut.numpy()[:] = od_table_cached(np.ascontiguousarray(i0, np.float64)
+                                                  .tobytes()).reshape(-1)
+        self.lut.view(-1).copy_(self.pin_lut, non_blocking=True)
+        self.lut_ev = t.cuda.Event()
+        self.lut_ev.record()
+        return self.lut
+
+
+_TLS = threading.local()
+
+
+def buffers(device, target_pixels: int, max_outer: int) -> FitBuffers:
+    t = _dev.torch()
+    dev = t.device(device) if not isinstance(device, t.device) else device
+    if dev.index is None:
+        dev = t.device("cuda", t.cuda.current_device())
+    cache = getattr(_TLS, "bufs", None)
+    if cache is None:
+        cache = _TLS.bufs = {}
+    key = (dev.index, int(t.cuda.current_stream(dev).cuda_stream), int(target_pixels),
+           int(max_outer))
+    fb = cache.get(key)
+    if fb is None:
+        if len(cache) > 8:
+            cache.clear()
+        fb = cache[key] = FitBuffers(dev, target_pixels, max_outer)
+    return fb
+
+
+def cfg_fields(plan, cfg, code_lam, per_patch_stats):
+    return {"lambda": cfg.lam, "code_lambda": code_lam, "rel_tol": cfg.rel_tol,
+            "max_outer_iters": cfg.max_outer_iters, "snmf_seed": cfg.seed,
+            "sample_seed": plan.seed, "white_threshold": plan.white_threshold,
+            "sample_cap": plan.sample_cap, "target_pixels": plan.target_pixels,
+            "max_patches": plan.max_patches, "patch_size": plan.patch_size,
+            "background_fraction_cutoff": plan.background_fraction_cutoff,
+            "per_patch_stats": per_patch_stats}
+
+
+@lru_cache(maxsize=256)
+def _provenance_hash(items: tuple) -> str:
+    return config_hash(dict(items))
+
+
+def provenance(plan, cfg, code_lam, per_patch_stats, p99_mode, source_label) -> dict:
+    fields = cfg_fields(plan, cfg, code_lam, per_patch_stats)
+    if p99_mode != "sample":
+        fields["p99_mode"] = p99_mode
+    return {"source": str(source_label),
+            "config_hash": _provenance_hash(tuple(sorted((k, str(v)) for k, v in fields.items())))}
+
+
+def fit_tail(fb: FitBuffers, sample_flat, m: int, i0: np.ndarray, plan, cfg, *,
+             code_lam: float, per_patch_stats: bool, p99_mode: str, used_counts,
+             source_label: str = "", chunks=None, comm=None, stage=None) -> FitParams:
+    """src/pipeline.py:222-257 from the sample on: OD table → SNMF basis →
+    densities (code_lam) → p99 (pooled, per-patch median, or whole-slide),
+    FitParams with the reference's warnings, errors and provenance.
+
+    sample_flat: CUDA uint8 (3m,) RGB sample; i0: host (3,) background.
+    chunks: whole-slide pass generator (global p99 mode); comm: collectives of
+    a row-band group (global mode)."""
+    t = _dev.torch()
+    stage = stage or (lambda label, fn, *a, **k: fn(*a, **k))
+    if m < 10:
+        raise InsufficientPixelsError(
+            f"basis fit: insufficient pixels: need at least 10 OD samples, got {m}")
+    lut = fb.upload_lut(i0)
+    offsets = fb.offsets()
+    L = snmf._sig()
+    c = snmf_cfg_cached(float(cfg.lam), float(cfg.rel_tol), int(cfg.max_outer_iters),
+                        int(cfg.seed), snmf_cluster(m))
+    basis_d, info_d = fb.basis(), fb.info()
+    _lib.check(L.spcn_snmf_batched(_lib.ptr(sample_flat), None, _lib.ptr(offsets), 1,
+                                   _lib.ptr(lut), ctypes.byref(c), _lib.ptr(fb.scratch), m,
+                                   _lib.ptr(basis_d), _lib.ptr(fb.history), _lib.ptr(info_d),
+                                   _lib.stream_handle()), "snmf_batched")
+    h = fb.h[:2 * m].view(2, m)
+    _lib.check(L.spcn_code_samples(_lib.ptr(sample_flat), _lib.ptr(offsets), 1, m, _lib.ptr(lut),
+                                   _lib.ptr(basis_d), float(code_lam), 2000, _lib.ptr(h), m,
+                                   _lib.stream_handle()), "code_samples")
+    prov = provenance(plan, cfg, code_lam, per_patch_stats, p99_mode, source_label)
+    if p99_mode == "sample" and not per_patch_stats:
+        from . import stats as dstats
+
+        S = dstats._sig()
+        _lib.check(S.spcn_percentile_segments(_lib.ptr(h), m, _lib.ptr(offsets), 1, 99.0,
+                                              _lib.ptr(fb.q), _lib.ptr(fb.sel),
+                                              _lib.ptr(fb.p99()), _lib.ptr(fb.absent()),
+                                              _lib.stream_handle()), "percentile_segments")
+        raw = fb.read(fb.arena_b, fb.pin_b, B_BYTES)
+        basis = raw[B_BASIS:B_P99].view(np.float64).reshape(3, 2).copy()
+        p99 = raw[B_P99:B_INFO].view(np.float64).copy()
+        info = raw[B_INFO:B_ABSENT].view(np.int32)
+        absent = raw[B_ABSENT:B_BYTES].view(np.int32)
+        snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters, stacklevel=4)
+        for j in range(2):
+            if absent[j]:
+                raise StainAbsentError(f"density stats: stain absent: no {_STAIN_NAMES[j]} "
+                                       "density observed")
+        if not (np.isfinite(p99).all() and (p99 >= 0).all()):
+            raise ValueError(f"density stats: p99 must be finite and non-negative, got {p99}")
+        return FitParams(i0=np.asarray(i0, np.float64).copy(), basis=basis,
+                         stats=StainStats(p99=p99, sample_count=m), provenance=prov)
+    raw = fb.read(fb.arena_b, fb.pin_b, B_ABSENT)
+    basis = raw[B_BASIS:B_P99].view(np.float64).reshape(3, 2).copy()
+    snmf.warn_flags(m, int(raw[B_INFO:B_ABSENT].view(np.int32)[2]), cfg.max_outer_iters,
+                    stacklevel=4)
+    from .normalize import stain_stats
+
+    if p99_mode == "global":
+        from .global_stats import global_p99, sample_bracket
+
+        guess = sample_bracket(h)              # the sampled densities seed the first level
+        p99, nonwhite, _ = stage("density stats", global_p99, chunks, i0, basis, code_lam,
+                                 plan.white_threshold, comm=comm, guess=guess)
+        st = StainStats(p99=p99, sample_count=int(nonwhite))
+    elif per_patch_stats:
+        from . import stats as dstats
+
+        counts = [v for v in used_counts if v > 0]
+        seg = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        vals, _ = dstats.segment_percentiles(h, seg, 99.0)
+        st = stage("density stats", stain_stats,
+                   patch_p99s=[tuple(v) for v in vals.cpu().numpy()], sample_count=m)
+    else:
+        st = stage("density stats", stain_stats, h)
+    return FitParams(i0=np.asarray(i0, np.float64).copy(), basis=basis, stats=st, provenance=prov)

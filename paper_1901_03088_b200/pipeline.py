@@ -19,12 +19,11 @@ from threading import Lock
 
 import numpy as np
 
-from . import _dev, _lib, optics, snmf
-from .errors import (BlankSlideError, DegenerateStainError, InsufficientPixelsError,
-                     SlideNormError, StainAbsentError)
+from . import _dev, _lib, optics
+from .errors import BlankSlideError, DegenerateStainError, SlideNormError
 from .image_io import (DEFAULT_STRIP_HEIGHT, ArraySource, ArrayWriter, DeviceSource, DeviceWriter,
                        PixelBlock, plan_strips)
-from .normalize import FitParams, StainStats, config_hash, scale_factors, stain_stats
+from .normalize import FitParams, scale_factors
 from .optics import SAMPLE_CAP, WHITE_THRESHOLD
 from .stain_sep import SnmfConfig
 from .xform import XformPlan
@@ -250,69 +249,93 @@ def _visit_plan_type():
     return _VISIT_PLAN
 
 
-def _fit_sample_resident(slide: DeviceSource, plan: SamplePlan, need_counts: bool = False):
-    """Sampling + i0 for a device-resident slide with one host round trip in
-    the common case: count → visit loop (k_visit, on the device) → ordered
-    compaction → i0, then a single read of the results.  A further candidate
-    batch is only needed when the first ran out before a stop rule fired.
-    Returns (sample (target_pixels, 3) CUDA buffer, m, i0, PixelSample meta, empty)."""
+_VISIT_BATCH_MAX = 1024   # candidates per k_visit launch (its totals live in shared memory)
+
+
+def _resident_candidates(fb, slide: DeviceSource, plan: SamplePlan):
+    """Candidate patches of a resident slide geometry on the device (memoised
+    per (width, height, plan) in the fit buffers: a pure function of them)."""
+    key = (slide.width, slide.height, plan)
+    c = fb.cand.get(key)
+    if c is None:
+        t = _dev.torch()
+        VisitPlan = _visit_plan_type()
+        order, ncand, rects = _candidates(slide.width, slide.height, plan)
+        W = slide.width
+        desc = np.array([(y * W + x, w, h, W) for (x, y, w, h) in rects], dtype=PATCH_DT)
+        dims = np.array([(w, h) for (_, _, w, h) in rects], dtype=np.int32)
+        npx = dims[:, 0].astype(np.int64) * dims[:, 1]
+        chunks = int(max(1, -(-int(npx.max()) // CHUNK)))
+        batches, k0, n = [], 0, min(ncand, max(2, min(plan.max_patches, 8)))
+        while k0 < ncand:
+            n = min(n, ncand - k0, _VISIT_BATCH_MAX)
+            batches.append((k0, n))
+            k0 += n
+            n *= 2
+        c = dict(ncand=ncand, chunks=chunks, batches=batches,
+                 desc=t.from_numpy(desc.view(np.uint8).copy()).to(fb.device),
+                 dims=t.from_numpy(dims).to(fb.device),
+                 takes=t.zeros(ncand * TAKE_DT.itemsize, dtype=t.uint8, device=fb.device),
+                 counts=t.empty(max(n for _, n in batches) * chunks * 4, dtype=t.int32,
+                                device=fb.device),
+                 vp=VisitPlan(plan.target_pixels, plan.sample_cap, plan.max_patches, ncand,
+                              float(plan.background_fraction_cutoff)))
+        if len(fb.cand) > 16:
+            fb.cand.clear()
+        fb.cand[key] = c
+    return c
+
+
+def _fit_sample_resident(fb, slide: DeviceSource, plan: SamplePlan, need_counts: bool = False):
+    """Sampling + i0 of a device-resident slide with ONE host read in the
+    common case: count → visit loop (k_visit, on the device) → ordered
+    compaction → i0, then a single read of (state, i0, empty flags).  A
+    further candidate batch runs only when the first ran out before a stop
+    rule fired.  Returns (m, i0, PixelSample meta, empty flags); the sample is
+    fb.sample[:3m]."""
     import ctypes
 
-    t = _dev.torch()
     L = _lib_sample()
-    VisitPlan = _visit_plan_type()
-    order, ncand, rects = _candidates(slide.width, slide.height, plan)
-    W = slide.width
-    desc = np.array([(y * W + x, w, h, W) for (x, y, w, h) in rects], dtype=PATCH_DT)
-    dims = np.array([(w, h) for (_, _, w, h) in rects], dtype=np.int32)
-    d_desc = t.from_numpy(desc.view(np.uint8).copy()).cuda()
-    d_dims = t.from_numpy(dims).cuda()
-    vp = VisitPlan(plan.target_pixels, plan.sample_cap, plan.max_patches, ncand,
-                   float(plan.background_fraction_cutoff))
+    c = _resident_candidates(fb, slide, plan)
     thr = int(plan.white_threshold)
-    state = t.zeros(8, dtype=t.int64, device="cuda")
-    offsets = t.zeros(2, dtype=t.int64, device="cuda")
-    sample = t.empty((max(plan.target_pixels, 1), 3), dtype=t.uint8, device="cuda")
-    hist = t.zeros((1, 3, 256), dtype=t.int32, device="cuda")
-    i0 = t.empty(3, dtype=t.float64, device="cuda")
-    empty = t.empty(3, dtype=t.int32, device="cuda")
-    takes_all = t.zeros(ncand * TAKE_DT.itemsize, dtype=t.uint8, device="cuda")
     img, stream = slide.tensor, _lib.stream_handle()
-    k0, batch = 0, min(ncand, max(2, min(plan.max_patches, 8)))
-    while True:
-        n = min(batch, ncand - k0)
-        npx = dims[k0:k0 + n, 0].astype(np.int64) * dims[k0:k0 + n, 1]
-        chunks = int(max(1, -(-int(npx.max()) // CHUNK)))
-        counts = t.empty((n, chunks, 4), dtype=t.int32, device="cuda")
-        dsl = d_desc[k0 * PATCH_DT.itemsize:(k0 + n) * PATCH_DT.itemsize]
-        tks = takes_all[k0 * TAKE_DT.itemsize:(k0 + n) * TAKE_DT.itemsize]
-        _lib.check(L.spcn_sample_count(_lib.ptr(img), _lib.ptr(dsl), n, chunks, thr,
+    fb.arena_a.zero_()
+    state, hist = fb.state(), fb.hist()
+    from .fitcore import A_READ
+
+    for k0, n in c["batches"]:
+        dsl = c["desc"][k0 * PATCH_DT.itemsize:(k0 + n) * PATCH_DT.itemsize]
+        tks = c["takes"][k0 * TAKE_DT.itemsize:(k0 + n) * TAKE_DT.itemsize]
+        counts = c["counts"]
+        _lib.check(L.spcn_sample_count(_lib.ptr(img), _lib.ptr(dsl), n, c["chunks"], thr,
                                        _lib.ptr(counts), stream), "sample_count")
-        _lib.check(L.spcn_sample_visit(_lib.ptr(counts), n, chunks, k0,
-                                       _lib.ptr(d_dims[k0:]), ctypes.byref(vp), _lib.ptr(state),
-                                       _lib.ptr(tks), _lib.ptr(offsets), stream), "sample_visit")
-        _lib.check(L.spcn_sample_compact(_lib.ptr(img), _lib.ptr(dsl), n, chunks, thr,
-                                         _lib.ptr(counts), _lib.ptr(tks), _lib.ptr(sample),
+        _lib.check(L.spcn_sample_visit(_lib.ptr(counts), n, c["chunks"], k0,
+                                       _lib.ptr(c["dims"][k0:]), ctypes.byref(c["vp"]),
+                                       _lib.ptr(state), _lib.ptr(tks), _lib.ptr(fb.offsets()),
+                                       stream), "sample_visit")
+        _lib.check(L.spcn_sample_compact(_lib.ptr(img), _lib.ptr(dsl), n, c["chunks"], thr,
+                                         _lib.ptr(counts), _lib.ptr(tks), _lib.ptr(fb.sample),
                                          _lib.ptr(hist), stream), "sample_compact")
-        _lib.check(L.spcn_i0_from_hist(_lib.ptr(hist), 1, _lib.ptr(i0), _lib.ptr(empty), stream),
-                   "i0_from_hist")
-        # one read: state (8 int64) | i0 (3 f64) | empty flags (3 int32 widened)
-        packed = t.cat([state.view(t.float64), i0, empty.to(t.float64)]).cpu().numpy()
-        st = packed[:8].view(np.int64)
-        if st[7]:                                  # the batch ran out: next candidates
-            k0 += n
-            batch *= 2
-            continue
-        break
+        _lib.check(L.spcn_i0_from_hist(_lib.ptr(hist), 1, _lib.ptr(fb.i0()),
+                                       _lib.ptr(fb.empty()), stream), "i0_from_hist")
+        raw = fb.read(fb.arena_a, fb.pin_a, A_READ)
+        st = raw[:64].view(np.int64)
+        if not st[7]:                              # a stop rule fired (or all candidates seen)
+            break
+    from .fitcore import A_EMPTY, A_I0
+
     m = int(st[0])
     used_counts = []
     if need_counts:                                # per-patch stats only (one more read)
-        tk = np.frombuffer(takes_all[:(k0 + n) * TAKE_DT.itemsize].cpu().numpy().tobytes(),
+        tk = np.frombuffer(c["takes"][:(k0 + n) * TAKE_DT.itemsize].cpu().numpy().tobytes(),
                            dtype=TAKE_DT)
         used_counts = [int(v) for v in tk["take_nonwhite"] if v > 0]
-    meta = PixelSample(non_white=sample[:m], patch_counts=used_counts, bright=None,
-                       patches_visited=int(st[1]), patches_used=int(st[2]), bright_hist=None)
-    return sample, m, packed[8:11].copy(), meta, packed[11:14].astype(bool)
+    meta = PixelSample(non_white=fb.sample[:3 * m].view(m, 3), patch_counts=used_counts,
+                       bright=None, patches_visited=int(st[1]), patches_used=int(st[2]),
+                       bright_hist=None)
+    i0 = raw[A_I0:A_EMPTY].view(np.float64).copy()
+    empty = raw[A_EMPTY:A_EMPTY + 12].view(np.int32).astype(bool)
+    return m, i0, meta, empty
 
 
 def _sample_device(slide, plan: SamplePlan):
@@ -382,13 +405,9 @@ def sample_pixels(slide, plan: SamplePlan = SamplePlan()) -> PixelSample:
 
 # ----------------------------------------------------------------------------- fit
 def _cfg_fields(plan, cfg, code_lam, per_patch_stats):
-    return {"lambda": cfg.lam, "code_lambda": code_lam, "rel_tol": cfg.rel_tol,
-            "max_outer_iters": cfg.max_outer_iters, "snmf_seed": cfg.seed,
-            "sample_seed": plan.seed, "white_threshold": plan.white_threshold,
-            "sample_cap": plan.sample_cap, "target_pixels": plan.target_pixels,
-            "max_patches": plan.max_patches, "patch_size": plan.patch_size,
-            "background_fraction_cutoff": plan.background_fraction_cutoff,
-            "per_patch_stats": per_patch_stats}
+    from .fitcore import cfg_fields
+
+    return cfg_fields(plan, cfg, code_lam, per_patch_stats)
 
 
 def slide_chunks(slide, rows: int = 2048):
@@ -428,19 +447,23 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
         slide = ArraySource(slide)
     elif _dev.is_tensor(slide):
         slide = DeviceSource(slide)
+    from . import fitcore
+
+    fb = fitcore.buffers(slide.tensor.device if isinstance(slide, DeviceSource) else "cuda",
+                         plan.target_pixels, cfg.max_outer_iters)
     t0 = time.perf_counter()
     if isinstance(slide, DeviceSource):
         # resident slide: visit loop + i0 on the device, one host round trip
-        sample, m, i0, meta, empty = _stage("sampling", _fit_sample_resident, slide, plan,
-                                            per_patch_stats)
+        m, i0, meta, empty = _stage("sampling", _fit_sample_resident, fb, slide, plan,
+                                    per_patch_stats)
         if m == 0:
             raise BlankSlideError("sampling: blank slide: no non-white pixels found in any "
                                   "sampled patch")
-        sample = sample[:m]
         for c in np.flatnonzero(empty):
             warnings.warn(f"no pixels brighter than the white threshold in the "
                           f"{('red', 'green', 'blue')[c]} channel; falling back to 255",
                           optics.BackgroundEstimateWarning, stacklevel=2)
+        sample_flat = fb.sample[:3 * m]
         stats.sampling_s += time.perf_counter() - t0
         t0 = time.perf_counter()
     else:
@@ -449,64 +472,17 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
         m = int(sample.shape[0])
         t0 = time.perf_counter()
         i0 = _stage("background estimation", optics.i0_from_counts, meta.bright_hist)
+        sample_flat = sample.reshape(-1)
+        fb.offsets().copy_(t.tensor([0, m], dtype=t.int64), non_blocking=False)
     stats.sampled_pixels = m
     stats.patches = meta.patches_used
-    lut = t.from_numpy(optics.od_table(i0)).cuda().reshape(1, 3, 256)
-    if m < 10:
-        raise InsufficientPixelsError(
-            f"basis fit: insufficient pixels: need at least 10 OD samples, got {m}")
-    offsets = t.tensor([0, m], dtype=t.int64, device="cuda")
-    flat = sample.reshape(-1)
-    r = snmf.fit_slide(flat, offsets, lut, cfg, m)
-    h = snmf.code_samples(flat, offsets, lut, r.basis, code_lam, m)
-    if p99_mode == "sample" and not per_patch_stats:
-        # basis, SNMF info, pooled p99 and the absent flags in ONE read
-        from . import stats as dstats
-        from .normalize import _STAIN_NAMES
-
-        vals, absent = dstats.segment_percentiles(h, offsets, 99.0)
-        packed = t.cat([r.basis.reshape(-1), r.info.reshape(-1).to(t.float64),
-                        vals.reshape(-1), absent.reshape(-1).to(t.float64)]).cpu().numpy()
-        basis, info = packed[:6].reshape(3, 2).copy(), packed[6:10].astype(np.int64)
-        snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
-        for j in range(2):
-            if packed[12 + j]:
-                raise StainAbsentError(f"density stats: stain absent: no {_STAIN_NAMES[j]} "
-                                       "density observed")
-        p99 = packed[10:12].copy()
-        if not (np.isfinite(p99).all() and (p99 >= 0).all()):
-            raise ValueError(f"density stats: p99 must be finite and non-negative, got {p99}")
-        st = StainStats(p99=p99, sample_count=m)
-        stats.basis_fit_s += time.perf_counter() - t0
-        fields = _cfg_fields(plan, cfg, code_lam, per_patch_stats)
-        provenance = {"source": str(source_label), "config_hash": config_hash(fields)}
-        return FitParams(i0=i0, basis=basis, stats=st, provenance=provenance)
-    info = r.info.cpu().numpy()[0]
-    basis = r.basis.cpu().numpy()[0]
-    snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters)
-    if p99_mode == "global":
-        from .global_stats import global_p99, sample_bracket
-
-        guess = sample_bracket(h)         # the sampled densities seed the first level
-        p99, nonwhite, _ = _stage("density stats", global_p99, slide_chunks(slide), i0, basis,
-                                  code_lam, plan.white_threshold, guess=guess)
-        st = StainStats(p99=p99, sample_count=int(nonwhite))
-    elif per_patch_stats:
-        from . import stats as dstats
-
-        counts = [c for c in meta.patch_counts if c > 0]
-        seg = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-        vals, _ = dstats.segment_percentiles(h, seg, 99.0)
-        pairs = [tuple(v) for v in vals.cpu().numpy()]
-        st = _stage("density stats", stain_stats, patch_p99s=pairs, sample_count=m)
-    else:
-        st = _stage("density stats", stain_stats, h)
+    fp = fitcore.fit_tail(fb, sample_flat, m, i0, plan, cfg, code_lam=code_lam,
+                          per_patch_stats=per_patch_stats, p99_mode=p99_mode,
+                          used_counts=meta.patch_counts, source_label=source_label,
+                          chunks=slide_chunks(slide) if p99_mode == "global" else None,
+                          stage=_stage)
     stats.basis_fit_s += time.perf_counter() - t0
-    fields = _cfg_fields(plan, cfg, code_lam, per_patch_stats)
-    if p99_mode != "sample":
-        fields["p99_mode"] = p99_mode
-    provenance = {"source": str(source_label), "config_hash": config_hash(fields)}
-    return FitParams(i0=i0, basis=basis, stats=st, provenance=provenance)
+    return fp
 
 
 # ----------------------------------------------------------------------------- transform
@@ -641,11 +617,15 @@ def transform(slide, source: FitParams, target: FitParams, sink, *,
         src = slide.tensor
         if isinstance(sink, DeviceWriter):
             plan.run(src, sink.pixels, width * slide.height)
-            for y, h in strips:
-                gauge.add(h * width)
-                sink.mark_written(y, h)
-                gauge.release(h * width)
-                if progress is not None:
+            if progress is None:            # one launch wrote every strip in place
+                gauge.add(strips[0][1] * width)
+                sink.mark_written(0, slide.height)
+                gauge.release(strips[0][1] * width)
+            else:
+                for y, h in strips:
+                    gauge.add(h * width)
+                    sink.mark_written(y, h)
+                    gauge.release(h * width)
                     progress(y + h, slide.height)
             t.cuda.current_stream().synchronize()
         else:

@@ -26,7 +26,12 @@ class XformPlan:
                  precision: str = "exact", max_sweeps: int = 2000):
         if precision not in _lib.PREC:
             raise ValueError(f"precision must be one of {sorted(_lib.PREC)}")
-        self.table = od_table(src_i0)               # exact reference OD table (host numpy)
+        from .fitcore import od_table_cached
+
+        i0b = _dev.f64_array(src_i0, 3, "src_i0")
+        if (i0b < 1.0).any():
+            od_table(i0b)                            # raises the reference's ValueError
+        self.table = od_table_cached(i0b.tobytes())  # exact reference OD table (host numpy)
         p = _lib.XformParams()
         p.src_i0[:] = [float(x) for x in _dev.f64_array(src_i0, 3, "src_i0")]
         p.src_basis[:] = [float(x) for x in _dev.f64_array(src_basis, 6, "src_basis")]
