@@ -288,8 +288,14 @@ cudaError_t launch_strict_batch(const uint8_t* src, uint8_t* dst, const StrictP*
   if (nitems <= 0) return cudaSuccess;
   int64_t gx = (max_pix + 255) / 256;
   if (gx > 64) gx = 64;
-  k_strict_batch<<<dim3((unsigned)gx, nitems), 256, 0, st>>>(src, dst, sps, off, status, nitems);
-  return launched();
+  for (int i0 = 0; i0 < nitems; i0 += kMaxGridY) {   // gridDim.y <= 65535
+    const int ni = nitems - i0 < kMaxGridY ? nitems - i0 : kMaxGridY;
+    k_strict_batch<<<dim3((unsigned)gx, ni), 256, 0, st>>>(src, dst, sps + i0, off + i0,
+                                                           status + i0, ni);
+    const cudaError_t e = launched();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace spcn

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 namespace spcn {
+constexpr int kMaxGridY = 65535;   // launches with items on gridDim.y are split at this size
 extern std::atomic<unsigned long long> g_launches;
 inline cudaError_t launched(unsigned n = 1) {
   g_launches.fetch_add(n, std::memory_order_relaxed);

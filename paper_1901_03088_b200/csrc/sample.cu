@@ -276,9 +276,14 @@ __global__ void k_od_tables(const double* __restrict__ i0, int nprob, double* __
 cudaError_t launch_sample_count(const uint8_t* img, const spcn_patch* patches, int npatches,
                                 int max_chunks, int thr, int32_t* counts, cudaStream_t st) {
   if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;
-  k_sample_count<<<dim3(max_chunks, npatches), kSThreads, 0, st>>>(img, patches, max_chunks, thr,
-                                                                   counts);
-  return launched();
+  for (int y0 = 0; y0 < npatches; y0 += kMaxGridY) {   // gridDim.y <= 65535
+    const int ny = npatches - y0 < kMaxGridY ? npatches - y0 : kMaxGridY;
+    k_sample_count<<<dim3(max_chunks, ny), kSThreads, 0, st>>>(
+        img, patches + y0, max_chunks, thr, counts + (int64_t)y0 * max_chunks * 4);
+    const cudaError_t e = launched();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches, int npatches,
@@ -286,9 +291,15 @@ cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches,
                                   const spcn_patch_take* takes, uint8_t* out_px,
                                   int32_t* bright_hist, cudaStream_t st) {
   if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;
-  k_sample_compact<<<dim3(max_chunks, npatches), kSThreads, 0, st>>>(
-      img, patches, max_chunks, thr, counts, takes, out_px, bright_hist);
-  return launched();
+  for (int y0 = 0; y0 < npatches; y0 += kMaxGridY) {   // gridDim.y <= 65535
+    const int ny = npatches - y0 < kMaxGridY ? npatches - y0 : kMaxGridY;
+    k_sample_compact<<<dim3(max_chunks, ny), kSThreads, 0, st>>>(
+        img, patches + y0, max_chunks, thr, counts + (int64_t)y0 * max_chunks * 4, takes + y0,
+        out_px, bright_hist);
+    const cudaError_t e = launched();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_i0_from_hist(const int32_t* hist, int nprob, double* i0, int32_t* empty,
@@ -374,8 +385,13 @@ __global__ void __launch_bounds__(256) k_visit(const int32_t* __restrict__ count
 cudaError_t launch_visit(const int32_t* counts, int n, int max_chunks, int k0, const int32_t* dims,
                          const spcn_visit_plan& plan, int64_t* state, spcn_patch_take* takes,
                          int64_t* offsets, cudaStream_t st) {
-  k_visit<<<1, 256, 4 * n * sizeof(int64_t), st>>>(counts, n, max_chunks, k0, dims, plan, state,
-                                                  takes, offsets);
+  const size_t smem = 4 * (size_t)n * sizeof(int64_t);   // n <= 4096: up to 128 KiB
+  if (smem > 48 * 1024) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_visit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_visit<<<1, 256, smem, st>>>(counts, n, max_chunks, k0, dims, plan, state, takes, offsets);
   return launched();
 }
 

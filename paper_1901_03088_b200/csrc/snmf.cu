@@ -360,9 +360,16 @@ cudaError_t launch_code_table(const uint32_t* ukey, const int32_t* ucount, const
   int64_t gx = (max_m + 255) / 256;
   if (gx > 16) gx = 16;
   if (gx < 1) gx = 1;
-  k_code_table<<<dim3((unsigned)gx, nprob), 256, 0, st>>>(ukey, ucount, offsets, nprob, luts,
-                                                          bases, lam, max_sweeps, h, total);
-  return launched();
+  for (int p0 = 0; p0 < nprob; p0 += kMaxGridY) {   // gridDim.y <= 65535
+    const int np = nprob - p0 < kMaxGridY ? nprob - p0 : kMaxGridY;
+    k_code_table<<<dim3((unsigned)gx, np), 256, 0, st>>>(ukey, ucount + p0, offsets + p0, np,
+                                                         luts + (int64_t)p0 * 768,
+                                                         bases + (int64_t)p0 * 6, lam, max_sweeps,
+                                                         h, total);
+    const cudaError_t e = launched();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------
@@ -541,9 +548,16 @@ cudaError_t launch_code_samples(const uint8_t* samples, const int64_t* offsets, 
   if (nprob <= 0 || max_m <= 0) return cudaSuccess;
   int64_t gx = (max_m + 255) / 256;
   if (gx > 64) gx = 64;
-  k_code_samples<<<dim3((unsigned)gx, nprob), 256, 0, st>>>(samples, offsets, nprob, luts, bases,
-                                                            lam, max_sweeps, h, total);
-  return launched();
+  for (int p0 = 0; p0 < nprob; p0 += kMaxGridY) {   // gridDim.y <= 65535
+    const int np = nprob - p0 < kMaxGridY ? nprob - p0 : kMaxGridY;
+    k_code_samples<<<dim3((unsigned)gx, np), 256, 0, st>>>(samples, offsets + p0, np,
+                                                           luts + (int64_t)p0 * 768,
+                                                           bases + (int64_t)p0 * 6, lam,
+                                                           max_sweeps, h, total);
+    const cudaError_t e = launched();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace spcn

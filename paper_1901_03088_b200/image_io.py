@@ -2,10 +2,13 @@
 
 Kept: ``PixelBlock`` (src/image_io.py:40-59), ``SlideSource`` protocol
 (:62-92), ``ArraySource`` (:95-107), ``StripWriter`` protocol (:261-313),
-``plan_strips`` (:248-258).  Added for the device path: ``DeviceSource``
-(a CUDA (H, W, 3) u8 tensor) and ``DeviceWriter`` / ``ArrayWriter`` sinks
-whose storage the transform can write into directly.  PNG/TIFF codecs are
-out of scope for this round.
+``plan_strips`` (:248-258) — ``plan_strips`` and ``StripWriter`` follow the
+reference closely on purpose: they are the protocol users subclass.  Added
+for the device path: ``DeviceSource`` (a CUDA (H, W, 3) u8 tensor) and
+``DeviceWriter`` / ``ArrayWriter`` sinks whose storage the transform can
+write into directly.  Files: PNG in through Pillow and
+out through the streaming ``PngStripWriter`` (:316-358), tiled/striped RGB8
+(Big)TIFF through the package's own codec (tiff.py), ``.npy`` memory-mapped.
 """
 from __future__ import annotations
 
@@ -324,24 +327,80 @@ class TiffStripWriter(StripWriter):
             self._tw.abort()
 
 
+class PngStripWriter(StripWriter):
+    """Streaming 8-bit RGB PNG encoder (src/image_io.py:316-358): the file is
+    opened (and an unwritable path reported) on construction, every strip's
+    scanlines — filter byte 0 in front of each — go straight through one
+    zlib stream into IDAT chunks, so memory stays bounded by one strip.  A
+    failed or incomplete image leaves no file."""
+
+    _SIG = b"\x89PNG\r\n\x1a\n"
+
+    def __init__(self, path, width, height, compress_level: int = 6):
+        import struct
+        import zlib
+
+        super().__init__(width, height)
+        self.path = str(path)
+        self._fh = open(self.path, "wb")
+        self._fh.write(self._SIG)
+        self._chunk(b"IHDR", struct.pack(">IIBBBBB", width, height, 8, 2, 0, 0, 0))
+        self._z = zlib.compressobj(compress_level)
+
+    def _chunk(self, kind: bytes, data: bytes):
+        import struct
+        import zlib
+
+        self._fh.write(struct.pack(">I", len(data)) + kind)
+        self._fh.write(data)
+        self._fh.write(struct.pack(">I", zlib.crc32(data, zlib.crc32(kind)) & 0xFFFFFFFF))
+
+    def _write(self, rows):
+        if hasattr(rows, "cpu"):
+            rows = rows.cpu().numpy()
+        rows = np.asarray(rows)
+        h = rows.shape[0]
+        lines = np.empty((h, 1 + 3 * self.width), dtype=np.uint8)
+        lines[:, 0] = 0
+        lines[:, 1:] = rows.reshape(h, 3 * self.width)
+        payload = self._z.compress(lines)
+        if payload:
+            self._chunk(b"IDAT", payload)
+
+    def close(self):
+        if self._closed:
+            return
+        if self._rows_written != self.height:
+            self.abort()
+            raise ValueError(f"incomplete image: {self._rows_written} of {self.height} rows")
+        self._chunk(b"IDAT", self._z.flush())
+        self._chunk(b"IEND", b"")
+        self._fh.close()
+        self._closed = True
+
+    def abort(self):
+        import os
+
+        if not self._closed:
+            self._closed = True
+            self._fh.close()
+            if os.path.exists(self.path):
+                os.remove(self.path)
+
+
 class FileWriter(ArrayWriter):
-    """Output file fed in-order strips; encoded on close (PNG) or written
-    through a memory map (.npy).  A failed or incomplete image leaves no file."""
+    """`.npy` output fed in-order strips through a memory map.  A failed or
+    incomplete image leaves no file."""
 
     def __init__(self, path, width, height):
         from .errors import UnsupportedFormatError
 
         self.path = str(path)
-        low = self.path.lower()
-        if low.endswith(".npy"):
-            self.kind = "npy"
-            out = np.lib.format.open_memmap(self.path, mode="w+", dtype=np.uint8,
-                                            shape=(height, width, 3))
-        elif low.endswith(".png"):
-            self.kind = "png"
-            out = None
-        else:
-            raise UnsupportedFormatError(f"{path}: output must be .png, .npy or .tif(f)")  # noqa
+        if not self.path.lower().endswith(".npy"):
+            raise UnsupportedFormatError(f"{path}: output must be .png, .npy or .tif(f)")
+        self.kind = "npy"
+        out = np.lib.format.open_memmap(self.path, mode="w+", dtype=np.uint8,
+                                        shape=(height, width, 3))
         super().__init__(width, height, out=out)
 
     def close(self):
@@ -352,25 +411,22 @@ class FileWriter(ArrayWriter):
         except ValueError:
             self.abort()
             raise
-        if self.kind == "png":
-            from PIL import Image
-
-            Image.fromarray(self.pixels, mode="RGB").save(self.path, compress_level=6)
-        else:
-            self.pixels.flush()
+        self.pixels.flush()
 
     def abort(self):
         import os
 
         self._closed = True
-        if self.kind == "npy":
-            del self.pixels
+        del self.pixels
         if os.path.exists(self.path):
             os.remove(self.path)
 
 
 def open_writer(path, width: int, height: int) -> StripWriter:
     """src/image_io.py:457-466: a StripWriter for an output file."""
-    if str(path).lower().endswith((".tif", ".tiff")):
+    low = str(path).lower()
+    if low.endswith((".tif", ".tiff")):
         return TiffStripWriter(path, width, height)
+    if low.endswith(".png"):
+        return PngStripWriter(path, width, height)
     return FileWriter(path, width, height)

@@ -360,7 +360,7 @@ def _sample_device(slide, plan: SamplePlan):
             c, chunks = _count(L, img, desc, thr)
             dev_counts.append((lo, hi, c, chunks, img, desc))
             tot = np.concatenate([tot, c.sum(dim=1).cpu().numpy().astype(np.int64)])
-            batch *= 2
+            batch = min(2 * batch, _VISIT_BATCH_MAX)
         return tuple(int(v) for v in tot[k])
 
     takes, used_counts, collected, visited, used = _visit(plan, order[:ncand], rects, counts_of)

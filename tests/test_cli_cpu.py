@@ -160,3 +160,27 @@ def test_tiff_strip_writer_through_open_writer(tmp_path):
         with io.open_writer(tmp_path / "p.tif", 300, 513) as w:
             w.write_strip(io.PixelBlock(0, 0, a[:100]))
     assert not os.path.exists(tmp_path / "p.tif")
+
+
+def test_png_strip_writer_streams_with_bounded_memory(tmp_path):
+    """The PNG sink encodes strip by strip (src/image_io.py:316-358): the
+    file exists once opened, holds IDAT data before close, decodes to the
+    written pixels, and an unwritable path fails on open."""
+    import numpy as np
+    from PIL import Image
+
+    from paper_1901_03088_b200 import image_io as io
+
+    rng = np.random.default_rng(4)
+    img = rng.integers(0, 256, size=(300, 257, 3), dtype=np.uint8)
+    path = tmp_path / "s.png"
+    w = io.open_writer(path, 257, 300)
+    assert isinstance(w, io.PngStripWriter) and os.path.exists(path)
+    for y in range(0, 300, 64):
+        w.write_strip(io.PixelBlock(0, y, img[y:y + 64]))
+        if y >= 128:
+            assert os.path.getsize(path) > 1000          # data already on disk
+    w.close()
+    assert np.array_equal(np.asarray(Image.open(path)), img)
+    with pytest.raises(OSError):
+        io.open_writer(tmp_path / "missing" / "x.png", 10, 10)

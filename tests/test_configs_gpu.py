@@ -278,3 +278,47 @@ def test_gpu_rendered_slide_fit_recovers_generator():
     for j in range(2):
         truth = orc.pct(h[j, non_white], 99.0)
         assert abs(fp.stats.p99[j] - truth) / truth < 0.05
+
+
+# --------------------------------------------------------------------------- large candidate counts
+def test_many_candidates_on_mostly_white_slide_match_oracle():
+    """max_patches=300 on a 6000² slide of 3600 patches with ~1 % tissue:
+    3000 candidates visited in growing batches (capped at 1024 per k_visit
+    launch) by both device samplers, equal to the oracle's sampling/fit."""
+    pb = _pb()
+    from paper_1901_03088_b200 import synthetic
+
+    d = synthetic.render_slide(6000, 6000, 8, tissue_fraction=0.01, layout="block")
+    view = _DeviceView(d)
+    for target in (100_000, 1_000_000):
+        kw = dict(max_patches=300, patch_size=100, seed=3, target_pixels=target)
+        ref = orc.fit_params(view, orc.Plan(**kw))
+        s_ref = ref["sample"]
+        meta = pb.sample_pixels(pb.DeviceSource(d), pb.SamplePlan(**kw))
+        assert np.array_equal(meta.non_white, s_ref["non_white"])
+        assert [meta.patches_visited, meta.patches_used] == [s_ref["visited"], s_ref["used"]]
+        _assert_fit(_quiet(pb.fit, pb.DeviceSource(d), pb.SamplePlan(**kw)), ref, str(target))
+    assert s_ref["visited"] == 3000          # the second plan runs into the visit limit
+
+
+def test_batch_beyond_65535_grid_rows():
+    """4100 items x 16 candidate patches = 65 600 patch descriptors (> the
+    65 535 gridDim.y limit): launches are split, results per item unchanged."""
+    import torch
+
+    pb = _pb()
+    g = golden("c1")
+    tgt = pb.FitParams(i0=g["c1/tgt_i0"], basis=g["c1/tgt_basis"],
+                       stats=pb.StainStats(p99=g["c1/tgt_p99"]))
+    base = [orc.render(128, 128, s, tissue_fraction=0.6)[0] for s in range(4)]
+    n = 4100
+    x = torch.from_numpy(np.stack(base)).cuda()[torch.arange(n) % 4].contiguous()
+    plan = pb.SamplePlan(patch_size=32)
+    out, errors, fits = _quiet(pb.normalize_batch, x, tgt, plan=plan)
+    assert all(e is None for e in errors)
+    t = {"i0": tgt.i0, "basis": tgt.basis, "p99": tgt.stats.p99}
+    for i in (0, 1, 2, 3, 4099, 65535 // 16):
+        ref = orc.fit_params(base[i % 4], orc.Plan(patch_size=32))
+        _assert_fit(fits.params(i), ref, f"item {i}")
+        want = orc.run_transform(base[i % 4], ref, t, workers=1)
+        assert np.array_equal(out[i].cpu().numpy(), want), i
