@@ -367,6 +367,14 @@ uint64_t spcn_launch_count(void);
 /* Launch shape of the recolor kernel on the current device (diagnostics).   */
 const char* spcn_xform_shape(void);
 
+/* Per-launch timing of the main recolor kernel (measurement): while enabled,
+ * spcn_xform_rgb8 records a CUDA event pair on its stream around each
+ * k_xform_warp launch.  spcn_xform_timing synchronizes on the recorded events
+ * and returns the number of timed launches and their summed duration (ms),
+ * then clears the record.                                                  */
+int spcn_xform_timing_enable(int32_t on);
+int spcn_xform_timing(int64_t* launches, double* total_ms);
+
 #ifdef __cplusplus
 }
 #endif

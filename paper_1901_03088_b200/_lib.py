@@ -38,6 +38,7 @@ EXPORTS = (
     "spcn_stats_hist", "spcn_stats_refine", "spcn_stats_table", "spcn_stats_table_scan",
     "spcn_sample_visit",
     "spcn_readback", "spcn_last_error", "spcn_version", "spcn_launch_count", "spcn_xform_shape",
+    "spcn_xform_timing_enable", "spcn_xform_timing",
 )
 
 
@@ -79,6 +80,8 @@ _SIGS = {
     "spcn_version": (ctypes.c_char_p, []),
     "spcn_launch_count": (ctypes.c_uint64, []),
     "spcn_xform_shape": (ctypes.c_char_p, []),
+    "spcn_xform_timing_enable": (ctypes.c_int, [I32]),
+    "spcn_xform_timing": (ctypes.c_int, [ctypes.POINTER(I64), ctypes.POINTER(DBL)]),
 }
 
 

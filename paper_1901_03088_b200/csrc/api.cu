@@ -9,6 +9,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <string>
 
 #include "spcn.h"
@@ -79,6 +83,25 @@ bool fill_fast(FastP& fp, const StrictP& sp, bool exact) {
 
 constexpr size_t kWsHeader = 16;
 
+// Opt-in per-launch timing of the main recolor kernel (spcn_xform_timing_*).
+std::atomic<int> g_timing{0};
+std::mutex g_timing_mu;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timing_ev;
+
+void timing_begin(cudaStream_t st, cudaEvent_t& t0, cudaEvent_t& t1) {
+  if (cudaEventCreate(&t0) != cudaSuccess || cudaEventCreate(&t1) != cudaSuccess) {
+    t0 = t1 = nullptr;
+    return;
+  }
+  cudaEventRecord(t0, st);
+}
+
+void timing_end(cudaStream_t st, cudaEvent_t t0, cudaEvent_t t1) {
+  cudaEventRecord(t1, st);
+  std::lock_guard<std::mutex> lk(g_timing_mu);
+  g_timing_ev.emplace_back(t0, t1);
+}
+
 }  // namespace
 
 extern "C" {
@@ -90,6 +113,35 @@ const char* spcn_version(void) { return "spcn-b200 0.1.0 (sm_100a)"; }
 uint64_t spcn_launch_count(void) { return spcn::g_launches.load(std::memory_order_relaxed); }
 
 const char* spcn_xform_shape(void) { return spcn::xform_shape_name(); }
+
+int spcn_xform_timing_enable(int32_t on) {
+  g_timing.store(on ? 1 : 0);
+  return SPCN_OK;
+}
+
+int spcn_xform_timing(int64_t* launches, double* total_ms) {
+  g_err.clear();
+  if (!launches || !total_ms) return fail(SPCN_EINVAL, "NULL argument");
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  {
+    std::lock_guard<std::mutex> lk(g_timing_mu);
+    ev.swap(g_timing_ev);
+  }
+  double sum = 0.0;
+  cudaError_t err = cudaSuccess;
+  for (auto& p : ev) {
+    float ms = 0.f;
+    cudaError_t e = cudaEventSynchronize(p.second);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, p.first, p.second);
+    if (e != cudaSuccess && err == cudaSuccess) err = e;
+    sum += ms;
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  *launches = static_cast<int64_t>(ev.size());
+  *total_ms = sum;
+  return err == cudaSuccess ? SPCN_OK : cuda_fail(err, "xform_timing");
+}
 
 size_t spcn_xform_workspace_bytes(int64_t npix) {
   const int64_t cap = 65536 + (npix > 0 ? npix / 32 : 0);
@@ -250,8 +302,11 @@ int spcn_xform_rgb8(const uint8_t* src, uint8_t* dst, int64_t npix, const spcn_x
     alpha_bits = reinterpret_cast<const unsigned int*>(static_cast<char*>(workspace) + 8);
   if (head > 0 && (e = launch_xform_strict(src, dst, head, sp, st)) != cudaSuccess)
     return cuda_fail(e, "xform_head");
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (g_timing.load(std::memory_order_relaxed)) timing_begin(st, t0, t1);
   e = launch_xform_main(mode, src + 3 * head, dst + 3 * head, body, fp, sp, count, items, cap,
                         alpha_bits, st);
+  if (t0) timing_end(st, t0, t1);
   if (e != cudaSuccess) return cuda_fail(e, "xform_tma");
   if (exact && (e = launch_xform_repair(src + 3 * head, dst + 3 * head, body, sp, count, items, cap,
                                         st)) != cudaSuccess)
