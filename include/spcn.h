@@ -314,8 +314,33 @@ int spcn_stats_refine(const uint8_t* src, int64_t npix, const spcn_xform_params*
  * spcn_stats_table_scan: for every colour with table[rgb] > 0, the exact
  * fp64 densities in the reference's order (x[2i], x[2i+1]) and its count w[i]
  * (the first `cap`, in no particular order); n_out[0] += present colours,
- * n_out[1] += their pixels.  The p-th percentile follows from a weighted
- * select over the entries with x >= lo (see global_stats.py).            */
+ * n_out[1] += their pixels, n_out[2 + j] = max(n_out[2 + j], bits of the
+ * largest x_j) (4 entries, caller zeroes).  The p-th percentile follows from
+ * a weighted select over the entries with x >= lo (see global_stats.py).
+ * spcn_stats_cube_classes + spcn_stats_table_cube: the same table pass with a
+ * class table in front, built from the same params/white/lo into `classes`
+ * (SPCN_CUBE_CLASS_BYTES: 32 KiB of cell classes, one byte per 8x8x8 RGB
+ * cell, then the 2 MiB bitmap of candidate colours): most pixels are decided
+ * by one shared-memory byte.  Same table/counts contract as spcn_stats_table. */
+#define SPCN_CUBE_CLASS_BYTES ((32u << 10) + (2u << 20))
+int spcn_stats_cube_classes(const spcn_xform_params* p, int32_t white_threshold,
+                            const double* lo, uint8_t* classes, void* stream);
+int spcn_stats_table_cube(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
+                          int32_t white_threshold, const double* lo, const uint8_t* classes,
+                          unsigned long long* table, unsigned long long* counts, void* stream);
+/* Exact selection over table entries without sorting them: hist[j*nbins + b]
+ * += w[i] for the entries with x[2i+j] >= lo[j] in bin b = min(nbins-1,
+ * floor((x - lo[j]) * scale[j])) (caller zeroes; sum across ranks), then
+ * spcn_table_entries_collect lists the entries of bins [bins[2j], bins[2j+1]]
+ * of stain j as (vals[j*cap + k], wts[j*cap + k]), nsel[j] += their number
+ * (entries past cap are counted, not stored).                             */
+int spcn_table_entries_hist(const double* x, const unsigned long long* w, int64_t m,
+                            const double* lo, const double* scale, int32_t nbins,
+                            unsigned long long* hist, void* stream);
+int spcn_table_entries_collect(const double* x, const unsigned long long* w, int64_t m,
+                               const double* lo, const double* scale, int32_t nbins,
+                               const int32_t* bins, double* vals, unsigned long long* wts,
+                               unsigned long long cap, unsigned long long* nsel, void* stream);
 int spcn_stats_table(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
                      int32_t white_threshold, const double* lo, unsigned long long* table,
                      unsigned long long* counts, void* stream);

@@ -36,6 +36,8 @@ EXPORTS = (
     "spcn_select_kth", "spcn_render_synthetic",
     "spcn_batch_sizes", "spcn_batch_params", "spcn_xform_batch",
     "spcn_stats_hist", "spcn_stats_refine", "spcn_stats_table", "spcn_stats_table_scan",
+    "spcn_stats_cube_classes", "spcn_stats_table_cube", "spcn_table_entries_hist",
+    "spcn_table_entries_collect",
     "spcn_sample_visit",
     "spcn_readback", "spcn_last_error", "spcn_version", "spcn_launch_count", "spcn_xform_shape",
     "spcn_xform_timing_enable", "spcn_xform_timing",

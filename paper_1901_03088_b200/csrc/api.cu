@@ -753,6 +753,73 @@ int spcn_stats_table(const uint8_t* src, int64_t npix, const spcn_xform_params* 
   return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_table");
 }
 
+int spcn_stats_cube_classes(const spcn_xform_params* p, int32_t white_threshold,
+                            const double* lo, uint8_t* classes, void* stream) {
+  g_err.clear();
+  if (!lo || !classes) return fail(SPCN_EINVAL, "NULL argument");
+  static thread_local StatsArgs a;
+  static thread_local StrictP sp;
+  int rc = stats_setup(p, white_threshold, a, sp);
+  if (rc) return rc;
+  for (int j = 0; j < 2; ++j)
+    if (!(lo[j] > 0.0)) return fail(SPCN_EINVAL, "table pass needs lo > 0");
+  stats_linear_forms(sp, lo, a);
+  const cudaError_t e = launch_cube_class(a, classes, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_cube_classes");
+}
+
+int spcn_stats_table_cube(const uint8_t* src, int64_t npix, const spcn_xform_params* p,
+                          int32_t white_threshold, const double* lo, const uint8_t* classes,
+                          unsigned long long* table, unsigned long long* counts, void* stream) {
+  g_err.clear();
+  if (npix < 0) return fail(SPCN_EINVAL, "npix must be >= 0");
+  if (!lo || !classes || !table || !counts) return fail(SPCN_EINVAL, "NULL argument");
+  if (npix > 0 && !src) return fail(SPCN_EINVAL, "src is NULL");
+  if (npix > 0 && (reinterpret_cast<uintptr_t>(src) & 15))
+    return fail(SPCN_EINVAL, "src must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(classes) & 15)
+    return fail(SPCN_EINVAL, "classes must be 16-byte aligned");
+  static thread_local StatsArgs a;
+  static thread_local StrictP sp;
+  int rc = stats_setup(p, white_threshold, a, sp);
+  if (rc) return rc;
+  for (int j = 0; j < 2; ++j)
+    if (!(lo[j] > 0.0)) return fail(SPCN_EINVAL, "table pass needs lo > 0");
+  stats_linear_forms(sp, lo, a);
+  const cudaError_t e = launch_stats_cube(src, npix, a, classes, table, counts,
+                                          static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stats_table_cube");
+}
+
+int spcn_table_entries_hist(const double* x, const unsigned long long* w, int64_t m,
+                            const double* lo, const double* scale, int32_t nbins,
+                            unsigned long long* hist, void* stream) {
+  g_err.clear();
+  if (m < 0) return fail(SPCN_EINVAL, "m must be >= 0");
+  if (nbins < 1 || nbins > 8192) return fail(SPCN_EINVAL, "nbins must be in [1, 8192]");
+  if (!lo || !scale || !hist || (m > 0 && (!x || !w))) return fail(SPCN_EINVAL, "NULL argument");
+  for (int j = 0; j < 2; ++j)
+    if (!(scale[j] >= 0.0) || !std::isfinite(scale[j]) || !std::isfinite(lo[j]))
+      return fail(SPCN_EINVAL, "lo/scale must be finite, scale >= 0");
+  const cudaError_t e = launch_entries_hist(x, w, m, lo, scale, nbins, hist,
+                                            static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "table_entries_hist");
+}
+
+int spcn_table_entries_collect(const double* x, const unsigned long long* w, int64_t m,
+                               const double* lo, const double* scale, int32_t nbins,
+                               const int32_t* bins, double* vals, unsigned long long* wts,
+                               unsigned long long cap, unsigned long long* nsel, void* stream) {
+  g_err.clear();
+  if (m < 0) return fail(SPCN_EINVAL, "m must be >= 0");
+  if (nbins < 1 || nbins > 8192) return fail(SPCN_EINVAL, "nbins must be in [1, 8192]");
+  if (!lo || !scale || !bins || !nsel || (m > 0 && (!x || !w)) || (cap > 0 && (!vals || !wts)))
+    return fail(SPCN_EINVAL, "NULL argument");
+  const cudaError_t e = launch_entries_collect(x, w, m, lo, scale, nbins, bins, vals, wts, cap,
+                                               nsel, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "table_entries_collect");
+}
+
 int spcn_stats_table_scan(const spcn_xform_params* p, const unsigned long long* table,
                           double* x, unsigned long long* w, unsigned long long cap,
                           unsigned long long* n_out, void* stream) {

@@ -39,10 +39,10 @@ constexpr int kSlicePx = 512;            // one TMA bulk load: 512 px = 1536 B
 constexpr int kSliceBytes = 3 * kSlicePx;
 
 // Ring geometry: CW warps per CTA, NSW slots per warp.
-template <int CW, int NSW>
+template <int CW, int NSW, int NSUB = 1>
 struct StRing {
   static constexpr int kThreads = 32 * CW;
-  static constexpr size_t kBytes = (size_t)CW * NSW * kSliceBytes + (size_t)CW * NSW * 8;
+  static constexpr size_t kBytes = (size_t)CW * NSW * NSUB * kSliceBytes + (size_t)CW * NSW * 8;
 };
 // histogram pass: 32 warps (<= 64 registers), 2 slots each
 #ifndef SPCN_HIST_CW
@@ -68,9 +68,16 @@ __device__ __forceinline__ uint32_t st_byte(const uint32_t* w, int idx) {
 // bytes, also readable at blk until body returns; inv = all ones for a lane
 // past the end of a short slice, whose pixels must all be ignored).  The
 // < 16-px tail is read from global memory by one lane: body(w, nvalid, 0, w).
-template <int CW, int NSW, class Body>
+struct NoAfter {
+  __device__ void operator()(const uint8_t*) const {}
+};
+
+// NSUB 512-px blocks per slice (each lane: NSUB x 16 px per slice, body once
+// per block); after(slot) runs once per slice after its blocks, warp-wide.
+template <int CW, int NSW, int NSUB = 1, class Body, class After = NoAfter>
 __device__ __forceinline__ void st_scan(const uint8_t* __restrict__ src, int64_t npix,
-                                        uint8_t* ring, Body&& body) {
+                                        uint8_t* ring, Body&& body, After&& after = After()) {
+  constexpr int kSlicePx = 512 * NSUB, kSliceBytes = 3 * kSlicePx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* myslots = ring + (size_t)warp * NSW * kSliceBytes;
   uint64_t* mybar = reinterpret_cast<uint64_t*>(ring + (size_t)CW * NSW * kSliceBytes) + warp * NSW;
@@ -94,25 +101,33 @@ __device__ __forceinline__ void st_scan(const uint8_t* __restrict__ src, int64_t
     for (int k = 0; k < NSW; ++k) issue(k);
   }
   __syncwarp();
-  for (int64_t k = 0;; ++k) {
-    const int64_t j = gw + k * GW;
+  int s = 0;
+  uint32_t phase = 0;
+  for (int k = 0;; ++k) {   // a warp's iterations fit 32 bits (slices / warps of the grid)
+    const int64_t j = gw + (int64_t)k * GW;
     if (j >= nsl) break;
-    const int s = (int)(k % NSW);
-    mbar_wait(&mybar[s], (uint32_t)((k / NSW) & 1));
+    mbar_wait(&mybar[s], phase);
     const int64_t left = nbody - j * kSlicePx;
-    {   // no divergent branch: lanes past the end of a short slice run on
-        // stale slot bytes with every pixel masked (body's `all_invalid`)
-      const uint4* q = reinterpret_cast<const uint4*>(myslots + s * kSliceBytes + 48 * lane);
+#pragma unroll
+    for (int u = 0; u < NSUB; ++u) {
+      // no divergent branch: lanes past the end of a short slice run on
+      // stale slot bytes with every pixel masked (body's `all_invalid`)
+      const uint8_t* blk = myslots + s * kSliceBytes + 1536 * u + 48 * lane;
+      const uint4* q = reinterpret_cast<const uint4*>(blk);
       const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
       const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y,
                               q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
-      body(w, 16, 16 * lane < left ? 0u : ~0u,
-           myslots + s * kSliceBytes + 48 * lane);
+      body(w, 16, 512 * u + 16 * lane < left ? 0u : ~0u, blk);
     }
+    after(myslots + s * kSliceBytes);
     __syncwarp();
     if (lane == 0) {
       fence_proxy_async_smem();   // the warp's reads of slot s precede its refill
       issue(k + NSW);
+    }
+    if (++s == NSW) {
+      s = 0;
+      phase ^= 1u;
     }
   }
   if (npix > nbody && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -654,9 +669,310 @@ __global__ void __launch_bounds__(256) k_table_scan(const unsigned long long* __
       x[2 * i + 1] = h1;
       w[i] = n;
     }
+    // per-stain maximum (densities are >= 0: the bit patterns order like the values)
+    atomicMax(&n_out[2], (unsigned long long)__double_as_longlong(h0));
+    atomicMax(&n_out[3], (unsigned long long)__double_as_longlong(h1));
   }
   for (int off = 16; off; off >>= 1) pix += __shfl_xor_sync(0xffffffffu, pix, off);
   if ((threadIdx.x & 31) == 0 && pix) atomicAdd(&n_out[1], pix);
+}
+
+// ---------------------------------------------------------------------------
+// Colour-cube classes in front of the one-pass table (k_stats_cube).  The RGB
+// cube is cut into 32^3 cells of 8x8x8 colours; every cell gets one class
+// from its 512 colours, evaluated with exactly the per-pixel tests:
+//   0  every colour white                      -> the pixel is skipped
+//   1  every colour non-white and surely below -> counted as non-white only
+//   2  anything else (white and non-white colours, or some candidate)
+//      -> per-pixel white test and candidate test (table insert)
+// so almost every pixel costs one shared-memory byte lookup instead of three
+// OD lookups and four fp32 linear forms.
+constexpr int kCubeCells = 1 << 15;
+
+__device__ __forceinline__ uint32_t cube_cell(uint32_t rgb) {   // r | g << 8 | b << 16
+  return ((rgb >> 3) & 0x1Fu) | ((rgb >> 6) & 0x3E0u) | ((rgb >> 9) & 0x7C00u);
+}
+
+// Not surely below lo in some stain: one of the four linear upper-bound forms
+// (stats_linear_forms, fp32 with the rounding bound folded in) is >= 0.  The
+// same expression serves the class builder and the pass.
+__device__ __forceinline__ bool cube_candidate(const StatsArgs& a, float v0, float v1, float v2) {
+  uint32_t all_neg = 0xffffffffu;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    all_neg &= __float_as_uint(__fmaf_rn(a.lf[i][0], v0,
+                                         __fmaf_rn(a.lf[i][1], v1, __fmaf_rn(a.lf[i][2], v2, a.lf[i][3]))));
+  return !(all_neg >> 31);
+}
+
+__global__ void __launch_bounds__(256) k_cube_class(const __grid_constant__ StatsArgs a,
+                                                    uint8_t* __restrict__ cls) {
+  __shared__ float lut[3 * 256];
+  for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = a.lut[i >> 8][i & 255];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int cell = blockIdx.x * 8 + (threadIdx.x >> 5); cell < kCubeCells; cell += gridDim.x * 8) {
+    const uint32_t r0 = (cell & 31) << 3, g0 = ((cell >> 5) & 31) << 3, b0 = (cell >> 10) << 3;
+    bool any_cand = false, any_white = false, any_nonwhite = false;
+    for (int t = 0; t < 16; ++t) {
+      const int i = lane * 16 + t;
+      const uint32_t r = r0 + (i & 7), g = g0 + ((i >> 3) & 7), b = b0 + (i >> 6);
+      const bool white = r > a.white && g > a.white && b > a.white;
+      any_white |= white;
+      any_nonwhite |= !white;
+      if (!white) any_cand |= cube_candidate(a, lut[r], lut[256 + g], lut[512 + b]);
+    }
+    any_cand = __any_sync(0xffffffffu, any_cand);
+    any_white = __any_sync(0xffffffffu, any_white);
+    any_nonwhite = __any_sync(0xffffffffu, any_nonwhite);
+    if (lane == 0) cls[cell] = any_cand ? 2 : (!any_nonwhite ? 0 : (!any_white ? 1 : 2));
+  }
+}
+
+// Candidate-colour bitmap (2^24 bits, rgb order): bit = non-white and not
+// surely below (cube_candidate) — the same test the cell classes aggregate,
+// read per pixel by the few class-2 pixels of k_stats_cube instead of
+// evaluating the OD table and the four linear forms.
+constexpr size_t kCandBitmapBytes = (size_t)1 << 21;
+
+__global__ void __launch_bounds__(256) k_cand_bitmap(const __grid_constant__ StatsArgs a,
+                                                     uint32_t* __restrict__ bits) {
+  __shared__ float lut[3 * 256];
+  for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = a.lut[i >> 8][i & 255];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  // a warp per word: lane t evaluates colour 32 * word + t
+  for (uint32_t word = blockIdx.x * 8 + (threadIdx.x >> 5); word < (1u << 19);
+       word += gridDim.x * 8) {
+    const uint32_t c = 32u * word + lane;
+    const uint32_t r = c & 255u, g = (c >> 8) & 255u, b = c >> 16;
+    const bool white = r > a.white && g > a.white && b > a.white;
+    const bool cand = !white && cube_candidate(a, lut[r], lut[256 + g], lut[512 + b]);
+    const uint32_t m = __ballot_sync(0xffffffffu, cand);
+    if (lane == 0) bits[word] = m;
+  }
+}
+
+// The one-pass table of k_stats_table with the cell classes in front: same
+// contract (table[rgb] counts the non-white pixels not surely below lo in
+// some stain, counts[0] the non-white pixels), pixels in class-0/1 cells
+// decided by the class alone.  Shared memory: class table 32 KB, fp32 OD
+// table (3 KB, read by the few class-2 pixels only), colour cache, TMA ring.
+// 32 warps x 2 ring slots of 512 px (measured at 10 Gpx: 16 warps x 2 slots
+// of 1024 px 11.9 ms, 32 x 3 slots 10.2 ms, this 9.6-9.7 ms).
+constexpr int kCubeCW = 32, kCubeNSW = 2, kCubeNSUB = 1;
+constexpr int kCubeQueue = 256;   // queued marked pixels per warp (flushed when full)
+constexpr int kCubeSlots = 2048;           // colour cache (a slide's candidate colours are few)
+// Shared-memory layout: colour cache, OD table and queues from the window
+// base; the class table at the ABSOLUTE shared address kCubeAbs (so a cell
+// index plus an immediate is its address: no base add per pixel); the TMA
+// ring above it.
+constexpr uint32_t kCubeAbs = 0x9000;
+constexpr size_t kCubeLow = (size_t)kCubeSlots * 8 + (size_t)kCubeCW * kCubeQueue * sizeof(uint16_t);
+static_assert(kCubeLow <= kCubeAbs - 4096, "cube pass: low region must leave room for the window base");
+constexpr size_t kStSmemCube = kCubeAbs + kCubeCells + StRing<kCubeCW, kCubeNSW, kCubeNSUB>::kBytes;
+
+__device__ __forceinline__ uint32_t lds_u8_cube(uint32_t cell) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1+36864];" : "=r"(v) : "r"(cell));   // + kCubeAbs
+  return v;
+}
+
+__device__ __forceinline__ uint32_t st_rgb(const uint32_t* w, int k) {   // pixel k's r|g<<8|b<<16 (+ junk byte 3)
+  const int j = 3 * k, o = j & 3;
+  const uint32_t sel = (uint32_t)o | ((uint32_t)(o + 1) << 4) | ((uint32_t)(o + 2) << 8);
+  return __byte_perm(w[j >> 2], w[(j >> 2) + (o >= 2 ? 1 : 0)], sel);
+}
+
+// One marked (class 2) pixel: exact white test, candidate test (one bit of
+// the k_cand_bitmap bitmap: the same test as cube_candidate) and the
+// colour-table insert.  Returns 1 if non-white.
+__device__ __forceinline__ int32_t cube_marked_pixel(const uint8_t* px, uint32_t white,
+                                                     const uint32_t* __restrict__ cbits,
+                                                     uint32_t* ckey, uint32_t* ccnt,
+                                                     unsigned long long* __restrict__ table) {
+  const uint32_t r = px[0], g = px[1], b = px[2];
+  if (r > white && g > white && b > white) return 0;
+  const uint32_t rgb = r | (g << 8) | (b << 16);
+  if (!((__ldg(&cbits[rgb >> 5]) >> (rgb & 31)) & 1u)) return 1;   // surely below (k_cand_bitmap)
+  uint32_t sl = (rgb * 2654435761u) >> 21;   // 11-bit hash
+  for (int probe = 0; probe < 8; ++probe, sl = (sl + 1) & (kCubeSlots - 1)) {
+    uint32_t key = ckey[sl];
+    if (key == kEmpty) {
+      const uint32_t prev = atomicCAS(&ckey[sl], kEmpty, rgb);
+      key = prev == kEmpty ? rgb : prev;
+    }
+    if (key == rgb) {
+      atomicAdd(&ccnt[sl], 1u);
+      return 1;
+    }
+  }
+  atomicAdd(&table[rgb], 1ull);    // cache full around this hash
+  return 1;
+}
+
+__global__ void __launch_bounds__(32 * kCubeCW, 1)
+    k_stats_cube(const uint8_t* __restrict__ src, int64_t npix, const __grid_constant__ StatsArgs a,
+                 const uint8_t* __restrict__ gcls, unsigned long long* __restrict__ table,
+                 unsigned long long* __restrict__ counts) {
+  const uint32_t* cbits = reinterpret_cast<const uint32_t*>(gcls + kCubeCells);
+  constexpr int kThreads = 32 * kCubeCW;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t base = smem_u32(smem);
+  if (base + kCubeLow > kCubeAbs) __trap();   // layout assumption (window base <= 4 KB)
+  uint32_t* ckey = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* ccnt = ckey + kCubeSlots;
+  uint16_t* queue = reinterpret_cast<uint16_t*>(ccnt + kCubeSlots) + (threadIdx.x >> 5) * kCubeQueue;
+  uint8_t* cls = smem + (kCubeAbs - base);
+  uint8_t* ring = cls + kCubeCells;
+  for (int i = threadIdx.x; i < kCubeCells / 16; i += kThreads)
+    reinterpret_cast<uint4*>(cls)[i] = reinterpret_cast<const uint4*>(gcls)[i];
+  for (int i = threadIdx.x; i < kCubeSlots; i += kThreads) {
+    ckey[i] = kEmpty;
+    ccnt[i] = 0;
+  }
+  __syncthreads();
+  const uint32_t white = a.white;
+  const int lane = threadIdx.x & 31;
+  int32_t nonwhite = 0;
+  int qn = 0;   // marked pixels queued in this slice (warp-uniform)
+  st_scan<kCubeCW, kCubeNSW, kCubeNSUB>(src, npix, ring,
+                             [&](const uint32_t* w, int nv, uint32_t inv, const uint8_t* blk) {
+    // the 16 classes side by side, 2 bits each (class <= 2: no carries).
+    // Cell index with few ALU operations: the 5-bit cell coordinates of every
+    // byte first (two operations per word), then per pixel one PRMT (its
+    // top byte a sign-replicated zero) and y - 224 (y >> 8) - 7168 (y >> 16)
+    // = r5 + 32 g5 + 1024 b5 — the multiply-adds run on the FMA pipe.
+    uint32_t w5[12];
+#pragma unroll
+    for (int t = 0; t < 12; ++t) w5[t] = (w[t] >> 3) & 0x1F1F1F1Fu;
+    uint32_t c2 = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int j = 3 * k, o = j & 3;
+      const uint32_t sel = (uint32_t)o | ((uint32_t)(o + 1) << 4) | ((uint32_t)(o + 2) << 8) |
+                           ((8u | (uint32_t)o) << 12);        // byte 3: sign of byte o = 0
+      uint32_t y;   // prmt with the sign-replicate bit (__byte_perm drops it)
+      asm("prmt.b32 %0, %1, %2, %3;"
+          : "=r"(y) : "r"(w5[j >> 2]), "r"(w5[(j >> 2) + (o >= 2 ? 1 : 0)]), "r"(sel));
+      c2 += lds_u8_cube(y - 224u * __umulhi(y, 1u << 24) - 7168u * __umulhi(y, 1u << 16))
+            << (2 * k);
+    }
+    if (nv < 16) c2 &= (1u << (2 * nv)) - 1u;   // the short tail: drop pixels past the end
+    c2 &= ~inv;                                 // lanes past the end of a short slice
+    nonwhite += __popc(c2 & 0x55555555u);       // class 1: non-white, surely below
+    uint32_t mark = c2 & 0xAAAAAAAAu;           // class 2: bit 2k+1
+    if (nv < 16) {   // the short tail (one thread): serial path
+      while (mark) {
+        const int k = (__ffs(mark) - 1) >> 1;
+        mark &= mark - 1;
+        nonwhite += cube_marked_pixel(blk + 3 * k, white, cbits, ckey, ccnt, table);
+      }
+      return;
+    }
+    // queue the marked pixels (byte offsets in the warp's slot) for the
+    // warp-cooperative pass after the slice's blocks
+    const int cnt = __popc(mark);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t off0 = (uint32_t)(blk - ring) % (uint32_t)(kCubeNSUB * kSliceBytes);
+    if (total > kCubeQueue) {        // a block this dense in marks: every lane its own
+      while (mark) {
+        const int k = (__ffs(mark) - 1) >> 1;
+        mark &= mark - 1;
+        nonwhite += cube_marked_pixel(blk + 3 * k, white, cbits, ckey, ccnt, table);
+      }
+      return;
+    }
+    if (qn + total > kCubeQueue) {   // queue full: work it off now (warp-uniform)
+      const uint8_t* slot = blk - off0;
+      __syncwarp();
+      for (int i = lane; i < qn; i += 32)
+        nonwhite += cube_marked_pixel(slot + queue[i], white, cbits, ckey, ccnt, table);
+      __syncwarp();
+      qn = 0;
+    }
+    int pos = qn + incl - cnt;
+    qn += total;
+    while (mark) {
+      const int bit = __ffs(mark) - 1;
+      mark &= mark - 1;
+      queue[pos++] = (uint16_t)(off0 + 3 * (bit >> 1));
+    }
+  }, [&](const uint8_t* slot) {
+    // every lane takes queued pixels in turn: no lane idles while another
+    // works through its own list
+    __syncwarp();
+    for (int i = lane; i < qn; i += 32)
+      nonwhite += cube_marked_pixel(slot + queue[i], white, cbits, ckey, ccnt, table);
+    qn = 0;
+  });
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCubeSlots; i += kThreads)
+    if (ccnt[i]) atomicAdd(&table[ckey[i]], (unsigned long long)ccnt[i]);
+  unsigned long long nwl = (unsigned long long)nonwhite;
+  for (int off = 16; off; off >>= 1) nwl += __shfl_xor_sync(0xffffffffu, nwl, off);
+  if ((threadIdx.x & 31) == 0 && nwl) atomicAdd(&counts[0], nwl);
+}
+
+// ---------------------------------------------------------------------------
+// Exact selection over the table entries (x[2i+j], w[i]) of k_table_scan,
+// without sorting them: a weighted histogram of each stain's entries with
+// x >= lo_j over nbins equal bins of [lo_j, lo_j + nbins / scale_j] (the host
+// sums it across ranks and finds the bins holding the requested ranks), then
+// the entries of bins [b0_j, b1_j] listed as (value, weight) for an exact
+// weighted select of the few that remain.  Both kernels compute the bin with
+// the same expression, so an entry is listed iff it was counted in those bins.
+__device__ __forceinline__ int64_t entry_bin(double x, double lo, double scale, int nbins) {
+  if (!(x >= lo)) return -1;
+  const double f = (x - lo) * scale;
+  return f >= (double)(nbins - 1) ? nbins - 1 : (int64_t)f;
+}
+
+__global__ void __launch_bounds__(256) k_entries_hist(const double* __restrict__ x,
+                                                      const unsigned long long* __restrict__ w,
+                                                      int64_t m, double lo0, double lo1,
+                                                      double sc0, double sc1, int nbins,
+                                                      unsigned long long* __restrict__ hist) {
+  extern __shared__ unsigned long long sh[];   // 2 x nbins
+  for (int i = threadIdx.x; i < 2 * nbins; i += 256) sh[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < m; i += 256ll * gridDim.x) {
+    const unsigned long long n = w[i];
+    const int64_t b0 = entry_bin(x[2 * i], lo0, sc0, nbins);
+    const int64_t b1 = entry_bin(x[2 * i + 1], lo1, sc1, nbins);
+    if (b0 >= 0) atomicAdd(&sh[b0], n);
+    if (b1 >= 0) atomicAdd(&sh[nbins + b1], n);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * nbins; i += 256)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void __launch_bounds__(256) k_entries_collect(
+    const double* __restrict__ x, const unsigned long long* __restrict__ w, int64_t m,
+    double lo0, double lo1, double sc0, double sc1, int nbins, int b00, int b01, int b10, int b11,
+    double* __restrict__ vals, unsigned long long* __restrict__ wts, unsigned long long cap,
+    unsigned long long* __restrict__ nsel) {
+  for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < m; i += 256ll * gridDim.x) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double v = x[2 * i + j];
+      const int64_t b = entry_bin(v, j ? lo1 : lo0, j ? sc1 : sc0, nbins);
+      if (b >= (j ? b10 : b00) && b <= (j ? b11 : b01)) {
+        const unsigned long long k = atomicAdd(&nsel[j], 1ull);
+        if (k < cap) {
+          vals[j * cap + k] = v;
+          wts[j * cap + k] = w[i];
+        }
+      }
+    }
+  }
 }
 
 static int st_grid() {
@@ -736,6 +1052,65 @@ cudaError_t launch_stats_table(const uint8_t* src, int64_t npix, const StatsArgs
   (a.white_by_od ? k_stats_table<true> : k_stats_table<false>)<<<(int)grid, 32 * kRefCW,
                                                                  kStSmemTable, st>>>(
       src, npix, a, table, counts);
+  return launched();
+}
+
+cudaError_t launch_cube_class(const StatsArgs& a, uint8_t* cls, cudaStream_t st) {
+  k_cube_class<<<kCubeCells / 8, 256, 0, st>>>(a, cls);
+  cudaError_t e = launched();
+  if (e != cudaSuccess) return e;
+  k_cand_bitmap<<<8 * st_grid(), 256, 0, st>>>(a, reinterpret_cast<uint32_t*>(cls + kCubeCells));
+  return launched();
+}
+
+cudaError_t launch_stats_cube(const uint8_t* src, int64_t npix, const StatsArgs& a,
+                              const uint8_t* cls, unsigned long long* table,
+                              unsigned long long* counts, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_stats_cube, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStSmemCube);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (npix <= 0) return cudaSuccess;
+  const int64_t nsl = (npix + kCubeNSUB * kSlicePx - 1) / (kCubeNSUB * kSlicePx);
+  int64_t grid = (nsl + kCubeCW - 1) / kCubeCW;
+  if (grid > st_grid()) grid = st_grid();
+  k_stats_cube<<<(int)grid, 32 * kCubeCW, kStSmemCube, st>>>(src, npix, a, cls, table, counts);
+  return launched();
+}
+
+cudaError_t launch_entries_hist(const double* x, const unsigned long long* w, int64_t m,
+                                const double* lo, const double* scale, int nbins,
+                                unsigned long long* hist, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  int64_t grid = (m + 255) / 256;
+  if (grid > 4 * st_grid()) grid = 4 * st_grid();
+  const size_t smem = 2 * (size_t)nbins * sizeof(unsigned long long);
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_entries_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_entries_hist<<<(int)grid, 256, smem, st>>>(x, w, m, lo[0], lo[1], scale[0], scale[1], nbins,
+                                               hist);
+  return launched();
+}
+
+cudaError_t launch_entries_collect(const double* x, const unsigned long long* w, int64_t m,
+                                   const double* lo, const double* scale, int nbins,
+                                   const int32_t* bins, double* vals, unsigned long long* wts,
+                                   unsigned long long cap, unsigned long long* nsel,
+                                   cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  int64_t grid = (m + 255) / 256;
+  if (grid > 4 * st_grid()) grid = 4 * st_grid();
+  k_entries_collect<<<(int)grid, 256, 0, st>>>(x, w, m, lo[0], lo[1], scale[0], scale[1], nbins,
+                                               bins[0], bins[1], bins[2], bins[3], vals, wts, cap,
+                                               nsel);
   return launched();
 }
 

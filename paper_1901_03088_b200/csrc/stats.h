@@ -28,6 +28,18 @@ cudaError_t launch_stats_refine(const uint8_t* src, int64_t npix, const StatsArg
 cudaError_t launch_stats_table(const uint8_t* src, int64_t npix, const StatsArgs& a,
                                unsigned long long* table, unsigned long long* counts,
                                cudaStream_t st);
+cudaError_t launch_cube_class(const StatsArgs& a, uint8_t* cls, cudaStream_t st);
+cudaError_t launch_stats_cube(const uint8_t* src, int64_t npix, const StatsArgs& a,
+                              const uint8_t* cls, unsigned long long* table,
+                              unsigned long long* counts, cudaStream_t st);
+cudaError_t launch_entries_hist(const double* x, const unsigned long long* w, int64_t m,
+                                const double* lo, const double* scale, int nbins,
+                                unsigned long long* hist, cudaStream_t st);
+cudaError_t launch_entries_collect(const double* x, const unsigned long long* w, int64_t m,
+                                   const double* lo, const double* scale, int nbins,
+                                   const int32_t* bins, double* vals, unsigned long long* wts,
+                                   unsigned long long cap, unsigned long long* nsel,
+                                   cudaStream_t st);
 cudaError_t launch_table_scan(const unsigned long long* table, const StrictP& sp, double* x,
                               unsigned long long* w, unsigned long long cap,
                               unsigned long long* n_out, cudaStream_t st);

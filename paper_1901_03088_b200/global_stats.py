@@ -131,76 +131,139 @@ class DeviceEngine:
 def _table_sig():
     L = _sig()
     if not getattr(L, "_spcn_table_declared", False):
-        P, I32, I64 = _lib.P, _lib.I32, _lib.I64
-        _lib.declare("spcn_stats_table", ctypes.c_int,
-                     [P, I64, ctypes.POINTER(_lib.XformParams), I32, P, P, P, P])
-        _lib.declare("spcn_stats_table_scan", ctypes.c_int,
-                     [ctypes.POINTER(_lib.XformParams), P, P, P, ctypes.c_uint64, P, P])
+        P, I32, I64, U64 = _lib.P, _lib.I32, _lib.I64, ctypes.c_uint64
+        XP = ctypes.POINTER(_lib.XformParams)
+        _lib.declare("spcn_stats_table", ctypes.c_int, [P, I64, XP, I32, P, P, P, P])
+        _lib.declare("spcn_stats_table_scan", ctypes.c_int, [XP, P, P, P, U64, P, P])
+        _lib.declare("spcn_stats_cube_classes", ctypes.c_int, [XP, I32, P, P, P])
+        _lib.declare("spcn_stats_table_cube", ctypes.c_int, [P, I64, XP, I32, P, P, P, P, P])
+        _lib.declare("spcn_table_entries_hist", ctypes.c_int, [P, P, I64, P, P, I32, P, P])
+        _lib.declare("spcn_table_entries_collect", ctypes.c_int,
+                     [P, P, I64, P, P, I32, P, P, P, U64, P, P])
         L._spcn_table_declared = True
     return L
 
 
 TABLE_CAP = 1 << 22      # present colours handled by the one-pass mode (else: histogram path)
+SEL_BINS = 4096          # bins of the entry histogram (exact selection without a sort)
 
 
 def _device_table(self, lo):
     """One pass: colour counts (2^24, int64 view of u64) of the pixels not
-    surely below lo, and the non-white count."""
+    surely below lo, and the non-white count.  The 8x8x8 colour-cell classes
+    (32 KiB) are built once per call from the same parameters."""
     t, L = self.t, _table_sig()
     table = t.zeros(1 << 24, dtype=t.int64, device="cuda")
     counts = t.zeros(1, dtype=t.int64, device="cuda")
+    cls = t.empty((32 << 10) + (2 << 20), dtype=t.uint8, device="cuda")   # SPCN_CUBE_CLASS_BYTES
     a = _F64x2(*lo)
+    _lib.check(L.spcn_stats_cube_classes(ctypes.byref(self.plan.params), self.thr, ctypes.byref(a),
+                                         _lib.ptr(cls), _lib.stream_handle()), "stats_cube_classes")
     for x in self.chunks():
-        _lib.check(L.spcn_stats_table(_lib.ptr(x), x.numel() // 3, ctypes.byref(self.plan.params),
-                                      self.thr, ctypes.byref(a), _lib.ptr(table),
-                                      _lib.ptr(counts), _lib.stream_handle()), "stats_table")
+        _lib.check(L.spcn_stats_table_cube(_lib.ptr(x), x.numel() // 3,
+                                           ctypes.byref(self.plan.params), self.thr,
+                                           ctypes.byref(a), _lib.ptr(cls), _lib.ptr(table),
+                                           _lib.ptr(counts), _lib.stream_handle()),
+                   "stats_table_cube")
     return table, counts
 
 
 def _device_scan(self, table, cap=TABLE_CAP):
-    """Present colours of a (reduced) table: exact densities (m, 2) and pixel
-    counts (m,), or None when there are more than `cap` colours."""
+    """Present colours of this rank's table: exact densities (m, 2), pixel
+    counts (m,), the per-stain maxima (2,) and whether more than `cap`
+    colours were present (then the entries are incomplete)."""
     t, L = self.t, _table_sig()
     x = t.empty((cap, 2), dtype=t.float64, device="cuda")
     w = t.empty(cap, dtype=t.int64, device="cuda")
-    n_out = t.zeros(2, dtype=t.int64, device="cuda")
+    n_out = t.zeros(4, dtype=t.int64, device="cuda")
     _lib.check(L.spcn_stats_table_scan(ctypes.byref(self.plan.params), _lib.ptr(table),
                                        _lib.ptr(x), _lib.ptr(w), cap, _lib.ptr(n_out),
                                        _lib.stream_handle()), "stats_table_scan")
-    m = int(n_out[0].item())
-    if m > cap:
-        return None
-    return x[:m], w[:m]
+    info = _dev.readback(n_out)
+    m = int(info[0])
+    xmax = info[2:4].view(np.float64).copy()
+    return x[:min(m, cap)], w[:min(m, cap)], xmax, m > cap
+
+
+def _device_entries_hist(self, x, w, lo, scale, nbins):
+    t, L = self.t, _table_sig()
+    hist = t.zeros((2, nbins), dtype=t.int64, device="cuda")
+    _lib.check(L.spcn_table_entries_hist(_lib.ptr(x), _lib.ptr(w), int(w.numel()),
+                                         ctypes.byref(_F64x2(*lo)), ctypes.byref(_F64x2(*scale)),
+                                         nbins, _lib.ptr(hist), _lib.stream_handle()),
+               "table_entries_hist")
+    return hist
+
+
+def _device_entries_collect(self, x, w, lo, scale, nbins, bins):
+    """(values, weights) of stain j's entries in bins [bins[2j], bins[2j+1]]."""
+    t, L = self.t, _table_sig()
+    b = (ctypes.c_int32 * 4)(*[int(v) for v in bins])
+    cap = 1 << 16
+    while True:
+        vals = t.empty((2, cap), dtype=t.float64, device="cuda")
+        wts = t.empty((2, cap), dtype=t.int64, device="cuda")
+        nsel = t.zeros(2, dtype=t.int64, device="cuda")
+        _lib.check(L.spcn_table_entries_collect(_lib.ptr(x), _lib.ptr(w), int(w.numel()),
+                                                ctypes.byref(_F64x2(*lo)),
+                                                ctypes.byref(_F64x2(*scale)), nbins, b,
+                                                _lib.ptr(vals), _lib.ptr(wts), cap, _lib.ptr(nsel),
+                                                _lib.stream_handle()), "table_entries_collect")
+        k = _dev.readback(nsel)
+        if max(k) <= cap:
+            return [(vals[j, :int(k[j])], wts[j, :int(k[j])]) for j in range(2)]
+        cap = int(max(k))
 
 
 DeviceEngine.table = _device_table
 DeviceEngine.scan = _device_scan
+DeviceEngine.entries_hist = _device_entries_hist
+DeviceEngine.entries_collect = _device_entries_collect
 
 
-def _table_select(x, w, n: int, lo, ks):
-    """Order statistics `ks` (0-based ranks among the n non-white pixels) of
-    both stains from the colour table: pixels off the table are < lo[j], so
-    rank k is the (k - below_j)-th of the entries with x_j >= lo[j], below_j =
-    pixels off the table + table pixels with x_j < lo[j].  Returns (values
-    (2, len(ks)), below list) or None when a rank falls below lo."""
-    import torch as t   # tensor plumbing on the tables' device
-    vals, belows = [], []
-    total = w.sum()
-    for j in range(2):
-        keep = x[:, j] >= lo[j]
-        below = n - total + w[~keep].sum()
-        xs, order = t.sort(x[keep, j])
-        c = t.cumsum(w[keep][order], 0)
-        kk = t.tensor(ks, dtype=t.int64, device=x.device) - below
-        idx = t.searchsorted(c, kk, right=True).clamp_(max=max(int(xs.numel()) - 1, 0))
-        vals.append(xs[idx] if xs.numel() else t.zeros(len(ks), dtype=x.dtype, device=x.device))
-        belows.append(below.reshape(1))
-    packed = t.cat([vals[0], vals[1], t.cat(belows).to(x.dtype)]).cpu().numpy()
-    below = [int(packed[2 * len(ks)]), int(packed[2 * len(ks) + 1])]
-    if any(min(ks) < b for b in below) or int(total.item()) == 0:
+def _table_select(eng, x, w, xmax, n: int, lo, ks, comm):
+    """Order statistics `ks` (0-based ranks among the n non-white pixels of all
+    ranks) of both stains from the per-rank colour-table entries, exactly and
+    without sorting them: pixels off the tables are < lo[j], so rank k is the
+    (k - below_j)-th smallest of the entries with x_j >= lo[j] (below_j = n -
+    their weight).  A weighted histogram of those entries over SEL_BINS equal
+    bins of [lo_j, max_j] (summed across ranks: 64 KiB) gives the bins that
+    hold the ranks; only their entries are gathered and selected exactly.
+    Returns (values (2, len(ks)), below) or None when a rank falls below lo."""
+    xm = np.max(np.stack([np.asarray(v.cpu() if hasattr(v, "cpu") else v, dtype=np.float64)
+                          for v in comm.allgather(_as_tensor(xmax, x))]), axis=0)
+    scale = [SEL_BINS / (xm[j] - lo[j]) if xm[j] > lo[j] else 0.0 for j in range(2)]
+    hist = comm.allreduce(eng.entries_hist(x, w, lo, scale, SEL_BINS))
+    hist = hist.cpu().numpy() if hasattr(hist, "cpu") else np.asarray(hist)
+    kept = hist.sum(axis=1)
+    below = [int(n - kept[j]) for j in range(2)]
+    if int(kept.min()) == 0 or any(min(ks) < b for b in below):
         return None
-    k = len(ks)
-    return np.stack([packed[:k], packed[k:2 * k]]), below
+    bins, before = [], []
+    for j in range(2):
+        c = np.cumsum(hist[j])
+        r = [k - below[j] for k in ks]
+        b0 = int(np.searchsorted(c, min(r), side="right"))
+        b1 = int(np.searchsorted(c, max(r), side="right"))
+        if b1 >= SEL_BINS:
+            return None
+        bins += [b0, b1]
+        before.append(int(c[b0 - 1]) if b0 else 0)
+    lists = eng.entries_collect(x, w, lo, scale, SEL_BINS, bins)
+    vals = np.empty((2, len(ks)))
+    for j in range(2):
+        v = np.concatenate([np.asarray(a.cpu() if hasattr(a, "cpu") else a, dtype=np.float64)
+                            for a in comm.allgather(lists[j][0])])
+        c = np.concatenate([np.asarray(a.cpu() if hasattr(a, "cpu") else a, dtype=np.int64)
+                            for a in comm.allgather(lists[j][1])])
+        vals[j] = weighted_select(v, c, [k - below[j] - before[j] for k in ks])
+    return vals, below
+
+
+def _as_tensor(v, like):
+    import torch
+
+    return torch.as_tensor(np.asarray(v, dtype=np.float64), device=like.device)
 
 
 def sample_bracket(h, p: float = 99.0):
@@ -279,22 +342,22 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
     if g is not None and g.shape == (2, 2) and np.isfinite(g).all() and (g[:, 0] > 0).all() \
             and hasattr(eng, "table"):
         lo_t = [float(g[0, 0]), float(g[1, 0])]
-        tab, cnt = eng.table(lo_t)
+        tab, cnt = eng.table(lo_t)          # this rank's table: never exchanged
         info["passes"] += 1
-        tab, cnt = comm.allreduce(tab), comm.allreduce(cnt)
-        n = int(cnt.reshape(-1)[0].item())
+        n = int(comm.allreduce(cnt).reshape(-1)[0].item())
         if n == 0:
             raise StainAbsentError("stain absent: no non-white pixels in the slide")
         rank = (p / 100.0) * (n - 1)
         klo, khi = int(math.floor(rank)), int(math.ceil(rank))
-        sc = eng.scan(tab)
-        res = None if sc is None else _table_select(sc[0], sc[1], n, lo_t, [klo, khi])
+        x, w, xmax, over = eng.scan(tab)
+        del tab
+        over = int(comm.allreduce(_as_tensor([1.0 if over else 0.0], x)).cpu().numpy()[0])
+        res = None if over else _table_select(eng, x, w, xmax, n, lo_t, [klo, khi], comm)
         if res is not None:
             vals, below = res
             p99 = np.array([interpolate(vals[j][0], vals[j][1], rank) for j in range(2)])
-            info.update(mode="table", nonwhite=n, colours=int(sc[1].numel()), below=below,
-                        table_pixels=int(sc[1].sum().item()),
-                        fp64_evaluations=int(sc[1].numel()), levels=0)
+            info.update(mode="table", nonwhite=n, colours=int(w.numel()), below=below,
+                        fp64_evaluations=int(w.numel()), levels=0)
             return p99, n, info
         info["table_miss"] = True
 

@@ -187,7 +187,35 @@ class _TableEngine(_NumpyEngine):
 
         present = torch.nonzero(tab).reshape(-1)
         x = torch.from_numpy(np.ascontiguousarray(self.pal.T))[present]
-        return x, tab[present]
+        xmax = x.max(dim=0).values.numpy() if x.numel() else np.zeros(2)
+        return x, tab[present], xmax, False
+
+    # the selection kernels' contract (csrc/stats.cu k_entries_hist / _collect)
+    @staticmethod
+    def _bins(v, lo, scale, nbins):
+        b = np.minimum(np.floor((v - lo) * scale), nbins - 1).astype(np.int64)
+        return np.where(v >= lo, b, -1)
+
+    def entries_hist(self, x, w, lo, scale, nbins):
+        import torch
+
+        x, w = x.numpy(), w.numpy()
+        hist = np.zeros((2, nbins), np.int64)
+        for j in range(2):
+            b = self._bins(x[:, j], lo[j], scale[j], nbins)
+            np.add.at(hist[j], b[b >= 0], w[b >= 0])
+        return torch.from_numpy(hist)
+
+    def entries_collect(self, x, w, lo, scale, nbins, bins):
+        import torch
+
+        x, w = x.numpy(), w.numpy()
+        out = []
+        for j in range(2):
+            b = self._bins(x[:, j], lo[j], scale[j], nbins)
+            sel = (b >= bins[2 * j]) & (b <= bins[2 * j + 1])
+            out.append((torch.from_numpy(x[sel, j].copy()), torch.from_numpy(w[sel].copy())))
+        return out
 
 
 def _palette_slide(n, seed):
