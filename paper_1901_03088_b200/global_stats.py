@@ -266,21 +266,39 @@ def _as_tensor(v, like):
     return torch.as_tensor(np.asarray(v, dtype=np.float64), device=like.device)
 
 
+def bracket_ranks(m: int, p: float = 99.0):
+    """0-based ranks of the sample quantiles p -+ d of an m-sample (see
+    sample_bracket)."""
+    q = p / 100.0
+    d = max(0.005, 6.0 * math.sqrt(q * (1.0 - q) / m) * 10.0)
+    return [int(math.floor(max(0.0, q - d) * (m - 1))), int(math.ceil(min(1.0, q + d) * (m - 1)))]
+
+
 def sample_bracket(h, p: float = 99.0):
     """[lo, hi] per stain around the p-th percentile of the sampled densities
     `h` ((2, m) device tensor, one row per stain): the sample quantiles
     p -+ d, d = max(0.5, 600 * sqrt(p (1 - p) / m)) percent (6 standard errors
-    of the quantile at a 100x smaller effective sample).  One device sort, one
-    host read; None when the sample is empty."""
+    of the quantile at a 100x smaller effective sample).  Exact k-th
+    selections on the device (libspcn), one host read; None when the sample
+    is empty."""
     m = int(h.shape[1])
     if m == 0:
         return None
-    q = p / 100.0
-    d = max(0.005, 6.0 * math.sqrt(q * (1.0 - q) / m) * 10.0)
-    idx = [int(math.floor(max(0.0, q - d) * (m - 1))), int(math.ceil(min(1.0, q + d) * (m - 1)))]
+    idx = bracket_ranks(m, p)
     import torch as t   # tensor plumbing on h's device
-    srt = t.sort(h, dim=1).values
-    return srt[:, t.tensor(idx, device=h.device)].cpu().numpy()
+    from . import stats as dstats
+
+    L = dstats._sig()
+    v = h.contiguous()
+    # four exact selections (2 stains x 2 ranks) in one libspcn call, no sort
+    begin = t.tensor([0, 0, m, m], dtype=t.int64, device=h.device)
+    end = t.tensor([m, m, 2 * m, 2 * m], dtype=t.int64, device=h.device)
+    ks = t.tensor([idx[0], idx[1], idx[0], idx[1]], dtype=t.int64, device=h.device)
+    q = t.empty(4 * dstats._QBYTES, dtype=t.uint8, device=h.device)
+    out = t.empty(4, dtype=t.float64, device=h.device)
+    _lib.check(L.spcn_select_kth(_lib.ptr(v), _lib.ptr(begin), _lib.ptr(end), _lib.ptr(ks), 4,
+                                 _lib.ptr(q), _lib.ptr(out), _lib.stream_handle()), "select_kth")
+    return _dev.readback(out).reshape(2, 2)
 
 
 def weighted_select(values: np.ndarray, weights: np.ndarray, ks):

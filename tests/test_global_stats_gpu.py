@@ -135,3 +135,21 @@ def test_global_p99_large_slide_window_logic():
     p99, nw, info = global_p99(slide_chunks(pb.DeviceSource(dev)), i0, basis)
     assert nw == n and np.array_equal(p99, ref), (p99, ref, info)
     assert max(info["candidates"]) < 1 << 23
+
+
+def test_sample_bracket_selects_exact_order_statistics():
+    """sample_bracket = the exact order statistics at bracket_ranks (libspcn
+    k-th selection, no sort), and None for an empty sample."""
+    import torch
+
+    from paper_1901_03088_b200.global_stats import bracket_ranks, sample_bracket
+
+    rng = np.random.default_rng(5)
+    for m in (1, 7, 1000, 100_000):
+        h = np.stack([rng.gamma(2.0, 0.4, m), rng.gamma(1.5, 0.3, m)])
+        br = sample_bracket(torch.from_numpy(h).cuda())
+        lo, hi = bracket_ranks(m)
+        for j in range(2):
+            srt = np.sort(h[j])
+            assert br[j, 0] == srt[lo] and br[j, 1] == srt[hi]
+    assert sample_bracket(torch.zeros((2, 0), dtype=torch.float64, device="cuda")) is None
