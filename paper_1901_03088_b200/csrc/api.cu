@@ -958,27 +958,28 @@ int spcn_xform_batch(const uint8_t* src, uint8_t* dst, int32_t nitems, const int
   }
   if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
     return fail(SPCN_EINVAL, "src/dst must be 16-byte aligned");
-  unsigned long long* count = nullptr;
-  unsigned long long* items = nullptr;
-  unsigned long long cap = 0;
   cudaError_t e = cudaSuccess;
+  // EXACT: workspace = [per-CTA counters][per-item segments][per-CTA lists]
+  BatchRepair br{nullptr, nullptr, 0, nullptr};
   if (exact) {
-    if (!workspace || workspace_bytes < kWsHeader + 8)
+    const size_t grid = static_cast<size_t>(batch_grid(nitems));
+    const size_t head = 8 * grid + 24 * static_cast<size_t>(nitems);
+    if (!workspace || workspace_bytes < head + 8 * grid)
       return fail(SPCN_EINVAL, "EXACT precision needs a workspace");
-    count = static_cast<unsigned long long*>(workspace);
-    items = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + kWsHeader);
-    cap = (workspace_bytes - kWsHeader) / 8;
-    if ((e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), st)) != cudaSuccess)
+    br.counts = static_cast<unsigned long long*>(workspace);
+    br.seg = br.counts + grid;
+    br.items = br.seg + 3 * static_cast<size_t>(nitems);
+    br.cap_cta = (workspace_bytes - head) / 8 / grid;
+    if ((e = cudaMemsetAsync(br.counts, 0, 8 * grid, st)) != cudaSuccess)
       return cuda_fail(e, "memset");
   }
   if (!strict_all && any_fast) {
     // one persistent launch over every fast-path item (status 0)
-    e = launch_xform_batch(exact ? 0 : 1, src, dst, nitems, off_dev, status_dev, fs, flut, count,
-                           items, cap, st);
+    e = launch_xform_batch(exact ? 0 : 1, src, dst, nitems, off_dev, status_dev, fs, flut, br, st);
     if (e != cudaSuccess) return cuda_fail(e, "xform_batch");
-    if (exact && (e = launch_repair_batch(src, dst, sps, off_dev, status_dev, nitems, count, items,
-                                          cap, st)) != cudaSuccess)
-      return cuda_fail(e, "repair_batch");
+    if (exact && (e = launch_repair_items(src, dst, sps, off_dev, status_dev, nitems, br, st)) !=
+                     cudaSuccess)
+      return cuda_fail(e, "repair_items");
   }
   if (any_strict) {
     // strict items: status 1 (or every valid item in STRICT precision)

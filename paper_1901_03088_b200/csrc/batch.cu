@@ -13,8 +13,9 @@
 //   k_xform_batch      per-warp TMA rings over the item's 512-px slices, the
 //                      item's FastS read from the kernel-parameter block
 //                      (uniform across the CTA), its table from global memory;
-//   k_repair_batch     fp64 reference-order recompute of uncertified pixels,
-//                      item located by binary search over the pixel offsets.
+//   k_repair_items     fp64 reference-order recompute of uncertified pixels,
+//                      one CTA per item over its segment of the per-CTA
+//                      repair lists k_xform_batch wrote.
 #include "batch.h"
 #include "launch_count.h"
 #include "params.cuh"
@@ -72,6 +73,11 @@ __global__ void __launch_bounds__(128) k_build_params(
 }
 
 // ---------------------------------------------------------------- batched recolour
+struct SmemLut {
+  const double* t;
+  __device__ double operator()(int c, uint32_t i) const { return t[c * 256 + i]; }
+};
+
 struct GlobalLut {
   const StrictP* p;
   __device__ double operator()(int c, uint32_t x) const { return p->lut[c][x]; }
@@ -87,7 +93,12 @@ template <int MODE>
 __global__ void __launch_bounds__(32 * kBW, 1)
     k_xform_batch(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int nitems,
                   const int64_t* __restrict__ off, const int32_t* __restrict__ status,
-                  const FastS* __restrict__ fs, const float* __restrict__ flut, RepairList rl) {
+                  const FastS* __restrict__ fs, const float* __restrict__ flut,
+                  BatchRepair br) {
+  // EXACT: this CTA's own repair list (no contention with other CTAs); the
+  // items it recolours leave contiguous segments of it, recorded per item
+  // for k_repair_items
+  RepairList rl{br.counts + blockIdx.x, br.items + (size_t)blockIdx.x * br.cap_cta, br.cap_cta};
   extern __shared__ __align__(128) uint8_t smem[];
   const uint8_t* lut = smem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -135,8 +146,16 @@ __global__ void __launch_bounds__(32 * kBW, 1)
   }
 
   int64_t k = 0;   // this warp's consumed-slice sequence number
+  int prev = -1;
   for (int it = next_item(blockIdx.x); it < nitems; it = next_item(it + G)) {
     __syncthreads();                                   // previous item's table no longer read
+    if (MODE == 0 && tid == 0) {                       // segment bookkeeping (EXACT)
+      const unsigned long long c = *(volatile unsigned long long*)rl.count;
+      if (prev >= 0) br.seg[3 * prev + 1] = c;
+      br.seg[3 * it] = c;
+      br.seg[3 * it + 2] = blockIdx.x;
+      prev = it;
+    }
     LutLayout<kBRep>::fill(smem, flut + (int64_t)it * 768, tid, 32 * kBW);
     const FastS fp = fs[it];
     __syncthreads();
@@ -163,44 +182,50 @@ __global__ void __launch_bounds__(32 * kBW, 1)
       }
     }
   }
+  if (MODE == 0) {
+    __syncthreads();
+    if (tid == 0 && prev >= 0) br.seg[3 * prev + 1] = *(volatile unsigned long long*)rl.count;
+  }
   if (lane == 0) bulk_wait_all();
 }
 
-// fp64 repair of the listed pixels (item found by binary search over the
-// offsets); if the list overflowed, every fast-path item is recomputed.
-__global__ void __launch_bounds__(256) k_repair_batch(const uint8_t* __restrict__ src,
+// fp64 repair, one CTA per item: the item's segment of its CTA's list (the
+// pixels k_xform_batch could not certify), with the item's fp64 OD table in
+// shared memory and its Gram factors formed once; if the segment overflowed
+// the CTA's list, every pixel of the item is recomputed instead.  Exact
+// either way (strict_pixel = the reference's operation order).
+__global__ void __launch_bounds__(256) k_repair_items(const uint8_t* __restrict__ src,
                                                       uint8_t* __restrict__ dst,
                                                       const StrictP* __restrict__ sps,
                                                       const int64_t* __restrict__ off,
                                                       const int32_t* __restrict__ status,
-                                                      int nitems, RepairList rl) {
-  const unsigned long long n = *rl.count;
-  if (n > rl.cap) {
-    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-      if (status[it] != 0) continue;
-      const StrictP& sp = sps[it];
-      const NnlsGram G = gram_of(sp);
-      for (int64_t i = off[it] + threadIdx.x; i < off[it + 1]; i += 256) {
-        const uint32_t out = strict_pixel(sp, G, GlobalLut{&sp}, src[3 * i], src[3 * i + 1],
-                                          src[3 * i + 2]);
-        dst[3 * i] = out & 255u;
-        dst[3 * i + 1] = (out >> 8) & 255u;
-        dst[3 * i + 2] = (out >> 16) & 255u;
-      }
+                                                      int nitems, BatchRepair br) {
+  const int it = blockIdx.x;
+  if (it >= nitems || status[it] != 0) return;
+  const unsigned long long s0 = br.seg[3 * it], s1 = br.seg[3 * it + 1];
+  if (s1 <= s0) return;                               // nothing to repair
+
+  __shared__ double lut[3 * 256];
+  const StrictP& sp = sps[it];
+  for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
+  __syncthreads();
+  const NnlsGram G = gram_of(sp);
+  if (s1 > br.cap_cta) {                              // the list overflowed: whole item
+    for (int64_t i = off[it] + threadIdx.x; i < off[it + 1]; i += 256) {
+      const uint32_t out = strict_pixel(sp, G, SmemLut{lut}, src[3 * i], src[3 * i + 1],
+                                        src[3 * i + 2]);
+      dst[3 * i] = out & 255u;
+      dst[3 * i + 1] = (out >> 8) & 255u;
+      dst[3 * i + 2] = (out >> 16) & 255u;
     }
     return;
   }
-  for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += 256ull * gridDim.x) {
-    const unsigned long long v = rl.items[i];
+  const unsigned long long* items = br.items + (size_t)br.seg[3 * it + 2] * br.cap_cta;
+  for (unsigned long long i = s0 + threadIdx.x; i < s1; i += 256) {
+    const unsigned long long v = items[i];
     const uint32_t rgb = static_cast<uint32_t>(v & 0xffffffu);
     const int64_t gp = static_cast<int64_t>(v >> 24);
-    int lo = 0, hi = nitems;          // find item: off[lo] <= gp < off[lo+1]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (off[mid] <= gp) lo = mid; else hi = mid;
-    }
-    const uint32_t out = strict_pixel(sps[lo], GlobalLut{sps + lo}, rgb & 255u, (rgb >> 8) & 255u,
-                                      rgb >> 16);
+    const uint32_t out = strict_pixel(sp, G, SmemLut{lut}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
     dst[3 * gp] = out & 255u;
     dst[3 * gp + 1] = (out >> 8) & 255u;
     dst[3 * gp + 2] = (out >> 16) & 255u;
@@ -239,11 +264,20 @@ cudaError_t launch_build_params(int nitems, const double* i0, const double* luts
   return launched();
 }
 
+int batch_grid(int nitems) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  return nitems < sms ? nitems : sms;
+}
+
 cudaError_t launch_xform_batch(int mode, const uint8_t* src, uint8_t* dst, int nitems,
                                const int64_t* off, const int32_t* status, const FastS* fs,
-                               const float* flut, unsigned long long* rcount,
-                               unsigned long long* ritems, unsigned long long rcap,
-                               cudaStream_t st) {
+                               const float* flut, const BatchRepair& br, cudaStream_t st) {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -261,24 +295,19 @@ cudaError_t launch_xform_batch(int mode, const uint8_t* src, uint8_t* dst, int n
     }
   }
   if (nitems <= 0) return cudaSuccess;
-  const int grid = nitems < sms ? nitems : sms;
-  RepairList rl{rcount, ritems, rcap};
+  const int grid = batch_grid(nitems);
   if (mode == 1)
-    k_xform_batch<1><<<grid, 32 * kBW, kBSmem, st>>>(src, dst, nitems, off, status, fs, flut, rl);
+    k_xform_batch<1><<<grid, 32 * kBW, kBSmem, st>>>(src, dst, nitems, off, status, fs, flut, br);
   else
-    k_xform_batch<0><<<grid, 32 * kBW, kBSmem, st>>>(src, dst, nitems, off, status, fs, flut, rl);
+    k_xform_batch<0><<<grid, 32 * kBW, kBSmem, st>>>(src, dst, nitems, off, status, fs, flut, br);
   return launched();
 }
 
-cudaError_t launch_repair_batch(const uint8_t* src, uint8_t* dst, const StrictP* sps,
+cudaError_t launch_repair_items(const uint8_t* src, uint8_t* dst, const StrictP* sps,
                                 const int64_t* off, const int32_t* status, int nitems,
-                                unsigned long long* rcount, unsigned long long* ritems,
-                                unsigned long long rcap, cudaStream_t st) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  k_repair_batch<<<sms * 4, 256, 0, st>>>(src, dst, sps, off, status, nitems,
-                                          RepairList{rcount, ritems, rcap});
+                                const BatchRepair& br, cudaStream_t st) {
+  if (nitems <= 0) return cudaSuccess;
+  k_repair_items<<<nitems, 256, 0, st>>>(src, dst, sps, off, status, nitems, br);
   return launched();
 }
 
