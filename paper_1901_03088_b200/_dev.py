@@ -1,6 +1,8 @@
 """Device plumbing (PyTorch is used for memory, streams and copies only)."""
 from __future__ import annotations
 
+import contextlib
+import os
 import threading
 
 import numpy as np
@@ -104,3 +106,16 @@ def readback(x) -> np.ndarray:
                "readback")
     t.cuda.current_stream().synchronize()
     return buf[:nbytes].view(x.dtype).reshape(x.shape).numpy().copy()
+
+
+_NVTX = os.environ.get("SPCN_NVTX", "") not in ("", "0")
+
+
+def nvtx(label: str):
+    """NVTX range around a pass (SPCN_NVTX=1: visible in nsys/ncu timelines;
+    otherwise a no-op context)."""
+    if not _NVTX:
+        return contextlib.nullcontext()
+    import torch as _t
+
+    return _t.cuda.nvtx.range(label)

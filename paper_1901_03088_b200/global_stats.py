@@ -360,17 +360,20 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
     if g is not None and g.shape == (2, 2) and np.isfinite(g).all() and (g[:, 0] > 0).all() \
             and hasattr(eng, "table"):
         lo_t = [float(g[0, 0]), float(g[1, 0])]
-        tab, cnt = eng.table(lo_t)          # this rank's table: never exchanged
+        with _dev.nvtx("spcn.global.table_pass"):
+            tab, cnt = eng.table(lo_t)      # this rank's table: never exchanged
         info["passes"] += 1
         n = int(comm.allreduce(cnt).reshape(-1)[0].item())
         if n == 0:
             raise StainAbsentError("stain absent: no non-white pixels in the slide")
         rank = (p / 100.0) * (n - 1)
         klo, khi = int(math.floor(rank)), int(math.ceil(rank))
-        x, w, xmax, over = eng.scan(tab)
+        with _dev.nvtx("spcn.global.scan"):
+            x, w, xmax, over = eng.scan(tab)
         del tab
         over = int(comm.allreduce(_as_tensor([1.0 if over else 0.0], x)).cpu().numpy()[0])
-        res = None if over else _table_select(eng, x, w, xmax, n, lo_t, [klo, khi], comm)
+        with _dev.nvtx("spcn.global.select"):
+            res = None if over else _table_select(eng, x, w, xmax, n, lo_t, [klo, khi], comm)
         if res is not None:
             vals, below = res
             p99 = np.array([interpolate(vals[j][0], vals[j][1], rank) for j in range(2)])

@@ -454,8 +454,9 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
     t0 = time.perf_counter()
     if isinstance(slide, DeviceSource):
         # resident slide: visit loop + i0 on the device, one host round trip
-        m, i0, meta, empty = _stage("sampling", _fit_sample_resident, fb, slide, plan,
-                                    per_patch_stats)
+        with _dev.nvtx("spcn.fit.sample"):
+            m, i0, meta, empty = _stage("sampling", _fit_sample_resident, fb, slide, plan,
+                                        per_patch_stats)
         if m == 0:
             raise BlankSlideError("sampling: blank slide: no non-white pixels found in any "
                                   "sampled patch")
@@ -476,11 +477,12 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
         fb.offsets().copy_(t.tensor([0, m], dtype=t.int64), non_blocking=False)
     stats.sampled_pixels = m
     stats.patches = meta.patches_used
-    fp = fitcore.fit_tail(fb, sample_flat, m, i0, plan, cfg, code_lam=code_lam,
-                          per_patch_stats=per_patch_stats, p99_mode=p99_mode,
-                          used_counts=meta.patch_counts, source_label=source_label,
-                          chunks=slide_chunks(slide) if p99_mode == "global" else None,
-                          stage=_stage)
+    with _dev.nvtx("spcn.fit.basis_stats"):
+        fp = fitcore.fit_tail(fb, sample_flat, m, i0, plan, cfg, code_lam=code_lam,
+                              per_patch_stats=per_patch_stats, p99_mode=p99_mode,
+                              used_counts=meta.patch_counts, source_label=source_label,
+                              chunks=slide_chunks(slide) if p99_mode == "global" else None,
+                              stage=_stage)
     stats.basis_fit_s += time.perf_counter() - t0
     return fp
 
@@ -591,7 +593,9 @@ def transform(slide, source: FitParams, target: FitParams, sink, *,
 
     Output is byte-identical for any strip height / worker count (and, with
     precision="exact", to the reference).  Device source + DeviceWriter: one
-    launch over the resident slide.  Host source: strips stream through
+    launch over the resident slide, stream-ordered on the current stream
+    (returns without waiting for it, like a torch op; RunStats.transform_s
+    is then the launch time).  Host source: strips stream through
     ``workers`` (default 2) CUDA streams — H2D, recolor, D2H overlap — and
     are committed to the sink in order; pinned host arrays are copied
     directly without a staging copy.
@@ -616,7 +620,8 @@ def transform(slide, source: FitParams, target: FitParams, sink, *,
     if isinstance(slide, DeviceSource):
         src = slide.tensor
         if isinstance(sink, DeviceWriter):
-            plan.run(src, sink.pixels, width * slide.height)
+            with _dev.nvtx("spcn.transform"):
+                plan.run(src, sink.pixels, width * slide.height)
             if progress is None:            # one launch wrote every strip in place
                 gauge.add(strips[0][1] * width)
                 sink.mark_written(0, slide.height)
@@ -627,7 +632,8 @@ def transform(slide, source: FitParams, target: FitParams, sink, *,
                     sink.mark_written(y, h)
                     gauge.release(h * width)
                     progress(y + h, slide.height)
-            t.cuda.current_stream().synchronize()
+            # device in, device out: stream-ordered like any torch op (no host
+            # wait; the next call's host work overlaps this launch)
         else:
             out = t.empty_like(src)
             plan.run(src, out, width * slide.height)
