@@ -373,6 +373,43 @@ int spcn_render_synthetic(uint8_t* out, int64_t width, int64_t row0, int64_t row
  * buffer is not mapped or not 4-byte aligned.                               */
 int spcn_readback(const void* src, void* host_pinned, int64_t bytes, void* stream);
 
+/* Wait for `stream` (after a spcn_readback, before reading the pinned bytes). */
+int spcn_stream_sync(void* stream);
+
+/* ---- one-slide fit in two stream-ordered steps (launch-bound path) ------
+ * The fit of one resident slide is ~0.2 ms of kernels; these two entry
+ * points issue each of its device phases with one call (the same kernels as
+ * the individual entries above) so the host pays one call per phase.
+ * Arena A (SPCN_FIT_ARENA_A bytes, device): state i64[8] @0 (collected,
+ * visited, used, bright counts x3, stopped, need-more-candidates), offsets
+ * i64[2] @64, i0 f64[3] @80, empty-pool flags i32[3] @104, bright histogram
+ * i32[3][256] @128.  Arena B (SPCN_FIT_ARENA_B bytes): ordered basis f64[6]
+ * @0, p99 f64[2] @48, SNMF info i32[4] @64, stain-absent flags i32[2] @80.
+ *
+ * spcn_fit_sample_step: one candidate batch of the visit loop (zeroing the
+ * arena first when zero_arena != 0): sample_count -> sample_visit ->
+ * sample_compact -> i0_from_hist, then the first readback_bytes of arena A
+ * into pinned host memory (caller syncs the stream before reading).
+ * spcn_fit_basis_step: the host OD table (pinned, 3x256 f64, the reference's
+ * own np.log values) -> device, SNMF basis, densities (code_lam), the pooled
+ * p99 when want_p99 != 0, then the first readback_bytes of arena B into
+ * pinned memory.  The pinned table must stay untouched until the stream has
+ * passed this call.                                                        */
+#define SPCN_FIT_ARENA_A 3200
+#define SPCN_FIT_ARENA_B 88
+int spcn_fit_sample_step(const uint8_t* img, const spcn_patch* patches, int32_t n,
+                         int32_t max_chunks, int32_t k0, const int32_t* dims,
+                         const spcn_visit_plan* plan, int32_t white_threshold, int32_t zero_arena,
+                         void* arena_a, int32_t* counts, spcn_patch_take* takes,
+                         uint8_t* sample_out, void* readback_pinned, int64_t readback_bytes,
+                         void* stream);
+int spcn_fit_basis_step(const uint8_t* sample, int64_t m, const int64_t* offsets,
+                        const double* lut_pinned, double* lut_dev, const spcn_snmf_cfg* cfg,
+                        double* hscratch, double* history, void* arena_b, double code_lam,
+                        int32_t max_sweeps, double* h, void* qbuf, double* selbuf,
+                        int32_t want_p99, void* readback_pinned, int64_t readback_bytes,
+                        void* stream);
+
 /* Exhaustive calibration of part `part` of `nparts` of the 2^24 colours into
  * the workspace's calibration word (zeroed first; stream-ordered).  With
  * every part's word max-reduced, cert_alpha = SPCN_CALIBRATE_DEVICE makes the

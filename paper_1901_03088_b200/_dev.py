@@ -11,12 +11,21 @@ _ws_lock = threading.Lock()
 _ws_cache: dict = {}
 
 
-def torch():
-    import torch as _t
+_TORCH_OK = None
 
-    if not _t.cuda.is_available():
-        raise RuntimeError("paper_1901_03088_b200 needs a CUDA device (B200); there is no CPU path")
-    return _t
+
+def torch():
+    """The torch module, once a CUDA device is known to be present (checked
+    on the first call: the availability query is slow and cannot change)."""
+    global _TORCH_OK
+    if _TORCH_OK is None:
+        import torch as _t
+
+        if not _t.cuda.is_available():
+            raise RuntimeError("paper_1901_03088_b200 needs a CUDA device (B200); "
+                               "there is no CPU path")
+        _TORCH_OK = _t
+    return _TORCH_OK
 
 
 def is_tensor(x) -> bool:
@@ -50,9 +59,11 @@ def workspace(nbytes: int, device=None, stream: int | None = None):
     stream): launches in flight on different streams (the streamed strips,
     the pipelined batch chunks) must not share a repair list."""
     t = torch()
-    dev = device if device is not None else t.cuda.current_device()
+    dev = device if device is not None else t._C._cuda_getDevice()
     if stream is None:
-        stream = int(t.cuda.current_stream().cuda_stream)
+        from . import _lib
+
+        stream = _lib.stream_handle()
     key = (int(dev), threading.get_ident(), int(stream))
     with _ws_lock:
         buf = _ws_cache.pop(key, None)

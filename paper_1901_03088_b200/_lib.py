@@ -40,7 +40,8 @@ EXPORTS = (
     "spcn_table_entries_collect",
     "spcn_sample_visit",
     "spcn_readback", "spcn_last_error", "spcn_version", "spcn_launch_count", "spcn_xform_shape",
-    "spcn_xform_timing_enable", "spcn_xform_timing",
+    "spcn_xform_timing_enable", "spcn_xform_timing", "spcn_stream_sync",
+    "spcn_fit_sample_step", "spcn_fit_basis_step",
 )
 
 
@@ -84,6 +85,11 @@ _SIGS = {
     "spcn_xform_shape": (ctypes.c_char_p, []),
     "spcn_xform_timing_enable": (ctypes.c_int, [I32]),
     "spcn_xform_timing": (ctypes.c_int, [ctypes.POINTER(I64), ctypes.POINTER(DBL)]),
+    "spcn_stream_sync": (ctypes.c_int, [P]),
+    "spcn_fit_sample_step": (ctypes.c_int, [P, P, I32, I32, I32, P, P, I32, I32, P, P, P, P, P,
+                                            I64, P]),
+    "spcn_fit_basis_step": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P, DBL, I32, P, P, P, I32, P,
+                                           I64, P]),
 }
 
 
@@ -134,11 +140,26 @@ def check(rc: int, what: str = "") -> None:
     raise exc(msg)
 
 
-def stream_handle(stream=None) -> int:
-    import torch
+_RAW_STREAM = None
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+
+def stream_handle(stream=None) -> int:
+    """cudaStream_t (as int) of `stream`, else of the current stream.  The
+    current stream is read through torch's raw C accessors: the Python-level
+    torch.cuda.current_stream() costs ~15 us of device-index checks per call,
+    paid a dozen times per fit."""
+    global _RAW_STREAM
+    if stream is not None:
+        return int(stream.cuda_stream)
+    if _RAW_STREAM is None:
+        import torch
+
+        C = torch._C
+        if hasattr(C, "_cuda_getCurrentRawStream") and hasattr(C, "_cuda_getDevice"):
+            _RAW_STREAM = lambda: C._cuda_getCurrentRawStream(C._cuda_getDevice())  # noqa: E731
+        else:  # pragma: no cover - older torch
+            _RAW_STREAM = lambda: int(torch.cuda.current_stream().cuda_stream)  # noqa: E731
+    return int(_RAW_STREAM())
 
 
 def ptr(t) -> int:

@@ -852,6 +852,71 @@ __global__ void k_copy_to_host(const uint32_t* __restrict__ src, uint32_t* __res
 // Device -> pinned host through the SMs (stores over PCIe into the mapped
 // allocation) instead of a copy engine: a read-back of a few KB never queues
 // behind multi-hundred-MB transfers another stream has on the copy engine.
+extern "C" int spcn_fit_sample_step(const uint8_t* img, const spcn_patch* patches, int32_t n,
+                                    int32_t max_chunks, int32_t k0, const int32_t* dims,
+                                    const spcn_visit_plan* plan, int32_t white_threshold,
+                                    int32_t zero_arena, void* arena_a, int32_t* counts,
+                                    spcn_patch_take* takes, uint8_t* sample_out,
+                                    void* readback_pinned, int64_t readback_bytes, void* stream) {
+  g_err.clear();
+  if (!arena_a || !readback_pinned || readback_bytes < 0 || readback_bytes > SPCN_FIT_ARENA_A)
+    return fail(SPCN_EINVAL, "bad arena / readback");
+  char* A = static_cast<char*>(arena_a);
+  int64_t* state = reinterpret_cast<int64_t*>(A);
+  int64_t* offsets = reinterpret_cast<int64_t*>(A + 64);
+  double* i0 = reinterpret_cast<double*>(A + 80);
+  int32_t* empty = reinterpret_cast<int32_t*>(A + 104);
+  int32_t* hist = reinterpret_cast<int32_t*>(A + 128);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (zero_arena) {
+    const cudaError_t e = cudaMemsetAsync(arena_a, 0, SPCN_FIT_ARENA_A, st);
+    if (e != cudaSuccess) return cuda_fail(e, "memset");
+  }
+  int rc = spcn_sample_count(img, patches, n, max_chunks, white_threshold, counts, stream);
+  if (!rc) rc = spcn_sample_visit(counts, n, max_chunks, k0, dims, plan, state, takes, offsets,
+                                  stream);
+  if (!rc) rc = spcn_sample_compact(img, patches, n, max_chunks, white_threshold, counts, takes,
+                                    sample_out, hist, stream);
+  if (!rc) rc = spcn_i0_from_hist(hist, 1, i0, empty, stream);
+  if (!rc) rc = spcn_readback(arena_a, readback_pinned, readback_bytes, stream);
+  return rc;
+}
+
+extern "C" int spcn_fit_basis_step(const uint8_t* sample, int64_t m, const int64_t* offsets,
+                                   const double* lut_pinned, double* lut_dev,
+                                   const spcn_snmf_cfg* cfg, double* hscratch, double* history,
+                                   void* arena_b, double code_lam, int32_t max_sweeps, double* h,
+                                   void* qbuf, double* selbuf, int32_t want_p99,
+                                   void* readback_pinned, int64_t readback_bytes, void* stream) {
+  g_err.clear();
+  if (!arena_b || !lut_pinned || !lut_dev || !readback_pinned || readback_bytes < 0 ||
+      readback_bytes > SPCN_FIT_ARENA_B)
+    return fail(SPCN_EINVAL, "bad arena / table / readback");
+  char* B = static_cast<char*>(arena_b);
+  double* basis = reinterpret_cast<double*>(B);
+  double* p99 = reinterpret_cast<double*>(B + 48);
+  int32_t* info = reinterpret_cast<int32_t*>(B + 64);
+  int32_t* absent = reinterpret_cast<int32_t*>(B + 80);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const cudaError_t e =
+      cudaMemcpyAsync(lut_dev, lut_pinned, 768 * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "od table upload");
+  int rc = spcn_snmf_batched(sample, nullptr, offsets, 1, lut_dev, cfg, hscratch, m, basis, history,
+                             info, stream);
+  if (!rc) rc = spcn_code_samples(sample, offsets, 1, m, lut_dev, basis, code_lam, max_sweeps, h, m,
+                                  stream);
+  if (!rc && want_p99)
+    rc = spcn_percentile_segments(h, m, offsets, 1, 99.0, qbuf, selbuf, p99, absent, stream);
+  if (!rc) rc = spcn_readback(arena_b, readback_pinned, readback_bytes, stream);
+  return rc;
+}
+
+extern "C" int spcn_stream_sync(void* stream) {
+  g_err.clear();
+  const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "stream_sync");
+}
+
 extern "C" int spcn_readback(const void* src, void* host_pinned, int64_t bytes, void* stream) {
   g_err.clear();
   if (bytes < 0) return fail(SPCN_EINVAL, "bytes must be >= 0");

@@ -72,61 +72,17 @@ class FitBuffers:
         self.pin_a = t.empty(256, dtype=t.uint8, pin_memory=True)
         self.pin_b = t.empty(256, dtype=t.uint8, pin_memory=True)
         self.pin_lut = t.empty(768, dtype=t.float64, pin_memory=True)
-        self.lut_ev = None
         self.cand = {}          # (W, H, plan) -> candidate descriptors on the device
-        L = _lib.lib()
-        if not getattr(L, "_spcn_rb_declared", False):
-            _lib.declare("spcn_readback", ctypes.c_int, [_lib.P, _lib.P, _lib.I64, _lib.P])
-            L._spcn_rb_declared = True
-
-    # views into the arenas
-    def state(self):
-        return self.arena_a[A_STATE:A_OFFS].view(_dev.torch().int64)
+        # raw pointers / numpy views of the fixed buffers (ctypes arguments)
+        self.arena_a_ptr, self.arena_b_ptr = _lib.ptr(self.arena_a), _lib.ptr(self.arena_b)
+        self.sample_ptr, self.pin_a_ptr = _lib.ptr(self.sample), _lib.ptr(self.pin_a)
+        self.pin_b_ptr, self.pin_lut_ptr = _lib.ptr(self.pin_b), _lib.ptr(self.pin_lut)
+        self.pin_a_np, self.pin_b_np = self.pin_a.numpy(), self.pin_b.numpy()
+        self.pin_lut_np = self.pin_lut.numpy()
 
     def offsets(self):
+        """[0, m] of the current sample (written by k_visit, or by the host)."""
         return self.arena_a[A_OFFS:A_I0].view(_dev.torch().int64)
-
-    def i0(self):
-        return self.arena_a[A_I0:A_EMPTY].view(_dev.torch().float64)
-
-    def empty(self):
-        return self.arena_a[A_EMPTY:A_EMPTY + 12].view(_dev.torch().int32)
-
-    def hist(self):
-        return self.arena_a[A_HIST:A_BYTES].view(_dev.torch().int32).view(1, 3, 256)
-
-    def basis(self):
-        return self.arena_b[B_BASIS:B_P99].view(_dev.torch().float64)
-
-    def p99(self):
-        return self.arena_b[B_P99:B_INFO].view(_dev.torch().float64)
-
-    def info(self):
-        return self.arena_b[B_INFO:B_ABSENT].view(_dev.torch().int32)
-
-    def absent(self):
-        return self.arena_b[B_ABSENT:B_BYTES].view(_dev.torch().int32)
-
-    def read(self, arena, pinned, nbytes: int) -> np.ndarray:
-        """Copy the first nbytes of a device arena to pinned memory with a
-        kernel (not queued behind other streams' bulk copies) and wait."""
-        t = _dev.torch()
-        _lib.check(_lib.lib().spcn_readback(_lib.ptr(arena), _lib.ptr(pinned), nbytes,
-                                            _lib.stream_handle()), "readback")
-        t.cuda.current_stream().synchronize()
-        return pinned[:nbytes].numpy().copy()
-
-    def upload_lut(self, i0: np.ndarray):
-        """The host OD table of i0 → self.lut (async from pinned memory)."""
-        t = _dev.torch()
-        if self.lut_ev is not None:
-            self.lut_ev.synchronize()          # previous upload has left the staging buffer
-        self.pin_lut.numpy()[:] = od_table_cached(np.ascontiguousarray(i0, np.float64)
-                                                  .tobytes()).reshape(-1)
-        self.lut.view(-1).copy_(self.pin_lut, non_blocking=True)
-        self.lut_ev = t.cuda.Event()
-        self.lut_ev.record()
-        return self.lut
 
 
 _TLS = threading.local()
@@ -136,12 +92,11 @@ def buffers(device, target_pixels: int, max_outer: int) -> FitBuffers:
     t = _dev.torch()
     dev = t.device(device) if not isinstance(device, t.device) else device
     if dev.index is None:
-        dev = t.device("cuda", t.cuda.current_device())
+        dev = t.device("cuda", t._C._cuda_getDevice())
     cache = getattr(_TLS, "bufs", None)
     if cache is None:
         cache = _TLS.bufs = {}
-    key = (dev.index, int(t.cuda.current_stream(dev).cuda_stream), int(target_pixels),
-           int(max_outer))
+    key = (dev.index, _lib.stream_handle(), int(target_pixels), int(max_outer))
     fb = cache.get(key)
     if fb is None:
         if len(cache) > 8:
@@ -183,35 +138,30 @@ def fit_tail(fb: FitBuffers, sample_flat, m: int, i0: np.ndarray, plan, cfg, *,
     sample_flat: CUDA uint8 (3m,) RGB sample; i0: host (3,) background.
     chunks: whole-slide pass generator (global p99 mode); comm: collectives of
     a row-band group (global mode)."""
-    t = _dev.torch()
     stage = stage or (lambda label, fn, *a, **k: fn(*a, **k))
     if m < 10:
         raise InsufficientPixelsError(
             f"basis fit: insufficient pixels: need at least 10 OD samples, got {m}")
-    lut = fb.upload_lut(i0)
-    offsets = fb.offsets()
-    L = snmf._sig()
+    L = _lib.lib()
+    # the reference's OD table (numpy log) into the pinned staging buffer; the
+    # previous fit's upload of it has completed (its read-back was waited for)
+    fb.pin_lut_np[:] = od_table_cached(np.ascontiguousarray(i0, np.float64).tobytes()).reshape(-1)
     c = snmf_cfg_cached(float(cfg.lam), float(cfg.rel_tol), int(cfg.max_outer_iters),
                         int(cfg.seed), snmf_cluster(m))
-    basis_d, info_d = fb.basis(), fb.info()
-    _lib.check(L.spcn_snmf_batched(_lib.ptr(sample_flat), None, _lib.ptr(offsets), 1,
-                                   _lib.ptr(lut), ctypes.byref(c), _lib.ptr(fb.scratch), m,
-                                   _lib.ptr(basis_d), _lib.ptr(fb.history), _lib.ptr(info_d),
-                                   _lib.stream_handle()), "snmf_batched")
     h = fb.h[:2 * m].view(2, m)
-    _lib.check(L.spcn_code_samples(_lib.ptr(sample_flat), _lib.ptr(offsets), 1, m, _lib.ptr(lut),
-                                   _lib.ptr(basis_d), float(code_lam), 2000, _lib.ptr(h), m,
-                                   _lib.stream_handle()), "code_samples")
+    pooled = p99_mode == "sample" and not per_patch_stats
+    st = _lib.stream_handle()
+    # table upload -> SNMF -> densities -> pooled p99 -> read-back, one call
+    _lib.check(L.spcn_fit_basis_step(_lib.ptr(sample_flat), m, _lib.ptr(fb.offsets()),
+                                     fb.pin_lut_ptr, _lib.ptr(fb.lut), ctypes.byref(c),
+                                     _lib.ptr(fb.scratch), _lib.ptr(fb.history), fb.arena_b_ptr,
+                                     float(code_lam), 2000, _lib.ptr(h), _lib.ptr(fb.q),
+                                     _lib.ptr(fb.sel), 1 if pooled else 0, fb.pin_b_ptr, B_BYTES,
+                                     st), "fit_basis_step")
+    _lib.check(L.spcn_stream_sync(st), "stream_sync")
     prov = provenance(plan, cfg, code_lam, per_patch_stats, p99_mode, source_label)
-    if p99_mode == "sample" and not per_patch_stats:
-        from . import stats as dstats
-
-        S = dstats._sig()
-        _lib.check(S.spcn_percentile_segments(_lib.ptr(h), m, _lib.ptr(offsets), 1, 99.0,
-                                              _lib.ptr(fb.q), _lib.ptr(fb.sel),
-                                              _lib.ptr(fb.p99()), _lib.ptr(fb.absent()),
-                                              _lib.stream_handle()), "percentile_segments")
-        raw = fb.read(fb.arena_b, fb.pin_b, B_BYTES)
+    if pooled:
+        raw = fb.pin_b_np[:B_BYTES].copy()
         basis = raw[B_BASIS:B_P99].view(np.float64).reshape(3, 2).copy()
         p99 = raw[B_P99:B_INFO].view(np.float64).copy()
         info = raw[B_INFO:B_ABSENT].view(np.int32)
@@ -225,7 +175,7 @@ def fit_tail(fb: FitBuffers, sample_flat, m: int, i0: np.ndarray, plan, cfg, *,
             raise ValueError(f"density stats: p99 must be finite and non-negative, got {p99}")
         return FitParams(i0=np.asarray(i0, np.float64).copy(), basis=basis,
                          stats=StainStats(p99=p99, sample_count=m), provenance=prov)
-    raw = fb.read(fb.arena_b, fb.pin_b, B_ABSENT)
+    raw = fb.pin_b_np[:B_ABSENT].copy()
     basis = raw[B_BASIS:B_P99].view(np.float64).reshape(3, 2).copy()
     snmf.warn_flags(m, int(raw[B_INFO:B_ABSENT].view(np.int32)[2]), cfg.max_outer_iters,
                     stacklevel=4)

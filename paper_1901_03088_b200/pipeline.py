@@ -280,6 +280,8 @@ def _resident_candidates(fb, slide: DeviceSource, plan: SamplePlan):
                                 device=fb.device),
                  vp=VisitPlan(plan.target_pixels, plan.sample_cap, plan.max_patches, ncand,
                               float(plan.background_fraction_cutoff)))
+        for k in ("desc", "dims", "takes", "counts"):
+            c[k + "_ptr"] = _lib.ptr(c[k])
         if len(fb.cand) > 16:
             fb.cand.clear()
         fb.cand[key] = c
@@ -295,30 +297,21 @@ def _fit_sample_resident(fb, slide: DeviceSource, plan: SamplePlan, need_counts:
     fb.sample[:3m]."""
     import ctypes
 
-    L = _lib_sample()
+    L = _lib.lib()
     c = _resident_candidates(fb, slide, plan)
     thr = int(plan.white_threshold)
     img, stream = slide.tensor, _lib.stream_handle()
-    fb.arena_a.zero_()
-    state, hist = fb.state(), fb.hist()
     from .fitcore import A_READ
 
     for k0, n in c["batches"]:
-        dsl = c["desc"][k0 * PATCH_DT.itemsize:(k0 + n) * PATCH_DT.itemsize]
-        tks = c["takes"][k0 * TAKE_DT.itemsize:(k0 + n) * TAKE_DT.itemsize]
-        counts = c["counts"]
-        _lib.check(L.spcn_sample_count(_lib.ptr(img), _lib.ptr(dsl), n, c["chunks"], thr,
-                                       _lib.ptr(counts), stream), "sample_count")
-        _lib.check(L.spcn_sample_visit(_lib.ptr(counts), n, c["chunks"], k0,
-                                       _lib.ptr(c["dims"][k0:]), ctypes.byref(c["vp"]),
-                                       _lib.ptr(state), _lib.ptr(tks), _lib.ptr(fb.offsets()),
-                                       stream), "sample_visit")
-        _lib.check(L.spcn_sample_compact(_lib.ptr(img), _lib.ptr(dsl), n, c["chunks"], thr,
-                                         _lib.ptr(counts), _lib.ptr(tks), _lib.ptr(fb.sample),
-                                         _lib.ptr(hist), stream), "sample_compact")
-        _lib.check(L.spcn_i0_from_hist(_lib.ptr(hist), 1, _lib.ptr(fb.i0()),
-                                       _lib.ptr(fb.empty()), stream), "i0_from_hist")
-        raw = fb.read(fb.arena_a, fb.pin_a, A_READ)
+        # count -> visit -> compact -> i0 -> read-back, one library call
+        _lib.check(L.spcn_fit_sample_step(
+            _lib.ptr(img), c["desc_ptr"] + k0 * PATCH_DT.itemsize, n, c["chunks"], k0,
+            c["dims_ptr"] + 8 * k0, ctypes.byref(c["vp"]), thr, 1 if k0 == 0 else 0,
+            fb.arena_a_ptr, c["counts_ptr"], c["takes_ptr"] + k0 * TAKE_DT.itemsize,
+            fb.sample_ptr, fb.pin_a_ptr, A_READ, stream), "fit_sample_step")
+        _lib.check(L.spcn_stream_sync(stream), "stream_sync")
+        raw = fb.pin_a_np[:A_READ].copy()
         st = raw[:64].view(np.int64)
         if not st[7]:                              # a stop rule fired (or all candidates seen)
             break
