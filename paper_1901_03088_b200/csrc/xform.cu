@@ -92,24 +92,27 @@ __global__ void __launch_bounds__(32 * CW, BLK)
   const int64_t nslices = (npix + kSlicePx - 1) / kSlicePx;
   const int64_t gw = (int64_t)blockIdx.x * CW + warp, GW = (int64_t)gridDim.x * CW;
   uint64_t pol = 0;
-  auto issue_load = [&](int64_t k) {   // lane 0 only
-    const int64_t j = gw + k * GW;
-    if (j >= nslices) return;
-    const int s = (int)(k % NSW);
-    const uint32_t bytes = static_cast<uint32_t>(3 * min64(kSlicePx, npix - j * kSlicePx));
-    mbar_expect_tx(&mybar[s], bytes);
-    bulk_g2s(myslots + s * kSlotBytes, src + 3 * j * kSlicePx, bytes, &mybar[s], pol);
+  // slot indices as running counters (no 64-bit modulo per slice)
+  int ls = 0;                            // lane 0: slot of the next load
+  int64_t lj = gw;                       // lane 0: slice of the next load
+  auto issue_load = [&]() {   // lane 0 only: next slice into slot ls
+    if (lj < nslices) {
+      const uint32_t bytes = static_cast<uint32_t>(3 * min64(kSlicePx, npix - lj * kSlicePx));
+      mbar_expect_tx(&mybar[ls], bytes);
+      bulk_g2s(myslots + ls * kSlotBytes, src + 3 * lj * kSlicePx, bytes, &mybar[ls], pol);
+    }
+    lj += GW;
+    ls = ls + 1 == NSW ? 0 : ls + 1;
   };
   if (lane == 0) {
     pol = policy_evict_first();
-    for (int k = 0; k < NSW; ++k) issue_load(k);
+    for (int k = 0; k < NSW; ++k) issue_load();
   }
 
-  for (int64_t k = 0;; ++k) {
-    const int64_t j = gw + k * GW;
-    if (j >= nslices) break;
-    const int s = (int)(k % NSW);
-    mbar_wait(&mybar[s], (uint32_t)((k / NSW) & 1));
+  int s = 0;
+  uint32_t phase = 0;
+  for (int64_t j = gw, k = 0; j < nslices; j += GW, ++k) {
+    mbar_wait(&mybar[s], phase);
     const int n = (int)min64(kSlicePx, npix - j * kSlicePx);
     uint8_t* sbase = myslots + s * kSlotBytes;
 #pragma unroll
@@ -122,9 +125,13 @@ __global__ void __launch_bounds__(32 * CW, BLK)
       bulk_s2g(dst + 3 * j * kSlicePx, sbase, static_cast<uint32_t>(3 * n));
       bulk_commit();
       if (k >= 1) {
-        bulk_wait_read<1>();          // the store of item k-1 has read its slot
-        issue_load(k - 1 + NSW);      // refill that slot
+        bulk_wait_read<1>();          // the store of slice k-1 has read its slot
+        issue_load();                 // refill that slot (load number k-1+NSW)
       }
+    }
+    if (++s == NSW) {
+      s = 0;
+      phase ^= 1u;
     }
   }
   if (lane == 0) bulk_wait_all();
