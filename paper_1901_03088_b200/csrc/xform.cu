@@ -271,7 +271,8 @@ static Shape g_shapes[] = {
     make_wshape<16, 16, 3, 1, 2>(), make_wshape<16, 32, 4, 1, 1>(),
     make_wshape<16, 16, 2, 1, 3>(), make_wshape<12, 16, 3, 1, 3>(), make_wshape<16, 16, 4, 1, 1>(),
     make_wshape<8, 16, 2, 2, 2>(), make_wshape<8, 16, 3, 2, 1>(),
-    make_wshape<20, 16, 2, 1, 2>(), make_wshape<16, 32, 2, 1, 2>(), make_wshape<20, 24, 2, 1, 2>()};
+    make_wshape<20, 16, 2, 1, 2>(), make_wshape<16, 32, 2, 1, 2>(), make_wshape<20, 24, 2, 1, 2>(),
+    make_wshape<16, 24, 4, 1, 1>()};
 static Shape* g_shape = nullptr;
 static bool g_identity = false;
 
