@@ -85,27 +85,28 @@ __device__ __forceinline__ void st_scan(const uint8_t* __restrict__ src, int64_t
   const int64_t nsl = (nbody + kSlicePx - 1) / kSlicePx;
   const int64_t gw = (int64_t)blockIdx.x * CW + warp, GW = (int64_t)gridDim.x * CW;
   uint64_t pol = 0;
-  auto issue = [&](int64_t k) {   // lane 0 only
-    const int64_t j = gw + k * GW;
-    if (j >= nsl) return;
-    const int s = (int)(k % NSW);
-    const int64_t left = nbody - j * kSlicePx;
-    const uint32_t bytes = static_cast<uint32_t>(3 * (left < kSlicePx ? left : kSlicePx));
-    mbar_expect_tx(&mybar[s], bytes);
-    bulk_g2s(myslots + s * kSliceBytes, src + 3 * j * kSlicePx, bytes, &mybar[s], pol);
+  int ls = 0;              // lane 0: slot of the next load (running counter)
+  int64_t lj = gw;         // lane 0: slice of the next load
+  auto issue = [&]() {     // lane 0 only
+    if (lj < nsl) {
+      const int64_t left = nbody - lj * kSlicePx;
+      const uint32_t bytes = static_cast<uint32_t>(3 * (left < kSlicePx ? left : kSlicePx));
+      mbar_expect_tx(&mybar[ls], bytes);
+      bulk_g2s(myslots + ls * kSliceBytes, src + 3 * lj * kSlicePx, bytes, &mybar[ls], pol);
+    }
+    lj += GW;
+    ls = ls + 1 == NSW ? 0 : ls + 1;
   };
   if (lane == 0) {
     for (int s = 0; s < NSW; ++s) mbar_init(&mybar[s], 1);
     mbar_fence_init();
     pol = policy_evict_first();
-    for (int k = 0; k < NSW; ++k) issue(k);
+    for (int k = 0; k < NSW; ++k) issue();
   }
   __syncwarp();
   int s = 0;
   uint32_t phase = 0;
-  for (int k = 0;; ++k) {   // a warp's iterations fit 32 bits (slices / warps of the grid)
-    const int64_t j = gw + (int64_t)k * GW;
-    if (j >= nsl) break;
+  for (int64_t j = gw; j < nsl; j += GW) {
     mbar_wait(&mybar[s], phase);
     const int64_t left = nbody - j * kSlicePx;
 #pragma unroll
@@ -123,7 +124,7 @@ __device__ __forceinline__ void st_scan(const uint8_t* __restrict__ src, int64_t
     __syncwarp();
     if (lane == 0) {
       fence_proxy_async_smem();   // the warp's reads of slot s precede its refill
-      issue(k + NSW);
+      issue();                    // slot s again (the loads run NSW slices ahead)
     }
     if (++s == NSW) {
       s = 0;

@@ -64,8 +64,7 @@ struct WCfg {
 template <int MODE, int CW, int REP, int NSW, int BLK, int NSUB>
 __global__ void __launch_bounds__(32 * CW, BLK)
     k_xform_warp(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
-                 const __grid_constant__ FastP fp, const __grid_constant__ StrictP sp,
-                 RepairList rl) {
+                 const __grid_constant__ FastP fp, RepairList rl) {
   using C = WCfg<CW, REP, NSW, BLK, NSUB>;
   constexpr int kSlicePx = C::kSlicePx, kSlotBytes = C::kSlotBytes;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -245,7 +244,7 @@ __global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP
 // ------------------------------------------------------------------ launchers
 static int g_sm_count = 0;
 
-using XformFn = void (*)(const uint8_t*, uint8_t*, int64_t, FastP, StrictP, RepairList);
+using XformFn = void (*)(const uint8_t*, uint8_t*, int64_t, FastP, RepairList);
 
 struct Shape {
   int cw, rep, nsub, blk, nsw, threads, tile_px, blocks_per_sm;
@@ -318,7 +317,7 @@ cudaError_t launch_xform_main(int mode, const uint8_t* src, uint8_t* dst, int64_
   const int64_t ntiles = (npix + s.tile_px - 1) / s.tile_px;
   const int grid = static_cast<int>(min64(ntiles, (int64_t)g_sm_count * s.blocks_per_sm));
   RepairList rl{count, items, cap, alpha_bits};
-  s.fn[g_identity ? 3 : mode]<<<grid, s.threads, s.smem, st>>>(src, dst, npix, fp, sp, rl);
+  s.fn[g_identity ? 3 : mode]<<<grid, s.threads, s.smem, st>>>(src, dst, npix, fp, rl);
   return launched();
 }
 

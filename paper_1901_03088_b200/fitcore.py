@@ -120,12 +120,19 @@ def _provenance_hash(items: tuple) -> str:
     return config_hash(dict(items))
 
 
-def provenance(plan, cfg, code_lam, per_patch_stats, p99_mode, source_label) -> dict:
+@lru_cache(maxsize=256)
+def _config_hash_of(plan, cfg, code_lam, per_patch_stats, p99_mode) -> str:
     fields = cfg_fields(plan, cfg, code_lam, per_patch_stats)
     if p99_mode != "sample":
         fields["p99_mode"] = p99_mode
+    return _provenance_hash(tuple(sorted((k, str(v)) for k, v in fields.items())))
+
+
+def provenance(plan, cfg, code_lam, per_patch_stats, p99_mode, source_label) -> dict:
+    """src/pipeline.py:241-256 (the hash memoised per configuration)."""
     return {"source": str(source_label),
-            "config_hash": _provenance_hash(tuple(sorted((k, str(v)) for k, v in fields.items())))}
+            "config_hash": _config_hash_of(plan, cfg, float(code_lam), bool(per_patch_stats),
+                                           p99_mode)}
 
 
 def fit_tail(fb: FitBuffers, sample_flat, m: int, i0: np.ndarray, plan, cfg, *,

@@ -599,7 +599,14 @@ def transform(slide, source: FitParams, target: FitParams, sink, *,
     factors = scale_factors(source.stats, target.stats)
     if np.any(factors <= 0):
         raise DegenerateStainError("degenerate stain density: target p99 is zero for a stain")
-    strips = plan_strips(slide.height, strip_height)
+    device_only = isinstance(slide, DeviceSource) and isinstance(sink, DeviceWriter) and \
+        progress is None
+    if device_only:                      # one launch: only the first strip's height is needed
+        if strip_height < 1 or slide.height < 1:
+            plan_strips(slide.height, strip_height)      # raises the reference's ValueError
+        strips = [(0, min(strip_height, slide.height))]
+    else:
+        strips = plan_strips(slide.height, strip_height)
     width = slide.width
     plan = XformPlan(source.i0, source.basis, code_lam, factors, target.basis, target.i0,
                      precision=precision)

@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
 
 from . import _dev, _lib
 from .optics import od_table
@@ -33,12 +35,11 @@ class XformPlan:
             od_table(i0b)                            # raises the reference's ValueError
         self.table = od_table_cached(i0b.tobytes())  # exact reference OD table (host numpy)
         p = _lib.XformParams()
-        p.src_i0[:] = [float(x) for x in _dev.f64_array(src_i0, 3, "src_i0")]
-        p.src_basis[:] = [float(x) for x in _dev.f64_array(src_basis, 6, "src_basis")]
-        p.code_lam = float(code_lam)
-        p.factors[:] = [float(x) for x in _dev.f64_array(factors, 2, "factors")]
-        p.tgt_basis[:] = [float(x) for x in _dev.f64_array(tgt_basis, 6, "tgt_basis")]
-        p.tgt_i0[:] = [float(x) for x in _dev.f64_array(tgt_i0, 3, "tgt_i0")]
+        # the 21 leading doubles of spcn_xform_params in one numpy assignment
+        np.frombuffer(p, dtype=np.float64, count=21)[:] = np.concatenate([
+            i0b, _dev.f64_array(src_basis, 6, "src_basis"), [float(code_lam)],
+            _dev.f64_array(factors, 2, "factors"), _dev.f64_array(tgt_basis, 6, "tgt_basis"),
+            _dev.f64_array(tgt_i0, 3, "tgt_i0")])
         p.od_table = self.table.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         p.precision = _lib.PREC[precision]
         p.max_sweeps = int(max_sweeps)
