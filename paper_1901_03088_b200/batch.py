@@ -93,12 +93,16 @@ def _od_tables_exact(i0: np.ndarray, device):
     expanded to the items on the device."""
     t = _dev.torch()
     ramp = np.arange(256, dtype=np.float64)
-    per_channel = []
+    rows, idx, base = [], np.empty((i0.shape[0], 3), np.int64), 0
     for c in range(3):
         vals, inv = np.unique(i0[:, c], return_inverse=True)
-        rows = np.log(vals[:, None] / np.clip(ramp[None, :], 1.0, vals[:, None]))
-        per_channel.append(t.from_numpy(rows).to(device)[t.from_numpy(inv.ravel()).to(device)])
-    return t.stack(per_channel, dim=1).contiguous()
+        rows.append(np.log(vals[:, None] / np.clip(ramp[None, :], 1.0, vals[:, None])))
+        idx[:, c] = base + inv.ravel()
+        base += vals.size
+    # one upload of the distinct rows and one of the per-item row indices,
+    # one gather on the device
+    table = t.from_numpy(np.concatenate(rows)).to(device)
+    return table[t.from_numpy(idx).to(device)].contiguous()
 
 
 def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), *,
