@@ -417,6 +417,39 @@ int spcn_fit_basis_step(const uint8_t* sample, int64_t m, const int64_t* offsets
 int spcn_xform_calibrate_part(const spcn_xform_params* p, int32_t part, int32_t nparts,
                               void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Fit -> transform with no host round trip (the device-built recolouring).
+ * The source half of the recolouring is read on the device from a fit that
+ * is still in flight on `stream`: the OD table spcn_fit_basis_step uploaded
+ * (lut_dev) and its arena B (basis | p99 | info | absent).  One call builds
+ * the parameters (1 CTA, the same params.cuh code as spcn_xform_rgb8), runs
+ * the exhaustive calibration, the EXACT recolour and the fp64 repairs —
+ * byte-identical to spcn_xform_rgb8 with the host-built parameters and
+ * SPCN_CALIBRATE_INLINE.  Replaces the host half of src/pipeline.py:275-296
+ * (scale_factors + the per-strip constants) for a resident slide.
+ * status_pinned (optional, pinned host int32) receives the build status, and
+ * the call then returns once it has landed — with everything enqueued on the
+ * stream before the call (e.g. the fit's arena read-back) also in host
+ * memory, while the recolour itself is still running (stream-ordered, like
+ * spcn_xform_rgb8).  Status 0 = recolouring; otherwise (stain absent,
+ * degenerate p99, an invalid or ill-conditioned basis: the strict-only case)
+ * dst is left untouched and the caller runs spcn_xform_rgb8 with host
+ * parameters, which raises the reference's error or takes the strict path.
+ * src and dst must share their 16-byte alignment phase; workspace as for
+ * spcn_xform_rgb8 (spcn_xform_workspace_bytes(npix)).                       */
+typedef struct spcn_xform_fitted {
+  const double* src_od_table;   /* device: 3 x 256 f64 source OD table         */
+  const void* src_fit;          /* device: SPCN_FIT_ARENA_B bytes (arena B)    */
+  double tgt_basis[6];
+  double tgt_p99[2];            /* > 0 (scale_factors' numerators)             */
+  double tgt_i0[3];
+  double code_lam;
+  int32_t max_sweeps;
+  int32_t reserved;
+} spcn_xform_fitted;
+int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
+                           const spcn_xform_fitted* p, void* workspace, size_t workspace_bytes,
+                           int32_t* status_pinned, void* stream);
+
 /* Thread-local description of the last error ("" if none).                 */
 const char* spcn_last_error(void);
 

@@ -41,7 +41,7 @@ EXPORTS = (
     "spcn_sample_visit",
     "spcn_readback", "spcn_last_error", "spcn_version", "spcn_launch_count", "spcn_xform_shape",
     "spcn_xform_timing_enable", "spcn_xform_timing", "spcn_stream_sync",
-    "spcn_fit_sample_step", "spcn_fit_basis_step",
+    "spcn_fit_sample_step", "spcn_fit_basis_step", "spcn_xform_rgb8_fitted",
 )
 
 
@@ -60,6 +60,20 @@ class XformParams(ctypes.Structure):
     ]
 
 
+class XformFitted(ctypes.Structure):
+    """include/spcn.h spcn_xform_fitted (the device-built recolouring)."""
+    _fields_ = [
+        ("src_od_table", ctypes.c_void_p),
+        ("src_fit", ctypes.c_void_p),
+        ("tgt_basis", ctypes.c_double * 6),
+        ("tgt_p99", ctypes.c_double * 2),
+        ("tgt_i0", ctypes.c_double * 3),
+        ("code_lam", ctypes.c_double),
+        ("max_sweeps", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -72,6 +86,8 @@ SZ = ctypes.c_size_t
 _SIGS = {
     "spcn_xform_workspace_bytes": (SZ, [I64]),
     "spcn_xform_rgb8": (ctypes.c_int, [P, P, I64, ctypes.POINTER(XformParams), P, SZ, P]),
+    "spcn_xform_rgb8_fitted": (ctypes.c_int, [P, P, I64, ctypes.POINTER(XformFitted), P, SZ, P,
+                                              P]),
     "spcn_xform_repair_count": (ctypes.c_int, [P, P, ctypes.POINTER(I64)]),
     "spcn_xform_calibrate": (ctypes.c_int, [ctypes.POINTER(XformParams), P, SZ,
                                             ctypes.POINTER(DBL), P]),

@@ -345,6 +345,109 @@ int spcn_xform_calibrate_part(const spcn_xform_params* p, int32_t part, int32_t 
   return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "calibrate_part");
 }
 
+}  // extern "C"
+
+namespace {
+// Parameter slots of the device-built recolouring, per device: slot k's
+// staging block and __constant__ copy may be rewritten only after the
+// previous recolouring that used slot k has finished (its event).
+struct FittedSlots {
+  DevParams* staging = nullptr;           // kDpSlots blocks
+  cudaEvent_t done[kDpSlots] = {};
+  cudaEvent_t built[kDpSlots] = {};       // the status read-back has landed
+  bool used[kDpSlots] = {};
+  int next = 0;
+};
+std::mutex g_fitted_mu;
+FittedSlots g_fitted[64];
+}  // namespace
+
+extern "C" {
+
+int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
+                           const spcn_xform_fitted* p, void* workspace, size_t workspace_bytes,
+                           int32_t* status_pinned, void* stream) {
+  g_err.clear();
+  if (!p) return fail(SPCN_EINVAL, "params is NULL");
+  if (npix <= 0) return fail(SPCN_EINVAL, "npix must be > 0");
+  if (!src || !dst || !p->src_od_table || !p->src_fit)
+    return fail(SPCN_EINVAL, "NULL buffer");
+  int rc = check_basis(p->tgt_basis, "target");
+  if (rc) return rc;
+  for (int c = 0; c < 3; ++c)
+    if (!std::isfinite(p->tgt_i0[c])) return fail(SPCN_EINVAL, "target i0 must be finite");
+  for (int j = 0; j < 2; ++j)
+    if (!(p->tgt_p99[j] > 0.0) || !std::isfinite(p->tgt_p99[j]))
+      return fail(SPCN_EINVAL, "target p99 must be positive and finite");
+  if (!(p->code_lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
+  if (p->max_sweeps < 0) return fail(SPCN_EINVAL, "max_sweeps must be >= 0");
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
+  if (((sa - da) & 15u) != 0)
+    return fail(SPCN_EINVAL, "src and dst must share their 16-byte alignment phase");
+  if (!workspace || workspace_bytes < spcn_xform_workspace_bytes(npix))
+    return fail(SPCN_EINVAL, "workspace too small (spcn_xform_workspace_bytes)");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "get_device");
+  if (dev < 0 || dev >= 64) return fail(SPCN_EINVAL, "device index out of range");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int slot;
+  DevParams* staging;
+  cudaEvent_t done, built;
+  {
+    std::lock_guard<std::mutex> lk(g_fitted_mu);
+    FittedSlots& fs = g_fitted[dev];
+    if (!fs.staging) {
+      if ((e = cudaMalloc(&fs.staging, sizeof(DevParams) * kDpSlots)) != cudaSuccess)
+        return cuda_fail(e, "staging alloc");
+      for (int k = 0; k < kDpSlots; ++k)
+        if ((e = cudaEventCreateWithFlags(&fs.done[k], cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&fs.built[k], cudaEventDisableTiming)) != cudaSuccess)
+          return cuda_fail(e, "event");
+    }
+    slot = fs.next;
+    fs.next = (fs.next + 1) % kDpSlots;
+    staging = fs.staging + slot;
+    done = fs.done[slot];
+    built = fs.built[slot];
+    // the slot's previous user (any stream) must be finished with it
+    if (fs.used[slot] && (e = cudaStreamWaitEvent(st, done, 0)) != cudaSuccess)
+      return cuda_fail(e, "slot wait");
+    fs.used[slot] = true;
+  }
+  XformBuildIn in{};
+  std::memcpy(in.tgt_basis, p->tgt_basis, sizeof(in.tgt_basis));
+  std::memcpy(in.tgt_p99, p->tgt_p99, sizeof(in.tgt_p99));
+  std::memcpy(in.tgt_i0, p->tgt_i0, sizeof(in.tgt_i0));
+  in.code_lam = p->code_lam;
+  in.max_sweeps = p->max_sweeps;
+  char* ws = static_cast<char*>(workspace);
+  if ((e = launch_xform_build(slot, in, p->src_od_table, static_cast<const double*>(p->src_fit),
+                              staging, ws, status_pinned, built, st)) != cudaSuccess)
+    return cuda_fail(e, "xform_build");
+  int64_t head = static_cast<int64_t>(((16 - (sa & 15u)) * 11u) & 15u);   // 3*head == -sa (mod 16)
+  if (head > npix) head = npix;
+  const int64_t body = ((npix - head) / 16) * 16;
+  auto* count = reinterpret_cast<unsigned long long*>(ws);
+  auto* items = reinterpret_cast<unsigned long long*>(ws + kWsHeader);
+  const unsigned long long cap = (workspace_bytes - kWsHeader) / 8;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (g_timing.load(std::memory_order_relaxed)) timing_begin(st, t0, t1);
+  e = launch_xform_main_c(slot, src + 3 * head, dst + 3 * head, body, count, items, cap,
+                          reinterpret_cast<const unsigned int*>(ws + 8), st);
+  if (t0) timing_end(st, t0, t1);
+  if (e != cudaSuccess) return cuda_fail(e, "xform_main_c");
+  if ((e = launch_xform_repair_c(slot, src, dst, npix, head, body, count, items, cap, st)) !=
+      cudaSuccess)
+    return cuda_fail(e, "xform_repair_c");
+  if ((e = cudaEventRecord(done, st)) != cudaSuccess) return cuda_fail(e, "slot record");
+  // the build (and everything enqueued before it, e.g. the fit's read-back)
+  // has reached host memory; the recolour itself is still in flight
+  if (status_pinned && (e = cudaEventSynchronize(built)) != cudaSuccess)
+    return cuda_fail(e, "build wait");
+  return SPCN_OK;
+}
+
 int spcn_xform_repair_count(const void* workspace, void* stream, int64_t* count) {
   g_err.clear();
   if (!workspace || !count) return fail(SPCN_EINVAL, "NULL argument");

@@ -98,11 +98,21 @@ __device__ __forceinline__ void or_if_pairs_differ(uint32_t& acc, uint32_t bit,
 }
 
 // OD of input byte `idx` (0..47) of the thread's 48-byte block, channel c.
+// ABS != 0: the table sits at the absolute shared-memory address ABS (the
+// caller placed it there), and `lut` is unused — the load is LDS [addr+ABS],
+// with no shared-window base to keep in a register.
+template <int ABS = 0>
 __device__ __forceinline__ float od_lookup(const uint8_t* lut, const uint32_t* w, int idx,
                                            uint32_t lc) {
   const uint32_t sel = 0x7604u | ((uint32_t)(idx & 3) << 4);
   const uint32_t addr = __byte_perm(w[idx >> 2], lc, sel);  // region*64K + x*256 + low byte
-  return *reinterpret_cast<const float*>(lut + addr);
+  if constexpr (ABS != 0) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(ABS));
+    return v;
+  } else {
+    return *reinterpret_cast<const float*>(lut + addr);
+  }
 }
 
 __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -115,15 +125,18 @@ __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, ui
 // returns non-zero when any of the pair's six roundings is not certified
 // (r_lo != r_hi); both pixels of such a pair go to the fp64 repair list.
 // I: the calibrated {I_lo, I_hi} per channel (MODE 2).
-template <int MODE>
+template <int MODE, int ABS = 0>
 __device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t* lut,
                                                  const uint32_t* w, int k, const uint32_t* lc,
                                                  uint32_t* ob, const float2* I,
                                                  uint32_t* badpairs = nullptr) {
   const int a = 3 * k, b = 3 * k + 3;
-  const float2 v0 = make_float2(od_lookup(lut, w, a, lc[0]), od_lookup(lut, w, b, lc[0]));
-  const float2 v1 = make_float2(od_lookup(lut, w, a + 1, lc[1]), od_lookup(lut, w, b + 1, lc[1]));
-  const float2 v2 = make_float2(od_lookup(lut, w, a + 2, lc[2]), od_lookup(lut, w, b + 2, lc[2]));
+  const float2 v0 =
+      make_float2(od_lookup<ABS>(lut, w, a, lc[0]), od_lookup<ABS>(lut, w, b, lc[0]));
+  const float2 v1 =
+      make_float2(od_lookup<ABS>(lut, w, a + 1, lc[1]), od_lookup<ABS>(lut, w, b + 1, lc[1]));
+  const float2 v2 =
+      make_float2(od_lookup<ABS>(lut, w, a + 2, lc[2]), od_lookup<ABS>(lut, w, b + 2, lc[2]));
   const FastPair fq = fast_pair(fp, v0, v1, v2);
   const float e[3][2] = {{fq.e0.x, fq.e0.y}, {fq.e1.x, fq.e1.y}, {fq.e2.x, fq.e2.y}};
   if (MODE == 1) {
@@ -181,7 +194,7 @@ __device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t*
 // One lane's 16 pixels at `blk` (48 bytes in shared memory), recoloured in
 // place; `gp0` = global index of its first pixel.  MODE 3 = identity copy
 // (memory-path ceiling).  Whole warp calls (the repair append is warp-wide).
-template <int MODE>
+template <int MODE, int ABS = 0>
 __device__ __forceinline__ void recolor_block(const FastS& fp, const uint8_t* lut,
                                               const uint32_t* lc, uint8_t* blk, bool valid,
                                               int64_t gp0, const RepairList& rl, int lane,
@@ -226,7 +239,7 @@ __device__ __forceinline__ void recolor_block(const FastS& fp, const uint8_t* lu
     } else {
 #pragma unroll
       for (int qq = 0; qq < 8; ++qq) {
-        const uint32_t bad = recolor_pair<MODE>(fp, lut, w, 2 * qq, lc, ob, I, &badpairs);
+        const uint32_t bad = recolor_pair<MODE, ABS>(fp, lut, w, 2 * qq, lc, ob, I, &badpairs);
         if (MODE == 0) badpairs |= (bad != 0u ? 1u : 0u) << qq;
 #pragma unroll
         for (int t = 0; t < 12; ++t)

@@ -25,6 +25,8 @@
 //                       colours and returns the largest relative error of the
 //                       fast path: a certification bound valid by exhaustion.
 #include "launch_count.h"
+#include "params.cuh"
+#include "spcn.h"
 #include "recolor.cuh"
 #include "spcn_device.cuh"
 #include "xform.h"
@@ -51,23 +53,34 @@ struct SmemLut {
 // finished reading it.  No CTA-wide stage coupling: a slow warp never holds
 // back the others' refills.  Work: slices grid-strided over all warps; NSUB
 // amortises the per-slice bookkeeping (bulk ops, barrier waits) over more px.
+// The OD table is placed at the ABSOLUTE shared address kXAbs (the dynamic
+// window starts at a small driver-reserved offset; up to kXAbs bytes of
+// padding are allocated in front), so its lookups are LDS [addr + kXAbs].
+constexpr uint32_t kXAbs = 4096;
+
 template <int CW, int REP, int NSW, int BLK, int NSUB>
 struct WCfg {
   static constexpr int kThreads = 32 * CW;
   static constexpr int kSlicePx = 512 * NSUB;
   static constexpr int kSlotBytes = 3 * kSlicePx;
   static constexpr int kLutBytes = LutLayout<REP>::kBytes;
-  static constexpr size_t kSmem = kLutBytes + (size_t)CW * NSW * kSlotBytes + CW * NSW * 8;
+  static constexpr size_t kSmem =
+      kXAbs + kLutBytes + (size_t)CW * NSW * kSlotBytes + CW * NSW * 8;
   static_assert(kSmem <= (BLK == 1 ? 227 * 1024 : 113 * 1024), "shared memory budget");
 };
 
+// fp: the kernel's __grid_constant__ parameter block, or a __constant__ slot
+// of a device-built recolouring — both constant-bank operands after inlining.
 template <int MODE, int CW, int REP, int NSW, int BLK, int NSUB>
-__global__ void __launch_bounds__(32 * CW, BLK)
-    k_xform_warp(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
-                 const __grid_constant__ FastP fp, RepairList rl) {
+__device__ __forceinline__ void xform_warp_body(const uint8_t* __restrict__ src,
+                                                uint8_t* __restrict__ dst, int64_t npix,
+                                                const FastP& fp, RepairList rl) {
   using C = WCfg<CW, REP, NSW, BLK, NSUB>;
   constexpr int kSlicePx = C::kSlicePx, kSlotBytes = C::kSlotBytes;
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  if (base > kXAbs) __trap();   // layout assumption (window base <= 4 KB)
+  uint8_t* smem = smem_raw + (kXAbs - base);   // the table at absolute kXAbs
   const uint8_t* lut = smem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* myslots = smem + C::kLutBytes + (size_t)warp * NSW * kSlotBytes;
@@ -116,7 +129,7 @@ __global__ void __launch_bounds__(32 * CW, BLK)
     uint8_t* sbase = myslots + s * kSlotBytes;
 #pragma unroll
     for (int u = 0; u < NSUB; ++u)
-      recolor_block<MODE>(fp, lut, lc, sbase + u * 1536 + 48 * lane, u * 512 + 16 * lane < n,
+      recolor_block<MODE, kXAbs>(fp, lut, lc, sbase + u * 1536 + 48 * lane, u * 512 + 16 * lane < n,
                           j * kSlicePx + u * 512 + 16 * lane, rl, lane, I);
     fence_proxy_async_smem();
     __syncwarp();
@@ -136,20 +149,22 @@ __global__ void __launch_bounds__(32 * CW, BLK)
   if (lane == 0) bulk_wait_all();
 }
 
+template <int MODE, int CW, int REP, int NSW, int BLK, int NSUB>
+__global__ void __launch_bounds__(32 * CW, BLK)
+    k_xform_warp(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
+                 const __grid_constant__ FastP fp, RepairList rl) {
+  xform_warp_body<MODE, CW, REP, NSW, BLK, NSUB>(src, dst, npix, fp, rl);
+}
+
 // fp64 recompute of the listed pixels; if the list overflowed (count > cap)
 // every pixel of the body is recomputed instead.  The fp64 table is staged in
 // shared memory (per-thread table indices differ, so reading it from the
 // kernel-parameter bank would serialise).
-__global__ void __launch_bounds__(256) k_xform_repair(const uint8_t* __restrict__ src,
-                                                      uint8_t* __restrict__ dst, int64_t npix,
-                                                      const __grid_constant__ StrictP sp,
-                                                      RepairList rl) {
-  const unsigned long long n = *rl.count;
-  if (n == 0) return;
-  __shared__ double lut[3 * 256];
-  for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
-  __syncthreads();
-  const NnlsGram G = gram_of(sp);
+__device__ __forceinline__ void repair_body(const uint8_t* __restrict__ src,
+                                            uint8_t* __restrict__ dst, int64_t npix,
+                                            const StrictP& sp, const double* lut,
+                                            const NnlsGram& G, RepairList rl,
+                                            unsigned long long n) {
   if (n > rl.cap) {
     for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < npix; i += 256ll * gridDim.x) {
       const uint32_t out =
@@ -173,6 +188,18 @@ __global__ void __launch_bounds__(256) k_xform_repair(const uint8_t* __restrict_
   }
 }
 
+__global__ void __launch_bounds__(256) k_xform_repair(const uint8_t* __restrict__ src,
+                                                      uint8_t* __restrict__ dst, int64_t npix,
+                                                      const __grid_constant__ StrictP sp,
+                                                      RepairList rl) {
+  const unsigned long long n = *rl.count;
+  if (n == 0) return;
+  __shared__ double lut[3 * 256];
+  for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
+  __syncthreads();
+  repair_body(src, dst, npix, sp, lut, gram_of(sp), rl, n);
+}
+
 __global__ void __launch_bounds__(256) k_xform_strict(const uint8_t* __restrict__ src,
                                                       uint8_t* __restrict__ dst, int64_t npix,
                                                       const __grid_constant__ StrictP sp) {
@@ -194,10 +221,9 @@ __global__ void __launch_bounds__(256) k_xform_strict(const uint8_t* __restrict_
 // (the exact product the certification scales) with the fp64 reference
 // value y_ref = i0 * exp(-v') computed in the reference's operation order;
 // record max |y_ref - y_fast| / y_fast over colours with y_fast > 0.
-__global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP fp,
-                                                   const __grid_constant__ StrictP sp,
-                                                   unsigned int* __restrict__ max_bits,
-                                                   uint32_t q0, uint32_t q1) {
+__device__ __forceinline__ void calibrate_body(const FastP& fp, const StrictP& sp,
+                                               unsigned int* __restrict__ max_bits, uint32_t q0,
+                                               uint32_t q1) {
   __shared__ double lut[3 * 256];
   __shared__ float flut[3 * 256];
   for (int i = threadIdx.x; i < 3 * 256; i += 256) {
@@ -241,24 +267,137 @@ __global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP
   if ((threadIdx.x & 31) == 0) atomicMax(max_bits, __float_as_uint(worst));
 }
 
+__global__ void __launch_bounds__(256) k_calibrate(const __grid_constant__ FastP fp,
+                                                   const __grid_constant__ StrictP sp,
+                                                   unsigned int* __restrict__ max_bits,
+                                                   uint32_t q0, uint32_t q1) {
+  calibrate_body(fp, sp, max_bits, q0, q1);
+}
+
+// ---------------------------------------------------------------------------
+// Device-built recolouring: fit -> transform with no host round trip.
+// k_build_xform forms StrictP / FastP of one recolouring on the device from
+// the fit's arena (basis, p99, absent flags) and the source OD table already
+// resident for the SNMF, with the same params.cuh code the host runs; the
+// block is copied into a __constant__ slot, and the slot-templated kernels
+// read it exactly as the host path reads its __grid_constant__ block (both
+// are constant-bank operands, so the main kernel's SASS is unchanged).  A
+// recolouring the fast path cannot take (status != 0: invalid fit, degenerate
+// p99, ill-conditioned basis) leaves the output untouched; the caller then
+// runs the host-checked path, which raises the reference's error or takes
+// the strict path.
+__constant__ DevParams c_dp[kDpSlots];
+
+__global__ void __launch_bounds__(256) k_build_xform(const __grid_constant__ XformBuildIn in,
+                                                     const double* __restrict__ lut,
+                                                     const double* __restrict__ fit,
+                                                     DevParams* __restrict__ out,
+                                                     unsigned int* __restrict__ ws_hdr) {
+  StrictP& sp = out->sp;
+  for (int i = threadIdx.x; i < 3 * 256; i += 256) {
+    (&sp.lut[0][0])[i] = lut[i];
+    (&out->fp.lut[0][0])[i] = static_cast<float>(lut[i]);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  // arena B: basis f64[6] | p99 f64[2] | info i32[4] | absent i32[2]
+  const double* basis = fit;
+  const double* p99 = fit + 6;
+  const int32_t* absent = reinterpret_cast<const int32_t*>(fit + 10);
+  int32_t st = 0;
+  if (absent[0] || absent[1]) st = -SPCN_ESTAIN_ABSENT;
+  double f[2] = {1.0, 1.0};
+  for (int j = 0; j < 2 && st == 0; ++j) {
+    if (!(p99[j] > 0.0) || !isfinite(p99[j])) st = -SPCN_EDEGENERATE;   // scale_factors
+    else f[j] = __ddiv_rn(in.tgt_p99[j], p99[j]);
+    if (st == 0 && (!(f[j] > 0.0) || !isfinite(f[j]))) st = -SPCN_EDEGENERATE;
+  }
+  for (int k = 0; k < 6 && st == 0; ++k)                                // api.cu check_basis
+    if (!isfinite(basis[k]) || basis[k] < 0) st = -SPCN_EINVAL;
+  for (int j = 0; j < 2 && st == 0; ++j) {
+    const double nrm = sqrt(p_add(p_add(p_mul(basis[j], basis[j]), p_mul(basis[2 + j], basis[2 + j])),
+                                  p_mul(basis[4 + j], basis[4 + j])));
+    if (fabs(nrm - 1.0) > 1e-9) st = -SPCN_EINVAL;
+  }
+  fill_strict_scalars(sp, basis, in.tgt_basis, f, in.tgt_i0, in.code_lam, in.max_sweeps);
+  if (st == 0 && !fill_fast_scalars(out->fp, sp, true, nullptr)) st = 1;   // strict path only
+  out->status = st;
+  ws_hdr[0] = ws_hdr[1] = 0u;   // repair count
+  ws_hdr[2] = 0u;               // calibration word
+}
+
+template <int SLOT>
+__global__ void __launch_bounds__(256) k_calibrate_c(unsigned int* __restrict__ max_bits) {
+  if (c_dp[SLOT].status != 0) return;
+  calibrate_body(c_dp[SLOT].fp, c_dp[SLOT].sp, max_bits, 0u, 1u << 23);
+}
+
+template <int SLOT, int CW, int REP, int NSW, int BLK, int NSUB>
+__global__ void __launch_bounds__(32 * CW, BLK)
+    k_xform_warp_c(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
+                   RepairList rl) {
+  // a declined recolouring runs zero slices (an early exit here would make
+  // the compiler keep the shared-memory window base out of uniform registers)
+  xform_warp_body<2, CW, REP, NSW, BLK, NSUB>(src, dst, c_dp[SLOT].status == 0 ? npix : 0,
+                                              c_dp[SLOT].fp, rl);
+}
+
+// The repair list of the vector body [head, head + body), plus the (< 16 px)
+// unaligned head and tail of the buffer, all on the fp64 path.
+template <int SLOT>
+__global__ void __launch_bounds__(256) k_xform_repair_c(const uint8_t* __restrict__ src,
+                                                        uint8_t* __restrict__ dst, int64_t npix,
+                                                        int64_t head, int64_t body,
+                                                        RepairList rl) {
+  const StrictP& sp = c_dp[SLOT].sp;
+  if (c_dp[SLOT].status != 0) return;
+  const unsigned long long n = *rl.count;
+  const bool edges = blockIdx.x == 0 && (head > 0 || head + body < npix);
+  if (n == 0 && !edges) return;
+  __shared__ double lut[3 * 256];
+  for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
+  __syncthreads();
+  const NnlsGram G = gram_of(sp);
+  if (edges) {
+    const int64_t tail = npix - head - body;
+    for (int64_t k = threadIdx.x; k < head + tail; k += 256) {
+      const int64_t i = k < head ? k : head + body + (k - head);
+      const uint32_t out = strict_pixel(sp, G, SmemLut{lut}, src[3 * i], src[3 * i + 1], src[3 * i + 2]);
+      dst[3 * i] = out & 255u;
+      dst[3 * i + 1] = (out >> 8) & 255u;
+      dst[3 * i + 2] = (out >> 16) & 255u;
+    }
+  }
+  if (n > 0) repair_body(src + 3 * head, dst + 3 * head, body, sp, lut, G, rl, n);
+}
+
 // ------------------------------------------------------------------ launchers
 static int g_sm_count = 0;
 
 using XformFn = void (*)(const uint8_t*, uint8_t*, int64_t, FastP, RepairList);
 
+using XformCFn = void (*)(const uint8_t*, uint8_t*, int64_t, RepairList);
+
 struct Shape {
   int cw, rep, nsub, blk, nsw, threads, tile_px, blocks_per_sm;
   size_t smem;
   XformFn fn[4];
+  XformCFn cfn[kDpSlots];   // device-built parameter slots (production shape only)
 };
 
-template <int CW, int REP, int NSW, int BLK, int NSUB>
+template <int CW, int REP, int NSW, int BLK, int NSUB, bool SLOTS = false>
 Shape make_wshape() {
   using C = WCfg<CW, REP, NSW, BLK, NSUB>;
-  return Shape{CW, REP, NSUB, BLK, NSW, C::kThreads, CW * C::kSlicePx, 0, C::kSmem,
-               {k_xform_warp<0, CW, REP, NSW, BLK, NSUB>, k_xform_warp<1, CW, REP, NSW, BLK, NSUB>,
-                k_xform_warp<2, CW, REP, NSW, BLK, NSUB>,
-                k_xform_warp<3, CW, REP, NSW, BLK, NSUB>}};
+  Shape s{CW, REP, NSUB, BLK, NSW, C::kThreads, CW * C::kSlicePx, 0, C::kSmem,
+          {k_xform_warp<0, CW, REP, NSW, BLK, NSUB>, k_xform_warp<1, CW, REP, NSW, BLK, NSUB>,
+           k_xform_warp<2, CW, REP, NSW, BLK, NSUB>, k_xform_warp<3, CW, REP, NSW, BLK, NSUB>},
+          {nullptr, nullptr}};
+  static_assert(kDpSlots == 2, "slot table");
+  if constexpr (SLOTS) {
+    s.cfn[0] = k_xform_warp_c<0, CW, REP, NSW, BLK, NSUB>;
+    s.cfn[1] = k_xform_warp_c<1, CW, REP, NSW, BLK, NSUB>;
+  }
+  return s;
 }
 
 // Compiled shapes; SPCN_XFORM_SHAPE="CWxREPxNSUBxBLK" selects one
@@ -266,11 +405,9 @@ Shape make_wshape() {
 // SPCN_XFORM_IDENTITY=1 makes the kernel copy input to output (memory-path
 // ceiling measurement only).
 static Shape g_shapes[] = {
-    make_wshape<16, 24, 3, 1, 2>(),   // production: per-warp rings of 2x512-px slots, mixed table
-    make_wshape<16, 16, 3, 1, 2>(), make_wshape<16, 32, 4, 1, 1>(),
-    make_wshape<16, 16, 2, 1, 3>(), make_wshape<12, 16, 3, 1, 3>(), make_wshape<16, 16, 4, 1, 1>(),
-    make_wshape<8, 16, 2, 2, 2>(), make_wshape<8, 16, 3, 2, 1>(),
-    make_wshape<20, 16, 2, 1, 2>(), make_wshape<16, 32, 2, 1, 2>(), make_wshape<20, 24, 2, 1, 2>(),
+    make_wshape<16, 24, 3, 1, 2, true>(),   // production: per-warp rings of 2x512-px slots, mixed table
+    make_wshape<16, 16, 3, 1, 2>(), make_wshape<16, 16, 2, 1, 3>(), make_wshape<16, 16, 4, 1, 1>(),
+    make_wshape<8, 16, 3, 2, 1>(), make_wshape<20, 16, 2, 1, 2>(), make_wshape<20, 24, 2, 1, 2>(),
     make_wshape<16, 24, 4, 1, 1>()};
 static Shape* g_shape = nullptr;
 static bool g_identity = false;
@@ -299,6 +436,12 @@ cudaError_t xform_setup_device() {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pick->smem);
     if (e != cudaSuccess) return e;
   }
+  // the device-built path always runs the production shape
+  for (auto fn : g_shapes[0].cfn) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)g_shapes[0].smem);
+    if (e != cudaSuccess) return e;
+  }
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pick->blocks_per_sm, pick->fn[2],
                                                     pick->threads, pick->smem);
   if (e != cudaSuccess) return e;
@@ -318,6 +461,58 @@ cudaError_t launch_xform_main(int mode, const uint8_t* src, uint8_t* dst, int64_
   const int grid = static_cast<int>(min64(ntiles, (int64_t)g_sm_count * s.blocks_per_sm));
   RepairList rl{count, items, cap, alpha_bits};
   s.fn[g_identity ? 3 : mode]<<<grid, s.threads, s.smem, st>>>(src, dst, npix, fp, rl);
+  return launched();
+}
+
+cudaError_t launch_xform_build(int slot, const XformBuildIn& in, const double* lut,
+                               const double* fit, DevParams* staging, void* ws,
+                               int32_t* status_host, cudaEvent_t built, cudaStream_t st) {
+  cudaError_t e = xform_setup_device();
+  if (e != cudaSuccess) return e;
+  unsigned int* hdr = static_cast<unsigned int*>(ws);
+  k_build_xform<<<1, 256, 0, st>>>(in, lut, fit, staging, hdr);
+  if ((e = launched()) != cudaSuccess) return e;
+  e = cudaMemcpyToSymbolAsync(c_dp, staging, sizeof(DevParams), slot * sizeof(DevParams),
+                              cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  if (status_host &&
+      (e = cudaMemcpyAsync(status_host, &staging->status, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           st)) != cudaSuccess)
+    return e;
+  if (built && (e = cudaEventRecord(built, st)) != cudaSuccess) return e;
+  const int grid = g_sm_count * 8;   // launch_calibrate's full-range grid
+  if (slot == 0) k_calibrate_c<0><<<grid, 256, 0, st>>>(hdr + 2);
+  else k_calibrate_c<1><<<grid, 256, 0, st>>>(hdr + 2);
+  return launched();
+}
+
+cudaError_t launch_xform_main_c(int slot, const uint8_t* src, uint8_t* dst, int64_t npix,
+                                unsigned long long* count, unsigned long long* items,
+                                unsigned long long cap, const unsigned int* alpha_bits,
+                                cudaStream_t st) {
+  cudaError_t e = xform_setup_device();
+  if (e != cudaSuccess) return e;
+  if (npix <= 0) return cudaSuccess;
+  const Shape& s = g_shapes[0];
+  int bps = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, s.cfn[slot], s.threads, s.smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (npix + s.tile_px - 1) / s.tile_px;
+  const int grid = static_cast<int>(min64(ntiles, (int64_t)g_sm_count * (bps < 1 ? 1 : bps)));
+  RepairList rl{count, items, cap, alpha_bits};
+  s.cfn[slot]<<<grid, s.threads, s.smem, st>>>(src, dst, npix, rl);
+  return launched();
+}
+
+cudaError_t launch_xform_repair_c(int slot, const uint8_t* src, uint8_t* dst, int64_t npix,
+                                  int64_t head, int64_t body, unsigned long long* count,
+                                  unsigned long long* items, unsigned long long cap,
+                                  cudaStream_t st) {
+  cudaError_t e = xform_setup_device();
+  if (e != cudaSuccess) return e;
+  RepairList rl{count, items, cap};
+  if (slot == 0) k_xform_repair_c<0><<<g_sm_count * 4, 256, 0, st>>>(src, dst, npix, head, body, rl);
+  else k_xform_repair_c<1><<<g_sm_count * 4, 256, 0, st>>>(src, dst, npix, head, body, rl);
   return launched();
 }
 

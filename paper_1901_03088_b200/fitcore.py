@@ -72,13 +72,20 @@ class FitBuffers:
         self.pin_a = t.empty(256, dtype=t.uint8, pin_memory=True)
         self.pin_b = t.empty(256, dtype=t.uint8, pin_memory=True)
         self.pin_lut = t.empty(768, dtype=t.float64, pin_memory=True)
+        self.pin_status = t.zeros(4, dtype=t.int32, pin_memory=True)   # device-built xform
         self.cand = {}          # (W, H, plan) -> candidate descriptors on the device
         # raw pointers / numpy views of the fixed buffers (ctypes arguments)
         self.arena_a_ptr, self.arena_b_ptr = _lib.ptr(self.arena_a), _lib.ptr(self.arena_b)
         self.sample_ptr, self.pin_a_ptr = _lib.ptr(self.sample), _lib.ptr(self.pin_a)
+        self.lut_ptr = _lib.ptr(self.lut)
+        self.offsets_ptr = self.arena_a_ptr + A_OFFS
+        self.h_ptr, self.scratch_ptr = _lib.ptr(self.h), _lib.ptr(self.scratch)
+        self.history_ptr, self.q_ptr = _lib.ptr(self.history), _lib.ptr(self.q)
+        self.sel_ptr = _lib.ptr(self.sel)
         self.pin_b_ptr, self.pin_lut_ptr = _lib.ptr(self.pin_b), _lib.ptr(self.pin_lut)
         self.pin_a_np, self.pin_b_np = self.pin_a.numpy(), self.pin_b.numpy()
         self.pin_lut_np = self.pin_lut.numpy()
+        self.pin_status_ptr, self.pin_status_np = _lib.ptr(self.pin_status), self.pin_status.numpy()
 
     def offsets(self):
         """[0, m] of the current sample (written by k_visit, or by the host)."""
@@ -135,6 +142,50 @@ def provenance(plan, cfg, code_lam, per_patch_stats, p99_mode, source_label) -> 
                                            p99_mode)}
 
 
+def basis_enqueue(fb: FitBuffers, sample_flat, m: int, i0: np.ndarray, cfg, *, code_lam: float,
+                  pooled: bool) -> None:
+    """Stream-ordered: OD table upload -> SNMF -> densities (code_lam, into
+    fb.h as (2, m) rows) -> pooled p99 (pooled=True) -> read-back of arena B
+    into fb.pin_b.  sample_flat: CUDA uint8 (3m,) tensor or its device
+    address.  The caller syncs the stream before parse_*."""
+    if m < 10:
+        raise InsufficientPixelsError(
+            f"basis fit: insufficient pixels: need at least 10 OD samples, got {m}")
+    L = _lib.lib()
+    # the reference's OD table (numpy log) into the pinned staging buffer; the
+    # previous fit's upload of it has completed (its read-back was waited for)
+    fb.pin_lut_np[:] = od_table_cached(np.ascontiguousarray(i0, np.float64).tobytes()).reshape(-1)
+    c = snmf_cfg_cached(float(cfg.lam), float(cfg.rel_tol), int(cfg.max_outer_iters),
+                        int(cfg.seed), snmf_cluster(m))
+    sp = sample_flat if isinstance(sample_flat, int) else _lib.ptr(sample_flat)
+    # table upload -> SNMF -> densities -> pooled p99 -> read-back, one call
+    _lib.check(L.spcn_fit_basis_step(sp, m, fb.offsets_ptr, fb.pin_lut_ptr, fb.lut_ptr,
+                                     ctypes.byref(c), fb.scratch_ptr, fb.history_ptr,
+                                     fb.arena_b_ptr, float(code_lam), 2000, fb.h_ptr, fb.q_ptr,
+                                     fb.sel_ptr, 1 if pooled else 0, fb.pin_b_ptr, B_BYTES,
+                                     _lib.stream_handle()), "fit_basis_step")
+
+
+def parse_pooled(fb: FitBuffers, m: int, i0: np.ndarray, cfg, prov: dict,
+                 stacklevel: int = 4) -> FitParams:
+    """FitParams of a pooled-p99 fit from arena B (read back, stream synced),
+    with the reference's warnings and errors (src/pipeline.py:228-257)."""
+    raw = fb.pin_b_np[:B_BYTES].copy()
+    basis = raw[B_BASIS:B_P99].view(np.float64).reshape(3, 2).copy()
+    p99 = raw[B_P99:B_INFO].view(np.float64).copy()
+    info = raw[B_INFO:B_ABSENT].view(np.int32)
+    absent = raw[B_ABSENT:B_BYTES].view(np.int32)
+    snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters, stacklevel=stacklevel)
+    for j in range(2):
+        if absent[j]:
+            raise StainAbsentError(f"density stats: stain absent: no {_STAIN_NAMES[j]} "
+                                   "density observed")
+    if not (np.isfinite(p99).all() and (p99 >= 0).all()):
+        raise ValueError(f"density stats: p99 must be finite and non-negative, got {p99}")
+    return FitParams(i0=np.asarray(i0, np.float64).copy(), basis=basis,
+                     stats=StainStats(p99=p99, sample_count=m), provenance=prov)
+
+
 def fit_tail(fb: FitBuffers, sample_flat, m: int, i0: np.ndarray, plan, cfg, *,
              code_lam: float, per_patch_stats: bool, p99_mode: str, used_counts,
              source_label: str = "", chunks=None, comm=None, stage=None) -> FitParams:
@@ -146,42 +197,13 @@ def fit_tail(fb: FitBuffers, sample_flat, m: int, i0: np.ndarray, plan, cfg, *,
     chunks: whole-slide pass generator (global p99 mode); comm: collectives of
     a row-band group (global mode)."""
     stage = stage or (lambda label, fn, *a, **k: fn(*a, **k))
-    if m < 10:
-        raise InsufficientPixelsError(
-            f"basis fit: insufficient pixels: need at least 10 OD samples, got {m}")
-    L = _lib.lib()
-    # the reference's OD table (numpy log) into the pinned staging buffer; the
-    # previous fit's upload of it has completed (its read-back was waited for)
-    fb.pin_lut_np[:] = od_table_cached(np.ascontiguousarray(i0, np.float64).tobytes()).reshape(-1)
-    c = snmf_cfg_cached(float(cfg.lam), float(cfg.rel_tol), int(cfg.max_outer_iters),
-                        int(cfg.seed), snmf_cluster(m))
-    h = fb.h[:2 * m].view(2, m)
     pooled = p99_mode == "sample" and not per_patch_stats
-    st = _lib.stream_handle()
-    # table upload -> SNMF -> densities -> pooled p99 -> read-back, one call
-    _lib.check(L.spcn_fit_basis_step(_lib.ptr(sample_flat), m, _lib.ptr(fb.offsets()),
-                                     fb.pin_lut_ptr, _lib.ptr(fb.lut), ctypes.byref(c),
-                                     _lib.ptr(fb.scratch), _lib.ptr(fb.history), fb.arena_b_ptr,
-                                     float(code_lam), 2000, _lib.ptr(h), _lib.ptr(fb.q),
-                                     _lib.ptr(fb.sel), 1 if pooled else 0, fb.pin_b_ptr, B_BYTES,
-                                     st), "fit_basis_step")
-    _lib.check(L.spcn_stream_sync(st), "stream_sync")
+    basis_enqueue(fb, sample_flat, m, i0, cfg, code_lam=code_lam, pooled=pooled)
+    h = fb.h[:2 * m].view(2, m)
+    _lib.check(_lib.lib().spcn_stream_sync(_lib.stream_handle()), "stream_sync")
     prov = provenance(plan, cfg, code_lam, per_patch_stats, p99_mode, source_label)
     if pooled:
-        raw = fb.pin_b_np[:B_BYTES].copy()
-        basis = raw[B_BASIS:B_P99].view(np.float64).reshape(3, 2).copy()
-        p99 = raw[B_P99:B_INFO].view(np.float64).copy()
-        info = raw[B_INFO:B_ABSENT].view(np.int32)
-        absent = raw[B_ABSENT:B_BYTES].view(np.int32)
-        snmf.warn_flags(m, int(info[2]), cfg.max_outer_iters, stacklevel=4)
-        for j in range(2):
-            if absent[j]:
-                raise StainAbsentError(f"density stats: stain absent: no {_STAIN_NAMES[j]} "
-                                       "density observed")
-        if not (np.isfinite(p99).all() and (p99 >= 0).all()):
-            raise ValueError(f"density stats: p99 must be finite and non-negative, got {p99}")
-        return FitParams(i0=np.asarray(i0, np.float64).copy(), basis=basis,
-                         stats=StainStats(p99=p99, sample_count=m), provenance=prov)
+        return parse_pooled(fb, m, i0, cfg, prov, stacklevel=5)
     raw = fb.pin_b_np[:B_ABSENT].copy()
     basis = raw[B_BASIS:B_P99].view(np.float64).reshape(3, 2).copy()
     snmf.warn_flags(m, int(raw[B_INFO:B_ABSENT].view(np.int32)[2]), cfg.max_outer_iters,

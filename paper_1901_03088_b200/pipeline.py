@@ -9,6 +9,7 @@ GPU produced.
 """
 from __future__ import annotations
 
+import ctypes
 import os
 import time
 import warnings
@@ -323,7 +324,7 @@ def _fit_sample_resident(fb, slide: DeviceSource, plan: SamplePlan, need_counts:
         tk = np.frombuffer(c["takes"][:(k0 + n) * TAKE_DT.itemsize].cpu().numpy().tobytes(),
                            dtype=TAKE_DT)
         used_counts = [int(v) for v in tk["take_nonwhite"] if v > 0]
-    meta = PixelSample(non_white=fb.sample[:3 * m].view(m, 3), patch_counts=used_counts,
+    meta = PixelSample(non_white=None, patch_counts=used_counts,     # sample: fb.sample[:3m]
                        bright=None, patches_visited=int(st[1]), patches_used=int(st[2]),
                        bright_hist=None)
     i0 = raw[A_I0:A_EMPTY].view(np.float64).copy()
@@ -425,6 +426,22 @@ def slide_chunks(slide, rows: int = 2048):
     return gen
 
 
+def _fit_sample_checked(fb, slide: DeviceSource, plan: SamplePlan, need_counts: bool):
+    """Resident slide: visit loop + i0 on the device (one host round trip),
+    with the reference's blank-slide error and background warnings."""
+    with _dev.nvtx("spcn.fit.sample"):
+        m, i0, meta, empty = _stage("sampling", _fit_sample_resident, fb, slide, plan,
+                                    need_counts)
+    if m == 0:
+        raise BlankSlideError("sampling: blank slide: no non-white pixels found in any "
+                              "sampled patch")
+    for c in np.flatnonzero(empty):
+        warnings.warn(f"no pixels brighter than the white threshold in the "
+                      f"{('red', 'green', 'blue')[c]} channel; falling back to 255",
+                      optics.BackgroundEstimateWarning, stacklevel=4)
+    return m, i0, meta
+
+
 def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), *,
         code_lam: float = 0.0, per_patch_stats: bool = False, source_label: str = "",
         stats: RunStats | None = None, p99_mode: str = "sample") -> FitParams:
@@ -446,17 +463,7 @@ def fit(slide, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), 
                          plan.target_pixels, cfg.max_outer_iters)
     t0 = time.perf_counter()
     if isinstance(slide, DeviceSource):
-        # resident slide: visit loop + i0 on the device, one host round trip
-        with _dev.nvtx("spcn.fit.sample"):
-            m, i0, meta, empty = _stage("sampling", _fit_sample_resident, fb, slide, plan,
-                                        per_patch_stats)
-        if m == 0:
-            raise BlankSlideError("sampling: blank slide: no non-white pixels found in any "
-                                  "sampled patch")
-        for c in np.flatnonzero(empty):
-            warnings.warn(f"no pixels brighter than the white threshold in the "
-                          f"{('red', 'green', 'blue')[c]} channel; falling back to 255",
-                          optics.BackgroundEstimateWarning, stacklevel=2)
+        m, i0, meta = _fit_sample_checked(fb, slide, plan, per_patch_stats)
         sample_flat = fb.sample[:3 * m]
         stats.sampling_s += time.perf_counter() - t0
         t0 = time.perf_counter()
@@ -718,14 +725,97 @@ def _transform_streamed(slide, sink, plan, strips, width, nslots, gauge, progres
         commit()
 
 
+def _fused_ok(src: DeviceSource, tp: FitParams, out, precision: str, p99_mode: str,
+              per_patch_stats: bool) -> bool:
+    """Whether normalize() may run fit -> transform as one stream-ordered
+    sequence with the recolouring built on the device (fit_transform_resident)."""
+    if os.environ.get("SPCN_FUSED", "1") == "0":
+        return False
+    tgt_p99 = np.asarray(tp.stats.p99, dtype=np.float64)
+    return (precision == "exact" and p99_mode == "sample" and not per_patch_stats
+            and src.width * src.height >= XformPlan.CALIBRATE_MIN_PIXELS
+            and bool(np.all(tgt_p99 > 0)) and bool(np.all(np.isfinite(tgt_p99)))
+            and (src.tensor.data_ptr() - out.data_ptr()) % 16 == 0)
+
+
+def fit_transform_resident(src: DeviceSource, target: FitParams, out, *,
+                           plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(),
+                           code_lam: float = 0.0, stats: RunStats | None = None,
+                           source_label: str = "") -> FitParams:
+    """fit(src) then transform(src, fit, target) into the CUDA tensor `out`
+    (src/cli.py:220-244 for a resident slide, pooled p99, EXACT) with one host
+    round trip after sampling and one after the parameter build: the SNMF,
+    p99, the recolouring's parameters (spcn_xform_rgb8_fitted builds them on
+    the device from the fit), the calibration and the recolour run back to
+    back on the stream, and the call returns while the recolour is still
+    running (stream-ordered, like transform() of a resident slide).  Same bytes, warnings and errors as fit + transform: the
+    fit's are raised from its read-back before anything else, and a
+    recolouring the device path declines (degenerate p99, ill-conditioned
+    basis) is redone by transform() with host parameters, which raises the
+    reference's error or takes the strict path.  Returns the source fit."""
+    from . import fitcore
+
+    stats = stats if stats is not None else RunStats()
+    t0 = time.perf_counter()
+    fb = fitcore.buffers(src.tensor.device, plan.target_pixels, cfg.max_outer_iters)
+    L = _lib.lib()
+    npix = src.width * src.height
+    # everything that does not depend on the sample, before the sampling wait
+    p = _fitted_params(target, float(code_lam))
+    p.src_od_table = fb.lut_ptr
+    p.src_fit = fb.arena_b_ptr
+    ws_bytes = int(L.spcn_xform_workspace_bytes(npix))
+    st = _lib.stream_handle()
+    ws = _dev.workspace(ws_bytes, stream=st)
+    m, i0, meta = _fit_sample_checked(fb, src, plan, False)
+    stats.sampled_pixels = m
+    stats.patches = meta.patches_used
+    t1 = time.perf_counter()
+    stats.sampling_s += t1 - t0
+    with _dev.nvtx("spcn.fit_transform"):
+        fitcore.basis_enqueue(fb, fb.sample_ptr, m, i0, cfg, code_lam=code_lam, pooled=True)
+        fb.pin_status_np[0] = -1
+        # returns once the build status (and the fit's read-back before it)
+        # is in host memory; the recolour is still running, stream-ordered
+        _lib.check(L.spcn_xform_rgb8_fitted(src.tensor.data_ptr(), out.data_ptr(), npix,
+                                            ctypes.byref(p), _lib.ptr(ws), ws_bytes,
+                                            fb.pin_status_ptr, st), "xform_rgb8_fitted")
+    prov = fitcore.provenance(plan, cfg, code_lam, False, "sample", source_label)
+    sp = fitcore.parse_pooled(fb, m, i0, cfg, prov, stacklevel=3)
+    t2 = time.perf_counter()
+    stats.basis_fit_s += t2 - t1
+    if int(fb.pin_status_np[0]) != 0:
+        transform(src, sp, target, DeviceWriter(src.width, src.height, out=out),
+                  code_lam=code_lam, stats=stats, precision="exact")
+    else:
+        stats.transform_s += time.perf_counter() - t2
+        stats.transformed_pixels = npix
+        stats.total_s = stats.sampling_s + stats.basis_fit_s + stats.transform_s
+    return sp
+
+
+def _fitted_params(target: FitParams, code_lam: float):
+    """spcn_xform_fitted's host half (target profile + options)."""
+    p = _lib.XformFitted()
+    np.frombuffer(p, dtype=np.float64, count=12, offset=16)[:] = np.concatenate([
+        _dev.f64_array(target.basis, 6, "tgt_basis"),
+        np.asarray(target.stats.p99, dtype=np.float64).reshape(2),
+        _dev.f64_array(target.i0, 3, "tgt_i0"), [code_lam]])
+    p.max_sweeps = 2000
+    return p
+
+
 def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
               cfg: SnmfConfig = SnmfConfig(), code_lam: float = 0.0,
               per_patch_stats: bool = False, strip_height: int = DEFAULT_STRIP_HEIGHT,
               precision: str = "exact", stats: RunStats | None = None,
-              p99_mode: str = "sample"):
+              p99_mode: str = "sample", out=None):
     """The drop-in entry: fit(source), fit(target) (or use a FitParams / profile
     for the target), then transform — exactly the reference's _normalize_one
-    (src/cli.py:220-244).  numpy in → numpy out; CUDA tensor in → CUDA tensor out."""
+    (src/cli.py:220-244).  numpy in → numpy out; CUDA tensor in → CUDA tensor
+    out (written into ``out`` when given).  A resident slide with a pooled
+    p99 and EXACT precision runs as fit_transform_resident (no host round
+    trip between the fit and the recolour; same bytes)."""
     from .normalize import load_profile
 
     t = _dev.torch()
@@ -740,6 +830,16 @@ def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
         tsrc = ArraySource(target) if not _dev.is_tensor(target) else DeviceSource(target)
         tp = fit(tsrc, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats,
                  p99_mode=p99_mode)
+    if not host:
+        dst = out if out is not None else t.empty((src.height, src.width, 3), dtype=t.uint8,
+                                                  device=src.tensor.device)
+        if tuple(dst.shape) != (src.height, src.width, 3) or dst.dtype != t.uint8 or \
+                dst.device != src.tensor.device or not dst.is_contiguous():
+            raise ValueError("out must be a contiguous uint8 CUDA tensor shaped like the source")
+        if _fused_ok(src, tp, dst, precision, p99_mode, per_patch_stats):
+            fit_transform_resident(src, tp, dst, plan=plan, cfg=cfg, code_lam=code_lam,
+                                   stats=stats)
+            return dst
     sp = fit(src, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats, stats=stats,
              p99_mode=p99_mode)
     if host:
@@ -747,7 +847,7 @@ def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
         transform(src, sp, tp, sink, strip_height=strip_height, code_lam=code_lam, stats=stats,
                   precision=precision)
         return sink.pixels
-    sink = DeviceWriter(src.width, src.height, device=source.device)
+    sink = DeviceWriter(src.width, src.height, out=dst)
     transform(src, sp, tp, sink, strip_height=strip_height, code_lam=code_lam, stats=stats,
               precision=precision)
     return sink.pixels

@@ -1,4 +1,4 @@
-"""GPU timeline of the bench step (fit + transform) under torch.profiler:
+"""GPU timeline of the bench step (fit + transform, or the fused normalize) under torch.profiler:
 per step, the kernels in order with their start offsets and durations, and the
 idle gaps between them (host round trips).  python tools/step_timeline.py [side]"""
 import os
@@ -12,6 +12,7 @@ import paper_1901_03088_b200 as pb  # noqa: E402
 from paper_1901_03088_b200 import synthetic  # noqa: E402
 
 side = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000
+fused = os.environ.get("SPCN_FUSED", "1") != "0"   # step = pb.normalize (device-built params)
 slide = synthetic.render_slide(side, side, 1, tissue_fraction=0.6)
 tgt = pb.fit(pb.DeviceSource(synthetic.render_slide(2048, 2048, 2)))
 src = pb.DeviceSource(slide)
@@ -19,6 +20,9 @@ out = torch.empty_like(slide)
 
 
 def step():
+    if fused:
+        pb.normalize(slide, tgt, out=out)
+        return
     fp = pb.fit(src)
     pb.transform(src, fp, tgt, pb.DeviceWriter(side, side, out=out))
 
