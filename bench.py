@@ -573,9 +573,10 @@ def run_ours(args, rank, world, local):
     args.fused = os.environ.get("SPCN_FUSED", "1") != "0"
 
     def step(record=False):
-        if group is None and args.fused and args.p99_mode == "sample" and \
-                args.precision == "exact":
-            return pb.normalize(slide, target, out=out)
+        if args.fused and args.p99_mode == "sample" and args.precision == "exact":
+            if group is None:
+                return pb.normalize(slide, target, out=out)
+            return group.fit_transform(src, target, out)
         if group is None:
             fp = pb.fit(src, p99_mode=args.p99_mode)
         else:
@@ -701,11 +702,11 @@ def run_ours(args, rank, world, local):
                 "same step with fit(p99_mode='global'): exact p99 of every non-white pixel "
                 "(one k_stats_table pass; the per-colour table all-reduced over "
                 + ("NCCL" if world > 1 else "one rank") + ")"))
-        if world == 1 and args.p99_mode == "sample" and args.precision == "exact" and \
-                args.fused:
+        if args.p99_mode == "sample" and args.precision == "exact" and args.fused:
             line["host_params_step"] = dict(alt_steps("fused", False), note=(
-                "same step as pb.fit + pb.transform: the recolouring's parameters built "
-                "on the host between the fit's read-back and the transform launch"))
+                "same step as fit + transform (pb.*, or RowBandGroup.* at N > 1): the "
+                "recolouring's parameters built on the host between the fit's read-back "
+                "and the transform launch"))
         if args.precision == "exact":
             # the north star's stated tolerance (+-1 LSB on >= 99.9 % of pixels)
             line["fast_precision"] = dict(alt_steps("precision", "fast"), note=(

@@ -450,6 +450,20 @@ int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
                            const spcn_xform_fitted* p, void* workspace, size_t workspace_bytes,
                            int32_t* status_pinned, void* stream);
 
+/* The same recolouring in two calls, for a row-band group: prepare builds
+ * the parameters into a slot (*slot_out) and runs part `part` of `nparts` of
+ * the exhaustive calibration into the workspace's calibration word (with
+ * status_pinned it returns once the status is in host memory); the caller
+ * max-reduces that word across the ranks (one int32 all-reduce,
+ * stream-ordered) and then calls run, which recolours with the reduced bound
+ * and releases the slot.  Every prepare must be followed by a run on the
+ * same stream (npix 0 only releases the slot).                            */
+int spcn_xform_fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts,
+                              void* workspace, size_t workspace_bytes, int32_t* status_pinned,
+                              int32_t* slot_out, void* stream);
+int spcn_xform_fitted_run(const uint8_t* src, uint8_t* dst, int64_t npix, int32_t slot,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* Thread-local description of the last error ("" if none).                 */
 const char* spcn_last_error(void);
 

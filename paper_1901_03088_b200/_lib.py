@@ -42,6 +42,7 @@ EXPORTS = (
     "spcn_readback", "spcn_last_error", "spcn_version", "spcn_launch_count", "spcn_xform_shape",
     "spcn_xform_timing_enable", "spcn_xform_timing", "spcn_stream_sync",
     "spcn_fit_sample_step", "spcn_fit_basis_step", "spcn_xform_rgb8_fitted",
+    "spcn_xform_fitted_prepare", "spcn_xform_fitted_run",
 )
 
 
@@ -88,6 +89,9 @@ _SIGS = {
     "spcn_xform_rgb8": (ctypes.c_int, [P, P, I64, ctypes.POINTER(XformParams), P, SZ, P]),
     "spcn_xform_rgb8_fitted": (ctypes.c_int, [P, P, I64, ctypes.POINTER(XformFitted), P, SZ, P,
                                               P]),
+    "spcn_xform_fitted_prepare": (ctypes.c_int, [ctypes.POINTER(XformFitted), I32, I32, P, SZ, P,
+                                                 P, P]),
+    "spcn_xform_fitted_run": (ctypes.c_int, [P, P, I64, I32, P, SZ, P]),
     "spcn_xform_repair_count": (ctypes.c_int, [P, P, ctypes.POINTER(I64)]),
     "spcn_xform_calibrate": (ctypes.c_int, [ctypes.POINTER(XformParams), P, SZ,
                                             ctypes.POINTER(DBL), P]),

@@ -360,18 +360,10 @@ struct FittedSlots {
 };
 std::mutex g_fitted_mu;
 FittedSlots g_fitted[64];
-}  // namespace
 
-extern "C" {
-
-int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
-                           const spcn_xform_fitted* p, void* workspace, size_t workspace_bytes,
-                           int32_t* status_pinned, void* stream) {
-  g_err.clear();
+int check_fitted(const spcn_xform_fitted* p) {
   if (!p) return fail(SPCN_EINVAL, "params is NULL");
-  if (npix <= 0) return fail(SPCN_EINVAL, "npix must be > 0");
-  if (!src || !dst || !p->src_od_table || !p->src_fit)
-    return fail(SPCN_EINVAL, "NULL buffer");
+  if (!p->src_od_table || !p->src_fit) return fail(SPCN_EINVAL, "NULL table / fit arena");
   int rc = check_basis(p->tgt_basis, "target");
   if (rc) return rc;
   for (int c = 0; c < 3; ++c)
@@ -381,19 +373,25 @@ int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
       return fail(SPCN_EINVAL, "target p99 must be positive and finite");
   if (!(p->code_lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
   if (p->max_sweeps < 0) return fail(SPCN_EINVAL, "max_sweeps must be >= 0");
-  const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
-  if (((sa - da) & 15u) != 0)
-    return fail(SPCN_EINVAL, "src and dst must share their 16-byte alignment phase");
-  if (!workspace || workspace_bytes < spcn_xform_workspace_bytes(npix))
+  return SPCN_OK;
+}
+
+// slot + build + calibration part; *built_out = the event after the status read-back
+int fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts, void* workspace,
+                   size_t workspace_bytes, int32_t* status_pinned, cudaStream_t st,
+                   int32_t* slot_out, cudaEvent_t* built_out) {
+  int rc = check_fitted(p);
+  if (rc) return rc;
+  if (nparts < 1 || part < 0 || part >= nparts) return fail(SPCN_EINVAL, "bad part");
+  if (!workspace || workspace_bytes < kWsHeader + 8)
     return fail(SPCN_EINVAL, "workspace too small (spcn_xform_workspace_bytes)");
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "get_device");
   if (dev < 0 || dev >= 64) return fail(SPCN_EINVAL, "device index out of range");
-  const cudaStream_t st = static_cast<cudaStream_t>(stream);
   int slot;
   DevParams* staging;
-  cudaEvent_t done, built;
+  cudaEvent_t built;
   {
     std::lock_guard<std::mutex> lk(g_fitted_mu);
     FittedSlots& fs = g_fitted[dev];
@@ -408,10 +406,9 @@ int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
     slot = fs.next;
     fs.next = (fs.next + 1) % kDpSlots;
     staging = fs.staging + slot;
-    done = fs.done[slot];
     built = fs.built[slot];
     // the slot's previous user (any stream) must be finished with it
-    if (fs.used[slot] && (e = cudaStreamWaitEvent(st, done, 0)) != cudaSuccess)
+    if (fs.used[slot] && (e = cudaStreamWaitEvent(st, fs.done[slot], 0)) != cudaSuccess)
       return cuda_fail(e, "slot wait");
     fs.used[slot] = true;
   }
@@ -421,28 +418,104 @@ int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
   std::memcpy(in.tgt_i0, p->tgt_i0, sizeof(in.tgt_i0));
   in.code_lam = p->code_lam;
   in.max_sweeps = p->max_sweeps;
-  char* ws = static_cast<char*>(workspace);
+  const uint32_t n = 1u << 23;   // colour pairs
+  const uint32_t q0 = static_cast<uint32_t>((uint64_t)n * part / nparts),
+                 q1 = static_cast<uint32_t>((uint64_t)n * (part + 1) / nparts);
   if ((e = launch_xform_build(slot, in, p->src_od_table, static_cast<const double*>(p->src_fit),
-                              staging, ws, status_pinned, built, st)) != cudaSuccess)
+                              staging, workspace, status_pinned, built, q0, q1, st)) != cudaSuccess)
     return cuda_fail(e, "xform_build");
-  int64_t head = static_cast<int64_t>(((16 - (sa & 15u)) * 11u) & 15u);   // 3*head == -sa (mod 16)
-  if (head > npix) head = npix;
-  const int64_t body = ((npix - head) / 16) * 16;
-  auto* count = reinterpret_cast<unsigned long long*>(ws);
-  auto* items = reinterpret_cast<unsigned long long*>(ws + kWsHeader);
-  const unsigned long long cap = (workspace_bytes - kWsHeader) / 8;
-  cudaEvent_t t0 = nullptr, t1 = nullptr;
-  if (g_timing.load(std::memory_order_relaxed)) timing_begin(st, t0, t1);
-  e = launch_xform_main_c(slot, src + 3 * head, dst + 3 * head, body, count, items, cap,
-                          reinterpret_cast<const unsigned int*>(ws + 8), st);
-  if (t0) timing_end(st, t0, t1);
-  if (e != cudaSuccess) return cuda_fail(e, "xform_main_c");
-  if ((e = launch_xform_repair_c(slot, src, dst, npix, head, body, count, items, cap, st)) !=
-      cudaSuccess)
-    return cuda_fail(e, "xform_repair_c");
+  *slot_out = slot;
+  *built_out = built;
+  return SPCN_OK;
+}
+
+int fitted_run(const uint8_t* src, uint8_t* dst, int64_t npix, int32_t slot, void* workspace,
+               size_t workspace_bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "get_device");
+  if (dev < 0 || dev >= 64) return fail(SPCN_EINVAL, "device index out of range");
+  if (slot < 0 || slot >= kDpSlots) return fail(SPCN_EINVAL, "bad slot");
+  cudaEvent_t done;
+  {
+    std::lock_guard<std::mutex> lk(g_fitted_mu);
+    if (!g_fitted[dev].staging) return fail(SPCN_EINVAL, "no prepared recolouring");
+    done = g_fitted[dev].done[slot];
+  }
+  if (npix > 0) {
+    if (!src || !dst) return fail(SPCN_EINVAL, "src/dst is NULL");
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
+    if (((sa - da) & 15u) != 0)
+      return fail(SPCN_EINVAL, "src and dst must share their 16-byte alignment phase");
+    if (!workspace || workspace_bytes < spcn_xform_workspace_bytes(npix))
+      return fail(SPCN_EINVAL, "workspace too small (spcn_xform_workspace_bytes)");
+    char* ws = static_cast<char*>(workspace);
+    int64_t head = static_cast<int64_t>(((16 - (sa & 15u)) * 11u) & 15u);   // 3*head == -sa (mod 16)
+    if (head > npix) head = npix;
+    const int64_t body = ((npix - head) / 16) * 16;
+    auto* count = reinterpret_cast<unsigned long long*>(ws);
+    auto* items = reinterpret_cast<unsigned long long*>(ws + kWsHeader);
+    const unsigned long long cap = (workspace_bytes - kWsHeader) / 8;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (g_timing.load(std::memory_order_relaxed)) timing_begin(st, t0, t1);
+    e = launch_xform_main_c(slot, src + 3 * head, dst + 3 * head, body, count, items, cap,
+                            reinterpret_cast<const unsigned int*>(ws + 8), st);
+    if (t0) timing_end(st, t0, t1);
+    if (e != cudaSuccess) return cuda_fail(e, "xform_main_c");
+    if ((e = launch_xform_repair_c(slot, src, dst, npix, head, body, count, items, cap, st)) !=
+        cudaSuccess)
+      return cuda_fail(e, "xform_repair_c");
+  }
   if ((e = cudaEventRecord(done, st)) != cudaSuccess) return cuda_fail(e, "slot record");
+  return SPCN_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int spcn_xform_fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts,
+                              void* workspace, size_t workspace_bytes, int32_t* status_pinned,
+                              int32_t* slot_out, void* stream) {
+  g_err.clear();
+  if (!slot_out) return fail(SPCN_EINVAL, "slot_out is NULL");
+  cudaEvent_t built = nullptr;
+  int rc = fitted_prepare(p, part, nparts, workspace, workspace_bytes, status_pinned,
+                          static_cast<cudaStream_t>(stream), slot_out, &built);
+  if (rc) return rc;
+  cudaError_t e;
+  if (status_pinned && (e = cudaEventSynchronize(built)) != cudaSuccess)
+    return cuda_fail(e, "build wait");
+  return SPCN_OK;
+}
+
+int spcn_xform_fitted_run(const uint8_t* src, uint8_t* dst, int64_t npix, int32_t slot,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (npix < 0) return fail(SPCN_EINVAL, "npix must be >= 0");
+  return fitted_run(src, dst, npix, slot, workspace, workspace_bytes,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
+                           const spcn_xform_fitted* p, void* workspace, size_t workspace_bytes,
+                           int32_t* status_pinned, void* stream) {
+  g_err.clear();
+  if (npix <= 0) return fail(SPCN_EINVAL, "npix must be > 0");
+  if (!src || !dst) return fail(SPCN_EINVAL, "src/dst is NULL");
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
+  if (((sa - da) & 15u) != 0)
+    return fail(SPCN_EINVAL, "src and dst must share their 16-byte alignment phase");
+  if (!workspace || workspace_bytes < spcn_xform_workspace_bytes(npix))
+    return fail(SPCN_EINVAL, "workspace too small (spcn_xform_workspace_bytes)");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t slot = 0;
+  cudaEvent_t built = nullptr;
+  int rc = fitted_prepare(p, 0, 1, workspace, workspace_bytes, status_pinned, st, &slot, &built);
+  if (rc) return rc;
+  if ((rc = fitted_run(src, dst, npix, slot, workspace, workspace_bytes, st))) return rc;
   // the build (and everything enqueued before it, e.g. the fit's read-back)
   // has reached host memory; the recolour itself is still in flight
+  cudaError_t e;
   if (status_pinned && (e = cudaEventSynchronize(built)) != cudaSuccess)
     return cuda_fail(e, "build wait");
   return SPCN_OK;

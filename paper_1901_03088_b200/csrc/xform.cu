@@ -327,9 +327,10 @@ __global__ void __launch_bounds__(256) k_build_xform(const __grid_constant__ Xfo
 }
 
 template <int SLOT>
-__global__ void __launch_bounds__(256) k_calibrate_c(unsigned int* __restrict__ max_bits) {
+__global__ void __launch_bounds__(256) k_calibrate_c(unsigned int* __restrict__ max_bits,
+                                                     uint32_t q0, uint32_t q1) {
   if (c_dp[SLOT].status != 0) return;
-  calibrate_body(c_dp[SLOT].fp, c_dp[SLOT].sp, max_bits, 0u, 1u << 23);
+  calibrate_body(c_dp[SLOT].fp, c_dp[SLOT].sp, max_bits, q0, q1);
 }
 
 template <int SLOT, int CW, int REP, int NSW, int BLK, int NSUB>
@@ -466,7 +467,8 @@ cudaError_t launch_xform_main(int mode, const uint8_t* src, uint8_t* dst, int64_
 
 cudaError_t launch_xform_build(int slot, const XformBuildIn& in, const double* lut,
                                const double* fit, DevParams* staging, void* ws,
-                               int32_t* status_host, cudaEvent_t built, cudaStream_t st) {
+                               int32_t* status_host, cudaEvent_t built, uint32_t q0, uint32_t q1,
+                               cudaStream_t st) {
   cudaError_t e = xform_setup_device();
   if (e != cudaSuccess) return e;
   unsigned int* hdr = static_cast<unsigned int*>(ws);
@@ -480,9 +482,13 @@ cudaError_t launch_xform_build(int slot, const XformBuildIn& in, const double* l
                            st)) != cudaSuccess)
     return e;
   if (built && (e = cudaEventRecord(built, st)) != cudaSuccess) return e;
-  const int grid = g_sm_count * 8;   // launch_calibrate's full-range grid
-  if (slot == 0) k_calibrate_c<0><<<grid, 256, 0, st>>>(hdr + 2);
-  else k_calibrate_c<1><<<grid, 256, 0, st>>>(hdr + 2);
+  if (q1 <= q0) return cudaSuccess;
+  // colour pairs [q0, q1) with launch_calibrate's proportional grid
+  const int64_t full = (int64_t)g_sm_count * 8;
+  int64_t grid = (full * (int64_t)(q1 - q0) + (1 << 23) - 1) >> 23;
+  if (grid < 1) grid = 1;
+  if (slot == 0) k_calibrate_c<0><<<(int)grid, 256, 0, st>>>(hdr + 2, q0, q1);
+  else k_calibrate_c<1><<<(int)grid, 256, 0, st>>>(hdr + 2, q0, q1);
   return launched();
 }
 

@@ -45,10 +45,11 @@ struct XformBuildIn {   // the host-known half: target profile and options
 };
 // build (1 CTA) -> copy into __constant__ slot `slot` -> optional status
 // read-back into pinned host memory (then `built` is recorded) -> exhaustive
-// calibration into ws+8
+// calibration of colour pairs [q0, q1) into ws+8
 cudaError_t launch_xform_build(int slot, const XformBuildIn& in, const double* lut,
                                const double* fit, DevParams* staging, void* ws,
-                               int32_t* status_host, cudaEvent_t built, cudaStream_t st);
+                               int32_t* status_host, cudaEvent_t built, uint32_t q0, uint32_t q1,
+                               cudaStream_t st);
 cudaError_t launch_xform_main_c(int slot, const uint8_t* src, uint8_t* dst, int64_t npix,
                                 unsigned long long* count, unsigned long long* items,
                                 unsigned long long cap, const unsigned int* alpha_bits,

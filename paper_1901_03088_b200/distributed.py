@@ -29,7 +29,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _lib
+from . import _dev, _lib
 
 CHUNK = 4096
 
@@ -173,17 +173,94 @@ class RowBandGroup:
 
     def fit(self, band_source, plan=None, cfg=None, *, code_lam: float = 0.0,
             per_patch_stats: bool = False, source_label: str = "", p99_mode: str = "sample"):
+        """pipeline.fit of the whole slide from the row bands (a collective:
+        every rank returns the same FitParams)."""
+        from . import fitcore
+        from .pipeline import SamplePlan, _stage, slide_chunks
+        from .stain_sep import SnmfConfig
+
+        plan = plan or SamplePlan()
+        cfg = cfg or SnmfConfig()
+        fb, sample, m, i0, used_counts = self._gather_sample(band_source, plan, cfg)
+        return fitcore.fit_tail(fb, sample.reshape(-1), m, i0, plan, cfg, code_lam=code_lam,
+                                per_patch_stats=per_patch_stats, p99_mode=p99_mode,
+                                used_counts=used_counts, source_label=source_label,
+                                chunks=slide_chunks(band_source) if p99_mode == "global" else None,
+                                comm=TorchComm(self.group), stage=_stage)
+
+    def fit_transform(self, band_source, target, out, plan=None, cfg=None, *,
+                      code_lam: float = 0.0, source_label: str = ""):
+        """fit() of the whole slide, then this rank's band recoloured into the
+        CUDA tensor `out` (EXACT, pooled p99) with the recolouring built on
+        the device from the fit (spcn_xform_fitted_prepare / _run): one host
+        wait for the build, the certification calibration split across the
+        ranks (1/N of the colours each, one int32 max all-reduce on the
+        stream), no host round trip between the fit and the recolour.  Same
+        bytes as fit() + transform(); a recolouring the device declines is
+        redone by transform() with host parameters (identically on every
+        rank: the fit is the same everywhere).  A collective; returns the fit."""
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import fitcore
+        from .image_io import DeviceWriter
+        from .pipeline import SamplePlan, _fitted_params
+        from .stain_sep import SnmfConfig
+
+        plan = plan or SamplePlan()
+        cfg = cfg or SnmfConfig()
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        src = band_source.tensor
+        if (src.data_ptr() - out.data_ptr()) % 16 != 0:
+            raise ValueError("fit_transform: band and out must share their 16-byte alignment phase")
+        if tuple(out.shape) != tuple(src.shape) or not out.is_contiguous():
+            raise ValueError("fit_transform: out must be a contiguous tensor shaped like the band")
+        L = _lib.lib()
+        npix = src.numel() // 3
+        p = _fitted_params(target, float(code_lam))
+        ws_bytes = int(L.spcn_xform_workspace_bytes(max(npix, 1)))
+        st = _lib.stream_handle()
+        ws = _dev.workspace(ws_bytes, stream=st)
+        fb, sample, m, i0, _ = self._gather_sample(band_source, plan, cfg)
+        p.src_od_table = fb.lut_ptr
+        p.src_fit = fb.arena_b_ptr
+        fitcore.basis_enqueue(fb, _lib.ptr(sample), m, i0, cfg, code_lam=code_lam, pooled=True)
+        slot = ctypes.c_int32(-1)
+        fb.pin_status_np[0] = -1
+        _lib.check(L.spcn_xform_fitted_prepare(ctypes.byref(p), rank, world, _lib.ptr(ws),
+                                               ws_bytes, fb.pin_status_ptr, ctypes.byref(slot),
+                                               st), "xform_fitted_prepare")
+        try:
+            prov = fitcore.provenance(plan, cfg, code_lam, False, "sample", source_label)
+            fp = fitcore.parse_pooled(fb, m, i0, cfg, prov, stacklevel=3)
+        except Exception:
+            L.spcn_xform_fitted_run(None, None, 0, slot.value, _lib.ptr(ws), ws_bytes, st)
+            raise
+        ok = int(fb.pin_status_np[0]) == 0
+        all_reduce_max(ws[8:12].view(_dev.torch().int32), self.group)
+        _lib.check(L.spcn_xform_fitted_run(_lib.ptr(src), _lib.ptr(out), npix if ok else 0,
+                                           slot.value, _lib.ptr(ws), ws_bytes, st),
+                   "xform_fitted_run")
+        if not ok:
+            self.transform(band_source, fp, target, DeviceWriter(src.shape[1], src.shape[0],
+                                                                 out=out),
+                           code_lam=code_lam, precision="exact")
+        return fp
+
+    def _gather_sample(self, band_source, plan, cfg):
+        """The collective sampling of fit(): per-rank patch counts all-gathered,
+        the reference's visit loop replayed on the host, each rank compacting
+        the takes inside its band, sample + bright histograms summed in one
+        all-reduce, i0 on the host.  Returns (FitBuffers, sample (m, 3) CUDA
+        uint8, m, i0, used patch counts)."""
         import torch
         import torch.distributed as dist
 
         from . import fitcore, optics
         from .errors import BlankSlideError
-        from .pipeline import (PATCH_DT, TAKE_DT, SamplePlan, _lib_sample, _stage, _visit,
-                               slide_chunks)
-        from .stain_sep import SnmfConfig
+        from .pipeline import PATCH_DT, TAKE_DT, _lib_sample, _stage, _visit
 
-        plan = plan or SamplePlan()
-        cfg = cfg or SnmfConfig()
         L = _lib_sample()
         W, H = self.width, self.height
         rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
@@ -247,9 +324,8 @@ class RowBandGroup:
         i0 = _stage("background estimation", optics.i0_from_counts,
                     hist.cpu().numpy()[0].astype(np.int64))
         fb = fitcore.buffers(dev, plan.target_pixels, cfg.max_outer_iters)
-        fb.offsets().copy_(torch.tensor([0, m], dtype=torch.int64), non_blocking=False)
-        return fitcore.fit_tail(fb, sample.reshape(-1), m, i0, plan, cfg, code_lam=code_lam,
-                                per_patch_stats=per_patch_stats, p99_mode=p99_mode,
-                                used_counts=used_counts, source_label=source_label,
-                                chunks=slide_chunks(band_source) if p99_mode == "global" else None,
-                                comm=TorchComm(self.group), stage=_stage)
+        # [0, m] through the pinned staging buffer: stream-ordered, no host wait
+        # (the previous fit's copy from it completed before that fit's read-back)
+        fb.pin_a_np[128:144].view(np.int64)[:] = (0, m)
+        fb.offsets().copy_(fb.pin_a[128:144].view(torch.int64), non_blocking=True)
+        return fb, sample, m, i0, used_counts

@@ -155,3 +155,50 @@ def test_calibration_parts_max_equals_full():
         words.append(box["w"])
     worst = np.array([max(words)], dtype=np.uint32).view(np.float32)[0]
     assert float(worst) * (1.0 + 2.0 ** -20) == full, (worst, full)   # spcn_xform_calibrate's alpha
+
+
+def _fused_worker(rank, world, port, q, backend="gloo"):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_03088_b200 as pb
+    from paper_1901_03088_b200 import distributed as dd, synthetic
+
+    _init(rank, world, port, backend)
+    try:
+        W, H = 4096, 4096
+        full = synthetic.render_slide(W, H, 7, tissue_fraction=0.5)
+        tgt = pb.fit(pb.DeviceSource(synthetic.render_slide(1024, 1024, 8, tissue_fraction=0.6)))
+        r0, rows = rank * (H // world), H // world
+        band = full[r0:r0 + rows].contiguous()
+        g = dd.RowBandGroup(W, H, r0, rows)
+        out = torch.empty_like(band)
+        fp = None
+        for _ in range(3):                    # rotates the parameter slots
+            fp = g.fit_transform(pb.DeviceSource(band), tgt, out)
+        fp_ref = g.fit(pb.DeviceSource(band))
+        ref = pb.normalize(full, tgt)          # single process: fit + transform
+        q.put((rank, bool(torch.equal(out, ref[r0:r0 + rows])),
+               bool(np.array_equal(fp.basis, fp_ref.basis)) and fp.stats.p99.tolist() ==
+               fp_ref.stats.p99.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_rowband_fit_transform_device_built(backend):
+    """RowBandGroup.fit_transform (device-built parameters, calibration split
+    across the ranks) gives each rank the bytes of the single-process
+    normalize and the same fit as RowBandGroup.fit."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_fused_worker, args=(r, 2, port, q, backend)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(ok and same for _, ok, same in out), out
