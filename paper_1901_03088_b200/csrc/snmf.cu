@@ -20,6 +20,8 @@
 // summation order (basis within cosine 1e-3, measured
 // ~1e-15).
 #include <cooperative_groups.h>
+#include <cstdlib>
+#include <cstring>
 
 #include "launch_count.h"
 #include "ctable.cuh"
@@ -69,8 +71,8 @@ struct SnmfShared {
   int flag;
 };
 
-// NT threads per CTA, MINB CTAs per SM (512 x 1 measured best for both the
-// cluster fit of one slide and the one-CTA-per-problem batch).
+// NT threads per CTA, MINB CTAs per SM (512 x 1 for the cluster fit of one
+// slide; 128 x 4 for the one-CTA-per-problem batch, see launch_snmf).
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_snmf(
     const uint8_t* __restrict__ samples, const double* __restrict__ od,
@@ -514,12 +516,37 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
     if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
   }
+  // one-CTA-per-problem batches: 128 threads x 4 CTAs per SM (each problem's
+  // serial W-step and barriers overlap other CTAs' H-step passes: 9.3 ms vs
+  // 11.5 ms for 512 x 1 on the 4096-patch batch).  SPCN_SNMF_BATCH = "512x1" |
+  // "256x2" | "128x4" | "64x8" | "32x16" selects another shape (experiments).
+  static int bshape = -1, occ_b = 1;
+  if (bshape < 0) {
+    bshape = 2;
+    if (const char* env = getenv("SPCN_SNMF_BATCH")) {
+      if (!strcmp(env, "512x1")) bshape = 0;
+      if (!strcmp(env, "256x2")) bshape = 1;
+      if (!strcmp(env, "128x4")) bshape = 2;
+      if (!strcmp(env, "64x8")) bshape = 3;
+      if (!strcmp(env, "32x16")) bshape = 4;
+    }
+    const void* fns[5] = {nullptr, (const void*)k_snmf<256, 2>, (const void*)k_snmf<128, 4>,
+                          (const void*)k_snmf<64, 8>, (const void*)k_snmf<32, 16>};
+    const void* fn = fns[bshape];
+    const int nt = 512 >> bshape;
+    if (bshape) {
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, fn, nt, 0);
+      if (e != cudaSuccess) return e;
+      if (occ_b < 1) occ_b = 1;
+    }
+  }
+  const bool alt = single && bshape != 0 && nprob >= sms;   // (a few problems: 512 threads each)
   int nclusters = nprob;
-  const int max_clusters = single ? sms * occ1 : (sms * 2) / cluster;   // occ1: resident CTAs/SM
+  const int max_clusters = alt ? sms * occ_b : single ? sms * occ1 : (sms * 2) / cluster;
   if (nclusters > max_clusters) nclusters = max_clusters;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nclusters * cluster);
-  cfg.blockDim = dim3(512);
+  cfg.blockDim = dim3(alt ? (512 >> bshape) : 512);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -532,8 +559,20 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
   const uint32_t* ck = ukey;
   const uint32_t* cc = ucnt;
   const int32_t* cu = ucount;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_snmf<512, 1>, samples, od, offsets, nprob, luts, a,
-                                     ticket, total, basis_out, hist_out, info_out, ck, cc, cu);
+  cudaError_t e =
+      !alt ? cudaLaunchKernelEx(&cfg, k_snmf<512, 1>, samples, od, offsets, nprob, luts, a, ticket,
+                                total, basis_out, hist_out, info_out, ck, cc, cu)
+      : bshape == 1
+          ? cudaLaunchKernelEx(&cfg, k_snmf<256, 2>, samples, od, offsets, nprob, luts, a, ticket,
+                               total, basis_out, hist_out, info_out, ck, cc, cu)
+      : bshape == 2
+          ? cudaLaunchKernelEx(&cfg, k_snmf<128, 4>, samples, od, offsets, nprob, luts, a, ticket,
+                               total, basis_out, hist_out, info_out, ck, cc, cu)
+      : bshape == 3
+          ? cudaLaunchKernelEx(&cfg, k_snmf<64, 8>, samples, od, offsets, nprob, luts, a, ticket,
+                               total, basis_out, hist_out, info_out, ck, cc, cu)
+          : cudaLaunchKernelEx(&cfg, k_snmf<32, 16>, samples, od, offsets, nprob, luts, a, ticket,
+                               total, basis_out, hist_out, info_out, ck, cc, cu);
   if (own_ticket) {
     const cudaError_t e2 = cudaFreeAsync(ticket, st);
     if (e == cudaSuccess) e = e2;
