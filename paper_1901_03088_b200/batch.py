@@ -134,28 +134,21 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
     thr = int(plan.white_threshold)
     _lib.check(L.spcn_sample_count(_lib.ptr(imgs), _lib.ptr(d_desc), n * ncand, chunks, thr,
                                    _lib.ptr(counts), _lib.stream_handle()), "sample_count")
+    if ncand == 1:
+        return _fit_batch_single_patch(imgs, n, rects[0], d_desc, counts, chunks, thr, plan, cfg,
+                                       code_lam)
     tot = _dev.readback(counts.sum(dim=1)).astype(np.int64).reshape(n, ncand, 4)
-    # the reference's visit loop per item (vectorised for single-patch grids)
+    # the reference's visit loop per item
     take_nw = np.zeros((n, ncand), np.int64)
     take_b = np.zeros((n, ncand, 3), np.int64)
     collected = np.zeros(n, np.int64)
-    patch_counts = [None] * n
-    if ncand == 1:
-        npx = rects[0][2] * rects[0][3]
-        min_frac = 1.0 - plan.background_fraction_cutoff
-        take_b[:, 0, :] = np.minimum(tot[:, 0, 1:], plan.sample_cap)
-        used = tot[:, 0, 0] >= min_frac * npx
-        take_nw[:, 0] = np.where(used, np.minimum(tot[:, 0, 0], plan.target_pixels), 0)
-        collected = take_nw[:, 0].copy()
-    else:
-        for i in range(n):
-            takes, uc, coll, _, _ = _visit(plan, order[:ncand], rects,
-                                           lambda k, i=i: tuple(int(v) for v in tot[i, k]))
-            for (k, tnw, _base, tb) in takes:
-                take_nw[i, k] = tnw
-                take_b[i, k] = tb
-            collected[i] = coll
-            patch_counts[i] = uc
+    for i in range(n):
+        takes, _uc, coll, _, _ = _visit(plan, order[:ncand], rects,
+                                        lambda k, i=i: tuple(int(v) for v in tot[i, k]))
+        for (k, tnw, _base, tb) in takes:
+            take_nw[i, k] = tnw
+            take_b[i, k] = tb
+        collected[i] = coll
     offsets = np.concatenate([[0], np.cumsum(collected)]).astype(np.int64)
     total = int(offsets[-1])
     base_in_item = np.cumsum(take_nw, axis=1) - take_nw
@@ -165,28 +158,78 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
     tk["take_bright"] = take_b
     tk["problem"] = np.arange(n, dtype=np.int32)[:, None]
     sample = t.empty((max(total, 1), 3), dtype=t.uint8, device=dev)
-    hist = t.zeros((n, 3, 256), dtype=t.int32, device=dev)
     d_tk = t.from_numpy(tk.ravel().view(np.uint8).copy()).to(dev)
+    i0, ie = _compact_i0(imgs, n, ncand, d_desc, counts, chunks, thr, d_tk, sample, None)
+    return _fit_batch_tail(n, sample, collected, offsets, i0, ie, cfg, plan, code_lam)
+
+
+def _compact_i0(imgs, n, ncand, d_desc, counts, chunks, thr, d_tk, sample, extra):
+    """Ordered compaction + bright histograms, i0 per item, and ONE read of
+    (i0, empty flags[, extra]) — extra: a device int64 vector appended."""
+    t = _dev.torch()
+    L = _lib_sample()
+    dev = imgs.device
+    hist = t.zeros((n, 3, 256), dtype=t.int32, device=dev)
     _lib.check(L.spcn_sample_compact(_lib.ptr(imgs), _lib.ptr(d_desc), n * ncand, chunks, thr,
                                      _lib.ptr(counts), _lib.ptr(d_tk), _lib.ptr(sample),
                                      _lib.ptr(hist), _lib.stream_handle()), "sample_compact")
-    status = np.zeros(n, np.int32)
-    status[collected == 0] = -_lib.SPCN_EBLANK
-    status[(collected > 0) & (collected < 10)] = -_lib.SPCN_EINSUFFICIENT
     # background i0 per item (exact order statistic of the 8-bit pools)
     i0 = t.empty((n, 3), dtype=t.float64, device=dev)
     empty = t.empty((n, 3), dtype=t.int32, device=dev)
     _lib.check(L.spcn_i0_from_hist(_lib.ptr(hist), n, _lib.ptr(i0), _lib.ptr(empty),
                                    _lib.stream_handle()), "i0_from_hist")
-    ie = _dev.readback(t.cat([i0.reshape(-1), empty.reshape(-1).to(t.float64)]))   # one read
+    parts = [i0.reshape(-1), empty.reshape(-1).to(t.float64)]
+    if extra is not None:
+        parts.append(extra.to(t.float64))             # counts < 2^53: exact in f64
+    return i0, _dev.readback(t.cat(parts))            # one read
+
+
+def _fit_batch_single_patch(imgs, n, rect, d_desc, counts, chunks, thr, plan, cfg, code_lam):
+    """fit_batch for a one-candidate grid (every item is one patch, e.g. 512²
+    tiles with patch_size 1000): the reference's visit rules
+    (src/pipeline.py:156-184) reduce to per-item elementwise ones, evaluated on
+    the device, so the counts are never read back — the compaction follows
+    the count pass directly; the take sizes come back with i0."""
+    t = _dev.torch()
+    dev = imgs.device
+    npx = rect[2] * rect[3]
+    min_frac = 1.0 - plan.background_fraction_cutoff
+    tot = counts.sum(dim=1, dtype=t.int64)                       # (n, 4)
+    take_b = t.clamp(tot[:, 1:], max=plan.sample_cap)
+    used = tot[:, 0].to(t.float64) >= min_frac * npx
+    take_nw = t.where(used, t.clamp(tot[:, 0], max=plan.target_pixels), t.zeros_like(tot[:, 0]))
+    base = t.cumsum(take_nw, 0) - take_nw
+    tk = t.empty((n, 8), dtype=t.int32, device=dev)               # TAKE_DT rows (32 B)
+    tk[:, 0:4] = t.stack([take_nw, base], 1).view(t.int32)
+    tk[:, 4:7] = take_b.to(t.int32)
+    tk[:, 7] = t.arange(n, dtype=t.int32, device=dev)
+    # the sample at its largest (every item taking target_pixels): no read of
+    # the totals before the compaction
+    sample = t.empty((max(1, n * min(plan.target_pixels, npx)), 3), dtype=t.uint8, device=dev)
+    i0, ie = _compact_i0(imgs, n, 1, d_desc, counts, chunks, thr, tk.view(-1).view(t.uint8),
+                         sample, take_nw)
+    collected = ie[6 * n:].astype(np.int64)
+    offsets = np.concatenate([[0], np.cumsum(collected)]).astype(np.int64)
+    return _fit_batch_tail(n, sample, collected, offsets, i0, ie[:6 * n], cfg, plan, code_lam,
+                           stacklevel=4)
+
+
+def _fit_batch_tail(n, sample, collected, offsets, i0, ie, cfg, plan, code_lam, stacklevel=3):
+    """From the sample and i0 on: OD tables, SNMF, densities, p99, statuses."""
+    t = _dev.torch()
+    dev = sample.device
+    total = int(offsets[-1])
+    status = np.zeros(n, np.int32)
+    status[collected == 0] = -_lib.SPCN_EBLANK
+    status[(collected > 0) & (collected < 10)] = -_lib.SPCN_EINSUFFICIENT
     i0_h = ie[:3 * n].reshape(n, 3)
     if ie[3 * n:].any():
         warnings.warn("some items had no pixels brighter than the white threshold in a "
                       "channel; their i0 fell back to 255", optics.BackgroundEstimateWarning,
-                      stacklevel=2)
+                      stacklevel=stacklevel)
     luts = _od_tables_exact(i0_h, dev)
     d_off = t.from_numpy(offsets).to(dev)
-    flat = sample.reshape(-1)
+    flat = sample.reshape(-1)[:3 * max(total, 1)]   # (the single-patch path over-allocates)
     r = snmf.snmf_batched(flat, d_off, luts, cfg, cluster=1)
     mmax = int(collected.max(initial=0))
     if r.table is not None and total > 0:
@@ -259,6 +302,8 @@ def transform_batch(images, fits: BatchFit, target: FitParams, out=None, *,
     ws_bytes = max(int(_lib.lib().spcn_xform_workspace_bytes(n * per)),
                    16 + 8 * (65536 + n * per // 8))
     ws = _dev.workspace(ws_bytes)
+    # (the host statuses skip the launches nothing needs; the read-back before
+    # the launch also keeps normalize_batch_host's chunk pipeline flowing)
     _lib.check(L.spcn_xform_batch(_lib.ptr(imgs), _lib.ptr(out), n, off.ctypes.data,
                                   _lib.ptr(d_off), _lib.ptr(fast), status_h.ctypes.data,
                                   _lib.ptr(status), _lib.ptr(flut), _lib.ptr(strict),
