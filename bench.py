@@ -572,8 +572,11 @@ def run_ours(args, rank, world, local):
     # with the recolouring built on the device (no host round trip between)
     args.fused = os.environ.get("SPCN_FUSED", "1") != "0"
 
+    def fused_step():
+        return args.fused and args.p99_mode == "sample" and args.precision == "exact"
+
     def step(record=False):
-        if args.fused and args.p99_mode == "sample" and args.precision == "exact":
+        if fused_step():
             if group is None:
                 return pb.normalize(slide, target, out=out)
             return group.fit_transform(src, target, out)
@@ -659,7 +662,10 @@ def run_ours(args, rank, world, local):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "traffic_bytes_per_px": traffic_px,
                          "traffic_source": "profiles/xform_traffic.json (ncu --set full)",
-                         "kernel": "k_xform_warp (main recolour launch of spcn_xform_rgb8)",
+                         "kernel": ("k_xform_warp_c (main recolour launch of the device-built "
+                                    "recolouring, spcn_xform_rgb8_fitted / _run)"
+                                    if fused_step() else
+                                    "k_xform_warp (main recolour launch of spcn_xform_rgb8)"),
                          "kernel_ms": round(x_ms, 4), "kernel_launches_timed": int(n_k.value),
                          "share_of_step": round(x_ms / ms, 4),
                          "transform_call_ms": round(call_ms, 4) if call_ms else None,
