@@ -444,8 +444,12 @@ typedef struct spcn_xform_fitted {
   double tgt_i0[3];
   double code_lam;
   int32_t max_sweeps;
-  int32_t reserved;
+  int32_t flags;                /* SPCN_FITTED_* (0: calibrated bound)          */
 } spcn_xform_fitted;
+/* flags: the analytic per-pixel certification bound instead of the
+ * exhaustive calibration (images below ~2^24 px, where the 0.3 ms
+ * calibration does not pay) — the same bytes either way.                    */
+#define SPCN_FITTED_ANALYTIC 1
 int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
                            const spcn_xform_fitted* p, void* workspace, size_t workspace_bytes,
                            int32_t* status_pinned, void* stream);

@@ -71,7 +71,7 @@ class XformFitted(ctypes.Structure):
         ("tgt_i0", ctypes.c_double * 3),
         ("code_lam", ctypes.c_double),
         ("max_sweeps", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
 
 

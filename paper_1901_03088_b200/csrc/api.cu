@@ -356,6 +356,7 @@ struct FittedSlots {
   cudaEvent_t done[kDpSlots] = {};
   cudaEvent_t built[kDpSlots] = {};       // the status read-back has landed
   bool used[kDpSlots] = {};
+  bool analytic[kDpSlots] = {};           // the slot's recolouring uses the analytic bound
   int next = 0;
 };
 std::mutex g_fitted_mu;
@@ -373,6 +374,7 @@ int check_fitted(const spcn_xform_fitted* p) {
       return fail(SPCN_EINVAL, "target p99 must be positive and finite");
   if (!(p->code_lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
   if (p->max_sweeps < 0) return fail(SPCN_EINVAL, "max_sweeps must be >= 0");
+  if (p->flags & ~SPCN_FITTED_ANALYTIC) return fail(SPCN_EINVAL, "unknown flags");
   return SPCN_OK;
 }
 
@@ -411,6 +413,7 @@ int fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts, voi
     if (fs.used[slot] && (e = cudaStreamWaitEvent(st, fs.done[slot], 0)) != cudaSuccess)
       return cuda_fail(e, "slot wait");
     fs.used[slot] = true;
+    fs.analytic[slot] = (p->flags & SPCN_FITTED_ANALYTIC) != 0;
   }
   XformBuildIn in{};
   std::memcpy(in.tgt_basis, p->tgt_basis, sizeof(in.tgt_basis));
@@ -418,7 +421,7 @@ int fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts, voi
   std::memcpy(in.tgt_i0, p->tgt_i0, sizeof(in.tgt_i0));
   in.code_lam = p->code_lam;
   in.max_sweeps = p->max_sweeps;
-  const uint32_t n = 1u << 23;   // colour pairs
+  const uint32_t n = (p->flags & SPCN_FITTED_ANALYTIC) ? 0u : 1u << 23;   // colour pairs
   const uint32_t q0 = static_cast<uint32_t>((uint64_t)n * part / nparts),
                  q1 = static_cast<uint32_t>((uint64_t)n * (part + 1) / nparts);
   if ((e = launch_xform_build(slot, in, p->src_od_table, static_cast<const double*>(p->src_fit),
@@ -437,10 +440,12 @@ int fitted_run(const uint8_t* src, uint8_t* dst, int64_t npix, int32_t slot, voi
   if (dev < 0 || dev >= 64) return fail(SPCN_EINVAL, "device index out of range");
   if (slot < 0 || slot >= kDpSlots) return fail(SPCN_EINVAL, "bad slot");
   cudaEvent_t done;
+  bool analytic;
   {
     std::lock_guard<std::mutex> lk(g_fitted_mu);
     if (!g_fitted[dev].staging) return fail(SPCN_EINVAL, "no prepared recolouring");
     done = g_fitted[dev].done[slot];
+    analytic = g_fitted[dev].analytic[slot];
   }
   if (npix > 0) {
     if (!src || !dst) return fail(SPCN_EINVAL, "src/dst is NULL");
@@ -458,8 +463,8 @@ int fitted_run(const uint8_t* src, uint8_t* dst, int64_t npix, int32_t slot, voi
     const unsigned long long cap = (workspace_bytes - kWsHeader) / 8;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (g_timing.load(std::memory_order_relaxed)) timing_begin(st, t0, t1);
-    e = launch_xform_main_c(slot, src + 3 * head, dst + 3 * head, body, count, items, cap,
-                            reinterpret_cast<const unsigned int*>(ws + 8), st);
+    e = launch_xform_main_c(slot, analytic, src + 3 * head, dst + 3 * head, body, count, items,
+                            cap, reinterpret_cast<const unsigned int*>(ws + 8), st);
     if (t0) timing_end(st, t0, t1);
     if (e != cudaSuccess) return cuda_fail(e, "xform_main_c");
     if ((e = launch_xform_repair_c(slot, src, dst, npix, head, body, count, items, cap, st)) !=

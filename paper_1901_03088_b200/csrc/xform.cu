@@ -333,14 +333,16 @@ __global__ void __launch_bounds__(256) k_calibrate_c(unsigned int* __restrict__ 
   calibrate_body(c_dp[SLOT].fp, c_dp[SLOT].sp, max_bits, q0, q1);
 }
 
-template <int SLOT, int CW, int REP, int NSW, int BLK, int NSUB>
+// MODE 2: the calibrated bound (calibration word in the workspace); MODE 0:
+// the analytic per-pixel bound (images too small to amortise a calibration)
+template <int SLOT, int MODE, int CW, int REP, int NSW, int BLK, int NSUB>
 __global__ void __launch_bounds__(32 * CW, BLK)
     k_xform_warp_c(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t npix,
                    RepairList rl) {
   // a declined recolouring runs zero slices (an early exit here would make
   // the compiler keep the shared-memory window base out of uniform registers)
-  xform_warp_body<2, CW, REP, NSW, BLK, NSUB>(src, dst, c_dp[SLOT].status == 0 ? npix : 0,
-                                              c_dp[SLOT].fp, rl);
+  xform_warp_body<MODE, CW, REP, NSW, BLK, NSUB>(src, dst, c_dp[SLOT].status == 0 ? npix : 0,
+                                                 c_dp[SLOT].fp, rl);
 }
 
 // The repair list of the vector body [head, head + body), plus the (< 16 px)
@@ -383,7 +385,7 @@ struct Shape {
   int cw, rep, nsub, blk, nsw, threads, tile_px, blocks_per_sm;
   size_t smem;
   XformFn fn[4];
-  XformCFn cfn[kDpSlots];   // device-built parameter slots (production shape only)
+  XformCFn cfn[kDpSlots][2];   // device-built slots x {calibrated, analytic} (production only)
 };
 
 template <int CW, int REP, int NSW, int BLK, int NSUB, bool SLOTS = false>
@@ -392,11 +394,13 @@ Shape make_wshape() {
   Shape s{CW, REP, NSUB, BLK, NSW, C::kThreads, CW * C::kSlicePx, 0, C::kSmem,
           {k_xform_warp<0, CW, REP, NSW, BLK, NSUB>, k_xform_warp<1, CW, REP, NSW, BLK, NSUB>,
            k_xform_warp<2, CW, REP, NSW, BLK, NSUB>, k_xform_warp<3, CW, REP, NSW, BLK, NSUB>},
-          {nullptr, nullptr}};
+          {{nullptr, nullptr}, {nullptr, nullptr}}};
   static_assert(kDpSlots == 2, "slot table");
   if constexpr (SLOTS) {
-    s.cfn[0] = k_xform_warp_c<0, CW, REP, NSW, BLK, NSUB>;
-    s.cfn[1] = k_xform_warp_c<1, CW, REP, NSW, BLK, NSUB>;
+    s.cfn[0][0] = k_xform_warp_c<0, 2, CW, REP, NSW, BLK, NSUB>;
+    s.cfn[0][1] = k_xform_warp_c<0, 0, CW, REP, NSW, BLK, NSUB>;
+    s.cfn[1][0] = k_xform_warp_c<1, 2, CW, REP, NSW, BLK, NSUB>;
+    s.cfn[1][1] = k_xform_warp_c<1, 0, CW, REP, NSW, BLK, NSUB>;
   }
   return s;
 }
@@ -411,6 +415,7 @@ static Shape g_shapes[] = {
     make_wshape<8, 16, 3, 2, 1>(), make_wshape<20, 16, 2, 1, 2>(), make_wshape<20, 24, 2, 1, 2>(),
     make_wshape<16, 24, 4, 1, 1>()};
 static Shape* g_shape = nullptr;
+static int g_slot_bps = 1;   // resident CTAs/SM of the slot kernels
 static bool g_identity = false;
 
 cudaError_t xform_setup_device() {
@@ -438,11 +443,16 @@ cudaError_t xform_setup_device() {
     if (e != cudaSuccess) return e;
   }
   // the device-built path always runs the production shape
-  for (auto fn : g_shapes[0].cfn) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)g_shapes[0].smem);
-    if (e != cudaSuccess) return e;
-  }
+  for (auto& pair : g_shapes[0].cfn)
+    for (auto fn : pair) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)g_shapes[0].smem);
+      if (e != cudaSuccess) return e;
+    }
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_slot_bps, g_shapes[0].cfn[0][0],
+                                                    g_shapes[0].threads, g_shapes[0].smem);
+  if (e != cudaSuccess) return e;
+  if (g_slot_bps < 1) g_slot_bps = 1;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pick->blocks_per_sm, pick->fn[2],
                                                     pick->threads, pick->smem);
   if (e != cudaSuccess) return e;
@@ -492,21 +502,18 @@ cudaError_t launch_xform_build(int slot, const XformBuildIn& in, const double* l
   return launched();
 }
 
-cudaError_t launch_xform_main_c(int slot, const uint8_t* src, uint8_t* dst, int64_t npix,
-                                unsigned long long* count, unsigned long long* items,
-                                unsigned long long cap, const unsigned int* alpha_bits,
-                                cudaStream_t st) {
+cudaError_t launch_xform_main_c(int slot, bool analytic, const uint8_t* src, uint8_t* dst,
+                                int64_t npix, unsigned long long* count,
+                                unsigned long long* items, unsigned long long cap,
+                                const unsigned int* alpha_bits, cudaStream_t st) {
   cudaError_t e = xform_setup_device();
   if (e != cudaSuccess) return e;
   if (npix <= 0) return cudaSuccess;
   const Shape& s = g_shapes[0];
-  int bps = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, s.cfn[slot], s.threads, s.smem);
-  if (e != cudaSuccess) return e;
   const int64_t ntiles = (npix + s.tile_px - 1) / s.tile_px;
-  const int grid = static_cast<int>(min64(ntiles, (int64_t)g_sm_count * (bps < 1 ? 1 : bps)));
-  RepairList rl{count, items, cap, alpha_bits};
-  s.cfn[slot]<<<grid, s.threads, s.smem, st>>>(src, dst, npix, rl);
+  const int grid = static_cast<int>(min64(ntiles, (int64_t)g_sm_count * g_slot_bps));
+  RepairList rl{count, items, cap, analytic ? nullptr : alpha_bits};
+  s.cfn[slot][analytic ? 1 : 0]<<<grid, s.threads, s.smem, st>>>(src, dst, npix, rl);
   return launched();
 }
 

@@ -50,10 +50,10 @@ cudaError_t launch_xform_build(int slot, const XformBuildIn& in, const double* l
                                const double* fit, DevParams* staging, void* ws,
                                int32_t* status_host, cudaEvent_t built, uint32_t q0, uint32_t q1,
                                cudaStream_t st);
-cudaError_t launch_xform_main_c(int slot, const uint8_t* src, uint8_t* dst, int64_t npix,
-                                unsigned long long* count, unsigned long long* items,
-                                unsigned long long cap, const unsigned int* alpha_bits,
-                                cudaStream_t st);
+cudaError_t launch_xform_main_c(int slot, bool analytic, const uint8_t* src, uint8_t* dst,
+                                int64_t npix, unsigned long long* count,
+                                unsigned long long* items, unsigned long long cap,
+                                const unsigned int* alpha_bits, cudaStream_t st);
 cudaError_t launch_xform_repair_c(int slot, const uint8_t* src, uint8_t* dst, int64_t npix,
                                   int64_t head, int64_t body, unsigned long long* count,
                                   unsigned long long* items, unsigned long long cap,

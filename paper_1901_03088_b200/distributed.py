@@ -218,7 +218,7 @@ class RowBandGroup:
             raise ValueError("fit_transform: out must be a contiguous tensor shaped like the band")
         L = _lib.lib()
         npix = src.numel() // 3
-        p = _fitted_params(target, float(code_lam))
+        p = _fitted_params(target, float(code_lam), self.width * self.height)
         ws_bytes = int(L.spcn_xform_workspace_bytes(max(npix, 1)))
         st = _lib.stream_handle()
         ws = _dev.workspace(ws_bytes, stream=st)

@@ -733,7 +733,6 @@ def _fused_ok(src: DeviceSource, tp: FitParams, out, precision: str, p99_mode: s
         return False
     tgt_p99 = np.asarray(tp.stats.p99, dtype=np.float64)
     return (precision == "exact" and p99_mode == "sample" and not per_patch_stats
-            and src.width * src.height >= XformPlan.CALIBRATE_MIN_PIXELS
             and bool(np.all(tgt_p99 > 0)) and bool(np.all(np.isfinite(tgt_p99)))
             and (src.tensor.data_ptr() - out.data_ptr()) % 16 == 0)
 
@@ -761,7 +760,7 @@ def fit_transform_resident(src: DeviceSource, target: FitParams, out, *,
     L = _lib.lib()
     npix = src.width * src.height
     # everything that does not depend on the sample, before the sampling wait
-    p = _fitted_params(target, float(code_lam))
+    p = _fitted_params(target, float(code_lam), npix)
     p.src_od_table = fb.lut_ptr
     p.src_fit = fb.arena_b_ptr
     ws_bytes = int(L.spcn_xform_workspace_bytes(npix))
@@ -794,14 +793,20 @@ def fit_transform_resident(src: DeviceSource, target: FitParams, out, *,
     return sp
 
 
-def _fitted_params(target: FitParams, code_lam: float):
-    """spcn_xform_fitted's host half (target profile + options)."""
+FITTED_ANALYTIC = 1   # include/spcn.h SPCN_FITTED_ANALYTIC
+
+
+def _fitted_params(target: FitParams, code_lam: float, total_pixels: int):
+    """spcn_xform_fitted's host half (target profile + options).  Images
+    below XformPlan.CALIBRATE_MIN_PIXELS use the analytic bound, as
+    XformPlan.maybe_calibrate decides for the host-built path."""
     p = _lib.XformFitted()
     np.frombuffer(p, dtype=np.float64, count=12, offset=16)[:] = np.concatenate([
         _dev.f64_array(target.basis, 6, "tgt_basis"),
         np.asarray(target.stats.p99, dtype=np.float64).reshape(2),
         _dev.f64_array(target.i0, 3, "tgt_i0"), [code_lam]])
     p.max_sweeps = 2000
+    p.flags = FITTED_ANALYTIC if total_pixels < XformPlan.CALIBRATE_MIN_PIXELS else 0
     return p
 
 

@@ -151,7 +151,7 @@ def _fitted_call(src, out, lut_dev, arena, target, code_lam=0.0):
 
     L = _lib.lib()
     npix = src.numel() // 3
-    p = pipeline._fitted_params(target, code_lam)
+    p = pipeline._fitted_params(target, code_lam, npix)
     p.src_od_table = _lib.ptr(lut_dev)
     p.src_fit = _lib.ptr(arena)
     ws_bytes = int(L.spcn_xform_workspace_bytes(npix))
@@ -231,10 +231,34 @@ def test_fitted_entry_argument_errors(slides):
 
     src, target = slides
     L = _lib.lib()
-    p = pipeline._fitted_params(target, 0.0)
+    p = pipeline._fitted_params(target, 0.0, src.numel() // 3)
     ws = torch.empty(1024, dtype=torch.uint8, device="cuda")
     rc = L.spcn_xform_rgb8_fitted(_lib.ptr(src), _lib.ptr(src), src.numel() // 3, ctypes.byref(p),
                                   _lib.ptr(ws), 1024, None, _lib.stream_handle())
     assert rc != 0   # NULL table / arena
     assert L.spcn_last_error()
     del pb
+
+
+@pytest.mark.parametrize("shape", [(320, 384), (333, 517), (2048, 2048)])
+def test_fused_small_images_analytic_bound(shape, monkeypatch):
+    """Below 2^24 px the device-built recolouring takes the analytic bound
+    (no calibration), as the host path does: same bytes."""
+    import torch
+
+    from paper_1901_03088_b200 import synthetic
+
+    pb = _pb()
+    h, w = shape
+    img = synthetic.render_slide(w, h, 40 + h, tissue_fraction=0.6)
+    tgt = synthetic.render_slide(512, 512, 41, tissue_fraction=0.6, i0=(250, 243, 230))
+    target = _quiet(pb.fit, pb.DeviceSource(tgt))
+    ref = _unfused(img, target, monkeypatch)
+    out = torch.empty_like(img)
+    _quiet(pb.normalize, img, target, out=out)
+    assert torch.equal(out, ref)
+    # and normalize(image, image): the target fitted in the same call
+    both = _quiet(pb.normalize, img, tgt)
+    monkeypatch.setenv("SPCN_FUSED", "0")
+    both_ref = _quiet(pb.normalize, img, tgt)
+    assert torch.equal(both, both_ref)
