@@ -445,6 +445,12 @@ typedef struct spcn_xform_fitted {
   double code_lam;
   int32_t max_sweeps;
   int32_t flags;                /* SPCN_FITTED_* (0: calibrated bound)          */
+  /* optional: a target fitted on the device in the same stream — its arena B
+   * (basis | p99 | info | absent) and its i0 (3 f64); tgt_basis / tgt_p99 /
+   * tgt_i0 above are then ignored and the target's checks (absent stain, p99
+   * > 0, valid basis) join the device-side decline conditions              */
+  const void* tgt_fit;
+  const double* tgt_i0_dev;
 } spcn_xform_fitted;
 /* flags: the analytic per-pixel certification bound instead of the
  * exhaustive calibration (images below ~2^24 px, where the 0.3 ms

@@ -72,6 +72,8 @@ class XformFitted(ctypes.Structure):
         ("code_lam", ctypes.c_double),
         ("max_sweeps", ctypes.c_int32),
         ("flags", ctypes.c_int32),
+        ("tgt_fit", ctypes.c_void_p),
+        ("tgt_i0_dev", ctypes.c_void_p),
     ]
 
 

@@ -365,13 +365,16 @@ FittedSlots g_fitted[64];
 int check_fitted(const spcn_xform_fitted* p) {
   if (!p) return fail(SPCN_EINVAL, "params is NULL");
   if (!p->src_od_table || !p->src_fit) return fail(SPCN_EINVAL, "NULL table / fit arena");
-  int rc = check_basis(p->tgt_basis, "target");
-  if (rc) return rc;
-  for (int c = 0; c < 3; ++c)
-    if (!std::isfinite(p->tgt_i0[c])) return fail(SPCN_EINVAL, "target i0 must be finite");
-  for (int j = 0; j < 2; ++j)
-    if (!(p->tgt_p99[j] > 0.0) || !std::isfinite(p->tgt_p99[j]))
-      return fail(SPCN_EINVAL, "target p99 must be positive and finite");
+  if (p->tgt_fit && !p->tgt_i0_dev) return fail(SPCN_EINVAL, "tgt_fit needs tgt_i0_dev");
+  if (!p->tgt_fit) {   // a host-side target profile (a device-side one is checked on the device)
+    int rc = check_basis(p->tgt_basis, "target");
+    if (rc) return rc;
+    for (int c = 0; c < 3; ++c)
+      if (!std::isfinite(p->tgt_i0[c])) return fail(SPCN_EINVAL, "target i0 must be finite");
+    for (int j = 0; j < 2; ++j)
+      if (!(p->tgt_p99[j] > 0.0) || !std::isfinite(p->tgt_p99[j]))
+        return fail(SPCN_EINVAL, "target p99 must be positive and finite");
+  }
   if (!(p->code_lam >= 0.0)) return fail(SPCN_EINVAL, "lam must be >= 0");
   if (p->max_sweeps < 0) return fail(SPCN_EINVAL, "max_sweeps must be >= 0");
   if (p->flags & ~SPCN_FITTED_ANALYTIC) return fail(SPCN_EINVAL, "unknown flags");
@@ -421,6 +424,8 @@ int fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts, voi
   std::memcpy(in.tgt_i0, p->tgt_i0, sizeof(in.tgt_i0));
   in.code_lam = p->code_lam;
   in.max_sweeps = p->max_sweeps;
+  in.tgt_fit_dev = static_cast<const double*>(p->tgt_fit);
+  in.tgt_i0_dev = p->tgt_fit ? p->tgt_i0_dev : nullptr;
   const uint32_t n = (p->flags & SPCN_FITTED_ANALYTIC) ? 0u : 1u << 23;   // colour pairs
   const uint32_t q0 = static_cast<uint32_t>((uint64_t)n * part / nparts),
                  q1 = static_cast<uint32_t>((uint64_t)n * (part + 1) / nparts);

@@ -301,25 +301,41 @@ __global__ void __launch_bounds__(256) k_build_xform(const __grid_constant__ Xfo
   __syncthreads();
   if (threadIdx.x != 0) return;
   // arena B: basis f64[6] | p99 f64[2] | info i32[4] | absent i32[2]
+  auto absent_of = [](const double* a) { return reinterpret_cast<const int32_t*>(a + 10); };
+  auto basis_ok = [](const double* w) {                                 // api.cu check_basis
+    for (int k = 0; k < 6; ++k)
+      if (!isfinite(w[k]) || w[k] < 0) return false;
+    for (int j = 0; j < 2; ++j) {
+      const double nrm = sqrt(p_add(p_add(p_mul(w[j], w[j]), p_mul(w[2 + j], w[2 + j])),
+                                    p_mul(w[4 + j], w[4 + j])));
+      if (fabs(nrm - 1.0) > 1e-9) return false;
+    }
+    return true;
+  };
   const double* basis = fit;
   const double* p99 = fit + 6;
-  const int32_t* absent = reinterpret_cast<const int32_t*>(fit + 10);
+  const double* tgt = in.tgt_fit_dev;               // a target fitted on the device, or null
+  const double* tbasis = tgt ? tgt : in.tgt_basis;
+  const double* tp99 = tgt ? tgt + 6 : in.tgt_p99;
+  const double* ti0v = tgt ? in.tgt_i0_dev : in.tgt_i0;
   int32_t st = 0;
-  if (absent[0] || absent[1]) st = -SPCN_ESTAIN_ABSENT;
+  if (absent_of(fit)[0] || absent_of(fit)[1]) st = -SPCN_ESTAIN_ABSENT;
+  if (tgt && st == 0) {                             // the host checked a host-side target
+    if (absent_of(tgt)[0] || absent_of(tgt)[1]) st = -SPCN_ESTAIN_ABSENT;
+    for (int j = 0; j < 2 && st == 0; ++j)
+      if (!(tp99[j] > 0.0) || !isfinite(tp99[j])) st = -SPCN_EDEGENERATE;
+    if (st == 0 && !basis_ok(tbasis)) st = -SPCN_EINVAL;
+    for (int c = 0; c < 3 && st == 0; ++c)
+      if (!isfinite(ti0v[c])) st = -SPCN_EINVAL;
+  }
   double f[2] = {1.0, 1.0};
   for (int j = 0; j < 2 && st == 0; ++j) {
     if (!(p99[j] > 0.0) || !isfinite(p99[j])) st = -SPCN_EDEGENERATE;   // scale_factors
-    else f[j] = __ddiv_rn(in.tgt_p99[j], p99[j]);
+    else f[j] = __ddiv_rn(tp99[j], p99[j]);
     if (st == 0 && (!(f[j] > 0.0) || !isfinite(f[j]))) st = -SPCN_EDEGENERATE;
   }
-  for (int k = 0; k < 6 && st == 0; ++k)                                // api.cu check_basis
-    if (!isfinite(basis[k]) || basis[k] < 0) st = -SPCN_EINVAL;
-  for (int j = 0; j < 2 && st == 0; ++j) {
-    const double nrm = sqrt(p_add(p_add(p_mul(basis[j], basis[j]), p_mul(basis[2 + j], basis[2 + j])),
-                                  p_mul(basis[4 + j], basis[4 + j])));
-    if (fabs(nrm - 1.0) > 1e-9) st = -SPCN_EINVAL;
-  }
-  fill_strict_scalars(sp, basis, in.tgt_basis, f, in.tgt_i0, in.code_lam, in.max_sweeps);
+  if (st == 0 && !basis_ok(basis)) st = -SPCN_EINVAL;
+  fill_strict_scalars(sp, basis, tbasis, f, ti0v, in.code_lam, in.max_sweeps);
   if (st == 0 && !fill_fast_scalars(out->fp, sp, true, nullptr)) st = 1;   // strict path only
   out->status = st;
   ws_hdr[0] = ws_hdr[1] = 0u;   // repair count

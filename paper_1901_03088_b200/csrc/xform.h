@@ -42,6 +42,8 @@ struct XformBuildIn {   // the host-known half: target profile and options
   double code_lam;
   int32_t max_sweeps;
   int32_t pad_;
+  const double* tgt_fit_dev;   // device (optional): the target's arena B, read instead of the above
+  const double* tgt_i0_dev;    // device: the target's i0 (with tgt_fit_dev)
 };
 // build (1 CTA) -> copy into __constant__ slot `slot` -> optional status
 // read-back into pinned host memory (then `built` is recorded) -> exhaustive

@@ -95,7 +95,9 @@ class FitBuffers:
 _TLS = threading.local()
 
 
-def buffers(device, target_pixels: int, max_outer: int) -> FitBuffers:
+def buffers(device, target_pixels: int, max_outer: int, slot: int = 0) -> FitBuffers:
+    """The thread's fit buffers for (device, current stream, sizes); `slot`
+    gives a second set for a fit in flight beside another (target + source)."""
     t = _dev.torch()
     dev = t.device(device) if not isinstance(device, t.device) else device
     if dev.index is None:
@@ -103,7 +105,7 @@ def buffers(device, target_pixels: int, max_outer: int) -> FitBuffers:
     cache = getattr(_TLS, "bufs", None)
     if cache is None:
         cache = _TLS.bufs = {}
-    key = (dev.index, _lib.stream_handle(), int(target_pixels), int(max_outer))
+    key = (dev.index, _lib.stream_handle(), int(target_pixels), int(max_outer), int(slot))
     fb = cache.get(key)
     if fb is None:
         if len(cache) > 8:

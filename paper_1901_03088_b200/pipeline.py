@@ -289,28 +289,46 @@ def _resident_candidates(fb, slide: DeviceSource, plan: SamplePlan):
     return c
 
 
-def _fit_sample_resident(fb, slide: DeviceSource, plan: SamplePlan, need_counts: bool = False):
+def _sample_batch(fb, slide: DeviceSource, plan: SamplePlan, c, k0: int, n: int) -> None:
+    """count -> visit -> compact -> i0 -> read-back of candidates [k0, k0+n),
+    one library call, stream-ordered (the first batch zeroes the arena)."""
+    import ctypes
+
+    from .fitcore import A_READ
+
+    _lib.check(_lib.lib().spcn_fit_sample_step(
+        _lib.ptr(slide.tensor), c["desc_ptr"] + k0 * PATCH_DT.itemsize, n, c["chunks"], k0,
+        c["dims_ptr"] + 8 * k0, ctypes.byref(c["vp"]), int(plan.white_threshold),
+        1 if k0 == 0 else 0, fb.arena_a_ptr, c["counts_ptr"],
+        c["takes_ptr"] + k0 * TAKE_DT.itemsize, fb.sample_ptr, fb.pin_a_ptr, A_READ,
+        _lib.stream_handle()), "fit_sample_step")
+
+
+def _sample_start(fb, slide: DeviceSource, plan: SamplePlan):
+    """Enqueue the first candidate batch of a resident slide's sampling (no
+    wait); _fit_sample_resident(..., started=<this>) finishes it."""
+    c = _resident_candidates(fb, slide, plan)
+    k0, n = c["batches"][0]
+    _sample_batch(fb, slide, plan, c, k0, n)
+    return c
+
+
+def _fit_sample_resident(fb, slide: DeviceSource, plan: SamplePlan, need_counts: bool = False,
+                         started=None):
     """Sampling + i0 of a device-resident slide with ONE host read in the
     common case: count → visit loop (k_visit, on the device) → ordered
     compaction → i0, then a single read of (state, i0, empty flags).  A
     further candidate batch runs only when the first ran out before a stop
     rule fired.  Returns (m, i0, PixelSample meta, empty flags); the sample is
     fb.sample[:3m]."""
-    import ctypes
-
     L = _lib.lib()
-    c = _resident_candidates(fb, slide, plan)
-    thr = int(plan.white_threshold)
-    img, stream = slide.tensor, _lib.stream_handle()
+    c = started if started is not None else _resident_candidates(fb, slide, plan)
+    stream = _lib.stream_handle()
     from .fitcore import A_READ
 
-    for k0, n in c["batches"]:
-        # count -> visit -> compact -> i0 -> read-back, one library call
-        _lib.check(L.spcn_fit_sample_step(
-            _lib.ptr(img), c["desc_ptr"] + k0 * PATCH_DT.itemsize, n, c["chunks"], k0,
-            c["dims_ptr"] + 8 * k0, ctypes.byref(c["vp"]), thr, 1 if k0 == 0 else 0,
-            fb.arena_a_ptr, c["counts_ptr"], c["takes_ptr"] + k0 * TAKE_DT.itemsize,
-            fb.sample_ptr, fb.pin_a_ptr, A_READ, stream), "fit_sample_step")
+    for i, (k0, n) in enumerate(c["batches"]):
+        if i > 0 or started is None:
+            _sample_batch(fb, slide, plan, c, k0, n)
         _lib.check(L.spcn_stream_sync(stream), "stream_sync")
         raw = fb.pin_a_np[:A_READ].copy()
         st = raw[:64].view(np.int64)
@@ -426,12 +444,13 @@ def slide_chunks(slide, rows: int = 2048):
     return gen
 
 
-def _fit_sample_checked(fb, slide: DeviceSource, plan: SamplePlan, need_counts: bool):
+def _fit_sample_checked(fb, slide: DeviceSource, plan: SamplePlan, need_counts: bool,
+                        started=None):
     """Resident slide: visit loop + i0 on the device (one host round trip),
     with the reference's blank-slide error and background warnings."""
     with _dev.nvtx("spcn.fit.sample"):
         m, i0, meta, empty = _stage("sampling", _fit_sample_resident, fb, slide, plan,
-                                    need_counts)
+                                    need_counts, started=started)
     if m == 0:
         raise BlankSlideError("sampling: blank slide: no non-white pixels found in any "
                               "sampled patch")
@@ -731,9 +750,11 @@ def _fused_ok(src: DeviceSource, tp: FitParams, out, precision: str, p99_mode: s
     sequence with the recolouring built on the device (fit_transform_resident)."""
     if os.environ.get("SPCN_FUSED", "1") == "0":
         return False
-    tgt_p99 = np.asarray(tp.stats.p99, dtype=np.float64)
+    if tp is not None:          # (None: a target fitted on the device, checked there)
+        tgt_p99 = np.asarray(tp.stats.p99, dtype=np.float64)
+        if not (np.all(tgt_p99 > 0) and np.all(np.isfinite(tgt_p99))):
+            return False
     return (precision == "exact" and p99_mode == "sample" and not per_patch_stats
-            and bool(np.all(tgt_p99 > 0)) and bool(np.all(np.isfinite(tgt_p99)))
             and (src.tensor.data_ptr() - out.data_ptr()) % 16 == 0)
 
 
@@ -793,6 +814,71 @@ def fit_transform_resident(src: DeviceSource, target: FitParams, out, *,
     return sp
 
 
+def fit_pair_transform_resident(src: DeviceSource, tgt: DeviceSource, out, *,
+                                plan: SamplePlan = SamplePlan(),
+                                cfg: SnmfConfig = SnmfConfig(), code_lam: float = 0.0,
+                                stats: RunStats | None = None):
+    """normalize(source, target) for two resident images (src/cli.py:220-244:
+    fit(target), fit(source), transform): the two fits run in lockstep — both
+    samplings, one wait, both SNMF/p99 tails — and the recolouring is built
+    on the device from both fits (spcn_xform_rgb8_fitted with tgt_fit), so a
+    call has two host waits instead of four.  The target's errors and
+    warnings come first, as in the reference; a recolouring the device
+    declines is redone by transform() with host parameters.  Returns
+    (source fit, target fit)."""
+    from . import fitcore
+
+    stats = stats if stats is not None else RunStats()
+    t0 = time.perf_counter()
+    fb_s = fitcore.buffers(src.tensor.device, plan.target_pixels, cfg.max_outer_iters, slot=0)
+    fb_t = fitcore.buffers(tgt.tensor.device, plan.target_pixels, cfg.max_outer_iters, slot=1)
+    L = _lib.lib()
+    npix = src.width * src.height
+    p = _lib.XformFitted()
+    p.code_lam = float(code_lam)
+    p.max_sweeps = 2000
+    p.flags = FITTED_ANALYTIC if npix < XformPlan.CALIBRATE_MIN_PIXELS else 0
+    p.src_od_table, p.src_fit = fb_s.lut_ptr, fb_s.arena_b_ptr
+    p.tgt_fit, p.tgt_i0_dev = fb_t.arena_b_ptr, fb_t.arena_a_ptr + fitcore.A_I0
+    ws_bytes = int(L.spcn_xform_workspace_bytes(npix))
+    st = _lib.stream_handle()
+    ws = _dev.workspace(ws_bytes, stream=st)
+    started_t = _sample_start(fb_t, tgt, plan)
+    started_s = _sample_start(fb_s, src, plan)
+    m_t, i0_t, _ = _fit_sample_checked(fb_t, tgt, plan, False, started=started_t)
+    m_s, i0_s, meta = _fit_sample_checked(fb_s, src, plan, False, started=started_s)
+    stats.sampled_pixels = m_s
+    stats.patches = meta.patches_used
+    t1 = time.perf_counter()
+    stats.sampling_s += t1 - t0
+    with _dev.nvtx("spcn.fit_pair_transform"):
+        fitcore.basis_enqueue(fb_t, fb_t.sample_ptr, m_t, i0_t, cfg, code_lam=code_lam,
+                              pooled=True)
+        fitcore.basis_enqueue(fb_s, fb_s.sample_ptr, m_s, i0_s, cfg, code_lam=code_lam,
+                              pooled=True)
+        fb_s.pin_status_np[0] = -1
+        # returns once the build status (and both fits' read-backs before it)
+        # is in host memory; the recolour is still running, stream-ordered
+        _lib.check(L.spcn_xform_rgb8_fitted(src.tensor.data_ptr(), out.data_ptr(), npix,
+                                            ctypes.byref(p), _lib.ptr(ws), ws_bytes,
+                                            fb_s.pin_status_ptr, st), "xform_rgb8_fitted")
+    from . import fitcore as fc
+
+    prov = fc.provenance(plan, cfg, code_lam, False, "sample", "")
+    tp = fc.parse_pooled(fb_t, m_t, i0_t, cfg, prov, stacklevel=3)
+    sp = fc.parse_pooled(fb_s, m_s, i0_s, cfg, prov, stacklevel=3)
+    t2 = time.perf_counter()
+    stats.basis_fit_s += t2 - t1
+    if int(fb_s.pin_status_np[0]) != 0:
+        transform(src, sp, tp, DeviceWriter(src.width, src.height, out=out),
+                  code_lam=code_lam, stats=stats, precision="exact")
+    else:
+        stats.transform_s += time.perf_counter() - t2
+        stats.transformed_pixels = npix
+        stats.total_s = stats.sampling_s + stats.basis_fit_s + stats.transform_s
+    return sp, tp
+
+
 FITTED_ANALYTIC = 1   # include/spcn.h SPCN_FITTED_ANALYTIC
 
 
@@ -827,20 +913,30 @@ def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
     stats = stats if stats is not None else RunStats()
     host = not _dev.is_tensor(source)
     src = ArraySource(source) if host else DeviceSource(source)
-    if isinstance(target, FitParams):
-        tp = target
-    elif isinstance(target, (str, os.PathLike)):
-        tp = load_profile(target)
-    else:
-        tsrc = ArraySource(target) if not _dev.is_tensor(target) else DeviceSource(target)
-        tp = fit(tsrc, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats,
-                 p99_mode=p99_mode)
+    dst = None
     if not host:
         dst = out if out is not None else t.empty((src.height, src.width, 3), dtype=t.uint8,
                                                   device=src.tensor.device)
         if tuple(dst.shape) != (src.height, src.width, 3) or dst.dtype != t.uint8 or \
                 dst.device != src.tensor.device or not dst.is_contiguous():
             raise ValueError("out must be a contiguous uint8 CUDA tensor shaped like the source")
+    if isinstance(target, FitParams):
+        tp = target
+    elif isinstance(target, (str, os.PathLike)):
+        tp = load_profile(target)
+    else:
+        tsrc = ArraySource(target) if not _dev.is_tensor(target) else DeviceSource(target)
+        if dst is not None and isinstance(tsrc, DeviceSource) and \
+                tsrc.tensor.device == src.tensor.device and \
+                _fused_ok(src, None, dst, precision, p99_mode, per_patch_stats):
+            # both resident: the two fits in lockstep, the recolouring built
+            # from both on the device (fit_pair_transform_resident)
+            fit_pair_transform_resident(src, tsrc, dst, plan=plan, cfg=cfg, code_lam=code_lam,
+                                        stats=stats)
+            return dst
+        tp = fit(tsrc, plan, cfg, code_lam=code_lam, per_patch_stats=per_patch_stats,
+                 p99_mode=p99_mode)
+    if not host:
         if _fused_ok(src, tp, dst, precision, p99_mode, per_patch_stats):
             fit_transform_resident(src, tp, dst, plan=plan, cfg=cfg, code_lam=code_lam,
                                    stats=stats)

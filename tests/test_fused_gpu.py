@@ -262,3 +262,48 @@ def test_fused_small_images_analytic_bound(shape, monkeypatch):
     monkeypatch.setenv("SPCN_FUSED", "0")
     both_ref = _quiet(pb.normalize, img, tgt)
     assert torch.equal(both, both_ref)
+
+
+def test_fused_pair_errors_match_the_host_order(monkeypatch):
+    """normalize(image, image) with both resident runs the two fits in
+    lockstep: the target's errors still come first, with the reference's
+    types and messages."""
+    import torch
+
+    from paper_1901_03088_b200 import synthetic
+
+    pb = _pb()
+    img = synthetic.render_slide(640, 480, 77, tissue_fraction=0.6)
+    blank = torch.full_like(img, 255)
+    sparse = blank.clone()
+    sparse[0, :5] = 40                                   # 5 non-white pixels: < 10
+    for tgt, src in ((blank, img), (img, blank), (sparse, img), (img, sparse)):
+        got = exp = None
+        try:
+            _quiet(pb.normalize, src, tgt)
+        except Exception as exc:      # noqa: BLE001
+            got = exc
+        monkeypatch.setenv("SPCN_FUSED", "0")
+        try:
+            _quiet(pb.normalize, src, tgt)
+        except Exception as exc:      # noqa: BLE001
+            exp = exc
+        monkeypatch.delenv("SPCN_FUSED")
+        assert exp is not None
+        assert type(got) is type(exp) and str(got) == str(exp), (got, exp)
+
+
+def test_fused_pair_large_calibrated(monkeypatch):
+    """Pair path above 2^24 px (calibrated bound), target fitted on the device."""
+    import torch
+
+    pb = _pb()
+    from paper_1901_03088_b200 import synthetic
+
+    img = synthetic.render_slide(4096, 4100, 91, tissue_fraction=0.5)
+    tgt = synthetic.render_slide(1500, 1400, 92, tissue_fraction=0.6, i0=(250, 243, 230))
+    out = torch.empty_like(img)
+    _quiet(pb.normalize, img, tgt, out=out)
+    monkeypatch.setenv("SPCN_FUSED", "0")
+    ref = _quiet(pb.normalize, img, tgt)
+    assert torch.equal(out, ref)
