@@ -843,19 +843,34 @@ def fit_pair_transform_resident(src: DeviceSource, tgt: DeviceSource, out, *,
     ws_bytes = int(L.spcn_xform_workspace_bytes(npix))
     st = _lib.stream_handle()
     ws = _dev.workspace(ws_bytes, stream=st)
-    started_t = _sample_start(fb_t, tgt, plan)
+    # the target's fit on a side stream beside the source's (each fit's
+    # kernels fill only a few SMs: its SNMF is one 16-CTA cluster)
+    t = _dev.torch()
+    main = t.cuda.current_stream()
+    if os.environ.get("SPCN_PAIR_SIDE", "1") == "0":       # (A/B: one stream)
+        side, fork, join = main, t.cuda.Event(), t.cuda.Event()
+    else:
+        side, fork, join = _side_stream(src.tensor.device)
+    fork.record(main)
+    side.wait_event(fork)
+    with t.cuda.stream(side):
+        started_t = _sample_start(fb_t, tgt, plan)
     started_s = _sample_start(fb_s, src, plan)
-    m_t, i0_t, _ = _fit_sample_checked(fb_t, tgt, plan, False, started=started_t)
+    with t.cuda.stream(side):
+        m_t, i0_t, _ = _fit_sample_checked(fb_t, tgt, plan, False, started=started_t)
     m_s, i0_s, meta = _fit_sample_checked(fb_s, src, plan, False, started=started_s)
     stats.sampled_pixels = m_s
     stats.patches = meta.patches_used
     t1 = time.perf_counter()
     stats.sampling_s += t1 - t0
     with _dev.nvtx("spcn.fit_pair_transform"):
-        fitcore.basis_enqueue(fb_t, fb_t.sample_ptr, m_t, i0_t, cfg, code_lam=code_lam,
-                              pooled=True)
+        with t.cuda.stream(side):
+            fitcore.basis_enqueue(fb_t, fb_t.sample_ptr, m_t, i0_t, cfg, code_lam=code_lam,
+                                  pooled=True)
+            join.record(side)
         fitcore.basis_enqueue(fb_s, fb_s.sample_ptr, m_s, i0_s, cfg, code_lam=code_lam,
                               pooled=True)
+        main.wait_event(join)      # the build reads the target's arena
         fb_s.pin_status_np[0] = -1
         # returns once the build status (and both fits' read-backs before it)
         # is in host memory; the recolour is still running, stream-ordered
@@ -877,6 +892,22 @@ def fit_pair_transform_resident(src: DeviceSource, tgt: DeviceSource, out, *,
         stats.transformed_pixels = npix
         stats.total_s = stats.sampling_s + stats.basis_fit_s + stats.transform_s
     return sp, tp
+
+
+_SIDE = threading.local()
+
+
+def _side_stream(device):
+    """Per-thread side stream + fork/join events of a device (reused: fresh
+    streams per call would defeat the caching allocator's per-stream pools)."""
+    t = _dev.torch()
+    key = t.device(device).index
+    cache = _SIDE.__dict__.setdefault("by_dev", {})
+    hit = cache.get(key)
+    if hit is None:
+        with t.cuda.device(key):
+            hit = cache[key] = (t.cuda.Stream(), t.cuda.Event(), t.cuda.Event())
+    return hit
 
 
 FITTED_ANALYTIC = 1   # include/spcn.h SPCN_FITTED_ANALYTIC

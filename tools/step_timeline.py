@@ -14,7 +14,10 @@ from paper_1901_03088_b200 import synthetic  # noqa: E402
 side = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000
 fused = os.environ.get("SPCN_FUSED", "1") != "0"   # step = pb.normalize (device-built params)
 slide = synthetic.render_slide(side, side, 1, tissue_fraction=0.6)
-tgt = pb.fit(pb.DeviceSource(synthetic.render_slide(2048, 2048, 2)))
+tgt_img = synthetic.render_slide(2048, 2048, 2)
+tgt = pb.fit(pb.DeviceSource(tgt_img))
+if os.environ.get("SPCN_PAIR") == "1":   # C1: the target is an image fitted every step
+    tgt = tgt_img
 src = pb.DeviceSource(slide)
 out = torch.empty_like(slide)
 
