@@ -927,6 +927,23 @@ def _fitted_params(target: FitParams, code_lam: float, total_pixels: int):
     return p
 
 
+WHOLE_UPLOAD_PIXELS = 1 << 26     # 64 Mpx (192 MB): host images up to this go up whole
+
+
+def _whole_upload_ok(source, target) -> bool:
+    """A host (numpy, uint8 (h, w, 3)) source — and a numpy target image, if
+    one — small enough to go to the GPU whole."""
+    if os.environ.get("SPCN_WHOLE_UPLOAD", "1") == "0":
+        return False
+    if not (isinstance(source, np.ndarray) and source.dtype == np.uint8 and
+            source.ndim == 3 and source.shape[2] == 3 and 0 < source.size // 3 <= WHOLE_UPLOAD_PIXELS):
+        return False
+    if isinstance(target, np.ndarray):
+        return (target.dtype == np.uint8 and target.ndim == 3 and target.shape[2] == 3
+                and 0 < target.size // 3 <= WHOLE_UPLOAD_PIXELS)
+    return isinstance(target, (FitParams, str, os.PathLike))
+
+
 def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
               cfg: SnmfConfig = SnmfConfig(), code_lam: float = 0.0,
               per_patch_stats: bool = False, strip_height: int = DEFAULT_STRIP_HEIGHT,
@@ -937,12 +954,24 @@ def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
     (src/cli.py:220-244).  numpy in → numpy out; CUDA tensor in → CUDA tensor
     out (written into ``out`` when given).  A resident slide with a pooled
     p99 and EXACT precision runs as fit_transform_resident (no host round
-    trip between the fit and the recolour; same bytes)."""
+    trip between the fit and the recolour; same bytes).  A host image small
+    enough (≤ WHOLE_UPLOAD_PIXELS) is uploaded whole and takes the device
+    path (a tile's fits then need no per-patch uploads and run in lockstep
+    with the target's); larger ones stream strips through the GPU."""
     from .normalize import load_profile
 
     t = _dev.torch()
     stats = stats if stats is not None else RunStats()
     host = not _dev.is_tensor(source)
+    if host and out is None and _whole_upload_ok(source, target):
+        dev_t = target
+        if isinstance(target, np.ndarray):
+            dev_t = t.from_numpy(np.ascontiguousarray(target)).cuda()
+        res = normalize(t.from_numpy(np.ascontiguousarray(source)).cuda(), dev_t, plan=plan,
+                        cfg=cfg, code_lam=code_lam, per_patch_stats=per_patch_stats,
+                        strip_height=strip_height, precision=precision, stats=stats,
+                        p99_mode=p99_mode)
+        return res.cpu().numpy()
     src = ArraySource(source) if host else DeviceSource(source)
     dst = None
     if not host:
