@@ -15,27 +15,36 @@ constexpr int kTabSlots = 1 << kTabBits;
 constexpr uint32_t kTabEmpty = 0xffffffffu;
 constexpr uint32_t kNoColour = 0xffffffffu;   // a lane without a sample
 
-// One colour per lane (kNoColour: none), all 32 lanes present: lanes holding
-// the same colour insert once with their count.  Sets *full when the table
-// passes 3/4 load or a probe sequence fails (the caller then lists samples).
-__device__ __forceinline__ void ct_insert(uint32_t* key, uint32_t* cnt, int* used, int* full,
-                                          uint32_t rgb) {
-  const unsigned peers = __match_any_sync(0xffffffffu, rgb);
-  if (rgb == kNoColour || (int)(threadIdx.x & 31) != __ffs(peers) - 1) return;
-  const uint32_t add = __popc(peers);
+// One colour per lane (kNoColour: none).  Sets *full when a probe sequence
+// fails; the load test (more than 3/4 of the slots taken — the distinct
+// colours, a set property) is made once after all inserts (ct_overfull), so
+// no shared counter is contended per new key.  The caller lists the samples
+// one by one when either fires.
+__device__ __forceinline__ void ct_insert(uint32_t* key, uint32_t* cnt, int* full, uint32_t rgb) {
+  if (rgb == kNoColour) return;
   uint32_t slot = (rgb * 2654435761u) >> (32 - kTabBits);
   for (int probe = 0; probe < 64; ++probe, slot = (slot + 1) & (kTabSlots - 1)) {
     uint32_t k = key[slot];
-    if (k == kTabEmpty) {
-      k = atomicCAS(&key[slot], kTabEmpty, rgb);
-      if (k == kTabEmpty && atomicAdd(used, 1) >= (3 * kTabSlots) / 4) *full = 1;
-    }
+    if (k == kTabEmpty) k = atomicCAS(&key[slot], kTabEmpty, rgb);
     if (k == kTabEmpty || k == rgb) {
-      atomicAdd(&cnt[slot], add);
+      atomicAdd(&cnt[slot], 1u);
       return;
     }
   }
   *full = 1;
+}
+
+// After the inserts (and a barrier): sets *full if more than 3/4 of the
+// slots are taken.  NT threads; *used must be 0 on entry; ends with a barrier.
+template <int NT>
+__device__ __forceinline__ void ct_overfull(const uint32_t* key, int* used, int* full) {
+  int occ = 0;
+  for (int i = threadIdx.x; i < kTabSlots; i += NT) occ += key[i] != kTabEmpty;
+  occ = __reduce_add_sync(0xffffffffu, occ);
+  if ((threadIdx.x & 31) == 0) atomicAdd(used, occ);
+  __syncthreads();
+  if (threadIdx.x == 0 && *used > (3 * kTabSlots) / 4) *full = 1;
+  __syncthreads();
 }
 
 // Write the table as (rgb, count) entries at ukey/ucnt[o0 ..], *ucount_p = #.

@@ -426,8 +426,8 @@ __global__ void __launch_bounds__(kCT) k_colour_table(const uint8_t* __restrict_
 #pragma unroll
         for (int j = 0; j < 16; ++j) rgb[j] = kNoColour;
       }
-#pragma unroll 1
-      for (int j = 0; j < 16; ++j) ct_insert(key, cnt, &s_used, &s_full, rgb[j]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) ct_insert(key, cnt, &s_full, rgb[j]);
     }
     // head [0, a) and tail [rest0, m): < 32 samples, one warp
     if (tid < 32) {
@@ -437,9 +437,10 @@ __global__ void __launch_bounds__(kCT) k_colour_table(const uint8_t* __restrict_
         const uint8_t* px = samples + 3 * (o0 + i);
         rgb = px[0] | (px[1] << 8) | (px[2] << 16);
       }
-      ct_insert(key, cnt, &s_used, &s_full, rgb);
+      ct_insert(key, cnt, &s_full, rgb);
     }
     __syncthreads();
+    ct_overfull<kCT>(key, &s_used, &s_full);
     if (!s_full) {
       ct_finish<kCT>(key, cnt, s_scan, ukey, ucnt, o0, &ucount[p]);
     } else {
