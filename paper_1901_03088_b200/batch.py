@@ -93,16 +93,19 @@ def _od_tables_exact(i0: np.ndarray, device):
     expanded to the items on the device."""
     t = _dev.torch()
     ramp = np.arange(256, dtype=np.float64)
-    rows, idx, base = [], np.empty((i0.shape[0], 3), np.int64), 0
+    n = i0.shape[0]
+    rows, idx, base = [], np.empty((n, 3), np.int64), 0
     for c in range(3):
-        vals, inv = np.unique(i0[:, c], return_inverse=True)
+        vals = np.unique(i0[:, c])                       # (sort only; few distinct)
         rows.append(np.log(vals[:, None] / np.clip(ramp[None, :], 1.0, vals[:, None])))
-        idx[:, c] = base + inv.ravel()
+        idx[:, c] = base + np.searchsorted(vals, i0[:, c])
         base += vals.size
-    # one upload of the distinct rows and one of the per-item row indices,
-    # one gather on the device
-    table = t.from_numpy(np.concatenate(rows)).to(device)
-    return table[t.from_numpy(idx).to(device)].contiguous()
+    # ONE upload (distinct rows | per-item row indices, as bytes), one gather
+    rows = np.concatenate(rows)
+    buf = np.concatenate([rows.reshape(-1).view(np.uint8), idx.reshape(-1).view(np.uint8)])
+    d = t.from_numpy(buf).to(device)
+    table = d[:rows.nbytes].view(t.float64).view(base, 256)
+    return table[d[rows.nbytes:].view(t.int64).view(n, 3)].contiguous()
 
 
 def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), *,
@@ -284,7 +287,9 @@ def transform_batch(images, fits: BatchFit, target: FitParams, out=None, *,
     if precision == "strict":
         status = t.where(status == 0, t.ones_like(status), status)
     status_h = _dev.readback(status)
-    errors = [None if s >= 0 else _ERR[int(s)](_MSG[int(s)]) for s in status_h]
+    errors = [None] * n
+    for i in np.flatnonzero(status_h < 0):
+        errors[i] = _ERR[int(status_h[i])](_MSG[int(status_h[i])])
     if per % 16:
         # item boundaries not 16-pixel aligned: one aligned-head/tail launch per item
         for i in range(n):
