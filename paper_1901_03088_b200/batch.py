@@ -12,6 +12,7 @@ build and one persistent recolour launch (+ the fp64 repair launch).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import warnings
 from dataclasses import dataclass
@@ -381,12 +382,13 @@ def normalize_batch_host(images, target, out=None, *, chunk: int = 256, streams:
             slot["d_in"] = d
 
     errors = [None] * n
-    if starts:
-        upload(0)
+    ahead = max(1, min(int(os.environ.get("SPCN_BATCH_AHEAD", "2")), len(slots) - 2))
+    for k in range(min(ahead, len(starts))):
+        upload(k)
     for k, a in enumerate(starts):
         b = min(n, a + chunk)
-        if k + 1 < len(starts):
-            upload(k + 1)                # next chunk's copy overlaps this chunk's compute
+        if k + ahead < len(starts):
+            upload(k + ahead)            # later chunks' copies overlap this chunk's compute
         slot = slots[k % len(slots)]
         with t.cuda.stream(slot["stream"]):
             d_in = slot["d_in"]
