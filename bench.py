@@ -706,8 +706,9 @@ def run_ours(args, rank, world, local):
             # all-reduced across the row bands)
             line["global_p99_mode"] = dict(alt_steps("p99_mode", "global"), note=(
                 "same step with fit(p99_mode='global'): exact p99 of every non-white pixel "
-                "(one k_stats_table pass; the per-colour table all-reduced over "
-                + ("NCCL" if world > 1 else "one rank") + ")"))
+                "(one k_stats_cube pass into per-rank colour tables; "
+                + ("a 64 KiB entry-histogram all-reduce + a small all-gather over NCCL"
+                   if world > 1 else "selection on this rank") + ")"))
         if args.p99_mode == "sample" and args.precision == "exact" and args.fused:
             line["host_params_step"] = dict(alt_steps("fused", False), note=(
                 "same step as fit + transform (pb.*, or RowBandGroup.* at N > 1): the "

@@ -230,8 +230,12 @@ def _table_select(eng, x, w, xmax, n: int, lo, ks, comm):
     bins of [lo_j, max_j] (summed across ranks: 64 KiB) gives the bins that
     hold the ranks; only their entries are gathered and selected exactly.
     Returns (values (2, len(ks)), below) or None when a rank falls below lo."""
-    xm = np.max(np.stack([np.asarray(v.cpu() if hasattr(v, "cpu") else v, dtype=np.float64)
-                          for v in comm.allgather(_as_tensor(xmax, x))]), axis=0)
+    local = isinstance(comm, _Local)
+    if local:                      # one process: no device round trip for the maxima
+        xm = np.asarray(xmax, dtype=np.float64)
+    else:
+        xm = np.max(np.stack([np.asarray(v.cpu() if hasattr(v, "cpu") else v, dtype=np.float64)
+                              for v in comm.allgather(_as_tensor(xmax, x))]), axis=0)
     scale = [SEL_BINS / (xm[j] - lo[j]) if xm[j] > lo[j] else 0.0 for j in range(2)]
     hist = comm.allreduce(eng.entries_hist(x, w, lo, scale, SEL_BINS))
     hist = hist.cpu().numpy() if hasattr(hist, "cpu") else np.asarray(hist)
@@ -251,6 +255,18 @@ def _table_select(eng, x, w, xmax, n: int, lo, ks, comm):
         before.append(int(c[b0 - 1]) if b0 else 0)
     lists = eng.entries_collect(x, w, lo, scale, SEL_BINS, bins)
     vals = np.empty((2, len(ks)))
+    if local and getattr(lists[0][0], "is_cuda", False):
+        # one read of both stains' (value, weight) lists (weights as f64 bits)
+        t = _dev.torch()
+        parts = [lists[0][0], lists[1][0], lists[0][1].view(t.float64),
+                 lists[1][1].view(t.float64)]
+        flat = _dev.readback(t.cat(parts))
+        n0, n1 = int(lists[0][0].numel()), int(lists[1][0].numel())
+        got = [(flat[:n0], flat[n0 + n1:2 * n0 + n1].view(np.int64)),
+               (flat[n0:n0 + n1], flat[2 * n0 + n1:].view(np.int64))]
+        for j in range(2):
+            vals[j] = weighted_select(got[j][0], got[j][1], [k - below[j] - before[j] for k in ks])
+        return vals, below
     for j in range(2):
         v = np.concatenate([np.asarray(a.cpu() if hasattr(a, "cpu") else a, dtype=np.float64)
                             for a in comm.allgather(lists[j][0])])
@@ -371,7 +387,8 @@ def global_p99(chunks, src_i0, basis, code_lam: float = 0.0, white_threshold: in
         with _dev.nvtx("spcn.global.scan"):
             x, w, xmax, over = eng.scan(tab)
         del tab
-        over = int(comm.allreduce(_as_tensor([1.0 if over else 0.0], x)).cpu().numpy()[0])
+        if not isinstance(comm, _Local):   # any rank's table overflowing sends all to the fallback
+            over = int(comm.allreduce(_as_tensor([1.0 if over else 0.0], x)).cpu().numpy()[0])
         with _dev.nvtx("spcn.global.select"):
             res = None if over else _table_select(eng, x, w, xmax, n, lo_t, [klo, khi], comm)
         if res is not None:

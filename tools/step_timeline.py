@@ -22,7 +22,14 @@ src = pb.DeviceSource(slide)
 out = torch.empty_like(slide)
 
 
+p99_mode = os.environ.get("SPCN_P99_MODE", "sample")
+
+
 def step():
+    if p99_mode != "sample":
+        fp = pb.fit(src, p99_mode=p99_mode)
+        pb.transform(src, fp, tgt, pb.DeviceWriter(side, side, out=out))
+        return
     if fused:
         pb.normalize(slide, tgt, out=out)
         return
