@@ -157,7 +157,7 @@ def test_calibration_parts_max_equals_full():
     assert float(worst) * (1.0 + 2.0 ** -20) == full, (worst, full)   # spcn_xform_calibrate's alpha
 
 
-def _fused_worker(rank, world, port, q, backend="gloo"):
+def _fused_worker(rank, world, port, q, backend="gloo", side=4096):
     import torch
     import torch.distributed as dist
 
@@ -166,7 +166,7 @@ def _fused_worker(rank, world, port, q, backend="gloo"):
 
     _init(rank, world, port, backend)
     try:
-        W, H = 4096, 4096
+        W, H = side, side
         full = synthetic.render_slide(W, H, 7, tissue_fraction=0.5)
         tgt = pb.fit(pb.DeviceSource(synthetic.render_slide(1024, 1024, 8, tissue_fraction=0.6)))
         r0, rows = rank * (H // world), H // world
@@ -185,8 +185,9 @@ def _fused_worker(rank, world, port, q, backend="gloo"):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("side", [4096, 1024])      # calibrated bound / analytic bound
 @pytest.mark.parametrize("backend", BACKENDS)
-def test_rowband_fit_transform_device_built(backend):
+def test_rowband_fit_transform_device_built(backend, side):
     """RowBandGroup.fit_transform (device-built parameters, calibration split
     across the ranks) gives each rank the bytes of the single-process
     normalize and the same fit as RowBandGroup.fit."""
@@ -195,7 +196,8 @@ def test_rowband_fit_transform_device_built(backend):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_fused_worker, args=(r, 2, port, q, backend)) for r in range(2)]
+    ps = [ctx.Process(target=_fused_worker, args=(r, 2, port, q, backend, side))
+          for r in range(2)]
     for p in ps:
         p.start()
     out = [q.get(timeout=300) for _ in ps]
