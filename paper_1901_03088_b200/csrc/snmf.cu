@@ -541,7 +541,8 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
       if (occ_b < 1) occ_b = 1;
     }
   }
-  const bool alt = single && bshape != 0 && nprob >= sms;   // (a few problems: 512 threads each)
+  // (fewer problems than 4 per SM: 512 threads each finish sooner)
+  const bool alt = single && bshape != 0 && nprob >= 4 * sms;
   int nclusters = nprob;
   const int max_clusters = alt ? sms * occ_b : single ? sms * occ1 : (sms * 2) / cluster;
   if (nclusters > max_clusters) nclusters = max_clusters;
