@@ -28,7 +28,12 @@ __device__ __forceinline__ double val_of(uint64_t k) {
   return __longlong_as_double(static_cast<long long>(b));
 }
 
-// keys: values[stride*j + i] for i in [begin, end) — j = component (stain) picked per query
+// keys: values[stride*j + i] for i in [begin, end) — j = component (stain) picked per query.
+// Once the keys sharing the selected prefix fit in shared memory (kSelCand),
+// one more pass gathers them there and the remaining digits are resolved on
+// the copy — two or three passes over the segment instead of six.
+constexpr int kSelCand = 4096;
+
 __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict__ values,
                                                        const SelQuery* __restrict__ qs,
                                                        double* __restrict__ out) {
@@ -37,22 +42,49 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
   __shared__ uint32_t s_scan[kSelThreads];
   __shared__ uint64_t s_prefix;
   __shared__ int64_t s_k;
+  __shared__ uint32_t s_binc;       // keys with the selected prefix
+  __shared__ uint32_t s_ncand;
+  __shared__ uint64_t cand[kSelCand];
   if (threadIdx.x == 0) {
     s_prefix = 0;
     s_k = q.k;
+    s_binc = 0xffffffffu;
   }
   const double* v = values + q.offset;
   int used = 0;  // bits of the prefix fixed so far
+  bool in_smem = false;
+  uint32_t ncand = 0;
   while (used < 64) {
     const int dbits = (64 - used) < kDigit ? (64 - used) : kDigit;
     const int shift = 64 - used - dbits;
     for (int i = threadIdx.x; i < kBins; i += kSelThreads) hist[i] = 0;
     __syncthreads();
     const uint64_t prefix = s_prefix;
-    for (int64_t i = q.begin + threadIdx.x; i < q.end; i += kSelThreads) {
-      const uint64_t key = key_of(v[i]);
-      if (used == 0 || (key >> (64 - used)) == prefix)
-        hist_add_agg(hist, (uint32_t)((key >> shift) & ((1u << dbits) - 1u)));
+    if (!in_smem && used > 0 && s_binc <= (uint32_t)kSelCand) {
+      // gather the keys with this prefix into shared memory (any order: the
+      // histograms below only count)
+      if (threadIdx.x == 0) s_ncand = 0;
+      __syncthreads();
+      for (int64_t i = q.begin + threadIdx.x; i < q.end; i += kSelThreads) {
+        const uint64_t key = key_of(v[i]);
+        if ((key >> (64 - used)) == prefix) cand[atomicAdd(&s_ncand, 1u)] = key;
+      }
+      __syncthreads();
+      ncand = s_ncand;
+      in_smem = true;
+    }
+    if (in_smem) {
+      for (uint32_t i = threadIdx.x; i < ncand; i += kSelThreads) {
+        const uint64_t key = cand[i];
+        if ((key >> (64 - used)) == prefix)
+          atomicAdd(&hist[(uint32_t)((key >> shift) & ((1u << dbits) - 1u))], 1u);
+      }
+    } else {
+      for (int64_t i = q.begin + threadIdx.x; i < q.end; i += kSelThreads) {
+        const uint64_t key = key_of(v[i]);
+        if (used == 0 || (key >> (64 - used)) == prefix)
+          hist_add_agg(hist, (uint32_t)((key >> shift) & ((1u << dbits) - 1u)));
+      }
     }
     __syncthreads();
     // locate the digit holding rank k: per-thread chunk sums + block scan
@@ -79,6 +111,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
         if (k < c + hist[bin]) {
           s_prefix = (prefix << dbits) | (uint64_t)bin;
           s_k = k - c;
+          s_binc = hist[bin];
           break;
         }
         c += hist[bin];
