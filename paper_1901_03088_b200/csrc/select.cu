@@ -33,13 +33,14 @@ __device__ __forceinline__ double val_of(uint64_t k) {
 // one more pass gathers them there and the remaining digits are resolved on
 // the copy — two or three passes over the segment instead of six.
 constexpr int kSelCand = 4096;
+constexpr int kSelQThreads = 1024;   // k_select: one CTA per query, as wide as it goes
 
-__global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict__ values,
+__global__ void __launch_bounds__(kSelQThreads) k_select(const double* __restrict__ values,
                                                        const SelQuery* __restrict__ qs,
                                                        double* __restrict__ out) {
   const SelQuery q = qs[blockIdx.x];
   __shared__ uint32_t hist[kBins];
-  __shared__ uint32_t s_scan[kSelThreads];
+  __shared__ uint32_t s_scan[kSelQThreads];
   __shared__ uint64_t s_prefix;
   __shared__ int64_t s_k;
   __shared__ uint32_t s_binc;       // keys with the selected prefix
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
   while (used < 64) {
     const int dbits = (64 - used) < kDigit ? (64 - used) : kDigit;
     const int shift = 64 - used - dbits;
-    for (int i = threadIdx.x; i < kBins; i += kSelThreads) hist[i] = 0;
+    for (int i = threadIdx.x; i < kBins; i += kSelQThreads) hist[i] = 0;
     __syncthreads();
     const uint64_t prefix = s_prefix;
     if (!in_smem && used > 0 && s_binc <= (uint32_t)kSelCand) {
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
       // histograms below only count)
       if (threadIdx.x == 0) s_ncand = 0;
       __syncthreads();
-      for (int64_t i = q.begin + threadIdx.x; i < q.end; i += kSelThreads) {
+      for (int64_t i = q.begin + threadIdx.x; i < q.end; i += kSelQThreads) {
         const uint64_t key = key_of(v[i]);
         if ((key >> (64 - used)) == prefix) cand[atomicAdd(&s_ncand, 1u)] = key;
       }
@@ -74,13 +75,13 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
       in_smem = true;
     }
     if (in_smem) {
-      for (uint32_t i = threadIdx.x; i < ncand; i += kSelThreads) {
+      for (uint32_t i = threadIdx.x; i < ncand; i += kSelQThreads) {
         const uint64_t key = cand[i];
         if ((key >> (64 - used)) == prefix)
           atomicAdd(&hist[(uint32_t)((key >> shift) & ((1u << dbits) - 1u))], 1u);
       }
     } else {
-      for (int64_t i = q.begin + threadIdx.x; i < q.end; i += kSelThreads) {
+      for (int64_t i = q.begin + threadIdx.x; i < q.end; i += kSelQThreads) {
         const uint64_t key = key_of(v[i]);
         if (used == 0 || (key >> (64 - used)) == prefix)
           hist_add_agg(hist, (uint32_t)((key >> shift) & ((1u << dbits) - 1u)));
@@ -88,13 +89,13 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
     }
     __syncthreads();
     // locate the digit holding rank k: per-thread chunk sums + block scan
-    constexpr int kPer = kBins / kSelThreads;  // 4 bins per thread
+    constexpr int kPer = kBins / kSelQThreads;  // bins per thread
     uint32_t loc = 0;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) loc += hist[threadIdx.x * kPer + j];
     s_scan[threadIdx.x] = loc;
     __syncthreads();
-    for (int off = 1; off < kSelThreads; off <<= 1) {
+    for (int off = 1; off < kSelQThreads; off <<= 1) {
       const uint32_t y = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0u;
       __syncthreads();
       s_scan[threadIdx.x] += y;
@@ -505,7 +506,7 @@ cudaError_t launch_build_queries(const int64_t* b, const int64_t* e, const int64
 cudaError_t launch_select(const double* values, const SelQuery* qs, int nq, double* out,
                           cudaStream_t st) {
   if (nq <= 0) return cudaSuccess;
-  k_select<<<nq, kSelThreads, 0, st>>>(values, qs, out);
+  k_select<<<nq, kSelQThreads, 0, st>>>(values, qs, out);
   return launched();
 }
 
