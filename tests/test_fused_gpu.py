@@ -307,3 +307,35 @@ def test_fused_pair_large_calibrated(monkeypatch):
     monkeypatch.setenv("SPCN_FUSED", "0")
     ref = _quiet(pb.normalize, img, tgt)
     assert torch.equal(out, ref)
+
+
+def test_fused_random_shapes_match_host_path(monkeypatch):
+    """Fuzz: odd shapes (down to a few pixels, blank and near-blank images,
+    odd strides of the output) — the fused normalize and fit + transform with
+    host parameters agree byte for byte, or raise the same error."""
+    import torch
+
+    from paper_1901_03088_b200 import synthetic
+
+    pb = _pb()
+    rng = np.random.default_rng(7)
+    tgt = synthetic.render_slide(300, 260, 5, tissue_fraction=0.6, i0=(250, 243, 230))
+    target = _quiet(pb.fit, pb.DeviceSource(tgt))
+    for trial in range(24):
+        h, w = (int(v) for v in rng.integers(1, 600, size=2))
+        tissue = float(rng.choice([0.0, 0.02, 0.3, 0.7]))
+        img = synthetic.render_slide(w, h, 100 + trial, tissue_fraction=tissue)
+        for tg in (target, tgt):
+            res = {}
+            for mode in ("1", "0"):
+                monkeypatch.setenv("SPCN_FUSED", mode)
+                try:
+                    res[mode] = _quiet(pb.normalize, img, tg)
+                except Exception as exc:      # noqa: BLE001
+                    res[mode] = exc
+            monkeypatch.delenv("SPCN_FUSED")
+            a, b = res["1"], res["0"]
+            if isinstance(b, Exception):
+                assert type(a) is type(b) and str(a) == str(b), (trial, h, w, a, b)
+            else:
+                assert torch.is_tensor(a) and torch.equal(a, b), (trial, h, w)
