@@ -106,7 +106,9 @@ def code_samples(samples, offsets, luts, bases, lam, max_m, max_sweeps=2000):
     return h
 
 
-_BIG_CLUSTER = [16]   # one slide's fit: clusters of 16 CTAs (non-portable), else 8
+# one slide's fit: clusters of 16 CTAs (non-portable), else 8; SPCN_SNMF_CLUSTER
+# overrides (A/B measurements: the cluster size fixes the reduction order)
+_BIG_CLUSTER = [int(__import__("os").environ.get("SPCN_SNMF_CLUSTER", "16"))]
 
 
 def fit_slide(samples, offsets, luts, cfg, m: int, od=None) -> BatchFit:
