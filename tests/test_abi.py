@@ -125,3 +125,26 @@ def test_profile_files_byte_compatible_with_reference(tmp_path):
     out = tmp_path / "ours.txt"
     nz.save_profile(out, p)
     assert out.read_bytes() == open(ref_path, "rb").read()
+
+
+@pytest.mark.gpu
+def test_integration_binding_in_the_reference_transform_loop(monkeypatch):
+    """the reference's transform loop (restated by the
+    oracle: strips through a bounded worker pool, in-order commit) with its
+    per-strip unit swapped for the ctypes binding gives the same bytes."""
+    import integration_binding as ib
+    from oracle import spcn_oracle as orc
+
+    px, _, _ = orc.render(700, 530, 21, tissue_fraction=0.6)
+    tg, _, _ = orc.render(400, 400, 22, tissue_fraction=0.6, i0=(250, 243, 230))
+    src, tgt = orc.fit_params(px), orc.fit_params(tg)
+    ref = orc.run_transform(px, src, tgt, strip_height=128, workers=3)
+    table = orc.od_table(src["i0"])
+
+    def gpu_strip(strip, s, t, f, code_lam=0.0):
+        return ib.process_strip_gpu(strip, s["i0"], s["basis"], code_lam, f, t["basis"],
+                                    t["i0"], table)
+
+    monkeypatch.setattr(orc, "recolor_strip", gpu_strip)
+    got = orc.run_transform(px, src, tgt, strip_height=128, workers=3)
+    assert np.array_equal(got, ref)
