@@ -194,24 +194,43 @@ __global__ void __launch_bounds__(32 * kBW, 1)
 // shared memory and its Gram factors formed once; if the segment overflowed
 // the CTA's list, every pixel of the item is recomputed instead.  Exact
 // either way (strict_pixel = the reference's operation order).
-__global__ void __launch_bounds__(256) k_repair_items(const uint8_t* __restrict__ src,
-                                                      uint8_t* __restrict__ dst,
-                                                      const StrictP* __restrict__ sps,
-                                                      const int64_t* __restrict__ off,
-                                                      const int32_t* __restrict__ status,
-                                                      int nitems, BatchRepair br) {
+// Per item, the uncertified pixels' colours are deduplicated first: the
+// certification outcome is a function of the colour, so a colour that fails
+// fails for every pixel that has it, and the list repeats colours about as
+// often as the item does (~10x).  Phase 1 inserts the list's colours into a
+// shared-memory table, phase 2 evaluates each distinct colour once in fp64,
+// phase 3 writes every listed pixel from the table (colours that did not fit
+// in the table are evaluated directly) — the same bytes, a fraction of the
+// fp64 work.
+constexpr int kRepThreads = 512;
+constexpr int kRepBits = 13, kRepSlots = 1 << kRepBits;
+constexpr uint32_t kRepEmpty = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t rep_slot(uint32_t rgb) {
+  return (rgb * 2654435761u) >> (32 - kRepBits);
+}
+
+__global__ void __launch_bounds__(kRepThreads) k_repair_items(const uint8_t* __restrict__ src,
+                                                              uint8_t* __restrict__ dst,
+                                                              const StrictP* __restrict__ sps,
+                                                              const int64_t* __restrict__ off,
+                                                              const int32_t* __restrict__ status,
+                                                              int nitems, BatchRepair br) {
   const int it = blockIdx.x;
   if (it >= nitems || status[it] != 0) return;
   const unsigned long long s0 = br.seg[3 * it], s1 = br.seg[3 * it + 1];
   if (s1 <= s0) return;                               // nothing to repair
 
   __shared__ double lut[3 * 256];
+  extern __shared__ uint32_t rtab[];                  // keys [kRepSlots] | outputs [kRepSlots]
+  uint32_t* rkey = rtab;
+  uint32_t* rout = rtab + kRepSlots;
   const StrictP& sp = sps[it];
-  for (int i = threadIdx.x; i < 3 * 256; i += 256) lut[i] = sp.lut[i >> 8][i & 255];
-  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * 256; i += kRepThreads) lut[i] = sp.lut[i >> 8][i & 255];
   const NnlsGram G = gram_of(sp);
   if (s1 > br.cap_cta) {                              // the list overflowed: whole item
-    for (int64_t i = off[it] + threadIdx.x; i < off[it + 1]; i += 256) {
+    __syncthreads();
+    for (int64_t i = off[it] + threadIdx.x; i < off[it + 1]; i += kRepThreads) {
       const uint32_t out = strict_pixel(sp, G, SmemLut{lut}, src[3 * i], src[3 * i + 1],
                                         src[3 * i + 2]);
       dst[3 * i] = out & 255u;
@@ -220,12 +239,44 @@ __global__ void __launch_bounds__(256) k_repair_items(const uint8_t* __restrict_
     }
     return;
   }
+  for (int i = threadIdx.x; i < kRepSlots; i += kRepThreads) rkey[i] = kRepEmpty;
+  __syncthreads();
   const unsigned long long* items = br.items + (size_t)br.seg[3 * it + 2] * br.cap_cta;
-  for (unsigned long long i = s0 + threadIdx.x; i < s1; i += 256) {
+  // phase 1: distinct colours of the list (a colour that finds no slot within
+  // 32 probes is evaluated directly in phase 3)
+  for (unsigned long long i = s0 + threadIdx.x; i < s1; i += kRepThreads) {
+    const uint32_t rgb = static_cast<uint32_t>(items[i] & 0xffffffu);
+    uint32_t sl = rep_slot(rgb);
+    for (int probe = 0; probe < 32; ++probe, sl = (sl + 1) & (kRepSlots - 1)) {
+      const uint32_t k = atomicCAS(&rkey[sl], kRepEmpty, rgb);
+      if (k == kRepEmpty || k == rgb) break;
+    }
+  }
+  __syncthreads();
+  // phase 2: one fp64 evaluation per distinct colour
+  for (int i = threadIdx.x; i < kRepSlots; i += kRepThreads) {
+    const uint32_t rgb = rkey[i];
+    if (rgb != kRepEmpty)
+      rout[i] = strict_pixel(sp, G, SmemLut{lut}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
+  }
+  __syncthreads();
+  // phase 3: every listed pixel from the table
+  for (unsigned long long i = s0 + threadIdx.x; i < s1; i += kRepThreads) {
     const unsigned long long v = items[i];
     const uint32_t rgb = static_cast<uint32_t>(v & 0xffffffu);
     const int64_t gp = static_cast<int64_t>(v >> 24);
-    const uint32_t out = strict_pixel(sp, G, SmemLut{lut}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
+    uint32_t sl = rep_slot(rgb), out = 0;
+    bool hit = false;
+    for (int probe = 0; probe < 32; ++probe, sl = (sl + 1) & (kRepSlots - 1)) {
+      const uint32_t k = rkey[sl];
+      if (k == rgb) {
+        out = rout[sl];
+        hit = true;
+        break;
+      }
+      if (k == kRepEmpty) break;
+    }
+    if (!hit) out = strict_pixel(sp, G, SmemLut{lut}, rgb & 255u, (rgb >> 8) & 255u, rgb >> 16);
     dst[3 * gp] = out & 255u;
     dst[3 * gp + 1] = (out >> 8) & 255u;
     dst[3 * gp + 2] = (out >> 16) & 255u;
@@ -307,7 +358,15 @@ cudaError_t launch_repair_items(const uint8_t* src, uint8_t* dst, const StrictP*
                                 const int64_t* off, const int32_t* status, int nitems,
                                 const BatchRepair& br, cudaStream_t st) {
   if (nitems <= 0) return cudaSuccess;
-  k_repair_items<<<nitems, 256, 0, st>>>(src, dst, sps, off, status, nitems, br);
+  constexpr int kSmem = 2 * kRepSlots * sizeof(uint32_t);
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(k_repair_items,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_repair_items<<<nitems, kRepThreads, kSmem, st>>>(src, dst, sps, off, status, nitems, br);
   return launched();
 }
 
