@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(32 * kBW, 1)
 // phase 3 writes every listed pixel from the table (colours that did not fit
 // in the table are evaluated directly) — the same bytes, a fraction of the
 // fp64 work.
-constexpr int kRepThreads = 512;
+constexpr int kRepThreads = 1024;
 constexpr int kRepBits = 13, kRepSlots = 1 << kRepBits;
 constexpr uint32_t kRepEmpty = 0xffffffffu;
 
