@@ -168,8 +168,28 @@ __device__ __forceinline__ uint32_t recolor_pair(const FastS& fp, const uint8_t*
     or_if_pairs_differ(*badpairs, 1u << (k >> 1), lo, hi);
     return 0u;
   }
+  if (MODE == 0) {
+    // analytic per-pixel bound: alpha of both pixels in one FFMA2, then per
+    // channel the interval ends of BOTH pixels (lo pair, hi pair: two FFMA2.RD
+    // with the same element operations as cert_interval), their roundings in
+    // two FFMA2 and the compare as in MODE 2 (no per-pixel operand shuffles)
+    const float2 alpha = __ffma2_rn(bc2(fp.a1), fq.T, bc2(fp.a0));
+    float2 lo[3], hi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float2 pw = make_float2(ex2_approx(e[c][0]), ex2_approx(e[c][1]));
+      const float2 ilo = __ffma2_rd(bc2(-fp.i0t[c]), alpha, bc2(fp.i0t[c]));
+      const float2 ihi = __ffma2_rd(bc2(fp.i0t[c]), alpha, bc2(fp.i0t[c]));
+      lo[c] = __ffma2_rn(ilo, pw, bc2(kMagic));
+      hi[c] = __ffma2_rn(ihi, pw, bc2(kMagic));
+      ob[a + c] = __float_as_uint(hi[c].x);
+      ob[b + c] = __float_as_uint(hi[c].y);
+    }
+    uint32_t bad = 0;
+    or_if_pairs_differ(bad, 1u, lo, hi);
+    return bad;
+  }
   float2 alpha = bc2(0.f);
-  if (MODE == 0) alpha = __ffma2_rn(bc2(fp.a1), fq.T, bc2(fp.a0));
   uint32_t bad = 0;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
