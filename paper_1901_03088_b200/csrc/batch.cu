@@ -27,11 +27,12 @@ namespace spcn {
 constexpr int kBW = 16;                      // warps per CTA
 constexpr int kBNSW = 3;                     // ring slots per warp
 constexpr int kBNSub = 2;                    // 512-px sub-slices per slot
-constexpr int kBRep = 16;                    // OD table replicas
+constexpr int kBRep = 24;                    // OD table replicas (mixed layout, recolor.cuh)
+constexpr uint32_t kBAbs = 4096;             // absolute shared address of the OD table
 constexpr int kBSlicePx = 512 * kBNSub;
 constexpr int kBSlotBytes = 3 * kBSlicePx;
 constexpr int kBLut = LutLayout<kBRep>::kBytes;
-constexpr size_t kBSmem = kBLut + (size_t)kBW * kBNSW * kBSlotBytes + kBW * kBNSW * 8;
+constexpr size_t kBSmem = kBAbs + kBLut + (size_t)kBW * kBNSW * kBSlotBytes + kBW * kBNSW * 8;
 static_assert(kBSmem <= 227 * 1024, "shared memory budget");
 
 __device__ __forceinline__ int64_t bmin64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -99,7 +100,10 @@ __global__ void __launch_bounds__(32 * kBW, 1)
   // items it recolours leave contiguous segments of it, recorded per item
   // for k_repair_items
   RepairList rl{br.counts + blockIdx.x, br.items + (size_t)blockIdx.x * br.cap_cta, br.cap_cta};
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  if (wbase > kBAbs) __trap();                 // layout assumption (window base <= 4 KB)
+  uint8_t* smem = smem_raw + (kBAbs - wbase);  // the OD table at absolute kBAbs
   const uint8_t* lut = smem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* myslots = smem + kBLut + (size_t)warp * kBNSW * kBSlotBytes;
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(32 * kBW, 1)
       uint8_t* sbase = myslots + q * kBSlotBytes;
 #pragma unroll
       for (int u = 0; u < kBNSub; ++u)
-        recolor_block<MODE>(fp, lut, lc, sbase + u * 1536 + 48 * lane, u * 512 + 16 * lane < n,
+        recolor_block<MODE, kBAbs>(fp, lut, lc, sbase + u * 1536 + 48 * lane, u * 512 + 16 * lane < n,
                             base + j * kBSlicePx + u * 512 + 16 * lane, rl, lane, fp.I);
       fence_proxy_async_smem();
       __syncwarp();
