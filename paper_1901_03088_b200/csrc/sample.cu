@@ -128,6 +128,9 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
   __shared__ int scratch[kSThreads / 32][4];
   __shared__ int s_hist[3][256];
   __shared__ int s_wsum[kSThreads / 32][4];
+  // the chunk's taken non-white pixels, staged in rank order (they are one
+  // contiguous run of the output) and written with coalesced word stores
+  __shared__ __align__(16) uint32_t s_stage[(3 * kChunk) / 4 + 2];
   // prefix over earlier chunks of this patch
   int pre[4] = {0, 0, 0, 0};
   for (int j = threadIdx.x; j < k; j += kSThreads) {
@@ -186,13 +189,15 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
     for (int w = 0; w < warp; ++w) wpre += s_wsum[w][q];
     rank[q] = s_pre[q] + wpre + inc[q] - cnt[q];
   }
+  const int blk_r0 = s_pre[0];                 // the chunk's first non-white rank
+  uint8_t* stage = reinterpret_cast<uint8_t*>(s_stage);
 #pragma unroll
   for (int j = 0; j < kPerThread; ++j) {
     if (rgb[j] == 0xffffffffu) continue;
     const int a = rgb[j] & 255, b = (rgb[j] >> 8) & 255, d = (rgb[j] >> 16) & 255;
     if (!(a > thr && b > thr && d > thr)) {
       if (rank[0] < tk.take_nonwhite) {
-        uint8_t* o = out_px + 3 * (tk.out_base + rank[0]);
+        uint8_t* o = stage + 3 * (rank[0] - blk_r0);
         o[0] = a; o[1] = b; o[2] = d;
       }
       ++rank[0];
@@ -202,6 +207,23 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
     if (d > thr) { if (rank[3] < tk.take_bright[2]) atomicAdd(&s_hist[2][d], 1); ++rank[3]; }
   }
   __syncthreads();
+  {   // the staged run [blk_r0, min(take, blk_r0 + chunk non-white)) to the output
+    int blk_nw = 0;
+    for (int w = 0; w < kSThreads / 32; ++w) blk_nw += s_wsum[w][0];
+    const int64_t t1 = min((int64_t)tk.take_nonwhite, (int64_t)blk_r0 + blk_nw);
+    const int nb = t1 > blk_r0 ? (int)(3 * (t1 - blk_r0)) : 0;
+    uint8_t* dstb = out_px + 3 * (tk.out_base + blk_r0);
+    const int head = min(nb, (int)((4u - (reinterpret_cast<uintptr_t>(dstb) & 3u)) & 3u));
+    if (threadIdx.x < head) dstb[threadIdx.x] = stage[threadIdx.x];
+    const int nw = (nb - head) >> 2, sh = 8 * (head & 3);
+    uint32_t* dw = reinterpret_cast<uint32_t*>(dstb + head);
+    for (int w = threadIdx.x; w < nw; w += kSThreads) {
+      const int q = (head >> 2) + w;               // source word index (offset head + 4w)
+      dw[w] = sh ? __funnelshift_r(s_stage[q], s_stage[q + 1], sh) : s_stage[q];
+    }
+    const int tail0 = head + 4 * nw;
+    if (threadIdx.x < nb - tail0) dstb[tail0 + threadIdx.x] = stage[tail0 + threadIdx.x];
+  }
   int32_t* gh = bright_hist + (int64_t)tk.problem * 3 * 256;
   for (int i = threadIdx.x; i < 3 * 256; i += kSThreads) {
     const int v = (&s_hist[0][0])[i];
