@@ -7,6 +7,7 @@ sample of RGB8 pixels plus its OD table, solved by one thread-block cluster.
 from __future__ import annotations
 
 import ctypes
+import functools
 import warnings
 
 import numpy as np
@@ -39,6 +40,11 @@ def _sig():
 
 def initial_basis(seed: int) -> np.ndarray:
     """The reference initializer (src/stain_sep.py:271-274), evaluated with numpy."""
+    return _initial_basis(int(seed)).copy()
+
+
+@functools.lru_cache(maxsize=64)
+def _initial_basis(seed: int) -> np.ndarray:    # a pure function of the seed
     from .stain_sep import reference_basis
 
     w = reference_basis() + np.random.default_rng(seed).uniform(0.0, 0.05, size=(3, 2))
