@@ -555,6 +555,7 @@ cudaError_t launch_p99(const double* h, int64_t total, const int64_t* seg, int n
 // k_p99_combine.
 constexpr int kWThreads = 512;
 constexpr int kWCap = 12288;   // entries staged in shared memory (k_colour_table's fill limit)
+constexpr bool kWStage = false;   // with the candidate gather, 3-4 passes read L2 directly
 
 __device__ __forceinline__ unsigned long long wkey(double x) {
   const unsigned long long b = __double_as_longlong(x);
@@ -571,6 +572,12 @@ __global__ void __launch_bounds__(kWThreads) k_p99_weighted(
   __shared__ unsigned long long s_red[kWThreads / 32];
   __shared__ unsigned long long s_bc[2];   // chosen prefix, remaining rank
   __shared__ uint32_t s_binw;
+  // entries sharing the first two digits with the selected rank: after two
+  // passes they are gathered here and the last six digits only visit them
+  constexpr int kWCand = 1024;
+  __shared__ unsigned long long c_key[kWCand];
+  __shared__ uint32_t c_w[kWCand];
+  __shared__ int s_nc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
     const int64_t o0 = seg[sg], n = seg[sg + 1] - o0;
@@ -586,7 +593,7 @@ __global__ void __launch_bounds__(kWThreads) k_p99_weighted(
       }
       const double* hv = h + (int64_t)j * total + o0;
       const uint32_t* wv = w + o0;
-      const bool staged = ne <= kWCap;
+      const bool staged = kWStage && ne <= kWCap;
       if (staged)
         for (int i = tid; i < ne; i += kWThreads) {
           s_key[i] = wkey(hv[i]);
@@ -618,13 +625,22 @@ __global__ void __launch_bounds__(kWThreads) k_p99_weighted(
       // weight of entries equal to it, s_bc[1] = k's rank among them
       auto select = [&](int64_t k) {
         unsigned long long prefix = 0;
+        bool cand = false;
+        int nc = 0;
         for (int shift = 56; shift >= 0; shift -= 8) {
           if (tid < 256) hist[tid] = 0;
           __syncthreads();
           const unsigned long long mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
-          for (int i = tid; i < ne; i += kWThreads) {
-            const unsigned long long kk = key_at(i);
-            if ((kk & mask) == prefix) atomicAdd(&hist[(kk >> shift) & 255u], w_at(i));
+          if (cand) {
+            for (int i = tid; i < nc; i += kWThreads) {
+              const unsigned long long kk = c_key[i];
+              if ((kk & mask) == prefix) atomicAdd(&hist[(kk >> shift) & 255u], c_w[i]);
+            }
+          } else {
+            for (int i = tid; i < ne; i += kWThreads) {
+              const unsigned long long kk = key_at(i);
+              if ((kk & mask) == prefix) atomicAdd(&hist[(kk >> shift) & 255u], w_at(i));
+            }
           }
           __syncthreads();
           if (warp == 0) {   // warp scan of 256 bins (8 per lane)
@@ -652,6 +668,24 @@ __global__ void __launch_bounds__(kWThreads) k_p99_weighted(
           prefix = s_bc[0];
           k = (int64_t)s_bc[1];
           __syncthreads();
+          if (!cand && shift == 48) {   // gather the entries with this 16-bit prefix
+            if (tid == 0) s_nc = 0;
+            __syncthreads();
+            for (int i = tid; i < ne; i += kWThreads) {
+              const unsigned long long kk = key_at(i);
+              if ((kk & (~0ull << 48)) == prefix) {
+                const int j = atomicAdd(&s_nc, 1);
+                if (j < kWCand) {
+                  c_key[j] = kk;
+                  c_w[j] = w_at(i);
+                }
+              }
+            }
+            __syncthreads();
+            nc = s_nc;
+            cand = nc <= kWCand;      // (more: keep scanning every entry)
+            __syncthreads();
+          }
         }
         return prefix;
       };
@@ -687,7 +721,7 @@ cudaError_t launch_p99_weighted(const double* h, int64_t total, const uint32_t* 
                                 const int32_t* ucount, const int64_t* seg, int nseg, double p,
                                 double* p99, int32_t* absent, cudaStream_t st) {
   if (nseg <= 0) return cudaSuccess;
-  constexpr int smem = kWCap * (8 + 4);
+  constexpr int smem = kWStage ? kWCap * (8 + 4) : 0;
   static bool attr = false;
   if (!attr) {
     const cudaError_t e =
@@ -698,7 +732,7 @@ cudaError_t launch_p99_weighted(const double* h, int64_t total, const uint32_t* 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int g = nseg < 2 * sms ? nseg : 2 * sms;
+  const int g = nseg < 4 * sms ? nseg : 4 * sms;
   k_p99_weighted<<<g, kWThreads, smem, st>>>(h, total, w, ucount, seg, nseg, p, p99, absent);
   return launched();
 }
