@@ -148,6 +148,17 @@ int spcn_sample_count(const uint8_t* img, const spcn_patch* patches, int32_t npa
                       int32_t max_chunks, int32_t white_threshold, int32_t* counts,
                       void* stream);
 
+/* One-patch items (every item's candidate grid is one patch, e.g. a batch of
+ * 512^2 tiles with patch_size 1000): the visit rules of src/pipeline.py:
+ * 156-184 per item from the chunk counts of spcn_sample_count — non-white
+ * take = min(total, target) if total >= used_min (the background cutoff
+ * times the patch area) else 0, bright takes = min(total, cap) — and the
+ * sample offsets as an exclusive scan of the takes: the take rows
+ * spcn_sample_compact reads, and take_nw[i] (device) for the read-back.   */
+int spcn_visit_single(const int32_t* counts, int32_t n, int32_t chunks, double used_min,
+                      int64_t target, int64_t cap, spcn_patch_take* takes, int64_t* take_nw,
+                      void* stream);
+
 /* Ordered compaction of the decided takes: the first take_nonwhite non-white
  * pixels of each patch (raster order) → out_px[out_base ...] (RGB8), and the
  * first take_bright[c] values > thr of channel c → bright_hist[problem][c][v]

@@ -42,7 +42,7 @@ EXPORTS = (
     "spcn_readback", "spcn_last_error", "spcn_version", "spcn_launch_count", "spcn_xform_shape",
     "spcn_xform_timing_enable", "spcn_xform_timing", "spcn_stream_sync",
     "spcn_fit_sample_step", "spcn_fit_basis_step", "spcn_xform_rgb8_fitted",
-    "spcn_xform_fitted_prepare", "spcn_xform_fitted_run",
+    "spcn_xform_fitted_prepare", "spcn_xform_fitted_run", "spcn_visit_single",
 )
 
 

@@ -202,22 +202,19 @@ def _compact_i0(imgs, n, ncand, d_desc, counts, chunks, thr, d_tk, sample, extra
 def _fit_batch_single_patch(imgs, n, rect, d_desc, counts, chunks, thr, plan, cfg, code_lam):
     """fit_batch for a one-candidate grid (every item is one patch, e.g. 512²
     tiles with patch_size 1000): the reference's visit rules
-    (src/pipeline.py:156-184) reduce to per-item elementwise ones, evaluated on
-    the device, so the counts are never read back — the compaction follows
-    the count pass directly; the take sizes come back with i0."""
+    (src/pipeline.py:156-184) reduce to per-item ones, evaluated on the device
+    (spcn_visit_single), so the counts are never read back — the compaction
+    follows the count pass directly; the take sizes come back with i0."""
     t = _dev.torch()
     dev = imgs.device
     npx = rect[2] * rect[3]
     min_frac = 1.0 - plan.background_fraction_cutoff
-    tot = counts.sum(dim=1, dtype=t.int64)                       # (n, 4)
-    take_b = t.clamp(tot[:, 1:], max=plan.sample_cap)
-    used = tot[:, 0].to(t.float64) >= min_frac * npx
-    take_nw = t.where(used, t.clamp(tot[:, 0], max=plan.target_pixels), t.zeros_like(tot[:, 0]))
-    base = t.cumsum(take_nw, 0) - take_nw
     tk = t.empty((n, 8), dtype=t.int32, device=dev)               # TAKE_DT rows (32 B)
-    tk[:, 0:4] = t.stack([take_nw, base], 1).view(t.int32)
-    tk[:, 4:7] = take_b.to(t.int32)
-    tk[:, 7] = t.arange(n, dtype=t.int32, device=dev)
+    take_nw = t.empty(n, dtype=t.int64, device=dev)
+    L = _lib_sample()
+    _lib.check(L.spcn_visit_single(_lib.ptr(counts), n, int(counts.shape[1]), min_frac * npx,
+                                   int(plan.target_pixels), int(plan.sample_cap), _lib.ptr(tk),
+                                   _lib.ptr(take_nw), _lib.stream_handle()), "visit_single")
     # the sample at its largest (every item taking target_pixels): no read of
     # the totals before the compaction
     sample = t.empty((max(1, n * min(plan.target_pixels, npx)), 3), dtype=t.uint8, device=dev)

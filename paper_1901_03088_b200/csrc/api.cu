@@ -632,6 +632,19 @@ int spcn_sample_count(const uint8_t* img, const spcn_patch* patches, int32_t npa
   return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "sample_count");
 }
 
+int spcn_visit_single(const int32_t* counts, int32_t n, int32_t chunks, double used_min,
+                      int64_t target, int64_t cap, spcn_patch_take* takes, int64_t* take_nw,
+                      void* stream) {
+  g_err.clear();
+  if (n < 0 || chunks < 1) return fail(SPCN_EINVAL, "bad size");
+  if (n == 0) return SPCN_OK;
+  if (!counts || !takes || !take_nw) return fail(SPCN_EINVAL, "NULL argument");
+  if (target < 0 || cap < 0) return fail(SPCN_EINVAL, "negative take");
+  cudaError_t e = launch_visit_single(counts, n, chunks, used_min, target, cap, takes, take_nw,
+                                      static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPCN_OK : cuda_fail(e, "visit_single");
+}
+
 int spcn_sample_compact(const uint8_t* img, const spcn_patch* patches, int32_t npatches,
                         int32_t max_chunks, int32_t white_threshold, const int32_t* counts,
                         const spcn_patch_take* takes, uint8_t* out_px, int32_t* bright_hist,

@@ -295,6 +295,79 @@ __global__ void k_od_tables(const double* __restrict__ i0, int nprob, double* __
   lut[idx] = log(__ddiv_rn(a, x));
 }
 
+// One-patch items (a batch of tiles smaller than a patch): the reference's
+// visit rules (src/pipeline.py:156-184) reduce to per-item ones — take the
+// first min(non-white, target) non-white pixels if the non-white count
+// reaches the background cutoff, and the first min(bright, cap) bright
+// values per channel — and the sample offsets are an exclusive scan of the
+// takes.  One CTA: totals per item from the chunk counts, the rules, a
+// running block scan, the take rows and the per-item non-white takes.
+constexpr int kVS = 1024;
+
+// item totals, one warp per item, parked in the item's 32-byte take row
+__global__ void __launch_bounds__(256) k_visit_totals(const int32_t* __restrict__ counts, int n,
+                                                      int chunks, int64_t* __restrict__ rows) {
+  const int item = (int)((blockIdx.x * 256ll + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (item >= n) return;
+  int64_t t[4] = {0, 0, 0, 0};
+  for (int c = lane; c < chunks; c += 32)
+    for (int q = 0; q < 4; ++q) t[q] += counts[((int64_t)item * chunks + c) * 4 + q];
+  for (int q = 0; q < 4; ++q)
+    for (int off = 16; off; off >>= 1) t[q] += __shfl_xor_sync(0xffffffffu, t[q], off);
+  if (lane < 4) rows[4 * (int64_t)item + lane] = t[lane];
+}
+
+__global__ void __launch_bounds__(kVS) k_visit_single(const int32_t* __restrict__ counts, int n,
+                                                      int chunks, double used_min, int64_t target,
+                                                      int64_t cap, spcn_patch_take* __restrict__ takes,
+                                                      int64_t* __restrict__ take_nw) {
+  __shared__ int64_t s_scan[kVS];
+  __shared__ int64_t s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += kVS) {
+    const int i = i0 + threadIdx.x;
+    int64_t tot[4] = {0, 0, 0, 0};
+    if (i < n)
+      for (int q = 0; q < 4; ++q) tot[q] = reinterpret_cast<const int64_t*>(takes)[4 * (int64_t)i + q];
+    const bool used = (double)tot[0] >= used_min;
+    const int64_t nw = (i < n && used) ? (tot[0] < target ? tot[0] : target) : 0;
+    s_scan[threadIdx.x] = nw;
+    __syncthreads();
+    for (int off = 1; off < kVS; off <<= 1) {           // inclusive block scan
+      const int64_t y = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0;
+      __syncthreads();
+      s_scan[threadIdx.x] += y;
+      __syncthreads();
+    }
+    const int64_t base = s_carry + s_scan[threadIdx.x] - nw;
+    if (i < n) {
+      spcn_patch_take t;
+      t.take_nonwhite = nw;
+      t.out_base = base;
+      for (int q = 0; q < 3; ++q) t.take_bright[q] = (int32_t)(tot[1 + q] < cap ? tot[1 + q] : cap);
+      t.problem = i;
+      takes[i] = t;
+      take_nw[i] = nw;
+    }
+    __syncthreads();
+    if (threadIdx.x == kVS - 1) s_carry += s_scan[kVS - 1];
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_visit_single(const int32_t* counts, int n, int chunks, double used_min,
+                                int64_t target, int64_t cap, spcn_patch_take* takes,
+                                int64_t* take_nw, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_visit_totals<<<(unsigned)((n * 32ll + 255) / 256), 256, 0, st>>>(
+      counts, n, chunks, reinterpret_cast<int64_t*>(takes));
+  cudaError_t e = launched();
+  if (e != cudaSuccess) return e;
+  k_visit_single<<<1, kVS, 0, st>>>(counts, n, chunks, used_min, target, cap, takes, take_nw);
+  return launched();
+}
+
 cudaError_t launch_sample_count(const uint8_t* img, const spcn_patch* patches, int npatches,
                                 int max_chunks, int thr, int32_t* counts, cudaStream_t st) {
   if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;

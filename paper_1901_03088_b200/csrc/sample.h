@@ -5,6 +5,9 @@
 #include "spcn.h"
 
 namespace spcn {
+cudaError_t launch_visit_single(const int32_t* counts, int n, int chunks, double used_min,
+                                int64_t target, int64_t cap, spcn_patch_take* takes,
+                                int64_t* take_nw, cudaStream_t st);
 cudaError_t launch_sample_count(const uint8_t* img, const spcn_patch* patches, int npatches,
                                 int max_chunks, int thr, int32_t* counts, cudaStream_t st);
 cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches, int npatches,

@@ -132,6 +132,8 @@ def _lib_sample():
         _lib.declare("spcn_sample_compact", _lib.ctypes.c_int, [P, P, I32, I32, I32, P, P, P, P, P])
         _lib.declare("spcn_i0_from_hist", _lib.ctypes.c_int, [P, I32, P, P, P])
         _lib.declare("spcn_od_tables", _lib.ctypes.c_int, [P, I32, P, P])
+        _lib.declare("spcn_visit_single", _lib.ctypes.c_int,
+                     [P, I32, I32, _lib.DBL, _lib.I64, _lib.I64, P, P, P])
         L._spcn_sample_declared = True
     return L
 
