@@ -954,7 +954,7 @@ def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
     """The drop-in entry: fit(source), fit(target) (or use a FitParams / profile
     for the target), then transform — exactly the reference's _normalize_one
     (src/cli.py:220-244).  numpy in → numpy out; CUDA tensor in → CUDA tensor
-    out (written into ``out`` when given).  A resident slide with a pooled
+    out (written into ``out`` when given, of the matching kind).  A resident slide with a pooled
     p99 and EXACT precision runs as fit_transform_resident (no host round
     trip between the fit and the recolour; same bytes).  A host image small
     enough (≤ WHOLE_UPLOAD_PIXELS) is uploaded whole and takes the device
@@ -965,7 +965,15 @@ def normalize(source, target, *, plan: SamplePlan = SamplePlan(),
     t = _dev.torch()
     stats = stats if stats is not None else RunStats()
     host = not _dev.is_tensor(source)
-    if host and out is None and _whole_upload_ok(source, target):
+    if host and out is not None:          # host image, caller's host buffer
+        res = normalize(source, target, plan=plan, cfg=cfg, code_lam=code_lam,
+                        per_patch_stats=per_patch_stats, strip_height=strip_height,
+                        precision=precision, stats=stats, p99_mode=p99_mode)
+        if tuple(np.shape(out)) != tuple(res.shape):
+            raise ValueError("out must have the source's shape")
+        np.copyto(out, res)
+        return out
+    if host and _whole_upload_ok(source, target):
         dev_t = target
         if isinstance(target, np.ndarray):
             dev_t = t.from_numpy(np.ascontiguousarray(target)).cuda()
