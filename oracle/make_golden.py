@@ -243,8 +243,37 @@ def make_profile_fixture(out_dir):
     rn.save_profile(os.path.join(out_dir, "profile_ref.txt"), w)
 
 
+PNG_SHAPE, PNG_STRIP, PNG_SEED = (37, 53), 10, 2024
+
+
+def png_pixels():
+    """The pixels of the PNG fixture (regenerated by the test)."""
+    h, w = PNG_SHAPE
+    return np.random.default_rng(PNG_SEED).integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+
+
+def make_png_fixture(out_dir):
+    """A PNG written strip by strip by the reference's own streaming encoder
+    (PngStripWriter, src/image_io.py:316-358), for the byte-level parity of
+    ours and of our reader."""
+    import importlib
+
+    from slidenorm.image_io import PixelBlock
+
+    rio = importlib.import_module("slidenorm.image_io")
+    px = png_pixels()
+    h, w = PNG_SHAPE
+    wr = rio.PngStripWriter(os.path.join(out_dir, "png_ref_strips.png"), w, h)
+    for y in range(0, h, PNG_STRIP):
+        wr.write_strip(PixelBlock(0, y, px[y:y + PNG_STRIP]))
+    wr.close()
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--png" in sys.argv:
+        make_png_fixture(OUT)
+        return
     for name, fn in [("optics", optics_fixture), ("coder", coder_fixture),
                      ("pct", pct_fixture), ("snmf", snmf_fixture),
                      ("slides", slide_fixture), ("c1", c1_fixture)]:
@@ -253,6 +282,7 @@ def main():
         np.savez_compressed(path, **data)
         print(f"{path}: {os.path.getsize(path) / 1e6:.2f} MB")
     make_profile_fixture(OUT)
+    make_png_fixture(OUT)
 
 
 if __name__ == "__main__":

@@ -184,3 +184,23 @@ def test_png_strip_writer_streams_with_bounded_memory(tmp_path):
     assert np.array_equal(np.asarray(Image.open(path)), img)
     with pytest.raises(OSError):
         io.open_writer(tmp_path / "missing" / "x.png", 10, 10)
+
+
+def test_png_bytes_equal_the_reference_writer(tmp_path):
+    """A PNG written strip by strip is byte-identical to the one the
+    reference's own PngStripWriter wrote (tests/golden/png_ref_strips.png,
+    oracle/make_golden.py --png), and reads back to the same pixels."""
+    import numpy as np
+
+    from paper_1901_03088_b200 import image_io as io
+
+    golden = os.path.join(os.path.dirname(__file__), "golden", "png_ref_strips.png")
+    h, w = 37, 53
+    px = np.random.default_rng(2024).integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+    path = tmp_path / "ours.png"
+    with io.open_writer(path, w, h) as wr:
+        for y in range(0, h, 10):
+            wr.write_strip(io.PixelBlock(0, y, px[y:y + 10]))
+    assert open(path, "rb").read() == open(golden, "rb").read()
+    src = io.open_slide(golden)                 # our reader on the reference's file
+    assert np.array_equal(np.asarray(src.read_region(0, 0, w, h).pixels), px)
