@@ -723,7 +723,7 @@ def run_ours(args, rank, world, local):
     # ---- end-to-end through the public API with pinned host buffers
     if not args.no_e2e:
         try:
-            line["e2e"] = e2e(args, pb, slide, target, rank, world)
+            line["e2e"] = e2e(args, pb, slide, target, rank, world, group)
         except Exception as exc:  # pragma: no cover
             line["e2e"] = {"value": None, "unit": "Mpx/s", "error": repr(exc)[:200]}
     # ---- CPU baseline (rank 0, N = 1 only)
@@ -739,9 +739,16 @@ def run_ours(args, rank, world, local):
     return 0
 
 
-def e2e(args, pb, slide, target, rank, world):
-    """Same metric through pb.fit/pb.transform with host (pinned) input and output."""
+def e2e(args, pb, slide, target, rank, world, group=None):
+    """Same metric through pb.fit/pb.transform with host (pinned) input and output.
+    N > 1: the whole slide's fit is a collective over the row bands
+    (RowBandGroup), which reads resident bands, so each rank uploads its band
+    (pinned, timed), runs RowBandGroup.fit_transform and downloads its band
+    (timed) — the same bytes as the device step."""
     import torch
+
+    if world > 1 and group is not None:
+        return _e2e_group(args, pb, slide, target, group, world)
 
     rows, W = slide.shape[0], slide.shape[1]
     nbytes = slide.numel()
@@ -783,6 +790,37 @@ def e2e(args, pb, slide, target, rank, world):
            "path": f"pb.fit(ArraySource(pinned)) + pb.transform(-> ArrayWriter(pinned)), "
                    f"{args.e2e_workers} streams"}
     del h_src, h_dst
+    return res
+
+
+def _e2e_group(args, pb, slide, target, group, world):
+    import torch
+
+    rows, W = slide.shape[0], slide.shape[1]
+    h_src = torch.empty((rows, W, 3), dtype=torch.uint8, pin_memory=True)
+    h_src.copy_(slide)
+    h_dst = torch.empty_like(h_src).pin_memory()
+    d_src = torch.empty_like(slide)
+    d_dst = torch.empty_like(slide)
+    dev = slide.device
+    times = []
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        t0 = time.perf_counter()
+        d_src.copy_(h_src, non_blocking=True)
+        group.fit_transform(pb.DeviceSource(d_src), target, d_dst)
+        h_dst.copy_(d_dst, non_blocking=True)
+        torch.cuda.synchronize()
+        if i:
+            times.append(time.perf_counter() - t0)
+    sec = _max_over_ranks(min(times), dev)
+    res = {"value": round(rows * W * world / sec / 1e6, 3), "unit": "Mpx/s",
+           "h2d_bytes_per_step": int(rows * W * 3), "d2h_bytes_per_step": int(rows * W * 3),
+           "rows_per_gpu": rows, "seconds_per_step": round(sec, 4),
+           "path": "per rank: band H2D (pinned) -> RowBandGroup.fit_transform -> band D2H "
+                   "(pinned); max over ranks"}
+    del h_src, h_dst, d_src, d_dst
     return res
 
 
