@@ -231,6 +231,11 @@ __device__ __forceinline__ void calibrate_body(const FastP& fp, const StrictP& s
     flut[i] = fp.lut[i >> 8][i & 255];
   }
   __syncthreads();
+  // the worst relative error as a (numerator, denominator) pair compared by
+  // cross-multiplication (no fp64 division per colour); divided once at the
+  // end.  A pair within fp64 rounding of the true maximum may be kept instead
+  // of it — well inside the 2^-20 margin spcn_xform_calibrate adds.
+  double wnum = 0.0, wden = 1.0;
   float worst = 0.f;
   const NnlsGram G = gram_of(sp);
   for (uint32_t q = q0 + blockIdx.x * 256u + threadIdx.x; q < q1; q += 256u * gridDim.x) {
@@ -255,14 +260,18 @@ __device__ __forceinline__ void calibrate_body(const FastP& fp, const StrictP& s
         const double yref = __dmul_rn(sp.i0t[c], exp(-od));
         const double yfast = (double)fp.i0t[c] * (double)ex2_approx(e[c][side]);
         if (yfast > 0.0) {
-          const float rel = (float)(fabs(yref - yfast) / yfast);
-          worst = fmaxf(worst, rel);
+          const double num = fabs(yref - yfast);
+          if (num * wden > wnum * yfast) {
+            wnum = num;
+            wden = yfast;
+          }
         } else if (yref >= 0.25) {
           worst = 1.0f;  // cannot happen for finite inputs; forces the analytic path
         }
       }
     }
   }
+  worst = fmaxf(worst, (float)(wnum / wden));
   for (int off = 16; off; off >>= 1) worst = fmaxf(worst, __shfl_xor_sync(0xffffffffu, worst, off));
   if ((threadIdx.x & 31) == 0) atomicMax(max_bits, __float_as_uint(worst));
 }
