@@ -519,7 +519,7 @@ cudaError_t launch_xform_build(int slot, const XformBuildIn& in, const double* l
   if (built && (e = cudaEventRecord(built, st)) != cudaSuccess) return e;
   if (q1 <= q0) return cudaSuccess;
   // colour pairs [q0, q1) with launch_calibrate's proportional grid
-  const int64_t full = (int64_t)g_sm_count * 8;
+  const int64_t full = (int64_t)g_sm_count * 16;
   int64_t grid = (full * (int64_t)(q1 - q0) + (1 << 23) - 1) >> 23;
   if (grid < 1) grid = 1;
   if (slot == 0) k_calibrate_c<0><<<(int)grid, 256, 0, st>>>(hdr + 2, q0, q1);
@@ -589,7 +589,7 @@ cudaError_t launch_calibrate(const FastP& fp, const StrictP& sp, unsigned int* m
   if (e != cudaSuccess) return e;
   if (q1 <= q0) return cudaSuccess;
   // colour pairs [q0, q1); a share of the 2^23 pairs gets a proportional grid
-  const int64_t full = (int64_t)g_sm_count * 8;
+  const int64_t full = (int64_t)g_sm_count * 16;
   int64_t grid = (full * (int64_t)(q1 - q0) + (1 << 23) - 1) >> 23;
   if (grid < 1) grid = 1;
   k_calibrate<<<(int)grid, 256, 0, st>>>(fp, sp, max_bits, q0, q1);
