@@ -262,36 +262,54 @@ class RowBandGroup:
         from .pipeline import PATCH_DT, TAKE_DT, _lib_sample, _stage, _visit
 
         L = _lib_sample()
-        W, H = self.width, self.height
-        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
-        rng = np.random.default_rng(plan.seed)
-        origins = [(x, y) for y in range(0, H, plan.patch_size) for x in range(0, W, plan.patch_size)]
-        order = rng.permutation(len(origins))
-        ncand = min(len(order), 10 * plan.max_patches)
-        rects = [(origins[i][0], origins[i][1], min(plan.patch_size, W - origins[i][0]),
-                  min(plan.patch_size, H - origins[i][1])) for i in order[:ncand]]
-        parts = local_parts(rects, self.r0, self.rows, W)
+        W = self.width
+        rank = dist.get_rank(self.group)
         img = band_source.tensor
         thr = int(plan.white_threshold)
         dev = img.device
-        present = [i for i, p in enumerate(parts) if p is not None]
-        chunks = max([1] + [-(-(p[1] * p[2]) // CHUNK) for p in parts if p is not None])
+        # the seeded candidate patches and this band's parts of them: a pure
+        # function of (slide geometry, band, plan), built once per plan (the
+        # 10 000-origin grid of a 100 k^2 slide costs ~3 ms of Python)
+        cache = self.__dict__.setdefault("_cand", {})
+        c = cache.get((plan, dev))
+        if c is None:
+            H = self.height
+            rng = np.random.default_rng(plan.seed)
+            origins = [(x, y) for y in range(0, H, plan.patch_size)
+                       for x in range(0, W, plan.patch_size)]
+            order = rng.permutation(len(origins))
+            ncand = min(len(order), 10 * plan.max_patches)
+            rects = [(origins[i][0], origins[i][1], min(plan.patch_size, W - origins[i][0]),
+                      min(plan.patch_size, H - origins[i][1])) for i in order[:ncand]]
+            parts = local_parts(rects, self.r0, self.rows, W)
+            present = [i for i, p in enumerate(parts) if p is not None]
+            chunks = max([1] + [-(-(p[1] * p[2]) // CHUNK) for p in parts if p is not None])
+            c = dict(order=order[:ncand].copy(), ncand=ncand, rects=rects, parts=parts,
+                     present=present, chunks=chunks)
+            if present:
+                desc = np.array([(parts[i][0], parts[i][1], parts[i][2], W) for i in present],
+                                dtype=PATCH_DT)
+                c["d"] = torch.from_numpy(desc.view(np.uint8).copy()).to(dev)
+                c["present_dev"] = torch.tensor(present, dtype=torch.int64, device=dev)
+            if len(cache) > 8:
+                cache.clear()
+            cache[(plan, dev)] = c
+        order, ncand, rects, parts = c["order"], c["ncand"], c["rects"], c["parts"]
+        present, chunks = c["present"], c["chunks"]
         lt = torch.zeros((ncand, 4), dtype=torch.int64, device=dev)
         cnt_dev = None
         if present:
-            desc = np.array([(parts[i][0], parts[i][1], parts[i][2], W) for i in present],
-                            dtype=PATCH_DT)
-            d = torch.from_numpy(desc.view(np.uint8).copy()).to(dev)
             cnt_dev = torch.empty((len(present), chunks, 4), dtype=torch.int32, device=dev)
-            _lib.check(L.spcn_sample_count(_lib.ptr(img), _lib.ptr(d), len(present), chunks, thr,
-                                           _lib.ptr(cnt_dev), _lib.stream_handle()), "sample_count")
-            lt[torch.tensor(present, dtype=torch.int64, device=dev)] = cnt_dev.sum(dim=1).to(torch.int64)
+            _lib.check(L.spcn_sample_count(_lib.ptr(img), _lib.ptr(c["d"]), len(present), chunks,
+                                           thr, _lib.ptr(cnt_dev), _lib.stream_handle()),
+                       "sample_count")
+            lt[c["present_dev"]] = cnt_dev.sum(dim=1).to(torch.int64)
         # all-gather of per-rank totals (ranks in band order), one host read
         gathered = all_gather_list(lt, self.group)
         per_rank = torch.stack([g.to(dev) for g in gathered]).cpu().numpy()
         glob = per_rank.sum(axis=0)
         takes, used_counts, collected, visited, used = _visit(
-            plan, order[:ncand], rects, lambda k: tuple(int(v) for v in glob[k]))
+            plan, order, rects, lambda k: tuple(int(v) for v in glob[k]))
         if collected == 0:
             raise BlankSlideError("sampling: blank slide: no non-white pixels found in any "
                                   "sampled patch")
