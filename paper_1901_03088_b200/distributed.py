@@ -273,14 +273,9 @@ class RowBandGroup:
         cache = self.__dict__.setdefault("_cand", {})
         c = cache.get((plan, dev))
         if c is None:
-            H = self.height
-            rng = np.random.default_rng(plan.seed)
-            origins = [(x, y) for y in range(0, H, plan.patch_size)
-                       for x in range(0, W, plan.patch_size)]
-            order = rng.permutation(len(origins))
-            ncand = min(len(order), 10 * plan.max_patches)
-            rects = [(origins[i][0], origins[i][1], min(plan.patch_size, W - origins[i][0]),
-                      min(plan.patch_size, H - origins[i][1])) for i in order[:ncand]]
+            from .pipeline import _candidates
+
+            order, ncand, rects = _candidates(W, self.height, plan)
             parts = local_parts(rects, self.r0, self.rows, W)
             present = [i for i, p in enumerate(parts) if p is not None]
             chunks = max([1] + [-(-(p[1] * p[2]) // CHUNK) for p in parts if p is not None])

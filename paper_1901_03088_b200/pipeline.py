@@ -10,6 +10,7 @@ GPU produced.
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 import time
 import warnings
@@ -218,9 +219,11 @@ def _visit(plan, order, rects, counts_of):
     return takes, used_counts, collected, visited, used
 
 
+@functools.lru_cache(maxsize=32)
 def _candidates(width: int, height: int, plan: SamplePlan):
     """The seeded visit order of the patch grid (src/pipeline.py:138-142):
-    (order, ncand, rects of the first ncand candidates)."""
+    (order, ncand, rects of the first ncand candidates).  Memoised: a pure
+    function of the geometry and the plan (callers do not modify it)."""
     ps = plan.patch_size
     ncols, nrows = -(-width // ps), -(-height // ps)
     order = np.random.default_rng(plan.seed).permutation(ncols * nrows)
