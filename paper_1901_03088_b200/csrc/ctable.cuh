@@ -102,4 +102,55 @@ __device__ void ct_finish(uint32_t* key, uint32_t* cnt, uint32_t* scan, uint32_t
   __syncthreads();
 }
 
+// ct_finish with the in-cluster sort done in parallel and without moving the
+// table: every occupied slot's key finds its cluster (the maximal run of
+// occupied slots around it) and its rank r among the cluster's keys; its
+// sorted slot is (cluster start + r), and that slot's position in slot order
+// (pos16, from one block scan) is where the entry goes — the same entries in
+// the same order as ct_finish's serial insertion sort + compaction, in O(L)
+// work per key instead of O(L^2) per cluster on one thread.  pos16: SLOTS
+// uint16 of shared scratch.  Requires at least one empty slot (the caller
+// rejects tables above 3/4 load).  Ends with a barrier.
+template <int NT>
+__device__ void ct_finish_par(const uint32_t* key, const uint32_t* cnt, uint32_t* scan,
+                              uint16_t* pos16, uint32_t* __restrict__ ukey,
+                              uint32_t* __restrict__ ucnt, int64_t o0, int32_t* ucount_p) {
+  constexpr int kMask = kTabSlots - 1;
+  const int tid = threadIdx.x;
+  constexpr int kPer = kTabSlots / NT;
+  uint32_t occ = 0;
+  for (int j = 0; j < kPer; ++j) occ += key[tid * kPer + j] != kTabEmpty;
+  scan[tid] = occ;
+  __syncthreads();
+  for (int off = 1; off < NT; off <<= 1) {
+    const uint32_t y = tid >= off ? scan[tid - off] : 0u;
+    __syncthreads();
+    scan[tid] += y;
+    __syncthreads();
+  }
+  uint32_t pos = scan[tid] - occ;
+  for (int j = 0; j < kPer; ++j) {
+    const int sl = tid * kPer + j;
+    if (key[sl] != kTabEmpty) pos16[sl] = static_cast<uint16_t>(pos++);
+  }
+  if (tid == NT - 1) *ucount_p = (int32_t)scan[NT - 1];
+  __syncthreads();
+  for (int s = tid; s < kTabSlots; s += NT) {
+    const uint32_t k = key[s];
+    if (k == kTabEmpty) continue;
+    int b = s;                                    // cluster start (walk back)
+    while (key[(b - 1) & kMask] != kTabEmpty) --b;
+    int r = 0;                                    // rank among the cluster's keys
+    for (int t = b;; ++t) {
+      const uint32_t kt = key[t & kMask];
+      if (kt == kTabEmpty) break;
+      r += kt < k;
+    }
+    const int dst = pos16[(b + r) & kMask];
+    ukey[o0 + dst] = k;
+    ucnt[o0 + dst] = cnt[s];
+  }
+  __syncthreads();
+}
+
 }  // namespace spcn

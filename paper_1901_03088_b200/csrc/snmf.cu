@@ -442,7 +442,8 @@ __global__ void __launch_bounds__(kCT) k_colour_table(const uint8_t* __restrict_
     __syncthreads();
     ct_overfull<kCT>(key, &s_used, &s_full);
     if (!s_full) {
-      ct_finish<kCT>(key, cnt, s_scan, ukey, ucnt, o0, &ucount[p]);
+      ct_finish_par<kCT>(key, cnt, s_scan, reinterpret_cast<uint16_t*>(tab + 2 * kTabSlots),
+                         ukey, ucnt, o0, &ucount[p]);
     } else {
       for (int64_t i = tid; i < m; i += kCT) {
         const uint8_t* px = samples + 3 * (o0 + i);
@@ -485,7 +486,7 @@ cudaError_t launch_snmf(const uint8_t* samples, const double* od, const int64_t*
   // table of one problem is built by one CTA and would cost more than it saves)
   if (hbuf && !od && samples && single) {
     static bool attr = false;
-    constexpr int kTabSmem = 2 * kTabSlots * sizeof(uint32_t);
+    constexpr int kTabSmem = 2 * kTabSlots * sizeof(uint32_t) + kTabSlots * sizeof(uint16_t);
     if (!attr) {
       const cudaError_t e0 = cudaFuncSetAttribute(k_colour_table,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
