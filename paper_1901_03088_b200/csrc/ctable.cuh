@@ -50,65 +50,14 @@ __device__ __forceinline__ void ct_overfull(const uint32_t* key, int* used, int*
 // Write the table as (rgb, count) entries at ukey/ucnt[o0 ..], *ucount_p = #.
 // With linear probing the SET of occupied slots, hence every cluster (maximal
 // run of occupied slots) and its key set, does not depend on insertion order
-// — only the order inside a cluster does.  Sorting each cluster by colour
-// makes the entry order, and every later floating-point summation order,
-// deterministic.  NT threads, scan[NT] shared scratch; ends with a barrier.
-template <int NT>
-__device__ void ct_finish(uint32_t* key, uint32_t* cnt, uint32_t* scan, uint32_t* __restrict__ ukey,
-                          uint32_t* __restrict__ ucnt, int64_t o0, int32_t* ucount_p) {
-  const int tid = threadIdx.x;
-  for (int s0 = tid; s0 < kTabSlots; s0 += NT) {
-    if (key[s0] == kTabEmpty || key[(s0 - 1) & (kTabSlots - 1)] != kTabEmpty) continue;
-    int len = 1;                                     // this thread owns the cluster at s0
-    while (len < kTabSlots && key[(s0 + len) & (kTabSlots - 1)] != kTabEmpty) ++len;
-    for (int x = 1; x < len; ++x) {                  // insertion sort, clusters are short
-      const int sx = (s0 + x) & (kTabSlots - 1);
-      const uint32_t kx = key[sx], cx = cnt[sx];
-      int y = x - 1;
-      while (y >= 0 && key[(s0 + y) & (kTabSlots - 1)] > kx) {
-        const int sy = (s0 + y) & (kTabSlots - 1), sy1 = (s0 + y + 1) & (kTabSlots - 1);
-        key[sy1] = key[sy];
-        cnt[sy1] = cnt[sy];
-        --y;
-      }
-      const int sd = (s0 + y + 1) & (kTabSlots - 1);
-      key[sd] = kx;
-      cnt[sd] = cx;
-    }
-  }
-  __syncthreads();
-  // compact in slot order (block scan)
-  constexpr int kPer = kTabSlots / NT;
-  uint32_t occ = 0;
-  for (int j = 0; j < kPer; ++j) occ += key[tid * kPer + j] != kTabEmpty;
-  scan[tid] = occ;
-  __syncthreads();
-  for (int off = 1; off < NT; off <<= 1) {
-    const uint32_t y = tid >= off ? scan[tid - off] : 0u;
-    __syncthreads();
-    scan[tid] += y;
-    __syncthreads();
-  }
-  uint32_t pos = scan[tid] - occ;
-  for (int j = 0; j < kPer; ++j) {
-    const int sl = tid * kPer + j;
-    if (key[sl] != kTabEmpty) {
-      ukey[o0 + pos] = key[sl];
-      ucnt[o0 + pos] = cnt[sl];
-      ++pos;
-    }
-  }
-  if (tid == NT - 1) *ucount_p = (int32_t)scan[NT - 1];
-  __syncthreads();
-}
-
-// ct_finish with the in-cluster sort done in parallel and without moving the
-// table: every occupied slot's key finds its cluster (the maximal run of
-// occupied slots around it) and its rank r among the cluster's keys; its
-// sorted slot is (cluster start + r), and that slot's position in slot order
-// (pos16, from one block scan) is where the entry goes — the same entries in
-// the same order as ct_finish's serial insertion sort + compaction, in O(L)
-// work per key instead of O(L^2) per cluster on one thread.  pos16: SLOTS
+// — only the order inside a cluster does.  Entries are written as if each
+// cluster were sorted by colour in place and the table compacted in slot
+// order, which makes the entry order, and every later floating-point
+// summation order, deterministic.  Done in parallel without moving the table:
+// every occupied slot's key finds its cluster and its rank r among the
+// cluster's keys; its sorted slot is (cluster start + r), and that slot's
+// position in slot order (pos16, from one block scan) is where the entry goes
+// — O(L) work per key instead of a serial O(L^2) insertion sort per cluster.  pos16: SLOTS
 // uint16 of shared scratch.  Requires at least one empty slot (the caller
 // rejects tables above 3/4 load).  Ends with a barrier.
 template <int NT>
