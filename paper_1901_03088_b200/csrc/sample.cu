@@ -27,41 +27,82 @@ constexpr int kChunk = SPCN_SAMPLE_CHUNK;     // raster pixels per chunk (4096)
 constexpr int kSThreads = 256;
 constexpr int kPerThread = kChunk / kSThreads; // 16
 
-// The kPerThread raster-consecutive pixels r0.. of a patch as packed RGB
-// (0xffffffff = past the end of the patch).  One division per thread; a run
-// inside one row at a 16-byte-aligned address is read with three 16-byte
-// loads, anything else pixel by pixel with an incremental (row, col).
-__device__ __forceinline__ void patch_run(const uint8_t* img, const spcn_patch& p, int64_t r0,
-                                          int64_t npx, uint32_t (&rgb)[kPerThread]) {
+// The kPerThread raster-consecutive pixels r0.. of a patch as their 48 RGB
+// bytes packed into 12 words (pixel j = bytes 3j..3j+2); returns how many of
+// them exist (a prefix: the run ends at the patch's last pixel).  One division
+// per thread; a run inside one row at a 16-byte-aligned address is three
+// 16-byte loads, anything else pixel by pixel with an incremental (row, col)
+// and packed with byte permutes.
+__device__ __forceinline__ int patch_run(const uint8_t* img, const spcn_patch& p, int64_t r0,
+                                         int64_t npx, uint32_t (&w)[12]) {
+  static_assert(kPerThread == 16, "16 px = 48 bytes = 12 words");
   int64_t row = r0 / p.width, col = r0 - row * p.width;
   const uint8_t* q = img + 3 * (p.base + row * p.row_stride + col);
   if (r0 + kPerThread <= npx && col + kPerThread <= p.width &&
       (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
-    static_assert(kPerThread == 16, "16 px = 48 bytes = 3 vector loads");
     const uint4* v = reinterpret_cast<const uint4*>(q);
     const uint4 a = __ldg(v), b = __ldg(v + 1), c = __ldg(v + 2);
-    const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
-#pragma unroll
-    for (int j = 0; j < kPerThread; ++j) {
-      const int i = 3 * j;   // byte offset of pixel j
-      const uint64_t pair = ((uint64_t)w[(i >> 2) + ((i >> 2) < 11 ? 1 : 0)] << 32) | w[i >> 2];
-      rgb[j] = (uint32_t)(pair >> (8 * (i & 3))) & 0xffffffu;
-    }
-    return;
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    w[8] = c.x; w[9] = c.y; w[10] = c.z; w[11] = c.w;
+    return kPerThread;
   }
+  uint32_t rgb[kPerThread];
+  const int nv = (int)min((int64_t)kPerThread, npx - r0);
 #pragma unroll
   for (int j = 0; j < kPerThread; ++j) {
-    if (r0 + j < npx) {
+    rgb[j] = 0;
+    if (j < nv) {
       const uint8_t* t = img + 3 * (p.base + row * p.row_stride + col);
       rgb[j] = t[0] | (t[1] << 8) | (t[2] << 16);
       if (++col == p.width) {
         col = 0;
         ++row;
       }
-    } else {
-      rgb[j] = 0xffffffffu;
     }
   }
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {   // word k = bytes 4k..4k+3 = pixel 4k/3 from byte 4k%3 on
+    const int j = (4 * k) / 3, o = (4 * k) % 3;
+    w[k] = __byte_perm(rgb[j], rgb[j + 1], o == 0 ? 0x4210 : o == 1 ? 0x5421 : 0x6542);
+  }
+  return nv;
+}
+
+// Byte-parallel "value > thr" (SWAR): 0x80 in every byte of x above thr.
+// thr is clamped to [-1, 255] (same predicate on 8-bit values); per byte the
+// sum stays below 256, so no carry crosses a byte.
+struct GtThr {
+  uint32_t k;
+  bool hi;
+};
+__device__ __forceinline__ GtThr gt_thr(int thr) {
+  thr = min(max(thr, -1), 255);
+  const bool hi = thr >= 128;   // x > thr  <=>  x >= 128 and (x & 127) > thr - 128
+  return GtThr{(uint32_t)(hi ? 255 - thr : 127 - thr) * 0x01010101u, hi};
+}
+__device__ __forceinline__ uint32_t gt80(uint32_t x, GtThr t) {
+  const uint32_t s = (x & 0x7f7f7f7fu) + t.k;
+  return (t.hi ? (x & s) : (x | s)) & 0x80808080u;
+}
+
+// Flags of pixels 4g..4g+3 (words 3g..3g+2 hold R0 G0 B0 R1 | G1 B1 R2 G2 |
+// B2 R3 G3 B3): per channel "> thr" and "non-white & present", bit 7 of
+// byte i = pixel 4g+i.
+__device__ __forceinline__ void group_flags(const uint32_t (&w)[12], int g, int nv, GtThr t,
+                                            uint32_t (&f)[4]) {
+  const uint32_t m0 = gt80(w[3 * g], t), m1 = gt80(w[3 * g + 1], t), m2 = gt80(w[3 * g + 2], t);
+  const int np = nv - 4 * g;
+  const uint32_t vb = np >= 4 ? 0x80808080u : np <= 0 ? 0u : 0x80808080u & ((1u << (8 * np)) - 1u);
+  f[0] = __byte_perm(__byte_perm(m0, m1, 0x0630), m2, 0x5210) & vb;   // R0 R1 R2 R3
+  f[1] = __byte_perm(__byte_perm(m0, m1, 0x0741), m2, 0x6210) & vb;   // G
+  f[2] = __byte_perm(__byte_perm(m0, m1, 0x0052), m2, 0x7410) & vb;   // B
+  f[3] = vb ^ (f[0] & f[1] & f[2]);                                    // non-white
+}
+
+__device__ __forceinline__ uint32_t pixel_of(const uint32_t (&w)[12], int j) {
+  const int i = 3 * j, k = i >> 2, o = i & 3;   // bytes i..i+2, from word k at offset o
+  return __byte_perm(w[k], w[k < 11 ? k + 1 : 11], o == 0 ? 0x210 : o == 1 ? 0x321 : o == 2 ? 0x432 : 0x543);
 }
 
 template <int N>
@@ -95,16 +136,17 @@ __global__ void __launch_bounds__(kSThreads) k_sample_count(const uint8_t* __res
   const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
   int c[4] = {0, 0, 0, 0};  // non-white, bright R, G, B
   if (r0 < npx) {
-    uint32_t rgb[kPerThread];
-    patch_run(img, p, r0, npx, rgb);
+    uint32_t w[12];
+    const int nv = patch_run(img, p, r0, npx, w);
+    const GtThr t = gt_thr(thr);
 #pragma unroll
-    for (int j = 0; j < kPerThread; ++j) {
-      if (rgb[j] == 0xffffffffu) continue;
-      const int a = rgb[j] & 255, b = (rgb[j] >> 8) & 255, d = rgb[j] >> 16;
-      c[0] += !(a > thr && b > thr && d > thr);
-      c[1] += a > thr;
-      c[2] += b > thr;
-      c[3] += d > thr;
+    for (int g = 0; g < 4; ++g) {
+      uint32_t f[4];
+      group_flags(w, g, nv, t, f);
+      c[0] += __popc(f[3]);
+      c[1] += __popc(f[0]);
+      c[2] += __popc(f[1]);
+      c[3] += __popc(f[2]);
     }
   }
   __shared__ int scratch[kSThreads / 32][4];
@@ -112,6 +154,38 @@ __global__ void __launch_bounds__(kSThreads) k_sample_count(const uint8_t* __res
   if (threadIdx.x == 0) {
     int32_t* o = counts + ((int64_t)pi * max_chunks + k) * 4;
     o[0] = c[0]; o[1] = c[1]; o[2] = c[2]; o[3] = c[3];
+  }
+}
+
+// The ordered take of one thread's 16 pixels.  BOUND: some pool's take limit
+// falls inside this chunk, so every pixel checks its rank; otherwise each
+// pool takes all or nothing of the chunk (take_nw / take_c, block-uniform).
+template <bool BOUND>
+__device__ __forceinline__ void compact_run(const uint32_t (&w)[12], const uint32_t (&f)[4][4],
+                                            int (&rank)[4], const int (&lim)[4], bool take_nw,
+                                            const bool (&take_c)[3], uint32_t* stage, int blk_r0,
+                                            int dump, int* hist) {
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j) {
+    const int g = j >> 2, sh = 8 * (j & 3) + 7;
+    const uint32_t px = pixel_of(w, j);
+    const int nwf = (f[g][3] >> sh) & 1;
+    if (BOUND) {
+      stage[nwf && rank[0] < lim[0] ? rank[0] - blk_r0 : dump] = px;
+    } else if (take_nw) {
+      stage[nwf ? rank[0] - blk_r0 : dump] = px;
+    }
+    rank[0] += nwf;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int bf = (f[g][c] >> sh) & 1;
+      if (BOUND) {
+        if (bf && rank[c + 1] < lim[c + 1]) atomicAdd(&hist[256 * c + ((px >> (8 * c)) & 255)], 1);
+        rank[c + 1] += bf;
+      } else if (take_c[c] && bf) {
+        atomicAdd(&hist[256 * c + ((px >> (8 * c)) & 255)], 1);
+      }
+    }
   }
 }
 
@@ -127,10 +201,12 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
   __shared__ int s_pre[4];
   __shared__ int scratch[kSThreads / 32][4];
   __shared__ int s_hist[3][256];
-  __shared__ int s_wsum[kSThreads / 32][4];
-  // the chunk's taken non-white pixels, staged in rank order (they are one
-  // contiguous run of the output) and written with coalesced word stores
-  __shared__ __align__(16) uint32_t s_stage[(3 * kChunk) / 4 + 2];
+  __shared__ __align__(16) int s_wsum[kSThreads / 32][4];   // per-warp totals, then exclusive
+  __shared__ __align__(16) int s_tot[4];
+  // the chunk's taken non-white pixels as words in rank order (+ one dump
+  // slot per lane for the pixels that are not taken), then written out as
+  // one contiguous 3-byte-per-pixel run with coalesced word stores
+  __shared__ __align__(16) uint32_t s_stage[kChunk + 32];
   // prefix over earlier chunks of this patch
   int pre[4] = {0, 0, 0, 0};
   for (int j = threadIdx.x; j < k; j += kSThreads) {
@@ -148,24 +224,25 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
                     pb[1] < tk.take_bright[1] || pb[2] < tk.take_bright[2];
   if (!need) return;  // uniform across the block
 
-  // per-thread flags for its 16 raster-consecutive pixels
   const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
-  uint32_t rgb[kPerThread];   // 0xffffffff: not a pixel
-  int cnt[4] = {0, 0, 0, 0};
+  uint32_t w[12];
+  int nv = 0;
   if (r0 < npx) {
-    patch_run(img, p, r0, npx, rgb);
+    nv = patch_run(img, p, r0, npx, w);
   } else {
 #pragma unroll
-    for (int j = 0; j < kPerThread; ++j) rgb[j] = 0xffffffffu;
+    for (int i = 0; i < 12; ++i) w[i] = 0;
   }
+  const GtThr t = gt_thr(thr);
+  uint32_t f[4][4];
+  int cnt[4] = {0, 0, 0, 0};
 #pragma unroll
-  for (int j = 0; j < kPerThread; ++j) {
-    if (rgb[j] == 0xffffffffu) continue;
-    const int a = rgb[j] & 255, b = (rgb[j] >> 8) & 255, d = rgb[j] >> 16;
-    cnt[0] += !(a > thr && b > thr && d > thr);
-    cnt[1] += a > thr;
-    cnt[2] += b > thr;
-    cnt[3] += d > thr;
+  for (int g = 0; g < 4; ++g) {
+    group_flags(w, g, nv, t, f[g]);
+    cnt[0] += __popc(f[g][3]);
+    cnt[1] += __popc(f[g][0]);
+    cnt[2] += __popc(f[g][1]);
+    cnt[3] += __popc(f[g][2]);
   }
   // block exclusive scan of the four counters
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -182,47 +259,57 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
   if (lane == 31)
     for (int q = 0; q < 4; ++q) s_wsum[warp][q] = inc[q];
   __syncthreads();
-  int rank[4];
+  if (warp == 0) {   // lane = 4 * warp' + q: exclusive scan over the 8 warps per counter
+    static_assert(kSThreads == 256, "8 warps x 4 counters = one warp");
+    const int v = (&s_wsum[0][0])[lane];
+    int x = v;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    int wpre = 0;
-    for (int w = 0; w < warp; ++w) wpre += s_wsum[w][q];
-    rank[q] = s_pre[q] + wpre + inc[q] - cnt[q];
-  }
-  const int blk_r0 = s_pre[0];                 // the chunk's first non-white rank
-  uint8_t* stage = reinterpret_cast<uint8_t*>(s_stage);
-#pragma unroll
-  for (int j = 0; j < kPerThread; ++j) {
-    if (rgb[j] == 0xffffffffu) continue;
-    const int a = rgb[j] & 255, b = (rgb[j] >> 8) & 255, d = (rgb[j] >> 16) & 255;
-    if (!(a > thr && b > thr && d > thr)) {
-      if (rank[0] < tk.take_nonwhite) {
-        uint8_t* o = stage + 3 * (rank[0] - blk_r0);
-        o[0] = a; o[1] = b; o[2] = d;
-      }
-      ++rank[0];
+    for (int off = 4; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
     }
-    if (a > thr) { if (rank[1] < tk.take_bright[0]) atomicAdd(&s_hist[0][a], 1); ++rank[1]; }
-    if (b > thr) { if (rank[2] < tk.take_bright[1]) atomicAdd(&s_hist[1][b], 1); ++rank[2]; }
-    if (d > thr) { if (rank[3] < tk.take_bright[2]) atomicAdd(&s_hist[2][d], 1); ++rank[3]; }
+    __syncwarp();
+    (&s_wsum[0][0])[lane] = x - v;
+    if (lane >= 28) s_tot[lane - 28] = x;
   }
   __syncthreads();
+  const int4 wp = *reinterpret_cast<const int4*>(s_wsum[warp]);
+  const int4 tot = *reinterpret_cast<const int4*>(s_tot);
+  int rank[4] = {s_pre[0] + wp.x + inc[0] - cnt[0], s_pre[1] + wp.y + inc[1] - cnt[1],
+                 s_pre[2] + wp.z + inc[2] - cnt[2], s_pre[3] + wp.w + inc[3] - cnt[3]};
+  const int blk_r0 = s_pre[0];                 // the chunk's first non-white rank
+  const int lim[4] = {(int)min(tk.take_nonwhite, (int64_t)INT32_MAX), tk.take_bright[0],
+                      tk.take_bright[1], tk.take_bright[2]};
+  const int tsum[4] = {tot.x, tot.y, tot.z, tot.w};
+  bool bound = false, all[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {   // block-uniform: pool q takes all / none / part of the chunk
+    all[q] = s_pre[q] + tsum[q] <= lim[q];
+    bound |= !all[q] && s_pre[q] < lim[q];
+  }
+  const bool take_c[3] = {all[1], all[2], all[3]};
+  if (bound)
+    compact_run<true>(w, f, rank, lim, all[0], take_c, s_stage, blk_r0, kChunk + lane, &s_hist[0][0]);
+  else
+    compact_run<false>(w, f, rank, lim, all[0], take_c, s_stage, blk_r0, kChunk + lane, &s_hist[0][0]);
+  __syncthreads();
   {   // the staged run [blk_r0, min(take, blk_r0 + chunk non-white)) to the output
-    int blk_nw = 0;
-    for (int w = 0; w < kSThreads / 32; ++w) blk_nw += s_wsum[w][0];
-    const int64_t t1 = min((int64_t)tk.take_nonwhite, (int64_t)blk_r0 + blk_nw);
+    const int64_t t1 = min((int64_t)tk.take_nonwhite, (int64_t)blk_r0 + tsum[0]);
     const int nb = t1 > blk_r0 ? (int)(3 * (t1 - blk_r0)) : 0;
     uint8_t* dstb = out_px + 3 * (tk.out_base + blk_r0);
     const int head = min(nb, (int)((4u - (reinterpret_cast<uintptr_t>(dstb) & 3u)) & 3u));
-    if (threadIdx.x < head) dstb[threadIdx.x] = stage[threadIdx.x];
-    const int nw = (nb - head) >> 2, sh = 8 * (head & 3);
+    if (threadIdx.x < head) dstb[threadIdx.x] = s_stage[threadIdx.x / 3] >> (8 * (threadIdx.x % 3));
+    const int nw = (nb - head) >> 2;
     uint32_t* dw = reinterpret_cast<uint32_t*>(dstb + head);
-    for (int w = threadIdx.x; w < nw; w += kSThreads) {
-      const int q = (head >> 2) + w;               // source word index (offset head + 4w)
-      dw[w] = sh ? __funnelshift_r(s_stage[q], s_stage[q + 1], sh) : s_stage[q];
+    for (int i = threadIdx.x; i < nw; i += kSThreads) {
+      const int b = head + 4 * i, q = b / 3, o = b - 3 * q;   // run bytes b..b+3
+      dw[i] = __byte_perm(s_stage[q], s_stage[q + 1], o == 0 ? 0x4210 : o == 1 ? 0x5421 : 0x6542);
     }
     const int tail0 = head + 4 * nw;
-    if (threadIdx.x < nb - tail0) dstb[tail0 + threadIdx.x] = stage[tail0 + threadIdx.x];
+    if (threadIdx.x < nb - tail0) {
+      const int b = tail0 + threadIdx.x;
+      dstb[b] = s_stage[b / 3] >> (8 * (b % 3));
+    }
   }
   int32_t* gh = bright_hist + (int64_t)tk.problem * 3 * 256;
   for (int i = threadIdx.x; i < 3 * 256; i += kSThreads) {
