@@ -36,7 +36,15 @@ constexpr int kPerThread = kChunk / kSThreads; // 16
 __device__ __forceinline__ int patch_run(const uint8_t* img, const spcn_patch& p, int64_t r0,
                                          int64_t npx, uint32_t (&w)[12]) {
   static_assert(kPerThread == 16, "16 px = 48 bytes = 12 words");
-  int64_t row = r0 / p.width, col = r0 - row * p.width;
+  int64_t row, col;
+  if (r0 <= 0xffffffffll) {   // 32-bit division (the common case)
+    const uint32_t r = (uint32_t)r0 / (uint32_t)p.width;
+    row = r;
+    col = (int64_t)((uint32_t)r0 - r * (uint32_t)p.width);
+  } else {
+    row = r0 / p.width;
+    col = r0 - row * p.width;
+  }
   const uint8_t* q = img + 3 * (p.base + row * p.row_stride + col);
   if (r0 + kPerThread <= npx && col + kPerThread <= p.width &&
       (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
@@ -71,33 +79,45 @@ __device__ __forceinline__ int patch_run(const uint8_t* img, const spcn_patch& p
 
 // Byte-parallel "value > thr" (SWAR): 0x80 in every byte of x above thr.
 // thr is clamped to [-1, 255] (same predicate on 8-bit values); per byte the
-// sum stays below 256, so no carry crosses a byte.
-struct GtThr {
-  uint32_t k;
-  bool hi;
-};
-__device__ __forceinline__ GtThr gt_thr(int thr) {
-  thr = min(max(thr, -1), 255);
-  const bool hi = thr >= 128;   // x > thr  <=>  x >= 128 and (x & 127) > thr - 128
-  return GtThr{(uint32_t)(hi ? 255 - thr : 127 - thr) * 0x01010101u, hi};
+// sum stays below 256, so no carry crosses a byte.  HI (thr >= 128):
+// x > thr  <=>  x >= 128 and (x & 127) > thr - 128.
+__host__ __device__ __forceinline__ int clamp_thr(int thr) { return thr < -1 ? -1 : thr > 255 ? 255 : thr; }
+__device__ __forceinline__ uint32_t gt_k(int thr) {
+  thr = clamp_thr(thr);
+  return (uint32_t)(thr >= 128 ? 255 - thr : 127 - thr) * 0x01010101u;
 }
-__device__ __forceinline__ uint32_t gt80(uint32_t x, GtThr t) {
-  const uint32_t s = (x & 0x7f7f7f7fu) + t.k;
-  return (t.hi ? (x & s) : (x | s)) & 0x80808080u;
+template <bool HI>
+__device__ __forceinline__ uint32_t gt80(uint32_t x, uint32_t k) {
+  const uint32_t s = (x & 0x7f7f7f7fu) + k;
+  return (HI ? (x & s) : (x | s)) & 0x80808080u;
 }
 
-// Flags of pixels 4g..4g+3 (words 3g..3g+2 hold R0 G0 B0 R1 | G1 B1 R2 G2 |
-// B2 R3 G3 B3): per channel "> thr" and "non-white & present", bit 7 of
-// byte i = pixel 4g+i.
-__device__ __forceinline__ void group_flags(const uint32_t (&w)[12], int g, int nv, GtThr t,
-                                            uint32_t (&f)[4]) {
-  const uint32_t m0 = gt80(w[3 * g], t), m1 = gt80(w[3 * g + 1], t), m2 = gt80(w[3 * g + 2], t);
-  const int np = nv - 4 * g;
-  const uint32_t vb = np >= 4 ? 0x80808080u : np <= 0 ? 0u : 0x80808080u & ((1u << (8 * np)) - 1u);
-  f[0] = __byte_perm(__byte_perm(m0, m1, 0x0630), m2, 0x5210) & vb;   // R0 R1 R2 R3
-  f[1] = __byte_perm(__byte_perm(m0, m1, 0x0741), m2, 0x6210) & vb;   // G
-  f[2] = __byte_perm(__byte_perm(m0, m1, 0x0052), m2, 0x7410) & vb;   // B
-  f[3] = vb ^ (f[0] & f[1] & f[2]);                                    // non-white
+// Flags of a thread's 16 pixels: f[g][c] (c = R, G, B: "> thr"; c = 3:
+// "non-white"), bit 7 of byte i = pixel 4g+i.  Words 3g..3g+2 hold
+// R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3; missing pixels (j >= nv) flag 0.
+template <bool HI>
+__device__ __forceinline__ void run_flags(const uint32_t (&w)[12], int nv, uint32_t k,
+                                          uint32_t (&f)[4][4]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const uint32_t m0 = gt80<HI>(w[3 * g], k), m1 = gt80<HI>(w[3 * g + 1], k),
+                   m2 = gt80<HI>(w[3 * g + 2], k);
+    f[g][0] = __byte_perm(__byte_perm(m0, m1, 0x0630), m2, 0x5210);   // R0 R1 R2 R3
+    f[g][1] = __byte_perm(__byte_perm(m0, m1, 0x0741), m2, 0x6210);   // G
+    f[g][2] = __byte_perm(__byte_perm(m0, m1, 0x0052), m2, 0x7410);   // B
+  }
+  if (nv >= kPerThread) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) f[g][3] = 0x80808080u ^ (f[g][0] & f[g][1] & f[g][2]);
+  } else {
+    const uint32_t vbits = (1u << max(nv, 0)) - 1u;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {   // 4 bits -> bit 7 of 4 bytes
+      const uint32_t vb = (((vbits >> (4 * g)) & 15u) * 0x10204080u) & 0x80808080u;
+      f[g][0] &= vb; f[g][1] &= vb; f[g][2] &= vb;
+      f[g][3] = vb ^ (f[g][0] & f[g][1] & f[g][2]);
+    }
+  }
 }
 
 __device__ __forceinline__ uint32_t pixel_of(const uint32_t (&w)[12], int j) {
@@ -105,27 +125,7 @@ __device__ __forceinline__ uint32_t pixel_of(const uint32_t (&w)[12], int j) {
   return __byte_perm(w[k], w[k < 11 ? k + 1 : 11], o == 0 ? 0x210 : o == 1 ? 0x321 : o == 2 ? 0x432 : 0x543);
 }
 
-template <int N>
-__device__ __forceinline__ void block_sum(int (&v)[N], int (*scratch)[N]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < N; ++q)
-#pragma unroll
-    for (int off = 16; off; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < N; ++q) scratch[warp][q] = v[q];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      int s = 0;
-      for (int w = 0; w < kSThreads / 32; ++w) s += scratch[w][q];
-      v[q] = s;
-    }
-  }
-}
-
+template <bool HI>
 __global__ void __launch_bounds__(kSThreads) k_sample_count(const uint8_t* __restrict__ img,
                                                             const spcn_patch* __restrict__ patches,
                                                             int max_chunks, int thr,
@@ -134,61 +134,82 @@ __global__ void __launch_bounds__(kSThreads) k_sample_count(const uint8_t* __res
   const spcn_patch p = patches[pi];
   const int64_t npx = (int64_t)p.width * p.height;
   const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
-  int c[4] = {0, 0, 0, 0};  // non-white, bright R, G, B
+  unsigned c[4] = {0, 0, 0, 0};  // non-white, bright R, G, B
   if (r0 < npx) {
-    uint32_t w[12];
+    uint32_t w[12], f[4][4];
     const int nv = patch_run(img, p, r0, npx, w);
-    const GtThr t = gt_thr(thr);
+    run_flags<HI>(w, nv, gt_k(thr), f);
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-      uint32_t f[4];
-      group_flags(w, g, nv, t, f);
-      c[0] += __popc(f[3]);
-      c[1] += __popc(f[0]);
-      c[2] += __popc(f[1]);
-      c[3] += __popc(f[2]);
+      c[0] += __popc(f[g][3]);
+      c[1] += __popc(f[g][0]);
+      c[2] += __popc(f[g][1]);
+      c[3] += __popc(f[g][2]);
     }
   }
-  __shared__ int scratch[kSThreads / 32][4];
-  block_sum<4>(c, scratch);
-  if (threadIdx.x == 0) {
-    int32_t* o = counts + ((int64_t)pi * max_chunks + k) * 4;
-    o[0] = c[0]; o[1] = c[1]; o[2] = c[2]; o[3] = c[3];
+  __shared__ unsigned scratch[kSThreads / 32][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) c[q] = __reduce_add_sync(0xffffffffu, c[q]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) scratch[warp][q] = c[q];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    unsigned v = 0;
+#pragma unroll
+    for (int i = 0; i < kSThreads / 32; ++i) v += scratch[i][threadIdx.x];
+    counts[((int64_t)pi * max_chunks + k) * 4 + threadIdx.x] = (int32_t)v;
   }
 }
 
-// The ordered take of one thread's 16 pixels.  BOUND: some pool's take limit
-// falls inside this chunk, so every pixel checks its rank; otherwise each
-// pool takes all or nothing of the chunk (take_nw / take_c, block-uniform).
-template <bool BOUND>
+// The ordered take of one thread's 16 pixels from its flags (already cut to
+// what the pools take): STAGE puts the taken non-white pixels at their rank
+// in the chunk's stage (the others in a per-lane dump slot); every taken
+// bright value goes into its channel's 256-bin histogram.
+// Shared-memory increment without a branch: an untaken value goes to the
+// lane's own dump word (hist[768 + lane]) instead of being predicated off.
+__device__ __forceinline__ void hist_inc(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(addr) : "memory");
+}
+
+template <bool STAGE>
 __device__ __forceinline__ void compact_run(const uint32_t (&w)[12], const uint32_t (&f)[4][4],
-                                            int (&rank)[4], const int (&lim)[4], bool take_nw,
-                                            const bool (&take_c)[3], uint32_t* stage, int blk_r0,
-                                            int dump, int* hist) {
+                                            int rank0, uint32_t* stage, int dump, int* hist) {
+  const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(hist);
+  const uint32_t hdump = hbase + 4 * (3 * 256 + (threadIdx.x & 31));
 #pragma unroll
   for (int j = 0; j < kPerThread; ++j) {
     const int g = j >> 2, sh = 8 * (j & 3) + 7;
-    const uint32_t px = pixel_of(w, j);
-    const int nwf = (f[g][3] >> sh) & 1;
-    if (BOUND) {
-      stage[nwf && rank[0] < lim[0] ? rank[0] - blk_r0 : dump] = px;
-    } else if (take_nw) {
-      stage[nwf ? rank[0] - blk_r0 : dump] = px;
+    if (STAGE) {
+      const int nwf = (f[g][3] >> sh) & 1;
+      stage[nwf ? rank0 : dump] = pixel_of(w, j);
+      rank0 += nwf;
     }
-    rank[0] += nwf;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const int bf = (f[g][c] >> sh) & 1;
-      if (BOUND) {
-        if (bf && rank[c + 1] < lim[c + 1]) atomicAdd(&hist[256 * c + ((px >> (8 * c)) & 255)], 1);
-        rank[c + 1] += bf;
-      } else if (take_c[c] && bf) {
-        atomicAdd(&hist[256 * c + ((px >> (8 * c)) & 255)], 1);
-      }
+      const int b = 3 * j + c;   // byte of channel c of pixel j
+      const uint32_t a = hbase + 4 * (256 * c + __byte_perm(w[b >> 2], 0, 0x4440 | (b & 3)));
+      hist_inc(f[g][c] & (1u << sh) ? a : hdump);
     }
   }
 }
 
+// Keep only the first `m` set flags (raster order) of f[.][q].
+__device__ __forceinline__ void limit_flags(uint32_t (&f)[4][4], int q, int m) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t bit = 0x80u << (8 * i);
+      if (f[g][q] & bit) {
+        if (m > 0) --m;
+        else f[g][q] &= ~bit;
+      }
+    }
+}
+
+template <bool HI>
 __global__ void __launch_bounds__(kSThreads) k_sample_compact(
     const uint8_t* __restrict__ img, const spcn_patch* __restrict__ patches, int max_chunks,
     int thr, const int32_t* __restrict__ counts, const spcn_patch_take* __restrict__ takes,
@@ -199,30 +220,42 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
   const int64_t npx = (int64_t)p.width * p.height;
   if ((int64_t)k * kChunk >= npx) return;
   __shared__ int s_pre[4];
-  __shared__ int scratch[kSThreads / 32][4];
-  __shared__ int s_hist[3][256];
-  __shared__ __align__(16) int s_wsum[kSThreads / 32][4];   // per-warp totals, then exclusive
-  __shared__ __align__(16) int s_tot[4];
+  __shared__ unsigned scratch[kSThreads / 32][4];
+  __shared__ int s_hist[3 * 256 + 32];   // + one dump word per lane
+  // per-warp totals of the packed counters (non-white | R << 16, G | B << 16),
+  // then their exclusive prefix over warps; s_tot: the chunk's totals
+  __shared__ __align__(8) uint32_t s_wsum[kSThreads / 32][2];
+  __shared__ __align__(8) uint32_t s_tot[2];
   // the chunk's taken non-white pixels as words in rank order (+ one dump
   // slot per lane for the pixels that are not taken), then written out as
   // one contiguous 3-byte-per-pixel run with coalesced word stores
   __shared__ __align__(16) uint32_t s_stage[kChunk + 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // prefix over earlier chunks of this patch
-  int pre[4] = {0, 0, 0, 0};
+  unsigned pre[4] = {0, 0, 0, 0};
   for (int j = threadIdx.x; j < k; j += kSThreads) {
     const int32_t* c = counts + ((int64_t)pi * max_chunks + j) * 4;
     pre[0] += c[0]; pre[1] += c[1]; pre[2] += c[2]; pre[3] += c[3];
   }
-  block_sum<4>(pre, scratch);
-  if (threadIdx.x == 0)
-    for (int q = 0; q < 4; ++q) s_pre[q] = pre[q];
-  for (int i = threadIdx.x; i < 3 * 256; i += kSThreads) (&s_hist[0][0])[i] = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) pre[q] = __reduce_add_sync(0xffffffffu, pre[q]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) scratch[warp][q] = pre[q];
+  for (int i = threadIdx.x; i < 3 * 256; i += kSThreads) s_hist[i] = 0;
   __syncthreads();
-  const int64_t pnw = s_pre[0];
-  const int pb[3] = {s_pre[1], s_pre[2], s_pre[3]};
-  const bool need = pnw < tk.take_nonwhite || pb[0] < tk.take_bright[0] ||
-                    pb[1] < tk.take_bright[1] || pb[2] < tk.take_bright[2];
-  if (!need) return;  // uniform across the block
+  if (threadIdx.x < 4) {
+    unsigned v = 0;
+#pragma unroll
+    for (int i = 0; i < kSThreads / 32; ++i) v += scratch[i][threadIdx.x];
+    s_pre[threadIdx.x] = (int)v;
+  }
+  __syncthreads();
+  const int spre[4] = {s_pre[0], s_pre[1], s_pre[2], s_pre[3]};
+  const int lim[4] = {(int)min(tk.take_nonwhite, (int64_t)INT32_MAX), tk.take_bright[0],
+                      tk.take_bright[1], tk.take_bright[2]};
+  if (!(spre[0] < lim[0] || spre[1] < lim[1] || spre[2] < lim[2] || spre[3] < lim[3]))
+    return;  // uniform across the block: every pool is full before this chunk
 
   const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
   uint32_t w[12];
@@ -233,68 +266,65 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
 #pragma unroll
     for (int i = 0; i < 12; ++i) w[i] = 0;
   }
-  const GtThr t = gt_thr(thr);
   uint32_t f[4][4];
-  int cnt[4] = {0, 0, 0, 0};
+  run_flags<HI>(w, nv, gt_k(thr), f);
+  uint32_t c01 = 0, c23 = 0;   // packed 16-bit counters: non-white | R << 16, G | B << 16
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
-    group_flags(w, g, nv, t, f[g]);
-    cnt[0] += __popc(f[g][3]);
-    cnt[1] += __popc(f[g][0]);
-    cnt[2] += __popc(f[g][1]);
-    cnt[3] += __popc(f[g][2]);
+    c01 += __popc(f[g][3]) | (__popc(f[g][0]) << 16);
+    c23 += __popc(f[g][1]) | (__popc(f[g][2]) << 16);
   }
-  // block exclusive scan of the four counters
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int inc[4];
+  // block exclusive scan of the packed counters (chunk totals <= 4096)
+  uint32_t i01 = c01, i23 = c23;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    inc[q] = cnt[q];
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, inc[q], off);
-      if (lane >= off) inc[q] += y;
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y01 = __shfl_up_sync(0xffffffffu, i01, off);
+    const uint32_t y23 = __shfl_up_sync(0xffffffffu, i23, off);
+    if (lane >= off) {
+      i01 += y01;
+      i23 += y23;
     }
   }
-  if (lane == 31)
-    for (int q = 0; q < 4; ++q) s_wsum[warp][q] = inc[q];
+  if (lane == 31) {
+    s_wsum[warp][0] = i01;
+    s_wsum[warp][1] = i23;
+  }
   __syncthreads();
-  if (warp == 0) {   // lane = 4 * warp' + q: exclusive scan over the 8 warps per counter
-    static_assert(kSThreads == 256, "8 warps x 4 counters = one warp");
-    const int v = (&s_wsum[0][0])[lane];
-    int x = v;
+  if (warp == 0) {   // lane 2w + h: exclusive scan over the 8 warps
+    static_assert(kSThreads / 32 * 2 <= 32, "one warp scans the per-warp totals");
+    const bool on = lane < 2 * (kSThreads / 32);
+    const uint32_t v = on ? (&s_wsum[0][0])[lane] : 0u;
+    uint32_t x = v;
 #pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, off);
+    for (int off = 2; off < 2 * (kSThreads / 32); off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
       if (lane >= off) x += y;
     }
     __syncwarp();
-    (&s_wsum[0][0])[lane] = x - v;
-    if (lane >= 28) s_tot[lane - 28] = x;
+    if (on) (&s_wsum[0][0])[lane] = x - v;
+    if (lane >= 2 * (kSThreads / 32) - 2 && on) s_tot[lane - (2 * (kSThreads / 32) - 2)] = x;
   }
   __syncthreads();
-  const int4 wp = *reinterpret_cast<const int4*>(s_wsum[warp]);
-  const int4 tot = *reinterpret_cast<const int4*>(s_tot);
-  int rank[4] = {s_pre[0] + wp.x + inc[0] - cnt[0], s_pre[1] + wp.y + inc[1] - cnt[1],
-                 s_pre[2] + wp.z + inc[2] - cnt[2], s_pre[3] + wp.w + inc[3] - cnt[3]};
-  const int blk_r0 = s_pre[0];                 // the chunk's first non-white rank
-  const int lim[4] = {(int)min(tk.take_nonwhite, (int64_t)INT32_MAX), tk.take_bright[0],
-                      tk.take_bright[1], tk.take_bright[2]};
-  const int tsum[4] = {tot.x, tot.y, tot.z, tot.w};
-  bool bound = false, all[4];
+  const uint2 wp = *reinterpret_cast<const uint2*>(s_wsum[warp]);
+  const uint2 tt = *reinterpret_cast<const uint2*>(s_tot);
+  const uint32_t e01 = wp.x + i01 - c01, e23 = wp.y + i23 - c23;
+  const int rank[4] = {spre[0] + (int)(e01 & 0xffffu), spre[1] + (int)(e01 >> 16),
+                       spre[2] + (int)(e23 & 0xffffu), spre[3] + (int)(e23 >> 16)};
+  const int tot[4] = {(int)(tt.x & 0xffffu), (int)(tt.x >> 16), (int)(tt.y & 0xffffu),
+                      (int)(tt.y >> 16)};
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {   // block-uniform: pool q takes all / none / part of the chunk
-    all[q] = s_pre[q] + tsum[q] <= lim[q];
-    bound |= !all[q] && s_pre[q] < lim[q];
+  for (int q = 0; q < 4; ++q) {   // pool q takes all / none / the first part of the chunk
+    const int fq = q == 0 ? 3 : q - 1;
+    if (spre[q] + tot[q] > lim[q]) limit_flags(f, fq, lim[q] - rank[q]);   // block-uniform test
   }
-  const bool take_c[3] = {all[1], all[2], all[3]};
-  if (bound)
-    compact_run<true>(w, f, rank, lim, all[0], take_c, s_stage, blk_r0, kChunk + lane, &s_hist[0][0]);
+  const int blk_r0 = spre[0];                 // the chunk's first non-white rank
+  if (spre[0] < lim[0])
+    compact_run<true>(w, f, rank[0] - blk_r0, s_stage, kChunk + lane, s_hist);
   else
-    compact_run<false>(w, f, rank, lim, all[0], take_c, s_stage, blk_r0, kChunk + lane, &s_hist[0][0]);
+    compact_run<false>(w, f, 0, s_stage, kChunk + lane, s_hist);
   __syncthreads();
   {   // the staged run [blk_r0, min(take, blk_r0 + chunk non-white)) to the output
-    const int64_t t1 = min((int64_t)tk.take_nonwhite, (int64_t)blk_r0 + tsum[0]);
+    const int64_t t1 = min((int64_t)tk.take_nonwhite, (int64_t)blk_r0 + tot[0]);
     const int nb = t1 > blk_r0 ? (int)(3 * (t1 - blk_r0)) : 0;
     uint8_t* dstb = out_px + 3 * (tk.out_base + blk_r0);
     const int head = min(nb, (int)((4u - (reinterpret_cast<uintptr_t>(dstb) & 3u)) & 3u));
@@ -313,7 +343,7 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
   }
   int32_t* gh = bright_hist + (int64_t)tk.problem * 3 * 256;
   for (int i = threadIdx.x; i < 3 * 256; i += kSThreads) {
-    const int v = (&s_hist[0][0])[i];
+    const int v = s_hist[i];
     if (v) atomicAdd(&gh[i], v);
   }
 }
@@ -460,7 +490,8 @@ cudaError_t launch_sample_count(const uint8_t* img, const spcn_patch* patches, i
   if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;
   for (int y0 = 0; y0 < npatches; y0 += kMaxGridY) {   // gridDim.y <= 65535
     const int ny = npatches - y0 < kMaxGridY ? npatches - y0 : kMaxGridY;
-    k_sample_count<<<dim3(max_chunks, ny), kSThreads, 0, st>>>(
+    auto kern = clamp_thr(thr) >= 128 ? k_sample_count<true> : k_sample_count<false>;
+    kern<<<dim3(max_chunks, ny), kSThreads, 0, st>>>(
         img, patches + y0, max_chunks, thr, counts + (int64_t)y0 * max_chunks * 4);
     const cudaError_t e = launched();
     if (e != cudaSuccess) return e;
@@ -475,7 +506,8 @@ cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches,
   if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;
   for (int y0 = 0; y0 < npatches; y0 += kMaxGridY) {   // gridDim.y <= 65535
     const int ny = npatches - y0 < kMaxGridY ? npatches - y0 : kMaxGridY;
-    k_sample_compact<<<dim3(max_chunks, ny), kSThreads, 0, st>>>(
+    auto kern = clamp_thr(thr) >= 128 ? k_sample_compact<true> : k_sample_compact<false>;
+    kern<<<dim3(max_chunks, ny), kSThreads, 0, st>>>(
         img, patches + y0, max_chunks, thr, counts + (int64_t)y0 * max_chunks * 4, takes + y0,
         out_px, bright_hist);
     const cudaError_t e = launched();
