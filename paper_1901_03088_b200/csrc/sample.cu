@@ -209,16 +209,20 @@ __device__ __forceinline__ void limit_flags(uint32_t (&f)[4][4], int q, int m) {
     }
 }
 
+// kCPB consecutive chunks of one patch per CTA: the histograms are zeroed and
+// flushed once and the chunk prefix carried from chunk to chunk.
+constexpr int kCPB = 4;
+
 template <bool HI>
 __global__ void __launch_bounds__(kSThreads) k_sample_compact(
     const uint8_t* __restrict__ img, const spcn_patch* __restrict__ patches, int max_chunks,
     int thr, const int32_t* __restrict__ counts, const spcn_patch_take* __restrict__ takes,
     uint8_t* __restrict__ out_px, int32_t* __restrict__ bright_hist) {
-  const int k = blockIdx.x, pi = blockIdx.y;
+  const int k0 = blockIdx.x * kCPB, pi = blockIdx.y;
   const spcn_patch p = patches[pi];
   const spcn_patch_take tk = takes[pi];
   const int64_t npx = (int64_t)p.width * p.height;
-  if ((int64_t)k * kChunk >= npx) return;
+  if ((int64_t)k0 * kChunk >= npx) return;
   __shared__ int s_pre[4];
   __shared__ unsigned scratch[kSThreads / 32][4];
   __shared__ int s_hist[3 * 256 + 32];   // + one dump word per lane
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // prefix over earlier chunks of this patch
   unsigned pre[4] = {0, 0, 0, 0};
-  for (int j = threadIdx.x; j < k; j += kSThreads) {
+  for (int j = threadIdx.x; j < k0; j += kSThreads) {
     const int32_t* c = counts + ((int64_t)pi * max_chunks + j) * 4;
     pre[0] += c[0]; pre[1] += c[1]; pre[2] += c[2]; pre[3] += c[3];
   }
@@ -251,95 +255,105 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
     s_pre[threadIdx.x] = (int)v;
   }
   __syncthreads();
-  const int spre[4] = {s_pre[0], s_pre[1], s_pre[2], s_pre[3]};
+  int spre[4] = {s_pre[0], s_pre[1], s_pre[2], s_pre[3]};
   const int lim[4] = {(int)min(tk.take_nonwhite, (int64_t)INT32_MAX), tk.take_bright[0],
                       tk.take_bright[1], tk.take_bright[2]};
-  if (!(spre[0] < lim[0] || spre[1] < lim[1] || spre[2] < lim[2] || spre[3] < lim[3]))
-    return;  // uniform across the block: every pool is full before this chunk
+  for (int k = k0; k < k0 + kCPB && (int64_t)k * kChunk < npx; ++k) {
+    if (!(spre[0] < lim[0] || spre[1] < lim[1] || spre[2] < lim[2] || spre[3] < lim[3]))
+      break;  // uniform across the block: every pool is full before this chunk
 
-  const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
-  uint32_t w[12];
-  int nv = 0;
-  if (r0 < npx) {
-    nv = patch_run(img, p, r0, npx, w);
-  } else {
+    const int64_t r0 = (int64_t)k * kChunk + threadIdx.x * kPerThread;
+    uint32_t w[12];
+    int nv = 0;
+    if (r0 < npx) {
+      nv = patch_run(img, p, r0, npx, w);
+    } else {
 #pragma unroll
-    for (int i = 0; i < 12; ++i) w[i] = 0;
-  }
-  uint32_t f[4][4];
-  run_flags<HI>(w, nv, gt_k(thr), f);
-  uint32_t c01 = 0, c23 = 0;   // packed 16-bit counters: non-white | R << 16, G | B << 16
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    c01 += __popc(f[g][3]) | (__popc(f[g][0]) << 16);
-    c23 += __popc(f[g][1]) | (__popc(f[g][2]) << 16);
-  }
-  // block exclusive scan of the packed counters (chunk totals <= 4096)
-  uint32_t i01 = c01, i23 = c23;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t y01 = __shfl_up_sync(0xffffffffu, i01, off);
-    const uint32_t y23 = __shfl_up_sync(0xffffffffu, i23, off);
-    if (lane >= off) {
-      i01 += y01;
-      i23 += y23;
+      for (int i = 0; i < 12; ++i) w[i] = 0;
     }
-  }
-  if (lane == 31) {
-    s_wsum[warp][0] = i01;
-    s_wsum[warp][1] = i23;
-  }
-  __syncthreads();
-  if (warp == 0) {   // lane 2w + h: exclusive scan over the 8 warps
-    static_assert(kSThreads / 32 * 2 <= 32, "one warp scans the per-warp totals");
-    const bool on = lane < 2 * (kSThreads / 32);
-    const uint32_t v = on ? (&s_wsum[0][0])[lane] : 0u;
-    uint32_t x = v;
+    uint32_t f[4][4];
+    run_flags<HI>(w, nv, gt_k(thr), f);
+    uint32_t c01 = 0, c23 = 0;   // packed 16-bit counters: non-white | R << 16, G | B << 16
 #pragma unroll
-    for (int off = 2; off < 2 * (kSThreads / 32); off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
-      if (lane >= off) x += y;
+    for (int g = 0; g < 4; ++g) {
+      c01 += __popc(f[g][3]) | (__popc(f[g][0]) << 16);
+      c23 += __popc(f[g][1]) | (__popc(f[g][2]) << 16);
     }
-    __syncwarp();
-    if (on) (&s_wsum[0][0])[lane] = x - v;
-    if (lane >= 2 * (kSThreads / 32) - 2 && on) s_tot[lane - (2 * (kSThreads / 32) - 2)] = x;
-  }
-  __syncthreads();
-  const uint2 wp = *reinterpret_cast<const uint2*>(s_wsum[warp]);
-  const uint2 tt = *reinterpret_cast<const uint2*>(s_tot);
-  const uint32_t e01 = wp.x + i01 - c01, e23 = wp.y + i23 - c23;
-  const int rank[4] = {spre[0] + (int)(e01 & 0xffffu), spre[1] + (int)(e01 >> 16),
-                       spre[2] + (int)(e23 & 0xffffu), spre[3] + (int)(e23 >> 16)};
-  const int tot[4] = {(int)(tt.x & 0xffffu), (int)(tt.x >> 16), (int)(tt.y & 0xffffu),
-                      (int)(tt.y >> 16)};
+    // block exclusive scan of the packed counters (chunk totals <= 4096)
+    uint32_t i01 = c01, i23 = c23;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {   // pool q takes all / none / the first part of the chunk
-    const int fq = q == 0 ? 3 : q - 1;
-    if (spre[q] + tot[q] > lim[q]) limit_flags(f, fq, lim[q] - rank[q]);   // block-uniform test
-  }
-  const int blk_r0 = spre[0];                 // the chunk's first non-white rank
-  if (spre[0] < lim[0])
-    compact_run<true>(w, f, rank[0] - blk_r0, s_stage, kChunk + lane, s_hist);
-  else
-    compact_run<false>(w, f, 0, s_stage, kChunk + lane, s_hist);
-  __syncthreads();
-  {   // the staged run [blk_r0, min(take, blk_r0 + chunk non-white)) to the output
-    const int64_t t1 = min((int64_t)tk.take_nonwhite, (int64_t)blk_r0 + tot[0]);
-    const int nb = t1 > blk_r0 ? (int)(3 * (t1 - blk_r0)) : 0;
-    uint8_t* dstb = out_px + 3 * (tk.out_base + blk_r0);
-    const int head = min(nb, (int)((4u - (reinterpret_cast<uintptr_t>(dstb) & 3u)) & 3u));
-    if (threadIdx.x < head) dstb[threadIdx.x] = s_stage[threadIdx.x / 3] >> (8 * (threadIdx.x % 3));
-    const int nw = (nb - head) >> 2;
-    uint32_t* dw = reinterpret_cast<uint32_t*>(dstb + head);
-    for (int i = threadIdx.x; i < nw; i += kSThreads) {
-      const int b = head + 4 * i, q = b / 3, o = b - 3 * q;   // run bytes b..b+3
-      dw[i] = __byte_perm(s_stage[q], s_stage[q + 1], o == 0 ? 0x4210 : o == 1 ? 0x5421 : 0x6542);
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y01 = __shfl_up_sync(0xffffffffu, i01, off);
+      const uint32_t y23 = __shfl_up_sync(0xffffffffu, i23, off);
+      if (lane >= off) {
+        i01 += y01;
+        i23 += y23;
+      }
     }
-    const int tail0 = head + 4 * nw;
-    if (threadIdx.x < nb - tail0) {
-      const int b = tail0 + threadIdx.x;
-      dstb[b] = s_stage[b / 3] >> (8 * (b % 3));
+    if (lane == 31) {
+      s_wsum[warp][0] = i01;
+      s_wsum[warp][1] = i23;
     }
+    __syncthreads();
+    if (warp == 0) {   // lane 2w + h: exclusive scan over the 8 warps
+      static_assert(kSThreads / 32 * 2 <= 32, "one warp scans the per-warp totals");
+      const bool on = lane < 2 * (kSThreads / 32);
+      const uint32_t v = on ? (&s_wsum[0][0])[lane] : 0u;
+      uint32_t x = v;
+#pragma unroll
+      for (int off = 2; off < 2 * (kSThreads / 32); off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      __syncwarp();
+      if (on) (&s_wsum[0][0])[lane] = x - v;
+      if (lane >= 2 * (kSThreads / 32) - 2 && on) s_tot[lane - (2 * (kSThreads / 32) - 2)] = x;
+    }
+    __syncthreads();
+    const uint2 wp = *reinterpret_cast<const uint2*>(s_wsum[warp]);
+    const uint2 tt = *reinterpret_cast<const uint2*>(s_tot);
+    const uint32_t e01 = wp.x + i01 - c01, e23 = wp.y + i23 - c23;
+    const int rank[4] = {spre[0] + (int)(e01 & 0xffffu), spre[1] + (int)(e01 >> 16),
+                         spre[2] + (int)(e23 & 0xffffu), spre[3] + (int)(e23 >> 16)};
+    const int tot[4] = {(int)(tt.x & 0xffffu), (int)(tt.x >> 16), (int)(tt.y & 0xffffu),
+                        (int)(tt.y >> 16)};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {   // pool q takes all / none / the first part of the chunk
+      const int fq = q == 0 ? 3 : q - 1;
+      if (spre[q] >= lim[q]) {                        // block-uniform tests
+#pragma unroll
+        for (int g = 0; g < 4; ++g) f[g][fq] = 0;
+      } else if (spre[q] + tot[q] > lim[q]) {
+        limit_flags(f, fq, lim[q] - rank[q]);
+      }
+    }
+    const int blk_r0 = spre[0];                 // the chunk's first non-white rank
+    if (spre[0] < lim[0])
+      compact_run<true>(w, f, rank[0] - blk_r0, s_stage, kChunk + lane, s_hist);
+    else
+      compact_run<false>(w, f, 0, s_stage, kChunk + lane, s_hist);
+    __syncthreads();
+    {   // the staged run [blk_r0, min(take, blk_r0 + chunk non-white)) to the output
+      const int64_t t1 = min((int64_t)tk.take_nonwhite, (int64_t)blk_r0 + tot[0]);
+      const int nb = t1 > blk_r0 ? (int)(3 * (t1 - blk_r0)) : 0;
+      uint8_t* dstb = out_px + 3 * (tk.out_base + blk_r0);
+      const int head = min(nb, (int)((4u - (reinterpret_cast<uintptr_t>(dstb) & 3u)) & 3u));
+      if (threadIdx.x < head) dstb[threadIdx.x] = s_stage[threadIdx.x / 3] >> (8 * (threadIdx.x % 3));
+      const int nw = (nb - head) >> 2;
+      uint32_t* dw = reinterpret_cast<uint32_t*>(dstb + head);
+      for (int i = threadIdx.x; i < nw; i += kSThreads) {
+        const int b = head + 4 * i, q = b / 3, o = b - 3 * q;   // run bytes b..b+3
+        dw[i] = __byte_perm(s_stage[q], s_stage[q + 1], o == 0 ? 0x4210 : o == 1 ? 0x5421 : 0x6542);
+      }
+      const int tail0 = head + 4 * nw;
+      if (threadIdx.x < nb - tail0) {
+        const int b = tail0 + threadIdx.x;
+        dstb[b] = s_stage[b / 3] >> (8 * (b % 3));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) spre[q] += tot[q];
+    __syncthreads();   // s_stage / s_wsum / s_tot are reused by the next chunk
   }
   int32_t* gh = bright_hist + (int64_t)tk.problem * 3 * 256;
   for (int i = threadIdx.x; i < 3 * 256; i += kSThreads) {
@@ -507,7 +521,7 @@ cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches,
   for (int y0 = 0; y0 < npatches; y0 += kMaxGridY) {   // gridDim.y <= 65535
     const int ny = npatches - y0 < kMaxGridY ? npatches - y0 : kMaxGridY;
     auto kern = clamp_thr(thr) >= 128 ? k_sample_compact<true> : k_sample_compact<false>;
-    kern<<<dim3(max_chunks, ny), kSThreads, 0, st>>>(
+    kern<<<dim3((max_chunks + kCPB - 1) / kCPB, ny), kSThreads, 0, st>>>(
         img, patches + y0, max_chunks, thr, counts + (int64_t)y0 * max_chunks * 4, takes + y0,
         out_px, bright_hist);
     const cudaError_t e = launched();
