@@ -209,11 +209,14 @@ __device__ __forceinline__ void limit_flags(uint32_t (&f)[4][4], int q, int m) {
     }
 }
 
-// kCPB consecutive chunks of one patch per CTA: the histograms are zeroed and
-// flushed once and the chunk prefix carried from chunk to chunk.
-constexpr int kCPB = 4;
+// CPB consecutive chunks of one patch per CTA: the histograms are zeroed and
+// flushed once and the chunk prefix carried from chunk to chunk.  Many-patch
+// launches (batches of tiles) use 4; a slide's few visited patches need only
+// their first chunks, which then run in parallel with 1.
+constexpr int kCPBMany = 4;
+constexpr int kManyPatches = 1024;
 
-template <bool HI>
+template <bool HI, int kCPB>
 __global__ void __launch_bounds__(kSThreads) k_sample_compact(
     const uint8_t* __restrict__ img, const spcn_patch* __restrict__ patches, int max_chunks,
     int thr, const int32_t* __restrict__ counts, const spcn_patch_take* __restrict__ takes,
@@ -520,8 +523,11 @@ cudaError_t launch_sample_compact(const uint8_t* img, const spcn_patch* patches,
   if (npatches <= 0 || max_chunks <= 0) return cudaSuccess;
   for (int y0 = 0; y0 < npatches; y0 += kMaxGridY) {   // gridDim.y <= 65535
     const int ny = npatches - y0 < kMaxGridY ? npatches - y0 : kMaxGridY;
-    auto kern = clamp_thr(thr) >= 128 ? k_sample_compact<true> : k_sample_compact<false>;
-    kern<<<dim3((max_chunks + kCPB - 1) / kCPB, ny), kSThreads, 0, st>>>(
+    const bool hi = clamp_thr(thr) >= 128, many = npatches >= kManyPatches;
+    auto kern = hi ? (many ? k_sample_compact<true, kCPBMany> : k_sample_compact<true, 1>)
+                   : (many ? k_sample_compact<false, kCPBMany> : k_sample_compact<false, 1>);
+    const int cpb = many ? kCPBMany : 1;
+    kern<<<dim3((max_chunks + cpb - 1) / cpb, ny), kSThreads, 0, st>>>(
         img, patches + y0, max_chunks, thr, counts + (int64_t)y0 * max_chunks * 4, takes + y0,
         out_px, bright_hist);
     const cudaError_t e = launched();

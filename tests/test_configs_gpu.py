@@ -133,6 +133,33 @@ def test_c2_batch_of_512_patches_matches_oracle_per_item():
         assert np.array_equal(out[i], want), (i, int((out[i] != want).sum()))
 
 
+def test_c2_full_width_batch_spot_items_match_oracle():
+    """1024 config-2 patches in one batch (the many-patch compaction: several
+    chunks per CTA, histograms flushed once): the fits of items spread over
+    the batch — first, last, dense and sparse groups — equal the oracle's."""
+    import torch
+
+    pb = _pb()
+    from paper_1901_03088_b200 import synthetic
+
+    n, P = 1024, 512
+    imgs = torch.empty((n, P, P, 3), dtype=torch.uint8, device="cuda")
+    for g in range(4):
+        a, b = g * (n // 4), (g + 1) * (n // 4)
+        synthetic.render_rows(imgs[a:b].view(-1), P, (b - a) * P, 0, (b - a) * P, 11 + g,
+                              i0=(255 - 3 * g, 252 - 2 * g, 255 - g),
+                              tissue_fraction=0.3 + 0.15 * g, dense=bool(g & 1))
+    fits = _quiet(pb.fit_batch, imgs)
+    for i in (0, 1, 300, 511, 700, 1023):
+        px = imgs[i].cpu().numpy()
+        ref = orc.fit_params(px)
+        fp = fits.params(i)
+        _assert_fit(fp, ref, f"item {i}")
+        assert fp.stats.sample_count == ref["count"], i
+    del imgs
+    torch.cuda.empty_cache()
+
+
 # --------------------------------------------------------------------------- C3
 def test_c3_20k_slide_fit_and_bands_match_oracle():
     """Config 3: 20 000² (400 Mpx) rendered on the GPU.  The fit over the
