@@ -90,47 +90,67 @@ class BatchFit:
 _OD_ROWS = threading.local()     # sorted i0 values seen, their OD rows (host + per device)
 
 
-def _od_tables_exact(i0: np.ndarray, device):
+def _od_tables_exact(i0: np.ndarray, device, i0_dev=None):
     """(n, 3, 256) fp64 OD tables (CUDA) with the reference's numpy expression
     (src/optics.py:89-94), evaluated once per distinct i0 value on the host —
     i0 are order statistics of 8-bit pools, so there are few, and a row
     depends on the value only — and expanded to the items on the device.
     The rows are memoised per thread (a pure function of the value): a batch
-    whose values were all seen before uploads only the per-item indices."""
+    whose values were all seen before only looks its items up — on the device
+    when i0_dev (the same values, CUDA) is given (a host binary search per
+    value costs ~30 ns x 3n)."""
     t = _dev.torch()
     dev = t.device(device)
     key = dev.index if dev.index is not None else t._C._cuda_getDevice()
     st = _OD_ROWS.__dict__
     vals = st.get("vals")
-    n = i0.shape[0]
+    u = np.unique(i0)
     hit = False
     if vals is not None and vals.size:
-        idx = np.searchsorted(vals, i0)
-        hit = bool(np.all(vals[np.minimum(idx, vals.size - 1)] == i0))
+        pos = np.searchsorted(vals, u)
+        hit = bool(np.all(vals[np.minimum(pos, vals.size - 1)] == u))
+    st["last_hit"] = hit
     if not hit or key not in st.get("dev_rows", {}):
-        new = np.unique(i0) if vals is None else np.union1d(vals, i0.ravel())
+        new = u if vals is None else np.union1d(vals, u)
         if new.size > 4096:                      # bound the memo
-            new = np.unique(i0)
+            new = u
         ramp = np.arange(256, dtype=np.float64)
         rows = np.log(new[:, None] / np.clip(ramp[None, :], 1.0, new[:, None]))
-        st["vals"], st["dev_rows"] = new, {key: t.from_numpy(rows).to(dev)}
-        vals = new
-        idx = np.searchsorted(vals, i0)
-    d_idx = t.from_numpy(idx.astype(np.int64)).to(dev)
-    return st["dev_rows"][key][d_idx].contiguous()
+        st["vals"] = new
+        st["dev_rows"] = {key: (t.from_numpy(rows).to(dev), t.from_numpy(new).to(dev))}
+    rows_d, vals_d = st["dev_rows"][key]
+    if i0_dev is not None:
+        d_idx = t.searchsorted(vals_d, i0_dev.reshape(-1).to(t.float64)).reshape(i0.shape)
+    else:
+        d_idx = t.from_numpy(np.searchsorted(st["vals"], i0).astype(np.int64)).to(dev)
+    return rows_d[d_idx].contiguous()
 
 
-def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), *,
-              code_lam: float = 0.0) -> BatchFit:
-    """fit() of every image of a (n, H, W, 3) uint8 CUDA tensor, all on the device."""
+def _od_rows_device(dev):
+    """(rows, values) of the OD-row memo on this device when the last batch's
+    values were all in it (worth speculating on), else None."""
     t = _dev.torch()
-    L = _lib_sample()
-    if images.ndim != 4 or images.shape[3] != 3 or str(images.dtype) != "torch.uint8":
-        raise ValueError("images must be an (n, H, W, 3) uint8 tensor")
-    imgs = images.contiguous() if images.is_cuda else images.cuda().contiguous()
-    n, H, W = int(imgs.shape[0]), int(imgs.shape[1]), int(imgs.shape[2])
-    dev = imgs.device
-    # identical seeded visit order for every item (same grid, same seed)
+    d = t.device(dev)
+    key = d.index if d.index is not None else t._C._cuda_getDevice()
+    st = _OD_ROWS.__dict__
+    if os.environ.get("SPCN_BATCH_SPECULATE", "1") == "0" or not st.get("last_hit", False):
+        return None
+    return st.get("dev_rows", {}).get(key)
+
+
+_GRIDS = threading.local()         # memoised patch grids (pure functions of their key)
+
+
+def _batch_grid(n, H, W, plan, dev):
+    """The seeded visit order (same for every item: same grid, same seed),
+    the candidate rectangles, the chunk count and the device patch
+    descriptors of an (n, H, W) batch; memoised per thread (a few keys)."""
+    key = (n, H, W, plan.patch_size, plan.seed, plan.max_patches, str(dev))
+    memo = _GRIDS.__dict__.setdefault("m", {})
+    got = memo.get(key)
+    if got is not None:
+        return got
+    t = _dev.torch()
     origins = [(x, y) for y in range(0, H, plan.patch_size) for x in range(0, W, plan.patch_size)]
     order = np.random.default_rng(plan.seed).permutation(len(origins))
     ncand = min(len(order), 10 * plan.max_patches)
@@ -145,6 +165,23 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
     desc = desc.ravel()
     chunks = max(1, -(-max(w * h for (_, _, w, h) in rects) // CHUNK))
     d_desc = t.from_numpy(desc.view(np.uint8).copy()).to(dev)
+    got = (order, ncand, rects, chunks, d_desc)
+    if len(memo) < 8:   # (never evicted: a launch on another stream may still read one)
+        memo[key] = got
+    return got
+
+
+def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfConfig(), *,
+              code_lam: float = 0.0) -> BatchFit:
+    """fit() of every image of a (n, H, W, 3) uint8 CUDA tensor, all on the device."""
+    t = _dev.torch()
+    L = _lib_sample()
+    if images.ndim != 4 or images.shape[3] != 3 or str(images.dtype) != "torch.uint8":
+        raise ValueError("images must be an (n, H, W, 3) uint8 tensor")
+    imgs = images.contiguous() if images.is_cuda else images.cuda().contiguous()
+    n, H, W = int(imgs.shape[0]), int(imgs.shape[1]), int(imgs.shape[2])
+    dev = imgs.device
+    order, ncand, rects, chunks, d_desc = _batch_grid(n, H, W, plan, dev)
     counts = t.empty((n * ncand, chunks, 4), dtype=t.int32, device=dev)
     thr = int(plan.white_threshold)
     _lib.check(L.spcn_sample_count(_lib.ptr(imgs), _lib.ptr(d_desc), n * ncand, chunks, thr,
@@ -178,9 +215,10 @@ def fit_batch(images, plan: SamplePlan = SamplePlan(), cfg: SnmfConfig = SnmfCon
     return _fit_batch_tail(n, sample, collected, offsets, i0, ie, cfg, plan, code_lam)
 
 
-def _compact_i0(imgs, n, ncand, d_desc, counts, chunks, thr, d_tk, sample, extra):
+def _compact_i0(imgs, n, ncand, d_desc, counts, chunks, thr, d_tk, sample, extra, read=True):
     """Ordered compaction + bright histograms, i0 per item, and ONE read of
-    (i0, empty flags[, extra]) — extra: a device int64 vector appended."""
+    (i0, empty flags[, extra]) — extra: a device int64 vector appended.
+    read=False: no read; returns (i0, the device vector that would be read)."""
     t = _dev.torch()
     L = _lib_sample()
     dev = imgs.device
@@ -196,7 +234,8 @@ def _compact_i0(imgs, n, ncand, d_desc, counts, chunks, thr, d_tk, sample, extra
     parts = [i0.reshape(-1), empty.reshape(-1).to(t.float64)]
     if extra is not None:
         parts.append(extra.to(t.float64))             # counts < 2^53: exact in f64
-    return i0, _dev.readback(t.cat(parts))            # one read
+    v = t.cat(parts)
+    return (i0, _dev.readback(v)) if read else (i0, v)   # one read
 
 
 def _fit_batch_single_patch(imgs, n, rect, d_desc, counts, chunks, thr, plan, cfg, code_lam):
@@ -204,7 +243,12 @@ def _fit_batch_single_patch(imgs, n, rect, d_desc, counts, chunks, thr, plan, cf
     tiles with patch_size 1000): the reference's visit rules
     (src/pipeline.py:156-184) reduce to per-item ones, evaluated on the device
     (spcn_visit_single), so the counts are never read back — the compaction
-    follows the count pass directly; the take sizes come back with i0."""
+    follows the count pass directly.  When every OD-table row the batch could
+    need is likely memoised (the rows of earlier batches on this device), the
+    SNMF, coding and p99 are enqueued right behind the compaction with the
+    rows looked up on the device, and ONE read at the end brings back i0, the
+    take sizes, the statuses and a flag telling whether every i0 value was
+    memoised; if one was not, the tail re-runs with the exact rows."""
     t = _dev.torch()
     dev = imgs.device
     npx = rect[2] * rect[3]
@@ -217,33 +261,56 @@ def _fit_batch_single_patch(imgs, n, rect, d_desc, counts, chunks, thr, plan, cf
                                    _lib.ptr(take_nw), _lib.stream_handle()), "visit_single")
     # the sample at its largest (every item taking target_pixels): no read of
     # the totals before the compaction
-    sample = t.empty((max(1, n * min(plan.target_pixels, npx)), 3), dtype=t.uint8, device=dev)
-    i0, ie = _compact_i0(imgs, n, 1, d_desc, counts, chunks, thr, tk.view(-1).view(t.uint8),
-                         sample, take_nw)
+    per_max = min(plan.target_pixels, npx)
+    sample = t.empty((max(1, n * per_max), 3), dtype=t.uint8, device=dev)
+    memo = _od_rows_device(dev)
+    i0, v = _compact_i0(imgs, n, 1, d_desc, counts, chunks, thr, tk.view(-1).view(t.uint8),
+                        sample, take_nw, read=memo is None)
+    if memo is None:                                  # cold: rows from the host values first
+        ie = v
+        collected = ie[6 * n:].astype(np.int64)
+        offsets = np.concatenate([[0], np.cumsum(collected)]).astype(np.int64)
+        total = int(offsets[-1])
+        luts = _od_tables_exact(ie[:3 * n].reshape(n, 3), dev, i0)
+        d_off = t.from_numpy(offsets).to(dev)
+        flat = sample.reshape(-1)[:3 * max(total, 1)]
+        r, p99, absent = _fit_batch_launch(n, flat, d_off, luts, cfg, code_lam,
+                                           int(collected.max(initial=0)), total)
+        ai = _dev.readback(t.cat([absent.reshape(-1), r.info.reshape(-1)]))
+        return _fit_batch_finish(n, collected, i0, ie[:6 * n], r, p99, ai, luts, cfg, plan,
+                                 code_lam, stacklevel=3)
+    # speculative: device offsets, memoised rows looked up on the device
+    d_off = t.zeros(n + 1, dtype=t.int64, device=dev)
+    t.cumsum(take_nw, 0, out=d_off[1:])
+    rows_d, vals_d = memo
+    idx = t.searchsorted(vals_d, i0.reshape(-1)).clamp_(max=vals_d.numel() - 1)
+    miss = (vals_d[idx] != i0.reshape(-1)).any().to(t.float64).reshape(1)
+    luts = rows_d[idx.reshape(n, 3)].contiguous()
+    total_cap = n * per_max
+    r, p99, absent = _fit_batch_launch(n, sample.reshape(-1), d_off, luts, cfg, code_lam,
+                                       per_max, total_cap)
+    allv = _dev.readback(t.cat([v, miss, absent.reshape(-1).to(t.float64),
+                                r.info.reshape(-1).to(t.float64)]))
+    ie = allv[:7 * n]
     collected = ie[6 * n:].astype(np.int64)
-    offsets = np.concatenate([[0], np.cumsum(collected)]).astype(np.int64)
-    return _fit_batch_tail(n, sample, collected, offsets, i0, ie[:6 * n], cfg, plan, code_lam,
-                           stacklevel=4)
+    rest = allv[7 * n:]
+    if rest[0] != 0:                                   # an i0 value without a memoised row
+        luts = _od_tables_exact(ie[:3 * n].reshape(n, 3), dev, i0)   # (clears last_hit)
+        r, p99, absent = _fit_batch_launch(n, sample.reshape(-1), d_off, luts, cfg, code_lam,
+                                           per_max, total_cap)
+        ai = _dev.readback(t.cat([absent.reshape(-1), r.info.reshape(-1)]))
+    else:
+        ai = rest[1:].astype(np.int64)
+    return _fit_batch_finish(n, collected, i0, ie[:6 * n], r, p99, ai, luts, cfg, plan,
+                             code_lam, stacklevel=3)
 
 
-def _fit_batch_tail(n, sample, collected, offsets, i0, ie, cfg, plan, code_lam, stacklevel=3):
-    """From the sample and i0 on: OD tables, SNMF, densities, p99, statuses."""
+def _fit_batch_launch(n, flat, d_off, luts, cfg, code_lam, mmax, total):
+    """Enqueue the SNMF (over per-item colour tables), the densities of every
+    distinct colour and the weighted p99.  `total` is the sample's length
+    (the colour-table layout; entries past an item's offsets are not read)."""
     t = _dev.torch()
-    dev = sample.device
-    total = int(offsets[-1])
-    status = np.zeros(n, np.int32)
-    status[collected == 0] = -_lib.SPCN_EBLANK
-    status[(collected > 0) & (collected < 10)] = -_lib.SPCN_EINSUFFICIENT
-    i0_h = ie[:3 * n].reshape(n, 3)
-    if ie[3 * n:].any():
-        warnings.warn("some items had no pixels brighter than the white threshold in a "
-                      "channel; their i0 fell back to 255", optics.BackgroundEstimateWarning,
-                      stacklevel=stacklevel)
-    luts = _od_tables_exact(i0_h, dev)
-    d_off = t.from_numpy(offsets).to(dev)
-    flat = sample.reshape(-1)[:3 * max(total, 1)]   # (the single-patch path over-allocates)
     r = snmf.snmf_batched(flat, d_off, luts, cfg, cluster=1)
-    mmax = int(collected.max(initial=0))
     if r.table is not None and total > 0:
         # densities and p99 over the SNMF's colour table: one fp64 coding per
         # distinct colour, weighted exact select (same values as per sample)
@@ -254,7 +321,20 @@ def _fit_batch_tail(n, sample, collected, offsets, i0, ie, cfg, plan, code_lam, 
 
         h = snmf.code_samples(flat, d_off, luts, r.basis, code_lam, mmax)
         p99, absent = dstats.segment_percentiles(h, d_off, 99.0)
-    ai = _dev.readback(t.cat([absent.reshape(-1), r.info.reshape(-1)]))   # one read
+    if absent.dtype != t.int32:
+        absent = absent.to(t.int32)
+    return r, p99, absent
+
+
+def _fit_batch_finish(n, collected, i0, ie, r, p99, ai, luts, cfg, plan, code_lam, stacklevel):
+    """Statuses, warnings and the BatchFit from the host reads."""
+    status = np.zeros(n, np.int32)
+    status[collected == 0] = -_lib.SPCN_EBLANK
+    status[(collected > 0) & (collected < 10)] = -_lib.SPCN_EINSUFFICIENT
+    if ie[3 * n:6 * n].any():
+        warnings.warn("some items had no pixels brighter than the white threshold in a "
+                      "channel; their i0 fell back to 255", optics.BackgroundEstimateWarning,
+                      stacklevel=stacklevel + 1)
     absent_h = ai[:2 * n].reshape(n, 2).any(axis=1)
     info = ai[2 * n:].reshape(n, -1)
     status[(status == 0) & absent_h] = -_lib.SPCN_ESTAIN_ABSENT
@@ -262,6 +342,22 @@ def _fit_batch_tail(n, sample, collected, offsets, i0, ie, cfg, plan, code_lam, 
     return BatchFit(i0=i0, basis=r.basis, p99=p99, luts=luts, count=collected, status=status,
                     provenance=prov, iterations=info[:, 0].copy(), converged=info[:, 1] != 0,
                     warn_flags=info[:, 2].copy())
+
+
+def _fit_batch_tail(n, sample, collected, offsets, i0, ie, cfg, plan, code_lam, stacklevel=3):
+    """From the sample and i0 on (host offsets): OD tables, SNMF, densities,
+    p99, statuses."""
+    t = _dev.torch()
+    dev = sample.device
+    total = int(offsets[-1])
+    luts = _od_tables_exact(ie[:3 * n].reshape(n, 3), dev, i0)
+    d_off = t.from_numpy(offsets).to(dev)
+    flat = sample.reshape(-1)[:3 * max(total, 1)]
+    r, p99, absent = _fit_batch_launch(n, flat, d_off, luts, cfg, code_lam,
+                                       int(collected.max(initial=0)), total)
+    ai = _dev.readback(t.cat([absent.reshape(-1), r.info.reshape(-1)]))   # one read
+    return _fit_batch_finish(n, collected, i0, ie, r, p99, ai, luts, cfg, plan, code_lam,
+                             stacklevel)
 
 
 def transform_batch(images, fits: BatchFit, target: FitParams, out=None, *,

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <condition_variable>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -357,9 +358,14 @@ struct FittedSlots {
   cudaEvent_t built[kDpSlots] = {};       // the status read-back has landed
   bool used[kDpSlots] = {};
   bool analytic[kDpSlots] = {};           // the slot's recolouring uses the analytic bound
+  // prepared, its run not yet enqueued: `done` does not cover the slot's
+  // recolour yet, so another prepare must not take the slot (threads that
+  // prepare concurrently block here until the run is enqueued)
+  bool pending[kDpSlots] = {};
   int next = 0;
 };
 std::mutex g_fitted_mu;
+std::condition_variable g_fitted_cv;
 FittedSlots g_fitted[64];
 
 int check_fitted(const spcn_xform_fitted* p) {
@@ -381,6 +387,14 @@ int check_fitted(const spcn_xform_fitted* p) {
   return SPCN_OK;
 }
 
+void release_slot(int dev, int slot) {
+  {
+    std::lock_guard<std::mutex> lk(g_fitted_mu);
+    g_fitted[dev].pending[slot] = false;
+  }
+  g_fitted_cv.notify_all();
+}
+
 // slot + build + calibration part; *built_out = the event after the status read-back
 int fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts, void* workspace,
                    size_t workspace_bytes, int32_t* status_pinned, cudaStream_t st,
@@ -398,7 +412,7 @@ int fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts, voi
   DevParams* staging;
   cudaEvent_t built;
   {
-    std::lock_guard<std::mutex> lk(g_fitted_mu);
+    std::unique_lock<std::mutex> lk(g_fitted_mu);
     FittedSlots& fs = g_fitted[dev];
     if (!fs.staging) {
       if ((e = cudaMalloc(&fs.staging, sizeof(DevParams) * kDpSlots)) != cudaSuccess)
@@ -408,14 +422,21 @@ int fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts, voi
             (e = cudaEventCreateWithFlags(&fs.built[k], cudaEventDisableTiming)) != cudaSuccess)
           return cuda_fail(e, "event");
     }
+    g_fitted_cv.wait(lk, [&] {   // the next slot in ring order that is not pending
+      for (int k = 0; k < kDpSlots; ++k)
+        if (!fs.pending[(fs.next + k) % kDpSlots]) return true;
+      return false;
+    });
     slot = fs.next;
-    fs.next = (fs.next + 1) % kDpSlots;
+    while (fs.pending[slot]) slot = (slot + 1) % kDpSlots;
+    fs.next = (slot + 1) % kDpSlots;
     staging = fs.staging + slot;
     built = fs.built[slot];
     // the slot's previous user (any stream) must be finished with it
     if (fs.used[slot] && (e = cudaStreamWaitEvent(st, fs.done[slot], 0)) != cudaSuccess)
       return cuda_fail(e, "slot wait");
     fs.used[slot] = true;
+    fs.pending[slot] = true;
     fs.analytic[slot] = (p->flags & SPCN_FITTED_ANALYTIC) != 0;
   }
   XformBuildIn in{};
@@ -430,28 +451,18 @@ int fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts, voi
   const uint32_t q0 = static_cast<uint32_t>((uint64_t)n * part / nparts),
                  q1 = static_cast<uint32_t>((uint64_t)n * (part + 1) / nparts);
   if ((e = launch_xform_build(slot, in, p->src_od_table, static_cast<const double*>(p->src_fit),
-                              staging, workspace, status_pinned, built, q0, q1, st)) != cudaSuccess)
+                              staging, workspace, status_pinned, built, q0, q1, st)) != cudaSuccess) {
+    release_slot(dev, slot);
     return cuda_fail(e, "xform_build");
+  }
   *slot_out = slot;
   *built_out = built;
   return SPCN_OK;
 }
 
-int fitted_run(const uint8_t* src, uint8_t* dst, int64_t npix, int32_t slot, void* workspace,
-               size_t workspace_bytes, cudaStream_t st) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "get_device");
-  if (dev < 0 || dev >= 64) return fail(SPCN_EINVAL, "device index out of range");
-  if (slot < 0 || slot >= kDpSlots) return fail(SPCN_EINVAL, "bad slot");
-  cudaEvent_t done;
-  bool analytic;
-  {
-    std::lock_guard<std::mutex> lk(g_fitted_mu);
-    if (!g_fitted[dev].staging) return fail(SPCN_EINVAL, "no prepared recolouring");
-    done = g_fitted[dev].done[slot];
-    analytic = g_fitted[dev].analytic[slot];
-  }
+int fitted_run_launch(const uint8_t* src, uint8_t* dst, int64_t npix, int32_t slot, bool analytic,
+                      void* workspace, size_t workspace_bytes, cudaStream_t st) {
+  cudaError_t e;
   if (npix > 0) {
     if (!src || !dst) return fail(SPCN_EINVAL, "src/dst is NULL");
     const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
@@ -476,9 +487,34 @@ int fitted_run(const uint8_t* src, uint8_t* dst, int64_t npix, int32_t slot, voi
         cudaSuccess)
       return cuda_fail(e, "xform_repair_c");
   }
-  if ((e = cudaEventRecord(done, st)) != cudaSuccess) return cuda_fail(e, "slot record");
   return SPCN_OK;
 }
+
+// The recolour of a prepared slot; on every path the slot's `done` event is
+// recorded (covering its build and recolour) and the slot released.
+int fitted_run(const uint8_t* src, uint8_t* dst, int64_t npix, int32_t slot, void* workspace,
+               size_t workspace_bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "get_device");
+  if (dev < 0 || dev >= 64) return fail(SPCN_EINVAL, "device index out of range");
+  if (slot < 0 || slot >= kDpSlots) return fail(SPCN_EINVAL, "bad slot");
+  cudaEvent_t done;
+  bool analytic;
+  {
+    std::lock_guard<std::mutex> lk(g_fitted_mu);
+    if (!g_fitted[dev].staging) return fail(SPCN_EINVAL, "no prepared recolouring");
+    done = g_fitted[dev].done[slot];
+    analytic = g_fitted[dev].analytic[slot];
+  }
+  const int rc = fitted_run_launch(src, dst, npix, slot, analytic, workspace, workspace_bytes, st);
+  e = cudaEventRecord(done, st);
+  release_slot(dev, slot);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "slot record");
+  return SPCN_OK;
+}
+
 }  // namespace
 
 extern "C" {

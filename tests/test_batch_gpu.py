@@ -204,3 +204,55 @@ def test_table_percentiles_equal_per_sample_percentiles():
     assert np.array_equal(p_s.cpu().numpy(), p_t.cpu().numpy())
     assert np.array_equal(a_s.cpu().numpy(), a_t.cpu().numpy())
     assert np.array_equal(fits.p99.cpu().numpy(), p_t.cpu().numpy())
+
+
+def test_speculative_tail_hit_and_miss_equal_the_cold_path():
+    """One-patch batches enqueue the SNMF/p99 tail behind the compaction with
+    memoised OD rows looked up on the device once the previous batch's i0
+    values were all memoised; a batch with a new i0 value re-runs the tail
+    with the exact rows.  Both give what a cold thread (empty memo) gives."""
+    import threading
+
+    import torch
+
+    pb = _pb()
+    from paper_1901_03088_b200 import batch as bt
+
+    a = torch.from_numpy(np.stack(_items(96, 128, 6, seed=3))).cuda()
+    b = torch.from_numpy(np.stack(_items(96, 128, 6, seed=4))).cuda()
+
+    def fit(x):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            f = pb.fit_batch(x)
+        return [f.params(i) for i in range(x.shape[0])], f.status.copy()
+
+    def cold(x, box):
+        box.append(fit(x))
+
+    ref = {}
+    for name, x in (("a", a), ("b", b)):
+        box = []
+        th = threading.Thread(target=cold, args=(x, box))
+        th.start()
+        th.join()
+        ref[name] = box[0]
+
+    def same(got, want):
+        (pg, sg), (pw, sw) = got, want
+        assert np.array_equal(sg, sw)
+        for fg, fw in zip(pg, pw):
+            assert np.array_equal(fg.i0, fw.i0)
+            assert np.array_equal(fg.basis, fw.basis)
+            assert np.array_equal(fg.stats.p99, fw.stats.p99)
+            assert fg.stats.sample_count == fw.stats.sample_count
+
+    fit(a)
+    fit(a)                                     # memo now holds every value of a
+    assert bt._od_rows_device(a.device) is not None
+    same(fit(a), ref["a"])                     # speculative, all rows memoised
+    assert bt._od_rows_device(a.device) is not None
+    same(fit(b), ref["b"])                     # speculative, new values: re-run
+    if bt._od_rows_device(a.device) is None:   # (b had a value a did not)
+        same(fit(b), ref["b"])                 # cold, then speculative again
+        same(fit(b), ref["b"])

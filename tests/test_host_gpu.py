@@ -36,7 +36,10 @@ def test_numpy_path_concurrent_threads():
     warnings.simplefilter("ignore")
     pairs = [_pair(10 + k) for k in range(3)]
     ref = [pb.normalize(s, t) for s, t in pairs]
-    got = [None] * 6
+    # (more threads than recolouring parameter slots: a prepared slot must
+    # not be taken by another thread before its recolour is enqueued)
+    nthr = 12
+    got = [None] * nthr
     errs = []
 
     def work(i):
@@ -46,13 +49,13 @@ def test_numpy_path_concurrent_threads():
         except Exception as exc:   # pragma: no cover
             errs.append(exc)
 
-    th = [threading.Thread(target=work, args=(i,)) for i in range(6)]
+    th = [threading.Thread(target=work, args=(i,)) for i in range(nthr)]
     for x in th:
         x.start()
     for x in th:
         x.join()
     assert not errs, errs
-    for i in range(6):
+    for i in range(nthr):
         assert np.array_equal(got[i], ref[i % 3]), i
 
 
