@@ -175,19 +175,25 @@ __device__ __forceinline__ void hist_inc(uint32_t addr) {
 
 template <bool STAGE>
 __device__ __forceinline__ void compact_run(const uint32_t (&w)[12], const uint32_t (&f)[4][4],
-                                            int rank0, uint32_t* stage, int dump, int* hist) {
-  const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(hist);
-  const uint32_t hdump = hbase + 4 * (3 * 256 + (threadIdx.x & 31));
+                                            int rank0, uint32_t* stage, int dump, int* hist,
+                                            const bool (&act)[3]) {
+  if (STAGE) {
 #pragma unroll
-  for (int j = 0; j < kPerThread; ++j) {
-    const int g = j >> 2, sh = 8 * (j & 3) + 7;
-    if (STAGE) {
+    for (int j = 0; j < kPerThread; ++j) {
+      const int g = j >> 2, sh = 8 * (j & 3) + 7;
       const int nwf = (f[g][3] >> sh) & 1;
       stage[nwf ? rank0 : dump] = pixel_of(w, j);
       rank0 += nwf;
     }
+  }
+  const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(hist);
+  const uint32_t hdump = hbase + 4 * (3 * 256 + (threadIdx.x & 31));
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
+  for (int c = 0; c < 3; ++c) {
+    if (!act[c]) continue;   // block-uniform: the channel's pool is full
+#pragma unroll
+    for (int j = 0; j < kPerThread; ++j) {
+      const int g = j >> 2, sh = 8 * (j & 3) + 7;
       const int b = 3 * j + c;   // byte of channel c of pixel j
       const uint32_t a = hbase + 4 * (256 * c + __byte_perm(w[b >> 2], 0, 0x4440 | (b & 3)));
       hist_inc(f[g][c] & (1u << sh) ? a : hdump);
@@ -211,9 +217,9 @@ __device__ __forceinline__ void limit_flags(uint32_t (&f)[4][4], int q, int m) {
 
 // CPB consecutive chunks of one patch per CTA: the histograms are zeroed and
 // flushed once and the chunk prefix carried from chunk to chunk.  Many-patch
-// launches (batches of tiles) use 4; a slide's few visited patches need only
+// launches (batches of tiles) use 8; a slide's few visited patches need only
 // their first chunks, which then run in parallel with 1.
-constexpr int kCPBMany = 4;
+constexpr int kCPBMany = 8;
 constexpr int kManyPatches = 1024;
 
 template <bool HI, int kCPB>
@@ -331,10 +337,11 @@ __global__ void __launch_bounds__(kSThreads) k_sample_compact(
       }
     }
     const int blk_r0 = spre[0];                 // the chunk's first non-white rank
+    const bool act[3] = {spre[1] < lim[1], spre[2] < lim[2], spre[3] < lim[3]};
     if (spre[0] < lim[0])
-      compact_run<true>(w, f, rank[0] - blk_r0, s_stage, kChunk + lane, s_hist);
+      compact_run<true>(w, f, rank[0] - blk_r0, s_stage, kChunk + lane, s_hist, act);
     else
-      compact_run<false>(w, f, 0, s_stage, kChunk + lane, s_hist);
+      compact_run<false>(w, f, 0, s_stage, kChunk + lane, s_hist, act);
     __syncthreads();
     {   // the staged run [blk_r0, min(take, blk_r0 + chunk non-white)) to the output
       const int64_t t1 = min((int64_t)tk.take_nonwhite, (int64_t)blk_r0 + tot[0]);
