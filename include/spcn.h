@@ -478,7 +478,11 @@ int spcn_xform_rgb8_fitted(const uint8_t* src, uint8_t* dst, int64_t npix,
  * max-reduces that word across the ranks (one int32 all-reduce,
  * stream-ordered) and then calls run, which recolours with the reduced bound
  * and releases the slot.  Every prepare must be followed by a run on the
- * same stream (npix 0 only releases the slot).                            */
+ * same stream (npix 0 only releases the slot; a run that fails its argument
+ * checks releases it too).  There are SPCN_FITTED_SLOTS slots per device: a
+ * prepare while every slot is prepared-but-not-run (other threads) blocks
+ * until one of them runs.                                                   */
+#define SPCN_FITTED_SLOTS 2
 int spcn_xform_fitted_prepare(const spcn_xform_fitted* p, int32_t part, int32_t nparts,
                               void* workspace, size_t workspace_bytes, int32_t* status_pinned,
                               int32_t* slot_out, void* stream);

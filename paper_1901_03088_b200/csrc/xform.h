@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "spcn.h"
 #include "spcn_device.cuh"
 
 namespace spcn {
@@ -24,7 +25,7 @@ cudaError_t launch_beer_lambert(const uint8_t* px, double* od, int64_t n, const 
 cudaError_t launch_inverse_bl(const double* od, uint8_t* out, int64_t n, const StrictP& sp,
                               cudaStream_t st);
 // ---- device-built recolouring (xform.cu k_build_xform) -------------------
-constexpr int kDpSlots = 2;   // __constant__ parameter slots (ring; see api.cu)
+constexpr int kDpSlots = SPCN_FITTED_SLOTS;   // __constant__ parameter slots (ring; see api.cu)
 // fp sits at 8 mod 16, as the kernel-parameter copy does (after src, dst,
 // npix): the compiler then forms the same constant-operand / uniform-register
 // mix for both (at 0 mod 16 it batches the fields into LDCU.128 loads, and the
