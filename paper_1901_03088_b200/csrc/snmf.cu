@@ -359,8 +359,15 @@ cudaError_t launch_code_table(const uint32_t* ukey, const int32_t* ucount, const
                               double lam, int max_sweeps, double* h, int64_t total,
                               cudaStream_t st) {
   if (nprob <= 0) return cudaSuccess;
+  // CTAs per problem: each loads the problem's 6 KB OD table first, so few
+  // CTAs with more colours each (C2, ~10 k colours per problem: 16 -> 0.73
+  // ms, 4 -> 0.54, 2 -> 0.52); SPCN_CODE_TABLE_GX overrides (A/B)
+  static const int gx_cap = [] {
+    const char* e = std::getenv("SPCN_CODE_TABLE_GX");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 2;
+  }();
   int64_t gx = (max_m + 255) / 256;
-  if (gx > 16) gx = 16;
+  if (gx > gx_cap) gx = gx_cap;
   if (gx < 1) gx = 1;
   for (int p0 = 0; p0 < nprob; p0 += kMaxGridY) {   // gridDim.y <= 65535
     const int np = nprob - p0 < kMaxGridY ? nprob - p0 : kMaxGridY;
