@@ -196,3 +196,60 @@ def test_transform_degenerate_and_progress():
     pb.transform(pb.ArraySource(px), fp, fp, pb.ArrayWriter(256, 256), strip_height=100,
                  progress=lambda d, t: seen.append((d, t)))
     assert seen == [(100, 256), (200, 256), (256, 256)]
+
+
+@pytest.mark.parametrize("thr", [0, 60, 127, 128, 200, 254, 255])
+def test_sampling_white_thresholds_and_take_limits(thr):
+    """The byte-parallel flags of the count/compaction kernels on both sides
+    of thr = 128 (two SWAR forms) and at the ends of the range, on an odd
+    slide whose 100-px patches give unaligned rows and short tails, with a
+    small target and bright cap so pools fill inside chunks: the sample, the
+    visit counts and the bright pools equal the oracle's."""
+    import torch
+
+    pb = _pb()
+    px, _, _ = orc.render(517, 333, 21, tissue_fraction=0.5, i0=(250, 238, 226))
+    oplan = orc.Plan(max_patches=20, patch_size=100, target_pixels=7000,
+                     background_fraction_cutoff=0.95, seed=5, white_threshold=thr,
+                     sample_cap=3000)
+    plan = pb.SamplePlan(max_patches=20, patch_size=100, target_pixels=7000,
+                         background_fraction_cutoff=0.95, seed=5, white_threshold=thr,
+                         sample_cap=3000)
+    try:
+        ref = orc.gather_sample(px, oplan)
+    except orc.OracleError:
+        ref = None
+    for src in (pb.ArraySource(px), pb.DeviceSource(torch.from_numpy(px).cuda())):
+        if ref is None:
+            with pytest.raises(Exception):
+                pb.sample_pixels(src, plan)
+            continue
+        s = pb.sample_pixels(src, plan)
+        assert np.array_equal(s.non_white, ref["non_white"]), thr
+        assert list(s.patch_counts) == list(ref["counts"]), thr
+        assert [s.patches_visited, s.patches_used] == [ref["visited"], ref["used"]], thr
+        want = np.stack([np.bincount(ref["bright"][c], minlength=256) for c in range(3)])
+        assert np.array_equal(np.asarray(s.bright_hist).reshape(3, 256), want), thr
+
+
+@pytest.mark.parametrize("thr", [100, 220])
+def test_batch_sampling_many_items_take_limits(thr):
+    """1024 items of 96 x 96 (three chunks each: the many-patch compaction
+    with several chunks per CTA) with a target and bright cap that end inside
+    the chunks: per-item sample sizes and i0 equal the oracle's."""
+    import torch
+
+    pb = _pb()
+    n = 1024
+    imgs = np.stack([orc.render(96, 96, 300 + (k % 16), tissue_fraction=0.3 + 0.04 * (k % 16),
+                                i0=(252, 240, 231))[0] for k in range(n)])
+    plan = pb.SamplePlan(target_pixels=5000, white_threshold=thr, sample_cap=2500)
+    oplan = orc.Plan(target_pixels=5000, white_threshold=thr, sample_cap=2500)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        fits = pb.fit_batch(torch.from_numpy(imgs).cuda(), plan)
+    i0 = fits.i0.cpu().numpy()
+    for k in (0, 1, 7, 15, 500, 1023):
+        ref = orc.gather_sample(imgs[k], oplan)
+        assert int(fits.count[k]) == ref["non_white"].shape[0], k
+        assert np.array_equal(i0[k], orc.bg_intensity(ref["bright"])), k
