@@ -858,10 +858,10 @@ def fit_pair_transform_resident(src: DeviceSource, tgt: DeviceSource, out, *,
         side, fork, join = _side_stream(src.tensor.device)
     fork.record(main)
     side.wait_event(fork)
-    with t.cuda.stream(side):
+    with _dev.fast_stream(side):
         started_t = _sample_start(fb_t, tgt, plan)
     started_s = _sample_start(fb_s, src, plan)
-    with t.cuda.stream(side):
+    with _dev.fast_stream(side):
         m_t, i0_t, _ = _fit_sample_checked(fb_t, tgt, plan, False, started=started_t)
     m_s, i0_s, meta = _fit_sample_checked(fb_s, src, plan, False, started=started_s)
     stats.sampled_pixels = m_s
@@ -869,7 +869,7 @@ def fit_pair_transform_resident(src: DeviceSource, tgt: DeviceSource, out, *,
     t1 = time.perf_counter()
     stats.sampling_s += t1 - t0
     with _dev.nvtx("spcn.fit_pair_transform"):
-        with t.cuda.stream(side):
+        with _dev.fast_stream(side):
             fitcore.basis_enqueue(fb_t, fb_t.sample_ptr, m_t, i0_t, cfg, code_lam=code_lam,
                                   pooled=True)
             join.record(side)
